@@ -1,0 +1,122 @@
+"""Generate the committed golden fixtures from the UNMODIFIED reference.
+
+Runs oracle/_ref/ref_driver (the reference headers compiled by oracle/Makefile)
+and stores its outputs as compressed .npz files next to this script.  Only
+runnable where /root/reference exists (the build container); the fixtures
+themselves travel with the repo and are what the GPU-box tests read.
+
+    python tests/golden/make_golden.py
+"""
+from __future__ import annotations
+
+import hashlib
+import os
+import sys
+import tempfile
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+from oracle import oracle as O  # noqa: E402
+
+# (name, instance args, fos, n, seed, generations, keep full per-gen populations)
+RUN_CASES = [
+    ("c1_int", ["--torus", 10, 10, "--weights", "int:1:10", "--inst-seed", 1], "univariate", 32, 1, 20, True),
+    ("c1_pm5", ["--torus", 10, 10, "--weights", "int:-5:5", "--inst-seed", 1], "univariate", 32, 3, 20, True),
+    ("torus6_w", ["--torus", 6, 6, "--weights", "int:-3:5", "--inst-seed", 17], "univariate", 16, 91, 5, True),
+    ("neigh12", ["--torus", 12, 12, "--weights", "int:1:10", "--inst-seed", 2], "neigh", 64, 5, 10, True),
+    ("neigh_n40", ["--torus", 9, 7, "--weights", "int:-4:6", "--inst-seed", 4], "neigh", 40, 11, 8, True),
+    ("bflt10_40x40", ["--torus", 40, 40, "--weights", "unit", "--inst-seed", 1], "bflt:10", 16, 7, 50, False),
+    ("bflt4_8x8", ["--torus", 8, 8, "--weights", "int:1:9", "--inst-seed", 3], "bflt:4", 24, 2, 10, True),
+    ("reg4_float", ["@reg", 60, 4, 21], "univariate", 32, 4, 10, True),
+    ("reg3_float_neigh", ["@reg", 50, 3, 22], "neigh", 48, 6, 8, True),
+    ("c2_small_gens", ["--torus", 100, 100, "--weights", "int:1:10", "--inst-seed", 1], "neigh", 64, 1, 2, False),
+]
+
+COLOR_CASES = [
+    ("col_torus10_uni", ["--torus", 10, 10, "--weights", "unit"], "univariate"),
+    ("col_torus10_neigh", ["--torus", 10, 10, "--weights", "unit"], "neigh"),
+    ("col_torus100_neigh", ["--torus", 100, 100, "--weights", "unit"], "neigh"),
+    ("col_torus7x5_uni", ["--torus", 7, 5, "--weights", "unit"], "univariate"),
+    ("col_torus40_bflt10", ["--torus", 40, 40, "--weights", "unit"], "bflt:10"),
+    ("col_reg8", ["@reg", 200, 8, 31], "univariate"),
+    ("col_reg5odd", ["@reg", 64, 5, 32], "neigh"),
+]
+
+
+def random_regular(nv: int, d: int, seed: int):
+    """Random d-regular simple graph (configuration-model pairing, redrawn on
+    self-loops/duplicates) with fp64 weights uniform in [0, 1).  The reference
+    has no d-regular generator; this one only has to be
+    deterministic, since fixtures store the edge list itself."""
+    rs = np.random.RandomState(seed)
+    assert nv * d % 2 == 0
+    while True:
+        stubs = np.repeat(np.arange(nv), d)
+        rs.shuffle(stubs)
+        a, b = stubs[0::2], stubs[1::2]
+        u, v = np.minimum(a, b), np.maximum(a, b)
+        if (u == v).any():
+            continue
+        key = u.astype(np.int64) * nv + v
+        if len(np.unique(key)) != len(key):
+            continue
+        order = np.lexsort((v, u))
+        w = rs.random_sample(len(u))
+        return nv, u[order].astype(np.uint32), v[order].astype(np.uint32), w
+
+
+def write_edge_list(path, nv, u, v, w):
+    """maxcut.hpp:160-226 format (1-based, shortest round-trip floats)."""
+    with open(path, "w") as fh:
+        fh.write(f"{nv} {len(u)}\n")
+        for a, b, x in zip(u, v, w):
+            fh.write(f"{a + 1} {b + 1} {repr(float(x))}\n")
+
+
+def instance_args(spec, tmp):
+    if spec and spec[0] == "@reg":
+        nv, u, v, w = random_regular(spec[1], spec[2], spec[3])
+        path = os.path.join(tmp, f"reg_{spec[1]}_{spec[2]}_{spec[3]}.txt")
+        write_edge_list(path, nv, u, v, w)
+        return ["--edges", path]
+    return [str(x) for x in spec]
+
+
+def pop_hash(g: np.ndarray) -> np.uint64:
+    return np.frombuffer(hashlib.sha256(g.tobytes()).digest()[:8], np.uint64)[0]
+
+
+def main():
+    with tempfile.TemporaryDirectory() as tmp:
+        for name, inst, fos, n, seed, gens, full in RUN_CASES:
+            out = os.path.join(tmp, name + ".bin")
+            d = O.run_ref("run", *instance_args(inst, tmp), "--fos", fos, "--n", n, "--seed", seed,
+                          "--gens", gens, "--workers", 3, out=out)
+            d["n"] = np.array([n], np.uint64)
+            d["seed"] = np.array([seed], np.uint64)
+            d["gens"] = np.array([gens], np.uint64)
+            d["fos_kind"] = np.array([fos])
+            nv = int(d["num_vertices"][0])
+            pops = d["genotypes"].reshape(gens, n, nv)
+            d["pop_hash"] = np.array([pop_hash(p) for p in pops], np.uint64)
+            if not full:
+                d["final_genotypes"] = pops[-1].ravel().copy()
+                for key in ("genotypes", "donor", "delta", "present", "accept"):
+                    d.pop(key)
+            np.savez_compressed(os.path.join(HERE, name + ".npz"), **d)
+            print(f"{name}: nv={nv} groups={len(d['group_off']) - 1} "
+                  f"best={d['elitist'][-1]} trace={len(d['trace_fitness'])}")
+        for name, inst, fos in COLOR_CASES:
+            out = os.path.join(tmp, name + ".bin")
+            d = O.run_ref("color", *instance_args(inst, tmp), "--fos", fos, out=out)
+            d["fos_kind"] = np.array([fos])
+            np.savez_compressed(os.path.join(HERE, name + ".npz"), **d)
+            print(f"{name}: sets={len(d['set_off']) - 1} groups={len(d['group_off']) - 1} "
+                  f"lmig_edges={int(d['lmig_edges'][0])}")
+
+
+if __name__ == "__main__":
+    main()
