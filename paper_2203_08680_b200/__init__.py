@@ -1,0 +1,16 @@
+"""B200-native parallel Gene-pool Optimal Mixing (GOM) on Max-Cut.
+
+Hot path: hand-written sm_100a CUDA in libgomix_b200.so behind the C-ABI of
+include/gomix_gpu.h.  There is no CPU fallback: without the library (or a
+GPU) the engine raises.
+"""
+from .maxcut import (Fos, MaxCutInstance, generate_regular, generate_torus, load_edge_list,  # noqa: F401
+                     neighbourhood_fos, save_edge_list, univariate_fos)
+from .engine import (FitnessComparator, GpuParallelEngine, GpuProblem, RecordingSink,  # noqa: F401
+                     RunContext, RunControl, TerminationConfig, TraceSink, gpu_color, mix64,
+                     population_seed)
+
+__all__ = ["Fos", "MaxCutInstance", "generate_regular", "generate_torus", "load_edge_list", "neighbourhood_fos",
+           "save_edge_list", "univariate_fos", "FitnessComparator", "GpuParallelEngine", "GpuProblem",
+           "RecordingSink", "RunContext", "RunControl", "TerminationConfig", "TraceSink", "gpu_color", "mix64",
+           "population_seed"]

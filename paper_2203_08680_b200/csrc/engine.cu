@@ -1,0 +1,908 @@
+// engine.cu — host side of libgomix_b200: problem construction (validation,
+// CSR build), the per-population engine (ParallelEngine,
+// engine_parallel.hpp:255-368) and the C-ABI of include/gomix_gpu.h.
+//
+// Host work per generation is O(k) launches in Philox mode and one stream
+// sync; the device keeps population, fitness, elitist and the run-control
+// block resident across generations.  Replay mode additionally brings the
+// packed population back once per group to draw donors exactly like the
+// reference's sequential RngStream (engine_parallel.hpp:104-121).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "gomix_gpu.h"
+#include "internal.cuh"
+
+namespace gomix_b200 {
+void build_problem_device_impl(Problem& P, const int32_t* given_colour, const int32_t* eid);
+}
+
+using namespace gomix_b200;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return GOMIX_OK;
+  } catch (const GomixError& e) {
+    g_last_error = e.what();
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host out of memory";
+    return GOMIX_E_OOM;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return GOMIX_E_STATE;
+  }
+}
+
+// Region of DevCtl written by the host at the start of every call.
+constexpr size_t kCallOffset = offsetof(DevCtl, stop);
+
+uint32_t next_pow2(uint32_t x) {
+  uint32_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+}  // namespace
+
+// ===========================================================================
+// problem
+// ===========================================================================
+struct gomix_gpu_problem {
+  std::unique_ptr<Problem> P;
+};
+
+namespace {
+
+// validate_instance (maxcut.hpp:39-54) + Fos sanity (linkage.hpp:279-309) and
+// the CSR build: row v = edges (a, v), a < v, then (v, b), b > v, both in edge
+// order -> ascending neighbour = ascending edge id (the reference's order).
+std::unique_ptr<Problem> create_problem(const gomix_maxcut* inst, const gomix_fos* fos,
+                                        const int32_t* colour, int32_t device) {
+  if (!inst || !fos) invalid("problem: instance and fos are required");
+  const uint64_t nv = inst->num_vertices, q = inst->num_edges, m = fos->num_sets;
+  if (nv == 0) invalid("maxcut: instance needs at least one vertex");
+  if (nv >= (1ull << 31)) invalid("maxcut: at most 2^31-1 vertices");
+  if (q >= (1ull << 30)) invalid("maxcut: at most 2^30-1 edges");
+  if (q && (!inst->edge_u || !inst->edge_v || !inst->edge_w)) invalid("maxcut: missing edge arrays");
+  bool exact = true;
+  double maxw = 0.0;
+  for (uint64_t i = 0; i < q; ++i) {
+    const uint32_t u = inst->edge_u[i], v = inst->edge_v[i];
+    const double w = inst->edge_w[i];
+    if (u >= v) invalid("maxcut: edge endpoints must satisfy u < v");
+    if (v >= nv) invalid("maxcut: edge endpoint out of range");
+    if (!std::isfinite(w)) invalid("maxcut: non-finite edge weight");
+    if (i > 0) {
+      const uint32_t pu = inst->edge_u[i - 1], pv = inst->edge_v[i - 1];
+      if (pu > u || (pu == u && pv >= v)) invalid("maxcut: edges must be sorted and unique");
+    }
+    if (w != std::floor(w) || std::fabs(w) > 9e15) exact = false;
+    maxw = std::max(maxw, std::fabs(w));
+  }
+  if (m == 0) invalid("fos: needs at least one linkage set");
+  if (!fos->set_offset || !fos->set_vars) invalid("fos: missing arrays");
+  if (fos->set_offset[0] != 0) invalid("fos: set_offset[0] must be 0");
+
+  auto P = std::make_unique<Problem>();
+  P->nv = nv;
+  P->q = q;
+  P->m = m;
+  P->exact = exact;
+  P->h_set_off.assign(fos->set_offset, fos->set_offset + m + 1);
+  const uint64_t entries = P->h_set_off[m];
+  P->h_set_vars.assign(fos->set_vars, fos->set_vars + entries);
+  P->univariate = true;
+  for (uint64_t i = 0; i < m; ++i) {
+    const uint64_t a = P->h_set_off[i], b = P->h_set_off[i + 1];
+    if (b <= a) invalid("fos: set " + std::to_string(i) + " is empty");
+    if (b - a > (uint64_t)kMaxSetSize)
+      invalid("fos: set " + std::to_string(i) + " has more than 64 variables (unsupported)");
+    for (uint64_t t = a; t < b; ++t) {
+      if (P->h_set_vars[t] >= nv) invalid("scheduling: linkage set references unknown variable");
+      if (t > a && P->h_set_vars[t] <= P->h_set_vars[t - 1])
+        invalid("fos: set " + std::to_string(i) + " is not sorted and unique");
+    }
+    P->max_f = std::max<uint64_t>(P->max_f, b - a);
+    if (b - a != 1) P->univariate = false;
+  }
+  if (colour) {
+    for (uint64_t i = 0; i < m; ++i)
+      if (colour[i] < 0) invalid("colouring: negative colour");
+  }
+
+  if (device >= 0) GOMIX_CUDA(cudaSetDevice(device));
+  GOMIX_CUDA(cudaGetDevice(&P->device));
+
+  // CSR
+  std::vector<int32_t> row_ptr(nv + 1, 0), col(2 * q), eid(2 * q), wi(2 * q);
+  std::vector<double> w(2 * q);
+  std::vector<int64_t> indeg(nv, 0);
+  for (uint64_t i = 0; i < q; ++i) {
+    row_ptr[inst->edge_u[i] + 1]++;
+    row_ptr[inst->edge_v[i] + 1]++;
+    indeg[inst->edge_v[i]]++;
+  }
+  for (uint64_t v = 0; v < nv; ++v) row_ptr[v + 1] += row_ptr[v];
+  std::vector<int64_t> rev(nv), fwd(nv);
+  for (uint64_t v = 0; v < nv; ++v) {
+    rev[v] = row_ptr[v];
+    fwd[v] = row_ptr[v] + indeg[v];
+  }
+  uint64_t max_deg_sum = 0;
+  for (uint64_t i = 0; i < q; ++i) {
+    const uint32_t u = inst->edge_u[i], v = inst->edge_v[i];
+    const double x = inst->edge_w[i];
+    const int64_t a = fwd[u]++, b = rev[v]++;
+    col[a] = (int32_t)v;
+    col[b] = (int32_t)u;
+    eid[a] = eid[b] = (int32_t)i;
+    w[a] = w[b] = x;
+    wi[a] = wi[b] = exact && std::fabs(x) < 2147483648.0 ? (int32_t)x : 0;
+  }
+  for (uint64_t i = 0; i < m; ++i) {
+    uint64_t s = 0;
+    for (uint64_t t = P->h_set_off[i]; t < P->h_set_off[i + 1]; ++t)
+      s += (uint64_t)(row_ptr[P->h_set_vars[t] + 1] - row_ptr[P->h_set_vars[t]]);
+    max_deg_sum = std::max(max_deg_sum, s);
+  }
+  // int32 per-pair arithmetic is exact when |delta| <= max|w| * footprint < 2^30
+  P->i32 = exact && maxw * (double)std::max<uint64_t>(max_deg_sum, 1) < 1073741824.0;
+  if (P->univariate) {
+    for (uint64_t i = 0; i < m; ++i) {
+      const uint32_t v = P->h_set_vars[i];
+      P->max_fp = std::max<uint64_t>(P->max_fp, (uint64_t)(row_ptr[v + 1] - row_ptr[v]));
+    }
+  }
+
+  auto& A = P->allocations;
+  P->row_ptr = dev_alloc<int32_t>(A, nv + 1);
+  P->col = dev_alloc<int32_t>(A, 2 * q);
+  P->w = dev_alloc<double>(A, 2 * q);
+  P->wi = dev_alloc<int32_t>(A, 2 * q);
+  P->eu = dev_alloc<uint32_t>(A, q);
+  P->ev = dev_alloc<uint32_t>(A, q);
+  P->ew = dev_alloc<double>(A, q);
+  P->set_off = dev_alloc<int64_t>(A, m + 1);
+  P->set_vars = dev_alloc<uint32_t>(A, entries);
+  int32_t* d_eid = dev_alloc<int32_t>(A, 2 * q);
+  auto up = [](void* dst, const void* src, size_t bytes) {
+    if (bytes) GOMIX_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+  };
+  up(P->row_ptr, row_ptr.data(), (nv + 1) * 4);
+  up(P->col, col.data(), 2 * q * 4);
+  up(P->w, w.data(), 2 * q * 8);
+  up(P->wi, wi.data(), 2 * q * 4);
+  up(P->eu, inst->edge_u, q * 4);
+  up(P->ev, inst->edge_v, q * 4);
+  up(P->ew, inst->edge_w, q * 8);
+  std::vector<int64_t> so(P->h_set_off.begin(), P->h_set_off.end());
+  up(P->set_off, so.data(), (m + 1) * 8);
+  up(P->set_vars, P->h_set_vars.data(), entries * 4);
+  build_problem_device_impl(*P, colour, d_eid);
+  if (P->univariate) {
+    for (uint64_t i = 0; i < m; ++i) {
+      const uint32_t v = P->h_set_vars[i];
+      P->footprint[i] = (uint64_t)(row_ptr[v + 1] - row_ptr[v]);
+    }
+  }
+  return P;
+}
+
+}  // namespace
+
+// ===========================================================================
+// engine
+// ===========================================================================
+struct gomix_gpu_engine {
+  Problem* P = nullptr;
+  uint64_t n = 0;
+  uint32_t W = 0, Wp = 0, wpt = 1, tw = 1, block = 256, teams = 8, stage_words = 0;
+  size_t smem = 0;
+  int grid_cap = 1;
+  uint32_t mode = GOMIX_MODE_PHILOX, flags = 0;
+  int32_t pop_id = 1;
+  int epi_mode = 0;  // 0 exact atomics, 1 float partials, 2 ordered
+  bool record = false;
+  uint64_t seed = 1;
+
+  std::vector<void*> allocs;
+  uint32_t* pop = nullptr;
+  double* fit = nullptr;
+  double* dfit = nullptr;
+  double* part = nullptr;
+  int32_t* ham = nullptr;
+  int32_t* dham = nullptr;
+  uint32_t* elit = nullptr;
+  DevCtl* ctl = nullptr;
+  DevCtl* h_ctl = nullptr;  // pinned
+  unsigned long long* gsteps = nullptr;
+  unsigned long long* gcalls = nullptr;
+  double* impr = nullptr;
+  uint64_t impr_cap = 0;
+  int32_t* tape = nullptr;
+  int32_t* h_tape_pinned = nullptr;
+  int32_t* rec_donor = nullptr;
+  double* rec_delta = nullptr;
+  uint8_t* rec_present = nullptr;
+  uint8_t* rec_accept = nullptr;
+  uint64_t max_group = 0;
+
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  ReplayStream rng{1};
+  int64_t generation = 0;
+  bool initialized = false;
+  double elit_fit = 0.0;
+  std::vector<uint32_t> h_pop;
+  std::vector<uint64_t> perm;
+  int64_t last_group = -1;
+  uint64_t launches = 0;
+  std::vector<cudaEvent_t> ev_free;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pending;
+
+  ~gomix_gpu_engine() {
+    if (stream) cudaStreamSynchronize(stream);
+    for (auto& pr : ev_pending) {
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
+    for (auto e : ev_free) cudaEventDestroy(e);
+    for (void* p : allocs) cudaFree(p);
+    if (h_ctl) cudaFreeHost(h_ctl);
+    if (h_tape_pinned) cudaFreeHost(h_tape_pinned);
+    if (own_stream && stream) cudaStreamDestroy(stream);
+  }
+
+  bool exact() const { return P->exact; }
+
+  bool better(double a, double b) const {
+    if (exact()) return a > b;
+    return a - b > 1e-9 * std::max({1.0, std::fabs(a), std::fabs(b)});
+  }
+
+  void setup(const gomix_engine_config& cfg) {
+    n = cfg.population_size;
+    if (n == 0) invalid("engine: population must be non-empty");
+    if (cfg.mode != GOMIX_MODE_REPLAY && cfg.mode != GOMIX_MODE_PHILOX) invalid("engine: unknown mode");
+    if (cfg.world_size > 1) invalid("engine: multi-GPU sharding is driven by gomix_gpu_engine_create_sharded");
+    mode = cfg.mode;
+    flags = cfg.flags;
+    seed = cfg.seed;
+    pop_id = cfg.population_id ? cfg.population_id : 1;
+    rng = ReplayStream(seed);
+    W = (uint32_t)((n + 31) / 32);
+    if (W <= 8) {
+      Wp = next_pow2(W);
+      wpt = Wp;
+      tw = 1;
+      block = 256;
+    } else if (W <= 32) {
+      Wp = next_pow2(W);
+      wpt = 4;
+      tw = Wp / 4;
+      block = 32 * tw;
+    } else if (W <= 128) {
+      Wp = next_pow2(W);
+      wpt = 8;
+      tw = Wp / 8;
+      block = 32 * tw;
+    } else {
+      invalid("engine: population sizes above 4096 are not supported");
+    }
+    teams = block / 32 / tw;
+    stage_words = P->univariate ? 0 : (uint32_t)(P->max_f * Wp);
+    const size_t stage = (size_t)teams * 2 * stage_words * 4;
+    const size_t red = tw == 1 ? (size_t)teams * Wp * 32 * 12 : 0;
+    smem = std::max(stage, red);
+    if (smem > 227 * 1024) invalid("engine: set size x population too large for shared-memory staging");
+    record = (flags & GOMIX_FLAG_RECORD_BATCH) != 0;
+    const bool ordered = !P->exact && (mode == GOMIX_MODE_REPLAY || (flags & GOMIX_FLAG_ORDERED_FLOAT));
+    epi_mode = P->exact ? 0 : (ordered ? 2 : 1);
+
+    GOMIX_CUDA(cudaSetDevice(P->device));
+    GOMIX_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    own_stream = true;
+    int sms = 0;
+    GOMIX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, P->device));
+    const int per_sm = gom_max_blocks_per_sm(P->univariate, P->i32, (int)wpt, (int)block, smem);
+    if (per_sm < 1) invalid("engine: GOM kernel does not fit on an SM with this configuration");
+    grid_cap = per_sm * sms;
+    for (uint64_t c = 0; c < P->k; ++c)
+      max_group = std::max(max_group, P->group_off[c + 1] - P->group_off[c]);
+
+    const uint64_t nv = P->nv;
+    pop = dev_alloc<uint32_t>(allocs, nv * Wp);
+    fit = dev_alloc<double>(allocs, n);
+    dfit = dev_alloc<double>(allocs, n);
+    ham = dev_alloc<int32_t>(allocs, n);
+    dham = dev_alloc<int32_t>(allocs, n);
+    elit = dev_alloc<uint32_t>(allocs, (nv + 31) / 32);
+    ctl = dev_alloc<DevCtl>(allocs, 1);
+    gsteps = dev_alloc<unsigned long long>(allocs, P->k);
+    gcalls = dev_alloc<unsigned long long>(allocs, P->k);
+    impr_cap = std::min<uint64_t>(std::max<uint64_t>(4096, n * (P->k + 1)), 1ull << 22);
+    impr = dev_alloc<double>(allocs, impr_cap);
+    if (epi_mode == 1) part = dev_alloc<double>(allocs, (size_t)grid_cap * n);
+    tape = dev_alloc<int32_t>(allocs, max_group * n);
+    if (record || epi_mode == 2) {
+      rec_donor = dev_alloc<int32_t>(allocs, max_group * n);
+      rec_delta = dev_alloc<double>(allocs, max_group * n);
+      rec_present = dev_alloc<uint8_t>(allocs, max_group * n);
+      rec_accept = dev_alloc<uint8_t>(allocs, max_group * n);
+    }
+    GOMIX_CUDA(cudaMallocHost(&h_ctl, sizeof(DevCtl)));
+    GOMIX_CUDA(cudaMallocHost(&h_tape_pinned, std::max<uint64_t>(1, max_group * n) * sizeof(int32_t)));
+    std::memset(h_ctl, 0, sizeof(DevCtl));
+    h_ctl->elit_src = -1;
+    h_ctl->exact = P->exact;
+    h_ctl->q = (double)P->q;
+    GOMIX_CUDA(cudaMemcpy(ctl, h_ctl, sizeof(DevCtl), cudaMemcpyHostToDevice));
+    GOMIX_CUDA(cudaMemset(pop, 0, nv * Wp * 4));
+    GOMIX_CUDA(cudaMemset(gsteps, 0, P->k * 8));
+    GOMIX_CUDA(cudaMemset(gcalls, 0, P->k * 8));
+    GOMIX_CUDA(cudaMemset(dfit, 0, n * 8));
+    GOMIX_CUDA(cudaMemset(dham, 0, n * 4));
+  }
+
+  // ---- per-call control ------------------------------------------------------
+  void begin_call(const gomix_stop_criteria* stop) {
+    h_ctl->stop = 0;
+    h_ctl->stop_reason = GOMIX_STOP_NONE;
+    h_ctl->has_budget = stop && stop->has_max_evaluations;
+    h_ctl->has_target = stop && stop->has_target;
+    h_ctl->exact = P->exact;
+    h_ctl->max_evals = stop ? stop->max_evaluations : 0.0;
+    h_ctl->q = (double)P->q;
+    h_ctl->target = stop ? stop->target_fitness : 0.0;
+    h_ctl->calls_total = stop ? stop->evaluator_calls_before : 0;
+    h_ctl->grp_steps = h_ctl->grp_calls = 0;
+    h_ctl->run_steps = h_ctl->run_calls = h_ctl->groups_run = 0;
+    h_ctl->n_impr = 0;
+    GOMIX_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(ctl) + kCallOffset,
+                               reinterpret_cast<char*>(h_ctl) + kCallOffset,
+                               sizeof(DevCtl) - kCallOffset, cudaMemcpyHostToDevice, stream));
+  }
+
+  void read_ctl() {
+    GOMIX_CUDA(cudaMemcpyAsync(h_ctl, ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, stream));
+    GOMIX_CUDA(cudaStreamSynchronize(stream));
+  }
+
+  void fill_stats(gomix_run_stats* out) {
+    elit_fit = h_ctl->elit_fit;
+    if (!out) return;
+    out->groups_run = h_ctl->groups_run;
+    out->steps = h_ctl->run_steps;
+    out->evaluator_calls = h_ctl->run_calls;
+    out->stopped = h_ctl->stop;
+    out->stop_reason = h_ctl->stop_reason;
+    out->improvements = h_ctl->n_impr;
+    out->elitist_fitness = h_ctl->elit_fit;
+  }
+
+  RefreshArgs refresh_args() const {
+    RefreshArgs r;
+    r.pop = pop;
+    r.elit = elit;
+    r.ham = ham;
+    r.ctl = ctl;
+    r.nv = P->nv;
+    r.n = (uint32_t)n;
+    r.Wp = Wp;
+    const uint64_t warps = 148ull * 64;
+    const uint64_t per = std::max<uint64_t>(1, warps / Wp);
+    r.rows_per_chunk = (uint32_t)std::max<uint64_t>(64, (P->nv + per - 1) / per);
+    return r;
+  }
+
+  void refresh() {
+    const RefreshArgs r = refresh_args();
+    launch_refresh(r, 148 * 8, stream);
+    ++launches;
+  }
+
+  EpiArgs epi_args(uint64_t group, uint32_t G, uint32_t nparts) const {
+    EpiArgs e;
+    e.fit = fit;
+    e.part = part;
+    e.dfit = dfit;
+    e.ham = ham;
+    e.dham = dham;
+    e.rec_delta = rec_delta;
+    e.rec_accept = rec_accept;
+    e.ctl = ctl;
+    e.gsteps = gsteps;
+    e.gcalls = gcalls;
+    e.impr = impr;
+    e.impr_cap = impr_cap;
+    e.n = (uint32_t)n;
+    e.G = G;
+    e.nparts = nparts;
+    e.group = (uint32_t)group;
+    e.mode = epi_mode;
+    return e;
+  }
+
+  // ---- one batched group step -----------------------------------------------
+  void launch_group(uint64_t group, bool with_tape) {
+    const uint64_t g0 = P->group_off[group], G = P->group_off[group + 1] - g0;
+    GomArgs a;
+    a.row_ptr = P->row_ptr;
+    a.col = P->col;
+    a.w = P->w;
+    a.wi = P->wi;
+    a.set_off = P->set_off;
+    a.set_vars = P->set_vars;
+    a.fp_off = P->fp_off;
+    a.fp = P->fp;
+    a.gsets = P->gsets + g0;
+    a.G = (uint32_t)G;
+    a.pop = pop;
+    a.fit = fit;
+    a.ham = ham;
+    a.elit = elit;
+    a.dfit = epi_mode == 0 ? dfit : nullptr;
+    a.part = epi_mode == 1 ? part : nullptr;
+    a.dham = dham;
+    a.ctl = ctl;
+    a.tape = with_tape ? tape : nullptr;
+    const bool rec = record || epi_mode == 2;
+    a.rec_donor = rec ? rec_donor : nullptr;
+    a.rec_delta = rec ? rec_delta : nullptr;
+    a.rec_present = rec ? rec_present : nullptr;
+    a.rec_accept = rec ? rec_accept : nullptr;
+    a.n = (uint32_t)n;
+    a.Wp = Wp;
+    a.team_warps = tw;
+    a.stage_words = stage_words;
+    a.exact = P->exact;
+    a.generation = (uint32_t)generation;
+    a.seed = seed;
+    const uint64_t want = (G + teams - 1) / teams;
+    const int grid = (int)std::min<uint64_t>(want, (uint64_t)grid_cap);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (flags & GOMIX_FLAG_TIME_KERNELS) {
+      e0 = take_event();
+      e1 = take_event();
+      GOMIX_CUDA(cudaEventRecord(e0, stream));
+    }
+    launch_gom(a, P->univariate, P->i32, (int)wpt, grid, (int)block, smem, stream);
+    if (e1) {
+      GOMIX_CUDA(cudaEventRecord(e1, stream));
+      ev_pending.push_back({e0, e1});
+    }
+    launch_epilogue(epi_args(group, (uint32_t)G, (uint32_t)grid), stream);
+    launches += 2;
+    refresh();
+    last_group = (int64_t)group;
+  }
+
+  cudaEvent_t take_event() {
+    if (!ev_free.empty()) {
+      cudaEvent_t e = ev_free.back();
+      ev_free.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    GOMIX_CUDA(cudaEventCreate(&e));
+    return e;
+  }
+
+  // ---- replay: the reference's sequential donor draws ----------------------
+  // insert_donor_genes (engine_parallel.hpp:110-120) + select_donor
+  // (engine_serial.hpp:30-46) against the group-start population.
+  void draw_replay_tape(uint64_t group) {
+    const uint64_t nv = P->nv;
+    h_pop.resize(nv * Wp);
+    GOMIX_CUDA(cudaMemcpyAsync(h_pop.data(), pop, nv * Wp * 4, cudaMemcpyDeviceToHost, stream));
+    GOMIX_CUDA(cudaStreamSynchronize(stream));
+    const uint64_t g0 = P->group_off[group], G = P->group_off[group + 1] - g0;
+    perm.resize(n);
+    auto bit = [&](uint32_t v, uint64_t s) { return (h_pop[(uint64_t)v * Wp + (s >> 5)] >> (s & 31)) & 1u; };
+    for (uint64_t p = 0; p < G; ++p) {
+      const uint64_t sid = P->group_sets[g0 + p];
+      const uint32_t* vars = P->h_set_vars.data() + P->h_set_off[sid];
+      const uint64_t f = P->h_set_off[sid + 1] - P->h_set_off[sid];
+      for (uint64_t s = 0; s < n; ++s) {
+        for (uint64_t i = 0; i < n; ++i) perm[i] = i;
+        int32_t donor = -1;
+        for (uint64_t i = 0; i < n && donor < 0; ++i) {
+          const uint64_t j = i + rng.uniform_index(n - i);
+          std::swap(perm[i], perm[j]);
+          const uint64_t c = perm[i];
+          for (uint64_t t = 0; t < f; ++t)
+            if (bit(vars[t], c) != bit(vars[t], s)) {
+              donor = (int32_t)c;
+              break;
+            }
+        }
+        h_tape_pinned[p * n + s] = donor;
+      }
+    }
+    GOMIX_CUDA(cudaMemcpyAsync(tape, h_tape_pinned, G * n * 4, cudaMemcpyHostToDevice, stream));
+  }
+
+  void upload_tape(uint64_t group, const int32_t* donor_sp) {
+    const uint64_t g0 = P->group_off[group], G = P->group_off[group + 1] - g0;
+    for (uint64_t s = 0; s < n; ++s)
+      for (uint64_t p = 0; p < G; ++p) {
+        const int32_t d = donor_sp[s * G + p];
+        if (d >= (int64_t)n) invalid("run_group: donor index out of range");
+        h_tape_pinned[p * n + s] = d < 0 ? -1 : d;
+      }
+    GOMIX_CUDA(cudaMemcpyAsync(tape, h_tape_pinned, G * n * 4, cudaMemcpyHostToDevice, stream));
+  }
+
+  // ---- API operations ---------------------------------------------------------
+  void init_population(const uint8_t* genotypes, const gomix_stop_criteria* stop,
+                       gomix_run_stats* out) {
+    if (initialized) throw GomixError(GOMIX_E_STATE, "init_population: already initialised");
+    const uint64_t nv = P->nv;
+    if (genotypes) {
+      for (uint64_t i = 0; i < n * nv; ++i)
+        if (genotypes[i] > 1) invalid("graybox: genotype value outside alphabet");
+      uint8_t* d_bytes = nullptr;
+      GOMIX_CUDA(cudaMallocAsync(&d_bytes, n * nv, stream));
+      GOMIX_CUDA(cudaMemcpyAsync(d_bytes, genotypes, n * nv, cudaMemcpyHostToDevice, stream));
+      launch_pack(d_bytes, pop, nv, (uint32_t)n, Wp, stream);
+      GOMIX_CUDA(cudaFreeAsync(d_bytes, stream));
+      ++launches;
+    } else if (mode == GOMIX_MODE_REPLAY) {
+      // n*l draws of uniform_index(2) = low bit of each output (rng.hpp:28-35,
+      // threshold 0), solution-major (engine_parallel.hpp:334-336)
+      std::vector<uint32_t> words(nv * Wp, 0);
+      for (uint64_t s = 0; s < n; ++s)
+        for (uint64_t v = 0; v < nv; ++v)
+          if (rng.uniform_index(2)) words[v * Wp + (s >> 5)] |= 1u << (s & 31);
+      GOMIX_CUDA(cudaMemcpyAsync(pop, words.data(), nv * Wp * 4, cudaMemcpyHostToDevice, stream));
+      GOMIX_CUDA(cudaStreamSynchronize(stream));
+    } else {
+      launch_philox_init(pop, nv, (uint32_t)n, Wp, seed, stream);
+      ++launches;
+    }
+    launch_full_eval(*P, pop, fit, (uint32_t)n, Wp, !P->exact, stream);
+    ++launches;
+    begin_call(stop);
+    launch_init_epilogue(epi_args(0, 0, 0), stream);
+    ++launches;
+    refresh();
+    read_ctl();
+    fill_stats(out);
+    initialized = true;
+  }
+
+  void run_generation(const gomix_stop_criteria* stop, gomix_run_stats* out) {
+    if (!initialized) throw GomixError(GOMIX_E_STATE, "run_generation: population not initialised");
+    begin_call(stop);
+    std::vector<uint64_t> order;
+    rng.permutation(order, P->k);  // engine_parallel.hpp:291
+    for (uint64_t gi : order) {
+      if (mode == GOMIX_MODE_REPLAY) {
+        if (gi != order.front()) {
+          read_ctl();
+          if (h_ctl->stop) break;
+        }
+        draw_replay_tape(gi);
+      }
+      launch_group(gi, mode == GOMIX_MODE_REPLAY);
+    }
+    read_ctl();
+    fill_stats(out);
+    if (!h_ctl->stop) ++generation;  // engine_parallel.hpp:311-314
+  }
+
+  void run_group(uint64_t group, const int32_t* donor_tape, const gomix_stop_criteria* stop,
+                 gomix_run_stats* out) {
+    if (!initialized) throw GomixError(GOMIX_E_STATE, "run_group: population not initialised");
+    if (group >= P->k) invalid("run_group: group index out of range");
+    begin_call(stop);
+    bool with_tape = true;
+    if (donor_tape)
+      upload_tape(group, donor_tape);
+    else if (mode == GOMIX_MODE_REPLAY)
+      draw_replay_tape(group);
+    else
+      with_tape = false;
+    launch_group(group, with_tape);
+    read_ctl();
+    fill_stats(out);
+  }
+};
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+extern "C" {
+
+int gomix_gpu_abi_version(void) { return GOMIX_GPU_ABI_VERSION; }
+
+const char* gomix_gpu_last_error(void) { return g_last_error.c_str(); }
+
+int gomix_gpu_problem_create(const gomix_maxcut* instance, const gomix_fos* fos,
+                             const int32_t* set_colour, int32_t device, gomix_gpu_problem** out) {
+  return guarded([&] {
+    if (!out) invalid("problem_create: out is NULL");
+    *out = nullptr;
+    auto h = std::make_unique<gomix_gpu_problem>();
+    h->P = create_problem(instance, fos, set_colour, device);
+    *out = h.release();
+  });
+}
+
+int gomix_gpu_problem_destroy(gomix_gpu_problem* p) {
+  return guarded([&] { delete p; });
+}
+
+int gomix_gpu_problem_info(const gomix_gpu_problem* p, gomix_problem_info* out) {
+  return guarded([&] {
+    if (!p || !out) invalid("problem_info: NULL argument");
+    const Problem& P = *p->P;
+    out->num_vertices = P.nv;
+    out->num_edges = P.q;
+    out->num_sets = P.m;
+    out->num_groups = P.k;
+    out->lmig_edges = P.lmig_edges;
+    out->max_set_size = P.max_f;
+    out->exact = P.exact;
+    out->univariate = P.univariate;
+  });
+}
+
+int gomix_gpu_problem_groups(const gomix_gpu_problem* p, uint64_t* group_offset,
+                             uint64_t* group_sets) {
+  return guarded([&] {
+    if (!p) invalid("problem_groups: NULL problem");
+    if (group_offset) std::copy(p->P->group_off.begin(), p->P->group_off.end(), group_offset);
+    if (group_sets) std::copy(p->P->group_sets.begin(), p->P->group_sets.end(), group_sets);
+  });
+}
+
+int gomix_gpu_problem_footprints(const gomix_gpu_problem* p, uint64_t* footprint) {
+  return guarded([&] {
+    if (!p || !footprint) invalid("problem_footprints: NULL argument");
+    std::copy(p->P->footprint.begin(), p->P->footprint.end(), footprint);
+  });
+}
+
+int gomix_gpu_engine_create(gomix_gpu_problem* p, const gomix_engine_config* cfg,
+                            gomix_gpu_engine** out) {
+  return guarded([&] {
+    if (!p || !cfg || !out) invalid("engine_create: NULL argument");
+    *out = nullptr;
+    auto e = std::make_unique<gomix_gpu_engine>();
+    e->P = p->P.get();
+    e->setup(*cfg);
+    *out = e.release();
+  });
+}
+
+int gomix_gpu_engine_destroy(gomix_gpu_engine* e) {
+  return guarded([&] { delete e; });
+}
+
+int gomix_gpu_set_stream(gomix_gpu_engine* e, void* cuda_stream) {
+  return guarded([&] {
+    if (!e) invalid("set_stream: NULL engine");
+    GOMIX_CUDA(cudaStreamSynchronize(e->stream));
+    if (e->own_stream) GOMIX_CUDA(cudaStreamDestroy(e->stream));
+    if (cuda_stream) {
+      e->stream = static_cast<cudaStream_t>(cuda_stream);
+      e->own_stream = false;
+    } else {
+      GOMIX_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+      e->own_stream = true;
+    }
+  });
+}
+
+int gomix_gpu_init_population(gomix_gpu_engine* e, const uint8_t* genotypes,
+                              const gomix_stop_criteria* stop, gomix_run_stats* out) {
+  return guarded([&] {
+    if (!e) invalid("init_population: NULL engine");
+    e->init_population(genotypes, stop, out);
+  });
+}
+
+int gomix_gpu_run_generation(gomix_gpu_engine* e, const gomix_stop_criteria* stop,
+                             gomix_run_stats* out) {
+  return guarded([&] {
+    if (!e) invalid("run_generation: NULL engine");
+    e->run_generation(stop, out);
+  });
+}
+
+int gomix_gpu_run_group(gomix_gpu_engine* e, uint64_t group, const int32_t* donor_tape,
+                        const gomix_stop_criteria* stop, gomix_run_stats* out) {
+  return guarded([&] {
+    if (!e) invalid("run_group: NULL engine");
+    e->run_group(group, donor_tape, stop, out);
+  });
+}
+
+int gomix_gpu_read_batch(gomix_gpu_engine* e, int32_t* donor, double* delta, uint8_t* present,
+                         uint8_t* accept) {
+  return guarded([&] {
+    if (!e) invalid("read_batch: NULL engine");
+    if (!e->record) throw GomixError(GOMIX_E_STATE, "read_batch: engine created without GOMIX_FLAG_RECORD_BATCH");
+    if (e->last_group < 0) throw GomixError(GOMIX_E_STATE, "read_batch: no group has run");
+    const uint64_t g = (uint64_t)e->last_group;
+    const uint64_t G = e->P->group_off[g + 1] - e->P->group_off[g], n = e->n, pairs = G * n;
+    std::vector<int32_t> d(pairs);
+    std::vector<double> de(pairs);
+    std::vector<uint8_t> pr(pairs), ac(pairs);
+    GOMIX_CUDA(cudaMemcpyAsync(d.data(), e->rec_donor, pairs * 4, cudaMemcpyDeviceToHost, e->stream));
+    GOMIX_CUDA(cudaMemcpyAsync(de.data(), e->rec_delta, pairs * 8, cudaMemcpyDeviceToHost, e->stream));
+    GOMIX_CUDA(cudaMemcpyAsync(pr.data(), e->rec_present, pairs, cudaMemcpyDeviceToHost, e->stream));
+    GOMIX_CUDA(cudaMemcpyAsync(ac.data(), e->rec_accept, pairs, cudaMemcpyDeviceToHost, e->stream));
+    GOMIX_CUDA(cudaStreamSynchronize(e->stream));
+    for (uint64_t p = 0; p < G; ++p)
+      for (uint64_t s = 0; s < n; ++s) {
+        const uint64_t src = p * n + s, dst = s * G + p;
+        if (donor) donor[dst] = d[src];
+        if (delta) delta[dst] = de[src];
+        if (present) present[dst] = pr[src];
+        if (accept) accept[dst] = ac[src];
+      }
+  });
+}
+
+int gomix_gpu_read_population(gomix_gpu_engine* e, uint8_t* genotypes, double* fitness) {
+  return guarded([&] {
+    if (!e) invalid("read_population: NULL engine");
+    if (genotypes) {
+      const uint64_t bytes = e->n * e->P->nv;
+      uint8_t* d = nullptr;
+      GOMIX_CUDA(cudaMallocAsync(&d, bytes, e->stream));
+      launch_unpack(e->pop, d, e->P->nv, (uint32_t)e->n, e->Wp, e->stream);
+      ++e->launches;
+      GOMIX_CUDA(cudaMemcpyAsync(genotypes, d, bytes, cudaMemcpyDeviceToHost, e->stream));
+      GOMIX_CUDA(cudaFreeAsync(d, e->stream));
+    }
+    if (fitness)
+      GOMIX_CUDA(cudaMemcpyAsync(fitness, e->fit, e->n * 8, cudaMemcpyDeviceToHost, e->stream));
+    GOMIX_CUDA(cudaStreamSynchronize(e->stream));
+  });
+}
+
+int gomix_gpu_read_population_packed(gomix_gpu_engine* e, uint32_t* words, uint64_t* words_per_var) {
+  return guarded([&] {
+    if (!e) invalid("read_population_packed: NULL engine");
+    if (words_per_var) *words_per_var = e->Wp;
+    if (words) {
+      GOMIX_CUDA(cudaMemcpyAsync(words, e->pop, e->P->nv * e->Wp * 4, cudaMemcpyDeviceToHost, e->stream));
+      GOMIX_CUDA(cudaStreamSynchronize(e->stream));
+    }
+  });
+}
+
+int gomix_gpu_read_elitist(gomix_gpu_engine* e, uint8_t* genotype, double* fitness) {
+  return guarded([&] {
+    if (!e) invalid("read_elitist: NULL engine");
+    if (!e->initialized) throw GomixError(GOMIX_E_STATE, "read_elitist: population not initialised");
+    if (genotype) {
+      uint8_t* d = nullptr;
+      GOMIX_CUDA(cudaMallocAsync(&d, e->P->nv, e->stream));
+      launch_unpack_elitist(e->elit, d, e->P->nv, e->stream);
+      ++e->launches;
+      GOMIX_CUDA(cudaMemcpyAsync(genotype, d, e->P->nv, cudaMemcpyDeviceToHost, e->stream));
+      GOMIX_CUDA(cudaFreeAsync(d, e->stream));
+    }
+    GOMIX_CUDA(cudaStreamSynchronize(e->stream));
+    if (fitness) *fitness = e->elit_fit;
+  });
+}
+
+int gomix_gpu_offer_elitist(gomix_gpu_engine* e, const uint8_t* genotype, double fitness,
+                            int32_t* adopted) {
+  return guarded([&] {
+    if (!e || !genotype) invalid("offer_elitist: NULL argument");
+    if (!e->initialized) throw GomixError(GOMIX_E_STATE, "offer_elitist: population not initialised");
+    const bool take = e->better(fitness, e->elit_fit);
+    if (adopted) *adopted = take;
+    if (!take) return;
+    const uint64_t nv = e->P->nv;
+    uint8_t* d = nullptr;
+    GOMIX_CUDA(cudaMallocAsync(&d, nv, e->stream));
+    GOMIX_CUDA(cudaMemcpyAsync(d, genotype, nv, cudaMemcpyHostToDevice, e->stream));
+    launch_pack_elitist(d, e->elit, nv, e->stream);
+    GOMIX_CUDA(cudaFreeAsync(d, e->stream));
+    e->h_ctl->elit_fit = fitness;
+    e->h_ctl->elit_src = -2;
+    GOMIX_CUDA(cudaMemcpyAsync(e->ctl, e->h_ctl, offsetof(DevCtl, stop), cudaMemcpyHostToDevice,
+                               e->stream));
+    GOMIX_CUDA(cudaMemsetAsync(e->ham, 0, e->n * 4, e->stream));
+    e->refresh();
+    ++e->launches;
+    GOMIX_CUDA(cudaStreamSynchronize(e->stream));
+    e->elit_fit = fitness;
+  });
+}
+
+int gomix_gpu_read_improvements(gomix_gpu_engine* e, double* fitness, uint64_t capacity,
+                                uint64_t* count) {
+  return guarded([&] {
+    if (!e) invalid("read_improvements: NULL engine");
+    const uint64_t avail = std::min<uint64_t>(e->h_ctl->n_impr, e->impr_cap);
+    const uint64_t take = fitness ? std::min(avail, capacity) : 0;
+    if (take) {
+      GOMIX_CUDA(cudaMemcpyAsync(fitness, e->impr, take * 8, cudaMemcpyDeviceToHost, e->stream));
+      GOMIX_CUDA(cudaStreamSynchronize(e->stream));
+    }
+    if (count) *count = fitness ? take : avail;
+  });
+}
+
+int gomix_gpu_group_counters(gomix_gpu_engine* e, uint64_t* sets, uint64_t* steps,
+                             uint64_t* evaluator_calls) {
+  return guarded([&] {
+    if (!e) invalid("group_counters: NULL engine");
+    const uint64_t k = e->P->k;
+    if (sets)
+      for (uint64_t c = 0; c < k; ++c) sets[c] = e->P->group_off[c + 1] - e->P->group_off[c];
+    if (steps) GOMIX_CUDA(cudaMemcpyAsync(steps, e->gsteps, k * 8, cudaMemcpyDeviceToHost, e->stream));
+    if (evaluator_calls)
+      GOMIX_CUDA(cudaMemcpyAsync(evaluator_calls, e->gcalls, k * 8, cudaMemcpyDeviceToHost, e->stream));
+    GOMIX_CUDA(cudaStreamSynchronize(e->stream));
+  });
+}
+
+int gomix_gpu_generation(gomix_gpu_engine* e, int64_t* generation) {
+  return guarded([&] {
+    if (!e || !generation) invalid("generation: NULL argument");
+    *generation = e->generation;
+  });
+}
+
+int gomix_gpu_kernel_times(gomix_gpu_engine* e, float* ms, uint64_t capacity, uint64_t* count) {
+  return guarded([&] {
+    if (!e) invalid("kernel_times: NULL engine");
+    GOMIX_CUDA(cudaStreamSynchronize(e->stream));
+    uint64_t written = 0;
+    for (auto& pr : e->ev_pending) {
+      float t = 0.f;
+      GOMIX_CUDA(cudaEventElapsedTime(&t, pr.first, pr.second));
+      if (ms && written < capacity) ms[written] = t;
+      ++written;
+      e->ev_free.push_back(pr.first);
+      e->ev_free.push_back(pr.second);
+    }
+    e->ev_pending.clear();
+    if (count) *count = ms ? std::min(written, capacity) : written;
+  });
+}
+
+int gomix_gpu_launch_count(gomix_gpu_engine* e, uint64_t* count) {
+  return guarded([&] {
+    if (!e || !count) invalid("launch_count: NULL argument");
+    *count = e->launches;
+  });
+}
+
+int gomix_gpu_color(const gomix_maxcut* instance, const gomix_fos* fos, int32_t device,
+                    int32_t* set_colour, uint64_t* num_groups, uint64_t* lmig_edges) {
+  return guarded([&] {
+    auto P = create_problem(instance, fos, nullptr, device);
+    if (set_colour)
+      for (uint64_t c = 0; c < P->k; ++c)
+        for (uint64_t t = P->group_off[c]; t < P->group_off[c + 1]; ++t)
+          set_colour[P->group_sets[t]] = (int32_t)c;
+    if (num_groups) *num_groups = P->k;
+    if (lmig_edges) *lmig_edges = P->lmig_edges;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,835 @@
+// gom.cu — the hot path: one batched GOM step per colour class, plus its
+// epilogue (fitness commit, elitist scan, stop criteria) and the elitist
+// refresh, and the population init / full-evaluation kernels.
+//
+// Reference semantics (proj/include/gomix/engine_parallel.hpp):
+//   phase 1 insert_donor_genes        :104-121  -> donor per (s, set): replay tape
+//                                                  or counter-based Philox draw
+//   phase 2 parallel_partial_evals    :130-187  -> delta = sum_new - sum_old over the
+//                                                  set's footprint, ascending edge id
+//   phase 3 determine_improvements    :194-214  -> accept iff better, or equal and the
+//                                                  parent is not the elitist
+//   phase 4 apply_acceptance          :221-247  -> commit bits / fitness in place
+//   elitist scan                      :305-310  -> epilogue_kernel
+// all fused into gom_group_kernel: nothing per pair is materialised in HBM.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "internal.cuh"
+
+namespace gomix_b200 {
+
+// ---------------------------------------------------------------------------
+// Philox4x32-10 (Salmon et al., SC'11), counter-based: every (generation, set,
+// solution, call) has its own counter, so draws need no state and no order.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    k.x += 0x9E3779B9u;
+    k.y += 0xBB67AE85u;
+  }
+  return c;
+}
+
+__device__ __forceinline__ uint64_t lo64(uint4 r) { return (uint64_t)r.x | ((uint64_t)r.y << 32); }
+__device__ __forceinline__ uint64_t hi64(uint4 r) { return (uint64_t)r.z | ((uint64_t)r.w << 32); }
+// uniform in [0, n): high 64 bits of r*n (bias <= n / 2^64).
+__device__ __forceinline__ uint32_t bounded(uint64_t r, uint32_t n) {
+  return (uint32_t)__umul64hi(r, (uint64_t)n);
+}
+
+constexpr uint32_t kTagGom = 0x474F4D00u;   // "GOM"
+constexpr uint32_t kTagInit = 0x494E4900u;  // "INI"
+
+// FitnessComparator (graybox.hpp:22-35).
+__device__ __forceinline__ double cmp_scale(double a, double b) {
+  return 1e-9 * fmax(1.0, fmax(fabs(a), fabs(b)));
+}
+__device__ __forceinline__ bool cmp_better(bool exact, double a, double b) {
+  return exact ? a > b : a - b > cmp_scale(a, b);
+}
+__device__ __forceinline__ bool cmp_equal(bool exact, double a, double b) {
+  return exact ? a == b : fabs(a - b) <= cmp_scale(a, b);
+}
+
+__device__ __forceinline__ uint32_t valid_mask(uint32_t w, uint32_t n) {
+  const uint32_t lo = w * 32u;
+  if (lo + 32u <= n) return 0xFFFFFFFFu;
+  if (lo >= n) return 0u;
+  return (1u << (n - lo)) - 1u;
+}
+
+__device__ __forceinline__ void team_sync(uint32_t team_warps) {
+  if (team_warps == 1)
+    __syncwarp();
+  else
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// gom_group_kernel
+//
+// Work decomposition: a *team* (one warp, or the whole CTA when n > 256)
+// owns one linkage set at a time; inside the team, lane b of the warp that
+// holds word w is solution 32w+b, and each thread carries WPT words.  Teams
+// stride over the group's sets (persistent grid, sized to the SM count), so
+// per-solution fitness / elitist-distance deltas accumulate in registers and
+// reach HBM once per CTA.  Same-colour sets share no variable and no
+// interaction edge (scheduling.hpp:22-27), so teams update their rows in place
+// without races and without a shadow copy.
+// ---------------------------------------------------------------------------
+template <int WPT, bool UNIV, bool I32>
+__global__ void __launch_bounds__(512) gom_group_kernel(const GomArgs a) {
+  extern __shared__ __align__(16) uint32_t smem[];
+  if (*(volatile int32_t*)&a.ctl->stop) return;
+
+  using Acc = typename std::conditional<I32, long long, double>::type;
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const uint32_t tw = a.team_warps;
+  const uint32_t teams_per_cta = (blockDim.x >> 5) / tw;
+  const uint32_t team = warp / tw, wit = warp - team * tw;
+  const uint32_t tid_team = wit * 32u + lane, team_threads = tw * 32u;
+  const uint32_t Wp = a.Wp, n = a.n;
+  const bool exact = a.exact != 0;
+  const bool replay = a.tape != nullptr;
+  const bool record = a.rec_present != nullptr;
+  uint32_t* rowsF = smem + (size_t)team * 2u * a.stage_words;
+  uint32_t* newF = rowsF + a.stage_words;
+
+  Acc acc[WPT];
+  int32_t hacc[WPT];
+#pragma unroll
+  for (int j = 0; j < WPT; ++j) {
+    acc[j] = 0;
+    hacc[j] = 0;
+  }
+  uint32_t steps = 0;
+  unsigned long long calls = 0;
+
+  for (uint32_t p = blockIdx.x * teams_per_cta + team; p < a.G; p += gridDim.x * teams_per_cta) {
+    const uint32_t sid = a.gsets[p];
+    if constexpr (UNIV) {
+      // ---- univariate set {v}: the donor's value on v is forced to !x_v, so
+      // the pair is present iff some member holds the other value; the draw
+      // itself cannot change the outcome and is skipped in Philox mode.
+      const uint32_t v = a.set_vars[a.set_off[sid]];
+      const uint32_t* row = a.pop + (size_t)v * Wp;
+      uint32_t pw[WPT];
+#pragma unroll
+      for (int j = 0; j < WPT; ++j) pw[j] = row[wit + tw * j];
+      uint32_t ones = 0;
+      if (!replay) {
+        if (tw == 1) {
+#pragma unroll
+          for (int j = 0; j < WPT; ++j) ones += __popc(pw[j]);
+        } else {
+          for (uint32_t w = lane; w < Wp; w += 32) ones += __popc(row[w]);
+          ones = __reduce_add_sync(0xFFFFFFFFu, ones);
+        }
+      }
+      const uint32_t eb = (a.elit[v >> 5] >> (v & 31u)) & 1u;
+      const int32_t rs = a.row_ptr[v], re = a.row_ptr[v + 1];
+      const uint32_t deg = (uint32_t)(re - rs);
+      int32_t di[WPT];
+      double sn[WPT], so[WPT];
+#pragma unroll
+      for (int j = 0; j < WPT; ++j) {
+        di[j] = 0;
+        sn[j] = 0.0;
+        so[j] = 0.0;
+      }
+      for (int32_t e = rs; e < re; ++e) {
+        const uint32_t u = (uint32_t)a.col[e];
+        const uint32_t* urow = a.pop + (size_t)u * Wp;
+        if constexpr (I32) {
+          const int32_t wt = a.wi[e];
+#pragma unroll
+          for (int j = 0; j < WPT; ++j) {
+            const uint32_t cut_old = ((pw[j] ^ urow[wit + tw * j]) >> lane) & 1u;
+            di[j] += cut_old ? -wt : wt;
+          }
+        } else {
+          const double wt = a.w[e];
+#pragma unroll
+          for (int j = 0; j < WPT; ++j) {
+            const uint32_t cut_old = ((pw[j] ^ urow[wit + tw * j]) >> lane) & 1u;
+            sn[j] += cut_old ? 0.0 : wt;  // reference adds every value, 0.0 included
+            so[j] += cut_old ? wt : 0.0;
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < WPT; ++j) {
+        const uint32_t w = wit + tw * j;
+        const uint32_t s = w * 32u + lane;
+        const bool valid = s < n;
+        const uint32_t pv = (pw[j] >> lane) & 1u;
+        bool present;
+        int32_t dn = -1;
+        if (replay) {
+          dn = valid ? a.tape[(size_t)p * n + s] : -1;
+          present = dn >= 0;
+        } else {
+          present = valid && (pv ? (n - ones) : ones) > 0u;
+          dn = present ? (int32_t)n : -1;  // donor identity is not materialised
+        }
+        const double delta = I32 ? (double)di[j] : sn[j] - so[j];
+        bool accept = false;
+        if (present) {
+          const bool elit = a.ham[s] == 0;
+          if (exact) {
+            accept = delta > 0.0 || (delta == 0.0 && !elit);
+          } else {
+            const double pf = a.fit[s];
+            const double cand = pf + delta;
+            accept = cmp_better(false, cand, pf) || (cmp_equal(false, cand, pf) && !elit);
+          }
+        }
+        const uint32_t nb = accept ? (pv ^ 1u) : pv;
+        const uint32_t nw = __ballot_sync(0xFFFFFFFFu, nb);
+        if (lane == 0 && nw != pw[j]) a.pop[(size_t)v * Wp + w] = nw;
+        if (accept) {
+          acc[j] += I32 ? (Acc)di[j] : (Acc)delta;
+          hacc[j] += (pv == eb) ? 1 : -1;
+        }
+        steps += present ? 1u : 0u;
+        calls += present ? deg : 0u;
+        if (record && valid) {
+          const size_t at = (size_t)p * n + s;
+          a.rec_donor[at] = dn;
+          a.rec_delta[at] = present ? delta : 0.0;
+          a.rec_present[at] = present;
+          a.rec_accept[at] = accept;
+        }
+      }
+    } else {
+      // ---- general set F (|F| <= 64): stage F's rows (group-start values,
+      // the donor pool of engine_parallel.hpp:100-103) in shared memory.
+      const int64_t f0 = a.set_off[sid];
+      const uint32_t f = (uint32_t)(a.set_off[sid + 1] - f0);
+      const uint32_t* vars = a.set_vars + f0;
+      for (uint32_t idx = tid_team; idx < f * Wp; idx += team_threads) {
+        const uint32_t jv = idx / Wp, w = idx - jv * Wp;
+        rowsF[idx] = a.pop[(size_t)vars[jv] * Wp + w];
+      }
+      uint64_t em;
+      {
+        const uint32_t v0 = lane < f ? vars[lane] : 0u;
+        const uint32_t v1 = lane + 32u < f ? vars[lane + 32u] : 0u;
+        const uint32_t b0 = lane < f ? (a.elit[v0 >> 5] >> (v0 & 31u)) & 1u : 0u;
+        const uint32_t b1 = lane + 32u < f ? (a.elit[v1 >> 5] >> (v1 & 31u)) & 1u : 0u;
+        em = (uint64_t)__ballot_sync(0xFFFFFFFFu, b0) |
+             ((uint64_t)__ballot_sync(0xFFFFFFFFu, b1) << 32);
+      }
+      const uint64_t fm = f >= 64 ? ~0ull : ((1ull << f) - 1ull);
+      team_sync(tw);
+
+      uint64_t pm[WPT], dm[WPT];
+      bool present[WPT];
+      int32_t dsel[WPT];
+#pragma unroll
+      for (int j = 0; j < WPT; ++j) {
+        const uint32_t w = wit + tw * j;
+        const uint32_t s = w * 32u + lane;
+        const bool valid = s < n;
+        uint64_t m = 0;
+        for (uint32_t jv = 0; jv < f; ++jv) m |= (uint64_t)((rowsF[jv * Wp + w] >> lane) & 1u) << jv;
+        pm[j] = m;
+        int32_t d = -1;
+        uint64_t dmask = m;
+        if (valid) {
+          if (replay) {
+            d = a.tape[(size_t)p * n + s];
+            if (d >= 0) {
+              uint64_t x = 0;
+              for (uint32_t jv = 0; jv < f; ++jv)
+                x |= (uint64_t)((rowsF[jv * Wp + ((uint32_t)d >> 5)] >> (d & 31)) & 1u) << jv;
+              dmask = x;
+            }
+          } else {
+            // uniform over members that differ on F (the lazy Fisher-Yates scan
+            // of engine_serial.hpp:30-46 returns exactly that distribution):
+            // rejection sampling first, exact count-and-select as fallback.
+            const uint2 key = make_uint2((uint32_t)a.seed, (uint32_t)(a.seed >> 32));
+            for (uint32_t call = 0; call < 2 && d < 0; ++call) {
+              const uint4 r = philox4x32_10(make_uint4(s, sid, a.generation, kTagGom | call), key);
+#pragma unroll
+              for (int t = 0; t < 2; ++t) {
+                if (d >= 0) break;
+                const uint32_t c = bounded(t ? hi64(r) : lo64(r), n);
+                uint64_t x = 0;
+                for (uint32_t jv = 0; jv < f; ++jv)
+                  x |= (uint64_t)((rowsF[jv * Wp + (c >> 5)] >> (c & 31u)) & 1u) << jv;
+                if (x != m) {
+                  d = (int32_t)c;
+                  dmask = x;
+                }
+              }
+            }
+            if (d < 0) {
+              uint32_t total = 0;
+              for (uint32_t w2 = 0; w2 < Wp; ++w2) {
+                uint32_t dw = 0;
+                for (uint32_t jv = 0; jv < f; ++jv)
+                  dw |= rowsF[jv * Wp + w2] ^ (((m >> jv) & 1ull) ? 0xFFFFFFFFu : 0u);
+                total += __popc(dw & valid_mask(w2, n));
+              }
+              if (total > 0) {
+                const uint4 r = philox4x32_10(make_uint4(s, sid, a.generation, kTagGom | 2u), key);
+                uint32_t kth = bounded(lo64(r), total);
+                for (uint32_t w2 = 0; w2 < Wp; ++w2) {
+                  uint32_t dw = 0;
+                  for (uint32_t jv = 0; jv < f; ++jv)
+                    dw |= rowsF[jv * Wp + w2] ^ (((m >> jv) & 1ull) ? 0xFFFFFFFFu : 0u);
+                  dw &= valid_mask(w2, n);
+                  const uint32_t c = __popc(dw);
+                  if (kth < c) {
+                    for (uint32_t i = 0; i < kth; ++i) dw &= dw - 1u;  // drop kth lowest
+                    d = (int32_t)(w2 * 32u + (uint32_t)(__ffs(dw) - 1));
+                    break;
+                  }
+                  kth -= c;
+                }
+                uint64_t x = 0;
+                for (uint32_t jv = 0; jv < f; ++jv)
+                  x |= (uint64_t)((rowsF[jv * Wp + ((uint32_t)d >> 5)] >> (d & 31)) & 1u) << jv;
+                dmask = x;
+              }
+            }
+          }
+        }
+        dm[j] = dmask;
+        present[j] = d >= 0;
+        dsel[j] = d;
+      }
+
+      // phase 2: footprint sums, ascending edge id (engine_parallel.hpp:164-173)
+      int32_t di[WPT];
+      double sn[WPT], so[WPT];
+#pragma unroll
+      for (int j = 0; j < WPT; ++j) {
+        di[j] = 0;
+        sn[j] = 0.0;
+        so[j] = 0.0;
+      }
+      const int64_t e0 = a.fp_off[sid], e1 = a.fp_off[sid + 1];
+      for (int64_t e = e0; e < e1; ++e) {
+        const FpEntry E = a.fp[e];
+#pragma unroll
+        for (int j = 0; j < WPT; ++j) {
+          const uint32_t w = wit + tw * j;
+          uint32_t ao, an, bo, bn;
+          if (E.a & kInSet) {
+            const uint32_t ja = E.a & ~kInSet;
+            ao = (uint32_t)(pm[j] >> ja) & 1u;
+            an = (uint32_t)(dm[j] >> ja) & 1u;
+          } else {
+            ao = an = (a.pop[(size_t)E.a * Wp + w] >> lane) & 1u;
+          }
+          if (E.b & kInSet) {
+            const uint32_t jb = E.b & ~kInSet;
+            bo = (uint32_t)(pm[j] >> jb) & 1u;
+            bn = (uint32_t)(dm[j] >> jb) & 1u;
+          } else {
+            bo = bn = (a.pop[(size_t)E.b * Wp + w] >> lane) & 1u;
+          }
+          if constexpr (I32) {
+            const int32_t wt = (int32_t)E.w;
+            di[j] += ((int32_t)(an ^ bn) - (int32_t)(ao ^ bo)) * wt;
+          } else {
+            sn[j] += (an ^ bn) ? E.w : 0.0;
+            so[j] += (ao ^ bo) ? E.w : 0.0;
+          }
+        }
+      }
+      const uint32_t fpl = (uint32_t)(e1 - e0);
+
+      // phases 3 + 4
+#pragma unroll
+      for (int j = 0; j < WPT; ++j) {
+        const uint32_t w = wit + tw * j;
+        const uint32_t s = w * 32u + lane;
+        const bool valid = s < n;
+        const double delta = (e1 == e0) ? 0.0 : (I32 ? (double)di[j] : sn[j] - so[j]);
+        bool accept = false;
+        if (present[j]) {
+          const bool elit = a.ham[s] == 0;
+          if (exact) {
+            accept = delta > 0.0 || (delta == 0.0 && !elit);
+          } else {
+            const double pf = a.fit[s];
+            const double cand = pf + delta;
+            accept = cmp_better(false, cand, pf) || (cmp_equal(false, cand, pf) && !elit);
+          }
+        }
+        const uint64_t nm = accept ? dm[j] : pm[j];
+        for (uint32_t jv = 0; jv < f; ++jv) {
+          const uint32_t word = __ballot_sync(0xFFFFFFFFu, (uint32_t)(nm >> jv) & 1u);
+          if (lane == 0) newF[jv * Wp + w] = word;
+        }
+        if (accept) {
+          acc[j] += I32 ? (Acc)di[j] : (Acc)delta;
+          hacc[j] += __popcll((dm[j] ^ em) & fm) - __popcll((pm[j] ^ em) & fm);
+        }
+        steps += present[j] ? 1u : 0u;
+        calls += present[j] ? fpl : 0u;
+        if (record && valid) {
+          const size_t at = (size_t)p * n + s;
+          a.rec_donor[at] = dsel[j];
+          a.rec_delta[at] = delta;
+          a.rec_present[at] = present[j];
+          a.rec_accept[at] = accept;
+        }
+      }
+      team_sync(tw);
+      for (uint32_t idx = tid_team; idx < f * Wp; idx += team_threads) {
+        const uint32_t nw = newF[idx];
+        if (nw != rowsF[idx]) {
+          const uint32_t jv = idx / Wp, w = idx - jv * Wp;
+          a.pop[(size_t)vars[jv] * Wp + w] = nw;
+        }
+      }
+      team_sync(tw);
+    }
+  }
+
+  // ---- per-CTA reductions: counters, fitness deltas, elitist distances ----
+  __syncthreads();
+  __shared__ unsigned long long s_steps, s_calls;
+  if (threadIdx.x == 0) {
+    s_steps = 0;
+    s_calls = 0;
+  }
+  __syncthreads();
+  {
+    const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, steps);
+    unsigned long long wc = calls;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wc += __shfl_xor_sync(0xFFFFFFFFu, wc, o);
+    if (lane == 0 && (ws | wc)) {
+      atomicAdd(&s_steps, (unsigned long long)ws);
+      atomicAdd(&s_calls, wc);
+    }
+  }
+  const bool float_parts = a.part != nullptr;
+  if (tw == 1) {
+    // warp teams: combine the CTA's teams in fixed order (deterministic)
+    double* sacc = reinterpret_cast<double*>(smem);
+    int32_t* sham = reinterpret_cast<int32_t*>(sacc + (size_t)teams_per_cta * Wp * 32u);
+#pragma unroll
+    for (int j = 0; j < WPT; ++j) {
+      const uint32_t s = (uint32_t)j * 32u + lane;
+      sacc[(size_t)team * Wp * 32u + s] = (double)acc[j];
+      sham[(size_t)team * Wp * 32u + s] = hacc[j];
+    }
+    __syncthreads();
+    for (uint32_t s = threadIdx.x; s < Wp * 32u; s += blockDim.x) {
+      double v = 0.0;
+      int32_t h = 0;
+      for (uint32_t t = 0; t < teams_per_cta; ++t) {
+        v += sacc[(size_t)t * Wp * 32u + s];
+        h += sham[(size_t)t * Wp * 32u + s];
+      }
+      if (s < n) {
+        if (float_parts)
+          a.part[(size_t)blockIdx.x * n + s] = v;
+        else if (a.dfit && v != 0.0)
+          atomicAdd(&a.dfit[s], v);
+        if (h) atomicAdd(&a.dham[s], h);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < WPT; ++j) {
+      const uint32_t s = (wit + tw * (uint32_t)j) * 32u + lane;
+      if (s < n) {
+        if (float_parts)
+          a.part[(size_t)blockIdx.x * n + s] = (double)acc[j];
+        else if (a.dfit && acc[j] != 0)
+          atomicAdd(&a.dfit[s], (double)acc[j]);
+        if (hacc[j]) atomicAdd(&a.dham[s], hacc[j]);
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && (s_steps | s_calls)) {
+    atomicAdd(&a.ctl->grp_steps, s_steps);
+    atomicAdd(&a.ctl->grp_calls, s_calls);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// epilogue_kernel (1 CTA): commit the group's fitness deltas, account the
+// evaluator calls (budget stop first, runtime.hpp:75-80), then the elitist
+// scan of engine_parallel.hpp:305-310 — the first member strictly better than
+// the running elitist replaces it, the scan continuing against the new value —
+// logging every improvement and latching the target stop (runtime.hpp:88-93).
+// ---------------------------------------------------------------------------
+__device__ void request_stop(DevCtl* c, int reason) {
+  if (!c->stop) {
+    c->stop = 1;
+    c->stop_reason = reason;
+  }
+}
+
+__device__ void note_improvement(const EpiArgs& a, double f) {
+  DevCtl* c = a.ctl;
+  const unsigned long long i = c->n_impr++;
+  if (i < a.impr_cap) a.impr[i] = f;
+  if (c->has_target && (cmp_better(c->exact, f, c->target) || cmp_equal(c->exact, f, c->target)))
+    request_stop(c, GOMIX_STOP_TARGET);
+}
+
+__global__ void __launch_bounds__(kEpilogueThreads) epilogue_kernel(const EpiArgs a) {
+  DevCtl* c = a.ctl;
+  if (*(volatile int32_t*)&c->stop) return;
+  const uint32_t n = a.n;
+  __shared__ double s_chunkmax[kEpilogueThreads / 32];
+  __shared__ int32_t s_best;
+  for (uint32_t s = threadIdx.x; s < n; s += blockDim.x) {
+    double f = a.fit[s];
+    if (a.mode == 2) {
+      for (uint32_t p = 0; p < a.G; ++p)
+        if (a.rec_accept[(size_t)p * n + s]) f += a.rec_delta[(size_t)p * n + s];
+    } else if (a.mode == 1) {
+      double sum = 0.0;
+      for (uint32_t b = 0; b < a.nparts; ++b) sum += a.part[(size_t)b * n + s];
+      f += sum;
+    } else {
+      f += a.dfit[s];
+      a.dfit[s] = 0.0;
+    }
+    a.fit[s] = f;
+    a.ham[s] += a.dham[s];
+    a.dham[s] = 0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long st = c->grp_steps, ca = c->grp_calls;
+    c->grp_steps = 0;
+    c->grp_calls = 0;
+    c->calls_total += ca;
+    c->run_steps += st;
+    c->run_calls += ca;
+    c->groups_run += 1;
+    a.gsteps[a.group] += st;
+    a.gcalls[a.group] += ca;
+    if (c->has_budget && (double)c->calls_total / c->q >= c->max_evals)
+      request_stop(c, GOMIX_STOP_BUDGET);
+    s_best = -1;
+  }
+  // chunk maxima let the serial scan skip chunks that cannot hold a record
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  for (uint32_t chunk = warp; chunk * 32u < n; chunk += blockDim.x >> 5) {
+    const uint32_t s = chunk * 32u + lane;
+    double f = s < n ? a.fit[s] : -INFINITY;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) f = fmax(f, __shfl_xor_sync(0xFFFFFFFFu, f, o));
+    if (lane == 0 && chunk < kEpilogueThreads / 32) s_chunkmax[chunk] = f;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const bool exact = c->exact != 0;
+    double cur = c->elit_fit;
+    int32_t best = -1;
+    for (uint32_t base = 0; base < n; base += 32u) {
+      const uint32_t chunk = base >> 5;
+      if (chunk < kEpilogueThreads / 32 && !(s_chunkmax[chunk] > cur)) continue;
+      const uint32_t s = base + lane;
+      const double f = s < n ? a.fit[s] : -INFINITY;
+      uint32_t m = __ballot_sync(0xFFFFFFFFu, s < n && cmp_better(exact, f, cur));
+      while (m) {
+        const uint32_t l = __ffs(m) - 1;
+        cur = __shfl_sync(0xFFFFFFFFu, f, l);
+        best = (int32_t)(base + l);
+        if (lane == 0) note_improvement(a, cur);
+        m = __ballot_sync(0xFFFFFFFFu, s < n && lane > l && cmp_better(exact, f, cur));
+      }
+    }
+    if (lane == 0) {
+      c->elit_src = best;
+      if (best >= 0) c->elit_fit = cur;
+      s_best = best;
+    }
+  }
+  __syncthreads();
+  if (s_best >= 0)
+    for (uint32_t s = threadIdx.x; s < n; s += blockDim.x) a.ham[s] = 0;  // refresh recounts
+}
+
+// After init_population (engine_parallel.hpp:331-346): one add_evaluator_calls(q)
+// per solution and "i == 0 || better" elitist updates, interleaved in order.
+__global__ void init_epilogue_kernel(const EpiArgs a) {
+  DevCtl* c = a.ctl;
+  if (threadIdx.x == 0) {
+    const bool exact = c->exact != 0;
+    double cur = 0.0;
+    int32_t best = -1;
+    for (uint32_t i = 0; i < a.n; ++i) {
+      c->calls_total += (unsigned long long)c->q;
+      c->run_calls += (unsigned long long)c->q;
+      if (c->has_budget && (double)c->calls_total / c->q >= c->max_evals)
+        request_stop(c, GOMIX_STOP_BUDGET);
+      const double f = a.fit[i];
+      if (i == 0 || cmp_better(exact, f, cur)) {
+        cur = f;
+        best = (int32_t)i;
+        note_improvement(a, f);
+      }
+    }
+    c->elit_fit = cur;
+    c->elit_src = best;
+  }
+  __syncthreads();
+  for (uint32_t s = threadIdx.x; s < a.n; s += blockDim.x) {
+    a.ham[s] = 0;
+    a.dham[s] = 0;
+    a.dfit[s] = 0.0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// refresh_kernel: when the elitist changed, copy its genotype out of the
+// population column and recount every member's Hamming distance to it; the
+// batched accept rule only needs "parent == elitist" (engine_parallel.hpp:202),
+// i.e. distance 0, which the GOM kernel then maintains incrementally.
+// ---------------------------------------------------------------------------
+__global__ void refresh_kernel(const RefreshArgs a) {
+  const int32_t src = *(volatile const int32_t*)&a.ctl->elit_src;
+  if (src == -1) return;
+  const uint32_t Wp = a.Wp;
+  const uint64_t gtid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
+  const uint32_t sw = src >= 0 ? (uint32_t)src >> 5 : 0u, sb = src >= 0 ? (uint32_t)src & 31u : 0u;
+  if (src >= 0) {
+    const uint64_t nwords = (a.nv + 31) / 32;
+    for (uint64_t t = gtid; t < nwords; t += nthreads) {
+      uint32_t word = 0;
+      const uint64_t v0 = t * 32;
+      for (uint32_t k = 0; k < 32 && v0 + k < a.nv; ++k)
+        word |= ((a.pop[(v0 + k) * Wp + sw] >> sb) & 1u) << k;
+      a.elit[t] = word;
+    }
+  }
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t gwarp = gtid >> 5, nwarps = nthreads >> 5;
+  const uint64_t chunks = (a.nv + a.rows_per_chunk - 1) / a.rows_per_chunk;
+  for (uint64_t unit = gwarp; unit < chunks * Wp; unit += nwarps) {
+    const uint32_t w = (uint32_t)(unit % Wp);
+    const uint64_t v0 = (unit / Wp) * a.rows_per_chunk;
+    const uint64_t v1 = min(v0 + a.rows_per_chunk, a.nv);
+    if (w * 32u >= a.n) continue;
+    int32_t cnt = 0;
+    for (uint64_t v = v0; v < v1; ++v) {
+      const uint32_t x = a.pop[v * Wp + w];
+      const uint32_t eb = src >= 0 ? (a.pop[v * Wp + sw] >> sb) & 1u : (a.elit[v >> 5] >> (v & 31u)) & 1u;
+      cnt += ((x ^ (eb ? 0xFFFFFFFFu : 0u)) >> lane) & 1u;
+    }
+    const uint32_t s = w * 32u + lane;
+    if (s < a.n && cnt) atomicAdd(&a.ham[s], cnt);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// init / full evaluation / layout conversion
+// ---------------------------------------------------------------------------
+__global__ void philox_init_kernel(uint32_t* pop, uint64_t nv, uint32_t n, uint32_t Wp,
+                                   uint64_t seed) {
+  const uint64_t total = nv * Wp;
+  const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t w = (uint32_t)(i % Wp);
+    const uint4 r = philox4x32_10(make_uint4((uint32_t)i, (uint32_t)(i >> 32), 0u, kTagInit), key);
+    pop[i] = r.x & valid_mask(w, n);
+  }
+}
+
+// Exact (integer) fitness: any summation order is exact -> parallel over edges.
+__global__ void full_eval_parallel_kernel(const uint32_t* eu, const uint32_t* ev,
+                                          const double* ew, uint64_t q, const uint32_t* pop,
+                                          double* fit, uint32_t n, uint32_t Wp,
+                                          uint64_t edges_per_chunk) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t gwarp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t chunks = (q + edges_per_chunk - 1) / edges_per_chunk;
+  for (uint64_t unit = gwarp; unit < chunks * Wp; unit += nwarps) {
+    const uint32_t w = (uint32_t)(unit % Wp);
+    if (w * 32u >= n) continue;
+    const uint64_t e0 = (unit / Wp) * edges_per_chunk, e1 = min(e0 + edges_per_chunk, q);
+    double sum = 0.0;
+    for (uint64_t e = e0; e < e1; ++e) {
+      const uint32_t x = pop[(uint64_t)eu[e] * Wp + w] ^ pop[(uint64_t)ev[e] * Wp + w];
+      sum += ((x >> lane) & 1u) ? ew[e] : 0.0;
+    }
+    const uint32_t s = w * 32u + lane;
+    if (s < n && sum != 0.0) atomicAdd(&fit[s], sum);
+  }
+}
+
+// Float fitness in the reference's left-to-right edge order (graybox.hpp:139-144).
+__global__ void full_eval_ordered_kernel(const uint32_t* eu, const uint32_t* ev,
+                                         const double* ew, uint64_t q, const uint32_t* pop,
+                                         double* fit, uint32_t n, uint32_t Wp) {
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const uint32_t w = s >> 5, b = s & 31u;
+  double sum = 0.0;
+  for (uint64_t e = 0; e < q; ++e) {
+    const uint32_t x = pop[(uint64_t)eu[e] * Wp + w] ^ pop[(uint64_t)ev[e] * Wp + w];
+    sum += ((x >> b) & 1u) ? ew[e] : 0.0;
+  }
+  fit[s] = sum;
+}
+
+__global__ void unpack_kernel(const uint32_t* pop, uint8_t* out, uint64_t nv, uint32_t n,
+                              uint32_t Wp) {
+  const uint64_t total = (uint64_t)n * nv;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t s = i / nv, v = i - s * nv;
+    out[i] = (pop[v * Wp + (s >> 5)] >> (s & 31u)) & 1u;
+  }
+}
+
+__global__ void pack_kernel(const uint8_t* in, uint32_t* pop, uint64_t nv, uint32_t n,
+                            uint32_t Wp) {
+  const uint64_t total = nv * Wp;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t v = i / Wp;
+    const uint32_t w = (uint32_t)(i - v * Wp);
+    uint32_t word = 0;
+    for (uint32_t b = 0; b < 32; ++b) {
+      const uint32_t s = w * 32u + b;
+      if (s < n && in[(uint64_t)s * nv + v]) word |= 1u << b;
+    }
+    pop[i] = word;
+  }
+}
+
+__global__ void pack_elitist_kernel(const uint8_t* in, uint32_t* elit, uint64_t nv) {
+  const uint64_t nw = (nv + 31) / 32;
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nw;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t word = 0;
+    for (uint32_t k = 0; k < 32 && t * 32 + k < nv; ++k)
+      if (in[t * 32 + k]) word |= 1u << k;
+    elit[t] = word;
+  }
+}
+
+__global__ void unpack_elitist_kernel(const uint32_t* elit, uint8_t* out, uint64_t nv) {
+  for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv;
+       v += (uint64_t)gridDim.x * blockDim.x)
+    out[v] = (elit[v >> 5] >> (v & 31u)) & 1u;
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+namespace {
+template <int WPT>
+void* gom_kernel_ptr(bool univariate, bool i32) {
+  if (univariate) return i32 ? (void*)gom_group_kernel<WPT, true, true> : (void*)gom_group_kernel<WPT, true, false>;
+  return i32 ? (void*)gom_group_kernel<WPT, false, true> : (void*)gom_group_kernel<WPT, false, false>;
+}
+
+void* gom_kernel(bool univariate, bool i32, int wpt) {
+  switch (wpt) {
+    case 1: return gom_kernel_ptr<1>(univariate, i32);
+    case 2: return gom_kernel_ptr<2>(univariate, i32);
+    case 4: return gom_kernel_ptr<4>(univariate, i32);
+    case 8: return gom_kernel_ptr<8>(univariate, i32);
+  }
+  throw GomixError(GOMIX_E_INVALID, "unsupported words-per-thread");
+}
+
+int grid_for(uint64_t work, int block, uint64_t cap) {
+  uint64_t g = (work + block - 1) / block;
+  if (g > cap) g = cap;
+  return (int)(g ? g : 1);
+}
+}  // namespace
+
+void launch_gom(const GomArgs& a, bool univariate, bool i32, int wpt, int grid, int block,
+                size_t smem, cudaStream_t s) {
+  void* fn = gom_kernel(univariate, i32, wpt);
+  if (smem > 48 * 1024)
+    GOMIX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  void* args[] = {(void*)&a};
+  GOMIX_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(block), args, smem, s));
+}
+
+int gom_max_blocks_per_sm(bool univariate, bool i32, int wpt, int block, size_t smem) {
+  void* fn = gom_kernel(univariate, i32, wpt);
+  if (smem > 48 * 1024)
+    GOMIX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int blocks = 0;
+  GOMIX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, block, smem));
+  return blocks;
+}
+
+void launch_epilogue(const EpiArgs& a, cudaStream_t s) {
+  epilogue_kernel<<<1, kEpilogueThreads, 0, s>>>(a);
+  GOMIX_CUDA(cudaGetLastError());
+}
+
+void launch_init_epilogue(const EpiArgs& a, cudaStream_t s) {
+  init_epilogue_kernel<<<1, 256, 0, s>>>(a);
+  GOMIX_CUDA(cudaGetLastError());
+}
+
+void launch_refresh(const RefreshArgs& a, int grid, cudaStream_t s) {
+  refresh_kernel<<<grid, 256, 0, s>>>(a);
+  GOMIX_CUDA(cudaGetLastError());
+}
+
+void launch_philox_init(uint32_t* pop, uint64_t nv, uint32_t n, uint32_t Wp, uint64_t seed,
+                        cudaStream_t s) {
+  philox_init_kernel<<<grid_for(nv * Wp, 256, 4096), 256, 0, s>>>(pop, nv, n, Wp, seed);
+  GOMIX_CUDA(cudaGetLastError());
+}
+
+void launch_full_eval(const Problem& P, const uint32_t* pop, double* fit, uint32_t n,
+                      uint32_t Wp, bool ordered, cudaStream_t s) {
+  if (ordered) {
+    full_eval_ordered_kernel<<<(n + 127) / 128, 128, 0, s>>>(P.eu, P.ev, P.ew, P.q, pop, fit, n, Wp);
+  } else {
+    GOMIX_CUDA(cudaMemsetAsync(fit, 0, n * sizeof(double), s));
+    const uint64_t chunk = 1024;
+    const uint64_t units = ((P.q + chunk - 1) / chunk) * Wp;
+    full_eval_parallel_kernel<<<grid_for(units * 32, 256, 4096), 256, 0, s>>>(
+        P.eu, P.ev, P.ew, P.q, pop, fit, n, Wp, chunk);
+  }
+  GOMIX_CUDA(cudaGetLastError());
+}
+
+void launch_unpack(const uint32_t* pop, uint8_t* out, uint64_t nv, uint32_t n, uint32_t Wp,
+                   cudaStream_t s) {
+  unpack_kernel<<<grid_for(nv * n, 256, 8192), 256, 0, s>>>(pop, out, nv, n, Wp);
+  GOMIX_CUDA(cudaGetLastError());
+}
+
+void launch_pack(const uint8_t* in, uint32_t* pop, uint64_t nv, uint32_t n, uint32_t Wp,
+                 cudaStream_t s) {
+  pack_kernel<<<grid_for(nv * Wp, 256, 8192), 256, 0, s>>>(in, pop, nv, n, Wp);
+  GOMIX_CUDA(cudaGetLastError());
+}
+
+void launch_pack_elitist(const uint8_t* in, uint32_t* elit, uint64_t nv, cudaStream_t s) {
+  pack_elitist_kernel<<<grid_for((nv + 31) / 32, 256, 4096), 256, 0, s>>>(in, elit, nv);
+  GOMIX_CUDA(cudaGetLastError());
+}
+
+void launch_unpack_elitist(const uint32_t* elit, uint8_t* out, uint64_t nv, cudaStream_t s) {
+  unpack_elitist_kernel<<<grid_for(nv, 256, 4096), 256, 0, s>>>(elit, out, nv);
+  GOMIX_CUDA(cudaGetLastError());
+}
+
+}  // namespace gomix_b200

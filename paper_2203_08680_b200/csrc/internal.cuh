@@ -1,0 +1,221 @@
+// internal.cuh — device data layout and shared helpers of libgomix_b200.
+//
+// HBM layout:
+//   population  : num_vertices rows x Wp uint32 words ("variable-major, bit-
+//                 sliced"): bit b of word w of row v = allele of variable v in
+//                 solution 32w+b.  One coalesced row gives a variable's value in
+//                 every solution, so "does any member differ on F" is a few
+//                 word ops and a group touches each row it needs once.
+//   graph CSR   : row_ptr[nv+1], col[2q] (ascending neighbour = ascending edge
+//                 id, the reference's summation order), w[2q] fp64 and, when the
+//                 weights are small integers, wi[2q] int32.
+//   footprints  : per linkage set, its dependent subfunctions (edges) sorted by
+//                 edge id (make_group_plan, engine_parallel.hpp:37-59) as
+//                 FpEntry {a, b, w}; endpoints inside the set are encoded as
+//                 kInSet | position-in-set.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "gomix_gpu.h"
+
+namespace gomix_b200 {
+
+constexpr uint32_t kInSet = 0x80000000u;
+constexpr int kMaxSetSize = 64;     // per-lane set patterns are uint64 masks
+constexpr int kEpilogueThreads = 1024;
+
+struct FpEntry {
+  uint32_t a, b;  // endpoint vertex id, or kInSet | index within the set
+  double w;
+};
+
+// Run-control block living in device memory; updated by the epilogue kernel
+// after every group so stop criteria never need a host round trip.
+struct DevCtl {
+  double elit_fit;
+  int32_t elit_src;     // >= 0: elitist := solution elit_src; -2: elitist bits given; -1: none
+  int32_t stop;         // latched stop request (RunControl::request_stop, runtime.hpp:104-109)
+  int32_t stop_reason;  // GOMIX_STOP_*
+  int32_t has_budget;
+  int32_t has_target;
+  int32_t exact;
+  double max_evals;
+  double q;
+  double target;
+  unsigned long long calls_total;  // absolute evaluator calls (RunControl::calls_)
+  unsigned long long grp_steps, grp_calls;
+  unsigned long long run_steps, run_calls, groups_run;
+  unsigned long long n_impr;
+};
+
+struct Problem {
+  int device = 0;
+  uint64_t nv = 0, q = 0, m = 0, k = 0, lmig_edges = 0, max_f = 0, max_fp = 0;
+  bool exact = true, univariate = true, i32 = false;
+  // host mirrors (small)
+  std::vector<uint64_t> h_set_off;
+  std::vector<uint32_t> h_set_vars;
+  std::vector<uint64_t> group_off;   // k + 1
+  std::vector<uint64_t> group_sets;  // m, concatenated, ascending within a group
+  std::vector<uint64_t> footprint;   // per set
+  // device
+  int32_t* row_ptr = nullptr;
+  int32_t* col = nullptr;
+  double* w = nullptr;
+  int32_t* wi = nullptr;
+  uint32_t* eu = nullptr;
+  uint32_t* ev = nullptr;
+  double* ew = nullptr;
+  int64_t* set_off = nullptr;
+  uint32_t* set_vars = nullptr;
+  uint32_t* gsets = nullptr;
+  int64_t* fp_off = nullptr;
+  FpEntry* fp = nullptr;
+  std::vector<void*> allocations;
+  ~Problem();
+};
+
+struct GomArgs {
+  const int32_t* row_ptr;
+  const int32_t* col;
+  const double* w;
+  const int32_t* wi;
+  const int64_t* set_off;
+  const uint32_t* set_vars;
+  const int64_t* fp_off;
+  const FpEntry* fp;
+  const uint32_t* gsets;  // this group's members (ascending set ids)
+  uint32_t G;             // |G|
+  uint32_t* pop;
+  const double* fit;
+  const int32_t* ham;
+  const uint32_t* elit;
+  double* dfit;
+  double* part;
+  int32_t* dham;
+  DevCtl* ctl;
+  const int32_t* tape;  // replay donors, p-major [p*n + s]; nullptr -> Philox
+  int32_t* rec_donor;   // optional GroupBatch recording, p-major
+  double* rec_delta;
+  uint8_t* rec_present;
+  uint8_t* rec_accept;
+  uint32_t n, Wp, team_warps, stage_words;
+  int32_t exact;
+  uint32_t generation;
+  uint64_t seed;
+};
+
+struct EpiArgs {
+  double* fit;
+  const double* part;
+  double* dfit;
+  int32_t* ham;
+  int32_t* dham;
+  const double* rec_delta;
+  const uint8_t* rec_accept;
+  DevCtl* ctl;
+  unsigned long long* gsteps;
+  unsigned long long* gcalls;
+  double* impr;
+  uint64_t impr_cap;
+  uint32_t n, G, nparts, group;
+  int32_t mode;  // 0 exact atomics, 1 float partials, 2 ordered
+};
+
+struct RefreshArgs {
+  const uint32_t* pop;
+  uint32_t* elit;
+  int32_t* ham;
+  const DevCtl* ctl;
+  uint64_t nv;
+  uint32_t n, Wp, rows_per_chunk;
+};
+
+// -------------------------------------------------------------------------
+// errors
+// -------------------------------------------------------------------------
+struct GomixError : std::runtime_error {
+  int status;
+  GomixError(int s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+#define GOMIX_CUDA(call)                                                              \
+  do {                                                                                \
+    cudaError_t err__ = (call);                                                       \
+    if (err__ != cudaSuccess)                                                         \
+      throw ::gomix_b200::GomixError(err__ == cudaErrorMemoryAllocation ? GOMIX_E_OOM \
+                                                                        : GOMIX_E_CUDA, \
+                                     std::string(#call) + ": " + cudaGetErrorString(err__)); \
+  } while (0)
+
+inline void invalid(const std::string& m) { throw GomixError(GOMIX_E_INVALID, m); }
+
+template <typename T>
+T* dev_alloc(std::vector<void*>& owner, size_t count) {
+  void* p = nullptr;
+  if (count == 0) count = 1;
+  GOMIX_CUDA(cudaMalloc(&p, count * sizeof(T)));
+  owner.push_back(p);
+  return static_cast<T*>(p);
+}
+
+// -------------------------------------------------------------------------
+// Host replay stream: the reference's RngStream = std::mt19937_64 seeded with
+// mix64(seed) (rng.hpp:11-63).  std::mt19937_64 is pinned by the C++ standard.
+// -------------------------------------------------------------------------
+inline uint64_t mix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+
+class ReplayStream {
+ public:
+  explicit ReplayStream(uint64_t seed) : gen_(mix64(seed)) {}
+  uint64_t next() { return gen_(); }
+  // Lemire-free rejection draw identical to rng.hpp:28-35.
+  uint64_t uniform_index(uint64_t n) {
+    const uint64_t threshold = (0 - n) % n;
+    for (;;) {
+      const uint64_t r = gen_();
+      if (r >= threshold) return r % n;
+    }
+  }
+  void permutation(std::vector<uint64_t>& out, uint64_t n) {
+    out.resize(n);
+    for (uint64_t i = 0; i < n; ++i) out[i] = i;
+    for (uint64_t i = n; i > 1; --i) std::swap(out[i - 1], out[uniform_index(i)]);
+  }
+
+ private:
+  std::mt19937_64 gen_;
+};
+
+// kernel launchers (gom.cu)
+void launch_gom(const GomArgs& a, bool univariate, bool i32, int wpt, int grid, int block,
+                size_t smem, cudaStream_t s);
+int gom_max_blocks_per_sm(bool univariate, bool i32, int wpt, int block, size_t smem);
+void launch_epilogue(const EpiArgs& a, cudaStream_t s);
+void launch_init_epilogue(const EpiArgs& a, cudaStream_t s);
+void launch_refresh(const RefreshArgs& a, int grid, cudaStream_t s);
+void launch_philox_init(uint32_t* pop, uint64_t nv, uint32_t n, uint32_t Wp, uint64_t seed,
+                        cudaStream_t s);
+void launch_full_eval(const Problem& P, const uint32_t* pop, double* fit, uint32_t n,
+                      uint32_t Wp, bool ordered, cudaStream_t s);
+void launch_unpack(const uint32_t* pop, uint8_t* out, uint64_t nv, uint32_t n, uint32_t Wp,
+                   cudaStream_t s);
+void launch_pack(const uint8_t* in, uint32_t* pop, uint64_t nv, uint32_t n, uint32_t Wp,
+                 cudaStream_t s);
+void launch_pack_elitist(const uint8_t* in, uint32_t* elit, uint64_t nv, cudaStream_t s);
+void launch_unpack_elitist(const uint32_t* elit, uint8_t* out, uint64_t nv, cudaStream_t s);
+
+
+}  // namespace gomix_b200

@@ -1,0 +1,444 @@
+// problem.cu — the shared, immutable model of a run (ModelArtifacts,
+// model.hpp:25-29): validated Max-Cut instance as a device CSR graph, the FOS,
+// its linkage-set interaction graph (LMIG, scheduling.hpp:35-68) and an exact
+// GPU reproduction of the reference's Welsh-Powell colouring
+// (scheduling.hpp:85-114), the colour groups and every set's footprint plan
+// (make_group_plan, engine_parallel.hpp:37-59).
+//
+// Colouring: Welsh-Powell is greedy colouring in the order (degree desc,
+// index asc).  Jones-Plassmann with exactly that order as the priority is the
+// same function computed in parallel: a set is coloured once every
+// higher-priority neighbour is, with the smallest colour they do not use —
+// which is what the sequential greedy gives it.  So the groups, and with them
+// replay parity, are identical to the reference's.
+#include <cub/cub.cuh>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "internal.cuh"
+
+namespace gomix_b200 {
+
+Problem::~Problem() {
+  for (void* p : allocations) cudaFree(p);
+}
+
+namespace {
+
+int blocks_for(uint64_t n, int block = 256) {
+  uint64_t g = (n + block - 1) / block;
+  return (int)std::max<uint64_t>(1, std::min<uint64_t>(g, 65535ull * 16));
+}
+
+// entry -> owning set id, for a CSR of sets
+__global__ void entry_owner_kernel(const int64_t* off, uint64_t m, uint32_t* owner) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    for (int64_t k = off[i]; k < off[i + 1]; ++k) owner[k] = (uint32_t)i;
+}
+
+__global__ void count_kernel(const uint32_t* keys, uint64_t cnt, int64_t* hist) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cnt;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    atomicAdd((unsigned long long*)&hist[keys[i]], 1ull);
+}
+
+// LMIG candidate bound of set i: shared-variable sets plus sets of every
+// interaction neighbour (scheduling.hpp:369-373).
+__global__ void lmig_bound_kernel(const int64_t* set_off, const uint32_t* set_vars,
+                                  const int64_t* vs_off, const int32_t* row_ptr,
+                                  const int32_t* col, uint64_t m, int64_t* bound) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    int64_t b = 0;
+    for (int64_t k = set_off[i]; k < set_off[i + 1]; ++k) {
+      const uint32_t u = set_vars[k];
+      b += vs_off[u + 1] - vs_off[u];
+      for (int32_t e = row_ptr[u]; e < row_ptr[u + 1]; ++e) {
+        const uint32_t x = (uint32_t)col[e];
+        b += vs_off[x + 1] - vs_off[x];
+      }
+    }
+    bound[i] = b;
+  }
+}
+
+__global__ void lmig_fill_kernel(const int64_t* set_off, const uint32_t* set_vars,
+                                 const int64_t* vs_off, const uint32_t* vs_sets,
+                                 const int32_t* row_ptr, const int32_t* col, uint64_t m,
+                                 const int64_t* cand_off, uint32_t* cand) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    int64_t at = cand_off[i];
+    const uint32_t self = (uint32_t)i;
+    for (int64_t k = set_off[i]; k < set_off[i + 1]; ++k) {
+      const uint32_t u = set_vars[k];
+      for (int64_t t = vs_off[u]; t < vs_off[u + 1]; ++t) cand[at++] = vs_sets[t];
+      for (int32_t e = row_ptr[u]; e < row_ptr[u + 1]; ++e) {
+        const uint32_t x = (uint32_t)col[e];
+        for (int64_t t = vs_off[x]; t < vs_off[x + 1]; ++t) cand[at++] = vs_sets[t];
+      }
+    }
+    // self appears at least once (shared variable); marked for removal below
+    for (int64_t t = cand_off[i]; t < at; ++t)
+      if (cand[t] == self) cand[t] = 0xFFFFFFFFu;
+  }
+}
+
+// distinct values of a sorted segment, ignoring the 0xFFFFFFFF "self" marker
+__global__ void unique_count_kernel(const uint32_t* keys, const int64_t* off, uint64_t m,
+                                    int64_t* cnt) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    int64_t c = 0;
+    for (int64_t t = off[i]; t < off[i + 1]; ++t)
+      if (keys[t] != 0xFFFFFFFFu && (t == off[i] || keys[t] != keys[t - 1])) ++c;
+    cnt[i] = c;
+  }
+}
+
+__global__ void unique_fill_kernel(const uint32_t* keys, const int64_t* off, uint64_t m,
+                                   const int64_t* out_off, uint32_t* out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    int64_t at = out_off[i];
+    for (int64_t t = off[i]; t < off[i + 1]; ++t)
+      if (keys[t] != 0xFFFFFFFFu && (t == off[i] || keys[t] != keys[t - 1])) out[at++] = keys[t];
+  }
+}
+
+__global__ void wp_key_kernel(const int64_t* deg_off, uint64_t m, uint64_t maxdeg,
+                              uint64_t* key) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t d = (uint64_t)(deg_off[i + 1] - deg_off[i]);
+    key[i] = ((maxdeg - d) << 32) | i;  // degree desc, index asc (scheduling.hpp:89-93)
+  }
+}
+
+__global__ void rank_kernel(const uint64_t* sorted_key, uint64_t m, uint32_t* rank) {
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < m;
+       t += (uint64_t)gridDim.x * blockDim.x)
+    rank[sorted_key[t] & 0xFFFFFFFFull] = (uint32_t)t;
+}
+
+// One Jones-Plassmann round in Welsh-Powell priority.  Colours are final once
+// written, so reading a colour set earlier in the same round is safe.
+__global__ void jp_round_kernel(const int64_t* off, const uint32_t* adj, const uint32_t* rank,
+                                int32_t* colour, uint64_t m, unsigned long long* coloured) {
+  unsigned long long mine = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    volatile int32_t* vc = colour;
+    if (vc[i] >= 0) continue;
+    const uint32_t ri = rank[i];
+    bool ready = true;
+    for (int64_t t = off[i]; t < off[i + 1]; ++t) {
+      const uint32_t j = adj[t];
+      if (rank[j] < ri && vc[j] < 0) {
+        ready = false;
+        break;
+      }
+    }
+    if (!ready) continue;
+    int32_t c = -1;
+    for (int32_t base = 0; c < 0; base += 64) {
+      uint64_t used = 0;
+      for (int64_t t = off[i]; t < off[i + 1]; ++t) {
+        const uint32_t j = adj[t];
+        if (rank[j] < ri) {
+          const int32_t cj = vc[j];
+          if (cj >= base && cj < base + 64) used |= 1ull << (cj - base);
+        }
+      }
+      if (~used) c = base + __ffsll((long long)~used) - 1;
+    }
+    vc[i] = c;
+    __threadfence();
+    ++mine;
+  }
+  if (mine) atomicAdd(coloured, mine);
+}
+
+__global__ void check_colouring_kernel(const int64_t* off, const uint32_t* adj,
+                                       const int32_t* colour, uint64_t m, int32_t k,
+                                       int* bad) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    if (colour[i] < 0 || colour[i] >= k) {
+      atomicExch(bad, 1);
+      continue;
+    }
+    for (int64_t t = off[i]; t < off[i + 1]; ++t)
+      if (colour[adj[t]] == colour[i]) atomicExch(bad, 1);
+  }
+}
+
+__global__ void max_colour_kernel(const int32_t* colour, uint64_t m, int* mx) {
+  int c = -1;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    c = max(c, colour[i]);
+  atomicMax(mx, c);
+}
+
+// footprint candidates: every subfunction (edge id) touching a variable of the set
+__global__ void fp_bound_kernel(const int64_t* set_off, const uint32_t* set_vars,
+                                const int32_t* row_ptr, uint64_t m, int64_t* bound) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    int64_t b = 0;
+    for (int64_t k = set_off[i]; k < set_off[i + 1]; ++k)
+      b += row_ptr[set_vars[k] + 1] - row_ptr[set_vars[k]];
+    bound[i] = b;
+  }
+}
+
+__global__ void fp_fill_kernel(const int64_t* set_off, const uint32_t* set_vars,
+                               const int32_t* row_ptr, const int32_t* eid, uint64_t m,
+                               const int64_t* cand_off, uint32_t* cand) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    int64_t at = cand_off[i];
+    for (int64_t k = set_off[i]; k < set_off[i + 1]; ++k) {
+      const uint32_t v = set_vars[k];
+      for (int32_t e = row_ptr[v]; e < row_ptr[v + 1]; ++e) cand[at++] = (uint32_t)eid[e];
+    }
+  }
+}
+
+__device__ uint32_t encode_endpoint(uint32_t x, const uint32_t* vars, int64_t f) {
+  int64_t lo = 0, hi = f;  // sets are sorted: binary search
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (vars[mid] < x) lo = mid + 1; else hi = mid;
+  }
+  return (lo < f && vars[lo] == x) ? (kInSet | (uint32_t)lo) : x;
+}
+
+__global__ void fp_entries_kernel(const int64_t* set_off, const uint32_t* set_vars,
+                                  const uint32_t* eu, const uint32_t* ev, const double* ew,
+                                  uint64_t m, const int64_t* fp_off, const uint32_t* fp_eid,
+                                  FpEntry* fp) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t* vars = set_vars + set_off[i];
+    const int64_t f = set_off[i + 1] - set_off[i];
+    for (int64_t t = fp_off[i]; t < fp_off[i + 1]; ++t) {
+      const uint32_t e = fp_eid[t];
+      FpEntry x;
+      x.a = encode_endpoint(eu[e], vars, f);
+      x.b = encode_endpoint(ev[e], vars, f);
+      x.w = ew[e];
+      fp[t] = x;
+    }
+  }
+}
+
+struct Scratch {
+  std::vector<void*> bufs;
+  template <typename T>
+  T* get(size_t count) {
+    void* p = nullptr;
+    GOMIX_CUDA(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+    bufs.push_back(p);
+    return static_cast<T*>(p);
+  }
+  ~Scratch() {
+    for (void* p : bufs) cudaFree(p);
+  }
+};
+
+void exclusive_scan(Scratch& S, const int64_t* in, int64_t* out, uint64_t cnt) {
+  size_t bytes = 0;
+  GOMIX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, (int64_t)cnt));
+  void* tmp = S.get<char>(bytes);
+  GOMIX_CUDA(cub::DeviceScan::ExclusiveSum(tmp, bytes, in, out, (int64_t)cnt));
+}
+
+int64_t read_back(const int64_t* p) {
+  int64_t v = 0;
+  GOMIX_CUDA(cudaMemcpy(&v, p, sizeof(v), cudaMemcpyDeviceToHost));
+  return v;
+}
+
+// CSR of per-set candidate lists -> sorted, unique lists (seg sort + compaction)
+void seg_sort_unique(Scratch& S, uint32_t* cand, const int64_t* cand_off, uint64_t m,
+                     uint64_t total, int64_t** out_off, uint32_t** out_vals,
+                     std::vector<void*>* keep) {
+  uint32_t* sorted = S.get<uint32_t>(total);
+  if (total > 0) {
+    size_t bytes = 0;
+    GOMIX_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, bytes, cand, sorted, (int64_t)total,
+                                                  (int64_t)m, cand_off, cand_off + 1));
+    void* tmp = S.get<char>(bytes);
+    GOMIX_CUDA(cub::DeviceSegmentedSort::SortKeys(tmp, bytes, cand, sorted, (int64_t)total,
+                                                  (int64_t)m, cand_off, cand_off + 1));
+  }
+  int64_t* cnt = S.get<int64_t>(m + 1);
+  GOMIX_CUDA(cudaMemset(cnt, 0, (m + 1) * sizeof(int64_t)));
+  unique_count_kernel<<<blocks_for(m), 256>>>(sorted, cand_off, m, cnt);
+  GOMIX_CUDA(cudaGetLastError());
+  int64_t* off = keep ? dev_alloc<int64_t>(*keep, m + 1) : S.get<int64_t>(m + 1);
+  exclusive_scan(S, cnt, off, m + 1);
+  const int64_t uniq = read_back(off + m);
+  uint32_t* vals = keep ? dev_alloc<uint32_t>(*keep, (size_t)uniq) : S.get<uint32_t>((size_t)uniq);
+  unique_fill_kernel<<<blocks_for(m), 256>>>(sorted, cand_off, m, off, vals);
+  GOMIX_CUDA(cudaGetLastError());
+  *out_off = off;
+  *out_vals = vals;
+}
+
+}  // namespace
+
+// Device part of problem construction.  Expects P's CSR, edge list and FOS
+// already uploaded (row_ptr, col, eu, ev, ew, set_off, set_vars) and eid in
+// `eid` (CSR entry -> edge id).
+void build_problem_device_impl(Problem& P, const int32_t* given_colour, const int32_t* eid) {
+  Scratch S;
+  const uint64_t m = P.m, nv = P.nv, entries = P.h_set_off[m];
+  // 1. inverse FOS: variable -> sets (ascending set id)
+  uint32_t* owner = S.get<uint32_t>(entries);
+  entry_owner_kernel<<<blocks_for(m), 256>>>(P.set_off, m, owner);
+  GOMIX_CUDA(cudaGetLastError());
+  uint32_t* vs_var = S.get<uint32_t>(entries);
+  uint32_t* vs_sets = S.get<uint32_t>(entries);
+  {
+    size_t bytes = 0;
+    GOMIX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, P.set_vars, vs_var, owner, vs_sets,
+                                               (int64_t)entries));
+    void* tmp = S.get<char>(bytes);
+    GOMIX_CUDA(cub::DeviceRadixSort::SortPairs(tmp, bytes, P.set_vars, vs_var, owner, vs_sets,
+                                               (int64_t)entries));
+  }
+  int64_t* vs_cnt = S.get<int64_t>(nv + 1);
+  GOMIX_CUDA(cudaMemset(vs_cnt, 0, (nv + 1) * sizeof(int64_t)));
+  count_kernel<<<blocks_for(entries), 256>>>(vs_var, entries, vs_cnt);
+  GOMIX_CUDA(cudaGetLastError());
+  int64_t* vs_off = S.get<int64_t>(nv + 1);
+  exclusive_scan(S, vs_cnt, vs_off, nv + 1);
+
+  // 2. LMIG: sorted unique adjacency per set
+  int64_t* bound = S.get<int64_t>(m + 1);
+  GOMIX_CUDA(cudaMemset(bound, 0, (m + 1) * sizeof(int64_t)));
+  lmig_bound_kernel<<<blocks_for(m), 256>>>(P.set_off, P.set_vars, vs_off, P.row_ptr, P.col, m, bound);
+  GOMIX_CUDA(cudaGetLastError());
+  int64_t* cand_off = S.get<int64_t>(m + 1);
+  exclusive_scan(S, bound, cand_off, m + 1);
+  const int64_t total = read_back(cand_off + m);
+  uint32_t* cand = S.get<uint32_t>((size_t)total);
+  lmig_fill_kernel<<<blocks_for(m), 256>>>(P.set_off, P.set_vars, vs_off, vs_sets, P.row_ptr,
+                                           P.col, m, cand_off, cand);
+  GOMIX_CUDA(cudaGetLastError());
+  int64_t* lmig_off = nullptr;
+  uint32_t* lmig_adj = nullptr;
+  seg_sort_unique(S, cand, cand_off, m, (uint64_t)total, &lmig_off, &lmig_adj, nullptr);
+  std::vector<int64_t> h_lmig_off(m + 1);
+  GOMIX_CUDA(cudaMemcpy(h_lmig_off.data(), lmig_off, (m + 1) * sizeof(int64_t),
+                        cudaMemcpyDeviceToHost));
+  P.lmig_edges = (uint64_t)h_lmig_off[m] / 2;
+  uint64_t maxdeg = 0;
+  for (uint64_t i = 0; i < m; ++i)
+    maxdeg = std::max<uint64_t>(maxdeg, (uint64_t)(h_lmig_off[i + 1] - h_lmig_off[i]));
+
+  // 3. colouring
+  int32_t* colour = S.get<int32_t>(m);
+  if (given_colour) {
+    GOMIX_CUDA(cudaMemcpy(colour, given_colour, m * sizeof(int32_t), cudaMemcpyHostToDevice));
+  } else {
+    uint64_t* key = S.get<uint64_t>(m);
+    uint64_t* key_sorted = S.get<uint64_t>(m);
+    wp_key_kernel<<<blocks_for(m), 256>>>(lmig_off, m, maxdeg, key);
+    GOMIX_CUDA(cudaGetLastError());
+    size_t bytes = 0;
+    GOMIX_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, key, key_sorted, (int64_t)m));
+    void* tmp = S.get<char>(bytes);
+    GOMIX_CUDA(cub::DeviceRadixSort::SortKeys(tmp, bytes, key, key_sorted, (int64_t)m));
+    uint32_t* rank = S.get<uint32_t>(m);
+    rank_kernel<<<blocks_for(m), 256>>>(key_sorted, m, rank);
+    GOMIX_CUDA(cudaGetLastError());
+    GOMIX_CUDA(cudaMemset(colour, 0xFF, m * sizeof(int32_t)));
+    unsigned long long* coloured = S.get<unsigned long long>(1);
+    GOMIX_CUDA(cudaMemset(coloured, 0, sizeof(unsigned long long)));
+    unsigned long long done = 0;
+    for (uint64_t round = 0; done < m; ++round) {
+      for (int r = 0; r < 16; ++r)
+        jp_round_kernel<<<blocks_for(m), 256>>>(lmig_off, lmig_adj, rank, colour, m, coloured);
+      GOMIX_CUDA(cudaGetLastError());
+      GOMIX_CUDA(cudaMemcpy(&done, coloured, sizeof(done), cudaMemcpyDeviceToHost));
+      if (round > 4 * m + 16) throw GomixError(GOMIX_E_STATE, "colouring did not converge");
+    }
+  }
+  int* mx = S.get<int>(2);
+  const int init[2] = {-1, 0};
+  GOMIX_CUDA(cudaMemcpy(mx, init, sizeof(init), cudaMemcpyHostToDevice));
+  max_colour_kernel<<<blocks_for(m), 256>>>(colour, m, mx);
+  GOMIX_CUDA(cudaGetLastError());
+  int kmax = 0;
+  GOMIX_CUDA(cudaMemcpy(&kmax, mx, sizeof(int), cudaMemcpyDeviceToHost));
+  P.k = (uint64_t)(kmax + 1);
+  check_colouring_kernel<<<blocks_for(m), 256>>>(lmig_off, lmig_adj, colour, m, (int32_t)P.k, mx + 1);
+  GOMIX_CUDA(cudaGetLastError());
+  int bad = 0;
+  GOMIX_CUDA(cudaMemcpy(&bad, mx + 1, sizeof(int), cudaMemcpyDeviceToHost));
+  if (bad) invalid("colouring: adjacent linkage sets share a colour (groups must be independent)");
+
+  // 4. groups: sets by colour, ascending set id inside a colour (scheduling.hpp:418-422)
+  {
+    uint32_t* ids = S.get<uint32_t>(m);
+    std::vector<uint32_t> h_ids(m);
+    std::iota(h_ids.begin(), h_ids.end(), 0u);
+    GOMIX_CUDA(cudaMemcpy(ids, h_ids.data(), m * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    int32_t* col_sorted = S.get<int32_t>(m);
+    P.gsets = dev_alloc<uint32_t>(P.allocations, m);
+    size_t bytes = 0;
+    GOMIX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, colour, col_sorted, ids, P.gsets,
+                                               (int64_t)m));
+    void* tmp = S.get<char>(bytes);
+    GOMIX_CUDA(cub::DeviceRadixSort::SortPairs(tmp, bytes, colour, col_sorted, ids, P.gsets,
+                                               (int64_t)m));
+    std::vector<int32_t> h_col(m);
+    std::vector<uint32_t> h_gs(m);
+    GOMIX_CUDA(cudaMemcpy(h_col.data(), col_sorted, m * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    GOMIX_CUDA(cudaMemcpy(h_gs.data(), P.gsets, m * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    P.group_off.assign(P.k + 1, 0);
+    for (uint64_t i = 0; i < m; ++i) P.group_off[(size_t)h_col[i] + 1]++;
+    for (uint64_t c = 0; c < P.k; ++c) P.group_off[c + 1] += P.group_off[c];
+    P.group_sets.assign(h_gs.begin(), h_gs.end());
+  }
+
+  // 5. footprint plans (multi-variable sets only; singletons read the CSR row)
+  P.footprint.assign(m, 0);
+  if (!P.univariate) {
+    int64_t* fb = S.get<int64_t>(m + 1);
+    GOMIX_CUDA(cudaMemset(fb, 0, (m + 1) * sizeof(int64_t)));
+    fp_bound_kernel<<<blocks_for(m), 256>>>(P.set_off, P.set_vars, P.row_ptr, m, fb);
+    GOMIX_CUDA(cudaGetLastError());
+    int64_t* fc_off = S.get<int64_t>(m + 1);
+    exclusive_scan(S, fb, fc_off, m + 1);
+    const int64_t ftotal = read_back(fc_off + m);
+    uint32_t* fcand = S.get<uint32_t>((size_t)ftotal);
+    fp_fill_kernel<<<blocks_for(m), 256>>>(P.set_off, P.set_vars, P.row_ptr, eid, m, fc_off, fcand);
+    GOMIX_CUDA(cudaGetLastError());
+    uint32_t* fp_eid = nullptr;
+    seg_sort_unique(S, fcand, fc_off, m, (uint64_t)ftotal, &P.fp_off, &fp_eid, &P.allocations);
+    std::vector<int64_t> h_fp_off(m + 1);
+    GOMIX_CUDA(cudaMemcpy(h_fp_off.data(), P.fp_off, (m + 1) * sizeof(int64_t),
+                          cudaMemcpyDeviceToHost));
+    P.fp = dev_alloc<FpEntry>(P.allocations, (size_t)h_fp_off[m]);
+    fp_entries_kernel<<<blocks_for(m), 256>>>(P.set_off, P.set_vars, P.eu, P.ev, P.ew, m, P.fp_off,
+                                              fp_eid, P.fp);
+    GOMIX_CUDA(cudaGetLastError());
+    for (uint64_t i = 0; i < m; ++i) {
+      P.footprint[i] = (uint64_t)(h_fp_off[i + 1] - h_fp_off[i]);
+      P.max_fp = std::max(P.max_fp, P.footprint[i]);
+    }
+  }
+  GOMIX_CUDA(cudaDeviceSynchronize());
+}
+
+}  // namespace gomix_b200

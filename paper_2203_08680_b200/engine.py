@@ -1,0 +1,384 @@
+"""Python face of the B200 GOM engine, mirroring the reference's engine API.
+
+    reference (proj/include/gomix/)                here
+    ModelArtifacts + groups (model.hpp:25-29)   -> GpuProblem
+    ParallelEngine (engine_parallel.hpp:255)    -> GpuParallelEngine
+    TerminationConfig/RunControl/RunContext     -> TerminationConfig / RunControl / RunContext
+      (runtime.hpp:50-161)
+    ImsDriver (ims.hpp:38-101), run_parallel    -> ImsDriver, run_parallel (run.py)
+
+All compute goes through libgomix_b200.so (C-ABI, include/gomix_gpu.h); this
+module only marshals arrays and keeps the run-wide bookkeeping the reference
+keeps on the host.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass, field
+from typing import Callable, List, Optional
+
+import numpy as np
+
+from . import _capi
+from ._capi import check, lib
+from .maxcut import Fos, MaxCutInstance
+
+
+def mix64(x: int) -> int:
+    """rng.hpp:11-16."""
+    M = (1 << 64) - 1
+    x = (x + 0x9E3779B97F4A7C15) & M
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & M
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & M
+    return x ^ (x >> 31)
+
+
+def population_seed(run_seed: int, population_id: int) -> int:
+    """run.hpp:36-39."""
+    return mix64((run_seed + 0x9E3779B97F4A7C15 * population_id) & ((1 << 64) - 1))
+
+
+@dataclass
+class FitnessComparator:
+    """graybox.hpp:22-35."""
+    exact: bool = True
+    rel_tol: float = 1e-9
+
+    def scale(self, a, b):
+        return self.rel_tol * max(1.0, abs(a), abs(b))
+
+    def better(self, a, b):
+        return a > b if self.exact else a - b > self.scale(a, b)
+
+    def equal(self, a, b):
+        return a == b if self.exact else abs(a - b) <= self.scale(a, b)
+
+
+# ---------------------------------------------------------------------------
+# run bookkeeping (runtime.hpp)
+# ---------------------------------------------------------------------------
+@dataclass
+class TerminationConfig:
+    max_evaluations: Optional[float] = None  # gray-box units
+    max_seconds: Optional[float] = None
+    target_fitness: Optional[float] = None
+    max_generations: Optional[int] = None
+
+
+@dataclass
+class TraceRecord:
+    seconds: float
+    evaluations: float
+    generation: int
+    population: int
+    fitness: float
+
+
+class RunControl:
+    """runtime.hpp:60-123; evaluator calls are an exact integer count."""
+
+    def __init__(self, cfg: TerminationConfig, cmp: FitnessComparator, num_subfunctions: int):
+        self.cfg, self.cmp, self.q = cfg, cmp, num_subfunctions
+        self.calls = 0
+        self.stop = False
+        self.reason = "none"
+        self.start()
+
+    def start(self):
+        self._t0 = time.perf_counter()
+
+    def elapsed_seconds(self):
+        return time.perf_counter() - self._t0
+
+    def evaluations(self):
+        return 0.0 if self.q == 0 else self.calls / self.q
+
+    def add_evaluator_calls(self, calls: int):
+        self.calls += int(calls)
+        if self.cfg.max_evaluations is not None and self.evaluations() >= self.cfg.max_evaluations:
+            self.request_stop("evaluation-budget")
+
+    def check_time(self):
+        if not self.stop and self.cfg.max_seconds is not None and self.elapsed_seconds() >= self.cfg.max_seconds:
+            self.request_stop("wall-clock")
+
+    def note_best(self, fitness):
+        t = self.cfg.target_fitness
+        if not self.stop and t is not None and (self.cmp.better(fitness, t) or self.cmp.equal(fitness, t)):
+            self.request_stop("target-reached")
+
+    def stop_requested(self):
+        return self.stop
+
+    def request_stop(self, reason: str):
+        if not self.stop:
+            self.stop, self.reason = True, reason
+
+    def criteria(self) -> _capi.StopCriteria:
+        c = self.cfg
+        return _capi.StopCriteria(c.max_evaluations is not None, c.max_evaluations or 0.0, self.calls,
+                                  c.target_fitness is not None, c.target_fitness or 0.0)
+
+
+class TraceSink:
+    def improvement(self, rec: TraceRecord):
+        pass
+
+    def boundary(self, rec: TraceRecord):
+        pass
+
+
+class RecordingSink(TraceSink):
+    def __init__(self):
+        self.rows: List[TraceRecord] = []
+
+    def improvement(self, rec):
+        self.rows.append(rec)
+
+
+class RunContext:
+    """runtime.hpp:128-161: shared control, trace sink and monotone best."""
+
+    def __init__(self, cfg: TerminationConfig, cmp: FitnessComparator, num_subfunctions: int,
+                 sink: Optional[TraceSink] = None):
+        self.control = RunControl(cfg, cmp, num_subfunctions)
+        self.sink = sink
+        self.cmp = cmp
+        self.best: Optional[float] = None
+
+    def report_improvement(self, fitness, generation, population):
+        if self.best is not None and not self.cmp.better(fitness, self.best):
+            return
+        self.best = fitness
+        self.control.note_best(fitness)
+        if self.sink:
+            self.sink.improvement(TraceRecord(self.control.elapsed_seconds(), self.control.evaluations(),
+                                              generation, population, fitness))
+
+    def report_boundary(self, fitness, generation, population):
+        self.control.check_time()
+        if not self.sink:
+            return
+        if self.best is not None and self.cmp.better(self.best, fitness):
+            fitness = self.best
+        self.sink.boundary(TraceRecord(self.control.elapsed_seconds(), self.control.evaluations(),
+                                       generation, population, fitness))
+
+
+# ---------------------------------------------------------------------------
+# problem (shared model) and engine (one population)
+# ---------------------------------------------------------------------------
+class GpuProblem:
+    """Device-resident instance + FOS + GPU Welsh-Powell colour groups + plans.
+    colour: optional prebuilt ColorGroups as one colour per set (adopted like
+    EngineConfig::fixed_model, engine_parallel.hpp:271-272)."""
+
+    def __init__(self, instance: MaxCutInstance, fos: Fos, colour=None, device: int = 0):
+        self.instance, self.fos = instance, fos
+        L = lib()
+        h = C.c_void_p()
+        col = None if colour is None else np.ascontiguousarray(colour, np.int32)
+        check(L.gomix_gpu_problem_create(C.byref(instance._struct()), C.byref(fos._struct()),
+                                         _capi.ptr(col), device, C.byref(h)))
+        self.h = h
+        info = _capi.ProblemInfo()
+        check(L.gomix_gpu_problem_info(self.h, C.byref(info)))
+        self.info = info
+        k = info.num_groups
+        off = np.zeros(k + 1, np.uint64)
+        sets = np.zeros(info.num_sets, np.uint64)
+        check(L.gomix_gpu_problem_groups(self.h, off.ctypes.data, sets.ctypes.data))
+        self.group_offset, self.group_sets = off, sets
+        fp = np.zeros(info.num_sets, np.uint64)
+        check(L.gomix_gpu_problem_footprints(self.h, fp.ctypes.data))
+        self.footprints = fp
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().gomix_gpu_problem_destroy(self.h)
+            self.h = None
+
+    @property
+    def num_groups(self) -> int:
+        return int(self.info.num_groups)
+
+    @property
+    def groups(self):
+        o = self.group_offset
+        return [self.group_sets[o[c]:o[c + 1]] for c in range(self.num_groups)]
+
+    def colour(self) -> np.ndarray:
+        col = np.zeros(self.info.num_sets, np.int32)
+        for c, g in enumerate(self.groups):
+            col[g] = c
+        return col
+
+    @property
+    def exact(self) -> bool:
+        return bool(self.info.exact)
+
+    def comparator(self) -> FitnessComparator:
+        return FitnessComparator(self.exact)
+
+
+class GpuParallelEngine:
+    """ParallelEngine (engine_parallel.hpp:255-368) on a B200.
+
+    mode "replay": init, group order and donors follow the reference's
+    RngStream(seed) exactly (bit-identical populations); "philox": donors are
+    drawn on the device from a counter-based stream (production)."""
+
+    def __init__(self, problem: GpuProblem, population_size: int, seed: int = 1,
+                 ctx: Optional[RunContext] = None, population_id: int = 1, mode: str = "replay",
+                 record_batch: bool = False, ordered_float: bool = False, time_kernels: bool = False,
+                 genotypes: Optional[np.ndarray] = None, stream=None):
+        if population_size <= 0:
+            raise ValueError("engine: population must be non-empty")
+        self.problem = problem
+        self.n = int(population_size)
+        self.pop_id = population_id
+        self.ctx = ctx if ctx is not None else RunContext(TerminationConfig(), problem.comparator(),
+                                                          problem.info.num_edges)
+        flags = (_capi.FLAG_RECORD_BATCH if record_batch else 0) | (_capi.FLAG_ORDERED_FLOAT if ordered_float else 0) \
+            | (_capi.FLAG_TIME_KERNELS if time_kernels else 0)
+        cfg = _capi.EngineConfig(self.n, seed, _capi.MODE_REPLAY if mode == "replay" else _capi.MODE_PHILOX,
+                                 flags, population_id, 0, 1, None)
+        h = C.c_void_p()
+        check(lib().gomix_gpu_engine_create(problem.h, C.byref(cfg), C.byref(h)))
+        self.h = h
+        if stream is not None:
+            check(lib().gomix_gpu_set_stream(self.h, C.c_void_p(stream)))
+        self._elitist_fitness = None
+        g = None
+        if genotypes is not None:
+            g = np.ascontiguousarray(genotypes, np.uint8)
+            if g.shape != (self.n, problem.info.num_vertices):
+                raise ValueError("graybox: genotype shape mismatch")
+        stats = _capi.RunStats()
+        crit = self.ctx.control.criteria()
+        check(lib().gomix_gpu_init_population(self.h, _capi.ptr(g), C.byref(crit), C.byref(stats)))
+        self._absorb(stats, generation=0)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().gomix_gpu_engine_destroy(self.h)
+            self.h = None
+
+    # ---- bookkeeping shared with RunContext -----------------------------------
+    def _absorb(self, stats: _capi.RunStats, generation: int):
+        ctl = self.ctx.control
+        ctl.calls += int(stats.evaluator_calls)
+        if stats.stopped:
+            ctl.request_stop(_capi.STOP_NAMES[stats.stop_reason])
+        for f in self.improvements(int(stats.improvements)):
+            self.ctx.report_improvement(float(f), generation, self.pop_id)
+        self._elitist_fitness = float(stats.elitist_fitness)
+        self.last_stats = stats
+
+    def improvements(self, count: int) -> np.ndarray:
+        buf = np.zeros(max(count, 1), np.float64)
+        got = C.c_uint64()
+        check(lib().gomix_gpu_read_improvements(self.h, buf.ctypes.data, count, C.byref(got)))
+        return buf[:got.value]
+
+    # ---- GenerationRunner (ims.hpp:14-22) -----------------------------------------
+    def run_generation(self):
+        ctl = self.ctx.control
+        if ctl.stop_requested():
+            return
+        mg = ctl.cfg.max_generations
+        if mg is not None and self.generation() >= mg:
+            ctl.request_stop("generation-limit")
+            return
+        gen = self.generation()
+        stats = _capi.RunStats()
+        crit = ctl.criteria()
+        check(lib().gomix_gpu_run_generation(self.h, C.byref(crit), C.byref(stats)))
+        self._absorb(stats, gen)
+        if not stats.stopped:
+            self.ctx.report_boundary(self._elitist_fitness, self.generation(), self.pop_id)
+
+    def generation(self) -> int:
+        g = C.c_int64()
+        check(lib().gomix_gpu_generation(self.h, C.byref(g)))
+        return g.value
+
+    def elitist(self):
+        g = np.zeros(self.problem.info.num_vertices, np.uint8)
+        f = C.c_double()
+        check(lib().gomix_gpu_read_elitist(self.h, g.ctypes.data, C.byref(f)))
+        return g, f.value
+
+    @property
+    def elitist_fitness(self) -> float:
+        return self._elitist_fitness
+
+    def offer_elitist(self, genotype, fitness) -> bool:
+        adopted = C.c_int32()
+        g = np.ascontiguousarray(genotype, np.uint8)
+        check(lib().gomix_gpu_offer_elitist(self.h, g.ctypes.data, float(fitness), C.byref(adopted)))
+        if adopted.value:
+            self._elitist_fitness = float(fitness)
+        return bool(adopted.value)
+
+    # ---- batched group step (phase-level API) ----------------------------------
+    def run_group(self, group: int, donor=None):
+        """One batched GOM step over colour group `group`; donor (n x |G|,
+        GroupBatch order) given explicitly or drawn by the engine."""
+        d = None if donor is None else np.ascontiguousarray(donor, np.int32)
+        stats = _capi.RunStats()
+        crit = self.ctx.control.criteria()
+        check(lib().gomix_gpu_run_group(self.h, group, _capi.ptr(d), C.byref(crit), C.byref(stats)))
+        self._absorb(stats, self.generation())
+        return stats
+
+    def read_batch(self, group: int):
+        G = int(self.problem.group_offset[group + 1] - self.problem.group_offset[group])
+        d = np.zeros((self.n, G), np.int32)
+        de = np.zeros((self.n, G), np.float64)
+        p = np.zeros((self.n, G), np.uint8)
+        a = np.zeros((self.n, G), np.uint8)
+        check(lib().gomix_gpu_read_batch(self.h, d.ctypes.data, de.ctypes.data, p.ctypes.data, a.ctypes.data))
+        return d, de, p, a
+
+    # ---- introspection -------------------------------------------------------------
+    def population(self):
+        g = np.zeros((self.n, self.problem.info.num_vertices), np.uint8)
+        f = np.zeros(self.n, np.float64)
+        check(lib().gomix_gpu_read_population(self.h, g.ctypes.data, f.ctypes.data))
+        return g, f
+
+    def population_packed(self) -> np.ndarray:
+        wp = C.c_uint64()
+        check(lib().gomix_gpu_read_population_packed(self.h, None, C.byref(wp)))
+        out = np.zeros((self.problem.info.num_vertices, wp.value), np.uint32)
+        check(lib().gomix_gpu_read_population_packed(self.h, out.ctypes.data, C.byref(wp)))
+        return out
+
+    def group_counters(self):
+        k = self.problem.num_groups
+        s, st, ca = (np.zeros(k, np.uint64) for _ in range(3))
+        check(lib().gomix_gpu_group_counters(self.h, s.ctypes.data, st.ctypes.data, ca.ctypes.data))
+        return s, st, ca
+
+    def kernel_times(self) -> np.ndarray:
+        cnt = C.c_uint64()
+        check(lib().gomix_gpu_kernel_times(self.h, None, 0, C.byref(cnt)))
+        buf = np.zeros(max(cnt.value, 1), np.float32)
+        check(lib().gomix_gpu_kernel_times(self.h, buf.ctypes.data, cnt.value, C.byref(cnt)))
+        return buf[:cnt.value]
+
+    def launch_count(self) -> int:
+        c = C.c_uint64()
+        check(lib().gomix_gpu_launch_count(self.h, C.byref(c)))
+        return c.value
+
+
+def gpu_color(instance: MaxCutInstance, fos: Fos, device: int = 0):
+    """GPU Welsh-Powell colouring: (colour per set, k, LMIG edge count)."""
+    col = np.zeros(fos.num_sets, np.int32)
+    k, e = C.c_uint64(), C.c_uint64()
+    check(lib().gomix_gpu_color(C.byref(instance._struct()), C.byref(fos._struct()), device,
+                                col.ctypes.data, C.byref(k), C.byref(e)))
+    return col, k.value, e.value

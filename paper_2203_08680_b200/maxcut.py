@@ -1,0 +1,174 @@
+"""Max-Cut instances and linkage models (inputs of the GOM path).
+
+Mirrors the reference's MaxCutInstance (maxcut.hpp:21-37), generate_torus
+(maxcut.hpp:121-147), the edge-list format (maxcut.hpp:160-248) and the Fos
+type (linkage.hpp:124-131).  Generators run in the product library's host code
+(gomix_generate_*), so a torus equals the reference's for the same seed.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _capi
+
+
+@dataclass
+class MaxCutInstance:
+    num_vertices: int
+    edge_u: np.ndarray  # uint32, u < v, sorted by (u, v), unique
+    edge_v: np.ndarray
+    edge_w: np.ndarray  # float64
+
+    @property
+    def num_edges(self) -> int:
+        return len(self.edge_u)
+
+    def integer_weights(self) -> bool:  # maxcut.hpp:32-36
+        w = self.edge_w
+        return bool(np.all(w == np.floor(w)) and np.all(np.abs(w) <= 9e15))
+
+    def cut_value(self, genotype) -> float:  # maxcut.hpp:57-64 (left to right)
+        g = np.asarray(genotype)
+        cut = g[self.edge_u] != g[self.edge_v]
+        total = 0.0
+        for x in self.edge_w[cut]:
+            total += float(x)
+        return total
+
+    def cut_values(self, genotypes: np.ndarray) -> np.ndarray:
+        """Vectorised cut values (exact for integer weights)."""
+        g = np.asarray(genotypes)
+        cut = g[:, self.edge_u] != g[:, self.edge_v]
+        return cut.astype(np.float64) @ self.edge_w
+
+    def adjacency(self):
+        """VIG adjacency (graybox.hpp:305-323) as a list of sorted arrays."""
+        nbrs = [[] for _ in range(self.num_vertices)]
+        for a, b in zip(self.edge_u.tolist(), self.edge_v.tolist()):
+            nbrs[a].append(b)
+            nbrs[b].append(a)
+        return [np.array(sorted(x), np.uint32) for x in nbrs]
+
+    def _struct(self):
+        self._keep = (np.ascontiguousarray(self.edge_u, np.uint32), np.ascontiguousarray(self.edge_v, np.uint32),
+                      np.ascontiguousarray(self.edge_w, np.float64))
+        return _capi.Maxcut(self.num_vertices, len(self.edge_u), *(a.ctypes.data for a in self._keep))
+
+
+def _weights(weights):
+    if weights in ("unit", None) or weights[0] == "unit":
+        return 0, 1, 1
+    if weights[0] == "int":
+        return 1, int(weights[1]), int(weights[2])
+    if weights[0] == "real":
+        return 2, 0, 0
+    raise ValueError("weights: 'unit' | ('int', lo, hi) | ('real',)")
+
+
+def generate_torus(width: int, height: int, weights=("int", 1, 10), seed: int = 1) -> MaxCutInstance:
+    """maxcut.hpp:121-147: 2-D wrap-around grid, 2*width*height edges."""
+    kind, lo, hi = _weights(weights)
+    q = 2 * width * height
+    eu, ev, ew = np.zeros(q, np.uint32), np.zeros(q, np.uint32), np.zeros(q, np.float64)
+    _capi.check(_capi.lib().gomix_generate_torus(width, height, kind, lo, hi, seed, eu.ctypes.data,
+                                                  ev.ctypes.data, ew.ctypes.data))
+    return MaxCutInstance(width * height, eu, ev, ew)
+
+
+def generate_regular(num_vertices: int, degree: int, weights=("real",), seed: int = 1) -> MaxCutInstance:
+    """Random simple d-regular graph (BASELINE config C4)."""
+    kind, lo, hi = _weights(weights)
+    q = num_vertices * degree // 2
+    eu, ev, ew = np.zeros(q, np.uint32), np.zeros(q, np.uint32), np.zeros(q, np.float64)
+    _capi.check(_capi.lib().gomix_generate_regular(num_vertices, degree, kind, lo, hi, seed, eu.ctypes.data,
+                                                    ev.ctypes.data, ew.ctypes.data))
+    return MaxCutInstance(num_vertices, eu, ev, ew)
+
+
+def save_edge_list(path: str, inst: MaxCutInstance) -> None:
+    """maxcut.hpp:240-248: header, then 1-based "u v w"; integral weights as integers."""
+    with open(path, "w") as fh:
+        fh.write(f"{inst.num_vertices} {inst.num_edges}\n")
+        for a, b, w in zip(inst.edge_u.tolist(), inst.edge_v.tolist(), inst.edge_w.tolist()):
+            ws = str(int(w)) if w == math.floor(w) and abs(w) <= 9e15 else repr(float(w))
+            fh.write(f"{a + 1} {b + 1} {ws}\n")
+
+
+def load_edge_list(path: str) -> MaxCutInstance:
+    """maxcut.hpp:163-226 (1-based, '#' comments, duplicates rejected)."""
+    rows = []
+    header = None
+    with open(path) as fh:
+        for ln, line in enumerate(fh, 1):
+            s = line.strip()
+            if not s or s.startswith("#"):
+                continue
+            parts = s.split()
+            if header is None:
+                if len(parts) != 2:
+                    raise ValueError(f"line {ln}: malformed header")
+                header = (int(parts[0]), int(parts[1]))
+                continue
+            if len(parts) != 3:
+                raise ValueError(f"line {ln}: malformed edge line")
+            a, b, w = int(parts[0]) - 1, int(parts[1]) - 1, float(parts[2])
+            if a == b:
+                raise ValueError(f"line {ln}: self-loop")
+            rows.append((min(a, b), max(a, b), w))
+    if header is None:
+        raise ValueError("missing header")
+    if len(rows) != header[1]:
+        raise ValueError("edge count differs from the header")
+    rows.sort()
+    u = np.array([r[0] for r in rows], np.uint32)
+    v = np.array([r[1] for r in rows], np.uint32)
+    if len(set(zip(u.tolist(), v.tolist()))) != len(rows):
+        raise ValueError("duplicate edge")
+    return MaxCutInstance(header[0], u, v, np.array([r[2] for r in rows], np.float64))
+
+
+@dataclass
+class Fos:
+    """Family of linkage sets (linkage.hpp:124-131) in CSR form."""
+    num_variables: int
+    set_offset: np.ndarray  # uint64, num_sets + 1
+    set_vars: np.ndarray    # uint32
+
+    @property
+    def num_sets(self) -> int:
+        return len(self.set_offset) - 1
+
+    def set(self, i: int) -> np.ndarray:
+        return self.set_vars[self.set_offset[i]:self.set_offset[i + 1]]
+
+    @staticmethod
+    def from_sets(num_variables: int, sets) -> "Fos":
+        off = np.zeros(len(sets) + 1, np.uint64)
+        off[1:] = np.cumsum([len(s) for s in sets])
+        vars_ = np.concatenate([np.asarray(s, np.uint32) for s in sets]) if sets else np.zeros(0, np.uint32)
+        return Fos(num_variables, off, vars_)
+
+    def _struct(self):
+        self._keep = (np.ascontiguousarray(self.set_offset, np.uint64), np.ascontiguousarray(self.set_vars, np.uint32))
+        return _capi.Fos(self.num_sets, self._keep[0].ctypes.data, self._keep[1].ctypes.data)
+
+
+def univariate_fos(num_variables: int) -> Fos:
+    """Singletons in variable order (the CLI's `univariate` = bound 1)."""
+    return Fos(num_variables, np.arange(num_variables + 1, dtype=np.uint64),
+               np.arange(num_variables, dtype=np.uint32))
+
+
+def neighbourhood_fos(inst: MaxCutInstance) -> Fos:
+    """Set v = {v} U N(v), sorted (BASELINE config C2's 'neighbourhood FOS')."""
+    nv = inst.num_vertices
+    u = np.concatenate([inst.edge_u, inst.edge_v, np.arange(nv, dtype=np.uint32)])
+    v = np.concatenate([inst.edge_v, inst.edge_u, np.arange(nv, dtype=np.uint32)])
+    order = np.lexsort((v, u))
+    u, v = u[order], v[order]
+    off = np.zeros(nv + 1, np.uint64)
+    np.add.at(off, u.astype(np.int64) + 1, 1)
+    return Fos(nv, np.cumsum(off).astype(np.uint64), v.astype(np.uint32))
