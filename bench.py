@@ -1,0 +1,389 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 GOM engine on BASELINE.json's headline metric.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+
+One step = one GOM generation (ParallelEngine::run_generation,
+engine_parallel.hpp:283-316) of the workload; the unit of work is one partial
+evaluation = one executed (solution, linkage set) GOM step
+(RunResult::GroupCounter::steps, runtime.hpp:170-175).
+
+Default workload (BASELINE.json configs[1], the 1-B200 config): C2 = Max-Cut
+2-D torus 100x100 (10^4 vertices), integer weights U[1,10] (generate_torus,
+seed 1), neighbourhood FOS, population 64, Philox donors.
+
+ours:
+  value  device throughput, inputs resident in HBM: CUDA events on the engine's
+         stream around each generation; L2 flushed (256 MiB write) between
+         timed generations, outside the events.
+  e2e    through the C-ABI with HOST buffers: every step uploads the whole
+         population (genotypes + fitness), runs the generation and reads the
+         population back (gomix_gpu_load_population / run_generation /
+         read_population), wall clock.
+  roofline  gom_group_kernel (dominant kernel): algorithmic bytes (SURVEY.md
+         §8(d) B_step x steps) / its CUDA-event durations vs measured HBM peak.
+  cpu_baseline  the reference ParallelEngine (oracle/_ref, compiled from the
+         reference headers) with every host thread, a bounded sample.
+reference:
+  the reference's own CPU ParallelEngine (oracle/_ref/ref_driver) on this
+  box's host cores, W + K generations of the same workload; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Max-Cut partial evals/sec; time-to-best-known cut (s) at 1/2/4/8 B200"
+UNIT = "partial evaluations/s"
+
+CONFIGS = {
+    "c2": dict(workload="C2: Max-Cut 2-D torus 100x100 (1e4 vertices), integer weights U[1,10] "
+                        "(generate_torus seed 1), neighbourhood FOS, population 64",
+               width=100, height=100, weights=("int", 1, 10), fos="neigh", n=64, ref_fos="neigh"),
+    "c3": dict(workload="C3: Max-Cut 2-D torus 1000x1000 (1e6 vertices), integer weights U[1,10], "
+                        "univariate FOS, population 128",
+               width=1000, height=1000, weights=("int", 1, 10), fos="uni", n=128, ref_fos="univariate"),
+    "c1": dict(workload="C1: Max-Cut 2-D torus 10x10, integer weights U[1,10], univariate FOS, population 32",
+               width=10, height=10, weights=("int", 1, 10), fos="uni", n=32, ref_fos="univariate"),
+    "c5": dict(workload="C5: Max-Cut 2-D torus 316x316 (~1e5 vertices), integer weights U[1,10], "
+                        "univariate FOS, population 1024",
+               width=316, height=316, weights=("int", 1, 10), fos="uni", n=1024, ref_fos="univariate"),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--population", type=int, default=None)
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def ref_cmd(cfg, n, gens, workers):
+    w = cfg["weights"]
+    wspec = "unit" if w == "unit" else f"int:{w[1]}:{w[2]}"
+    return [os.path.join(ROOT, "oracle", "_ref", "ref_driver"), "bench", "--torus", str(cfg["width"]),
+            str(cfg["height"]), "--weights", wspec, "--inst-seed", "1", "--fos", cfg["ref_fos"], "--n", str(n),
+            "--seed", "1", "--gens", str(gens), "--workers", str(workers)]
+
+
+def run_reference(cfg, n, gens, workers, timeout=3600):
+    """The reference ParallelEngine compiled from its own headers (oracle/_ref)."""
+    res = subprocess.run(ref_cmd(cfg, n, gens, workers), capture_output=True, text=True, timeout=timeout)
+    if res.returncode != 0:
+        raise RuntimeError(f"ref_driver failed: {res.stderr.strip()}")
+    return json.loads(res.stdout)
+
+
+def base_line(args, cfg, n, world):
+    return {"metric": METRIC, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic (generated Max-Cut torus, reference generator and seed)",
+            "config": {"workload": cfg["workload"], "population": n, "population_per_gpu": n,
+                       "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "l2": "flushed between timed steps (256 MiB write)",
+                       "donors": "philox", "fos": cfg["fos"]}}
+
+
+# ---------------------------------------------------------------------------
+# reference arm
+# ---------------------------------------------------------------------------
+def bench_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    n = args.population or cfg["n"]
+    workers = os.cpu_count() or 1
+    if not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "ref_driver")):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/ref_driver was not built"}))
+        return
+    out = run_reference(cfg, n, args.warmup + args.steps, workers)
+    gens = out["gens"][args.warmup:]
+    secs = sum(g["seconds"] for g in gens)
+    steps = sum(g["steps"] for g in gens)
+    value = steps / secs
+    line = base_line(args, cfg, n, world)
+    line.update({"impl": "reference", "value": value, "ms_per_step": 1e3 * secs / len(gens), "dtype": "f64",
+                 "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "reference",
+                                  "sample": f"{len(gens)} generations of {args.config} after {args.warmup} "
+                                            f"warm-up, ParallelEngine(workers={workers})"},
+                 "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
+    line["config"]["parallelism"] = f"cpu ParallelEngine workers={workers}"
+    line["config"]["donors"] = "reference RngStream"
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                       "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.p.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 8 and parts[0] == str(self.idx):
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.p:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.p.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(self.rows[0][2]) if self.rows[0][2].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def algorithmic_bytes_per_step(inst, fos, n):
+    """B_step(F) = ((|F| + |N(F)|) + 2|F|)/8 + G_F/n with
+    G_F = 4(1+|F|) + sum_{v in F}(4 + deg(v)(4 + 8)), averaged over the sets."""
+    import numpy as np
+
+    nv = inst.num_vertices
+    deg = np.bincount(np.concatenate([inst.edge_u, inst.edge_v]), minlength=nv)
+    adj = inst.adjacency()
+    total = 0.0
+    for i in range(fos.num_sets):
+        F = fos.set(i)
+        nf = set()
+        for v in F.tolist():
+            nf.update(adj[v].tolist())
+        nf.difference_update(F.tolist())
+        gf = 4 * (1 + len(F)) + sum(4 + int(deg[v]) * 12 for v in F.tolist())
+        total += ((len(F) + len(nf)) + 2 * len(F)) / 8.0 + gf / n
+    return total / fos.num_sets
+
+
+def bench_ours(args):
+    import numpy as np
+    import torch
+
+    import paper_2203_08680_b200 as G
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist = None
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+    cfg = CONFIGS[args.config]
+    n = args.population or cfg["n"]
+    inst = G.generate_torus(cfg["width"], cfg["height"], cfg["weights"], 1)
+    fos = G.univariate_fos(inst.num_vertices) if cfg["fos"] == "uni" else G.neighbourhood_fos(inst)
+    P = G.GpuProblem(inst, fos, device=dev)
+    stream = torch.cuda.current_stream()
+    E = G.GpuParallelEngine(P, n, seed=1 + rank, mode="philox", time_kernels=True, stream=stream.cuda_stream)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    # warm-up
+    for _ in range(max(args.warmup, 3)):
+        E.run_generation_async()
+    E.synchronize()
+    E.kernel_times()
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MiB > 126 MB L2
+
+    # ---- device-resident timed region ----
+    _, steps0, calls0 = E.group_counters()
+    launches0 = E.launch_count()
+    gpu_index = local
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if vis:
+        try:
+            gpu_index = int(vis.split(",")[local])
+        except ValueError:
+            pass
+    clocks = ClockSampler(gpu_index)
+    clocks.start()
+    time.sleep(0.25)
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize()
+    t_wall0 = time.perf_counter()
+    for i in range(args.steps):
+        flush.zero_()
+        ev0[i].record(stream)
+        E.run_generation_async()
+        ev1[i].record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    t_wall = time.perf_counter() - t_wall0
+    _, steps1, calls1 = E.group_counters()
+    launches = E.launch_count() - launches0
+    step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
+    kern_ms = E.kernel_times()
+    # keep the GPU busy for the clock record when the timed region was short
+    soak_t0 = time.perf_counter()
+    while time.perf_counter() - soak_t0 < max(0.0, 0.6 - t_wall):
+        for _ in range(20):
+            E.run_generation_async()
+        torch.cuda.synchronize()
+    E.synchronize()
+    E.kernel_times()
+    clk = clocks.stop()
+
+    dev_s = sum(step_ms) / 1e3
+    steps = int((steps1 - steps0).sum())
+    calls = int((calls1 - calls0).sum())
+    if dist is not None:
+        t = torch.tensor([dev_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        s = torch.tensor([steps, calls], dtype=torch.float64, device="cuda")
+        dist.all_reduce(s, op=dist.ReduceOp.SUM)
+        dev_s, steps, calls = float(t.item()), int(s[0].item()), int(s[1].item())
+    value = steps / dev_s
+
+    # ---- e2e through the C-ABI with host buffers ----
+    e2e_steps = args.e2e_steps or min(args.steps, 50)
+    g_host, f_host = E.population()
+    g_host = np.ascontiguousarray(g_host)
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e2e_done = 0
+    for _ in range(e2e_steps):
+        E.load_population(g_host, f_host)          # H2D: n*l genotype bytes + n fitness doubles
+        E.run_generation()
+        e2e_done += int(E.last_stats.steps)
+        g_host, f_host = E.population()            # D2H: n*l genotype bytes + n fitness doubles
+    torch.cuda.synchronize()
+    barrier()
+    e2e_s = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        s = torch.tensor([e2e_done], dtype=torch.float64, device="cuda")
+        dist.all_reduce(s, op=dist.ReduceOp.SUM)
+        e2e_s, e2e_done = float(t.item()), int(s.item())
+    io_bytes = n * inst.num_vertices + 8 * n
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel ----
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peaks = json.load(fh)
+    except OSError:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"
+    b_step = algorithmic_bytes_per_step(inst, fos, n)
+    local_steps = int((steps1 - steps0).sum())
+    kern_s = float(np.sum(kern_ms)) / 1e3
+    achieved = local_steps * b_step / kern_s / 1e9 if kern_s > 0 else None
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            tr = json.load(fh).get(args.config)
+            if tr and tr.get("population") == n:
+                traffic = tr["dram_bytes_per_launch"]
+    except (OSError, ValueError):
+        pass
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak if achieved else None, "traffic": traffic,
+                "kernel": "gom_group_kernel", "bytes_per_step": b_step,
+                "launches": int(len(kern_ms)), "avg_launch_us": 1e6 * kern_s / max(1, len(kern_ms)),
+                "kernel_share_of_step": kern_s / dev_s if dev_s else None, "peak_source": peak_src}
+
+    cpu_baseline = None
+    if world == 1 and not args.no_cpu_baseline:
+        ref = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
+        workers = os.cpu_count() or 1
+        gens = 8 if args.config in ("c2", "c1") else 2
+        if os.path.exists(ref):
+            try:
+                out = run_reference(cfg, n, gens, workers, timeout=900)
+                secs = sum(g["seconds"] for g in out["gens"])
+                st = sum(g["steps"] for g in out["gens"])
+                cpu_baseline = {"value": st / secs, "unit": UNIT, "cores": workers, "kind": "reference",
+                                "sample": f"{gens} generations of {args.config} ({st} partial evaluations), "
+                                          f"reference ParallelEngine(workers={workers}) built from its headers"}
+            except Exception as exc:  # noqa: BLE001
+                cpu_baseline = {"value": None, "unit": UNIT, "cores": workers, "kind": "reference",
+                                "sample": f"failed: {exc}"}
+
+    line = base_line(args, cfg, n, world)
+    line.update({
+        "value": value,
+        "ms_per_step": 1e3 * dev_s / args.steps,
+        "e2e": {"value": e2e_done / e2e_s, "unit": UNIT, "h2d_bytes_per_step": io_bytes,
+                "d2h_bytes_per_step": io_bytes, "steps": e2e_steps,
+                "what": "load_population + run_generation + read_population via the C-ABI, host buffers"},
+        "roofline": roofline,
+        "cpu_baseline": cpu_baseline,
+        "clocks": clk,
+        "gpu_launches": int(launches),
+        "evaluator_calls_per_s": calls / dev_s,
+        "wall_s_timed_region": t_wall,
+        "elitist_fitness": E.elitist_fitness,
+    })
+    print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        bench_reference(args)
+    else:
+        bench_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -177,6 +177,18 @@ GOMIX_API int gomix_gpu_init_population(gomix_gpu_engine* e, const uint8_t* geno
 GOMIX_API int gomix_gpu_run_generation(gomix_gpu_engine* e, const gomix_stop_criteria* stop,
                              gomix_run_stats* out);
 
+/* Philox mode, no stop criteria: enqueue one generation on the engine's
+ * stream and return without synchronising (for back-to-back generations and
+ * CUDA-event timing).  gomix_gpu_synchronize waits and returns the stats of
+ * the last queued generation. */
+GOMIX_API int gomix_gpu_run_generation_async(gomix_gpu_engine* e);
+GOMIX_API int gomix_gpu_synchronize(gomix_gpu_engine* e, gomix_run_stats* out);
+
+/* Replace the population with n x num_vertices genotype bytes and their
+ * fitness (NULL = evaluate on the device); the elitist is kept. */
+GOMIX_API int gomix_gpu_load_population(gomix_gpu_engine* e, const uint8_t* genotypes,
+                                        const double* fitness);
+
 /* One batched GOM step over colour group `group` (phases 1-4 of
  * engine_parallel.hpp:104-247 plus the elitist scan :305-310) with the donors
  * given as a GroupBatch::donor array (s*|G| + p order, -1 = no donor).

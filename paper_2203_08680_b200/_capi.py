@@ -82,6 +82,9 @@ _SIGNATURES = {
     "gomix_gpu_set_stream": ([_P, _P], C.c_int),
     "gomix_gpu_init_population": ([_P, _P, C.POINTER(StopCriteria), C.POINTER(RunStats)], C.c_int),
     "gomix_gpu_run_generation": ([_P, C.POINTER(StopCriteria), C.POINTER(RunStats)], C.c_int),
+    "gomix_gpu_run_generation_async": ([_P], C.c_int),
+    "gomix_gpu_synchronize": ([_P, C.POINTER(RunStats)], C.c_int),
+    "gomix_gpu_load_population": ([_P, _P, _P], C.c_int),
     "gomix_gpu_run_group": ([_P, C.c_uint64, _P, C.POINTER(StopCriteria), C.POINTER(RunStats)], C.c_int),
     "gomix_gpu_read_batch": ([_P, _P, _P, _P, _P], C.c_int),
     "gomix_gpu_read_population": ([_P, _P, _P], C.c_int),

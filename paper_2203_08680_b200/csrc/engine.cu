@@ -47,9 +47,6 @@ int guarded(F&& f) {
   }
 }
 
-// Region of DevCtl written by the host at the start of every call.
-constexpr size_t kCallOffset = offsetof(DevCtl, stop);
-
 uint32_t next_pow2(uint32_t x) {
   uint32_t p = 1;
   while (p < x) p <<= 1;
@@ -192,6 +189,7 @@ std::unique_ptr<Problem> create_problem(const gomix_maxcut* inst, const gomix_fo
   std::vector<int64_t> so(P->h_set_off.begin(), P->h_set_off.end());
   up(P->set_off, so.data(), (m + 1) * 8);
   up(P->set_vars, P->h_set_vars.data(), entries * 4);
+  up(d_eid, eid.data(), 2 * q * 4);
   build_problem_device_impl(*P, colour, d_eid);
   if (P->univariate) {
     for (uint64_t i = 0; i < m; ++i) {
@@ -360,21 +358,17 @@ struct gomix_gpu_engine {
 
   // ---- per-call control ------------------------------------------------------
   void begin_call(const gomix_stop_criteria* stop) {
-    h_ctl->stop = 0;
-    h_ctl->stop_reason = GOMIX_STOP_NONE;
-    h_ctl->has_budget = stop && stop->has_max_evaluations;
-    h_ctl->has_target = stop && stop->has_target;
-    h_ctl->exact = P->exact;
-    h_ctl->max_evals = stop ? stop->max_evaluations : 0.0;
-    h_ctl->q = (double)P->q;
-    h_ctl->target = stop ? stop->target_fitness : 0.0;
-    h_ctl->calls_total = stop ? stop->evaluator_calls_before : 0;
-    h_ctl->grp_steps = h_ctl->grp_calls = 0;
-    h_ctl->run_steps = h_ctl->run_calls = h_ctl->groups_run = 0;
-    h_ctl->n_impr = 0;
-    GOMIX_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(ctl) + kCallOffset,
-                               reinterpret_cast<char*>(h_ctl) + kCallOffset,
-                               sizeof(DevCtl) - kCallOffset, cudaMemcpyHostToDevice, stream));
+    BeginArgs b;
+    b.ctl = ctl;
+    b.has_budget = stop && stop->has_max_evaluations;
+    b.has_target = stop && stop->has_target;
+    b.exact = P->exact;
+    b.max_evals = stop ? stop->max_evaluations : 0.0;
+    b.q = (double)P->q;
+    b.target = stop ? stop->target_fitness : 0.0;
+    b.calls_before = stop ? stop->evaluator_calls_before : 0;
+    launch_begin(b, stream);
+    ++launches;
   }
 
   void read_ctl() {
@@ -406,11 +400,13 @@ struct gomix_gpu_engine {
     const uint64_t warps = 148ull * 64;
     const uint64_t per = std::max<uint64_t>(1, warps / Wp);
     r.rows_per_chunk = (uint32_t)std::max<uint64_t>(64, (P->nv + per - 1) / per);
+    r.force_src = kNoForce;
     return r;
   }
 
-  void refresh() {
-    const RefreshArgs r = refresh_args();
+  void refresh(int32_t force_src = kNoForce) {
+    RefreshArgs r = refresh_args();
+    r.force_src = force_src;
     launch_refresh(r, 148 * 8, stream);
     ++launches;
   }
@@ -605,6 +601,51 @@ struct gomix_gpu_engine {
     if (!h_ctl->stop) ++generation;  // engine_parallel.hpp:311-314
   }
 
+  void set_elitist_fitness(double f) {
+    GOMIX_CUDA(cudaStreamSynchronize(stream));  // h_ctl is reused as the staging buffer
+    h_ctl->elit_fit = f;
+    GOMIX_CUDA(cudaMemcpyAsync(ctl, h_ctl, sizeof(double), cudaMemcpyHostToDevice, stream));
+  }
+
+  // Enqueue one generation without any host synchronisation (Philox mode,
+  // no stop criteria); results are read by synchronize().
+  void run_generation_async() {
+    if (!initialized) throw GomixError(GOMIX_E_STATE, "run_generation: population not initialised");
+    if (mode != GOMIX_MODE_PHILOX) invalid("run_generation_async: needs GOMIX_MODE_PHILOX");
+    begin_call(nullptr);
+    std::vector<uint64_t> order;
+    rng.permutation(order, P->k);
+    for (uint64_t gi : order) launch_group(gi, false);
+    ++generation;
+  }
+
+  void synchronize(gomix_run_stats* out) {
+    read_ctl();
+    fill_stats(out);
+  }
+
+  // Replace the population (n x nv bytes, row per solution) and its fitness
+  // (NULL = evaluate on the device); the elitist is kept.
+  void load_population(const uint8_t* genotypes, const double* fitness) {
+    if (!initialized) throw GomixError(GOMIX_E_STATE, "load_population: population not initialised");
+    const uint64_t nv = P->nv;
+    uint8_t* d = nullptr;
+    GOMIX_CUDA(cudaMallocAsync(&d, n * nv, stream));
+    GOMIX_CUDA(cudaMemcpyAsync(d, genotypes, n * nv, cudaMemcpyHostToDevice, stream));
+    launch_pack(d, pop, nv, (uint32_t)n, Wp, stream);
+    GOMIX_CUDA(cudaFreeAsync(d, stream));
+    ++launches;
+    if (fitness) {
+      GOMIX_CUDA(cudaMemcpyAsync(fit, fitness, n * 8, cudaMemcpyHostToDevice, stream));
+    } else {
+      launch_full_eval(*P, pop, fit, (uint32_t)n, Wp, !P->exact, stream);
+      ++launches;
+    }
+    GOMIX_CUDA(cudaMemsetAsync(ham, 0, n * 4, stream));
+    refresh(-2);  // distances to the current elitist bits
+    GOMIX_CUDA(cudaStreamSynchronize(stream));
+  }
+
   void run_group(uint64_t group, const int32_t* donor_tape, const gomix_stop_criteria* stop,
                  gomix_run_stats* out) {
     if (!initialized) throw GomixError(GOMIX_E_STATE, "run_group: population not initialised");
@@ -725,6 +766,29 @@ int gomix_gpu_run_generation(gomix_gpu_engine* e, const gomix_stop_criteria* sto
   });
 }
 
+int gomix_gpu_run_generation_async(gomix_gpu_engine* e) {
+  return guarded([&] {
+    if (!e) invalid("run_generation_async: NULL engine");
+    e->run_generation_async();
+  });
+}
+
+int gomix_gpu_synchronize(gomix_gpu_engine* e, gomix_run_stats* out) {
+  return guarded([&] {
+    if (!e) invalid("synchronize: NULL engine");
+    e->synchronize(out);
+  });
+}
+
+int gomix_gpu_load_population(gomix_gpu_engine* e, const uint8_t* genotypes, const double* fitness) {
+  return guarded([&] {
+    if (!e || !genotypes) invalid("load_population: NULL argument");
+    for (uint64_t i = 0; i < e->n * e->P->nv; ++i)
+      if (genotypes[i] > 1) invalid("graybox: genotype value outside alphabet");
+    e->load_population(genotypes, fitness);
+  });
+}
+
 int gomix_gpu_run_group(gomix_gpu_engine* e, uint64_t group, const int32_t* donor_tape,
                         const gomix_stop_criteria* stop, gomix_run_stats* out) {
   return guarded([&] {
@@ -820,13 +884,9 @@ int gomix_gpu_offer_elitist(gomix_gpu_engine* e, const uint8_t* genotype, double
     GOMIX_CUDA(cudaMemcpyAsync(d, genotype, nv, cudaMemcpyHostToDevice, e->stream));
     launch_pack_elitist(d, e->elit, nv, e->stream);
     GOMIX_CUDA(cudaFreeAsync(d, e->stream));
-    e->h_ctl->elit_fit = fitness;
-    e->h_ctl->elit_src = -2;
-    GOMIX_CUDA(cudaMemcpyAsync(e->ctl, e->h_ctl, offsetof(DevCtl, stop), cudaMemcpyHostToDevice,
-                               e->stream));
+    e->set_elitist_fitness(fitness);
     GOMIX_CUDA(cudaMemsetAsync(e->ham, 0, e->n * 4, e->stream));
-    e->refresh();
-    ++e->launches;
+    e->refresh(-2);
     GOMIX_CUDA(cudaStreamSynchronize(e->stream));
     e->elit_fit = fitness;
   });

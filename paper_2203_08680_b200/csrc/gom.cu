@@ -561,6 +561,22 @@ __global__ void __launch_bounds__(kEpilogueThreads) epilogue_kernel(const EpiArg
     for (uint32_t s = threadIdx.x; s < n; s += blockDim.x) a.ham[s] = 0;  // refresh recounts
 }
 
+__global__ void begin_call_kernel(const BeginArgs b) {
+  DevCtl* c = b.ctl;
+  c->stop = 0;
+  c->stop_reason = GOMIX_STOP_NONE;
+  c->has_budget = b.has_budget;
+  c->has_target = b.has_target;
+  c->exact = b.exact;
+  c->max_evals = b.max_evals;
+  c->q = b.q;
+  c->target = b.target;
+  c->calls_total = b.calls_before;
+  c->grp_steps = c->grp_calls = 0;
+  c->run_steps = c->run_calls = c->groups_run = 0;
+  c->n_impr = 0;
+}
+
 // After init_population (engine_parallel.hpp:331-346): one add_evaluator_calls(q)
 // per solution and "i == 0 || better" elitist updates, interleaved in order.
 __global__ void init_epilogue_kernel(const EpiArgs a) {
@@ -599,7 +615,7 @@ __global__ void init_epilogue_kernel(const EpiArgs a) {
 // i.e. distance 0, which the GOM kernel then maintains incrementally.
 // ---------------------------------------------------------------------------
 __global__ void refresh_kernel(const RefreshArgs a) {
-  const int32_t src = *(volatile const int32_t*)&a.ctl->elit_src;
+  const int32_t src = a.force_src != kNoForce ? a.force_src : *(volatile const int32_t*)&a.ctl->elit_src;
   if (src == -1) return;
   const uint32_t Wp = a.Wp;
   const uint64_t gtid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -777,6 +793,11 @@ int gom_max_blocks_per_sm(bool univariate, bool i32, int wpt, int block, size_t 
 
 void launch_epilogue(const EpiArgs& a, cudaStream_t s) {
   epilogue_kernel<<<1, kEpilogueThreads, 0, s>>>(a);
+  GOMIX_CUDA(cudaGetLastError());
+}
+
+void launch_begin(const BeginArgs& b, cudaStream_t s) {
+  begin_call_kernel<<<1, 1, 0, s>>>(b);
   GOMIX_CUDA(cudaGetLastError());
 }
 

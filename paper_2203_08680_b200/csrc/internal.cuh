@@ -136,6 +136,18 @@ struct RefreshArgs {
   const DevCtl* ctl;
   uint64_t nv;
   uint32_t n, Wp, rows_per_chunk;
+  int32_t force_src;  // kNoForce: use ctl->elit_src
+};
+
+constexpr int32_t kNoForce = -1000;
+
+// Per-call control values, passed as kernel parameters (captured at launch,
+// so host calls can be queued back to back without host syncs).
+struct BeginArgs {
+  DevCtl* ctl;
+  int32_t has_budget, has_target, exact;
+  double max_evals, q, target;
+  unsigned long long calls_before;
 };
 
 // -------------------------------------------------------------------------
@@ -204,6 +216,7 @@ void launch_gom(const GomArgs& a, bool univariate, bool i32, int wpt, int grid, 
                 size_t smem, cudaStream_t s);
 int gom_max_blocks_per_sm(bool univariate, bool i32, int wpt, int block, size_t smem);
 void launch_epilogue(const EpiArgs& a, cudaStream_t s);
+void launch_begin(const BeginArgs& b, cudaStream_t s);
 void launch_init_epilogue(const EpiArgs& a, cudaStream_t s);
 void launch_refresh(const RefreshArgs& a, int grid, cudaStream_t s);
 void launch_philox_init(uint32_t* pop, uint64_t nv, uint32_t n, uint32_t Wp, uint64_t seed,

@@ -299,6 +299,24 @@ class GpuParallelEngine:
         if not stats.stopped:
             self.ctx.report_boundary(self._elitist_fitness, self.generation(), self.pop_id)
 
+    def run_generation_async(self):
+        """Queue one generation without a host sync (Philox mode, no stop
+        criteria); the run-wide bookkeeping is not updated."""
+        check(lib().gomix_gpu_run_generation_async(self.h))
+
+    def synchronize(self) -> _capi.RunStats:
+        stats = _capi.RunStats()
+        check(lib().gomix_gpu_synchronize(self.h, C.byref(stats)))
+        self._elitist_fitness = float(stats.elitist_fitness)
+        return stats
+
+    def load_population(self, genotypes: np.ndarray, fitness: Optional[np.ndarray] = None):
+        g = np.ascontiguousarray(genotypes, np.uint8)
+        if g.shape != (self.n, self.problem.info.num_vertices):
+            raise ValueError("graybox: genotype shape mismatch")
+        f = None if fitness is None else np.ascontiguousarray(fitness, np.float64)
+        check(lib().gomix_gpu_load_population(self.h, g.ctypes.data, _capi.ptr(f)))
+
     def generation(self) -> int:
         g = C.c_int64()
         check(lib().gomix_gpu_generation(self.h, C.byref(g)))
