@@ -211,9 +211,13 @@ GOMIX_API int gomix_gpu_read_elitist(gomix_gpu_engine* e, uint8_t* genotype, dou
 /* offer_elitist (engine_parallel.hpp:320-322): adopt iff strictly better. */
 GOMIX_API int gomix_gpu_offer_elitist(gomix_gpu_engine* e, const uint8_t* genotype, double fitness,
                             int32_t* adopted);
-/* Elitist improvements of the last init/run call (values in report order). */
-GOMIX_API int gomix_gpu_read_improvements(gomix_gpu_engine* e, double* fitness, uint64_t capacity,
-                                uint64_t* count);
+/* Elitist improvements of the last init/run call, in report order: fitness
+ * and the run-wide evaluator-call count at the moment of the report (what the
+ * reference's TraceSink row records, runtime.hpp:136-143).  Either array may
+ * be NULL; with both NULL, count = number available. */
+GOMIX_API int gomix_gpu_read_improvements(gomix_gpu_engine* e, double* fitness,
+                                          uint64_t* evaluator_calls, uint64_t capacity,
+                                          uint64_t* count);
 /* group_counters() (engine_parallel.hpp:326-328). */
 GOMIX_API int gomix_gpu_group_counters(gomix_gpu_engine* e, uint64_t* sets, uint64_t* steps,
                              uint64_t* evaluator_calls);

@@ -91,7 +91,7 @@ _SIGNATURES = {
     "gomix_gpu_read_population_packed": ([_P, _P, C.POINTER(C.c_uint64)], C.c_int),
     "gomix_gpu_read_elitist": ([_P, _P, C.POINTER(C.c_double)], C.c_int),
     "gomix_gpu_offer_elitist": ([_P, _P, C.c_double, C.POINTER(C.c_int32)], C.c_int),
-    "gomix_gpu_read_improvements": ([_P, _P, C.c_uint64, C.POINTER(C.c_uint64)], C.c_int),
+    "gomix_gpu_read_improvements": ([_P, _P, _P, C.c_uint64, C.POINTER(C.c_uint64)], C.c_int),
     "gomix_gpu_group_counters": ([_P, _P, _P, _P], C.c_int),
     "gomix_gpu_generation": ([_P, C.POINTER(C.c_int64)], C.c_int),
     "gomix_gpu_kernel_times": ([_P, _P, C.c_uint64, C.POINTER(C.c_uint64)], C.c_int),

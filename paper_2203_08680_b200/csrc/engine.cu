@@ -211,6 +211,7 @@ struct gomix_gpu_engine {
   uint32_t W = 0, Wp = 0, wpt = 1, tw = 1, block = 256, teams = 8, stage_words = 0;
   size_t smem = 0;
   int grid_cap = 1;
+  int sms = 148;
   uint32_t mode = GOMIX_MODE_PHILOX, flags = 0;
   int32_t pop_id = 1;
   int epi_mode = 0;  // 0 exact atomics, 1 float partials, 2 ordered
@@ -230,6 +231,7 @@ struct gomix_gpu_engine {
   unsigned long long* gsteps = nullptr;
   unsigned long long* gcalls = nullptr;
   double* impr = nullptr;
+  unsigned long long* impr_calls = nullptr;
   uint64_t impr_cap = 0;
   int32_t* tape = nullptr;
   int32_t* h_tape_pinned = nullptr;
@@ -314,7 +316,6 @@ struct gomix_gpu_engine {
     GOMIX_CUDA(cudaSetDevice(P->device));
     GOMIX_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     own_stream = true;
-    int sms = 0;
     GOMIX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, P->device));
     const int per_sm = gom_max_blocks_per_sm(P->univariate, P->i32, (int)wpt, (int)block, smem);
     if (per_sm < 1) invalid("engine: GOM kernel does not fit on an SM with this configuration");
@@ -334,6 +335,7 @@ struct gomix_gpu_engine {
     gcalls = dev_alloc<unsigned long long>(allocs, P->k);
     impr_cap = std::min<uint64_t>(std::max<uint64_t>(4096, n * (P->k + 1)), 1ull << 22);
     impr = dev_alloc<double>(allocs, impr_cap);
+    impr_calls = dev_alloc<unsigned long long>(allocs, impr_cap);
     if (epi_mode == 1) part = dev_alloc<double>(allocs, (size_t)grid_cap * n);
     tape = dev_alloc<int32_t>(allocs, max_group * n);
     if (record || epi_mode == 2) {
@@ -397,9 +399,6 @@ struct gomix_gpu_engine {
     r.nv = P->nv;
     r.n = (uint32_t)n;
     r.Wp = Wp;
-    const uint64_t warps = 148ull * 64;
-    const uint64_t per = std::max<uint64_t>(1, warps / Wp);
-    r.rows_per_chunk = (uint32_t)std::max<uint64_t>(64, (P->nv + per - 1) / per);
     r.force_src = kNoForce;
     return r;
   }
@@ -407,9 +406,14 @@ struct gomix_gpu_engine {
   void refresh(int32_t force_src = kNoForce) {
     RefreshArgs r = refresh_args();
     r.force_src = force_src;
-    launch_refresh(r, 148 * 8, stream);
+    const uint64_t units = ((P->nv + 31) / 32) * Wp;
+    const int grid = (int)std::min<uint64_t>(std::max<uint64_t>(1, (units + 7) / 8), (uint64_t)sms * 8);
+    launch_refresh(r, grid, stream);
     ++launches;
   }
+
+  // the last CTA of the GOM kernel refreshes small populations itself
+  bool fuse_refresh() const { return P->nv * Wp <= (1u << 18); }
 
   EpiArgs epi_args(uint64_t group, uint32_t G, uint32_t nparts) const {
     EpiArgs e;
@@ -424,6 +428,7 @@ struct gomix_gpu_engine {
     e.gsteps = gsteps;
     e.gcalls = gcalls;
     e.impr = impr;
+    e.impr_calls = impr_calls;
     e.impr_cap = impr_cap;
     e.n = (uint32_t)n;
     e.G = G;
@@ -446,6 +451,7 @@ struct gomix_gpu_engine {
     a.fp_off = P->fp_off;
     a.fp = P->fp;
     a.gsets = P->gsets + g0;
+    a.gvars = P->gvars ? P->gvars + g0 : nullptr;
     a.G = (uint32_t)G;
     a.pop = pop;
     a.fit = fit;
@@ -476,14 +482,16 @@ struct gomix_gpu_engine {
       e1 = take_event();
       GOMIX_CUDA(cudaEventRecord(e0, stream));
     }
+    a.epi = epi_args(group, (uint32_t)G, (uint32_t)grid);
+    a.ref = refresh_args();
+    a.fuse_refresh = fuse_refresh();
     launch_gom(a, P->univariate, P->i32, (int)wpt, grid, (int)block, smem, stream);
+    ++launches;
     if (e1) {
       GOMIX_CUDA(cudaEventRecord(e1, stream));
       ev_pending.push_back({e0, e1});
     }
-    launch_epilogue(epi_args(group, (uint32_t)G, (uint32_t)grid), stream);
-    launches += 2;
-    refresh();
+    if (!a.fuse_refresh) refresh();
     last_group = (int64_t)group;
   }
 
@@ -892,17 +900,22 @@ int gomix_gpu_offer_elitist(gomix_gpu_engine* e, const uint8_t* genotype, double
   });
 }
 
-int gomix_gpu_read_improvements(gomix_gpu_engine* e, double* fitness, uint64_t capacity,
-                                uint64_t* count) {
+int gomix_gpu_read_improvements(gomix_gpu_engine* e, double* fitness, uint64_t* evaluator_calls,
+                                uint64_t capacity, uint64_t* count) {
   return guarded([&] {
     if (!e) invalid("read_improvements: NULL engine");
     const uint64_t avail = std::min<uint64_t>(e->h_ctl->n_impr, e->impr_cap);
-    const uint64_t take = fitness ? std::min(avail, capacity) : 0;
+    const bool any = fitness || evaluator_calls;
+    const uint64_t take = any ? std::min(avail, capacity) : 0;
     if (take) {
-      GOMIX_CUDA(cudaMemcpyAsync(fitness, e->impr, take * 8, cudaMemcpyDeviceToHost, e->stream));
+      if (fitness)
+        GOMIX_CUDA(cudaMemcpyAsync(fitness, e->impr, take * 8, cudaMemcpyDeviceToHost, e->stream));
+      if (evaluator_calls)
+        GOMIX_CUDA(cudaMemcpyAsync(evaluator_calls, e->impr_calls, take * 8, cudaMemcpyDeviceToHost,
+                                   e->stream));
       GOMIX_CUDA(cudaStreamSynchronize(e->stream));
     }
-    if (count) *count = fitness ? take : avail;
+    if (count) *count = any ? take : avail;
   });
 }
 
@@ -930,18 +943,22 @@ int gomix_gpu_generation(gomix_gpu_engine* e, int64_t* generation) {
 int gomix_gpu_kernel_times(gomix_gpu_engine* e, float* ms, uint64_t capacity, uint64_t* count) {
   return guarded([&] {
     if (!e) invalid("kernel_times: NULL engine");
+    if (!ms) {  // query only
+      if (count) *count = e->ev_pending.size();
+      return;
+    }
     GOMIX_CUDA(cudaStreamSynchronize(e->stream));
     uint64_t written = 0;
     for (auto& pr : e->ev_pending) {
       float t = 0.f;
       GOMIX_CUDA(cudaEventElapsedTime(&t, pr.first, pr.second));
-      if (ms && written < capacity) ms[written] = t;
+      if (written < capacity) ms[written] = t;
       ++written;
       e->ev_free.push_back(pr.first);
       e->ev_free.push_back(pr.second);
     }
     e->ev_pending.clear();
-    if (count) *count = ms ? std::min(written, capacity) : written;
+    if (count) *count = std::min(written, capacity);
   });
 }
 

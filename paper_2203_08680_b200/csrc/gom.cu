@@ -71,19 +71,182 @@ __device__ __forceinline__ void team_sync(uint32_t team_warps) {
 }
 
 // ---------------------------------------------------------------------------
+// epilogue (run by the last CTA of the GOM kernel to finish): commit the
+// group's fitness deltas, account the evaluator calls (budget stop first,
+// runtime.hpp:75-80), then the elitist scan of engine_parallel.hpp:305-310 —
+// the first member strictly better than the running elitist replaces it and
+// the scan continues against the new value — logging every improvement with
+// the call count at that moment and latching the target stop
+// (runtime.hpp:88-93,136-143).
+// ---------------------------------------------------------------------------
+__device__ void request_stop(DevCtl* c, int reason) {
+  if (!c->stop) {
+    c->stop = 1;
+    c->stop_reason = reason;
+  }
+}
+
+__device__ void note_improvement(const EpiArgs& a, double f) {
+  DevCtl* c = a.ctl;
+  const unsigned long long i = c->n_impr++;
+  if (i < a.impr_cap) {
+    a.impr[i] = f;
+    a.impr_calls[i] = c->calls_total;
+  }
+  if (c->has_target && (cmp_better(c->exact, f, c->target) || cmp_equal(c->exact, f, c->target)))
+    request_stop(c, GOMIX_STOP_TARGET);
+}
+
+__device__ void epilogue_body(const EpiArgs& a) {
+  DevCtl* c = a.ctl;
+  const uint32_t n = a.n;
+  __shared__ double s_chunkmax[32];
+  __shared__ int32_t s_best;
+  for (uint32_t s = threadIdx.x; s < n; s += blockDim.x) {
+    double f = a.fit[s];
+    if (a.mode == 2) {
+      for (uint32_t p = 0; p < a.G; ++p)
+        if (a.rec_accept[(size_t)p * n + s]) f += a.rec_delta[(size_t)p * n + s];
+    } else if (a.mode == 1) {
+      double sum = 0.0;
+      for (uint32_t b = 0; b < a.nparts; ++b) sum += a.part[(size_t)b * n + s];
+      f += sum;
+    } else {
+      f += a.dfit[s];
+      a.dfit[s] = 0.0;
+    }
+    a.fit[s] = f;
+    a.ham[s] += a.dham[s];
+    a.dham[s] = 0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long st = c->grp_steps, ca = c->grp_calls;
+    c->grp_steps = 0;
+    c->grp_calls = 0;
+    c->calls_total += ca;
+    c->run_steps += st;
+    c->run_calls += ca;
+    c->groups_run += 1;
+    a.gsteps[a.group] += st;
+    a.gcalls[a.group] += ca;
+    if (c->has_budget && (double)c->calls_total / c->q >= c->max_evals)
+      request_stop(c, GOMIX_STOP_BUDGET);
+    s_best = -1;
+  }
+  // chunk maxima let the serial scan skip chunks that cannot hold a record
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u, nwarps = blockDim.x >> 5;
+  for (uint32_t chunk = warp; chunk * 32u < n; chunk += nwarps) {
+    const uint32_t s = chunk * 32u + lane;
+    double f = s < n ? a.fit[s] : -INFINITY;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) f = fmax(f, __shfl_xor_sync(0xFFFFFFFFu, f, o));
+    if (lane == 0 && chunk < 32) s_chunkmax[chunk] = f;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const bool exact = c->exact != 0;
+    double cur = c->elit_fit;
+    int32_t best = -1;
+    for (uint32_t base = 0; base < n; base += 32u) {
+      const uint32_t chunk = base >> 5;
+      if (chunk < 32 && !(s_chunkmax[chunk] > cur)) continue;  // better() implies >
+      const uint32_t s = base + lane;
+      const double f = s < n ? a.fit[s] : -INFINITY;
+      uint32_t m = __ballot_sync(0xFFFFFFFFu, s < n && cmp_better(exact, f, cur));
+      while (m) {
+        const uint32_t l = __ffs(m) - 1;
+        cur = __shfl_sync(0xFFFFFFFFu, f, l);
+        best = (int32_t)(base + l);
+        if (lane == 0) note_improvement(a, cur);
+        m = __ballot_sync(0xFFFFFFFFu, s < n && lane > l && cmp_better(exact, f, cur));
+      }
+    }
+    if (lane == 0) {
+      c->elit_src = best;
+      if (best >= 0) c->elit_fit = cur;
+      s_best = best;
+    }
+  }
+  __syncthreads();
+  if (s_best >= 0)
+    for (uint32_t s = threadIdx.x; s < n; s += blockDim.x) a.ham[s] = 0;  // refresh recounts
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// refresh: when the elitist changed, copy its genotype out of the population
+// column and recount every member's Hamming distance to it.  The batched
+// accept rule only needs "parent == elitist" at group start
+// (engine_parallel.hpp:202), i.e. distance 0; the GOM kernel maintains the
+// distances incrementally between refreshes.  Lanes load 32 consecutive rows
+// of one word column; 32 ballots transpose the 32x32 bit block so lane k
+// counts solution 32w+k.
+// ---------------------------------------------------------------------------
+__device__ void refresh_body(const RefreshArgs& a, uint64_t gwarp, uint64_t nwarps) {
+  const int32_t src = a.force_src != kNoForce ? a.force_src : *(volatile const int32_t*)&a.ctl->elit_src;
+  if (src == -1) return;
+  const uint32_t lane = threadIdx.x & 31u, Wp = a.Wp;
+  const uint32_t sw = src >= 0 ? (uint32_t)src >> 5 : 0u, sb = src >= 0 ? (uint32_t)src & 31u : 0u;
+  const uint64_t blocks = (a.nv + 31) / 32;
+  int32_t cnt = 0;
+  uint32_t cur_w = 0xFFFFFFFFu;
+  for (uint64_t unit = gwarp; unit < blocks * Wp; unit += nwarps) {
+    const uint32_t w = (uint32_t)(unit % Wp);
+    if (w != cur_w) {
+      if (cur_w != 0xFFFFFFFFu && cur_w * 32u + lane < a.n && cnt) atomicAdd(&a.ham[cur_w * 32u + lane], cnt);
+      cnt = 0;
+      cur_w = w;
+    }
+    const uint64_t v = (unit / Wp) * 32u + lane;
+    const bool has = v < a.nv;
+    const uint32_t x = has ? a.pop[v * Wp + w] : 0u;
+    const uint32_t eb = !has ? 0u
+                        : src >= 0 ? (a.pop[v * Wp + sw] >> sb) & 1u
+                                   : (a.elit[v >> 5] >> (v & 31u)) & 1u;
+    if (src >= 0 && w == 0) {
+      const uint32_t word = __ballot_sync(0xFFFFFFFFu, eb);
+      if (lane == 0) a.elit[v >> 5] = word;
+    }
+    if (w * 32u >= a.n) continue;
+    const uint32_t diff = has ? (x ^ (eb ? 0xFFFFFFFFu : 0u)) : 0u;
+#pragma unroll
+    for (uint32_t k = 0; k < 32; ++k) {
+      const uint32_t c = __popc(__ballot_sync(0xFFFFFFFFu, (diff >> k) & 1u));
+      if (lane == k) cnt += (int32_t)c;
+    }
+  }
+  if (cur_w != 0xFFFFFFFFu && cur_w * 32u + lane < a.n && cnt) atomicAdd(&a.ham[cur_w * 32u + lane], cnt);
+}
+
+__global__ void refresh_kernel(const RefreshArgs a) {
+  const uint64_t gtid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  refresh_body(a, gtid >> 5, ((uint64_t)gridDim.x * blockDim.x) >> 5);
+}
+
+__device__ __forceinline__ double shfl_d(double x, int src) {
+  return __shfl_sync(0xFFFFFFFFu, x, src);
+}
+
+// ---------------------------------------------------------------------------
 // gom_group_kernel
 //
 // Work decomposition: a *team* (one warp, or the whole CTA when n > 256)
 // owns one linkage set at a time; inside the team, lane b of the warp that
 // holds word w is solution 32w+b, and each thread carries WPT words.  Teams
-// stride over the group's sets (persistent grid, sized to the SM count), so
+// stride over the group's sets (persistent grid sized to the SM count), so
 // per-solution fitness / elitist-distance deltas accumulate in registers and
 // reach HBM once per CTA.  Same-colour sets share no variable and no
 // interaction edge (scheduling.hpp:22-27), so teams update their rows in place
-// without races and without a shadow copy.
+// without races and without a shadow copy.  A set's footprint (its CSR row,
+// or its FpEntry list) and the neighbour rows it needs are fetched by the
+// lanes in parallel — one coalesced round of loads per 32 entries — then
+// broadcast with shuffles, so the sums below run without dependent loads.
+// The last CTA to finish runs the epilogue (and, for small populations, the
+// elitist refresh), so a group is one launch.
 // ---------------------------------------------------------------------------
 template <int WPT, bool UNIV, bool I32>
-__global__ void __launch_bounds__(512) gom_group_kernel(const GomArgs a) {
+__global__ void __launch_bounds__(512, 1) gom_group_kernel(const GomArgs a) {
   extern __shared__ __align__(16) uint32_t smem[];
   if (*(volatile int32_t*)&a.ctl->stop) return;
 
@@ -111,16 +274,17 @@ __global__ void __launch_bounds__(512) gom_group_kernel(const GomArgs a) {
   unsigned long long calls = 0;
 
   for (uint32_t p = blockIdx.x * teams_per_cta + team; p < a.G; p += gridDim.x * teams_per_cta) {
-    const uint32_t sid = a.gsets[p];
     if constexpr (UNIV) {
-      // ---- univariate set {v}: the donor's value on v is forced to !x_v, so
-      // the pair is present iff some member holds the other value; the draw
-      // itself cannot change the outcome and is skipped in Philox mode.
-      const uint32_t v = a.set_vars[a.set_off[sid]];
+      // ---- univariate set {v}: a donor differing on v holds !x_v, so the
+      // pair is present iff some member holds the other value and the move
+      // is the flip of v; in Philox mode the draw cannot change the outcome
+      // and is skipped.
+      const uint32_t v = a.gvars[p];
       const uint32_t* row = a.pop + (size_t)v * Wp;
       uint32_t pw[WPT];
 #pragma unroll
       for (int j = 0; j < WPT; ++j) pw[j] = row[wit + tw * j];
+      const int32_t rs = a.row_ptr[v], re = a.row_ptr[v + 1];
       uint32_t ones = 0;
       if (!replay) {
         if (tw == 1) {
@@ -132,7 +296,6 @@ __global__ void __launch_bounds__(512) gom_group_kernel(const GomArgs a) {
         }
       }
       const uint32_t eb = (a.elit[v >> 5] >> (v & 31u)) & 1u;
-      const int32_t rs = a.row_ptr[v], re = a.row_ptr[v + 1];
       const uint32_t deg = (uint32_t)(re - rs);
       int32_t di[WPT];
       double sn[WPT], so[WPT];
@@ -142,23 +305,34 @@ __global__ void __launch_bounds__(512) gom_group_kernel(const GomArgs a) {
         sn[j] = 0.0;
         so[j] = 0.0;
       }
-      for (int32_t e = rs; e < re; ++e) {
-        const uint32_t u = (uint32_t)a.col[e];
-        const uint32_t* urow = a.pop + (size_t)u * Wp;
-        if constexpr (I32) {
-          const int32_t wt = a.wi[e];
+      for (int32_t base = rs; base < re; base += 32) {
+        const int32_t e = base + (int32_t)lane;
+        const bool has = e < re;
+        const uint32_t u = has ? (uint32_t)a.col[e] : v;
+        int32_t wti = 0;
+        double wtd = 0.0;
+        if constexpr (I32) wti = has ? a.wi[e] : 0;
+        else wtd = has ? a.w[e] : 0.0;
+        uint32_t nb[WPT];
 #pragma unroll
-          for (int j = 0; j < WPT; ++j) {
-            const uint32_t cut_old = ((pw[j] ^ urow[wit + tw * j]) >> lane) & 1u;
-            di[j] += cut_old ? -wt : wt;
-          }
-        } else {
-          const double wt = a.w[e];
+        for (int j = 0; j < WPT; ++j) nb[j] = a.pop[(size_t)u * Wp + wit + tw * j];
+        const int cnt = min(32, re - base);
+        for (int t = 0; t < cnt; ++t) {
+          if constexpr (I32) {
+            const int32_t wt = __shfl_sync(0xFFFFFFFFu, wti, t);
 #pragma unroll
-          for (int j = 0; j < WPT; ++j) {
-            const uint32_t cut_old = ((pw[j] ^ urow[wit + tw * j]) >> lane) & 1u;
-            sn[j] += cut_old ? 0.0 : wt;  // reference adds every value, 0.0 included
-            so[j] += cut_old ? wt : 0.0;
+            for (int j = 0; j < WPT; ++j) {
+              const uint32_t x = __shfl_sync(0xFFFFFFFFu, nb[j], t);
+              di[j] += (((pw[j] ^ x) >> lane) & 1u) ? -wt : wt;
+            }
+          } else {
+            const double wt = shfl_d(wtd, t);
+#pragma unroll
+            for (int j = 0; j < WPT; ++j) {
+              const uint32_t cut_old = (((pw[j] ^ __shfl_sync(0xFFFFFFFFu, nb[j], t)) >> lane) & 1u);
+              sn[j] += cut_old ? 0.0 : wt;  // reference adds every value, 0.0 included
+              so[j] += cut_old ? wt : 0.0;
+            }
           }
         }
       }
@@ -189,8 +363,7 @@ __global__ void __launch_bounds__(512) gom_group_kernel(const GomArgs a) {
             accept = cmp_better(false, cand, pf) || (cmp_equal(false, cand, pf) && !elit);
           }
         }
-        const uint32_t nb = accept ? (pv ^ 1u) : pv;
-        const uint32_t nw = __ballot_sync(0xFFFFFFFFu, nb);
+        const uint32_t nw = __ballot_sync(0xFFFFFFFFu, accept ? (pv ^ 1u) : pv);
         if (lane == 0 && nw != pw[j]) a.pop[(size_t)v * Wp + w] = nw;
         if (accept) {
           acc[j] += I32 ? (Acc)di[j] : (Acc)delta;
@@ -209,6 +382,7 @@ __global__ void __launch_bounds__(512) gom_group_kernel(const GomArgs a) {
     } else {
       // ---- general set F (|F| <= 64): stage F's rows (group-start values,
       // the donor pool of engine_parallel.hpp:100-103) in shared memory.
+      const uint32_t sid = a.gsets[p];
       const int64_t f0 = a.set_off[sid];
       const uint32_t f = (uint32_t)(a.set_off[sid + 1] - f0);
       const uint32_t* vars = a.set_vars + f0;
@@ -317,32 +491,48 @@ __global__ void __launch_bounds__(512) gom_group_kernel(const GomArgs a) {
         so[j] = 0.0;
       }
       const int64_t e0 = a.fp_off[sid], e1 = a.fp_off[sid + 1];
-      for (int64_t e = e0; e < e1; ++e) {
-        const FpEntry E = a.fp[e];
+      for (int64_t base = e0; base < e1; base += 32) {
+        const int64_t e = base + lane;
+        const bool has = e < e1;
+        FpEntry E;
+        if (has) {
+          E = a.fp[e];
+        } else {
+          E.a = kInSet;
+          E.b = kInSet;
+          E.w = 0.0;
+        }
+        const uint32_t ext = !(E.a & kInSet) ? E.a : (!(E.b & kInSet) ? E.b : vars[0]);
+        uint32_t xw[WPT];
 #pragma unroll
-        for (int j = 0; j < WPT; ++j) {
-          const uint32_t w = wit + tw * j;
-          uint32_t ao, an, bo, bn;
-          if (E.a & kInSet) {
-            const uint32_t ja = E.a & ~kInSet;
-            ao = (uint32_t)(pm[j] >> ja) & 1u;
-            an = (uint32_t)(dm[j] >> ja) & 1u;
-          } else {
-            ao = an = (a.pop[(size_t)E.a * Wp + w] >> lane) & 1u;
-          }
-          if (E.b & kInSet) {
-            const uint32_t jb = E.b & ~kInSet;
-            bo = (uint32_t)(pm[j] >> jb) & 1u;
-            bn = (uint32_t)(dm[j] >> jb) & 1u;
-          } else {
-            bo = bn = (a.pop[(size_t)E.b * Wp + w] >> lane) & 1u;
-          }
-          if constexpr (I32) {
-            const int32_t wt = (int32_t)E.w;
-            di[j] += ((int32_t)(an ^ bn) - (int32_t)(ao ^ bo)) * wt;
-          } else {
-            sn[j] += (an ^ bn) ? E.w : 0.0;
-            so[j] += (ao ^ bo) ? E.w : 0.0;
+        for (int j = 0; j < WPT; ++j) xw[j] = a.pop[(size_t)ext * Wp + wit + tw * j];
+        const int cnt = (int)(e1 - base < 32 ? e1 - base : 32);
+        for (int t = 0; t < cnt; ++t) {
+          const uint32_t ca = __shfl_sync(0xFFFFFFFFu, E.a, t);
+          const uint32_t cb = __shfl_sync(0xFFFFFFFFu, E.b, t);
+          const double wt = shfl_d(E.w, t);
+#pragma unroll
+          for (int j = 0; j < WPT; ++j) {
+            const uint32_t xb = (__shfl_sync(0xFFFFFFFFu, xw[j], t) >> lane) & 1u;
+            uint32_t ao, an, bo, bn;
+            if (ca & kInSet) {
+              ao = (uint32_t)(pm[j] >> (ca & ~kInSet)) & 1u;
+              an = (uint32_t)(dm[j] >> (ca & ~kInSet)) & 1u;
+            } else {
+              ao = an = xb;
+            }
+            if (cb & kInSet) {
+              bo = (uint32_t)(pm[j] >> (cb & ~kInSet)) & 1u;
+              bn = (uint32_t)(dm[j] >> (cb & ~kInSet)) & 1u;
+            } else {
+              bo = bn = xb;
+            }
+            if constexpr (I32) {
+              di[j] += ((int32_t)(an ^ bn) - (int32_t)(ao ^ bo)) * (int32_t)wt;
+            } else {
+              sn[j] += (an ^ bn) ? wt : 0.0;
+              so[j] += (ao ^ bo) ? wt : 0.0;
+            }
           }
         }
       }
@@ -400,6 +590,7 @@ __global__ void __launch_bounds__(512) gom_group_kernel(const GomArgs a) {
   // ---- per-CTA reductions: counters, fitness deltas, elitist distances ----
   __syncthreads();
   __shared__ unsigned long long s_steps, s_calls;
+  __shared__ int s_last;
   if (threadIdx.x == 0) {
     s_steps = 0;
     s_calls = 0;
@@ -456,109 +647,24 @@ __global__ void __launch_bounds__(512) gom_group_kernel(const GomArgs a) {
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0 && (s_steps | s_calls)) {
-    atomicAdd(&a.ctl->grp_steps, s_steps);
-    atomicAdd(&a.ctl->grp_calls, s_calls);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// epilogue_kernel (1 CTA): commit the group's fitness deltas, account the
-// evaluator calls (budget stop first, runtime.hpp:75-80), then the elitist
-// scan of engine_parallel.hpp:305-310 — the first member strictly better than
-// the running elitist replaces it, the scan continuing against the new value —
-// logging every improvement and latching the target stop (runtime.hpp:88-93).
-// ---------------------------------------------------------------------------
-__device__ void request_stop(DevCtl* c, int reason) {
-  if (!c->stop) {
-    c->stop = 1;
-    c->stop_reason = reason;
-  }
-}
-
-__device__ void note_improvement(const EpiArgs& a, double f) {
-  DevCtl* c = a.ctl;
-  const unsigned long long i = c->n_impr++;
-  if (i < a.impr_cap) a.impr[i] = f;
-  if (c->has_target && (cmp_better(c->exact, f, c->target) || cmp_equal(c->exact, f, c->target)))
-    request_stop(c, GOMIX_STOP_TARGET);
-}
-
-__global__ void __launch_bounds__(kEpilogueThreads) epilogue_kernel(const EpiArgs a) {
-  DevCtl* c = a.ctl;
-  if (*(volatile int32_t*)&c->stop) return;
-  const uint32_t n = a.n;
-  __shared__ double s_chunkmax[kEpilogueThreads / 32];
-  __shared__ int32_t s_best;
-  for (uint32_t s = threadIdx.x; s < n; s += blockDim.x) {
-    double f = a.fit[s];
-    if (a.mode == 2) {
-      for (uint32_t p = 0; p < a.G; ++p)
-        if (a.rec_accept[(size_t)p * n + s]) f += a.rec_delta[(size_t)p * n + s];
-    } else if (a.mode == 1) {
-      double sum = 0.0;
-      for (uint32_t b = 0; b < a.nparts; ++b) sum += a.part[(size_t)b * n + s];
-      f += sum;
-    } else {
-      f += a.dfit[s];
-      a.dfit[s] = 0.0;
-    }
-    a.fit[s] = f;
-    a.ham[s] += a.dham[s];
-    a.dham[s] = 0;
-  }
-  __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned long long st = c->grp_steps, ca = c->grp_calls;
-    c->grp_steps = 0;
-    c->grp_calls = 0;
-    c->calls_total += ca;
-    c->run_steps += st;
-    c->run_calls += ca;
-    c->groups_run += 1;
-    a.gsteps[a.group] += st;
-    a.gcalls[a.group] += ca;
-    if (c->has_budget && (double)c->calls_total / c->q >= c->max_evals)
-      request_stop(c, GOMIX_STOP_BUDGET);
-    s_best = -1;
-  }
-  // chunk maxima let the serial scan skip chunks that cannot hold a record
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-  for (uint32_t chunk = warp; chunk * 32u < n; chunk += blockDim.x >> 5) {
-    const uint32_t s = chunk * 32u + lane;
-    double f = s < n ? a.fit[s] : -INFINITY;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) f = fmax(f, __shfl_xor_sync(0xFFFFFFFFu, f, o));
-    if (lane == 0 && chunk < kEpilogueThreads / 32) s_chunkmax[chunk] = f;
+    if (s_steps | s_calls) {
+      atomicAdd(&a.ctl->grp_steps, s_steps);
+      atomicAdd(&a.ctl->grp_calls, s_calls);
+    }
+    // last-CTA-done ticket: everything above is visible to the last CTA
+    __threadfence();
+    s_last = atomicAdd(&a.ctl->done, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (warp == 0) {
-    const bool exact = c->exact != 0;
-    double cur = c->elit_fit;
-    int32_t best = -1;
-    for (uint32_t base = 0; base < n; base += 32u) {
-      const uint32_t chunk = base >> 5;
-      if (chunk < kEpilogueThreads / 32 && !(s_chunkmax[chunk] > cur)) continue;
-      const uint32_t s = base + lane;
-      const double f = s < n ? a.fit[s] : -INFINITY;
-      uint32_t m = __ballot_sync(0xFFFFFFFFu, s < n && cmp_better(exact, f, cur));
-      while (m) {
-        const uint32_t l = __ffs(m) - 1;
-        cur = __shfl_sync(0xFFFFFFFFu, f, l);
-        best = (int32_t)(base + l);
-        if (lane == 0) note_improvement(a, cur);
-        m = __ballot_sync(0xFFFFFFFFu, s < n && lane > l && cmp_better(exact, f, cur));
-      }
-    }
-    if (lane == 0) {
-      c->elit_src = best;
-      if (best >= 0) c->elit_fit = cur;
-      s_best = best;
-    }
+  if (!s_last) return;
+  __threadfence();
+  epilogue_body(a.epi);
+  if (threadIdx.x == 0) a.ctl->done = 0;
+  if (a.fuse_refresh) {
+    refresh_body(a.ref, threadIdx.x >> 5, blockDim.x >> 5);
+    __syncthreads();
   }
-  __syncthreads();
-  if (s_best >= 0)
-    for (uint32_t s = threadIdx.x; s < n; s += blockDim.x) a.ham[s] = 0;  // refresh recounts
 }
 
 __global__ void begin_call_kernel(const BeginArgs b) {
@@ -575,6 +681,7 @@ __global__ void begin_call_kernel(const BeginArgs b) {
   c->grp_steps = c->grp_calls = 0;
   c->run_steps = c->run_calls = c->groups_run = 0;
   c->n_impr = 0;
+  c->done = 0;
 }
 
 // After init_population (engine_parallel.hpp:331-346): one add_evaluator_calls(q)
@@ -605,48 +712,6 @@ __global__ void init_epilogue_kernel(const EpiArgs a) {
     a.ham[s] = 0;
     a.dham[s] = 0;
     a.dfit[s] = 0.0;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// refresh_kernel: when the elitist changed, copy its genotype out of the
-// population column and recount every member's Hamming distance to it; the
-// batched accept rule only needs "parent == elitist" (engine_parallel.hpp:202),
-// i.e. distance 0, which the GOM kernel then maintains incrementally.
-// ---------------------------------------------------------------------------
-__global__ void refresh_kernel(const RefreshArgs a) {
-  const int32_t src = a.force_src != kNoForce ? a.force_src : *(volatile const int32_t*)&a.ctl->elit_src;
-  if (src == -1) return;
-  const uint32_t Wp = a.Wp;
-  const uint64_t gtid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
-  const uint32_t sw = src >= 0 ? (uint32_t)src >> 5 : 0u, sb = src >= 0 ? (uint32_t)src & 31u : 0u;
-  if (src >= 0) {
-    const uint64_t nwords = (a.nv + 31) / 32;
-    for (uint64_t t = gtid; t < nwords; t += nthreads) {
-      uint32_t word = 0;
-      const uint64_t v0 = t * 32;
-      for (uint32_t k = 0; k < 32 && v0 + k < a.nv; ++k)
-        word |= ((a.pop[(v0 + k) * Wp + sw] >> sb) & 1u) << k;
-      a.elit[t] = word;
-    }
-  }
-  const uint32_t lane = threadIdx.x & 31u;
-  const uint64_t gwarp = gtid >> 5, nwarps = nthreads >> 5;
-  const uint64_t chunks = (a.nv + a.rows_per_chunk - 1) / a.rows_per_chunk;
-  for (uint64_t unit = gwarp; unit < chunks * Wp; unit += nwarps) {
-    const uint32_t w = (uint32_t)(unit % Wp);
-    const uint64_t v0 = (unit / Wp) * a.rows_per_chunk;
-    const uint64_t v1 = min(v0 + a.rows_per_chunk, a.nv);
-    if (w * 32u >= a.n) continue;
-    int32_t cnt = 0;
-    for (uint64_t v = v0; v < v1; ++v) {
-      const uint32_t x = a.pop[v * Wp + w];
-      const uint32_t eb = src >= 0 ? (a.pop[v * Wp + sw] >> sb) & 1u : (a.elit[v >> 5] >> (v & 31u)) & 1u;
-      cnt += ((x ^ (eb ? 0xFFFFFFFFu : 0u)) >> lane) & 1u;
-    }
-    const uint32_t s = w * 32u + lane;
-    if (s < a.n && cnt) atomicAdd(&a.ham[s], cnt);
   }
 }
 
@@ -789,11 +854,6 @@ int gom_max_blocks_per_sm(bool univariate, bool i32, int wpt, int block, size_t 
   int blocks = 0;
   GOMIX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, block, smem));
   return blocks;
-}
-
-void launch_epilogue(const EpiArgs& a, cudaStream_t s) {
-  epilogue_kernel<<<1, kEpilogueThreads, 0, s>>>(a);
-  GOMIX_CUDA(cudaGetLastError());
 }
 
 void launch_begin(const BeginArgs& b, cudaStream_t s) {

@@ -53,6 +53,7 @@ struct DevCtl {
   unsigned long long grp_steps, grp_calls;
   unsigned long long run_steps, run_calls, groups_run;
   unsigned long long n_impr;
+  unsigned int done;  // last-CTA-done ticket of the GOM kernel
 };
 
 struct Problem {
@@ -76,10 +77,39 @@ struct Problem {
   int64_t* set_off = nullptr;
   uint32_t* set_vars = nullptr;
   uint32_t* gsets = nullptr;
+  uint32_t* gvars = nullptr;
   int64_t* fp_off = nullptr;
   FpEntry* fp = nullptr;
   std::vector<void*> allocations;
   ~Problem();
+};
+
+struct EpiArgs {
+  double* fit;
+  const double* part;
+  double* dfit;
+  int32_t* ham;
+  int32_t* dham;
+  const double* rec_delta;
+  const uint8_t* rec_accept;
+  DevCtl* ctl;
+  unsigned long long* gsteps;
+  unsigned long long* gcalls;
+  double* impr;
+  unsigned long long* impr_calls;  // RunControl call count when the improvement was reported
+  uint64_t impr_cap;
+  uint32_t n, G, nparts, group;
+  int32_t mode;  // 0 exact atomics, 1 float partials, 2 ordered
+};
+
+struct RefreshArgs {
+  const uint32_t* pop;
+  uint32_t* elit;
+  int32_t* ham;
+  const DevCtl* ctl;
+  uint64_t nv;
+  uint32_t n, Wp;
+  int32_t force_src;  // kNoForce: use ctl->elit_src
 };
 
 struct GomArgs {
@@ -92,6 +122,7 @@ struct GomArgs {
   const int64_t* fp_off;
   const FpEntry* fp;
   const uint32_t* gsets;  // this group's members (ascending set ids)
+  const uint32_t* gvars;  // singleton FOS: the variable of each member
   uint32_t G;             // |G|
   uint32_t* pop;
   const double* fit;
@@ -110,33 +141,9 @@ struct GomArgs {
   int32_t exact;
   uint32_t generation;
   uint64_t seed;
-};
-
-struct EpiArgs {
-  double* fit;
-  const double* part;
-  double* dfit;
-  int32_t* ham;
-  int32_t* dham;
-  const double* rec_delta;
-  const uint8_t* rec_accept;
-  DevCtl* ctl;
-  unsigned long long* gsteps;
-  unsigned long long* gcalls;
-  double* impr;
-  uint64_t impr_cap;
-  uint32_t n, G, nparts, group;
-  int32_t mode;  // 0 exact atomics, 1 float partials, 2 ordered
-};
-
-struct RefreshArgs {
-  const uint32_t* pop;
-  uint32_t* elit;
-  int32_t* ham;
-  const DevCtl* ctl;
-  uint64_t nv;
-  uint32_t n, Wp, rows_per_chunk;
-  int32_t force_src;  // kNoForce: use ctl->elit_src
+  EpiArgs epi;         // run by the last CTA
+  RefreshArgs ref;
+  int32_t fuse_refresh;
 };
 
 constexpr int32_t kNoForce = -1000;
@@ -215,7 +222,6 @@ class ReplayStream {
 void launch_gom(const GomArgs& a, bool univariate, bool i32, int wpt, int grid, int block,
                 size_t smem, cudaStream_t s);
 int gom_max_blocks_per_sm(bool univariate, bool i32, int wpt, int block, size_t smem);
-void launch_epilogue(const EpiArgs& a, cudaStream_t s);
 void launch_begin(const BeginArgs& b, cudaStream_t s);
 void launch_init_epilogue(const EpiArgs& a, cudaStream_t s);
 void launch_refresh(const RefreshArgs& a, int grid, cudaStream_t s);

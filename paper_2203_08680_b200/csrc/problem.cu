@@ -409,6 +409,12 @@ void build_problem_device_impl(Problem& P, const int32_t* given_colour, const in
     for (uint64_t i = 0; i < m; ++i) P.group_off[(size_t)h_col[i] + 1]++;
     for (uint64_t c = 0; c < P.k; ++c) P.group_off[c + 1] += P.group_off[c];
     P.group_sets.assign(h_gs.begin(), h_gs.end());
+    if (P.univariate) {  // variable of each member, in group order
+      std::vector<uint32_t> gv(m);
+      for (uint64_t i = 0; i < m; ++i) gv[i] = P.h_set_vars[P.h_set_off[h_gs[i]]];
+      P.gvars = dev_alloc<uint32_t>(P.allocations, m);
+      GOMIX_CUDA(cudaMemcpy(P.gvars, gv.data(), m * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    }
   }
 
   // 5. footprint plans (multi-variable sets only; singletons read the CSR row)

@@ -267,20 +267,30 @@ class GpuParallelEngine:
 
     # ---- bookkeeping shared with RunContext -----------------------------------
     def _absorb(self, stats: _capi.RunStats, generation: int):
+        """Replay the call's accounting into the run-wide RunContext in the
+        reference's order: evaluator calls up to each improvement, the
+        improvement, then the rest (engine_parallel.hpp:298-310)."""
         ctl = self.ctx.control
-        ctl.calls += int(stats.evaluator_calls)
+        start = ctl.calls
+        end = start + int(stats.evaluator_calls)
+        fit, calls_at = self.improvements(int(stats.improvements))
+        if stats.stopped and stats.stop_reason == 1:
+            ctl.request_stop("evaluation-budget")
+        for f, c in zip(fit.tolist(), calls_at.tolist()):
+            ctl.calls = max(ctl.calls, int(c))
+            self.ctx.report_improvement(float(f), generation, self.pop_id)
+        ctl.calls = end
         if stats.stopped:
             ctl.request_stop(_capi.STOP_NAMES[stats.stop_reason])
-        for f in self.improvements(int(stats.improvements)):
-            self.ctx.report_improvement(float(f), generation, self.pop_id)
         self._elitist_fitness = float(stats.elitist_fitness)
         self.last_stats = stats
 
-    def improvements(self, count: int) -> np.ndarray:
+    def improvements(self, count: int):
         buf = np.zeros(max(count, 1), np.float64)
+        calls = np.zeros(max(count, 1), np.uint64)
         got = C.c_uint64()
-        check(lib().gomix_gpu_read_improvements(self.h, buf.ctypes.data, count, C.byref(got)))
-        return buf[:got.value]
+        check(lib().gomix_gpu_read_improvements(self.h, buf.ctypes.data, calls.ctypes.data, count, C.byref(got)))
+        return buf[:got.value], calls[:got.value]
 
     # ---- GenerationRunner (ims.hpp:14-22) -----------------------------------------
     def run_generation(self):

@@ -76,7 +76,10 @@ def test_replay_generations_match_reference(name):
         assert (f == F[gen]).all(), gen
         eg, ef = E.elitist()
         assert ef == d["elitist"][gen]
-        assert inst.cut_value(eg) == ef
+        # the elitist's fitness is accumulated (init + deltas) like the
+        # reference's; with float weights it equals a fresh evaluation only
+        # to within rounding
+        assert inst.cut_value(eg) == (ef if P.exact else pytest.approx(ef, rel=1e-12))
         assert ctx.control.calls == int(d["calls"][gen])
         assert E.generation() == gen + 1
     if "final_genotypes" in d:
@@ -85,6 +88,7 @@ def test_replay_generations_match_reference(name):
     assert (steps == d["counter_steps"]).all() and (calls == d["counter_calls"]).all()
     assert [r.fitness for r in sink.rows] == d["trace_fitness"].tolist()
     assert [r.generation for r in sink.rows] == d["trace_generation"].tolist()
+    assert [r.evaluations for r in sink.rows] == d["trace_evals"].tolist()
 
 
 @pytest.mark.parametrize("name", ["c1_int", "c1_pm5", "torus6_w", "neigh12", "neigh_n40", "bflt4_8x8",
