@@ -219,7 +219,8 @@ def bench_ours(args):
     inst = G.generate_torus(cfg["width"], cfg["height"], cfg["weights"], 1)
     fos = G.univariate_fos(inst.num_vertices) if cfg["fos"] == "uni" else G.neighbourhood_fos(inst)
     P = G.GpuProblem(inst, fos, device=dev)
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()  # a real stream: the legacy NULL stream would not see our kernels
+    torch.cuda.set_stream(stream)
     E = G.GpuParallelEngine(P, n, seed=1 + rank, mode="philox", time_kernels=True, stream=stream.cuda_stream)
 
     def barrier():

@@ -413,7 +413,7 @@ struct gomix_gpu_engine {
   }
 
   // the last CTA of the GOM kernel refreshes small populations itself
-  bool fuse_refresh() const { return P->nv * Wp <= (1u << 18); }
+  bool fuse_refresh() const { return P->nv * Wp <= 4096; }
 
   EpiArgs epi_args(uint64_t group, uint32_t G, uint32_t nparts) const {
     EpiArgs e;

@@ -185,14 +185,15 @@ def test_float_regular_graph_vs_oracle():
     assert (g == og).all() and (f == of).all()
 
 
-@pytest.mark.parametrize("crit", [dict(max_evaluations=6000.0), dict(target_fitness=1000.0),
-                                  dict(max_generations=3)])
+@pytest.mark.parametrize("crit", [dict(max_evaluations=1000.0), dict(max_evaluations=777.0),
+                                  dict(target_fitness=1000.0), dict(max_generations=3)])
 def test_stop_criteria_match_oracle(crit):
     inst = G.generate_torus(10, 10, ("int", 1, 10), 1)
     fos = G.univariate_fos(100)
     P = G.GpuProblem(inst, fos)
     Oe = _oracle_for(inst, fos, P.colour(), 32, 1)
-    Oe.set_termination(**crit)
+    Oe.set_termination(max_evaluations=crit.get("max_evaluations"), target=crit.get("target_fitness"),
+                       max_generations=crit.get("max_generations"))
     ctx = G.RunContext(G.TerminationConfig(**crit), P.comparator(), inst.num_edges)
     E = G.GpuParallelEngine(P, 32, 1, ctx=ctx, mode="replay")
     for _ in range(60):
