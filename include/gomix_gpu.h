@@ -225,6 +225,10 @@ GOMIX_API int gomix_gpu_generation(gomix_gpu_engine* e, int64_t* generation);
 /* Durations (ms) of the GOM kernel launches since the last call (needs
  * GOMIX_FLAG_TIME_KERNELS); count = number written. */
 GOMIX_API int gomix_gpu_kernel_times(gomix_gpu_engine* e, float* ms, uint64_t capacity, uint64_t* count);
+/* Turn GOMIX_FLAG_TIME_KERNELS on or off.  While on, generations are issued
+ * launch by launch (events around every GOM kernel) instead of as one CUDA
+ * graph. */
+GOMIX_API int gomix_gpu_set_timing(gomix_gpu_engine* e, int32_t enable);
 /* Number of device kernels this engine has launched so far. */
 GOMIX_API int gomix_gpu_launch_count(gomix_gpu_engine* e, uint64_t* count);
 

@@ -240,6 +240,10 @@ struct gomix_gpu_engine {
   uint8_t* rec_present = nullptr;
   uint8_t* rec_accept = nullptr;
   uint64_t max_group = 0;
+  uint32_t* d_order = nullptr;
+  GroupDesc* d_groups = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  uint64_t graph_launches = 0;
 
   cudaStream_t stream = nullptr;
   bool own_stream = false;
@@ -256,6 +260,7 @@ struct gomix_gpu_engine {
 
   ~gomix_gpu_engine() {
     if (stream) cudaStreamSynchronize(stream);
+    if (graph_exec) cudaGraphExecDestroy(graph_exec);
     for (auto& pr : ev_pending) {
       cudaEventDestroy(pr.first);
       cudaEventDestroy(pr.second);
@@ -285,10 +290,20 @@ struct gomix_gpu_engine {
     pop_id = cfg.population_id ? cfg.population_id : 1;
     rng = ReplayStream(seed);
     W = (uint32_t)((n + 31) / 32);
+    GOMIX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, P->device));
     if (W <= 8) {
       Wp = next_pow2(W);
-      wpt = Wp;
-      tw = 1;
+      // few sets per group (small instances / big sets): one word per warp and
+      // Wp warps per set, for parallelism; otherwise a warp per set with every
+      // word in registers.
+      const uint64_t avg_group = (P->m + P->k - 1) / P->k;
+      if (Wp > 1 && avg_group * Wp <= (uint64_t)sms * 32) {
+        wpt = 1;
+        tw = Wp;
+      } else {
+        wpt = Wp;
+        tw = 1;
+      }
       block = 256;
     } else if (W <= 32) {
       Wp = next_pow2(W);
@@ -304,9 +319,12 @@ struct gomix_gpu_engine {
       invalid("engine: population sizes above 4096 are not supported");
     }
     teams = block / 32 / tw;
-    stage_words = P->univariate ? 0 : (uint32_t)(P->max_f * Wp);
-    const size_t stage = (size_t)teams * 2 * stage_words * 4;
-    const size_t red = tw == 1 ? (size_t)teams * Wp * 32 * 12 : 0;
+    if (!P->univariate) {
+      stage_words = (uint32_t)(3 * P->max_f * Wp + 64 * Wp);  // rows, donor rows, new rows, patterns
+      stage_words += stage_words & 1u;                         // keep patterns 8-byte aligned
+    }
+    const size_t stage = (size_t)teams * stage_words * 4;
+    const size_t red = teams > 1 ? (size_t)teams * Wp * 32 * 12 : 0;
     smem = std::max(stage, red);
     if (smem > 227 * 1024) invalid("engine: set size x population too large for shared-memory staging");
     record = (flags & GOMIX_FLAG_RECORD_BATCH) != 0;
@@ -316,7 +334,6 @@ struct gomix_gpu_engine {
     GOMIX_CUDA(cudaSetDevice(P->device));
     GOMIX_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     own_stream = true;
-    GOMIX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, P->device));
     const int per_sm = gom_max_blocks_per_sm(P->univariate, P->i32, (int)wpt, (int)block, smem);
     if (per_sm < 1) invalid("engine: GOM kernel does not fit on an SM with this configuration");
     grid_cap = per_sm * sms;
@@ -338,6 +355,15 @@ struct gomix_gpu_engine {
     impr_calls = dev_alloc<unsigned long long>(allocs, impr_cap);
     if (epi_mode == 1) part = dev_alloc<double>(allocs, (size_t)grid_cap * n);
     tape = dev_alloc<int32_t>(allocs, max_group * n);
+    d_order = dev_alloc<uint32_t>(allocs, P->k);
+    d_groups = dev_alloc<GroupDesc>(allocs, P->k);
+    {
+      std::vector<GroupDesc> gd(P->k);
+      for (uint64_t c = 0; c < P->k; ++c)
+        gd[c] = GroupDesc{(uint32_t)P->group_off[c], (uint32_t)(P->group_off[c + 1] - P->group_off[c])};
+      GOMIX_CUDA(cudaMemcpy(d_groups, gd.data(), P->k * sizeof(GroupDesc), cudaMemcpyHostToDevice));
+    }
+    prepare_gom(P->univariate, P->i32, (int)wpt, smem);
     if (record || epi_mode == 2) {
       rec_donor = dev_alloc<int32_t>(allocs, max_group * n);
       rec_delta = dev_alloc<double>(allocs, max_group * n);
@@ -369,8 +395,41 @@ struct gomix_gpu_engine {
     b.q = (double)P->q;
     b.target = stop ? stop->target_fitness : 0.0;
     b.calls_before = stop ? stop->evaluator_calls_before : 0;
+    b.gen = (uint32_t)generation;
     launch_begin(b, stream);
     ++launches;
+  }
+
+  static bool no_criteria(const gomix_stop_criteria* stop) {
+    return !stop || (!stop->has_max_evaluations && !stop->has_target);
+  }
+
+  // One CUDA graph per engine for a whole Philox generation: the order
+  // kernel, then k (GOM [+ refresh]) launches that find their group through
+  // the device-side order.  Replaces ~2k launches by one graph launch.
+  void launch_generation_graph() {
+    if (!graph_exec) {
+      cudaStream_t cap = nullptr;
+      GOMIX_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+      GOMIX_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+      BeginArgs b{};
+      b.ctl = ctl;
+      b.exact = P->exact;
+      b.q = (double)P->q;
+      OrderArgs o{ctl, d_order, (uint32_t)P->k, seed};
+      launch_order(b, o, cap);
+      const uint64_t saved = launches;
+      for (uint64_t slot = 0; slot < P->k; ++slot) launch_group(0, false, (int32_t)slot, cap);
+      graph_launches = launches - saved + 1;
+      launches = saved;
+      cudaGraph_t g = nullptr;
+      GOMIX_CUDA(cudaStreamEndCapture(cap, &g));
+      GOMIX_CUDA(cudaGraphInstantiate(&graph_exec, g, 0));
+      GOMIX_CUDA(cudaGraphDestroy(g));
+      GOMIX_CUDA(cudaStreamDestroy(cap));
+    }
+    GOMIX_CUDA(cudaGraphLaunch(graph_exec, stream));
+    launches += graph_launches;
   }
 
   void read_ctl() {
@@ -403,12 +462,13 @@ struct gomix_gpu_engine {
     return r;
   }
 
-  void refresh(int32_t force_src = kNoForce) {
+  void refresh(int32_t force_src = kNoForce, cudaStream_t st = nullptr) {
+    if (!st) st = stream;
     RefreshArgs r = refresh_args();
     r.force_src = force_src;
     const uint64_t units = ((P->nv + 31) / 32) * Wp;
     const int grid = (int)std::min<uint64_t>(std::max<uint64_t>(1, (units + 7) / 8), (uint64_t)sms * 8);
-    launch_refresh(r, grid, stream);
+    launch_refresh(r, grid, st);
     ++launches;
   }
 
@@ -439,8 +499,10 @@ struct gomix_gpu_engine {
   }
 
   // ---- one batched group step -----------------------------------------------
-  void launch_group(uint64_t group, bool with_tape) {
-    const uint64_t g0 = P->group_off[group], G = P->group_off[group + 1] - g0;
+  void launch_group(uint64_t group, bool with_tape, int32_t slot = -1, cudaStream_t st = nullptr) {
+    if (!st) st = stream;
+    const uint64_t g0 = slot >= 0 ? 0 : P->group_off[group];
+    const uint64_t G = slot >= 0 ? max_group : P->group_off[group + 1] - g0;
     GomArgs a;
     a.row_ptr = P->row_ptr;
     a.col = P->col;
@@ -474,25 +536,28 @@ struct gomix_gpu_engine {
     a.exact = P->exact;
     a.generation = (uint32_t)generation;
     a.seed = seed;
+    a.slot = slot;
+    a.order = d_order;
+    a.groups = d_groups;
     const uint64_t want = (G + teams - 1) / teams;
     const int grid = (int)std::min<uint64_t>(want, (uint64_t)grid_cap);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (flags & GOMIX_FLAG_TIME_KERNELS) {
+    if ((flags & GOMIX_FLAG_TIME_KERNELS) && slot < 0) {
       e0 = take_event();
       e1 = take_event();
-      GOMIX_CUDA(cudaEventRecord(e0, stream));
+      GOMIX_CUDA(cudaEventRecord(e0, st));
     }
     a.epi = epi_args(group, (uint32_t)G, (uint32_t)grid);
     a.ref = refresh_args();
     a.fuse_refresh = fuse_refresh();
-    launch_gom(a, P->univariate, P->i32, (int)wpt, grid, (int)block, smem, stream);
+    launch_gom(a, P->univariate, P->i32, (int)wpt, grid, (int)block, smem, st);
     ++launches;
     if (e1) {
-      GOMIX_CUDA(cudaEventRecord(e1, stream));
+      GOMIX_CUDA(cudaEventRecord(e1, st));
       ev_pending.push_back({e0, e1});
     }
-    if (!a.fuse_refresh) refresh();
-    last_group = (int64_t)group;
+    if (!a.fuse_refresh) refresh(kNoForce, st);
+    if (slot < 0) last_group = (int64_t)group;
   }
 
   cudaEvent_t take_event() {
@@ -591,6 +656,13 @@ struct gomix_gpu_engine {
 
   void run_generation(const gomix_stop_criteria* stop, gomix_run_stats* out) {
     if (!initialized) throw GomixError(GOMIX_E_STATE, "run_generation: population not initialised");
+    if (mode == GOMIX_MODE_PHILOX && no_criteria(stop) && !(flags & GOMIX_FLAG_TIME_KERNELS)) {
+      launch_generation_graph();
+      read_ctl();
+      fill_stats(out);
+      if (!h_ctl->stop) ++generation;
+      return;
+    }
     begin_call(stop);
     std::vector<uint64_t> order;
     rng.permutation(order, P->k);  // engine_parallel.hpp:291
@@ -620,10 +692,14 @@ struct gomix_gpu_engine {
   void run_generation_async() {
     if (!initialized) throw GomixError(GOMIX_E_STATE, "run_generation: population not initialised");
     if (mode != GOMIX_MODE_PHILOX) invalid("run_generation_async: needs GOMIX_MODE_PHILOX");
-    begin_call(nullptr);
-    std::vector<uint64_t> order;
-    rng.permutation(order, P->k);
-    for (uint64_t gi : order) launch_group(gi, false);
+    if (flags & GOMIX_FLAG_TIME_KERNELS) {
+      begin_call(nullptr);
+      std::vector<uint64_t> order;
+      rng.permutation(order, P->k);
+      for (uint64_t gi : order) launch_group(gi, false);
+    } else {
+      launch_generation_graph();
+    }
     ++generation;
   }
 
@@ -959,6 +1035,16 @@ int gomix_gpu_kernel_times(gomix_gpu_engine* e, float* ms, uint64_t capacity, ui
     }
     e->ev_pending.clear();
     if (count) *count = std::min(written, capacity);
+  });
+}
+
+int gomix_gpu_set_timing(gomix_gpu_engine* e, int32_t enable) {
+  return guarded([&] {
+    if (!e) invalid("set_timing: NULL engine");
+    if (enable)
+      e->flags |= GOMIX_FLAG_TIME_KERNELS;
+    else
+      e->flags &= ~(uint32_t)GOMIX_FLAG_TIME_KERNELS;
   });
 }
 

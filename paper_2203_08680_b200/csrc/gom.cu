@@ -63,11 +63,39 @@ __device__ __forceinline__ uint32_t valid_mask(uint32_t w, uint32_t n) {
   return (1u << (n - lo)) - 1u;
 }
 
-__device__ __forceinline__ void team_sync(uint32_t team_warps) {
-  if (team_warps == 1)
+// Teams of tw warps; several teams per CTA synchronise on their own named
+// barrier (ids 1..8, 0 is __syncthreads).
+__device__ __forceinline__ void team_sync(uint32_t tw, uint32_t teams_per_cta, uint32_t team) {
+  if (tw == 1)
     __syncwarp();
-  else
+  else if (teams_per_cta == 1)
     __syncthreads();
+  else
+    asm volatile("bar.sync %0, %1;" ::"r"(team + 1), "r"(tw * 32) : "memory");
+}
+
+// Members of word w2 that differ from pattern m somewhere on F.
+__device__ __forceinline__ uint32_t differ_word(const uint32_t* rowsF, uint32_t f, uint32_t Wp,
+                                                uint32_t w2, uint64_t m, uint32_t n) {
+  uint32_t dw = 0;
+  for (uint32_t jv = 0; jv < f; ++jv)
+    dw |= rowsF[jv * Wp + w2] ^ (((m >> jv) & 1ull) ? 0xFFFFFFFFu : 0u);
+  return dw & valid_mask(w2, n);
+}
+
+// Position of the k-th (0-based) set bit of x; k < popc(x).
+__device__ __forceinline__ uint32_t select_bit(uint32_t x, uint32_t k) {
+  uint32_t pos = 0;
+#pragma unroll
+  for (uint32_t sh = 16; sh >= 1; sh >>= 1) {
+    const uint32_t c = __popc(x & ((1u << sh) - 1u));
+    if (k >= c) {
+      k -= c;
+      x >>= sh;
+      pos += sh;
+    }
+  }
+  return pos;
 }
 
 // ---------------------------------------------------------------------------
@@ -260,8 +288,21 @@ __global__ void __launch_bounds__(512, 1) gom_group_kernel(const GomArgs a) {
   const bool exact = a.exact != 0;
   const bool replay = a.tape != nullptr;
   const bool record = a.rec_present != nullptr;
-  uint32_t* rowsF = smem + (size_t)team * 2u * a.stage_words;
-  uint32_t* newF = rowsF + a.stage_words;
+  uint32_t* stage = smem + (size_t)team * a.stage_words;
+  uint32_t G = a.G, generation = a.generation;
+  const uint32_t* gsets = a.gsets;
+  const uint32_t* gvars = a.gvars;
+  EpiArgs epi = a.epi;
+  if (a.slot >= 0) {  // graph path: this launch's group comes from the device-side order
+    const uint32_t gi = a.order[a.slot];
+    const GroupDesc d = a.groups[gi];
+    G = d.G;
+    gsets += d.g0;
+    if (gvars) gvars += d.g0;
+    generation = *(volatile unsigned int*)&a.ctl->cur_gen;
+    epi.group = gi;
+    epi.G = G;
+  }
 
   Acc acc[WPT];
   int32_t hacc[WPT];
@@ -273,13 +314,13 @@ __global__ void __launch_bounds__(512, 1) gom_group_kernel(const GomArgs a) {
   uint32_t steps = 0;
   unsigned long long calls = 0;
 
-  for (uint32_t p = blockIdx.x * teams_per_cta + team; p < a.G; p += gridDim.x * teams_per_cta) {
+  for (uint32_t p = blockIdx.x * teams_per_cta + team; p < G; p += gridDim.x * teams_per_cta) {
     if constexpr (UNIV) {
       // ---- univariate set {v}: a donor differing on v holds !x_v, so the
       // pair is present iff some member holds the other value and the move
       // is the flip of v; in Philox mode the draw cannot change the outcome
       // and is skipped.
-      const uint32_t v = a.gvars[p];
+      const uint32_t v = gvars[p];
       const uint32_t* row = a.pop + (size_t)v * Wp;
       uint32_t pw[WPT];
 #pragma unroll
@@ -380,17 +421,23 @@ __global__ void __launch_bounds__(512, 1) gom_group_kernel(const GomArgs a) {
         }
       }
     } else {
-      // ---- general set F (|F| <= 64): stage F's rows (group-start values,
-      // the donor pool of engine_parallel.hpp:100-103) in shared memory.
-      const uint32_t sid = a.gsets[p];
+      // ---- general set F (|F| <= 64).  Shared memory per team holds the F
+      // rows at group start (the donor pool, engine_parallel.hpp:100-103),
+      // every solution's pattern on F (so a donor test is one load), the
+      // donor-inserted rows and the committed rows.
+      const uint32_t sid = gsets[p];
       const int64_t f0 = a.set_off[sid];
       const uint32_t f = (uint32_t)(a.set_off[sid + 1] - f0);
       const uint32_t* vars = a.set_vars + f0;
+      uint64_t* patt = reinterpret_cast<uint64_t*>(stage);
+      uint32_t* rowsF = stage + 64u * Wp;
+      uint32_t* newD = rowsF + f * Wp;
+      uint32_t* newF = newD + f * Wp;
       for (uint32_t idx = tid_team; idx < f * Wp; idx += team_threads) {
         const uint32_t jv = idx / Wp, w = idx - jv * Wp;
         rowsF[idx] = a.pop[(size_t)vars[jv] * Wp + w];
       }
-      uint64_t em;
+      uint64_t em;  // elitist genotype on F
       {
         const uint32_t v0 = lane < f ? vars[lane] : 0u;
         const uint32_t v1 = lane + 32u < f ? vars[lane + 32u] : 0u;
@@ -400,88 +447,92 @@ __global__ void __launch_bounds__(512, 1) gom_group_kernel(const GomArgs a) {
              ((uint64_t)__ballot_sync(0xFFFFFFFFu, b1) << 32);
       }
       const uint64_t fm = f >= 64 ? ~0ull : ((1ull << f) - 1ull);
-      team_sync(tw);
+      team_sync(tw, teams_per_cta, team);
+      uint64_t pm[WPT];
+#pragma unroll
+      for (int j = 0; j < WPT; ++j) {
+        const uint32_t w = wit + tw * j;
+        uint64_t m = 0;
+        for (uint32_t jv = 0; jv < f; ++jv) m |= (uint64_t)((rowsF[jv * Wp + w] >> lane) & 1u) << jv;
+        pm[j] = m;
+        patt[w * 32u + lane] = m;
+      }
+      team_sync(tw, teams_per_cta, team);
 
-      uint64_t pm[WPT], dm[WPT];
+      // phase 1: donors
+      uint64_t dm[WPT];
       bool present[WPT];
       int32_t dsel[WPT];
 #pragma unroll
       for (int j = 0; j < WPT; ++j) {
         const uint32_t w = wit + tw * j;
         const uint32_t s = w * 32u + lane;
-        const bool valid = s < n;
-        uint64_t m = 0;
-        for (uint32_t jv = 0; jv < f; ++jv) m |= (uint64_t)((rowsF[jv * Wp + w] >> lane) & 1u) << jv;
-        pm[j] = m;
+        const uint64_t m = pm[j];
         int32_t d = -1;
-        uint64_t dmask = m;
-        if (valid) {
+        uint64_t x = m;
+        if (s < n) {
           if (replay) {
             d = a.tape[(size_t)p * n + s];
-            if (d >= 0) {
-              uint64_t x = 0;
-              for (uint32_t jv = 0; jv < f; ++jv)
-                x |= (uint64_t)((rowsF[jv * Wp + ((uint32_t)d >> 5)] >> (d & 31)) & 1u) << jv;
-              dmask = x;
-            }
+            if (d >= 0) x = patt[d];
           } else {
-            // uniform over members that differ on F (the lazy Fisher-Yates scan
-            // of engine_serial.hpp:30-46 returns exactly that distribution):
-            // rejection sampling first, exact count-and-select as fallback.
+            // uniform over the members that differ on F — the distribution of
+            // the lazy Fisher-Yates scan of engine_serial.hpp:30-46: rejection
+            // sampling first, exact count-and-select when it keeps failing.
             const uint2 key = make_uint2((uint32_t)a.seed, (uint32_t)(a.seed >> 32));
             for (uint32_t call = 0; call < 2 && d < 0; ++call) {
-              const uint4 r = philox4x32_10(make_uint4(s, sid, a.generation, kTagGom | call), key);
-#pragma unroll
-              for (int t = 0; t < 2; ++t) {
-                if (d >= 0) break;
-                const uint32_t c = bounded(t ? hi64(r) : lo64(r), n);
-                uint64_t x = 0;
-                for (uint32_t jv = 0; jv < f; ++jv)
-                  x |= (uint64_t)((rowsF[jv * Wp + (c >> 5)] >> (c & 31u)) & 1u) << jv;
-                if (x != m) {
-                  d = (int32_t)c;
-                  dmask = x;
+              const uint4 r = philox4x32_10(make_uint4(s, sid, generation, kTagGom | call), key);
+              const uint32_t c0 = bounded(lo64(r), n);
+              const uint64_t x0 = patt[c0];
+              if (x0 != m) {
+                d = (int32_t)c0;
+                x = x0;
+              } else {
+                const uint32_t c1 = bounded(hi64(r), n);
+                const uint64_t x1 = patt[c1];
+                if (x1 != m) {
+                  d = (int32_t)c1;
+                  x = x1;
                 }
               }
             }
             if (d < 0) {
               uint32_t total = 0;
-              for (uint32_t w2 = 0; w2 < Wp; ++w2) {
-                uint32_t dw = 0;
-                for (uint32_t jv = 0; jv < f; ++jv)
-                  dw |= rowsF[jv * Wp + w2] ^ (((m >> jv) & 1ull) ? 0xFFFFFFFFu : 0u);
-                total += __popc(dw & valid_mask(w2, n));
-              }
+              for (uint32_t w2 = 0; w2 < Wp; ++w2) total += __popc(differ_word(rowsF, f, Wp, w2, m, n));
               if (total > 0) {
-                const uint4 r = philox4x32_10(make_uint4(s, sid, a.generation, kTagGom | 2u), key);
+                const uint4 r = philox4x32_10(make_uint4(s, sid, generation, kTagGom | 2u), key);
                 uint32_t kth = bounded(lo64(r), total);
                 for (uint32_t w2 = 0; w2 < Wp; ++w2) {
-                  uint32_t dw = 0;
-                  for (uint32_t jv = 0; jv < f; ++jv)
-                    dw |= rowsF[jv * Wp + w2] ^ (((m >> jv) & 1ull) ? 0xFFFFFFFFu : 0u);
-                  dw &= valid_mask(w2, n);
+                  const uint32_t dw = differ_word(rowsF, f, Wp, w2, m, n);
                   const uint32_t c = __popc(dw);
                   if (kth < c) {
-                    for (uint32_t i = 0; i < kth; ++i) dw &= dw - 1u;  // drop kth lowest
-                    d = (int32_t)(w2 * 32u + (uint32_t)(__ffs(dw) - 1));
+                    d = (int32_t)(w2 * 32u + select_bit(dw, kth));
                     break;
                   }
                   kth -= c;
                 }
-                uint64_t x = 0;
-                for (uint32_t jv = 0; jv < f; ++jv)
-                  x |= (uint64_t)((rowsF[jv * Wp + ((uint32_t)d >> 5)] >> (d & 31)) & 1u) << jv;
-                dmask = x;
+                x = patt[d];
               }
             }
           }
         }
-        dm[j] = dmask;
+        dm[j] = x;
         present[j] = d >= 0;
         dsel[j] = d;
+        uint32_t mine = 0, mine2 = 0;  // lane jv keeps the donor-inserted word of F's jv-th row
+        for (uint32_t jv = 0; jv < f; ++jv) {
+          const uint32_t word = __ballot_sync(0xFFFFFFFFu, (uint32_t)(x >> jv) & 1u);
+          if (lane == (jv & 31u)) {
+            if (jv < 32) mine = word; else mine2 = word;
+          }
+        }
+        if (lane < f) newD[lane * Wp + w] = mine;
+        if (lane + 32u < f) newD[(lane + 32u) * Wp + w] = mine2;
       }
+      team_sync(tw, teams_per_cta, team);
 
-      // phase 2: footprint sums, ascending edge id (engine_parallel.hpp:164-173)
+      // phase 2: footprint sums on whole row words, ascending edge id
+      // (engine_parallel.hpp:164-173); entries and outside rows prefetched by
+      // the lanes and broadcast with shuffles.
       int32_t di[WPT];
       double sn[WPT], so[WPT];
 #pragma unroll
@@ -506,32 +557,29 @@ __global__ void __launch_bounds__(512, 1) gom_group_kernel(const GomArgs a) {
         uint32_t xw[WPT];
 #pragma unroll
         for (int j = 0; j < WPT; ++j) xw[j] = a.pop[(size_t)ext * Wp + wit + tw * j];
+        const int32_t ewi = (int32_t)E.w;
         const int cnt = (int)(e1 - base < 32 ? e1 - base : 32);
         for (int t = 0; t < cnt; ++t) {
           const uint32_t ca = __shfl_sync(0xFFFFFFFFu, E.a, t);
           const uint32_t cb = __shfl_sync(0xFFFFFFFFu, E.b, t);
-          const double wt = shfl_d(E.w, t);
+          const bool ina = ca & kInSet, inb = cb & kInSet;
+          const uint32_t ja = (ca & ~kInSet) * Wp, jb = (cb & ~kInSet) * Wp;
+          int32_t wti = 0;
+          double wt = 0.0;
+          if constexpr (I32) wti = __shfl_sync(0xFFFFFFFFu, ewi, t);
+          else wt = shfl_d(E.w, t);
 #pragma unroll
           for (int j = 0; j < WPT; ++j) {
-            const uint32_t xb = (__shfl_sync(0xFFFFFFFFu, xw[j], t) >> lane) & 1u;
-            uint32_t ao, an, bo, bn;
-            if (ca & kInSet) {
-              ao = (uint32_t)(pm[j] >> (ca & ~kInSet)) & 1u;
-              an = (uint32_t)(dm[j] >> (ca & ~kInSet)) & 1u;
-            } else {
-              ao = an = xb;
-            }
-            if (cb & kInSet) {
-              bo = (uint32_t)(pm[j] >> (cb & ~kInSet)) & 1u;
-              bn = (uint32_t)(dm[j] >> (cb & ~kInSet)) & 1u;
-            } else {
-              bo = bn = xb;
-            }
+            const uint32_t w = wit + tw * j;
+            const uint32_t xo = (ina && inb) ? 0u : __shfl_sync(0xFFFFFFFFu, xw[j], t);
+            const uint32_t aO = ina ? rowsF[ja + w] : xo, aN = ina ? newD[ja + w] : xo;
+            const uint32_t bO = inb ? rowsF[jb + w] : xo, bN = inb ? newD[jb + w] : xo;
+            const uint32_t co = ((aO ^ bO) >> lane) & 1u, cn = ((aN ^ bN) >> lane) & 1u;
             if constexpr (I32) {
-              di[j] += ((int32_t)(an ^ bn) - (int32_t)(ao ^ bo)) * (int32_t)wt;
+              di[j] += ((int32_t)cn - (int32_t)co) * wti;
             } else {
-              sn[j] += (an ^ bn) ? wt : 0.0;
-              so[j] += (ao ^ bo) ? wt : 0.0;
+              sn[j] += cn ? wt : 0.0;
+              so[j] += co ? wt : 0.0;
             }
           }
         }
@@ -556,11 +604,9 @@ __global__ void __launch_bounds__(512, 1) gom_group_kernel(const GomArgs a) {
             accept = cmp_better(false, cand, pf) || (cmp_equal(false, cand, pf) && !elit);
           }
         }
-        const uint64_t nm = accept ? dm[j] : pm[j];
-        for (uint32_t jv = 0; jv < f; ++jv) {
-          const uint32_t word = __ballot_sync(0xFFFFFFFFu, (uint32_t)(nm >> jv) & 1u);
-          if (lane == 0) newF[jv * Wp + w] = word;
-        }
+        const uint32_t acc_w = __ballot_sync(0xFFFFFFFFu, accept);
+        for (uint32_t jv = lane; jv < f; jv += 32)
+          newF[jv * Wp + w] = (rowsF[jv * Wp + w] & ~acc_w) | (newD[jv * Wp + w] & acc_w);
         if (accept) {
           acc[j] += I32 ? (Acc)di[j] : (Acc)delta;
           hacc[j] += __popcll((dm[j] ^ em) & fm) - __popcll((pm[j] ^ em) & fm);
@@ -575,7 +621,7 @@ __global__ void __launch_bounds__(512, 1) gom_group_kernel(const GomArgs a) {
           a.rec_accept[at] = accept;
         }
       }
-      team_sync(tw);
+      team_sync(tw, teams_per_cta, team);
       for (uint32_t idx = tid_team; idx < f * Wp; idx += team_threads) {
         const uint32_t nw = newF[idx];
         if (nw != rowsF[idx]) {
@@ -583,7 +629,7 @@ __global__ void __launch_bounds__(512, 1) gom_group_kernel(const GomArgs a) {
           a.pop[(size_t)vars[jv] * Wp + w] = nw;
         }
       }
-      team_sync(tw);
+      team_sync(tw, teams_per_cta, team);
     }
   }
 
@@ -607,13 +653,13 @@ __global__ void __launch_bounds__(512, 1) gom_group_kernel(const GomArgs a) {
     }
   }
   const bool float_parts = a.part != nullptr;
-  if (tw == 1) {
-    // warp teams: combine the CTA's teams in fixed order (deterministic)
+  if (teams_per_cta > 1) {
+    // several teams per CTA: combine them in fixed order (deterministic)
     double* sacc = reinterpret_cast<double*>(smem);
     int32_t* sham = reinterpret_cast<int32_t*>(sacc + (size_t)teams_per_cta * Wp * 32u);
 #pragma unroll
     for (int j = 0; j < WPT; ++j) {
-      const uint32_t s = (uint32_t)j * 32u + lane;
+      const uint32_t s = (wit + tw * (uint32_t)j) * 32u + lane;
       sacc[(size_t)team * Wp * 32u + s] = (double)acc[j];
       sham[(size_t)team * Wp * 32u + s] = hacc[j];
     }
@@ -659,7 +705,7 @@ __global__ void __launch_bounds__(512, 1) gom_group_kernel(const GomArgs a) {
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  epilogue_body(a.epi);
+  epilogue_body(epi);
   if (threadIdx.x == 0) a.ctl->done = 0;
   if (a.fuse_refresh) {
     refresh_body(a.ref, threadIdx.x >> 5, blockDim.x >> 5);
@@ -682,6 +728,40 @@ __global__ void begin_call_kernel(const BeginArgs b) {
   c->run_steps = c->run_calls = c->groups_run = 0;
   c->n_impr = 0;
   c->done = 0;
+  c->cur_gen = b.gen;
+  c->gen_counter = b.gen + 1;
+}
+
+constexpr uint32_t kTagOrder = 0x4F524400u;  // "ORD"
+
+// Graph path: reset the per-call block and draw this generation's group
+// order (Fisher-Yates, engine_parallel.hpp:291) from the counter-based stream.
+__global__ void begin_generation_kernel(const BeginArgs b, const OrderArgs o) {
+  DevCtl* c = b.ctl;
+  c->stop = 0;
+  c->stop_reason = GOMIX_STOP_NONE;
+  c->has_budget = b.has_budget;
+  c->has_target = b.has_target;
+  c->exact = b.exact;
+  c->max_evals = b.max_evals;
+  c->q = b.q;
+  c->target = b.target;
+  c->calls_total = b.calls_before;
+  c->grp_steps = c->grp_calls = 0;
+  c->run_steps = c->run_calls = c->groups_run = 0;
+  c->n_impr = 0;
+  c->done = 0;
+  const uint32_t gen = c->gen_counter++;
+  c->cur_gen = gen;
+  const uint2 key = make_uint2((uint32_t)o.seed, (uint32_t)(o.seed >> 32));
+  for (uint32_t i = 0; i < o.k; ++i) o.order[i] = i;
+  for (uint32_t i = o.k; i > 1; --i) {
+    const uint4 r = philox4x32_10(make_uint4(i, gen, 0u, kTagOrder), key);
+    const uint32_t j = bounded(lo64(r), i);
+    const uint32_t t = o.order[i - 1];
+    o.order[i - 1] = o.order[j];
+    o.order[j] = t;
+  }
 }
 
 // After init_population (engine_parallel.hpp:331-346): one add_evaluator_calls(q)
@@ -838,11 +918,15 @@ int grid_for(uint64_t work, int block, uint64_t cap) {
 }
 }  // namespace
 
-void launch_gom(const GomArgs& a, bool univariate, bool i32, int wpt, int grid, int block,
-                size_t smem, cudaStream_t s) {
+void prepare_gom(bool univariate, bool i32, int wpt, size_t smem) {
   void* fn = gom_kernel(univariate, i32, wpt);
   if (smem > 48 * 1024)
     GOMIX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+}
+
+void launch_gom(const GomArgs& a, bool univariate, bool i32, int wpt, int grid, int block,
+                size_t smem, cudaStream_t s) {
+  void* fn = gom_kernel(univariate, i32, wpt);
   void* args[] = {(void*)&a};
   GOMIX_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(block), args, smem, s));
 }
@@ -858,6 +942,11 @@ int gom_max_blocks_per_sm(bool univariate, bool i32, int wpt, int block, size_t 
 
 void launch_begin(const BeginArgs& b, cudaStream_t s) {
   begin_call_kernel<<<1, 1, 0, s>>>(b);
+  GOMIX_CUDA(cudaGetLastError());
+}
+
+void launch_order(const BeginArgs& b, const OrderArgs& o, cudaStream_t s) {
+  begin_generation_kernel<<<1, 1, 0, s>>>(b, o);
   GOMIX_CUDA(cudaGetLastError());
 }
 

@@ -54,6 +54,15 @@ struct DevCtl {
   unsigned long long run_steps, run_calls, groups_run;
   unsigned long long n_impr;
   unsigned int done;  // last-CTA-done ticket of the GOM kernel
+  unsigned int gen_counter;  // device-side generation counter (graph path)
+  unsigned int cur_gen;
+};
+
+// One colour group as the device sees it (graph path: kernels look their
+// group up through the per-generation order array).
+struct GroupDesc {
+  uint32_t g0;  // offset of the group's members in gsets / gvars
+  uint32_t G;   // member count
 };
 
 struct Problem {
@@ -144,6 +153,16 @@ struct GomArgs {
   EpiArgs epi;         // run by the last CTA
   RefreshArgs ref;
   int32_t fuse_refresh;
+  int32_t slot;                 // >= 0: group = order[slot] (graph path)
+  const uint32_t* order;
+  const GroupDesc* groups;
+};
+
+struct OrderArgs {
+  DevCtl* ctl;
+  uint32_t* order;
+  uint32_t k;
+  uint64_t seed;
 };
 
 constexpr int32_t kNoForce = -1000;
@@ -155,6 +174,7 @@ struct BeginArgs {
   int32_t has_budget, has_target, exact;
   double max_evals, q, target;
   unsigned long long calls_before;
+  uint32_t gen;  // host generation (direct path keeps the device counter in step)
 };
 
 // -------------------------------------------------------------------------
@@ -223,6 +243,8 @@ void launch_gom(const GomArgs& a, bool univariate, bool i32, int wpt, int grid, 
                 size_t smem, cudaStream_t s);
 int gom_max_blocks_per_sm(bool univariate, bool i32, int wpt, int block, size_t smem);
 void launch_begin(const BeginArgs& b, cudaStream_t s);
+void launch_order(const BeginArgs& b, const OrderArgs& o, cudaStream_t s);
+void prepare_gom(bool univariate, bool i32, int wpt, size_t smem);
 void launch_init_epilogue(const EpiArgs& a, cudaStream_t s);
 void launch_refresh(const RefreshArgs& a, int grid, cudaStream_t s);
 void launch_philox_init(uint32_t* pop, uint64_t nv, uint32_t n, uint32_t Wp, uint64_t seed,

@@ -397,6 +397,9 @@ class GpuParallelEngine:
         check(lib().gomix_gpu_kernel_times(self.h, buf.ctypes.data, cnt.value, C.byref(cnt)))
         return buf[:cnt.value]
 
+    def set_timing(self, enable: bool):
+        check(lib().gomix_gpu_set_timing(self.h, int(bool(enable))))
+
     def launch_count(self) -> int:
         c = C.c_uint64()
         check(lib().gomix_gpu_launch_count(self.h, C.byref(c)))
