@@ -158,6 +158,8 @@ std::unique_ptr<Problem> create_problem(const gomix_maxcut* inst, const gomix_fo
   }
   // int32 per-pair arithmetic is exact when |delta| <= max|w| * footprint < 2^30
   P->i32 = exact && maxw * (double)std::max<uint64_t>(max_deg_sum, 1) < 1073741824.0;
+  P->wbits = 1;
+  while (P->i32 && P->wbits < 31 && (double)(1u << P->wbits) <= maxw) ++P->wbits;
   if (P->univariate) {
     for (uint64_t i = 0; i < m; ++i) {
       const uint32_t v = P->h_set_vars[i];
@@ -514,6 +516,8 @@ struct gomix_gpu_engine {
     a.fp = P->fp;
     a.gsets = P->gsets + g0;
     a.gvars = P->gvars ? P->gvars + g0 : nullptr;
+    a.gmeta = P->gmeta ? P->gmeta + g0 : nullptr;
+    a.wbits = P->wbits;
     a.G = (uint32_t)G;
     a.pop = pop;
     a.fit = fit;

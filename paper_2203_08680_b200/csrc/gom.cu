@@ -83,6 +83,19 @@ __device__ __forceinline__ uint32_t differ_word(const uint32_t* rowsF, uint32_t 
   return dw & valid_mask(w2, n);
 }
 
+// 32x32 bit-matrix transpose across a warp: lane r holds row r on entry;
+// on exit lane c holds column c (bit r = bit c of the old row r).
+__device__ __forceinline__ uint32_t transpose32(uint32_t x, uint32_t lane) {
+  constexpr uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+  for (int st = 0; st < 5; ++st) {
+    const uint32_t j = 16u >> st, m = masks[st];
+    const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x, j);
+    x = (lane & j) ? ((x & ~m) | ((y & ~m) >> j)) : ((x & m) | ((y & m) << j));
+  }
+  return x;
+}
+
 // Position of the k-th (0-based) set bit of x; k < popc(x).
 __device__ __forceinline__ uint32_t select_bit(uint32_t x, uint32_t k) {
   uint32_t pos = 0;
@@ -292,6 +305,7 @@ __global__ void __launch_bounds__(512, 1) gom_group_kernel(const GomArgs a) {
   uint32_t G = a.G, generation = a.generation;
   const uint32_t* gsets = a.gsets;
   const uint32_t* gvars = a.gvars;
+  const uint4* gmeta = a.gmeta;
   EpiArgs epi = a.epi;
   if (a.slot >= 0) {  // graph path: this launch's group comes from the device-side order
     const uint32_t gi = a.order[a.slot];
@@ -299,6 +313,7 @@ __global__ void __launch_bounds__(512, 1) gom_group_kernel(const GomArgs a) {
     G = d.G;
     gsets += d.g0;
     if (gvars) gvars += d.g0;
+    if (gmeta) gmeta += d.g0;
     generation = *(volatile unsigned int*)&a.ctl->cur_gen;
     epi.group = gi;
     epi.G = G;
@@ -425,10 +440,11 @@ __global__ void __launch_bounds__(512, 1) gom_group_kernel(const GomArgs a) {
       // rows at group start (the donor pool, engine_parallel.hpp:100-103),
       // every solution's pattern on F (so a donor test is one load), the
       // donor-inserted rows and the committed rows.
-      const uint32_t sid = gsets[p];
-      const int64_t f0 = a.set_off[sid];
-      const uint32_t f = (uint32_t)(a.set_off[sid + 1] - f0);
-      const uint32_t* vars = a.set_vars + f0;
+      const uint4 gm = gmeta[p];
+      const uint32_t sid = gm.x;
+      const uint32_t f = gm.w >> 24;
+      const uint32_t* vars = a.set_vars + gm.y;
+      const uint32_t e0 = gm.z, e1 = gm.z + (gm.w & 0xFFFFFFu);
       uint64_t* patt = reinterpret_cast<uint64_t*>(stage);
       uint32_t* rowsF = stage + 64u * Wp;
       uint32_t* newD = rowsF + f * Wp;
@@ -436,6 +452,23 @@ __global__ void __launch_bounds__(512, 1) gom_group_kernel(const GomArgs a) {
       for (uint32_t idx = tid_team; idx < f * Wp; idx += team_threads) {
         const uint32_t jv = idx / Wp, w = idx - jv * Wp;
         rowsF[idx] = a.pop[(size_t)vars[jv] * Wp + w];
+      }
+      // first footprint chunk: entry per lane and its outside row, fetched
+      // now so the loads overlap the staging above
+      FpEntry E0;
+      uint32_t xw0[WPT];
+      {
+        const uint32_t e = e0 + lane;
+        if (e < e1) {
+          E0 = a.fp[e];
+        } else {
+          E0.a = kInSet;
+          E0.b = kInSet;
+          E0.w = 0.0;
+        }
+        const uint32_t ext = !(E0.a & kInSet) ? E0.a : (!(E0.b & kInSet) ? E0.b : vars[0]);
+#pragma unroll
+        for (int j = 0; j < WPT; ++j) xw0[j] = a.pop[(size_t)ext * Wp + wit + tw * j];
       }
       uint64_t em;  // elitist genotype on F
       {
@@ -530,9 +563,7 @@ __global__ void __launch_bounds__(512, 1) gom_group_kernel(const GomArgs a) {
       }
       team_sync(tw, teams_per_cta, team);
 
-      // phase 2: footprint sums on whole row words, ascending edge id
-      // (engine_parallel.hpp:164-173); entries and outside rows prefetched by
-      // the lanes and broadcast with shuffles.
+      // phase 2: footprint sums, ascending edge id (engine_parallel.hpp:164-173)
       int32_t di[WPT];
       double sn[WPT], so[WPT];
 #pragma unroll
@@ -541,50 +572,70 @@ __global__ void __launch_bounds__(512, 1) gom_group_kernel(const GomArgs a) {
         sn[j] = 0.0;
         so[j] = 0.0;
       }
-      const int64_t e0 = a.fp_off[sid], e1 = a.fp_off[sid + 1];
-      for (int64_t base = e0; base < e1; base += 32) {
-        const int64_t e = base + lane;
-        const bool has = e < e1;
+      for (uint32_t base = e0; base < e1; base += 32) {
         FpEntry E;
-        if (has) {
-          E = a.fp[e];
-        } else {
-          E.a = kInSet;
-          E.b = kInSet;
-          E.w = 0.0;
-        }
-        const uint32_t ext = !(E.a & kInSet) ? E.a : (!(E.b & kInSet) ? E.b : vars[0]);
         uint32_t xw[WPT];
+        if (base == e0) {
+          E = E0;
 #pragma unroll
-        for (int j = 0; j < WPT; ++j) xw[j] = a.pop[(size_t)ext * Wp + wit + tw * j];
-        const int32_t ewi = (int32_t)E.w;
-        const int cnt = (int)(e1 - base < 32 ? e1 - base : 32);
-        for (int t = 0; t < cnt; ++t) {
-          const uint32_t ca = __shfl_sync(0xFFFFFFFFu, E.a, t);
-          const uint32_t cb = __shfl_sync(0xFFFFFFFFu, E.b, t);
-          const bool ina = ca & kInSet, inb = cb & kInSet;
-          const uint32_t ja = (ca & ~kInSet) * Wp, jb = (cb & ~kInSet) * Wp;
-          int32_t wti = 0;
-          double wt = 0.0;
-          if constexpr (I32) wti = __shfl_sync(0xFFFFFFFFu, ewi, t);
-          else wt = shfl_d(E.w, t);
+          for (int j = 0; j < WPT; ++j) xw[j] = xw0[j];
+        } else {
+          const uint32_t e = base + lane;
+          if (e < e1) {
+            E = a.fp[e];
+          } else {
+            E.a = kInSet;
+            E.b = kInSet;
+            E.w = 0.0;
+          }
+          const uint32_t ext = !(E.a & kInSet) ? E.a : (!(E.b & kInSet) ? E.b : vars[0]);
+#pragma unroll
+          for (int j = 0; j < WPT; ++j) xw[j] = a.pop[(size_t)ext * Wp + wit + tw * j];
+        }
+        const bool ina = E.a & kInSet, inb = E.b & kInSet;
+        const uint32_t ja = (E.a & ~kInSet) * Wp, jb = (E.b & ~kInSet) * Wp;
+        if constexpr (I32) {
+          // lane t = entry t: old / new cut words for 32 solutions at once,
+          // transposed so lane s holds its solution's entry masks, then delta
+          // = weighted popcounts over the weight bit-planes (exact integers).
+          const int32_t wt = (int32_t)E.w;
+          const uint32_t aw = wt < 0 ? (uint32_t)(-wt) : (uint32_t)wt;
 #pragma unroll
           for (int j = 0; j < WPT; ++j) {
             const uint32_t w = wit + tw * j;
-            const uint32_t xo = (ina && inb) ? 0u : __shfl_sync(0xFFFFFFFFu, xw[j], t);
-            const uint32_t aO = ina ? rowsF[ja + w] : xo, aN = ina ? newD[ja + w] : xo;
-            const uint32_t bO = inb ? rowsF[jb + w] : xo, bN = inb ? newD[jb + w] : xo;
-            const uint32_t co = ((aO ^ bO) >> lane) & 1u, cn = ((aN ^ bN) >> lane) & 1u;
-            if constexpr (I32) {
-              di[j] += ((int32_t)cn - (int32_t)co) * wti;
-            } else {
-              sn[j] += cn ? wt : 0.0;
-              so[j] += co ? wt : 0.0;
+            const uint32_t aO = ina ? rowsF[ja + w] : xw[j], aN = ina ? newD[ja + w] : xw[j];
+            const uint32_t bO = inb ? rowsF[jb + w] : xw[j], bN = inb ? newD[jb + w] : xw[j];
+            const uint32_t mo = transpose32((aO ^ bO) & (E.w != 0.0 ? 0xFFFFFFFFu : 0u), lane);
+            const uint32_t mn = transpose32((aN ^ bN) & (E.w != 0.0 ? 0xFFFFFFFFu : 0u), lane);
+            int32_t d = 0;
+            for (uint32_t k = 0; k < a.wbits; ++k) {
+              const uint32_t bp = __ballot_sync(0xFFFFFFFFu, wt > 0 && ((aw >> k) & 1u));
+              const uint32_t bn = __ballot_sync(0xFFFFFFFFu, wt < 0 && ((aw >> k) & 1u));
+              d += ((int32_t)(__popc(mn & bp) - __popc(mo & bp)) - (int32_t)(__popc(mn & bn) - __popc(mo & bn))) << k;
+            }
+            di[j] += d;
+          }
+        } else {
+          const int cnt = (int)(e1 - base < 32 ? e1 - base : 32);
+          for (int t = 0; t < cnt; ++t) {
+            const uint32_t ca = __shfl_sync(0xFFFFFFFFu, E.a, t);
+            const uint32_t cb = __shfl_sync(0xFFFFFFFFu, E.b, t);
+            const bool ina_t = ca & kInSet, inb_t = cb & kInSet;
+            const uint32_t ja_t = (ca & ~kInSet) * Wp, jb_t = (cb & ~kInSet) * Wp;
+            const double wt = shfl_d(E.w, t);
+#pragma unroll
+            for (int j = 0; j < WPT; ++j) {
+              const uint32_t w = wit + tw * j;
+              const uint32_t xo = (ina_t && inb_t) ? 0u : __shfl_sync(0xFFFFFFFFu, xw[j], t);
+              const uint32_t aO = ina_t ? rowsF[ja_t + w] : xo, aN = ina_t ? newD[ja_t + w] : xo;
+              const uint32_t bO = inb_t ? rowsF[jb_t + w] : xo, bN = inb_t ? newD[jb_t + w] : xo;
+              sn[j] += (((aN ^ bN) >> lane) & 1u) ? wt : 0.0;
+              so[j] += (((aO ^ bO) >> lane) & 1u) ? wt : 0.0;
             }
           }
         }
       }
-      const uint32_t fpl = (uint32_t)(e1 - e0);
+      const uint32_t fpl = e1 - e0;
 
       // phases 3 + 4
 #pragma unroll

@@ -87,6 +87,8 @@ struct Problem {
   uint32_t* set_vars = nullptr;
   uint32_t* gsets = nullptr;
   uint32_t* gvars = nullptr;
+  uint4* gmeta = nullptr;
+  uint32_t wbits = 1;
   int64_t* fp_off = nullptr;
   FpEntry* fp = nullptr;
   std::vector<void*> allocations;
@@ -132,6 +134,8 @@ struct GomArgs {
   const FpEntry* fp;
   const uint32_t* gsets;  // this group's members (ascending set ids)
   const uint32_t* gvars;  // singleton FOS: the variable of each member
+  const uint4* gmeta;     // general FOS: {set id, vars offset, footprint offset, f << 24 | footprint}
+  uint32_t wbits;         // bit-planes of max |w| (integer path)
   uint32_t G;             // |G|
   uint32_t* pop;
   const double* fit;

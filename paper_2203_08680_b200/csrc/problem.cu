@@ -443,6 +443,18 @@ void build_problem_device_impl(Problem& P, const int32_t* given_colour, const in
       P.footprint[i] = (uint64_t)(h_fp_off[i + 1] - h_fp_off[i]);
       P.max_fp = std::max(P.max_fp, P.footprint[i]);
     }
+    if ((uint64_t)h_fp_off[m] >= (1ull << 32) || P.h_set_off[m] >= (1ull << 32) || P.max_fp >= (1u << 24))
+      invalid("fos: footprint plans exceed 32-bit offsets");
+    // per group position: {set id, vars offset, footprint offset, f << 24 | footprint}
+    std::vector<uint4> gm(m);
+    for (uint64_t i = 0; i < m; ++i) {
+      const uint64_t sid = P.group_sets[i];
+      const uint64_t f = P.h_set_off[sid + 1] - P.h_set_off[sid];
+      gm[i] = make_uint4((uint32_t)sid, (uint32_t)P.h_set_off[sid], (uint32_t)h_fp_off[sid],
+                         (uint32_t)((f << 24) | P.footprint[sid]));
+    }
+    P.gmeta = dev_alloc<uint4>(P.allocations, m);
+    GOMIX_CUDA(cudaMemcpy(P.gmeta, gm.data(), m * sizeof(uint4), cudaMemcpyHostToDevice));
   }
   GOMIX_CUDA(cudaDeviceSynchronize());
 }
