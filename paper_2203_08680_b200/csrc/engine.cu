@@ -302,11 +302,12 @@ struct gomix_gpu_engine {
       if (Wp > 1 && avg_group * Wp <= (uint64_t)sms * 32) {
         wpt = 1;
         tw = Wp;
+        block = 32 * tw;  // one team per CTA: the whole group fits in one wave
       } else {
         wpt = Wp;
         tw = 1;
+        block = 256;
       }
-      block = 256;
     } else if (W <= 32) {
       Wp = next_pow2(W);
       wpt = 4;

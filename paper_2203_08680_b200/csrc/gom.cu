@@ -19,6 +19,8 @@
 
 namespace gomix_b200 {
 
+constexpr uint32_t kEpiSmemFit = 1024;  // fitness values the epilogue keeps in shared memory
+
 // ---------------------------------------------------------------------------
 // Philox4x32-10 (Salmon et al., SC'11), counter-based: every (generation, set,
 // solution, call) has its own counter, so draws need no state and no order.
@@ -143,6 +145,7 @@ __device__ void epilogue_body(const EpiArgs& a) {
   const uint32_t n = a.n;
   __shared__ double s_chunkmax[32];
   __shared__ int32_t s_best;
+  __shared__ double s_fit[kEpiSmemFit];  // this group's fitness, scanned without global loads
   for (uint32_t s = threadIdx.x; s < n; s += blockDim.x) {
     double f = a.fit[s];
     if (a.mode == 2) {
@@ -157,10 +160,10 @@ __device__ void epilogue_body(const EpiArgs& a) {
       a.dfit[s] = 0.0;
     }
     a.fit[s] = f;
+    if (s < kEpiSmemFit) s_fit[s] = f;
     a.ham[s] += a.dham[s];
     a.dham[s] = 0;
   }
-  __syncthreads();
   if (threadIdx.x == 0) {
     const unsigned long long st = c->grp_steps, ca = c->grp_calls;
     c->grp_steps = 0;
@@ -175,35 +178,49 @@ __device__ void epilogue_body(const EpiArgs& a) {
       request_stop(c, GOMIX_STOP_BUDGET);
     s_best = -1;
   }
+  __syncthreads();
   // chunk maxima let the serial scan skip chunks that cannot hold a record
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u, nwarps = blockDim.x >> 5;
-  for (uint32_t chunk = warp; chunk * 32u < n; chunk += nwarps) {
+  auto fit_at = [&](uint32_t s) { return s < kEpiSmemFit ? s_fit[s] : a.fit[s]; };
+  for (uint32_t chunk = warp; chunk * 32u < n && chunk < 32; chunk += nwarps) {
     const uint32_t s = chunk * 32u + lane;
-    double f = s < n ? a.fit[s] : -INFINITY;
+    double f = s < n ? fit_at(s) : -INFINITY;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) f = fmax(f, __shfl_xor_sync(0xFFFFFFFFu, f, o));
-    if (lane == 0 && chunk < 32) s_chunkmax[chunk] = f;
+    if (lane == 0) s_chunkmax[chunk] = f;
   }
   __syncthreads();
   if (warp == 0) {
     const bool exact = c->exact != 0;
+    const int32_t has_target = c->has_target;
+    const double target = c->target;
+    unsigned long long ni = c->n_impr;
+    const unsigned long long calls_now = c->calls_total;
     double cur = c->elit_fit;
     int32_t best = -1;
+    bool hit = false;
     for (uint32_t base = 0; base < n; base += 32u) {
       const uint32_t chunk = base >> 5;
       if (chunk < 32 && !(s_chunkmax[chunk] > cur)) continue;  // better() implies >
       const uint32_t s = base + lane;
-      const double f = s < n ? a.fit[s] : -INFINITY;
+      const double f = s < n ? fit_at(s) : -INFINITY;
       uint32_t m = __ballot_sync(0xFFFFFFFFu, s < n && cmp_better(exact, f, cur));
       while (m) {
         const uint32_t l = __ffs(m) - 1;
         cur = __shfl_sync(0xFFFFFFFFu, f, l);
         best = (int32_t)(base + l);
-        if (lane == 0) note_improvement(a, cur);
+        if (lane == 0 && ni < a.impr_cap) {
+          a.impr[ni] = cur;
+          a.impr_calls[ni] = calls_now;
+        }
+        ++ni;
+        hit |= has_target && (cmp_better(exact, cur, target) || cmp_equal(exact, cur, target));
         m = __ballot_sync(0xFFFFFFFFu, s < n && lane > l && cmp_better(exact, f, cur));
       }
     }
     if (lane == 0) {
+      c->n_impr = ni;
+      if (hit) request_stop(c, GOMIX_STOP_TARGET);
       c->elit_src = best;
       if (best >= 0) c->elit_fit = cur;
       s_best = best;
