@@ -322,6 +322,7 @@ struct gomix_gpu_engine {
       invalid("engine: population sizes above 4096 are not supported");
     }
     teams = block / 32 / tw;
+    if (tw > 1 && teams != 1) invalid("engine: internal team layout error");
     if (!P->univariate) {
       stage_words = (uint32_t)(3 * P->max_f * Wp + 64 * Wp);  // rows, donor rows, new rows, patterns
       stage_words += stage_words & 1u;                         // keep patterns 8-byte aligned

@@ -19,7 +19,7 @@
 
 namespace gomix_b200 {
 
-constexpr uint32_t kEpiSmemFit = 1024;  // fitness values the epilogue keeps in shared memory
+constexpr uint32_t kEpiSmemFit = 256;  // fitness values the epilogue keeps in shared memory
 
 // ---------------------------------------------------------------------------
 // Philox4x32-10 (Salmon et al., SC'11), counter-based: every (generation, set,
@@ -65,15 +65,14 @@ __device__ __forceinline__ uint32_t valid_mask(uint32_t w, uint32_t n) {
   return (1u << (n - lo)) - 1u;
 }
 
-// Teams of tw warps; several teams per CTA synchronise on their own named
-// barrier (ids 1..8, 0 is __syncthreads).
-__device__ __forceinline__ void team_sync(uint32_t tw, uint32_t teams_per_cta, uint32_t team) {
+// A team is one warp (several per CTA) or a whole CTA (tw > 1); the host
+// never builds multi-warp teams that share a CTA, so no named barriers are
+// needed (dynamic barrier ids would reserve all 16 and cap CTAs per SM).
+__device__ __forceinline__ void team_sync(uint32_t tw, uint32_t, uint32_t) {
   if (tw == 1)
     __syncwarp();
-  else if (teams_per_cta == 1)
-    __syncthreads();
   else
-    asm volatile("bar.sync %0, %1;" ::"r"(team + 1), "r"(tw * 32) : "memory");
+    __syncthreads();
 }
 
 // Members of word w2 that differ from pattern m somewhere on F.
