@@ -119,7 +119,7 @@ class GpuParallelEngine final : public GenerationRunner {
                             g.w.data()};
     const gomix_fos fos{model_->fos.sets.size(), off.data(), vars.data()};
     shared_ = shared_problem(inst, fos, colour.empty() ? nullptr : colour.data());
-    gomix_gpu_problem_info info{};
+    gomix_problem_info info{};
     gpu_detail::check(gomix_gpu_problem_info(shared_.get(), &info));
     k_ = info.num_groups;
     gomix_engine_config ec{};
