@@ -96,9 +96,10 @@ class GpuParallelEngine final : public GenerationRunner {
       throw std::invalid_argument("engine: population must be non-empty");
     if (cfg_.model.kind != LinkageKind::fixed_tree)
       throw std::invalid_argument("batch engine: needs a model that is fixed for the whole run");
-    // same adoption rule as ParallelEngine (engine_parallel.hpp:271-274); the
-    // colouring itself is recomputed on the GPU when no groups are given
-    if (cfg_.fixed_model)
+    // same adoption rule as ParallelEngine (engine_parallel.hpp:271-274): a
+    // model with groups is adopted, otherwise the FOS is rebuilt from the
+    // config; the colouring of a rebuilt model is computed on the GPU
+    if (cfg_.fixed_model && !cfg_.fixed_model->groups.groups.empty())
       model_ = cfg_.fixed_model;
     else
       model_ = build_fixed_model(problem_, cfg_.model, false);

@@ -303,7 +303,9 @@ __device__ __forceinline__ double shfl_d(double x, int src) {
 // elitist refresh), so a group is one launch.
 // ---------------------------------------------------------------------------
 template <int WPT, bool UNIV, bool I32>
-__global__ void __launch_bounds__(512, 1) gom_group_kernel(const GomArgs a) {
+// univariate launches with WPT <= 4 always use <= 256 threads: allow 3 CTAs/SM
+__global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <= 4) ? 3 : 1)
+    gom_group_kernel(const GomArgs a) {
   extern __shared__ __align__(16) uint32_t smem[];
   if (*(volatile int32_t*)&a.ctl->stop) return;
 
@@ -314,7 +316,7 @@ __global__ void __launch_bounds__(512, 1) gom_group_kernel(const GomArgs a) {
   const uint32_t team = warp / tw, wit = warp - team * tw;
   const uint32_t tid_team = wit * 32u + lane, team_threads = tw * 32u;
   const uint32_t Wp = a.Wp, n = a.n;
-  const bool exact = a.exact != 0;
+  const bool exact = I32 || a.exact != 0;  // integer-weight instances only take the I32 path
   const bool replay = a.tape != nullptr;
   const bool record = a.rec_present != nullptr;
   uint32_t* stage = smem + (size_t)team * a.stage_words;
@@ -335,6 +337,16 @@ __global__ void __launch_bounds__(512, 1) gom_group_kernel(const GomArgs a) {
     epi.G = G;
   }
 
+  // group-start state of this thread's solutions: "parent == elitist"
+  // (engine_parallel.hpp:202) and the parent fitness, read once per launch
+  bool is_elit[WPT];
+  double pfit[WPT];
+#pragma unroll
+  for (int j = 0; j < WPT; ++j) {
+    const uint32_t s = (wit + tw * (uint32_t)j) * 32u + lane;
+    is_elit[j] = s < n && a.ham[s] == 0;
+    pfit[j] = (!exact && s < n) ? a.fit[s] : 0.0;
+  }
   Acc acc[WPT];
   int32_t hacc[WPT];
 #pragma unroll
@@ -426,11 +438,11 @@ __global__ void __launch_bounds__(512, 1) gom_group_kernel(const GomArgs a) {
         const double delta = I32 ? (double)di[j] : sn[j] - so[j];
         bool accept = false;
         if (present) {
-          const bool elit = a.ham[s] == 0;
+          const bool elit = is_elit[j];
           if (exact) {
             accept = delta > 0.0 || (delta == 0.0 && !elit);
           } else {
-            const double pf = a.fit[s];
+            const double pf = pfit[j];
             const double cand = pf + delta;
             accept = cmp_better(false, cand, pf) || (cmp_equal(false, cand, pf) && !elit);
           }
@@ -662,11 +674,11 @@ __global__ void __launch_bounds__(512, 1) gom_group_kernel(const GomArgs a) {
         const double delta = (e1 == e0) ? 0.0 : (I32 ? (double)di[j] : sn[j] - so[j]);
         bool accept = false;
         if (present[j]) {
-          const bool elit = a.ham[s] == 0;
+          const bool elit = is_elit[j];
           if (exact) {
             accept = delta > 0.0 || (delta == 0.0 && !elit);
           } else {
-            const double pf = a.fit[s];
+            const double pf = pfit[j];
             const double cand = pf + delta;
             accept = cmp_better(false, cand, pf) || (cmp_equal(false, cand, pf) && !elit);
           }

@@ -5,6 +5,7 @@
 // build container and shipped as a binary); run by tests/test_cpp_adapter.py.
 #include <cstdio>
 #include <cstdlib>
+#include <optional>
 #include <string>
 #include <vector>
 
@@ -55,7 +56,7 @@ std::shared_ptr<ModelArtifacts> univariate_model(const GrayBoxProblem& problem) 
 }
 
 void engine_lockstep(const char* name, const MaxCutInstance& inst, std::shared_ptr<ModelArtifacts> model,
-                     std::size_t n, std::uint64_t seed, int gens) {
+                     std::size_t n, std::uint64_t seed, int gens, std::optional<std::size_t> bound = {}) {
   const GrayBoxProblem problem = as_graybox(inst);
   Log la, lb;
   RunContext ca({}, problem.comparator(), problem.num_subfunctions(), &la);
@@ -65,6 +66,7 @@ void engine_lockstep(const char* name, const MaxCutInstance& inst, std::shared_p
   cfg.seed = seed;
   cfg.workers = 2;
   cfg.fixed_model = model;
+  cfg.model.bound = bound;
   ParallelEngine ref(problem, cfg, ca);
   GpuParallelEngine gpu(problem, cfg, cb);
   bool pop_ok = true, elit_ok = true, calls_ok = true;
@@ -134,10 +136,11 @@ int main() {
     engine_lockstep("C1 torus 10x10, n=32", c1, univariate_model(as_graybox(c1)), 32, 1, 20);
     const MaxCutInstance pm = generate_torus(12, 9, WeightSpec{WeightSpec::Kind::uniform_int, -5, 5}, 4);
     engine_lockstep("+-5 torus 12x9, n=48", pm, univariate_model(as_graybox(pm)), 48, 9, 15);
-    {  // adopted model without groups: coloured on the GPU (engine_parallel.hpp:271-274)
+    {  // groupless model: rebuilt from the config (bflt:10 UPGMA) like the
+       // reference (engine_parallel.hpp:271-274), coloured on the GPU
       auto m = univariate_model(as_graybox(c1));
       m->groups.groups.clear();
-      engine_lockstep("GPU-coloured model, n=40", c1, m, 40, 3, 10);
+      engine_lockstep("groupless model -> rebuilt bflt:10, GPU-coloured, n=40", c1, m, 40, 3, 10, 10);
     }
     TerminationConfig budget;
     budget.max_evaluations = 4000.0;
