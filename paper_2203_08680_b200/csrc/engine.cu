@@ -225,8 +225,11 @@ struct gomix_gpu_engine {
   double* fit = nullptr;
   double* dfit = nullptr;
   double* part = nullptr;
-  int32_t* ham = nullptr;
-  int32_t* dham = nullptr;
+  unsigned long long* h1 = nullptr;  // per-solution Zobrist hashes
+  unsigned long long* h2 = nullptr;
+  unsigned long long* dh1 = nullptr;
+  unsigned long long* dh2 = nullptr;
+  uint32_t* ever = nullptr;  // per-row elitist snapshot version
   uint32_t* elit = nullptr;
   DevCtl* ctl = nullptr;
   DevCtl* h_ctl = nullptr;  // pinned
@@ -324,11 +327,12 @@ struct gomix_gpu_engine {
     teams = block / 32 / tw;
     if (tw > 1 && teams != 1) invalid("engine: internal team layout error");
     if (!P->univariate) {
-      stage_words = (uint32_t)(3 * P->max_f * Wp + 64 * Wp);  // rows, donor rows, new rows, patterns
-      stage_words += stage_words & 1u;                         // keep patterns 8-byte aligned
+      // patterns (64-bit per member), F rows, donor rows, new rows, Zobrist keys of F
+      stage_words = (uint32_t)(64 * Wp + 3 * P->max_f * Wp + 1 + 4 * P->max_f);
+      stage_words += stage_words & 1u;  // keep the next team's patterns 8-byte aligned
     }
     const size_t stage = (size_t)teams * stage_words * 4;
-    const size_t red = teams > 1 ? (size_t)teams * Wp * 32 * 12 : 0;
+    const size_t red = teams > 1 ? (size_t)teams * Wp * 32 * 24 : 0;  // fitness + 2 hash deltas
     smem = std::max(stage, red);
     if (smem > 227 * 1024) invalid("engine: set size x population too large for shared-memory staging");
     record = (flags & GOMIX_FLAG_RECORD_BATCH) != 0;
@@ -348,8 +352,11 @@ struct gomix_gpu_engine {
     pop = dev_alloc<uint32_t>(allocs, nv * Wp);
     fit = dev_alloc<double>(allocs, n);
     dfit = dev_alloc<double>(allocs, n);
-    ham = dev_alloc<int32_t>(allocs, n);
-    dham = dev_alloc<int32_t>(allocs, n);
+    h1 = dev_alloc<unsigned long long>(allocs, n);
+    h2 = dev_alloc<unsigned long long>(allocs, n);
+    dh1 = dev_alloc<unsigned long long>(allocs, n);
+    dh2 = dev_alloc<unsigned long long>(allocs, n);
+    ever = dev_alloc<uint32_t>(allocs, nv);
     elit = dev_alloc<uint32_t>(allocs, (nv + 31) / 32);
     ctl = dev_alloc<DevCtl>(allocs, 1);
     gsteps = dev_alloc<unsigned long long>(allocs, P->k);
@@ -385,7 +392,10 @@ struct gomix_gpu_engine {
     GOMIX_CUDA(cudaMemset(gsteps, 0, P->k * 8));
     GOMIX_CUDA(cudaMemset(gcalls, 0, P->k * 8));
     GOMIX_CUDA(cudaMemset(dfit, 0, n * 8));
-    GOMIX_CUDA(cudaMemset(dham, 0, n * 4));
+    GOMIX_CUDA(cudaMemset(dh1, 0, n * 8));
+    GOMIX_CUDA(cudaMemset(dh2, 0, n * 8));
+    GOMIX_CUDA(cudaMemset(ever, 0, nv * 4));
+    GOMIX_CUDA(cudaMemset(elit, 0, ((nv + 31) / 32) * 4));
   }
 
   // ---- per-call control ------------------------------------------------------
@@ -409,7 +419,7 @@ struct gomix_gpu_engine {
   }
 
   // One CUDA graph per engine for a whole Philox generation: the order
-  // kernel, then k (GOM [+ refresh]) launches that find their group through
+  // kernel, then k GOM launches that find their group through
   // the device-side order.  Replaces ~2k launches by one graph launch.
   void launch_generation_graph() {
     if (!graph_exec) {
@@ -453,39 +463,29 @@ struct gomix_gpu_engine {
     out->elitist_fitness = h_ctl->elit_fit;
   }
 
-  RefreshArgs refresh_args() const {
-    RefreshArgs r;
+  SnapArgs snap_args() const {
+    SnapArgs r;
     r.pop = pop;
     r.elit = elit;
-    r.ham = ham;
+    r.ever = ever;
     r.ctl = ctl;
+    r.h1 = h1;
+    r.h2 = h2;
     r.nv = P->nv;
     r.n = (uint32_t)n;
     r.Wp = Wp;
-    r.force_src = kNoForce;
     return r;
   }
-
-  void refresh(int32_t force_src = kNoForce, cudaStream_t st = nullptr) {
-    if (!st) st = stream;
-    RefreshArgs r = refresh_args();
-    r.force_src = force_src;
-    const uint64_t units = ((P->nv + 31) / 32) * Wp;
-    const int grid = (int)std::min<uint64_t>(std::max<uint64_t>(1, (units + 7) / 8), (uint64_t)sms * 8);
-    launch_refresh(r, grid, st);
-    ++launches;
-  }
-
-  // the last CTA of the GOM kernel refreshes small populations itself
-  bool fuse_refresh() const { return P->nv * Wp <= 4096; }
 
   EpiArgs epi_args(uint64_t group, uint32_t G, uint32_t nparts) const {
     EpiArgs e;
     e.fit = fit;
     e.part = part;
     e.dfit = dfit;
-    e.ham = ham;
-    e.dham = dham;
+    e.h1 = h1;
+    e.h2 = h2;
+    e.dh1 = dh1;
+    e.dh2 = dh2;
     e.rec_delta = rec_delta;
     e.rec_accept = rec_accept;
     e.ctl = ctl;
@@ -523,11 +523,14 @@ struct gomix_gpu_engine {
     a.G = (uint32_t)G;
     a.pop = pop;
     a.fit = fit;
-    a.ham = ham;
+    a.h1 = h1;
+    a.h2 = h2;
+    a.ever = ever;
     a.elit = elit;
     a.dfit = epi_mode == 0 ? dfit : nullptr;
     a.part = epi_mode == 1 ? part : nullptr;
-    a.dham = dham;
+    a.dh1 = dh1;
+    a.dh2 = dh2;
     a.ctl = ctl;
     a.tape = with_tape ? tape : nullptr;
     const bool rec = record || epi_mode == 2;
@@ -554,15 +557,12 @@ struct gomix_gpu_engine {
       GOMIX_CUDA(cudaEventRecord(e0, st));
     }
     a.epi = epi_args(group, (uint32_t)G, (uint32_t)grid);
-    a.ref = refresh_args();
-    a.fuse_refresh = fuse_refresh();
     launch_gom(a, P->univariate, P->i32, (int)wpt, grid, (int)block, smem, st);
     ++launches;
     if (e1) {
       GOMIX_CUDA(cudaEventRecord(e1, st));
       ev_pending.push_back({e0, e1});
     }
-    if (!a.fuse_refresh) refresh(kNoForce, st);
     if (slot < 0) last_group = (int64_t)group;
   }
 
@@ -650,11 +650,11 @@ struct gomix_gpu_engine {
       ++launches;
     }
     launch_full_eval(*P, pop, fit, (uint32_t)n, Wp, !P->exact, stream);
-    ++launches;
+    launch_hash_population(snap_args(), stream);
+    launches += 2;
     begin_call(stop);
     launch_init_epilogue(epi_args(0, 0, 0), stream);
     ++launches;
-    refresh();
     read_ctl();
     fill_stats(out);
     initialized = true;
@@ -687,12 +687,6 @@ struct gomix_gpu_engine {
     if (!h_ctl->stop) ++generation;  // engine_parallel.hpp:311-314
   }
 
-  void set_elitist_fitness(double f) {
-    GOMIX_CUDA(cudaStreamSynchronize(stream));  // h_ctl is reused as the staging buffer
-    h_ctl->elit_fit = f;
-    GOMIX_CUDA(cudaMemcpyAsync(ctl, h_ctl, sizeof(double), cudaMemcpyHostToDevice, stream));
-  }
-
   // Enqueue one generation without any host synchronisation (Philox mode,
   // no stop criteria); results are read by synchronize().
   void run_generation_async() {
@@ -719,6 +713,9 @@ struct gomix_gpu_engine {
   void load_population(const uint8_t* genotypes, const double* fitness) {
     if (!initialized) throw GomixError(GOMIX_E_STATE, "load_population: population not initialised");
     const uint64_t nv = P->nv;
+    // the elitist snapshot may still point into the old population: finish it
+    launch_finalize_elitist(snap_args(), stream);
+    ++launches;
     uint8_t* d = nullptr;
     GOMIX_CUDA(cudaMallocAsync(&d, n * nv, stream));
     GOMIX_CUDA(cudaMemcpyAsync(d, genotypes, n * nv, cudaMemcpyHostToDevice, stream));
@@ -731,8 +728,8 @@ struct gomix_gpu_engine {
       launch_full_eval(*P, pop, fit, (uint32_t)n, Wp, !P->exact, stream);
       ++launches;
     }
-    GOMIX_CUDA(cudaMemsetAsync(ham, 0, n * 4, stream));
-    refresh(-2);  // distances to the current elitist bits
+    launch_hash_population(snap_args(), stream);  // hashes of the new members
+    ++launches;
     GOMIX_CUDA(cudaStreamSynchronize(stream));
   }
 
@@ -948,9 +945,11 @@ int gomix_gpu_read_elitist(gomix_gpu_engine* e, uint8_t* genotype, double* fitne
     if (!e) invalid("read_elitist: NULL engine");
     if (!e->initialized) throw GomixError(GOMIX_E_STATE, "read_elitist: population not initialised");
     if (genotype) {
+      launch_finalize_elitist(e->snap_args(), e->stream);  // complete the copy-on-write snapshot
       uint8_t* d = nullptr;
       GOMIX_CUDA(cudaMallocAsync(&d, e->P->nv, e->stream));
       launch_unpack_elitist(e->elit, d, e->P->nv, e->stream);
+      ++e->launches;
       ++e->launches;
       GOMIX_CUDA(cudaMemcpyAsync(genotype, d, e->P->nv, cudaMemcpyDeviceToHost, e->stream));
       GOMIX_CUDA(cudaFreeAsync(d, e->stream));
@@ -974,9 +973,8 @@ int gomix_gpu_offer_elitist(gomix_gpu_engine* e, const uint8_t* genotype, double
     GOMIX_CUDA(cudaMemcpyAsync(d, genotype, nv, cudaMemcpyHostToDevice, e->stream));
     launch_pack_elitist(d, e->elit, nv, e->stream);
     GOMIX_CUDA(cudaFreeAsync(d, e->stream));
-    e->set_elitist_fitness(fitness);
-    GOMIX_CUDA(cudaMemsetAsync(e->ham, 0, e->n * 4, e->stream));
-    e->refresh(-2);
+    launch_external_elitist(e->snap_args(), fitness, e->stream);
+    e->launches += 2;
     GOMIX_CUDA(cudaStreamSynchronize(e->stream));
     e->elit_fit = fitness;
   });

@@ -1,6 +1,6 @@
-// gom.cu — the hot path: one batched GOM step per colour class, plus its
-// epilogue (fitness commit, elitist scan, stop criteria) and the elitist
-// refresh, and the population init / full-evaluation kernels.
+// gom.cu — the hot path: one batched GOM step per colour class with its fused
+// epilogue (fitness commit, elitist scan, stop criteria), the elitist
+// snapshot / hashing kernels, and the population init / full-evaluation kernels.
 //
 // Reference semantics (proj/include/gomix/engine_parallel.hpp):
 //   phase 1 insert_donor_genes        :104-121  -> donor per (s, set): replay tape
@@ -56,6 +56,33 @@ __device__ __forceinline__ bool cmp_better(bool exact, double a, double b) {
 }
 __device__ __forceinline__ bool cmp_equal(bool exact, double a, double b) {
   return exact ? a == b : fabs(a - b) <= cmp_scale(a, b);
+}
+
+// 128-bit Zobrist key of variable v (two independent splitmix64 streams).
+// A genotype's hash is the XOR of the keys of its variables set to 1, so a
+// flip of v toggles key(v): "parent == elitist" (engine_parallel.hpp:202) is
+// hash equality, maintained incrementally instead of recounted per group.
+__device__ __forceinline__ unsigned long long smix(unsigned long long x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+__device__ __forceinline__ void zobrist(uint32_t v, unsigned long long& z1, unsigned long long& z2) {
+  z1 = smix(0x5A0B0000000000ull ^ (unsigned long long)v);
+  z2 = smix(0xC3A5C85C97CB3127ull + 0x9E37ull * (unsigned long long)v);
+}
+
+// Copy-on-write elitist snapshot: before solution elit_src changes variable v
+// for the first time since it became the elitist, record its old bit.
+__device__ __forceinline__ void capture_row(uint32_t* elit, uint32_t* ever, uint32_t ver, uint32_t v,
+                                            uint32_t old_bit) {
+  if (ever[v] == ver) return;
+  if (old_bit)
+    atomicOr(&elit[v >> 5], 1u << (v & 31u));
+  else
+    atomicAnd(&elit[v >> 5], ~(1u << (v & 31u)));
+  ever[v] = ver;
 }
 
 __device__ __forceinline__ uint32_t valid_mask(uint32_t w, uint32_t n) {
@@ -160,8 +187,10 @@ __device__ void epilogue_body(const EpiArgs& a) {
     }
     a.fit[s] = f;
     if (s < kEpiSmemFit) s_fit[s] = f;
-    a.ham[s] += a.dham[s];
-    a.dham[s] = 0;
+    a.h1[s] ^= a.dh1[s];
+    a.h2[s] ^= a.dh2[s];
+    a.dh1[s] = 0;
+    a.dh2[s] = 0;
   }
   if (threadIdx.x == 0) {
     const unsigned long long st = c->grp_steps, ca = c->grp_calls;
@@ -220,65 +249,107 @@ __device__ void epilogue_body(const EpiArgs& a) {
     if (lane == 0) {
       c->n_impr = ni;
       if (hit) request_stop(c, GOMIX_STOP_TARGET);
-      c->elit_src = best;
-      if (best >= 0) c->elit_fit = cur;
+      if (best >= 0) {  // new elitist: member `best` (snapshot taken copy-on-write)
+        c->elit_fit = cur;
+        c->elit_src = best;
+        c->eh1 = a.h1[best];
+        c->eh2 = a.h2[best];
+        c->elit_ver += 1;
+      }
       s_best = best;
     }
   }
   __syncthreads();
-  if (s_best >= 0)
-    for (uint32_t s = threadIdx.x; s < n; s += blockDim.x) a.ham[s] = 0;  // refresh recounts
-  __syncthreads();
 }
 
 // ---------------------------------------------------------------------------
-// refresh: when the elitist changed, copy its genotype out of the population
-// column and recount every member's Hamming distance to it.  The batched
-// accept rule only needs "parent == elitist" at group start
-// (engine_parallel.hpp:202), i.e. distance 0; the GOM kernel maintains the
-// distances incrementally between refreshes.  Lanes load 32 consecutive rows
-// of one word column; 32 ballots transpose the 32x32 bit block so lane k
-// counts solution 32w+k.
+// hashes and the elitist snapshot
 // ---------------------------------------------------------------------------
-__device__ void refresh_body(const RefreshArgs& a, uint64_t gwarp, uint64_t nwarps) {
-  const int32_t src = a.force_src != kNoForce ? a.force_src : *(volatile const int32_t*)&a.ctl->elit_src;
-  if (src == -1) return;
-  const uint32_t lane = threadIdx.x & 31u, Wp = a.Wp;
-  const uint32_t sw = src >= 0 ? (uint32_t)src >> 5 : 0u, sb = src >= 0 ? (uint32_t)src & 31u : 0u;
+// h[s] = XOR of key(v) over the variables of solution s set to 1.  A warp takes
+// 32 rows of one word column; lane k accumulates solution 32w+k.
+__global__ void hash_population_kernel(const SnapArgs a) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t gwarp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint32_t Wp = a.Wp;
   const uint64_t blocks = (a.nv + 31) / 32;
-  int32_t cnt = 0;
-  uint32_t cur_w = 0xFFFFFFFFu;
   for (uint64_t unit = gwarp; unit < blocks * Wp; unit += nwarps) {
     const uint32_t w = (uint32_t)(unit % Wp);
-    if (w != cur_w) {
-      if (cur_w != 0xFFFFFFFFu && cur_w * 32u + lane < a.n && cnt) atomicAdd(&a.ham[cur_w * 32u + lane], cnt);
-      cnt = 0;
-      cur_w = w;
-    }
-    const uint64_t v = (unit / Wp) * 32u + lane;
-    const bool has = v < a.nv;
-    const uint32_t x = has ? a.pop[v * Wp + w] : 0u;
-    const uint32_t eb = !has ? 0u
-                        : src >= 0 ? (a.pop[v * Wp + sw] >> sb) & 1u
-                                   : (a.elit[v >> 5] >> (v & 31u)) & 1u;
-    if (src >= 0 && w == 0) {
-      const uint32_t word = __ballot_sync(0xFFFFFFFFu, eb);
-      if (lane == 0) a.elit[v >> 5] = word;
-    }
     if (w * 32u >= a.n) continue;
-    const uint32_t diff = has ? (x ^ (eb ? 0xFFFFFFFFu : 0u)) : 0u;
-#pragma unroll
-    for (uint32_t k = 0; k < 32; ++k) {
-      const uint32_t c = __popc(__ballot_sync(0xFFFFFFFFu, (diff >> k) & 1u));
-      if (lane == k) cnt += (int32_t)c;
+    const uint64_t v = (unit / Wp) * 32u + lane;
+    const uint32_t x = v < a.nv ? a.pop[v * Wp + w] : 0u;
+    unsigned long long z1 = 0, z2 = 0;
+    if (v < a.nv) zobrist((uint32_t)v, z1, z2);
+    unsigned long long h1 = 0, h2 = 0;
+    for (int r = 0; r < 32; ++r) {
+      const uint32_t xr = __shfl_sync(0xFFFFFFFFu, x, r);
+      const unsigned long long a1 = __shfl_sync(0xFFFFFFFFu, z1, r), a2 = __shfl_sync(0xFFFFFFFFu, z2, r);
+      if ((xr >> lane) & 1u) {
+        h1 ^= a1;
+        h2 ^= a2;
+      }
+    }
+    const uint32_t s = w * 32u + lane;
+    if (s < a.n && (h1 | h2)) {
+      atomicXor(&a.h1[s], h1);
+      atomicXor(&a.h2[s], h2);
     }
   }
-  if (cur_w != 0xFFFFFFFFu && cur_w * 32u + lane < a.n && cnt) atomicAdd(&a.ham[cur_w * 32u + lane], cnt);
 }
 
-__global__ void refresh_kernel(const RefreshArgs a) {
-  const uint64_t gtid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  refresh_body(a, gtid >> 5, ((uint64_t)gridDim.x * blockDim.x) >> 5);
+// Complete the copy-on-write snapshot: rows not captured since the elitist was
+// chosen still hold its bit in population column elit_src.
+__global__ void finalize_elitist_kernel(const SnapArgs a) {
+  const DevCtl* c = a.ctl;
+  const int32_t src = c->elit_src;
+  if (src < 0) return;
+  const uint32_t ver = c->elit_ver, sw = (uint32_t)src >> 5, sb = (uint32_t)src & 31u;
+  const uint64_t words = (a.nv + 31) / 32;
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < words;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t word = a.elit[t];
+    for (uint32_t k = 0; k < 32 && t * 32 + k < a.nv; ++k) {
+      const uint64_t v = t * 32 + k;
+      if (a.ever[v] != ver) {
+        const uint32_t b = (a.pop[v * a.Wp + sw] >> sb) & 1u;
+        word = (word & ~(1u << k)) | (b << k);
+        a.ever[v] = ver;
+      }
+    }
+    a.elit[t] = word;
+  }
+}
+
+// offer_elitist (engine_parallel.hpp:320-322): the elitist bits were uploaded;
+// recompute its hash, mark the snapshot complete.
+__global__ void external_elitist_reset_kernel(DevCtl* c, double fitness) {
+  c->elit_fit = fitness;
+  c->elit_src = -2;
+  c->eh1 = 0;
+  c->eh2 = 0;
+  c->elit_ver += 1;
+}
+
+__global__ void external_elitist_hash_kernel(const SnapArgs a) {
+  unsigned long long h1 = 0, h2 = 0;
+  for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < a.nv;
+       v += (uint64_t)gridDim.x * blockDim.x) {
+    if ((a.elit[v >> 5] >> (v & 31u)) & 1u) {
+      unsigned long long z1, z2;
+      zobrist((uint32_t)v, z1, z2);
+      h1 ^= z1;
+      h2 ^= z2;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    h1 ^= __shfl_xor_sync(0xFFFFFFFFu, h1, o);
+    h2 ^= __shfl_xor_sync(0xFFFFFFFFu, h2, o);
+  }
+  if ((threadIdx.x & 31u) == 0 && (h1 | h2)) {
+    atomicXor(&a.ctl->eh1, h1);
+    atomicXor(&a.ctl->eh2, h2);
+  }
 }
 
 __device__ __forceinline__ double shfl_d(double x, int src) {
@@ -299,8 +370,7 @@ __device__ __forceinline__ double shfl_d(double x, int src) {
 // or its FpEntry list) and the neighbour rows it needs are fetched by the
 // lanes in parallel — one coalesced round of loads per 32 entries — then
 // broadcast with shuffles, so the sums below run without dependent loads.
-// The last CTA to finish runs the epilogue (and, for small populations, the
-// elitist refresh), so a group is one launch.
+// The last CTA to finish runs the epilogue, so a group is one launch.
 // ---------------------------------------------------------------------------
 template <int WPT, bool UNIV, bool I32>
 // univariate launches with WPT <= 4 always use <= 256 threads: allow 3 CTAs/SM
@@ -339,20 +409,24 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
 
   // group-start state of this thread's solutions: "parent == elitist"
   // (engine_parallel.hpp:202) and the parent fitness, read once per launch
+  const unsigned long long eh1 = a.ctl->eh1, eh2 = a.ctl->eh2;
+  const int32_t esrc = a.ctl->elit_src;        // copy-on-write snapshot source
+  const uint32_t ever_cur = a.ctl->elit_ver;
   bool is_elit[WPT];
   double pfit[WPT];
 #pragma unroll
   for (int j = 0; j < WPT; ++j) {
     const uint32_t s = (wit + tw * (uint32_t)j) * 32u + lane;
-    is_elit[j] = s < n && a.ham[s] == 0;
+    is_elit[j] = s < n && a.h1[s] == eh1 && a.h2[s] == eh2;
     pfit[j] = (!exact && s < n) ? a.fit[s] : 0.0;
   }
   Acc acc[WPT];
-  int32_t hacc[WPT];
+  unsigned long long dh1[WPT], dh2[WPT];
 #pragma unroll
   for (int j = 0; j < WPT; ++j) {
     acc[j] = 0;
-    hacc[j] = 0;
+    dh1[j] = 0;
+    dh2[j] = 0;
   }
   uint32_t steps = 0;
   unsigned long long calls = 0;
@@ -379,8 +453,9 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
           ones = __reduce_add_sync(0xFFFFFFFFu, ones);
         }
       }
-      const uint32_t eb = (a.elit[v >> 5] >> (v & 31u)) & 1u;
       const uint32_t deg = (uint32_t)(re - rs);
+      unsigned long long zv1, zv2;
+      zobrist(v, zv1, zv2);
       int32_t di[WPT];
       double sn[WPT], so[WPT];
 #pragma unroll
@@ -451,7 +526,9 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
         if (lane == 0 && nw != pw[j]) a.pop[(size_t)v * Wp + w] = nw;
         if (accept) {
           acc[j] += I32 ? (Acc)di[j] : (Acc)delta;
-          hacc[j] += (pv == eb) ? 1 : -1;
+          dh1[j] ^= zv1;
+          dh2[j] ^= zv2;
+          if ((int32_t)s == esrc) capture_row(a.elit, a.ever, ever_cur, v, pv);
         }
         steps += present ? 1u : 0u;
         calls += present ? deg : 0u;
@@ -498,15 +575,8 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
 #pragma unroll
         for (int j = 0; j < WPT; ++j) xw0[j] = a.pop[(size_t)ext * Wp + wit + tw * j];
       }
-      uint64_t em;  // elitist genotype on F
-      {
-        const uint32_t v0 = lane < f ? vars[lane] : 0u;
-        const uint32_t v1 = lane + 32u < f ? vars[lane + 32u] : 0u;
-        const uint32_t b0 = lane < f ? (a.elit[v0 >> 5] >> (v0 & 31u)) & 1u : 0u;
-        const uint32_t b1 = lane + 32u < f ? (a.elit[v1 >> 5] >> (v1 & 31u)) & 1u : 0u;
-        em = (uint64_t)__ballot_sync(0xFFFFFFFFu, b0) |
-             ((uint64_t)__ballot_sync(0xFFFFFFFFu, b1) << 32);
-      }
+      unsigned long long* zF = reinterpret_cast<unsigned long long*>(newF + f * Wp + ((f * Wp) & 1u));
+      for (uint32_t jv = tid_team; jv < f; jv += team_threads) zobrist(vars[jv], zF[2 * jv], zF[2 * jv + 1]);
       const uint64_t fm = f >= 64 ? ~0ull : ((1ull << f) - 1ull);
       team_sync(tw, teams_per_cta, team);
       uint64_t pm[WPT];
@@ -688,7 +758,15 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
           newF[jv * Wp + w] = (rowsF[jv * Wp + w] & ~acc_w) | (newD[jv * Wp + w] & acc_w);
         if (accept) {
           acc[j] += I32 ? (Acc)di[j] : (Acc)delta;
-          hacc[j] += __popcll((dm[j] ^ em) & fm) - __popcll((pm[j] ^ em) & fm);
+          uint64_t changed = (dm[j] ^ pm[j]) & fm;
+          const bool cap = (int32_t)s == esrc;
+          while (changed) {
+            const uint32_t jv = (uint32_t)(__ffsll((long long)changed) - 1);
+            changed &= changed - 1;
+            dh1[j] ^= zF[2 * jv];
+            dh2[j] ^= zF[2 * jv + 1];
+            if (cap) capture_row(a.elit, a.ever, ever_cur, vars[jv], (uint32_t)(pm[j] >> jv) & 1u);
+          }
         }
         steps += present[j] ? 1u : 0u;
         calls += present[j] ? fpl : 0u;
@@ -735,27 +813,33 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
   if (teams_per_cta > 1) {
     // several teams per CTA: combine them in fixed order (deterministic)
     double* sacc = reinterpret_cast<double*>(smem);
-    int32_t* sham = reinterpret_cast<int32_t*>(sacc + (size_t)teams_per_cta * Wp * 32u);
+    unsigned long long* sh1 = reinterpret_cast<unsigned long long*>(sacc + (size_t)teams_per_cta * Wp * 32u);
+    unsigned long long* sh2 = sh1 + (size_t)teams_per_cta * Wp * 32u;
 #pragma unroll
     for (int j = 0; j < WPT; ++j) {
       const uint32_t s = (wit + tw * (uint32_t)j) * 32u + lane;
       sacc[(size_t)team * Wp * 32u + s] = (double)acc[j];
-      sham[(size_t)team * Wp * 32u + s] = hacc[j];
+      sh1[(size_t)team * Wp * 32u + s] = dh1[j];
+      sh2[(size_t)team * Wp * 32u + s] = dh2[j];
     }
     __syncthreads();
     for (uint32_t s = threadIdx.x; s < Wp * 32u; s += blockDim.x) {
       double v = 0.0;
-      int32_t h = 0;
+      unsigned long long x1 = 0, x2 = 0;
       for (uint32_t t = 0; t < teams_per_cta; ++t) {
         v += sacc[(size_t)t * Wp * 32u + s];
-        h += sham[(size_t)t * Wp * 32u + s];
+        x1 ^= sh1[(size_t)t * Wp * 32u + s];
+        x2 ^= sh2[(size_t)t * Wp * 32u + s];
       }
       if (s < n) {
         if (float_parts)
           a.part[(size_t)blockIdx.x * n + s] = v;
         else if (a.dfit && v != 0.0)
           atomicAdd(&a.dfit[s], v);
-        if (h) atomicAdd(&a.dham[s], h);
+        if (x1 | x2) {
+          atomicXor(&a.dh1[s], x1);
+          atomicXor(&a.dh2[s], x2);
+        }
       }
     }
   } else {
@@ -767,7 +851,10 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
           a.part[(size_t)blockIdx.x * n + s] = (double)acc[j];
         else if (a.dfit && acc[j] != 0)
           atomicAdd(&a.dfit[s], (double)acc[j]);
-        if (hacc[j]) atomicAdd(&a.dham[s], hacc[j]);
+        if (dh1[j] | dh2[j]) {
+          atomicXor(&a.dh1[s], dh1[j]);
+          atomicXor(&a.dh2[s], dh2[j]);
+        }
       }
     }
   }
@@ -786,10 +873,6 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
   __threadfence();
   epilogue_body(epi);
   if (threadIdx.x == 0) a.ctl->done = 0;
-  if (a.fuse_refresh) {
-    refresh_body(a.ref, threadIdx.x >> 5, blockDim.x >> 5);
-    __syncthreads();
-  }
 }
 
 __global__ void begin_call_kernel(const BeginArgs b) {
@@ -865,11 +948,14 @@ __global__ void init_epilogue_kernel(const EpiArgs a) {
     }
     c->elit_fit = cur;
     c->elit_src = best;
+    c->eh1 = a.h1[best];
+    c->eh2 = a.h2[best];
+    c->elit_ver += 1;
   }
   __syncthreads();
   for (uint32_t s = threadIdx.x; s < a.n; s += blockDim.x) {
-    a.ham[s] = 0;
-    a.dham[s] = 0;
+    a.dh1[s] = 0;
+    a.dh2[s] = 0;
     a.dfit[s] = 0.0;
   }
 }
@@ -1034,8 +1120,22 @@ void launch_init_epilogue(const EpiArgs& a, cudaStream_t s) {
   GOMIX_CUDA(cudaGetLastError());
 }
 
-void launch_refresh(const RefreshArgs& a, int grid, cudaStream_t s) {
-  refresh_kernel<<<grid, 256, 0, s>>>(a);
+void launch_hash_population(const SnapArgs& a, cudaStream_t s) {
+  GOMIX_CUDA(cudaMemsetAsync(a.h1, 0, a.n * sizeof(unsigned long long), s));
+  GOMIX_CUDA(cudaMemsetAsync(a.h2, 0, a.n * sizeof(unsigned long long), s));
+  const uint64_t units = ((a.nv + 31) / 32) * a.Wp;
+  hash_population_kernel<<<grid_for(units * 32, 256, 148 * 16), 256, 0, s>>>(a);
+  GOMIX_CUDA(cudaGetLastError());
+}
+
+void launch_finalize_elitist(const SnapArgs& a, cudaStream_t s) {
+  finalize_elitist_kernel<<<grid_for((a.nv + 31) / 32, 256, 148 * 16), 256, 0, s>>>(a);
+  GOMIX_CUDA(cudaGetLastError());
+}
+
+void launch_external_elitist(const SnapArgs& a, double fitness, cudaStream_t s) {
+  external_elitist_reset_kernel<<<1, 1, 0, s>>>(a.ctl, fitness);
+  external_elitist_hash_kernel<<<grid_for(a.nv, 256, 148 * 8), 256, 0, s>>>(a);
   GOMIX_CUDA(cudaGetLastError());
 }
 

@@ -40,7 +40,7 @@ struct FpEntry {
 // after every group so stop criteria never need a host round trip.
 struct DevCtl {
   double elit_fit;
-  int32_t elit_src;     // >= 0: elitist := solution elit_src; -2: elitist bits given; -1: none
+  int32_t elit_src;     // >= 0: elitist = population column elit_src (copy-on-write); -2: bits given; -1: none
   int32_t stop;         // latched stop request (RunControl::request_stop, runtime.hpp:104-109)
   int32_t stop_reason;  // GOMIX_STOP_*
   int32_t has_budget;
@@ -56,6 +56,9 @@ struct DevCtl {
   unsigned int done;  // last-CTA-done ticket of the GOM kernel
   unsigned int gen_counter;  // device-side generation counter (graph path)
   unsigned int cur_gen;
+  // device-owned elitist identity (never touched by the per-call reset)
+  unsigned long long eh1, eh2;  // 128-bit Zobrist hash of the elitist genotype
+  unsigned int elit_ver;        // snapshot version: row v is captured iff ever[v] == elit_ver
 };
 
 // One colour group as the device sees it (graph path: kernels look their
@@ -99,8 +102,10 @@ struct EpiArgs {
   double* fit;
   const double* part;
   double* dfit;
-  int32_t* ham;
-  int32_t* dham;
+  unsigned long long* h1;  // per-solution Zobrist hashes
+  unsigned long long* h2;
+  unsigned long long* dh1;  // this group's XOR deltas
+  unsigned long long* dh2;
   const double* rec_delta;
   const uint8_t* rec_accept;
   DevCtl* ctl;
@@ -113,14 +118,16 @@ struct EpiArgs {
   int32_t mode;  // 0 exact atomics, 1 float partials, 2 ordered
 };
 
-struct RefreshArgs {
+// elitist snapshot / hashing kernels
+struct SnapArgs {
   const uint32_t* pop;
   uint32_t* elit;
-  int32_t* ham;
-  const DevCtl* ctl;
+  uint32_t* ever;
+  DevCtl* ctl;
+  unsigned long long* h1;
+  unsigned long long* h2;
   uint64_t nv;
   uint32_t n, Wp;
-  int32_t force_src;  // kNoForce: use ctl->elit_src
 };
 
 struct GomArgs {
@@ -139,11 +146,14 @@ struct GomArgs {
   uint32_t G;             // |G|
   uint32_t* pop;
   const double* fit;
-  const int32_t* ham;
-  const uint32_t* elit;
+  const unsigned long long* h1;
+  const unsigned long long* h2;
+  uint32_t* elit;  // copy-on-write snapshot of the elitist genotype
+  uint32_t* ever;  // per-row snapshot version
   double* dfit;
   double* part;
-  int32_t* dham;
+  unsigned long long* dh1;
+  unsigned long long* dh2;
   DevCtl* ctl;
   const int32_t* tape;  // replay donors, p-major [p*n + s]; nullptr -> Philox
   int32_t* rec_donor;   // optional GroupBatch recording, p-major
@@ -155,8 +165,6 @@ struct GomArgs {
   uint32_t generation;
   uint64_t seed;
   EpiArgs epi;         // run by the last CTA
-  RefreshArgs ref;
-  int32_t fuse_refresh;
   int32_t slot;                 // >= 0: group = order[slot] (graph path)
   const uint32_t* order;
   const GroupDesc* groups;
@@ -168,8 +176,6 @@ struct OrderArgs {
   uint32_t k;
   uint64_t seed;
 };
-
-constexpr int32_t kNoForce = -1000;
 
 // Per-call control values, passed as kernel parameters (captured at launch,
 // so host calls can be queued back to back without host syncs).
@@ -250,7 +256,9 @@ void launch_begin(const BeginArgs& b, cudaStream_t s);
 void launch_order(const BeginArgs& b, const OrderArgs& o, cudaStream_t s);
 void prepare_gom(bool univariate, bool i32, int wpt, size_t smem);
 void launch_init_epilogue(const EpiArgs& a, cudaStream_t s);
-void launch_refresh(const RefreshArgs& a, int grid, cudaStream_t s);
+void launch_hash_population(const SnapArgs& a, cudaStream_t s);
+void launch_finalize_elitist(const SnapArgs& a, cudaStream_t s);
+void launch_external_elitist(const SnapArgs& a, double fitness, cudaStream_t s);
 void launch_philox_init(uint32_t* pop, uint64_t nv, uint32_t n, uint32_t Wp, uint64_t seed,
                         cudaStream_t s);
 void launch_full_eval(const Problem& P, const uint32_t* pop, double* fit, uint32_t n,
