@@ -342,7 +342,7 @@ struct gomix_gpu_engine {
     GOMIX_CUDA(cudaSetDevice(P->device));
     GOMIX_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     own_stream = true;
-    const int per_sm = gom_max_blocks_per_sm(P->univariate, P->i32, (int)wpt, (int)block, smem);
+    const int per_sm = gom_max_blocks_per_sm(P->univariate, P->i32, (int)wpt, tw > 1, (int)block, smem);
     if (per_sm < 1) invalid("engine: GOM kernel does not fit on an SM with this configuration");
     grid_cap = per_sm * sms;
     for (uint64_t c = 0; c < P->k; ++c)
@@ -374,7 +374,7 @@ struct gomix_gpu_engine {
         gd[c] = GroupDesc{(uint32_t)P->group_off[c], (uint32_t)(P->group_off[c + 1] - P->group_off[c])};
       GOMIX_CUDA(cudaMemcpy(d_groups, gd.data(), P->k * sizeof(GroupDesc), cudaMemcpyHostToDevice));
     }
-    prepare_gom(P->univariate, P->i32, (int)wpt, smem);
+    prepare_gom(P->univariate, P->i32, (int)wpt, tw > 1, smem);
     if (record || epi_mode == 2) {
       rec_donor = dev_alloc<int32_t>(allocs, max_group * n);
       rec_delta = dev_alloc<double>(allocs, max_group * n);
@@ -557,7 +557,7 @@ struct gomix_gpu_engine {
       GOMIX_CUDA(cudaEventRecord(e0, st));
     }
     a.epi = epi_args(group, (uint32_t)G, (uint32_t)grid);
-    launch_gom(a, P->univariate, P->i32, (int)wpt, grid, (int)block, smem, st);
+    launch_gom(a, P->univariate, P->i32, (int)wpt, tw > 1, grid, (int)block, smem, st);
     ++launches;
     if (e1) {
       GOMIX_CUDA(cudaEventRecord(e1, st));

@@ -352,6 +352,27 @@ __global__ void external_elitist_hash_kernel(const SnapArgs a) {
   }
 }
 
+// A row's words owned by this thread: all WPT words (vector loads) for a
+// one-warp team, every tw-th word otherwise.
+template <int WPT, bool TEAM>
+__device__ __forceinline__ void load_words(const uint32_t* row, uint32_t wit, uint32_t tw, uint32_t (&o)[WPT]) {
+  if constexpr (!TEAM && WPT == 4) {
+    const uint4 t = __ldg(reinterpret_cast<const uint4*>(row));
+    o[0] = t.x; o[1] = t.y; o[2] = t.z; o[3] = t.w;
+  } else if constexpr (!TEAM && WPT == 8) {
+    const uint4 t0 = __ldg(reinterpret_cast<const uint4*>(row));
+    const uint4 t1 = __ldg(reinterpret_cast<const uint4*>(row) + 1);
+    o[0] = t0.x; o[1] = t0.y; o[2] = t0.z; o[3] = t0.w;
+    o[4] = t1.x; o[5] = t1.y; o[6] = t1.z; o[7] = t1.w;
+  } else if constexpr (!TEAM && WPT == 2) {
+    const uint2 t = __ldg(reinterpret_cast<const uint2*>(row));
+    o[0] = t.x; o[1] = t.y;
+  } else {
+#pragma unroll
+    for (int j = 0; j < WPT; ++j) o[j] = row[wit + tw * j];
+  }
+}
+
 __device__ __forceinline__ double shfl_d(double x, int src) {
   return __shfl_sync(0xFFFFFFFFu, x, src);
 }
@@ -372,7 +393,7 @@ __device__ __forceinline__ double shfl_d(double x, int src) {
 // broadcast with shuffles, so the sums below run without dependent loads.
 // The last CTA to finish runs the epilogue, so a group is one launch.
 // ---------------------------------------------------------------------------
-template <int WPT, bool UNIV, bool I32>
+template <int WPT, bool UNIV, bool I32, bool TEAM>
 // univariate launches with WPT <= 4 always use <= 256 threads: allow 3 CTAs/SM
 __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <= 4) ? 3 : 1)
     gom_group_kernel(const GomArgs a) {
@@ -381,9 +402,11 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
 
   using Acc = typename std::conditional<I32, long long, double>::type;
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  const uint32_t tw = a.team_warps;
-  const uint32_t teams_per_cta = (blockDim.x >> 5) / tw;
-  const uint32_t team = warp / tw, wit = warp - team * tw;
+  // TEAM: the CTA is one team of tw warps; otherwise every warp is a team
+  // holding all Wp == WPT words of its solutions (compile-time index math)
+  const uint32_t tw = TEAM ? a.team_warps : 1u;
+  const uint32_t teams_per_cta = TEAM ? 1u : (blockDim.x >> 5);
+  const uint32_t team = TEAM ? 0u : warp, wit = TEAM ? warp : 0u;
   const uint32_t tid_team = wit * 32u + lane, team_threads = tw * 32u;
   const uint32_t Wp = a.Wp, n = a.n;
   const bool exact = I32 || a.exact != 0;  // integer-weight instances only take the I32 path
@@ -441,7 +464,8 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
       const uint32_t* row = a.pop + (size_t)v * Wp;
       uint32_t pw[WPT];
 #pragma unroll
-      for (int j = 0; j < WPT; ++j) pw[j] = row[wit + tw * j];
+      for (int j = 0; j < WPT; ++j) pw[j] = 0;
+      load_words<WPT, TEAM>(row, wit, tw, pw);
       const int32_t rs = a.row_ptr[v], re = a.row_ptr[v + 1];
       uint32_t ones = 0;
       if (!replay) {
@@ -474,7 +498,8 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
         else wtd = has ? a.w[e] : 0.0;
         uint32_t nb[WPT];
 #pragma unroll
-        for (int j = 0; j < WPT; ++j) nb[j] = a.pop[(size_t)u * Wp + wit + tw * j];
+        for (int j = 0; j < WPT; ++j) nb[j] = 0;
+        load_words<WPT, TEAM>(a.pop + (size_t)u * Wp, wit, tw, nb);
         const int cnt = min(32, re - base);
         for (int t = 0; t < cnt; ++t) {
           if constexpr (I32) {
@@ -1060,18 +1085,29 @@ __global__ void unpack_elitist_kernel(const uint32_t* elit, uint8_t* out, uint64
 // launchers
 // ---------------------------------------------------------------------------
 namespace {
-template <int WPT>
+template <int WPT, bool TEAM>
 void* gom_kernel_ptr(bool univariate, bool i32) {
-  if (univariate) return i32 ? (void*)gom_group_kernel<WPT, true, true> : (void*)gom_group_kernel<WPT, true, false>;
-  return i32 ? (void*)gom_group_kernel<WPT, false, true> : (void*)gom_group_kernel<WPT, false, false>;
+  if (univariate)
+    return i32 ? (void*)gom_group_kernel<WPT, true, true, TEAM> : (void*)gom_group_kernel<WPT, true, false, TEAM>;
+  return i32 ? (void*)gom_group_kernel<WPT, false, true, TEAM> : (void*)gom_group_kernel<WPT, false, false, TEAM>;
 }
 
-void* gom_kernel(bool univariate, bool i32, int wpt) {
-  switch (wpt) {
-    case 1: return gom_kernel_ptr<1>(univariate, i32);
-    case 2: return gom_kernel_ptr<2>(univariate, i32);
-    case 4: return gom_kernel_ptr<4>(univariate, i32);
-    case 8: return gom_kernel_ptr<8>(univariate, i32);
+// instantiated shapes: one-warp teams with all words per lane (WPT = Wp <= 8),
+// and CTA teams with WPT 1 (few sets), 4 or 8 words per thread (large n)
+void* gom_kernel(bool univariate, bool i32, int wpt, bool team) {
+  if (team) {
+    switch (wpt) {
+      case 1: return gom_kernel_ptr<1, true>(univariate, i32);
+      case 4: return gom_kernel_ptr<4, true>(univariate, i32);
+      case 8: return gom_kernel_ptr<8, true>(univariate, i32);
+    }
+  } else {
+    switch (wpt) {
+      case 1: return gom_kernel_ptr<1, false>(univariate, i32);
+      case 2: return gom_kernel_ptr<2, false>(univariate, i32);
+      case 4: return gom_kernel_ptr<4, false>(univariate, i32);
+      case 8: return gom_kernel_ptr<8, false>(univariate, i32);
+    }
   }
   throw GomixError(GOMIX_E_INVALID, "unsupported words-per-thread");
 }
@@ -1083,21 +1119,21 @@ int grid_for(uint64_t work, int block, uint64_t cap) {
 }
 }  // namespace
 
-void prepare_gom(bool univariate, bool i32, int wpt, size_t smem) {
-  void* fn = gom_kernel(univariate, i32, wpt);
+void prepare_gom(bool univariate, bool i32, int wpt, bool team, size_t smem) {
+  void* fn = gom_kernel(univariate, i32, wpt, team);
   if (smem > 48 * 1024)
     GOMIX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
 }
 
-void launch_gom(const GomArgs& a, bool univariate, bool i32, int wpt, int grid, int block,
+void launch_gom(const GomArgs& a, bool univariate, bool i32, int wpt, bool team, int grid, int block,
                 size_t smem, cudaStream_t s) {
-  void* fn = gom_kernel(univariate, i32, wpt);
+  void* fn = gom_kernel(univariate, i32, wpt, team);
   void* args[] = {(void*)&a};
   GOMIX_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(block), args, smem, s));
 }
 
-int gom_max_blocks_per_sm(bool univariate, bool i32, int wpt, int block, size_t smem) {
-  void* fn = gom_kernel(univariate, i32, wpt);
+int gom_max_blocks_per_sm(bool univariate, bool i32, int wpt, bool team, int block, size_t smem) {
+  void* fn = gom_kernel(univariate, i32, wpt, team);
   if (smem > 48 * 1024)
     GOMIX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int blocks = 0;

@@ -249,12 +249,12 @@ class ReplayStream {
 };
 
 // kernel launchers (gom.cu)
-void launch_gom(const GomArgs& a, bool univariate, bool i32, int wpt, int grid, int block,
+void launch_gom(const GomArgs& a, bool univariate, bool i32, int wpt, bool team, int grid, int block,
                 size_t smem, cudaStream_t s);
-int gom_max_blocks_per_sm(bool univariate, bool i32, int wpt, int block, size_t smem);
+int gom_max_blocks_per_sm(bool univariate, bool i32, int wpt, bool team, int block, size_t smem);
 void launch_begin(const BeginArgs& b, cudaStream_t s);
 void launch_order(const BeginArgs& b, const OrderArgs& o, cudaStream_t s);
-void prepare_gom(bool univariate, bool i32, int wpt, size_t smem);
+void prepare_gom(bool univariate, bool i32, int wpt, bool team, size_t smem);
 void launch_init_epilogue(const EpiArgs& a, cudaStream_t s);
 void launch_hash_population(const SnapArgs& a, cudaStream_t s);
 void launch_finalize_elitist(const SnapArgs& a, cudaStream_t s);
