@@ -245,6 +245,7 @@ struct gomix_gpu_engine {
   uint8_t* rec_present = nullptr;
   uint8_t* rec_accept = nullptr;
   uint64_t max_group = 0;
+  uint8_t* d_bytes = nullptr;  // n x nv genotype staging for host transfers
   uint32_t* d_order = nullptr;
   GroupDesc* d_groups = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
@@ -396,6 +397,11 @@ struct gomix_gpu_engine {
     GOMIX_CUDA(cudaMemset(dh2, 0, n * 8));
     GOMIX_CUDA(cudaMemset(ever, 0, nv * 4));
     GOMIX_CUDA(cudaMemset(elit, 0, ((nv + 31) / 32) * 4));
+  }
+
+  uint8_t* staging() {
+    if (!d_bytes) d_bytes = dev_alloc<uint8_t>(allocs, n * P->nv);
+    return d_bytes;
   }
 
   // ---- per-call control ------------------------------------------------------
@@ -630,11 +636,9 @@ struct gomix_gpu_engine {
     if (genotypes) {
       for (uint64_t i = 0; i < n * nv; ++i)
         if (genotypes[i] > 1) invalid("graybox: genotype value outside alphabet");
-      uint8_t* d_bytes = nullptr;
-      GOMIX_CUDA(cudaMallocAsync(&d_bytes, n * nv, stream));
-      GOMIX_CUDA(cudaMemcpyAsync(d_bytes, genotypes, n * nv, cudaMemcpyHostToDevice, stream));
-      launch_pack(d_bytes, pop, nv, (uint32_t)n, Wp, stream);
-      GOMIX_CUDA(cudaFreeAsync(d_bytes, stream));
+      uint8_t* d = staging();
+      GOMIX_CUDA(cudaMemcpyAsync(d, genotypes, n * nv, cudaMemcpyHostToDevice, stream));
+      launch_pack(d, pop, nv, (uint32_t)n, Wp, stream);
       ++launches;
     } else if (mode == GOMIX_MODE_REPLAY) {
       // n*l draws of uniform_index(2) = low bit of each output (rng.hpp:28-35,
@@ -716,11 +720,9 @@ struct gomix_gpu_engine {
     // the elitist snapshot may still point into the old population: finish it
     launch_finalize_elitist(snap_args(), stream);
     ++launches;
-    uint8_t* d = nullptr;
-    GOMIX_CUDA(cudaMallocAsync(&d, n * nv, stream));
+    uint8_t* d = staging();
     GOMIX_CUDA(cudaMemcpyAsync(d, genotypes, n * nv, cudaMemcpyHostToDevice, stream));
     launch_pack(d, pop, nv, (uint32_t)n, Wp, stream);
-    GOMIX_CUDA(cudaFreeAsync(d, stream));
     ++launches;
     if (fitness) {
       GOMIX_CUDA(cudaMemcpyAsync(fit, fitness, n * 8, cudaMemcpyHostToDevice, stream));
@@ -916,12 +918,10 @@ int gomix_gpu_read_population(gomix_gpu_engine* e, uint8_t* genotypes, double* f
     if (!e) invalid("read_population: NULL engine");
     if (genotypes) {
       const uint64_t bytes = e->n * e->P->nv;
-      uint8_t* d = nullptr;
-      GOMIX_CUDA(cudaMallocAsync(&d, bytes, e->stream));
+      uint8_t* d = e->staging();
       launch_unpack(e->pop, d, e->P->nv, (uint32_t)e->n, e->Wp, e->stream);
       ++e->launches;
       GOMIX_CUDA(cudaMemcpyAsync(genotypes, d, bytes, cudaMemcpyDeviceToHost, e->stream));
-      GOMIX_CUDA(cudaFreeAsync(d, e->stream));
     }
     if (fitness)
       GOMIX_CUDA(cudaMemcpyAsync(fitness, e->fit, e->n * 8, cudaMemcpyDeviceToHost, e->stream));

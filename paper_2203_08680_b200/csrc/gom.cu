@@ -373,6 +373,22 @@ __device__ __forceinline__ void load_words(const uint32_t* row, uint32_t wit, ui
   }
 }
 
+// Write back the words of a row that changed (one vector store for a
+// one-warp team).
+template <int WPT, bool TEAM>
+__device__ __forceinline__ void store_words(uint32_t* row, uint32_t wit, uint32_t tw, const uint32_t (&old)[WPT],
+                                            const uint32_t (&nw)[WPT]) {
+  if constexpr (!TEAM && WPT == 4) {
+    *reinterpret_cast<uint4*>(row) = make_uint4(nw[0], nw[1], nw[2], nw[3]);
+  } else if constexpr (!TEAM && WPT == 2) {
+    *reinterpret_cast<uint2*>(row) = make_uint2(nw[0], nw[1]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < WPT; ++j)
+      if (nw[j] != old[j]) row[wit + tw * j] = nw[j];
+  }
+}
+
 __device__ __forceinline__ double shfl_d(double x, int src) {
   return __shfl_sync(0xFFFFFFFFu, x, src);
 }
@@ -478,8 +494,6 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
         }
       }
       const uint32_t deg = (uint32_t)(re - rs);
-      unsigned long long zv1, zv2;
-      zobrist(v, zv1, zv2);
       int32_t di[WPT];
       double sn[WPT], so[WPT];
 #pragma unroll
@@ -520,6 +534,11 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
           }
         }
       }
+      // phases 3 + 4.  Philox mode: a singleton pair is present iff the row
+      // holds both values among the members (per set, all or nothing).
+      const bool set_present = ones > 0u && ones < n;
+      uint32_t accb = 0;  // bit j: this lane accepted in word j
+      uint32_t nw[WPT];
 #pragma unroll
       for (int j = 0; j < WPT; ++j) {
         const uint32_t w = wit + tw * j;
@@ -532,29 +551,29 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
           dn = valid ? a.tape[(size_t)p * n + s] : -1;
           present = dn >= 0;
         } else {
-          present = valid && (pv ? (n - ones) : ones) > 0u;
+          present = valid && set_present;
           dn = present ? (int32_t)n : -1;  // donor identity is not materialised
         }
-        const double delta = I32 ? (double)di[j] : sn[j] - so[j];
         bool accept = false;
-        if (present) {
-          const bool elit = is_elit[j];
-          if (exact) {
-            accept = delta > 0.0 || (delta == 0.0 && !elit);
-          } else {
+        double delta;
+        if constexpr (I32) {
+          const int32_t d = di[j];
+          delta = (double)d;
+          accept = present && (d > 0 || (d == 0 && !is_elit[j]));
+          if (accept) acc[j] += (Acc)d;
+        } else {
+          delta = sn[j] - so[j];
+          if (present) {
             const double pf = pfit[j];
             const double cand = pf + delta;
-            accept = cmp_better(false, cand, pf) || (cmp_equal(false, cand, pf) && !elit);
+            accept = exact ? (delta > 0.0 || (delta == 0.0 && !is_elit[j]))
+                           : (cmp_better(false, cand, pf) || (cmp_equal(false, cand, pf) && !is_elit[j]));
           }
+          if (accept) acc[j] += (Acc)delta;
         }
-        const uint32_t nw = __ballot_sync(0xFFFFFFFFu, accept ? (pv ^ 1u) : pv);
-        if (lane == 0 && nw != pw[j]) a.pop[(size_t)v * Wp + w] = nw;
-        if (accept) {
-          acc[j] += I32 ? (Acc)di[j] : (Acc)delta;
-          dh1[j] ^= zv1;
-          dh2[j] ^= zv2;
-          if ((int32_t)s == esrc) capture_row(a.elit, a.ever, ever_cur, v, pv);
-        }
+        nw[j] = pw[j] ^ __ballot_sync(0xFFFFFFFFu, accept);  // accepted members flip v
+        accb |= accept ? (1u << j) : 0u;
+        if (accept && (int32_t)s == esrc) capture_row(a.elit, a.ever, ever_cur, v, pv);
         steps += present ? 1u : 0u;
         calls += present ? deg : 0u;
         if (record && valid) {
@@ -564,6 +583,17 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
           a.rec_present[at] = present;
           a.rec_accept[at] = accept;
         }
+      }
+      if (__any_sync(0xFFFFFFFFu, accb != 0)) {
+        unsigned long long zv1, zv2;
+        zobrist(v, zv1, zv2);
+#pragma unroll
+        for (int j = 0; j < WPT; ++j)
+          if (accb & (1u << j)) {
+            dh1[j] ^= zv1;
+            dh2[j] ^= zv2;
+          }
+        if (lane == 0) store_words<WPT, TEAM>(a.pop + (size_t)v * Wp, wit, tw, pw, nw);
       }
     } else {
       // ---- general set F (|F| <= 64).  Shared memory per team holds the F

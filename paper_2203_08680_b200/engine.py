@@ -371,9 +371,13 @@ class GpuParallelEngine:
         return d, de, p, a
 
     # ---- introspection -------------------------------------------------------------
-    def population(self):
-        g = np.zeros((self.n, self.problem.info.num_vertices), np.uint8)
-        f = np.zeros(self.n, np.float64)
+    def population(self, genotypes_out: Optional[np.ndarray] = None, fitness_out: Optional[np.ndarray] = None):
+        """(genotypes n x l uint8, fitness n float64); optional caller buffers
+        (e.g. pinned host memory) are filled in place."""
+        g = genotypes_out if genotypes_out is not None else np.zeros((self.n, self.problem.info.num_vertices), np.uint8)
+        f = fitness_out if fitness_out is not None else np.zeros(self.n, np.float64)
+        assert g.dtype == np.uint8 and g.shape == (self.n, self.problem.info.num_vertices) and g.flags.c_contiguous
+        assert f.dtype == np.float64 and f.shape == (self.n,) and f.flags.c_contiguous
         check(lib().gomix_gpu_read_population(self.h, g.ctypes.data, f.ctypes.data))
         return g, f
 
