@@ -101,6 +101,7 @@ typedef struct {
 
 typedef struct gomix_gpu_problem gomix_gpu_problem;
 typedef struct gomix_gpu_engine gomix_gpu_engine;
+typedef struct gomix_gpu_local_group gomix_gpu_local_group;
 
 /* EngineConfig (engine_serial.hpp:18-24). */
 typedef struct {
@@ -109,11 +110,17 @@ typedef struct {
   uint32_t mode;  /* gomix_mode */
   uint32_t flags; /* GOMIX_FLAG_* */
   int32_t population_id; /* reporting only (engine_parallel.hpp:258) */
-  /* Sharding (one process per GPU).  world_size 1 = single GPU.  With
-   * world_size > 1, nccl_comm is an ncclComm_t owned by the caller and this
-   * rank holds solutions [rank*n/world_size, (rank+1)*n/world_size). */
+  /* Sharding of the population over GPUs (Philox mode).  world_size 1 = one
+   * GPU.  With world_size R > 1 rank r holds members [r*n/R, (r+1)*n/R)
+   * (population_size is the GLOBAL n, divisible by R); after every group the
+   * bit-packed rows (the next group's donor pool), fitness, hashes and
+   * counters are all-gathered, and every rank takes the same elitist / stop
+   * decisions.  Results equal a single-GPU run of the same n and seed.
+   * One process per GPU: every rank passes the same 128-byte NCCL unique id
+   * (gomix_gpu_nccl_unique_id on one rank, then broadcast by the caller).
+   * Several shards in one process: gomix_gpu_local_group_*. */
   int32_t rank, world_size;
-  void* nccl_comm;
+  const void* nccl_unique_id;
 } gomix_engine_config;
 
 /* Termination criteria evaluated after every group, in the reference's order:
@@ -231,6 +238,30 @@ GOMIX_API int gomix_gpu_kernel_times(gomix_gpu_engine* e, float* ms, uint64_t ca
 GOMIX_API int gomix_gpu_set_timing(gomix_gpu_engine* e, int32_t enable);
 /* Number of device kernels this engine has launched so far. */
 GOMIX_API int gomix_gpu_launch_count(gomix_gpu_engine* e, uint64_t* count);
+
+/* ---- multi-GPU sharding ------------------------------------------------------ */
+
+/* 128-byte NCCL unique id for gomix_engine_config.nccl_unique_id (NCCL is
+ * loaded at run time: the process's libnccl.so.2, e.g. PyTorch's). */
+GOMIX_API int gomix_gpu_nccl_unique_id(uint8_t* id);
+/* In-process shards: world_size engines (problems[r] on the device of rank r;
+ * the same problem may serve several ranks on one device) driven in lock step
+ * by one host thread; the exchange is device-to-device copies. */
+GOMIX_API int gomix_gpu_local_group_create(gomix_gpu_problem* const* problems,
+                                           const gomix_engine_config* cfg,
+                                           gomix_gpu_local_group** out);
+GOMIX_API int gomix_gpu_local_group_destroy(gomix_gpu_local_group* g);
+/* rank r's engine: read its shard with gomix_gpu_read_population / counters */
+GOMIX_API int gomix_gpu_local_group_engine(gomix_gpu_local_group* g, int32_t rank,
+                                           gomix_gpu_engine** out);
+GOMIX_API int gomix_gpu_local_group_init_population(gomix_gpu_local_group* g,
+                                                    const gomix_stop_criteria* stop,
+                                                    gomix_run_stats* out);
+GOMIX_API int gomix_gpu_local_group_run_generation(gomix_gpu_local_group* g,
+                                                   const gomix_stop_criteria* stop,
+                                                   gomix_run_stats* out);
+GOMIX_API int gomix_gpu_local_group_read_elitist(gomix_gpu_local_group* g, uint8_t* genotype,
+                                                 double* fitness);
 
 /* ---- synthetic instances (host only) ------------------------------------------ */
 

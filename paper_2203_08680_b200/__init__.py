@@ -6,11 +6,11 @@ GPU) the engine raises.
 """
 from .maxcut import (Fos, MaxCutInstance, generate_regular, generate_torus, load_edge_list,  # noqa: F401
                      neighbourhood_fos, save_edge_list, univariate_fos)
-from .engine import (FitnessComparator, GpuParallelEngine, GpuProblem, RecordingSink,  # noqa: F401
-                     RunContext, RunControl, TerminationConfig, TraceSink, gpu_color, mix64,
-                     population_seed)
+from .engine import (FitnessComparator, GpuLocalGroup, GpuParallelEngine, GpuProblem,  # noqa: F401
+                     RecordingSink, RunContext, RunControl, TerminationConfig, TraceSink, gpu_color, mix64,
+                     nccl_unique_id, population_seed, shard_range)
 
 __all__ = ["Fos", "MaxCutInstance", "generate_regular", "generate_torus", "load_edge_list", "neighbourhood_fos",
-           "save_edge_list", "univariate_fos", "FitnessComparator", "GpuParallelEngine", "GpuProblem",
+           "save_edge_list", "univariate_fos", "FitnessComparator", "GpuLocalGroup", "GpuParallelEngine", "GpuProblem",
            "RecordingSink", "RunContext", "RunControl", "TerminationConfig", "TraceSink", "gpu_color", "mix64",
-           "population_seed"]
+           "nccl_unique_id", "population_seed", "shard_range"]

@@ -53,7 +53,7 @@ class ProblemInfo(C.Structure):
 class EngineConfig(C.Structure):
     _fields_ = [("population_size", C.c_uint64), ("seed", C.c_uint64), ("mode", C.c_uint32),
                 ("flags", C.c_uint32), ("population_id", C.c_int32), ("rank", C.c_int32),
-                ("world_size", C.c_int32), ("nccl_comm", C.c_void_p)]
+                ("world_size", C.c_int32), ("nccl_unique_id", C.c_void_p)]
 
 
 class StopCriteria(C.Structure):
@@ -99,6 +99,13 @@ _SIGNATURES = {
     "gomix_gpu_set_timing": ([_P, C.c_int32], C.c_int),
     "gomix_gpu_color": ([C.POINTER(Maxcut), C.POINTER(Fos), C.c_int32, _P, C.POINTER(C.c_uint64),
                          C.POINTER(C.c_uint64)], C.c_int),
+    "gomix_gpu_nccl_unique_id": ([_P], C.c_int),
+    "gomix_gpu_local_group_create": ([_P, C.POINTER(EngineConfig), C.POINTER(_P)], C.c_int),
+    "gomix_gpu_local_group_destroy": ([_P], C.c_int),
+    "gomix_gpu_local_group_engine": ([_P, C.c_int32, C.POINTER(_P)], C.c_int),
+    "gomix_gpu_local_group_init_population": ([_P, C.POINTER(StopCriteria), C.POINTER(RunStats)], C.c_int),
+    "gomix_gpu_local_group_run_generation": ([_P, C.POINTER(StopCriteria), C.POINTER(RunStats)], C.c_int),
+    "gomix_gpu_local_group_read_elitist": ([_P, _P, C.POINTER(C.c_double)], C.c_int),
     "gomix_generate_torus": ([C.c_uint64, C.c_uint64, C.c_int32, C.c_int64, C.c_int64, C.c_uint64,
                               _P, _P, _P], C.c_int),
     "gomix_generate_regular": ([C.c_uint64, C.c_uint32, C.c_int32, C.c_int64, C.c_int64, C.c_uint64,

@@ -8,6 +8,8 @@
 // packed population back once per group to draw donors exactly like the
 // reference's sequential RngStream (engine_parallel.hpp:104-121).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: NCCL is resolved at run time with dlopen
 
 #include <algorithm>
 #include <cmath>
@@ -205,11 +207,80 @@ std::unique_ptr<Problem> create_problem(const gomix_maxcut* inst, const gomix_fo
 }  // namespace
 
 // ===========================================================================
+// NCCL, resolved at run time (the process's already-loaded libnccl.so.2, e.g.
+// PyTorch's, or the system one), so the library has no link-time dependency.
+// ===========================================================================
+namespace {
+struct NcclApi {
+  bool ok = false;
+  std::string why;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl_api() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      a.why = std::string("cannot load libnccl.so.2: ") + dlerror();
+      return a;
+    }
+#define GOMIX_SYM(field, name) a.field = reinterpret_cast<decltype(a.field)>(dlsym(h, name))
+    GOMIX_SYM(GetUniqueId, "ncclGetUniqueId");
+    GOMIX_SYM(CommInitRank, "ncclCommInitRank");
+    GOMIX_SYM(CommDestroy, "ncclCommDestroy");
+    GOMIX_SYM(AllGather, "ncclAllGather");
+    GOMIX_SYM(Broadcast, "ncclBroadcast");
+    GOMIX_SYM(GroupStart, "ncclGroupStart");
+    GOMIX_SYM(GroupEnd, "ncclGroupEnd");
+    GOMIX_SYM(GetErrorString, "ncclGetErrorString");
+#undef GOMIX_SYM
+    a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.AllGather && a.Broadcast &&
+           a.GroupStart && a.GroupEnd && a.GetErrorString;
+    if (!a.ok) a.why = "libnccl.so.2 lacks required symbols";
+    return a;
+  }();
+  return api;
+}
+
+const NcclApi& nccl_or_throw() {
+  const NcclApi& a = nccl_api();
+  if (!a.ok) throw GomixError(GOMIX_E_NCCL, a.why);
+  return a;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess)
+    throw GomixError(GOMIX_E_NCCL, std::string(what) + ": " + nccl_api().GetErrorString(r));
+}
+}  // namespace
+
+struct NcclComm {
+  ncclComm_t comm = nullptr;
+  ~NcclComm() {
+    if (comm) nccl_api().CommDestroy(comm);
+  }
+};
+
+// ===========================================================================
 // engine
 // ===========================================================================
+
 struct gomix_gpu_engine {
   Problem* P = nullptr;
-  uint64_t n = 0;
+  uint64_t n = 0;          // this rank's solutions
+  uint64_t n_global = 0;   // population size
+  uint32_t R = 1, rank = 0;
+  std::unique_ptr<NcclComm> nccl;    // one process per GPU
+  gomix_gpu_local_group* local = nullptr;  // several shards in one process
   uint32_t W = 0, Wp = 0, wpt = 1, tw = 1, block = 256, teams = 8, stage_words = 0;
   size_t smem = 0;
   int grid_cap = 1;
@@ -221,7 +292,12 @@ struct gomix_gpu_engine {
   uint64_t seed = 1;
 
   std::vector<void*> allocs;
-  uint32_t* pop = nullptr;
+  uint32_t* pool = nullptr;  // [R][nv][Wp]: every rank's rows (R == 1: the population)
+  uint32_t* pop = nullptr;   // this rank's slot of the pool
+  double* fit_all = nullptr;  // [n_global], this rank's slice at rank*n
+  unsigned long long* h1_all = nullptr;
+  unsigned long long* h2_all = nullptr;
+  unsigned long long* rank_cnt = nullptr;  // [R][steps, calls]
   double* fit = nullptr;
   double* dfit = nullptr;
   double* part = nullptr;
@@ -286,10 +362,18 @@ struct gomix_gpu_engine {
   }
 
   void setup(const gomix_engine_config& cfg) {
-    n = cfg.population_size;
-    if (n == 0) invalid("engine: population must be non-empty");
+    n_global = cfg.population_size;
+    if (n_global == 0) invalid("engine: population must be non-empty");
     if (cfg.mode != GOMIX_MODE_REPLAY && cfg.mode != GOMIX_MODE_PHILOX) invalid("engine: unknown mode");
-    if (cfg.world_size > 1) invalid("engine: multi-GPU sharding is driven by gomix_gpu_engine_create_sharded");
+    R = cfg.world_size > 1 ? (uint32_t)cfg.world_size : 1u;
+    rank = R > 1 ? (uint32_t)cfg.rank : 0u;
+    if (R > 1) {
+      if (cfg.rank < 0 || (uint32_t)cfg.rank >= R) invalid("engine: rank out of range");
+      if (cfg.mode != GOMIX_MODE_PHILOX) invalid("engine: sharded populations need GOMIX_MODE_PHILOX");
+      if (n_global % R) invalid("engine: population size must be divisible by world_size");
+      if (cfg.flags & GOMIX_FLAG_RECORD_BATCH) invalid("engine: batch recording is single-GPU only");
+    }
+    n = n_global / R;
     mode = cfg.mode;
     flags = cfg.flags;
     seed = cfg.seed;
@@ -328,8 +412,10 @@ struct gomix_gpu_engine {
     teams = block / 32 / tw;
     if (tw > 1 && teams != 1) invalid("engine: internal team layout error");
     if (!P->univariate) {
-      // patterns (64-bit per member), F rows, donor rows, new rows, Zobrist keys of F
-      stage_words = (uint32_t)(64 * Wp + 3 * P->max_f * Wp + 1 + 4 * P->max_f);
+      // patterns (64-bit per pool member), F pool rows, own donor rows, own new
+      // rows, Zobrist keys of F
+      const uint64_t RW = (uint64_t)R * Wp;
+      stage_words = (uint32_t)(64 * RW + P->max_f * RW + 2 * P->max_f * Wp + 1 + 4 * P->max_f);
       stage_words += stage_words & 1u;  // keep the next team's patterns 8-byte aligned
     }
     const size_t stage = (size_t)teams * stage_words * 4;
@@ -343,6 +429,13 @@ struct gomix_gpu_engine {
     GOMIX_CUDA(cudaSetDevice(P->device));
     GOMIX_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     own_stream = true;
+    if (R > 1 && cfg.nccl_unique_id) {  // one process per GPU: collective communicator
+      const NcclApi& api = nccl_or_throw();
+      ncclUniqueId id;
+      std::memcpy(&id, cfg.nccl_unique_id, sizeof(id));
+      nccl = std::make_unique<NcclComm>();
+      nccl_check(api.CommInitRank(&nccl->comm, (int)R, id, (int)rank), "ncclCommInitRank");
+    }
     const int per_sm = gom_max_blocks_per_sm(P->univariate, P->i32, (int)wpt, tw > 1, (int)block, smem);
     if (per_sm < 1) invalid("engine: GOM kernel does not fit on an SM with this configuration");
     grid_cap = per_sm * sms;
@@ -350,11 +443,16 @@ struct gomix_gpu_engine {
       max_group = std::max(max_group, P->group_off[c + 1] - P->group_off[c]);
 
     const uint64_t nv = P->nv;
-    pop = dev_alloc<uint32_t>(allocs, nv * Wp);
-    fit = dev_alloc<double>(allocs, n);
+    pool = dev_alloc<uint32_t>(allocs, (uint64_t)R * nv * Wp);
+    pop = pool + (uint64_t)rank * nv * Wp;
+    fit_all = dev_alloc<double>(allocs, n_global);
+    h1_all = dev_alloc<unsigned long long>(allocs, n_global);
+    h2_all = dev_alloc<unsigned long long>(allocs, n_global);
+    rank_cnt = dev_alloc<unsigned long long>(allocs, 2 * (uint64_t)R);
+    fit = fit_all + (uint64_t)rank * n;
+    h1 = h1_all + (uint64_t)rank * n;
+    h2 = h2_all + (uint64_t)rank * n;
     dfit = dev_alloc<double>(allocs, n);
-    h1 = dev_alloc<unsigned long long>(allocs, n);
-    h2 = dev_alloc<unsigned long long>(allocs, n);
     dh1 = dev_alloc<unsigned long long>(allocs, n);
     dh2 = dev_alloc<unsigned long long>(allocs, n);
     ever = dev_alloc<uint32_t>(allocs, nv);
@@ -362,7 +460,7 @@ struct gomix_gpu_engine {
     ctl = dev_alloc<DevCtl>(allocs, 1);
     gsteps = dev_alloc<unsigned long long>(allocs, P->k);
     gcalls = dev_alloc<unsigned long long>(allocs, P->k);
-    impr_cap = std::min<uint64_t>(std::max<uint64_t>(4096, n * (P->k + 1)), 1ull << 22);
+    impr_cap = std::min<uint64_t>(std::max<uint64_t>(4096, n_global * (P->k + 1)), 1ull << 22);
     impr = dev_alloc<double>(allocs, impr_cap);
     impr_calls = dev_alloc<unsigned long long>(allocs, impr_cap);
     if (epi_mode == 1) part = dev_alloc<double>(allocs, (size_t)grid_cap * n);
@@ -389,7 +487,7 @@ struct gomix_gpu_engine {
     h_ctl->exact = P->exact;
     h_ctl->q = (double)P->q;
     GOMIX_CUDA(cudaMemcpy(ctl, h_ctl, sizeof(DevCtl), cudaMemcpyHostToDevice));
-    GOMIX_CUDA(cudaMemset(pop, 0, nv * Wp * 4));
+    GOMIX_CUDA(cudaMemset(pool, 0, (uint64_t)R * nv * Wp * 4));
     GOMIX_CUDA(cudaMemset(gsteps, 0, P->k * 8));
     GOMIX_CUDA(cudaMemset(gcalls, 0, P->k * 8));
     GOMIX_CUDA(cudaMemset(dfit, 0, n * 8));
@@ -472,6 +570,7 @@ struct gomix_gpu_engine {
   SnapArgs snap_args() const {
     SnapArgs r;
     r.pop = pop;
+    r.pool = pool;
     r.elit = elit;
     r.ever = ever;
     r.ctl = ctl;
@@ -500,6 +599,13 @@ struct gomix_gpu_engine {
     e.impr = impr;
     e.impr_calls = impr_calls;
     e.impr_cap = impr_cap;
+    e.fit_all = fit_all;
+    e.h1_all = h1_all;
+    e.h2_all = h2_all;
+    e.rank_cnt = rank_cnt;
+    e.n_global = (uint32_t)n_global;
+    e.R = R;
+    e.rank = rank;
     e.n = (uint32_t)n;
     e.G = G;
     e.nparts = nparts;
@@ -546,6 +652,11 @@ struct gomix_gpu_engine {
     a.rec_accept = rec ? rec_accept : nullptr;
     a.n = (uint32_t)n;
     a.Wp = Wp;
+    a.pool = pool;
+    a.nv = P->nv;
+    a.R = R;
+    a.rank = rank;
+    a.n_global = (uint32_t)n_global;
     a.team_warps = tw;
     a.stage_words = stage_words;
     a.exact = P->exact;
@@ -650,12 +761,18 @@ struct gomix_gpu_engine {
       GOMIX_CUDA(cudaMemcpyAsync(pop, words.data(), nv * Wp * 4, cudaMemcpyHostToDevice, stream));
       GOMIX_CUDA(cudaStreamSynchronize(stream));
     } else {
-      launch_philox_init(pop, nv, (uint32_t)n, Wp, seed, stream);
+      launch_philox_init(pop, nv, (uint32_t)n, Wp, seed, rank, stream);
       ++launches;
     }
     launch_full_eval(*P, pop, fit, (uint32_t)n, Wp, !P->exact, stream);
     launch_hash_population(snap_args(), stream);
     launches += 2;
+    if (R > 1 && nccl) exchange();
+    if (R == 1 || nccl) init_global(stop, out);
+  }
+
+  // the part of init after every rank's fitness and hashes are known
+  void init_global(const gomix_stop_criteria* stop, gomix_run_stats* out) {
     begin_call(stop);
     launch_init_epilogue(epi_args(0, 0, 0), stream);
     ++launches;
@@ -664,8 +781,60 @@ struct gomix_gpu_engine {
     initialized = true;
   }
 
+  // ---- sharding ---------------------------------------------------------------
+  // Per-rank chunks exchanged after every group: rows (the donor pool of the
+  // next group, engine_parallel.hpp:100-103), fitness, hashes, counters.
+  struct Chunk {
+    void* base;
+    size_t bytes;  // rank r's chunk sits at base + r * bytes
+  };
+  std::vector<Chunk> shard_chunks() const {
+    return {{pool, P->nv * Wp * 4}, {fit_all, n * 8}, {h1_all, n * 8}, {h2_all, n * 8}, {rank_cnt, 16}};
+  }
+
+  // all-gather over NCCL (in place), one grouped call
+  void exchange() {
+    const NcclApi& api = nccl_or_throw();
+    nccl_check(api.GroupStart(), "ncclGroupStart");
+    for (const Chunk& c : shard_chunks())
+      nccl_check(api.AllGather(static_cast<char*>(c.base) + rank * c.bytes, c.base, c.bytes, ncclUint8,
+                               nccl->comm, stream),
+                 "ncclAllGather");
+    nccl_check(api.GroupEnd(), "ncclGroupEnd");
+  }
+
+  void global_epilogue(uint64_t group) {
+    const uint64_t G = P->group_off[group + 1] - P->group_off[group];
+    launch_global_epilogue(epi_args(group, (uint32_t)G, 0), stream);
+    ++launches;
+  }
+
+  // sharded generation (NCCL): local GOM step, exchange, global epilogue per group
+  void run_generation_sharded(const gomix_stop_criteria* stop, gomix_run_stats* out) {
+    begin_call(stop);
+    std::vector<uint64_t> order;
+    rng.permutation(order, P->k);  // same seed on every rank: same order
+    for (uint64_t gi : order) {
+      launch_group(gi, false);
+      exchange();
+      global_epilogue(gi);
+    }
+    read_ctl();
+    fill_stats(out);
+    if (!h_ctl->stop) ++generation;
+  }
+
+  int32_t elitist_owner() const {
+    return h_ctl->elit_src >= 0 ? (int32_t)((uint64_t)h_ctl->elit_src / n) : -1;
+  }
+
   void run_generation(const gomix_stop_criteria* stop, gomix_run_stats* out) {
     if (!initialized) throw GomixError(GOMIX_E_STATE, "run_generation: population not initialised");
+    if (R > 1) {
+      if (!nccl) throw GomixError(GOMIX_E_STATE, "run_generation: in-process shards are driven by their local group");
+      run_generation_sharded(stop, out);
+      return;
+    }
     if (mode == GOMIX_MODE_PHILOX && no_criteria(stop) && !(flags & GOMIX_FLAG_TIME_KERNELS)) {
       launch_generation_graph();
       read_ctl();
@@ -696,6 +865,7 @@ struct gomix_gpu_engine {
   void run_generation_async() {
     if (!initialized) throw GomixError(GOMIX_E_STATE, "run_generation: population not initialised");
     if (mode != GOMIX_MODE_PHILOX) invalid("run_generation_async: needs GOMIX_MODE_PHILOX");
+    if (R > 1) invalid("run_generation_async: single-GPU engines only");
     if (flags & GOMIX_FLAG_TIME_KERNELS) {
       begin_call(nullptr);
       std::vector<uint64_t> order;
@@ -716,6 +886,7 @@ struct gomix_gpu_engine {
   // (NULL = evaluate on the device); the elitist is kept.
   void load_population(const uint8_t* genotypes, const double* fitness) {
     if (!initialized) throw GomixError(GOMIX_E_STATE, "load_population: population not initialised");
+    if (R > 1) invalid("load_population: single-GPU engines only");
     const uint64_t nv = P->nv;
     // the elitist snapshot may still point into the old population: finish it
     launch_finalize_elitist(snap_args(), stream);
@@ -738,6 +909,7 @@ struct gomix_gpu_engine {
   void run_group(uint64_t group, const int32_t* donor_tape, const gomix_stop_criteria* stop,
                  gomix_run_stats* out) {
     if (!initialized) throw GomixError(GOMIX_E_STATE, "run_group: population not initialised");
+    if (R > 1) invalid("run_group: single-GPU engines only");
     if (group >= P->k) invalid("run_group: group index out of range");
     begin_call(stop);
     bool with_tape = true;
@@ -750,6 +922,98 @@ struct gomix_gpu_engine {
     launch_group(group, with_tape);
     read_ctl();
     fill_stats(out);
+  }
+};
+
+// ===========================================================================
+// In-process shards: R engines (one per device, or several on one device)
+// driven in lock step by one host thread; the exchange is device-to-device
+// copies ordered by events.  Same arithmetic as the NCCL path.
+// ===========================================================================
+struct gomix_gpu_local_group {
+  std::vector<std::unique_ptr<gomix_gpu_engine>> eng;
+  std::vector<cudaEvent_t> ev_step, ev_done;
+
+  ~gomix_gpu_local_group() {
+    for (auto& e : eng)
+      if (e && e->stream) cudaStreamSynchronize(e->stream);
+    for (auto e : ev_step) cudaEventDestroy(e);
+    for (auto e : ev_done) cudaEventDestroy(e);
+  }
+
+  uint32_t R() const { return (uint32_t)eng.size(); }
+
+  void set_device(uint32_t r) { GOMIX_CUDA(cudaSetDevice(eng[r]->P->device)); }
+
+  // every engine finished its local step -> copy every rank's chunks everywhere
+  void exchange() {
+    for (uint32_t r = 0; r < R(); ++r) {
+      set_device(r);
+      GOMIX_CUDA(cudaEventRecord(ev_step[r], eng[r]->stream));
+    }
+    for (uint32_t d = 0; d < R(); ++d) {
+      set_device(d);
+      gomix_gpu_engine& dst = *eng[d];
+      const auto dchunks = dst.shard_chunks();
+      for (uint32_t r = 0; r < R(); ++r) {
+        if (r == d) continue;
+        GOMIX_CUDA(cudaStreamWaitEvent(dst.stream, ev_step[r], 0));
+        const auto schunks = eng[r]->shard_chunks();
+        for (size_t c = 0; c < dchunks.size(); ++c)
+          GOMIX_CUDA(cudaMemcpyAsync(static_cast<char*>(dchunks[c].base) + r * dchunks[c].bytes,
+                                     static_cast<const char*>(schunks[c].base) + r * schunks[c].bytes,
+                                     dchunks[c].bytes, cudaMemcpyDefault, dst.stream));
+      }
+      GOMIX_CUDA(cudaEventRecord(ev_done[d], dst.stream));
+    }
+    // nobody overwrites its rows before every copy out of them is done
+    for (uint32_t r = 0; r < R(); ++r) {
+      set_device(r);
+      for (uint32_t d = 0; d < R(); ++d)
+        if (d != r) GOMIX_CUDA(cudaStreamWaitEvent(eng[r]->stream, ev_done[d], 0));
+    }
+  }
+
+  void init(const gomix_stop_criteria* stop, gomix_run_stats* out) {
+    for (uint32_t r = 0; r < R(); ++r) {
+      set_device(r);
+      eng[r]->init_population(nullptr, stop, nullptr);
+    }
+    exchange();
+    for (uint32_t r = 0; r < R(); ++r) {
+      set_device(r);
+      eng[r]->init_global(stop, r == 0 ? out : nullptr);
+    }
+  }
+
+  void run_generation(const gomix_stop_criteria* stop, gomix_run_stats* out) {
+    for (auto& e : eng)
+      if (!e->initialized) throw GomixError(GOMIX_E_STATE, "run_generation: population not initialised");
+    std::vector<uint64_t> order;
+    for (uint32_t r = 0; r < R(); ++r) {
+      set_device(r);
+      eng[r]->begin_call(stop);
+      std::vector<uint64_t> o;
+      eng[r]->rng.permutation(o, eng[r]->P->k);
+      if (r == 0) order = o;
+    }
+    for (uint64_t gi : order) {
+      for (uint32_t r = 0; r < R(); ++r) {
+        set_device(r);
+        eng[r]->launch_group(gi, false);
+      }
+      exchange();
+      for (uint32_t r = 0; r < R(); ++r) {
+        set_device(r);
+        eng[r]->global_epilogue(gi);
+      }
+    }
+    for (uint32_t r = 0; r < R(); ++r) {
+      set_device(r);
+      eng[r]->read_ctl();
+      eng[r]->fill_stats(r == 0 ? out : nullptr);
+      if (!eng[r]->h_ctl->stop) ++eng[r]->generation;
+    }
   }
 };
 
@@ -946,13 +1210,22 @@ int gomix_gpu_read_elitist(gomix_gpu_engine* e, uint8_t* genotype, double* fitne
     if (!e->initialized) throw GomixError(GOMIX_E_STATE, "read_elitist: population not initialised");
     if (genotype) {
       launch_finalize_elitist(e->snap_args(), e->stream);  // complete the copy-on-write snapshot
-      uint8_t* d = nullptr;
-      GOMIX_CUDA(cudaMallocAsync(&d, e->P->nv, e->stream));
+      ++e->launches;
+      if (e->R > 1) {
+        // collective over the ranks: the owner's snapshot is the valid one
+        if (!e->nccl) invalid("read_elitist: use gomix_gpu_local_group_read_elitist for in-process shards");
+        const int32_t owner = e->elitist_owner();
+        if (owner >= 0) {
+          const NcclApi& api = nccl_or_throw();
+          nccl_check(api.Broadcast(e->elit, e->elit, ((e->P->nv + 31) / 32) * 4, ncclUint8, owner,
+                                   e->nccl->comm, e->stream),
+                     "ncclBroadcast");
+        }
+      }
+      uint8_t* d = e->staging();
       launch_unpack_elitist(e->elit, d, e->P->nv, e->stream);
       ++e->launches;
-      ++e->launches;
       GOMIX_CUDA(cudaMemcpyAsync(genotype, d, e->P->nv, cudaMemcpyDeviceToHost, e->stream));
-      GOMIX_CUDA(cudaFreeAsync(d, e->stream));
     }
     GOMIX_CUDA(cudaStreamSynchronize(e->stream));
     if (fitness) *fitness = e->elit_fit;
@@ -1069,6 +1342,90 @@ int gomix_gpu_color(const gomix_maxcut* instance, const gomix_fos* fos, int32_t 
           set_colour[P->group_sets[t]] = (int32_t)c;
     if (num_groups) *num_groups = P->k;
     if (lmig_edges) *lmig_edges = P->lmig_edges;
+  });
+}
+
+int gomix_gpu_nccl_unique_id(uint8_t* id) {
+  return guarded([&] {
+    if (!id) invalid("nccl_unique_id: NULL buffer");
+    const NcclApi& api = nccl_or_throw();
+    ncclUniqueId u;
+    nccl_check(api.GetUniqueId(&u), "ncclGetUniqueId");
+    std::memcpy(id, &u, sizeof(u));
+  });
+}
+
+int gomix_gpu_local_group_create(gomix_gpu_problem* const* problems, const gomix_engine_config* cfg,
+                                 gomix_gpu_local_group** out) {
+  return guarded([&] {
+    if (!problems || !cfg || !out) invalid("local_group_create: NULL argument");
+    if (cfg->world_size < 1) invalid("local_group_create: world_size must be >= 1");
+    *out = nullptr;
+    auto g = std::make_unique<gomix_gpu_local_group>();
+    for (int32_t r = 0; r < cfg->world_size; ++r) {
+      if (!problems[r]) invalid("local_group_create: NULL problem");
+      gomix_engine_config c = *cfg;
+      c.rank = r;
+      c.nccl_unique_id = nullptr;
+      auto e = std::make_unique<gomix_gpu_engine>();
+      e->P = problems[r]->P.get();
+      if (e->P->nv != problems[0]->P->nv || e->P->k != problems[0]->P->k)
+        invalid("local_group_create: every rank needs the same problem");
+      e->setup(c);
+      e->local = g.get();
+      cudaEvent_t a, b;
+      GOMIX_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+      GOMIX_CUDA(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+      g->ev_step.push_back(a);
+      g->ev_done.push_back(b);
+      g->eng.push_back(std::move(e));
+    }
+    *out = g.release();
+  });
+}
+
+int gomix_gpu_local_group_destroy(gomix_gpu_local_group* g) {
+  return guarded([&] { delete g; });
+}
+
+int gomix_gpu_local_group_engine(gomix_gpu_local_group* g, int32_t rank, gomix_gpu_engine** out) {
+  return guarded([&] {
+    if (!g || !out || rank < 0 || (uint32_t)rank >= g->R()) invalid("local_group_engine: bad argument");
+    *out = g->eng[rank].get();
+  });
+}
+
+int gomix_gpu_local_group_init_population(gomix_gpu_local_group* g, const gomix_stop_criteria* stop,
+                                          gomix_run_stats* out) {
+  return guarded([&] {
+    if (!g) invalid("local_group_init_population: NULL group");
+    g->init(stop, out);
+  });
+}
+
+int gomix_gpu_local_group_run_generation(gomix_gpu_local_group* g, const gomix_stop_criteria* stop,
+                                         gomix_run_stats* out) {
+  return guarded([&] {
+    if (!g) invalid("local_group_run_generation: NULL group");
+    g->run_generation(stop, out);
+  });
+}
+
+int gomix_gpu_local_group_read_elitist(gomix_gpu_local_group* g, uint8_t* genotype, double* fitness) {
+  return guarded([&] {
+    if (!g) invalid("local_group_read_elitist: NULL group");
+    gomix_gpu_engine& e0 = *g->eng[0];
+    const int32_t owner = e0.elitist_owner();
+    gomix_gpu_engine& e = *g->eng[owner >= 0 ? owner : 0];
+    GOMIX_CUDA(cudaSetDevice(e.P->device));
+    if (genotype) {
+      launch_finalize_elitist(e.snap_args(), e.stream);
+      uint8_t* d = e.staging();
+      launch_unpack_elitist(e.elit, d, e.P->nv, e.stream);
+      GOMIX_CUDA(cudaMemcpyAsync(genotype, d, e.P->nv, cudaMemcpyDeviceToHost, e.stream));
+      GOMIX_CUDA(cudaStreamSynchronize(e.stream));
+    }
+    if (fitness) *fitness = e0.elit_fit;
   });
 }
 

@@ -103,12 +103,14 @@ __device__ __forceinline__ void team_sync(uint32_t tw, uint32_t, uint32_t) {
 }
 
 // Members of word w2 that differ from pattern m somewhere on F.
-__device__ __forceinline__ uint32_t differ_word(const uint32_t* rowsF, uint32_t f, uint32_t Wp,
-                                                uint32_t w2, uint64_t m, uint32_t n) {
+// word wg of the staged pool (stride RW per row; Wp words per rank's shard of
+// n members).
+__device__ __forceinline__ uint32_t differ_word(const uint32_t* rowsF, uint32_t f, uint32_t RW,
+                                                uint32_t wg, uint64_t m, uint32_t n, uint32_t Wp) {
   uint32_t dw = 0;
   for (uint32_t jv = 0; jv < f; ++jv)
-    dw |= rowsF[jv * Wp + w2] ^ (((m >> jv) & 1ull) ? 0xFFFFFFFFu : 0u);
-  return dw & valid_mask(w2, n);
+    dw |= rowsF[jv * RW + wg] ^ (((m >> jv) & 1ull) ? 0xFFFFFFFFu : 0u);
+  return dw & valid_mask(wg % Wp, n);
 }
 
 // 32x32 bit-matrix transpose across a warp: lane r holds row r on entry;
@@ -166,12 +168,10 @@ __device__ void note_improvement(const EpiArgs& a, double f) {
     request_stop(c, GOMIX_STOP_TARGET);
 }
 
-__device__ void epilogue_body(const EpiArgs& a) {
-  DevCtl* c = a.ctl;
+// Commit this rank's group deltas: fitness (exact atomics / float partials /
+// reference-ordered recorded deltas) and Zobrist hashes of its n solutions.
+__device__ void commit_local(const EpiArgs& a, double* s_fit) {
   const uint32_t n = a.n;
-  __shared__ double s_chunkmax[32];
-  __shared__ int32_t s_best;
-  __shared__ double s_fit[kEpiSmemFit];  // this group's fitness, scanned without global loads
   for (uint32_t s = threadIdx.x; s < n; s += blockDim.x) {
     double f = a.fit[s];
     if (a.mode == 2) {
@@ -186,16 +186,46 @@ __device__ void epilogue_body(const EpiArgs& a) {
       a.dfit[s] = 0.0;
     }
     a.fit[s] = f;
-    if (s < kEpiSmemFit) s_fit[s] = f;
+    if (s_fit && s < kEpiSmemFit) s_fit[s] = f;
     a.h1[s] ^= a.dh1[s];
     a.h2[s] ^= a.dh2[s];
     a.dh1[s] = 0;
     a.dh2[s] = 0;
   }
-  if (threadIdx.x == 0) {
-    const unsigned long long st = c->grp_steps, ca = c->grp_calls;
+  if (a.R > 1 && threadIdx.x == 0) {  // this rank's counters, all-gathered next
+    DevCtl* c = a.ctl;
+    a.rank_cnt[2 * a.rank] = c->grp_steps;
+    a.rank_cnt[2 * a.rank + 1] = c->grp_calls;
     c->grp_steps = 0;
     c->grp_calls = 0;
+  }
+}
+
+// Evaluator-call accounting (budget stop first, runtime.hpp:75-80), then the
+// elitist scan of engine_parallel.hpp:305-310 over all n_global members in
+// index order — the first member strictly better than the running elitist
+// replaces it and the scan continues against the new value — logging every
+// improvement with the call count at that moment and latching the target stop
+// (runtime.hpp:88-93,136-143).  Sharded runs execute it on every rank from the
+// gathered state, so all ranks take identical decisions.
+__device__ void elitist_scan(const EpiArgs& a, const double* s_fit) {
+  DevCtl* c = a.ctl;
+  const uint32_t n = a.n_global;
+  __shared__ double s_chunkmax[32];
+  __shared__ int32_t s_best;
+  if (threadIdx.x == 0) {
+    unsigned long long st = 0, ca = 0;
+    if (a.R > 1) {
+      for (uint32_t r = 0; r < a.R; ++r) {
+        st += a.rank_cnt[2 * r];
+        ca += a.rank_cnt[2 * r + 1];
+      }
+    } else {
+      st = c->grp_steps;
+      ca = c->grp_calls;
+      c->grp_steps = 0;
+      c->grp_calls = 0;
+    }
     c->calls_total += ca;
     c->run_steps += st;
     c->run_calls += ca;
@@ -209,7 +239,7 @@ __device__ void epilogue_body(const EpiArgs& a) {
   __syncthreads();
   // chunk maxima let the serial scan skip chunks that cannot hold a record
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u, nwarps = blockDim.x >> 5;
-  auto fit_at = [&](uint32_t s) { return s < kEpiSmemFit ? s_fit[s] : a.fit[s]; };
+  auto fit_at = [&](uint32_t s) { return (s_fit && s < kEpiSmemFit) ? s_fit[s] : a.fit_all[s]; };
   for (uint32_t chunk = warp; chunk * 32u < n && chunk < 32; chunk += nwarps) {
     const uint32_t s = chunk * 32u + lane;
     double f = s < n ? fit_at(s) : -INFINITY;
@@ -252,14 +282,28 @@ __device__ void epilogue_body(const EpiArgs& a) {
       if (best >= 0) {  // new elitist: member `best` (snapshot taken copy-on-write)
         c->elit_fit = cur;
         c->elit_src = best;
-        c->eh1 = a.h1[best];
-        c->eh2 = a.h2[best];
+        c->eh1 = a.h1_all[best];
+        c->eh2 = a.h2_all[best];
         c->elit_ver += 1;
       }
       s_best = best;
     }
   }
   __syncthreads();
+}
+
+__device__ void epilogue_body(const EpiArgs& a) {
+  __shared__ double s_fit[kEpiSmemFit];  // this group's fitness, scanned without global loads
+  commit_local(a, a.R == 1 ? s_fit : nullptr);
+  __syncthreads();
+  if (a.R == 1) elitist_scan(a, s_fit);
+}
+
+// Sharded runs: after the all-gather of populations, fitness, hashes and
+// counters, every rank runs the same scan.
+__global__ void global_epilogue_kernel(const EpiArgs a) {
+  if (*(volatile int32_t*)&a.ctl->stop) return;
+  elitist_scan(a, nullptr);
 }
 
 // ---------------------------------------------------------------------------
@@ -303,7 +347,10 @@ __global__ void finalize_elitist_kernel(const SnapArgs a) {
   const DevCtl* c = a.ctl;
   const int32_t src = c->elit_src;
   if (src < 0) return;
-  const uint32_t ver = c->elit_ver, sw = (uint32_t)src >> 5, sb = (uint32_t)src & 31u;
+  // column of global member src: shard src / n, local index src % n
+  const uint32_t owner = (uint32_t)src / a.n, loc = (uint32_t)src % a.n;
+  const uint32_t ver = c->elit_ver, sw = loc >> 5, sb = loc & 31u;
+  const uint32_t* rows = a.pool + (uint64_t)owner * a.nv * a.Wp;
   const uint64_t words = (a.nv + 31) / 32;
   for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < words;
        t += (uint64_t)gridDim.x * blockDim.x) {
@@ -311,7 +358,7 @@ __global__ void finalize_elitist_kernel(const SnapArgs a) {
     for (uint32_t k = 0; k < 32 && t * 32 + k < a.nv; ++k) {
       const uint64_t v = t * 32 + k;
       if (a.ever[v] != ver) {
-        const uint32_t b = (a.pop[v * a.Wp + sw] >> sb) & 1u;
+        const uint32_t b = (rows[v * a.Wp + sw] >> sb) & 1u;
         word = (word & ~(1u << k)) | (b << k);
         a.ever[v] = ver;
       }
@@ -483,9 +530,13 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
       for (int j = 0; j < WPT; ++j) pw[j] = 0;
       load_words<WPT, TEAM>(row, wit, tw, pw);
       const int32_t rs = a.row_ptr[v], re = a.row_ptr[v + 1];
-      uint32_t ones = 0;
+      uint32_t ones = 0;  // members holding 1 at v, over every rank's shard
       if (!replay) {
-        if (tw == 1) {
+        if (a.R > 1) {
+          for (uint32_t wg = lane; wg < a.R * Wp; wg += 32)
+            ones += __popc(a.pool[((size_t)(wg / Wp) * a.nv + v) * Wp + (wg % Wp)]);
+          ones = __reduce_add_sync(0xFFFFFFFFu, ones);
+        } else if (tw == 1) {
 #pragma unroll
           for (int j = 0; j < WPT; ++j) ones += __popc(pw[j]);
         } else {
@@ -536,7 +587,7 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
       }
       // phases 3 + 4.  Philox mode: a singleton pair is present iff the row
       // holds both values among the members (per set, all or nothing).
-      const bool set_present = ones > 0u && ones < n;
+      const bool set_present = ones > 0u && ones < a.n_global;
       uint32_t accb = 0;  // bit j: this lane accepted in word j
       uint32_t nw[WPT];
 #pragma unroll
@@ -573,7 +624,7 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
         }
         nw[j] = pw[j] ^ __ballot_sync(0xFFFFFFFFu, accept);  // accepted members flip v
         accb |= accept ? (1u << j) : 0u;
-        if (accept && (int32_t)s == esrc) capture_row(a.elit, a.ever, ever_cur, v, pv);
+        if (accept && (int32_t)(a.rank * n + s) == esrc) capture_row(a.elit, a.ever, ever_cur, v, pv);
         steps += present ? 1u : 0u;
         calls += present ? deg : 0u;
         if (record && valid) {
@@ -605,13 +656,15 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
       const uint32_t f = gm.w >> 24;
       const uint32_t* vars = a.set_vars + gm.y;
       const uint32_t e0 = gm.z, e1 = gm.z + (gm.w & 0xFFFFFFu);
-      uint64_t* patt = reinterpret_cast<uint64_t*>(stage);
-      uint32_t* rowsF = stage + 64u * Wp;
-      uint32_t* newD = rowsF + f * Wp;
-      uint32_t* newF = newD + f * Wp;
-      for (uint32_t idx = tid_team; idx < f * Wp; idx += team_threads) {
-        const uint32_t jv = idx / Wp, w = idx - jv * Wp;
-        rowsF[idx] = a.pop[(size_t)vars[jv] * Wp + w];
+      // pool words: RW = R*Wp per row (every rank's shard; R == 1: the population)
+      const uint32_t RW = a.R * Wp, own = a.rank * Wp;
+      uint64_t* patt = reinterpret_cast<uint64_t*>(stage);  // pattern of every member (padded index)
+      uint32_t* rowsF = stage + 64u * RW;                    // F rows at group start, stride RW
+      uint32_t* newD = rowsF + f * RW;                       // own donor-inserted rows, stride Wp
+      uint32_t* newF = newD + f * Wp;                        // own committed rows, stride Wp
+      for (uint32_t idx = tid_team; idx < f * RW; idx += team_threads) {
+        const uint32_t jv = idx / RW, wg = idx - jv * RW;
+        rowsF[idx] = a.pool[((size_t)(wg / Wp) * a.nv + vars[jv]) * Wp + (wg % Wp)];
       }
       // first footprint chunk: entry per lane and its outside row, fetched
       // now so the loads overlap the staging above
@@ -634,16 +687,15 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
       for (uint32_t jv = tid_team; jv < f; jv += team_threads) zobrist(vars[jv], zF[2 * jv], zF[2 * jv + 1]);
       const uint64_t fm = f >= 64 ? ~0ull : ((1ull << f) - 1ull);
       team_sync(tw, teams_per_cta, team);
-      uint64_t pm[WPT];
-#pragma unroll
-      for (int j = 0; j < WPT; ++j) {
-        const uint32_t w = wit + tw * j;
+      for (uint32_t wg = wit; wg < RW; wg += tw) {
         uint64_t m = 0;
-        for (uint32_t jv = 0; jv < f; ++jv) m |= (uint64_t)((rowsF[jv * Wp + w] >> lane) & 1u) << jv;
-        pm[j] = m;
-        patt[w * 32u + lane] = m;
+        for (uint32_t jv = 0; jv < f; ++jv) m |= (uint64_t)((rowsF[jv * RW + wg] >> lane) & 1u) << jv;
+        patt[wg * 32u + lane] = m;
       }
       team_sync(tw, teams_per_cta, team);
+      uint64_t pm[WPT];
+#pragma unroll
+      for (int j = 0; j < WPT; ++j) pm[j] = patt[(own + wit + tw * j) * 32u + lane];
 
       // phase 1: donors
       uint64_t dm[WPT];
@@ -653,6 +705,7 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
       for (int j = 0; j < WPT; ++j) {
         const uint32_t w = wit + tw * j;
         const uint32_t s = w * 32u + lane;
+        const uint32_t sg = a.rank * n + s;  // global member index (Philox counter, donors)
         const uint64_t m = pm[j];
         int32_t d = -1;
         uint64_t x = m;
@@ -665,16 +718,17 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
             // the lazy Fisher-Yates scan of engine_serial.hpp:30-46: rejection
             // sampling first, exact count-and-select when it keeps failing.
             const uint2 key = make_uint2((uint32_t)a.seed, (uint32_t)(a.seed >> 32));
+            const uint32_t ng = a.n_global, pad = 32u * Wp;
             for (uint32_t call = 0; call < 2 && d < 0; ++call) {
-              const uint4 r = philox4x32_10(make_uint4(s, sid, generation, kTagGom | call), key);
-              const uint32_t c0 = bounded(lo64(r), n);
-              const uint64_t x0 = patt[c0];
+              const uint4 r = philox4x32_10(make_uint4(sg, sid, generation, kTagGom | call), key);
+              const uint32_t c0 = bounded(lo64(r), ng);
+              const uint64_t x0 = patt[(c0 / n) * pad + c0 % n];
               if (x0 != m) {
                 d = (int32_t)c0;
                 x = x0;
               } else {
-                const uint32_t c1 = bounded(hi64(r), n);
-                const uint64_t x1 = patt[c1];
+                const uint32_t c1 = bounded(hi64(r), ng);
+                const uint64_t x1 = patt[(c1 / n) * pad + c1 % n];
                 if (x1 != m) {
                   d = (int32_t)c1;
                   x = x1;
@@ -683,20 +737,21 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
             }
             if (d < 0) {
               uint32_t total = 0;
-              for (uint32_t w2 = 0; w2 < Wp; ++w2) total += __popc(differ_word(rowsF, f, Wp, w2, m, n));
+              for (uint32_t wg = 0; wg < RW; ++wg) total += __popc(differ_word(rowsF, f, RW, wg, m, n, Wp));
               if (total > 0) {
-                const uint4 r = philox4x32_10(make_uint4(s, sid, generation, kTagGom | 2u), key);
+                const uint4 r = philox4x32_10(make_uint4(sg, sid, generation, kTagGom | 2u), key);
                 uint32_t kth = bounded(lo64(r), total);
-                for (uint32_t w2 = 0; w2 < Wp; ++w2) {
-                  const uint32_t dw = differ_word(rowsF, f, Wp, w2, m, n);
+                for (uint32_t wg = 0; wg < RW; ++wg) {
+                  const uint32_t dw = differ_word(rowsF, f, RW, wg, m, n, Wp);
                   const uint32_t c = __popc(dw);
                   if (kth < c) {
-                    d = (int32_t)(w2 * 32u + select_bit(dw, kth));
+                    const uint32_t b = select_bit(dw, kth);
+                    d = (int32_t)((wg / Wp) * n + (wg % Wp) * 32u + b);
+                    x = patt[wg * 32u + b];
                     break;
                   }
                   kth -= c;
                 }
-                x = patt[d];
               }
             }
           }
@@ -746,7 +801,8 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
           for (int j = 0; j < WPT; ++j) xw[j] = a.pop[(size_t)ext * Wp + wit + tw * j];
         }
         const bool ina = E.a & kInSet, inb = E.b & kInSet;
-        const uint32_t ja = (E.a & ~kInSet) * Wp, jb = (E.b & ~kInSet) * Wp;
+        const uint32_t ja = (E.a & ~kInSet) * Wp, jb = (E.b & ~kInSet) * Wp;            // newD rows
+        const uint32_t jaR = (E.a & ~kInSet) * RW + own, jbR = (E.b & ~kInSet) * RW + own;  // own old rows
         if constexpr (I32) {
           // lane t = entry t: old / new cut words for 32 solutions at once,
           // transposed so lane s holds its solution's entry masks, then delta
@@ -756,8 +812,8 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
 #pragma unroll
           for (int j = 0; j < WPT; ++j) {
             const uint32_t w = wit + tw * j;
-            const uint32_t aO = ina ? rowsF[ja + w] : xw[j], aN = ina ? newD[ja + w] : xw[j];
-            const uint32_t bO = inb ? rowsF[jb + w] : xw[j], bN = inb ? newD[jb + w] : xw[j];
+            const uint32_t aO = ina ? rowsF[jaR + w] : xw[j], aN = ina ? newD[ja + w] : xw[j];
+            const uint32_t bO = inb ? rowsF[jbR + w] : xw[j], bN = inb ? newD[jb + w] : xw[j];
             const uint32_t mo = transpose32((aO ^ bO) & (E.w != 0.0 ? 0xFFFFFFFFu : 0u), lane);
             const uint32_t mn = transpose32((aN ^ bN) & (E.w != 0.0 ? 0xFFFFFFFFu : 0u), lane);
             int32_t d = 0;
@@ -775,13 +831,14 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
             const uint32_t cb = __shfl_sync(0xFFFFFFFFu, E.b, t);
             const bool ina_t = ca & kInSet, inb_t = cb & kInSet;
             const uint32_t ja_t = (ca & ~kInSet) * Wp, jb_t = (cb & ~kInSet) * Wp;
+            const uint32_t jaR_t = (ca & ~kInSet) * RW + own, jbR_t = (cb & ~kInSet) * RW + own;
             const double wt = shfl_d(E.w, t);
 #pragma unroll
             for (int j = 0; j < WPT; ++j) {
               const uint32_t w = wit + tw * j;
               const uint32_t xo = (ina_t && inb_t) ? 0u : __shfl_sync(0xFFFFFFFFu, xw[j], t);
-              const uint32_t aO = ina_t ? rowsF[ja_t + w] : xo, aN = ina_t ? newD[ja_t + w] : xo;
-              const uint32_t bO = inb_t ? rowsF[jb_t + w] : xo, bN = inb_t ? newD[jb_t + w] : xo;
+              const uint32_t aO = ina_t ? rowsF[jaR_t + w] : xo, aN = ina_t ? newD[ja_t + w] : xo;
+              const uint32_t bO = inb_t ? rowsF[jbR_t + w] : xo, bN = inb_t ? newD[jb_t + w] : xo;
               sn[j] += (((aN ^ bN) >> lane) & 1u) ? wt : 0.0;
               so[j] += (((aO ^ bO) >> lane) & 1u) ? wt : 0.0;
             }
@@ -810,11 +867,11 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
         }
         const uint32_t acc_w = __ballot_sync(0xFFFFFFFFu, accept);
         for (uint32_t jv = lane; jv < f; jv += 32)
-          newF[jv * Wp + w] = (rowsF[jv * Wp + w] & ~acc_w) | (newD[jv * Wp + w] & acc_w);
+          newF[jv * Wp + w] = (rowsF[jv * RW + own + w] & ~acc_w) | (newD[jv * Wp + w] & acc_w);
         if (accept) {
           acc[j] += I32 ? (Acc)di[j] : (Acc)delta;
           uint64_t changed = (dm[j] ^ pm[j]) & fm;
-          const bool cap = (int32_t)s == esrc;
+          const bool cap = (int32_t)(a.rank * n + s) == esrc;
           while (changed) {
             const uint32_t jv = (uint32_t)(__ffsll((long long)changed) - 1);
             changed &= changed - 1;
@@ -835,11 +892,9 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
       }
       team_sync(tw, teams_per_cta, team);
       for (uint32_t idx = tid_team; idx < f * Wp; idx += team_threads) {
+        const uint32_t jv = idx / Wp, w = idx - jv * Wp;
         const uint32_t nw = newF[idx];
-        if (nw != rowsF[idx]) {
-          const uint32_t jv = idx / Wp, w = idx - jv * Wp;
-          a.pop[(size_t)vars[jv] * Wp + w] = nw;
-        }
+        if (nw != rowsF[jv * RW + own + w]) a.pop[(size_t)vars[jv] * Wp + w] = nw;
       }
       team_sync(tw, teams_per_cta, team);
     }
@@ -989,12 +1044,12 @@ __global__ void init_epilogue_kernel(const EpiArgs a) {
     const bool exact = c->exact != 0;
     double cur = 0.0;
     int32_t best = -1;
-    for (uint32_t i = 0; i < a.n; ++i) {
+    for (uint32_t i = 0; i < a.n_global; ++i) {
       c->calls_total += (unsigned long long)c->q;
       c->run_calls += (unsigned long long)c->q;
       if (c->has_budget && (double)c->calls_total / c->q >= c->max_evals)
         request_stop(c, GOMIX_STOP_BUDGET);
-      const double f = a.fit[i];
+      const double f = a.fit_all[i];
       if (i == 0 || cmp_better(exact, f, cur)) {
         cur = f;
         best = (int32_t)i;
@@ -1003,8 +1058,8 @@ __global__ void init_epilogue_kernel(const EpiArgs a) {
     }
     c->elit_fit = cur;
     c->elit_src = best;
-    c->eh1 = a.h1[best];
-    c->eh2 = a.h2[best];
+    c->eh1 = a.h1_all[best];
+    c->eh2 = a.h2_all[best];
     c->elit_ver += 1;
   }
   __syncthreads();
@@ -1018,15 +1073,26 @@ __global__ void init_epilogue_kernel(const EpiArgs a) {
 // ---------------------------------------------------------------------------
 // init / full evaluation / layout conversion
 // ---------------------------------------------------------------------------
+// Initial alleles: bit (v, g) of global member g is bit g%32 of Philox block
+// (v, g/32), so a shard of the population draws exactly the bits the same
+// members get in a single-GPU run.
 __global__ void philox_init_kernel(uint32_t* pop, uint64_t nv, uint32_t n, uint32_t Wp,
-                                   uint64_t seed) {
+                                   uint64_t seed, uint32_t rank) {
   const uint64_t total = nv * Wp;
   const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t w = (uint32_t)(i % Wp);
-    const uint4 r = philox4x32_10(make_uint4((uint32_t)i, (uint32_t)(i >> 32), 0u, kTagInit), key);
-    pop[i] = r.x & valid_mask(w, n);
+    const uint64_t v = i / Wp;
+    const uint64_t g0 = (uint64_t)rank * n + 32ull * w;  // global index of bit 0
+    const uint64_t blk = g0 >> 5;
+    const uint32_t off = (uint32_t)(g0 & 31u);
+    uint32_t word = philox4x32_10(make_uint4((uint32_t)v, (uint32_t)(v >> 32), (uint32_t)blk, kTagInit), key).x;
+    if (off) {
+      const uint32_t hi = philox4x32_10(make_uint4((uint32_t)v, (uint32_t)(v >> 32), (uint32_t)(blk + 1), kTagInit), key).x;
+      word = (word >> off) | (hi << (32u - off));
+    }
+    pop[i] = word & valid_mask(w, n);
   }
 }
 
@@ -1181,6 +1247,11 @@ void launch_order(const BeginArgs& b, const OrderArgs& o, cudaStream_t s) {
   GOMIX_CUDA(cudaGetLastError());
 }
 
+void launch_global_epilogue(const EpiArgs& a, cudaStream_t s) {
+  global_epilogue_kernel<<<1, 256, 0, s>>>(a);
+  GOMIX_CUDA(cudaGetLastError());
+}
+
 void launch_init_epilogue(const EpiArgs& a, cudaStream_t s) {
   init_epilogue_kernel<<<1, 256, 0, s>>>(a);
   GOMIX_CUDA(cudaGetLastError());
@@ -1206,8 +1277,8 @@ void launch_external_elitist(const SnapArgs& a, double fitness, cudaStream_t s) 
 }
 
 void launch_philox_init(uint32_t* pop, uint64_t nv, uint32_t n, uint32_t Wp, uint64_t seed,
-                        cudaStream_t s) {
-  philox_init_kernel<<<grid_for(nv * Wp, 256, 4096), 256, 0, s>>>(pop, nv, n, Wp, seed);
+                        uint32_t rank, cudaStream_t s) {
+  philox_init_kernel<<<grid_for(nv * Wp, 256, 4096), 256, 0, s>>>(pop, nv, n, Wp, seed, rank);
   GOMIX_CUDA(cudaGetLastError());
 }
 

@@ -114,13 +114,20 @@ struct EpiArgs {
   double* impr;
   unsigned long long* impr_calls;  // RunControl call count when the improvement was reported
   uint64_t impr_cap;
-  uint32_t n, G, nparts, group;
+  uint32_t n, G, nparts, group;  // n: this rank's solutions
   int32_t mode;  // 0 exact atomics, 1 float partials, 2 ordered
+  // sharding: fit/h1/h2 above are this rank's slices of the gathered arrays
+  const double* fit_all;
+  const unsigned long long* h1_all;
+  const unsigned long long* h2_all;
+  unsigned long long* rank_cnt;  // [R][steps, calls] of the current group
+  uint32_t n_global, R, rank;
 };
 
 // elitist snapshot / hashing kernels
 struct SnapArgs {
-  const uint32_t* pop;
+  const uint32_t* pop;   // this rank's rows
+  const uint32_t* pool;  // every rank's rows [R][nv][Wp] (elitist column lookup)
   uint32_t* elit;
   uint32_t* ever;
   DevCtl* ctl;
@@ -160,7 +167,10 @@ struct GomArgs {
   double* rec_delta;
   uint8_t* rec_present;
   uint8_t* rec_accept;
-  uint32_t n, Wp, team_warps, stage_words;
+  uint32_t n, Wp, team_warps, stage_words;  // n: this rank's solutions, Wp: words per row per rank
+  const uint32_t* pool;  // all ranks' rows, rank-major [R][nv][Wp] (== pop when R == 1)
+  uint64_t nv;
+  uint32_t R, rank, n_global;
   int32_t exact;
   uint32_t generation;
   uint64_t seed;
@@ -256,11 +266,12 @@ void launch_begin(const BeginArgs& b, cudaStream_t s);
 void launch_order(const BeginArgs& b, const OrderArgs& o, cudaStream_t s);
 void prepare_gom(bool univariate, bool i32, int wpt, bool team, size_t smem);
 void launch_init_epilogue(const EpiArgs& a, cudaStream_t s);
+void launch_global_epilogue(const EpiArgs& a, cudaStream_t s);
 void launch_hash_population(const SnapArgs& a, cudaStream_t s);
 void launch_finalize_elitist(const SnapArgs& a, cudaStream_t s);
 void launch_external_elitist(const SnapArgs& a, double fitness, cudaStream_t s);
 void launch_philox_init(uint32_t* pop, uint64_t nv, uint32_t n, uint32_t Wp, uint64_t seed,
-                        cudaStream_t s);
+                        uint32_t rank, cudaStream_t s);
 void launch_full_eval(const Problem& P, const uint32_t* pop, double* fit, uint32_t n,
                       uint32_t Wp, bool ordered, cudaStream_t s);
 void launch_unpack(const uint32_t* pop, uint8_t* out, uint64_t nv, uint32_t n, uint32_t Wp,

@@ -232,18 +232,27 @@ class GpuParallelEngine:
     def __init__(self, problem: GpuProblem, population_size: int, seed: int = 1,
                  ctx: Optional[RunContext] = None, population_id: int = 1, mode: str = "replay",
                  record_batch: bool = False, ordered_float: bool = False, time_kernels: bool = False,
-                 genotypes: Optional[np.ndarray] = None, stream=None):
+                 genotypes: Optional[np.ndarray] = None, stream=None, rank: int = 0, world_size: int = 1,
+                 nccl_unique_id: Optional[bytes] = None):
+        """world_size > 1: this process's shard of a population of
+        `population_size` members over world_size GPUs (Philox mode); every
+        rank passes the same nccl_unique_id (see nccl_unique_id()) and calls
+        run_generation / elitist collectively."""
         if population_size <= 0:
             raise ValueError("engine: population must be non-empty")
         self.problem = problem
-        self.n = int(population_size)
+        self.n_global = int(population_size)
+        self.world_size, self.rank = int(world_size), int(rank)
+        self.n = self.n_global // max(1, self.world_size)
         self.pop_id = population_id
         self.ctx = ctx if ctx is not None else RunContext(TerminationConfig(), problem.comparator(),
                                                           problem.info.num_edges)
         flags = (_capi.FLAG_RECORD_BATCH if record_batch else 0) | (_capi.FLAG_ORDERED_FLOAT if ordered_float else 0) \
             | (_capi.FLAG_TIME_KERNELS if time_kernels else 0)
-        cfg = _capi.EngineConfig(self.n, seed, _capi.MODE_REPLAY if mode == "replay" else _capi.MODE_PHILOX,
-                                 flags, population_id, 0, 1, None)
+        self._nid = None if nccl_unique_id is None else C.create_string_buffer(bytes(nccl_unique_id), 128)
+        cfg = _capi.EngineConfig(self.n_global, seed, _capi.MODE_REPLAY if mode == "replay" else _capi.MODE_PHILOX,
+                                 flags, population_id, self.rank, self.world_size,
+                                 None if self._nid is None else C.cast(self._nid, C.c_void_p))
         h = C.c_void_p()
         check(lib().gomix_gpu_engine_create(problem.h, C.byref(cfg), C.byref(h)))
         self.h = h
@@ -408,6 +417,103 @@ class GpuParallelEngine:
         c = C.c_uint64()
         check(lib().gomix_gpu_launch_count(self.h, C.byref(c)))
         return c.value
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (create on one rank, broadcast to the others)."""
+    buf = C.create_string_buffer(128)
+    check(lib().gomix_gpu_nccl_unique_id(C.cast(buf, C.c_void_p)))
+    return buf.raw
+
+
+def shard_range(population_size: int, world_size: int, rank: int):
+    """Members [lo, hi) held by `rank` (gomix_engine_config sharding rule)."""
+    if world_size < 1 or population_size % world_size:
+        raise ValueError("population size must be divisible by world_size")
+    per = population_size // world_size
+    return rank * per, (rank + 1) * per
+
+
+class _ShardView(GpuParallelEngine):
+    """Borrowed handle of one shard of a GpuLocalGroup (read-only helpers)."""
+
+    def __init__(self, problem, handle, n_local, rank, world_size):  # noqa: D107 (no engine creation)
+        self.problem, self.h, self.n, self.rank, self.world_size = problem, handle, n_local, rank, world_size
+        self.n_global = n_local * world_size
+
+    def __del__(self):
+        pass
+
+
+class GpuLocalGroup:
+    """A population sharded over `world_size` engines in this process (one per
+    device in `problems`, or several on one device), driven in lock step; the
+    per-group exchange is device-to-device copies.  Same arithmetic as one
+    process per GPU over NCCL, and equal to a single-engine Philox run."""
+
+    def __init__(self, problems, population_size: int, seed: int = 1, world_size: Optional[int] = None,
+                 ctx: Optional[RunContext] = None):
+        if isinstance(problems, GpuProblem):
+            problems = [problems] * int(world_size or 1)
+        self.problems = list(problems)
+        self.world_size = len(self.problems)
+        self.problem = self.problems[0]
+        self.n_global = int(population_size)
+        shard_range(self.n_global, self.world_size, 0)
+        self.ctx = ctx if ctx is not None else RunContext(TerminationConfig(), self.problem.comparator(),
+                                                          self.problem.info.num_edges)
+        arr = (C.c_void_p * self.world_size)(*[p.h for p in self.problems])
+        cfg = _capi.EngineConfig(self.n_global, seed, _capi.MODE_PHILOX, 0, 1, 0, self.world_size, None)
+        h = C.c_void_p()
+        check(lib().gomix_gpu_local_group_create(C.cast(arr, C.c_void_p), C.byref(cfg), C.byref(h)))
+        self.h = h
+        self.shards = []
+        for r in range(self.world_size):
+            eh = C.c_void_p()
+            check(lib().gomix_gpu_local_group_engine(self.h, r, C.byref(eh)))
+            self.shards.append(_ShardView(self.problems[r], eh, self.n_global // self.world_size, r,
+                                          self.world_size))
+        stats = _capi.RunStats()
+        crit = self.ctx.control.criteria()
+        check(lib().gomix_gpu_local_group_init_population(self.h, C.byref(crit), C.byref(stats)))
+        self.shards[0].ctx = self.ctx
+        self.shards[0].pop_id = 1
+        self.shards[0]._absorb(stats, 0)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().gomix_gpu_local_group_destroy(self.h)
+            self.h = None
+
+    def run_generation(self):
+        ctl = self.ctx.control
+        if ctl.stop_requested():
+            return
+        gen = self.generation()
+        stats = _capi.RunStats()
+        crit = ctl.criteria()
+        check(lib().gomix_gpu_local_group_run_generation(self.h, C.byref(crit), C.byref(stats)))
+        self.shards[0]._absorb(stats, gen)
+
+    def generation(self) -> int:
+        return self.shards[0].generation()
+
+    def population(self):
+        parts = [s.population() for s in self.shards]
+        return np.concatenate([p[0] for p in parts]), np.concatenate([p[1] for p in parts])
+
+    def elitist(self):
+        g = np.zeros(self.problem.info.num_vertices, np.uint8)
+        f = C.c_double()
+        check(lib().gomix_gpu_local_group_read_elitist(self.h, g.ctypes.data, C.byref(f)))
+        return g, f.value
+
+    @property
+    def elitist_fitness(self):
+        return self.shards[0].elitist_fitness
+
+    def group_counters(self):
+        return self.shards[0].group_counters()
 
 
 def gpu_color(instance: MaxCutInstance, fos: Fos, device: int = 0):

@@ -1,0 +1,121 @@
+"""Multi-GPU sharding of the population.
+
+GPU: a population sharded over R in-process engines (local transport, the
+same kernels and exchange schedule as one process per GPU over NCCL) must be
+bit-identical to a single-engine Philox run of the same population and seed —
+populations, fitness, elitist, counters, stop decisions.
+CPU (gloo, world_size 2): the host-side bootstrap — NCCL unique id created by
+rank 0 through the C-ABI and broadcast — and the shard partition.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import paper_2203_08680_b200 as G
+
+
+def test_shard_range_partitions_the_population():
+    for n, R in ((64, 2), (128, 8), (96, 3), (4096, 8)):
+        cover = np.zeros(n, int)
+        for r in range(R):
+            lo, hi = G.shard_range(n, R, r)
+            cover[lo:hi] += 1
+        assert (cover == 1).all()
+    with pytest.raises(ValueError):
+        G.shard_range(100, 8, 0)
+
+
+def _bootstrap(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    obj = [G.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    uid = obj[0]
+    ids = [None] * world
+    dist.all_gather_object(ids, uid)
+    lo, hi = G.shard_range(128, world, rank)
+    spans = [None] * world
+    dist.all_gather_object(spans, (lo, hi))
+    dist.destroy_process_group()
+    q.put((rank, len(uid), all(i == uid for i in ids), spans))
+
+
+def test_nccl_bootstrap_over_gloo_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + os.getpid() % 1000
+    procs = [ctx.Process(target=_bootstrap, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, ln, same, spans in out:
+        assert ln == 128 and same
+        assert spans == [(0, 64), (64, 128)]
+
+
+def _single(P, n, seed, crit=None):
+    ctx = G.RunContext(G.TerminationConfig(**(crit or {})), P.comparator(), P.info.num_edges)
+    E = G.GpuParallelEngine(P, n, seed, ctx=ctx, mode="philox")
+    E.set_timing(True)  # launch-by-launch path with the host group order, like the sharded path
+    return E, ctx
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,shape,n,R,gens", [
+    ("uni", (16, 16), 64, 2, 6),
+    ("neigh", (12, 12), 128, 4, 5),
+    ("uni", (20, 10), 96, 2, 5),      # 48 per shard: padded words, shard boundary inside a word
+    ("neigh", (9, 9), 96, 3, 4),
+    ("uni", (64, 64), 256, 8, 3),
+])
+def test_sharded_equals_single_engine(kind, shape, n, R, gens):
+    inst = G.generate_torus(shape[0], shape[1], ("int", -3, 9), 5)
+    fos = G.univariate_fos(inst.num_vertices) if kind == "uni" else G.neighbourhood_fos(inst)
+    P = G.GpuProblem(inst, fos)
+    E, _ = _single(P, n, 11)
+    S = G.GpuLocalGroup(P, n, seed=11, world_size=R)
+    g1, f1 = E.population()
+    g2, f2 = S.population()
+    assert (g1 == g2).all() and (f1 == f2).all()
+    for gen in range(gens):
+        E.run_generation()
+        S.run_generation()
+        g1, f1 = E.population()
+        g2, f2 = S.population()
+        assert (g1 == g2).all(), gen
+        assert (f1 == f2).all(), gen
+        assert E.elitist_fitness == S.elitist_fitness
+    eg1, ef1 = E.elitist()
+    eg2, ef2 = S.elitist()
+    assert ef1 == ef2 and (eg1 == eg2).all()
+    assert inst.cut_value(eg2) == ef2
+    for a, b in zip(E.group_counters(), S.group_counters()):
+        assert (a == b).all()
+    assert (inst.cut_values(g2) == f2).all()
+
+
+@pytest.mark.gpu
+def test_sharded_stop_criteria_match_single_engine():
+    inst = G.generate_torus(16, 16, ("int", 1, 10), 3)
+    P = G.GpuProblem(inst, G.univariate_fos(256))
+    crit = dict(max_evaluations=900.0)
+    E, ce = _single(P, 64, 4, crit)
+    cs = G.RunContext(G.TerminationConfig(**crit), P.comparator(), inst.num_edges)
+    S = G.GpuLocalGroup(P, 64, seed=4, world_size=4, ctx=cs)
+    for _ in range(50):
+        E.run_generation()
+        S.run_generation()
+        if ce.control.stop_requested():
+            break
+    assert ce.control.stop_requested() and cs.control.stop_requested()
+    assert ce.control.reason == cs.control.reason == "evaluation-budget"
+    assert ce.control.calls == cs.control.calls
+    assert E.generation() == S.generation()
+    assert (E.population()[0] == S.population()[0]).all()
