@@ -68,7 +68,10 @@ enum {
    * gomix_gpu_read_batch (engine_parallel.hpp:64-97). */
   GOMIX_FLAG_RECORD_BATCH = 1u << 1,
   /* Time every GOM kernel launch with CUDA events (gomix_gpu_kernel_times). */
-  GOMIX_FLAG_TIME_KERNELS = 1u << 2
+  GOMIX_FLAG_TIME_KERNELS = 1u << 2,
+  /* Univariate FOS, integer weights, PHILOX: use the lane-per-solution kernel
+   * instead of the bit-sliced lane-per-set kernel (same results; A/B tests). */
+  GOMIX_FLAG_LANE_PER_SOLUTION = 1u << 3
 };
 
 enum { GOMIX_STOP_NONE = 0, GOMIX_STOP_BUDGET = 1, GOMIX_STOP_CLOCK = 2, GOMIX_STOP_TARGET = 3,

@@ -166,6 +166,9 @@ std::unique_ptr<Problem> create_problem(const gomix_maxcut* inst, const gomix_fo
     for (uint64_t i = 0; i < m; ++i) {
       const uint32_t v = P->h_set_vars[i];
       P->max_fp = std::max<uint64_t>(P->max_fp, (uint64_t)(row_ptr[v + 1] - row_ptr[v]));
+      uint64_t a = 0;
+      for (int32_t e = row_ptr[v]; e < row_ptr[v + 1]; ++e) a += (uint64_t)std::llabs((long long)wi[e]);
+      P->max_abs_row = std::max(P->max_abs_row, a);
     }
   }
 
@@ -284,6 +287,8 @@ struct gomix_gpu_engine {
   uint32_t W = 0, Wp = 0, wpt = 1, tw = 1, block = 256, teams = 8, stage_words = 0;
   size_t smem = 0;
   int grid_cap = 1;
+  int univ_planes = 0;     // > 0: Philox groups run the bit-sliced lane-per-set kernel
+  int univ_grid_cap = 1;
   int sms = 148;
   uint32_t mode = GOMIX_MODE_PHILOX, flags = 0;
   int32_t pop_id = 1;
@@ -439,6 +444,12 @@ struct gomix_gpu_engine {
     const int per_sm = gom_max_blocks_per_sm(P->univariate, P->i32, (int)wpt, tw > 1, (int)block, smem);
     if (per_sm < 1) invalid("engine: GOM kernel does not fit on an SM with this configuration");
     grid_cap = per_sm * sms;
+    if (P->univariate && P->i32 && mode == GOMIX_MODE_PHILOX && !(flags & GOMIX_FLAG_RECORD_BATCH) &&
+        !(flags & GOMIX_FLAG_LANE_PER_SOLUTION) && Wp <= 4) {
+      univ_planes = univ_sliced_planes(P->max_abs_row);
+      if (univ_planes) univ_grid_cap = univ_sliced_max_blocks_per_sm(univ_planes, (int)Wp) * sms;
+      if (univ_grid_cap < 1) univ_planes = 0;
+    }
     for (uint64_t c = 0; c < P->k; ++c)
       max_group = std::max(max_group, P->group_off[c + 1] - P->group_off[c]);
 
@@ -673,8 +684,15 @@ struct gomix_gpu_engine {
       e1 = take_event();
       GOMIX_CUDA(cudaEventRecord(e0, st));
     }
-    a.epi = epi_args(group, (uint32_t)G, (uint32_t)grid);
-    launch_gom(a, P->univariate, P->i32, (int)wpt, tw > 1, grid, (int)block, smem, st);
+    if (univ_planes && !with_tape) {
+      const uint64_t per = (uint64_t)univ_sliced_sets_per_cta();
+      const int g = (int)std::max<uint64_t>(1, std::min<uint64_t>((G + per - 1) / per, (uint64_t)univ_grid_cap));
+      a.epi = epi_args(group, (uint32_t)G, (uint32_t)g);
+      launch_univ_sliced(a, univ_planes, (int)Wp, g, st);
+    } else {
+      a.epi = epi_args(group, (uint32_t)G, (uint32_t)grid);
+      launch_gom(a, P->univariate, P->i32, (int)wpt, tw > 1, grid, (int)block, smem, st);
+    }
     ++launches;
     if (e1) {
       GOMIX_CUDA(cudaEventRecord(e1, st));

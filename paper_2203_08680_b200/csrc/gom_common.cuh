@@ -1,0 +1,295 @@
+// gom_common.cuh — device helpers shared by the GOM kernels (gom.cu,
+// gom_univ.cu): Philox4x32-10, the reference's FitnessComparator, Zobrist
+// keys, the copy-on-write elitist capture, bit tricks, and the group epilogue
+// (fitness commit, evaluator-call accounting, elitist scan) run by the last
+// CTA of a GOM launch.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "internal.cuh"
+
+namespace gomix_b200 {
+
+constexpr uint32_t kEpiSmemFit = 256;  // fitness values the epilogue keeps in shared memory
+
+// ---------------------------------------------------------------------------
+// Philox4x32-10 (Salmon et al., SC'11), counter-based: every (generation, set,
+// solution, call) has its own counter, so draws need no state and no order.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    k.x += 0x9E3779B9u;
+    k.y += 0xBB67AE85u;
+  }
+  return c;
+}
+
+__device__ __forceinline__ uint64_t lo64(uint4 r) { return (uint64_t)r.x | ((uint64_t)r.y << 32); }
+__device__ __forceinline__ uint64_t hi64(uint4 r) { return (uint64_t)r.z | ((uint64_t)r.w << 32); }
+// uniform in [0, n): high 64 bits of r*n (bias <= n / 2^64).
+__device__ __forceinline__ uint32_t bounded(uint64_t r, uint32_t n) {
+  return (uint32_t)__umul64hi(r, (uint64_t)n);
+}
+
+constexpr uint32_t kTagGom = 0x474F4D00u;   // "GOM"
+constexpr uint32_t kTagInit = 0x494E4900u;  // "INI"
+
+// FitnessComparator (graybox.hpp:22-35).
+__device__ __forceinline__ double cmp_scale(double a, double b) {
+  return 1e-9 * fmax(1.0, fmax(fabs(a), fabs(b)));
+}
+__device__ __forceinline__ bool cmp_better(bool exact, double a, double b) {
+  return exact ? a > b : a - b > cmp_scale(a, b);
+}
+__device__ __forceinline__ bool cmp_equal(bool exact, double a, double b) {
+  return exact ? a == b : fabs(a - b) <= cmp_scale(a, b);
+}
+
+// 128-bit Zobrist key of variable v (two independent splitmix64 streams).
+// A genotype's hash is the XOR of the keys of its variables set to 1, so a
+// flip of v toggles key(v): "parent == elitist" (engine_parallel.hpp:202) is
+// hash equality, maintained incrementally instead of recounted per group.
+__device__ __forceinline__ unsigned long long smix(unsigned long long x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+__device__ __forceinline__ void zobrist(uint32_t v, unsigned long long& z1, unsigned long long& z2) {
+  z1 = smix(0x5A0B0000000000ull ^ (unsigned long long)v);
+  z2 = smix(0xC3A5C85C97CB3127ull + 0x9E37ull * (unsigned long long)v);
+}
+
+// Copy-on-write elitist snapshot: before solution elit_src changes variable v
+// for the first time since it became the elitist, record its old bit.
+__device__ __forceinline__ void capture_row(uint32_t* elit, uint32_t* ever, uint32_t ver, uint32_t v,
+                                            uint32_t old_bit) {
+  if (ever[v] == ver) return;
+  if (old_bit)
+    atomicOr(&elit[v >> 5], 1u << (v & 31u));
+  else
+    atomicAnd(&elit[v >> 5], ~(1u << (v & 31u)));
+  ever[v] = ver;
+}
+
+__device__ __forceinline__ uint32_t valid_mask(uint32_t w, uint32_t n) {
+  const uint32_t lo = w * 32u;
+  if (lo + 32u <= n) return 0xFFFFFFFFu;
+  if (lo >= n) return 0u;
+  return (1u << (n - lo)) - 1u;
+}
+
+// A team is one warp (several per CTA) or a whole CTA (tw > 1); the host
+// never builds multi-warp teams that share a CTA, so no named barriers are
+// needed (dynamic barrier ids would reserve all 16 and cap CTAs per SM).
+__device__ __forceinline__ void team_sync(uint32_t tw, uint32_t, uint32_t) {
+  if (tw == 1)
+    __syncwarp();
+  else
+    __syncthreads();
+}
+
+// Members of word w2 that differ from pattern m somewhere on F.
+// word wg of the staged pool (stride RW per row; Wp words per rank's shard of
+// n members).
+__device__ __forceinline__ uint32_t differ_word(const uint32_t* rowsF, uint32_t f, uint32_t RW,
+                                                uint32_t wg, uint64_t m, uint32_t n, uint32_t Wp) {
+  uint32_t dw = 0;
+  for (uint32_t jv = 0; jv < f; ++jv)
+    dw |= rowsF[jv * RW + wg] ^ (((m >> jv) & 1ull) ? 0xFFFFFFFFu : 0u);
+  return dw & valid_mask(wg % Wp, n);
+}
+
+// 32x32 bit-matrix transpose across a warp: lane r holds row r on entry;
+// on exit lane c holds column c (bit r = bit c of the old row r).
+__device__ __forceinline__ uint32_t transpose32(uint32_t x, uint32_t lane) {
+  constexpr uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+  for (int st = 0; st < 5; ++st) {
+    const uint32_t j = 16u >> st, m = masks[st];
+    const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x, j);
+    x = (lane & j) ? ((x & ~m) | ((y & ~m) >> j)) : ((x & m) | ((y & m) << j));
+  }
+  return x;
+}
+
+// Position of the k-th (0-based) set bit of x; k < popc(x).
+__device__ __forceinline__ uint32_t select_bit(uint32_t x, uint32_t k) {
+  uint32_t pos = 0;
+#pragma unroll
+  for (uint32_t sh = 16; sh >= 1; sh >>= 1) {
+    const uint32_t c = __popc(x & ((1u << sh) - 1u));
+    if (k >= c) {
+      k -= c;
+      x >>= sh;
+      pos += sh;
+    }
+  }
+  return pos;
+}
+
+// ---------------------------------------------------------------------------
+// epilogue (run by the last CTA of the GOM kernel to finish): commit the
+// group's fitness deltas, account the evaluator calls (budget stop first,
+// runtime.hpp:75-80), then the elitist scan of engine_parallel.hpp:305-310 —
+// the first member strictly better than the running elitist replaces it and
+// the scan continues against the new value — logging every improvement with
+// the call count at that moment and latching the target stop
+// (runtime.hpp:88-93,136-143).
+// ---------------------------------------------------------------------------
+static __device__ void request_stop(DevCtl* c, int reason) {
+  if (!c->stop) {
+    c->stop = 1;
+    c->stop_reason = reason;
+  }
+}
+
+static __device__ void note_improvement(const EpiArgs& a, double f) {
+  DevCtl* c = a.ctl;
+  const unsigned long long i = c->n_impr++;
+  if (i < a.impr_cap) {
+    a.impr[i] = f;
+    a.impr_calls[i] = c->calls_total;
+  }
+  if (c->has_target && (cmp_better(c->exact, f, c->target) || cmp_equal(c->exact, f, c->target)))
+    request_stop(c, GOMIX_STOP_TARGET);
+}
+
+// Commit this rank's group deltas: fitness (exact atomics / float partials /
+// reference-ordered recorded deltas) and Zobrist hashes of its n solutions.
+static __device__ void commit_local(const EpiArgs& a, double* s_fit) {
+  const uint32_t n = a.n;
+  for (uint32_t s = threadIdx.x; s < n; s += blockDim.x) {
+    double f = a.fit[s];
+    if (a.mode == 2) {
+      for (uint32_t p = 0; p < a.G; ++p)
+        if (a.rec_accept[(size_t)p * n + s]) f += a.rec_delta[(size_t)p * n + s];
+    } else if (a.mode == 1) {
+      double sum = 0.0;
+      for (uint32_t b = 0; b < a.nparts; ++b) sum += a.part[(size_t)b * n + s];
+      f += sum;
+    } else {
+      f += a.dfit[s];
+      a.dfit[s] = 0.0;
+    }
+    a.fit[s] = f;
+    if (s_fit && s < kEpiSmemFit) s_fit[s] = f;
+    a.h1[s] ^= a.dh1[s];
+    a.h2[s] ^= a.dh2[s];
+    a.dh1[s] = 0;
+    a.dh2[s] = 0;
+  }
+  if (a.R > 1 && threadIdx.x == 0) {  // this rank's counters, all-gathered next
+    DevCtl* c = a.ctl;
+    a.rank_cnt[2 * a.rank] = c->grp_steps;
+    a.rank_cnt[2 * a.rank + 1] = c->grp_calls;
+    c->grp_steps = 0;
+    c->grp_calls = 0;
+  }
+}
+
+// Evaluator-call accounting (budget stop first, runtime.hpp:75-80), then the
+// elitist scan of engine_parallel.hpp:305-310 over all n_global members in
+// index order — the first member strictly better than the running elitist
+// replaces it and the scan continues against the new value — logging every
+// improvement with the call count at that moment and latching the target stop
+// (runtime.hpp:88-93,136-143).  Sharded runs execute it on every rank from the
+// gathered state, so all ranks take identical decisions.
+static __device__ void elitist_scan(const EpiArgs& a, const double* s_fit) {
+  DevCtl* c = a.ctl;
+  const uint32_t n = a.n_global;
+  __shared__ double s_chunkmax[32];
+  __shared__ int32_t s_best;
+  if (threadIdx.x == 0) {
+    unsigned long long st = 0, ca = 0;
+    if (a.R > 1) {
+      for (uint32_t r = 0; r < a.R; ++r) {
+        st += a.rank_cnt[2 * r];
+        ca += a.rank_cnt[2 * r + 1];
+      }
+    } else {
+      st = c->grp_steps;
+      ca = c->grp_calls;
+      c->grp_steps = 0;
+      c->grp_calls = 0;
+    }
+    c->calls_total += ca;
+    c->run_steps += st;
+    c->run_calls += ca;
+    c->groups_run += 1;
+    a.gsteps[a.group] += st;
+    a.gcalls[a.group] += ca;
+    if (c->has_budget && (double)c->calls_total / c->q >= c->max_evals)
+      request_stop(c, GOMIX_STOP_BUDGET);
+    s_best = -1;
+  }
+  __syncthreads();
+  // chunk maxima let the serial scan skip chunks that cannot hold a record
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u, nwarps = blockDim.x >> 5;
+  auto fit_at = [&](uint32_t s) { return (s_fit && s < kEpiSmemFit) ? s_fit[s] : a.fit_all[s]; };
+  for (uint32_t chunk = warp; chunk * 32u < n && chunk < 32; chunk += nwarps) {
+    const uint32_t s = chunk * 32u + lane;
+    double f = s < n ? fit_at(s) : -INFINITY;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) f = fmax(f, __shfl_xor_sync(0xFFFFFFFFu, f, o));
+    if (lane == 0) s_chunkmax[chunk] = f;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const bool exact = c->exact != 0;
+    const int32_t has_target = c->has_target;
+    const double target = c->target;
+    unsigned long long ni = c->n_impr;
+    const unsigned long long calls_now = c->calls_total;
+    double cur = c->elit_fit;
+    int32_t best = -1;
+    bool hit = false;
+    for (uint32_t base = 0; base < n; base += 32u) {
+      const uint32_t chunk = base >> 5;
+      if (chunk < 32 && !(s_chunkmax[chunk] > cur)) continue;  // better() implies >
+      const uint32_t s = base + lane;
+      const double f = s < n ? fit_at(s) : -INFINITY;
+      uint32_t m = __ballot_sync(0xFFFFFFFFu, s < n && cmp_better(exact, f, cur));
+      while (m) {
+        const uint32_t l = __ffs(m) - 1;
+        cur = __shfl_sync(0xFFFFFFFFu, f, l);
+        best = (int32_t)(base + l);
+        if (lane == 0 && ni < a.impr_cap) {
+          a.impr[ni] = cur;
+          a.impr_calls[ni] = calls_now;
+        }
+        ++ni;
+        hit |= has_target && (cmp_better(exact, cur, target) || cmp_equal(exact, cur, target));
+        m = __ballot_sync(0xFFFFFFFFu, s < n && lane > l && cmp_better(exact, f, cur));
+      }
+    }
+    if (lane == 0) {
+      c->n_impr = ni;
+      if (hit) request_stop(c, GOMIX_STOP_TARGET);
+      if (best >= 0) {  // new elitist: member `best` (snapshot taken copy-on-write)
+        c->elit_fit = cur;
+        c->elit_src = best;
+        c->eh1 = a.h1_all[best];
+        c->eh2 = a.h2_all[best];
+        c->elit_ver += 1;
+      }
+      s_best = best;
+    }
+  }
+  __syncthreads();
+}
+
+static __device__ void epilogue_body(const EpiArgs& a) {
+  __shared__ double s_fit[kEpiSmemFit];  // this group's fitness, scanned without global loads
+  commit_local(a, a.R == 1 ? s_fit : nullptr);
+  __syncthreads();
+  if (a.R == 1) elitist_scan(a, s_fit);
+}
+
+}  // namespace gomix_b200

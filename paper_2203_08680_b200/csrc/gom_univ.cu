@@ -1,0 +1,387 @@
+// gom_univ.cu — the batched GOM step for a univariate FOS on integer weights
+// in Philox mode, bit-sliced: one linkage set {v} per LANE, the solutions of
+// that set as the bits of its packed row.
+//
+// Same semantics as gom_group_kernel's univariate path (engine_parallel.hpp:
+// 104-247): for F = {v} every donor that differs on F holds !x_v, so the pair
+// (s, {v}) is present iff some member holds the other value, and the GOM move
+// is the flip of v.  Its partial-evaluation delta over v's edges e = (v, u_e)
+// (the set's footprint, engine_parallel.hpp:48-55) is
+//     delta_s = sum_e w_e (1 - 2 c_e,s),   c_e,s = x_v,s xor x_u,s (edge cut now)
+//             = A - 2 T_s,   A = sum_e |w_e|,   T_s = sum_e |w_e| b_e,s
+// with b_e = c_e for w_e > 0 and !c_e for w_e < 0.  T is accumulated for all
+// solutions of the row at once as a B-plane bit-sliced counter (full adders
+// on 32-bit words: bit b of plane k = bit k of T for solution 32j+b), the
+// accept rule (determine_improvements, :194-214; exact comparator)
+//     delta > 0  or  (delta == 0 and parent != elitist)
+// becomes  T < h  or  (T == h and A even and not elitist),  h = (A+1)/2,
+// one bit-sliced comparison.  Accepted solutions flip v: one XOR per word.
+//
+// Per-solution results (fitness delta sum, Zobrist hash delta) are reduced
+// over the 32 sets of a warp by 32x32 bit transposes (bit l of lane b's word
+// = set l, solution b): fitness += sum_l acc (A_l - 2 T_l) = popcounts of the
+// transposed planes against ballots of the A_l bits; hash ^= XOR of key(v_l)
+// over accepted l via a 4-bit-chunk table of key XORs in shared memory.
+//
+// Why: the lane-per-solution path walks one set per warp with a chain of
+// dependent loads (set -> CSR row -> neighbour rows) and shuffles every
+// neighbour word to every lane; here the 32 sets of a warp load in parallel,
+// no neighbour data crosses lanes, and an edge costs ~3B+2 logic ops per 32
+// solutions.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "gom_common.cuh"
+
+namespace gomix_b200 {
+
+namespace {
+
+template <int WP>
+__device__ __forceinline__ void load_row(const uint32_t* row, uint32_t (&x)[WP]) {
+  if constexpr (WP == 4) {
+    const uint4 t = __ldg(reinterpret_cast<const uint4*>(row));
+    x[0] = t.x; x[1] = t.y; x[2] = t.z; x[3] = t.w;
+  } else if constexpr (WP == 2) {
+    const uint2 t = __ldg(reinterpret_cast<const uint2*>(row));
+    x[0] = t.x; x[1] = t.y;
+  } else {
+    x[0] = __ldg(row);
+  }
+}
+
+// neighbour rows are written by no lane of this launch (same-colour sets are
+// not adjacent), so the read-only path is safe for them too
+template <int WP>
+__device__ __forceinline__ void store_row(uint32_t* row, const uint32_t (&x)[WP]) {
+  if constexpr (WP == 4) {
+    *reinterpret_cast<uint4*>(row) = make_uint4(x[0], x[1], x[2], x[3]);
+  } else if constexpr (WP == 2) {
+    *reinterpret_cast<uint2*>(row) = make_uint2(x[0], x[1]);
+  } else {
+    row[0] = x[0];
+  }
+}
+
+constexpr int kUnivWarps = 8;  // warps per CTA
+constexpr int kNbChunk = 4;    // neighbour (col, w) pairs fetched per round
+
+}  // namespace
+
+template <int B, int WP>
+__global__ void __launch_bounds__(kUnivWarps * 32, 2) gom_univ_sliced_kernel(const GomArgs a) {
+  __shared__ unsigned long long s_key[kUnivWarps][32][2];
+  __shared__ unsigned long long s_tbl[kUnivWarps][8][16][2];
+  __shared__ long long s_dfit[WP * 32];
+  __shared__ unsigned long long s_dh1[WP * 32], s_dh2[WP * 32];
+  __shared__ uint32_t s_elit[WP];
+  __shared__ unsigned long long s_steps, s_calls;
+  __shared__ int s_last;
+  if (*(volatile int32_t*)&a.ctl->stop) return;
+
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const uint32_t n = a.n;
+  uint32_t G = a.G;
+  const uint32_t* gvars = a.gvars;
+  EpiArgs epi = a.epi;
+  if (a.slot >= 0) {  // graph path: this launch's group comes from the device-side order
+    const uint32_t gi = a.order[a.slot];
+    const GroupDesc d = a.groups[gi];
+    G = d.G;
+    gvars += d.g0;
+    epi.group = gi;
+    epi.G = G;
+  }
+  // group-start "parent == elitist" (engine_parallel.hpp:202) as word masks
+  const unsigned long long eh1 = a.ctl->eh1, eh2 = a.ctl->eh2;
+  const int32_t esrc_g = a.ctl->elit_src;
+  const uint32_t ever_cur = a.ctl->elit_ver;
+  const int32_t esrc = (esrc_g >= 0 && (uint32_t)esrc_g / n == a.rank) ? (int32_t)((uint32_t)esrc_g % n) : -1;
+  for (uint32_t j = warp; j < (uint32_t)WP; j += kUnivWarps) {
+    const uint32_t s = j * 32u + lane;
+    const bool e = s < n && a.h1[s] == eh1 && a.h2[s] == eh2;
+    const uint32_t m = __ballot_sync(0xFFFFFFFFu, e);
+    if (lane == 0) s_elit[j] = m;
+  }
+  for (uint32_t i = threadIdx.x; i < WP * 32u; i += blockDim.x) {
+    s_dfit[i] = 0;
+    s_dh1[i] = 0;
+    s_dh2[i] = 0;
+  }
+  if (threadIdx.x == 0) {
+    s_steps = 0;
+    s_calls = 0;
+  }
+  __syncthreads();
+  uint32_t elitw[WP], validw[WP];
+#pragma unroll
+  for (int j = 0; j < WP; ++j) {
+    elitw[j] = s_elit[j];
+    validw[j] = valid_mask((uint32_t)j, n);
+  }
+
+  long long dfit[WP];
+  unsigned long long dh1[WP], dh2[WP];
+#pragma unroll
+  for (int j = 0; j < WP; ++j) {
+    dfit[j] = 0;
+    dh1[j] = 0;
+    dh2[j] = 0;
+  }
+  unsigned long long steps = 0, calls = 0;
+
+  const uint32_t batches = (G + 31u) / 32u;
+  for (uint32_t bt = blockIdx.x * kUnivWarps + warp; bt < batches; bt += gridDim.x * kUnivWarps) {
+    const uint32_t p = bt * 32u + lane;
+    const bool live = p < G;
+    const uint32_t v = live ? gvars[p] : 0u;
+    uint32_t x[WP];
+#pragma unroll
+    for (int j = 0; j < WP; ++j) x[j] = 0;
+    int32_t rs = 0, re = 0;
+    if (live) {
+      load_row<WP>(a.pop + (size_t)v * WP, x);
+      rs = a.row_ptr[v];
+      re = a.row_ptr[v + 1];
+    }
+    // ---- T = sum_e |w_e| b_e (bit-sliced over the row's solutions) --------
+    uint32_t T[B][WP];
+#pragma unroll
+    for (int k = 0; k < B; ++k)
+#pragma unroll
+      for (int j = 0; j < WP; ++j) T[k][j] = 0;
+    uint32_t A = 0;
+    for (int32_t base = rs; base < re; base += kNbChunk) {
+      uint32_t u[kNbChunk];
+      int32_t w[kNbChunk];
+#pragma unroll
+      for (int t = 0; t < kNbChunk; ++t) {
+        const bool has = base + t < re;
+        u[t] = has ? (uint32_t)__ldg(a.col + base + t) : v;
+        w[t] = has ? __ldg(a.wi + base + t) : 0;
+      }
+      uint32_t nb[kNbChunk][WP];
+#pragma unroll
+      for (int t = 0; t < kNbChunk; ++t) load_row<WP>(a.pop + (size_t)u[t] * WP, nb[t]);
+#pragma unroll
+      for (int t = 0; t < kNbChunk; ++t) {
+        const uint32_t m = (uint32_t)(w[t] < 0 ? -w[t] : w[t]);
+        const uint32_t neg = w[t] < 0 ? 0xFFFFFFFFu : 0u;
+        A += m;
+#pragma unroll
+        for (int j = 0; j < WP; ++j) {
+          const uint32_t b = (x[j] ^ nb[t][j]) ^ neg;
+          uint32_t c = 0;
+#pragma unroll
+          for (int k = 0; k < B; ++k) {
+            const uint32_t xb = ((m >> k) & 1u) ? b : 0u;
+            const uint32_t tk = T[k][j];
+            T[k][j] = tk ^ xb ^ c;
+            c = (tk & xb) | (tk & c) | (xb & c);
+          }
+        }
+      }
+    }
+    // ---- presence: some member (over every rank's shard) holds the other value
+    uint32_t ones = 0;
+    if (live) {
+      if (a.R > 1) {
+        for (uint32_t r = 0; r < a.R; ++r) {
+          const uint32_t* row = a.pool + ((size_t)r * a.nv + v) * WP;
+#pragma unroll
+          for (int j = 0; j < WP; ++j) ones += __popc(__ldg(row + j));
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < WP; ++j) ones += __popc(x[j]);
+      }
+    }
+    const bool present = live && ones > 0u && ones < a.n_global;
+    // ---- accept: T < h, or T == h with A even and the parent not the elitist
+    const uint32_t h = (A + 1u) >> 1;
+    const uint32_t aeven = (A & 1u) ? 0u : 0xFFFFFFFFu;
+    uint32_t acc[WP];
+    bool any = false;
+#pragma unroll
+    for (int j = 0; j < WP; ++j) {
+      uint32_t lt = 0, eq = 0xFFFFFFFFu;
+#pragma unroll
+      for (int k = B - 1; k >= 0; --k) {
+        const uint32_t hk = ((h >> k) & 1u) ? 0xFFFFFFFFu : 0u;
+        lt |= eq & ~T[k][j] & hk;
+        eq &= ~(T[k][j] ^ hk);
+      }
+      acc[j] = present ? ((lt | (eq & aeven & ~elitw[j])) & validw[j]) : 0u;
+      any |= acc[j] != 0u;
+    }
+    if (present) {
+      steps += n;
+      calls += (unsigned long long)n * (uint32_t)(re - rs);
+    }
+    // ---- commit: accepted solutions flip v (apply_acceptance, :221-247)
+    if (any) {
+      uint32_t nx[WP];
+#pragma unroll
+      for (int j = 0; j < WP; ++j) nx[j] = x[j] ^ acc[j];
+      store_row<WP>(a.pop + (size_t)v * WP, nx);
+      if (esrc >= 0) {
+        const uint32_t ew = (uint32_t)esrc >> 5, eb = (uint32_t)esrc & 31u;
+        uint32_t aw = 0, xw = 0;
+#pragma unroll
+        for (int j = 0; j < WP; ++j)
+          if ((uint32_t)j == ew) {
+            aw = acc[j];
+            xw = x[j];
+          }
+        if ((aw >> eb) & 1u) capture_row(a.elit, a.ever, ever_cur, v, (xw >> eb) & 1u);
+      }
+    }
+    // ---- per-solution reductions over the warp's 32 sets ------------------
+    if (!__any_sync(0xFFFFFFFFu, any)) continue;
+    uint32_t Ab[B];
+#pragma unroll
+    for (int k = 0; k < B; ++k) Ab[k] = __ballot_sync(0xFFFFFFFFu, (A >> k) & 1u);
+    // Zobrist key XOR table: s_tbl[c][m] = XOR of key(v_{4c+i}) over bits i of m
+    {
+      unsigned long long z1 = 0, z2 = 0;
+      if (live && any) zobrist(v, z1, z2);
+      s_key[warp][lane][0] = z1;
+      s_key[warp][lane][1] = z2;
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t e = lane + 32u * i;
+        const uint32_t c = e >> 4, m = e & 15u;
+        unsigned long long t1 = 0, t2 = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const unsigned long long k1 = s_key[warp][4 * c + q][0], k2 = s_key[warp][4 * c + q][1];
+          t1 ^= ((m >> q) & 1u) ? k1 : 0ull;
+          t2 ^= ((m >> q) & 1u) ? k2 : 0ull;
+        }
+        s_tbl[warp][c][m][0] = t1;
+        s_tbl[warp][c][m][1] = t2;
+      }
+      __syncwarp();
+    }
+#pragma unroll
+    for (int j = 0; j < WP; ++j) {
+      const uint32_t accT = transpose32(acc[j], lane);  // lane b: sets l accepted by solution 32j+b
+      long long d = 0;
+#pragma unroll
+      for (int k = 0; k < B; ++k) d += (long long)__popc(accT & Ab[k]) << k;
+      // accepted pairs have T <= A/2 < 2^(B-1): the top plane is zero
+#pragma unroll
+      for (int k = 0; k < B - 1; ++k) d -= (long long)__popc(transpose32(T[k][j] & acc[j], lane)) << (k + 1);
+      dfit[j] += d;
+      unsigned long long x1 = 0, x2 = 0;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const uint32_t m = (accT >> (4 * c)) & 15u;
+        x1 ^= s_tbl[warp][c][m][0];
+        x2 ^= s_tbl[warp][c][m][1];
+      }
+      dh1[j] ^= x1;
+      dh2[j] ^= x2;
+    }
+    __syncwarp();
+  }
+
+  // ---- per-CTA reductions, then the group epilogue in the last CTA -------
+#pragma unroll
+  for (int j = 0; j < WP; ++j) {
+    const uint32_t s = (uint32_t)j * 32u + lane;
+    if (dfit[j]) atomicAdd(reinterpret_cast<unsigned long long*>(&s_dfit[s]), (unsigned long long)dfit[j]);
+    if (dh1[j] | dh2[j]) {
+      atomicXor(&s_dh1[s], dh1[j]);
+      atomicXor(&s_dh2[s], dh2[j]);
+    }
+  }
+  {
+    unsigned long long ws = steps, wc = calls;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ws += __shfl_xor_sync(0xFFFFFFFFu, ws, o);
+      wc += __shfl_xor_sync(0xFFFFFFFFu, wc, o);
+    }
+    if (lane == 0 && (ws | wc)) {
+      atomicAdd(&s_steps, ws);
+      atomicAdd(&s_calls, wc);
+    }
+  }
+  __syncthreads();
+  for (uint32_t s = threadIdx.x; s < n && s < WP * 32u; s += blockDim.x) {
+    if (s_dfit[s]) atomicAdd(&a.dfit[s], (double)s_dfit[s]);
+    if (s_dh1[s] | s_dh2[s]) {
+      atomicXor(&a.dh1[s], s_dh1[s]);
+      atomicXor(&a.dh2[s], s_dh2[s]);
+    }
+  }
+  if (threadIdx.x == 0) {
+    if (s_steps | s_calls) {
+      atomicAdd(&a.ctl->grp_steps, s_steps);
+      atomicAdd(&a.ctl->grp_calls, s_calls);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&a.ctl->done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  epilogue_body(epi);
+  if (threadIdx.x == 0) a.ctl->done = 0;
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+namespace {
+template <int WP>
+void* univ_kernel_wp(int planes) {
+  switch (planes) {
+    case 4: return (void*)gom_univ_sliced_kernel<4, WP>;
+    case 6: return (void*)gom_univ_sliced_kernel<6, WP>;
+    case 8: return (void*)gom_univ_sliced_kernel<8, WP>;
+    case 12: return (void*)gom_univ_sliced_kernel<12, WP>;
+    case 16: return (void*)gom_univ_sliced_kernel<16, WP>;
+  }
+  throw GomixError(GOMIX_E_INVALID, "univariate sliced kernel: unsupported plane count");
+}
+
+void* univ_kernel(int planes, int wp) {
+  switch (wp) {
+    case 1: return univ_kernel_wp<1>(planes);
+    case 2: return univ_kernel_wp<2>(planes);
+    case 4: return univ_kernel_wp<4>(planes);
+  }
+  throw GomixError(GOMIX_E_INVALID, "univariate sliced kernel: unsupported row width");
+}
+}  // namespace
+
+int univ_sliced_planes(uint64_t max_abs_row_sum) {
+  // T <= A <= max_abs_row_sum must fit in B planes
+  for (int b : {4, 6, 8, 12, 16})
+    if (max_abs_row_sum < (1ull << b)) return b;
+  return 0;
+}
+
+int univ_sliced_block() { return kUnivWarps * 32; }
+
+int univ_sliced_sets_per_cta() { return kUnivWarps * 32; }
+
+int univ_sliced_max_blocks_per_sm(int planes, int wp) {
+  int blocks = 0;
+  GOMIX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, univ_kernel(planes, wp), kUnivWarps * 32, 0));
+  return blocks;
+}
+
+void launch_univ_sliced(const GomArgs& a, int planes, int wp, int grid, cudaStream_t s) {
+  void* fn = univ_kernel(planes, wp);
+  void* args[] = {(void*)&a};
+  GOMIX_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kUnivWarps * 32), args, 0, s));
+}
+
+}  // namespace gomix_b200

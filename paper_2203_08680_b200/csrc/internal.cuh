@@ -71,6 +71,7 @@ struct GroupDesc {
 struct Problem {
   int device = 0;
   uint64_t nv = 0, q = 0, m = 0, k = 0, lmig_edges = 0, max_f = 0, max_fp = 0;
+  uint64_t max_abs_row = 0;  // univariate: max over sets {v} of sum |w| on v's edges (integer weights)
   bool exact = true, univariate = true, i32 = false;
   // host mirrors (small)
   std::vector<uint64_t> h_set_off;
@@ -261,6 +262,12 @@ class ReplayStream {
 // kernel launchers (gom.cu)
 void launch_gom(const GomArgs& a, bool univariate, bool i32, int wpt, bool team, int grid, int block,
                 size_t smem, cudaStream_t s);
+// bit-sliced univariate kernel (gom_univ.cu)
+int univ_sliced_planes(uint64_t max_abs_row_sum);  // 0: not representable
+int univ_sliced_block();
+int univ_sliced_sets_per_cta();
+int univ_sliced_max_blocks_per_sm(int planes, int wp);
+void launch_univ_sliced(const GomArgs& a, int planes, int wp, int grid, cudaStream_t s);
 int gom_max_blocks_per_sm(bool univariate, bool i32, int wpt, bool team, int block, size_t smem);
 void launch_begin(const BeginArgs& b, cudaStream_t s);
 void launch_order(const BeginArgs& b, const OrderArgs& o, cudaStream_t s);

@@ -1,0 +1,113 @@
+"""The bit-sliced lane-per-set univariate kernel (csrc/gom_univ.cu) against
+the lane-per-solution kernel (csrc/gom.cu) on identical Philox runs.
+
+For a univariate FOS the Philox outcome does not depend on the donor draw
+(every differing donor holds the flipped bit), so both kernels must produce
+bit-identical populations, fitness, elitists, counters and stop decisions —
+and fitness must equal the cut value of every genotype (the checksum the
+full-size runs use).  Cases cover signed and zero weights, isolated vertices,
+populations that are not multiples of 32, every row width (1/2/4 words) and
+every plane count the kernel instantiates (4..16).
+"""
+import numpy as np
+import pytest
+
+import paper_2203_08680_b200 as G
+
+pytestmark = pytest.mark.gpu
+
+
+def _pair(P, n, seed, **kw):
+    a = G.GpuParallelEngine(P, n, seed, mode="philox", **kw)
+    b = G.GpuParallelEngine(P, n, seed, mode="philox", lane_per_solution=True, **kw)
+    return a, b
+
+
+def _same(inst, a, b):
+    ga, fa = a.population()
+    gb, fb = b.population()
+    assert (ga == gb).all()
+    assert (fa == fb).all()
+    assert (inst.cut_values(ga) == fa).all()
+    ea, efa = a.elitist()
+    eb, efb = b.elitist()
+    assert efa == efb and (ea == eb).all()
+    for x, y in zip(a.group_counters(), b.group_counters()):
+        assert (x == y).all()
+
+
+def _sparse_graph(nv, avg_deg, wlo, whi, seed, isolated=0):
+    rs = np.random.RandomState(seed)
+    m = nv * avg_deg // 2
+    u = rs.randint(0, nv - isolated, m)
+    v = rs.randint(0, nv - isolated, m)
+    keep = u != v
+    a, b = np.minimum(u, v)[keep], np.maximum(u, v)[keep]
+    e = np.unique(np.stack([a, b], 1), axis=0)
+    w = rs.randint(wlo, whi + 1, len(e)).astype(np.float64)
+    return G.MaxCutInstance(nv, e[:, 0].astype(np.uint32), e[:, 1].astype(np.uint32), w)
+
+
+@pytest.mark.parametrize("shape,weights,n,gens", [
+    ((16, 12), ("int", -5, 9), 100, 6),   # signed weights, n % 32 != 0, 4 words
+    ((20, 20), ("int", 1, 10), 128, 5),   # C3 shape in small
+    ((10, 10), ("int", 1, 10), 32, 8),    # C1 shape, 1 word
+    ((14, 9), ("int", -3, 3), 64, 6),     # zero weights, 2 words
+    ((9, 7), ("int", 1, 10), 20, 6),      # odd torus (3 colours), 20 members
+])
+def test_sliced_equals_lane_per_solution_torus(shape, weights, n, gens):
+    inst = G.generate_torus(shape[0], shape[1], weights, 3)
+    P = G.GpuProblem(inst, G.univariate_fos(inst.num_vertices))
+    a, b = _pair(P, n, 7)
+    _same(inst, a, b)
+    for _ in range(gens):
+        a.run_generation()
+        b.run_generation()
+        _same(inst, a, b)
+
+
+@pytest.mark.parametrize("avg_deg,wlo,whi,n", [
+    (16, 1, 10, 128),       # A up to ~300: 12 planes
+    (6, -1000, 1000, 64),   # 16 planes
+    (3, 0, 1, 96),          # 4 planes, many zero weights
+])
+def test_sliced_equals_lane_per_solution_random_graphs(avg_deg, wlo, whi, n):
+    inst = _sparse_graph(3000, avg_deg, wlo, whi, 5, isolated=40)
+    P = G.GpuProblem(inst, G.univariate_fos(inst.num_vertices))
+    a, b = _pair(P, n, 9)
+    for _ in range(5):
+        a.run_generation()
+        b.run_generation()
+        _same(inst, a, b)
+
+
+def test_sliced_stop_criteria_match():
+    inst = G.generate_torus(30, 30, ("int", 1, 10), 2)
+    P = G.GpuProblem(inst, G.univariate_fos(900))
+    for crit in (dict(max_evaluations=5000.0), dict(target_fitness=3000.0)):
+        ca = G.RunContext(G.TerminationConfig(**crit), P.comparator(), inst.num_edges)
+        cb = G.RunContext(G.TerminationConfig(**crit), P.comparator(), inst.num_edges)
+        a = G.GpuParallelEngine(P, 64, 3, ctx=ca, mode="philox")
+        b = G.GpuParallelEngine(P, 64, 3, ctx=cb, mode="philox", lane_per_solution=True)
+        for _ in range(400):
+            a.run_generation()
+            b.run_generation()
+            if ca.control.stop_requested():
+                break
+        assert ca.control.stop_requested() and cb.control.stop_requested()
+        assert ca.control.reason == cb.control.reason
+        assert ca.control.calls == cb.control.calls
+        assert a.generation() == b.generation()
+        _same(inst, a, b)
+
+
+def test_sliced_full_size_c3():
+    """C3 (10^6 vertices, n=128): both kernels agree after two generations and
+    fitness is the cut value of every member."""
+    inst = G.generate_torus(1000, 1000, ("int", 1, 10), 1)
+    P = G.GpuProblem(inst, G.univariate_fos(inst.num_vertices))
+    a, b = _pair(P, 128, 1)
+    for _ in range(2):
+        a.run_generation()
+        b.run_generation()
+    _same(inst, a, b)
