@@ -105,6 +105,7 @@ typedef struct {
 typedef struct gomix_gpu_problem gomix_gpu_problem;
 typedef struct gomix_gpu_engine gomix_gpu_engine;
 typedef struct gomix_gpu_local_group gomix_gpu_local_group;
+typedef struct gomix_gpu_ims_best gomix_gpu_ims_best;
 
 /* EngineConfig (engine_serial.hpp:18-24). */
 typedef struct {
@@ -241,6 +242,23 @@ GOMIX_API int gomix_gpu_kernel_times(gomix_gpu_engine* e, float* ms, uint64_t ca
 GOMIX_API int gomix_gpu_set_timing(gomix_gpu_engine* e, int32_t enable);
 /* Number of device kernels this engine has launched so far. */
 GOMIX_API int gomix_gpu_launch_count(gomix_gpu_engine* e, uint64_t* count);
+
+/* ---- IMS on the device (ims.hpp:38-101) ---------------------------------------- */
+
+/* The run-wide best solution of an interleaved multistart run
+ * (ImsDriver::best_), resident on the problem's device. */
+GOMIX_API int gomix_gpu_ims_best_create(gomix_gpu_problem* p, gomix_gpu_ims_best** out);
+GOMIX_API int gomix_gpu_ims_best_destroy(gomix_gpu_ims_best* b);
+/* ImsDriver::collect (ims.hpp:89-95): best = e's elitist if strictly better
+ * (or no best yet).  Queued on e's stream, no host synchronisation; every
+ * collect / offer on the same best is ordered after the previous one. */
+GOMIX_API int gomix_gpu_ims_collect(gomix_gpu_ims_best* b, gomix_gpu_engine* e);
+/* runner->offer_elitist(best_) (ims.hpp:83, engine_parallel.hpp:320-322): e
+ * adopts the best iff strictly better than its elitist.  Queued, no sync. */
+GOMIX_API int gomix_gpu_ims_offer(gomix_gpu_ims_best* b, gomix_gpu_engine* e);
+/* Waits for the queued exchanges; genotype (num_vertices bytes) may be NULL. */
+GOMIX_API int gomix_gpu_ims_best_read(gomix_gpu_ims_best* b, uint8_t* genotype, double* fitness,
+                                      int32_t* valid);
 
 /* ---- multi-GPU sharding ------------------------------------------------------ */
 

@@ -9,8 +9,10 @@ from .maxcut import (Fos, MaxCutInstance, generate_regular, generate_torus, load
 from .engine import (FitnessComparator, GpuLocalGroup, GpuParallelEngine, GpuProblem,  # noqa: F401
                      RecordingSink, RunContext, RunControl, TerminationConfig, TraceSink, gpu_color, mix64,
                      nccl_unique_id, population_seed, shard_range)
+from .ims import DeviceBest, GpuImsDriver, ImsConfig, RunResult, run_gpu  # noqa: F401
 
 __all__ = ["Fos", "MaxCutInstance", "generate_regular", "generate_torus", "load_edge_list", "neighbourhood_fos",
            "save_edge_list", "univariate_fos", "FitnessComparator", "GpuLocalGroup", "GpuParallelEngine", "GpuProblem",
            "RecordingSink", "RunContext", "RunControl", "TerminationConfig", "TraceSink", "gpu_color", "mix64",
-           "nccl_unique_id", "population_seed", "shard_range"]
+           "nccl_unique_id", "population_seed", "shard_range", "DeviceBest", "GpuImsDriver", "ImsConfig",
+           "RunResult", "run_gpu"]

@@ -99,6 +99,11 @@ _SIGNATURES = {
     "gomix_gpu_set_timing": ([_P, C.c_int32], C.c_int),
     "gomix_gpu_color": ([C.POINTER(Maxcut), C.POINTER(Fos), C.c_int32, _P, C.POINTER(C.c_uint64),
                          C.POINTER(C.c_uint64)], C.c_int),
+    "gomix_gpu_ims_best_create": ([_P, C.POINTER(_P)], C.c_int),
+    "gomix_gpu_ims_best_destroy": ([_P], C.c_int),
+    "gomix_gpu_ims_collect": ([_P, _P], C.c_int),
+    "gomix_gpu_ims_offer": ([_P, _P], C.c_int),
+    "gomix_gpu_ims_best_read": ([_P, _P, C.POINTER(C.c_double), C.POINTER(C.c_int32)], C.c_int),
     "gomix_gpu_nccl_unique_id": ([_P], C.c_int),
     "gomix_gpu_local_group_create": ([_P, C.POINTER(EngineConfig), C.POINTER(_P)], C.c_int),
     "gomix_gpu_local_group_destroy": ([_P], C.c_int),

@@ -338,6 +338,7 @@ struct gomix_gpu_engine {
   int64_t generation = 0;
   bool initialized = false;
   double elit_fit = 0.0;
+  bool ctl_stale = false;  // a device-side IMS offer may have changed the elitist since read_ctl()
   std::vector<uint32_t> h_pop;
   std::vector<uint64_t> perm;
   int64_t last_group = -1;
@@ -564,6 +565,16 @@ struct gomix_gpu_engine {
   void read_ctl() {
     GOMIX_CUDA(cudaMemcpyAsync(h_ctl, ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, stream));
     GOMIX_CUDA(cudaStreamSynchronize(stream));
+    ctl_stale = false;
+  }
+
+  // host copy of the elitist fitness, refreshed after device-side IMS offers
+  double host_elit_fit() {
+    if (ctl_stale) {
+      read_ctl();
+      elit_fit = h_ctl->elit_fit;
+    }
+    return elit_fit;
   }
 
   void fill_stats(gomix_run_stats* out) {
@@ -1246,7 +1257,7 @@ int gomix_gpu_read_elitist(gomix_gpu_engine* e, uint8_t* genotype, double* fitne
       GOMIX_CUDA(cudaMemcpyAsync(genotype, d, e->P->nv, cudaMemcpyDeviceToHost, e->stream));
     }
     GOMIX_CUDA(cudaStreamSynchronize(e->stream));
-    if (fitness) *fitness = e->elit_fit;
+    if (fitness) *fitness = e->host_elit_fit();
   });
 }
 
@@ -1255,7 +1266,7 @@ int gomix_gpu_offer_elitist(gomix_gpu_engine* e, const uint8_t* genotype, double
   return guarded([&] {
     if (!e || !genotype) invalid("offer_elitist: NULL argument");
     if (!e->initialized) throw GomixError(GOMIX_E_STATE, "offer_elitist: population not initialised");
-    const bool take = e->better(fitness, e->elit_fit);
+    const bool take = e->better(fitness, e->host_elit_fit());
     if (adopted) *adopted = take;
     if (!take) return;
     const uint64_t nv = e->P->nv;
@@ -1268,6 +1279,94 @@ int gomix_gpu_offer_elitist(gomix_gpu_engine* e, const uint8_t* genotype, double
     e->launches += 2;
     GOMIX_CUDA(cudaStreamSynchronize(e->stream));
     e->elit_fit = fitness;
+  });
+}
+
+// ---- IMS on the device ---------------------------------------------------------
+struct gomix_gpu_ims_best {
+  Problem* P = nullptr;
+  int device = 0;
+  ImsBestDev* dev = nullptr;
+  uint32_t* bits = nullptr;
+  ImsBestDev* host = nullptr;  // pinned
+  cudaEvent_t ev = nullptr;    // last queued exchange
+  cudaStream_t last = nullptr;
+  std::vector<void*> allocs;
+  ~gomix_gpu_ims_best() {
+    if (ev) cudaEventSynchronize(ev), cudaEventDestroy(ev);
+    for (void* p : allocs) cudaFree(p);
+    if (host) cudaFreeHost(host);
+  }
+  void order_before(gomix_gpu_engine* e) {
+    if (e->P != P) invalid("ims: engine belongs to another problem");
+    if (e->R > 1) invalid("ims: sharded engines are not supported");
+    if (!e->initialized) throw GomixError(GOMIX_E_STATE, "ims: population not initialised");
+    GOMIX_CUDA(cudaStreamWaitEvent(e->stream, ev, 0));
+  }
+  void order_after(gomix_gpu_engine* e) {
+    GOMIX_CUDA(cudaEventRecord(ev, e->stream));
+    last = e->stream;
+  }
+};
+
+int gomix_gpu_ims_best_create(gomix_gpu_problem* p, gomix_gpu_ims_best** out) {
+  return guarded([&] {
+    if (!p || !out) invalid("ims_best_create: NULL argument");
+    auto b = std::make_unique<gomix_gpu_ims_best>();
+    b->P = p->P.get();
+    b->device = b->P->device;
+    GOMIX_CUDA(cudaSetDevice(b->device));
+    b->dev = dev_alloc<ImsBestDev>(b->allocs, 1);
+    b->bits = dev_alloc<uint32_t>(b->allocs, (b->P->nv + 31) / 32);
+    GOMIX_CUDA(cudaMemset(b->dev, 0, sizeof(ImsBestDev)));
+    GOMIX_CUDA(cudaMemset(b->bits, 0, ((b->P->nv + 31) / 32) * 4));
+    GOMIX_CUDA(cudaMallocHost(&b->host, sizeof(ImsBestDev)));
+    GOMIX_CUDA(cudaEventCreateWithFlags(&b->ev, cudaEventDisableTiming));
+    GOMIX_CUDA(cudaDeviceSynchronize());
+    *out = b.release();
+  });
+}
+
+int gomix_gpu_ims_best_destroy(gomix_gpu_ims_best* b) {
+  delete b;
+  return GOMIX_OK;
+}
+
+int gomix_gpu_ims_collect(gomix_gpu_ims_best* b, gomix_gpu_engine* e) {
+  return guarded([&] {
+    if (!b || !e) invalid("ims_collect: NULL argument");
+    b->order_before(e);
+    launch_ims_collect(e->snap_args(), b->dev, b->bits, e->P->exact, e->stream);
+    e->launches += 2;
+    b->order_after(e);
+  });
+}
+
+int gomix_gpu_ims_offer(gomix_gpu_ims_best* b, gomix_gpu_engine* e) {
+  return guarded([&] {
+    if (!b || !e) invalid("ims_offer: NULL argument");
+    b->order_before(e);
+    launch_ims_offer(e->snap_args(), b->dev, b->bits, e->P->exact, e->stream);
+    e->launches += 2;
+    e->ctl_stale = true;
+    b->order_after(e);
+  });
+}
+
+int gomix_gpu_ims_best_read(gomix_gpu_ims_best* b, uint8_t* genotype, double* fitness, int32_t* valid) {
+  return guarded([&] {
+    if (!b) invalid("ims_best_read: NULL argument");
+    GOMIX_CUDA(cudaSetDevice(b->device));
+    GOMIX_CUDA(cudaEventSynchronize(b->ev));
+    GOMIX_CUDA(cudaMemcpy(b->host, b->dev, sizeof(ImsBestDev), cudaMemcpyDeviceToHost));
+    if (fitness) *fitness = b->host->fit;
+    if (valid) *valid = b->host->valid;
+    if (genotype) {
+      const uint64_t nv = b->P->nv;
+      std::vector<uint32_t> w((nv + 31) / 32);
+      GOMIX_CUDA(cudaMemcpy(w.data(), b->bits, w.size() * 4, cudaMemcpyDeviceToHost));
+      for (uint64_t v = 0; v < nv; ++v) genotype[v] = (w[v >> 5] >> (v & 31)) & 1u;
+    }
   });
 }
 

@@ -121,6 +121,81 @@ __global__ void external_elitist_hash_kernel(const SnapArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// IMS elitist exchange on the device (ImsDriver::collect / offer_elitist,
+// ims.hpp:77-95, engine_parallel.hpp:320-322): the decision is taken by one
+// thread, the ℓ-bit copy by the grid, so no host round trip is needed.
+// ---------------------------------------------------------------------------
+__global__ void ims_collect_decide_kernel(const DevCtl* c, ImsBestDev* b, int exact) {
+  const bool take = c->elit_src != -1 && (!b->valid || cmp_better(exact != 0, c->elit_fit, b->fit));
+  b->flag = take;
+  if (take) b->pending = c->elit_fit;
+}
+
+// best bits = the engine's elitist genotype (copy-on-write snapshot rows where
+// captured, otherwise population column elit_src; elit_src == -2: given bits)
+__global__ void ims_collect_copy_kernel(const SnapArgs a, ImsBestDev* b, uint32_t* bits) {
+  if (!*(volatile int32_t*)&b->flag) return;
+  const DevCtl* c = a.ctl;
+  const int32_t src = c->elit_src;
+  const uint32_t ver = c->elit_ver;
+  const uint64_t words = (a.nv + 31) / 32;
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < words;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t word = a.elit[t];
+    if (src >= 0) {
+      const uint32_t sw = (uint32_t)src >> 5, sb = (uint32_t)src & 31u;
+      for (uint32_t k = 0; k < 32 && t * 32 + k < a.nv; ++k) {
+        const uint64_t v = t * 32 + k;
+        if (a.ever[v] != ver) word = (word & ~(1u << k)) | (((a.pop[v * a.Wp + sw] >> sb) & 1u) << k);
+      }
+    }
+    bits[t] = word;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    b->fit = b->pending;
+    b->valid = 1;
+  }
+}
+
+__global__ void ims_offer_decide_kernel(DevCtl* c, ImsBestDev* b, int exact) {
+  const bool take = b->valid && cmp_better(exact != 0, b->fit, c->elit_fit);
+  b->flag = take;
+  if (take) {
+    c->elit_fit = b->fit;
+    c->elit_src = -2;
+    c->eh1 = 0;
+    c->eh2 = 0;
+    c->elit_ver += 1;
+  }
+}
+
+__global__ void ims_offer_copy_kernel(const SnapArgs a, const ImsBestDev* b, const uint32_t* bits) {
+  if (!*(volatile const int32_t*)&b->flag) return;
+  unsigned long long h1 = 0, h2 = 0;
+  const uint64_t words = (a.nv + 31) / 32;
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < words;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t word = bits[t];
+    a.elit[t] = word;
+    for (uint32_t m = word; m; m &= m - 1) {
+      unsigned long long z1, z2;
+      zobrist((uint32_t)(t * 32 + (__ffs(m) - 1)), z1, z2);
+      h1 ^= z1;
+      h2 ^= z2;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    h1 ^= __shfl_xor_sync(0xFFFFFFFFu, h1, o);
+    h2 ^= __shfl_xor_sync(0xFFFFFFFFu, h2, o);
+  }
+  if ((threadIdx.x & 31u) == 0 && (h1 | h2)) {
+    atomicXor(&a.ctl->eh1, h1);
+    atomicXor(&a.ctl->eh2, h2);
+  }
+}
+
 // A row's words owned by this thread: all WPT words (vector loads) for a
 // one-warp team, every tw-th word otherwise.
 template <int WPT, bool TEAM>
@@ -996,6 +1071,18 @@ void launch_finalize_elitist(const SnapArgs& a, cudaStream_t s) {
 void launch_external_elitist(const SnapArgs& a, double fitness, cudaStream_t s) {
   external_elitist_reset_kernel<<<1, 1, 0, s>>>(a.ctl, fitness);
   external_elitist_hash_kernel<<<grid_for(a.nv, 256, 148 * 8), 256, 0, s>>>(a);
+  GOMIX_CUDA(cudaGetLastError());
+}
+
+void launch_ims_collect(const SnapArgs& a, ImsBestDev* b, uint32_t* bits, int exact, cudaStream_t s) {
+  ims_collect_decide_kernel<<<1, 1, 0, s>>>(a.ctl, b, exact);
+  ims_collect_copy_kernel<<<grid_for((a.nv + 31) / 32, 256, 148 * 4), 256, 0, s>>>(a, b, bits);
+  GOMIX_CUDA(cudaGetLastError());
+}
+
+void launch_ims_offer(const SnapArgs& a, ImsBestDev* b, const uint32_t* bits, int exact, cudaStream_t s) {
+  ims_offer_decide_kernel<<<1, 1, 0, s>>>(a.ctl, b, exact);
+  ims_offer_copy_kernel<<<grid_for((a.nv + 31) / 32, 256, 148 * 4), 256, 0, s>>>(a, b, bits);
   GOMIX_CUDA(cudaGetLastError());
 }
 

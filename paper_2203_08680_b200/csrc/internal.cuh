@@ -181,6 +181,14 @@ struct GomArgs {
   const GroupDesc* groups;
 };
 
+// Run-wide best of an IMS run (ImsDriver::best_, ims.hpp:98-99), device-resident.
+struct ImsBestDev {
+  double fit;
+  double pending;
+  int32_t valid;
+  int32_t flag;  // decision of the last collect / offer (consumed by its copy kernel)
+};
+
 struct OrderArgs {
   DevCtl* ctl;
   uint32_t* order;
@@ -277,6 +285,8 @@ void launch_global_epilogue(const EpiArgs& a, cudaStream_t s);
 void launch_hash_population(const SnapArgs& a, cudaStream_t s);
 void launch_finalize_elitist(const SnapArgs& a, cudaStream_t s);
 void launch_external_elitist(const SnapArgs& a, double fitness, cudaStream_t s);
+void launch_ims_collect(const SnapArgs& a, ImsBestDev* b, uint32_t* bits, int exact, cudaStream_t s);
+void launch_ims_offer(const SnapArgs& a, ImsBestDev* b, const uint32_t* bits, int exact, cudaStream_t s);
 void launch_philox_init(uint32_t* pop, uint64_t nv, uint32_t n, uint32_t Wp, uint64_t seed,
                         uint32_t rank, cudaStream_t s);
 void launch_full_eval(const Problem& P, const uint32_t* pop, double* fit, uint32_t n,

@@ -10,6 +10,7 @@ themselves travel with the repo and are what the GPU-box tests read.
 from __future__ import annotations
 
 import hashlib
+import json
 import os
 import sys
 import tempfile
@@ -43,6 +44,20 @@ COLOR_CASES = [
     ("col_torus40_bflt10", ["--torus", 40, 40, "--weights", "unit"], "bflt:10"),
     ("col_reg8", ["@reg", 200, 8, 31], "univariate"),
     ("col_reg5odd", ["@reg", 64, 5, 32], "neigh"),
+]
+
+
+# IMS runs (run_parallel with use_ims, run.hpp:72-82): (name, instance, fos,
+# seed, base, subgenerations, extra termination args)
+IMS_CASES = [
+    ("ims_c1", ["--torus", 10, 10, "--weights", "int:1:10", "--inst-seed", 1], "univariate", 1, 16, 4,
+     ["--max-evals", 3000]),
+    ("ims_pm5", ["--torus", 10, 10, "--weights", "int:-5:5", "--inst-seed", 1], "univariate", 3, 8, 2,
+     ["--max-evals", 4000]),
+    ("ims_neigh", ["--torus", 12, 12, "--weights", "int:1:10", "--inst-seed", 2], "neigh", 5, 16, 4,
+     ["--max-evals", 1500]),
+    ("ims_target", ["--torus", 8, 8, "--weights", "unit", "--inst-seed", 1], "univariate", 2, 4, 4,
+     ["--target", 128, "--max-evals", 100000]),
 ]
 
 
@@ -109,6 +124,19 @@ def main():
             np.savez_compressed(os.path.join(HERE, name + ".npz"), **d)
             print(f"{name}: nv={nv} groups={len(d['group_off']) - 1} "
                   f"best={d['elitist'][-1]} trace={len(d['trace_fitness'])}")
+        for name, inst, fos, seed, base, sub, term in IMS_CASES:
+            r = json.loads(O.run_ref("ims", *instance_args(inst, tmp), "--fos", fos, "--seed", seed, "--ims",
+                                     "--ims-base", base, "--ims-sub", sub, "--workers", 2, *term))
+            tr = np.array(r["trace"], np.float64).reshape(-1, 3)
+            d = {"best": np.array([r["best"]]), "reason": np.array([r["reason"]]),
+                 "evaluations": np.array([r["evaluations"]]), "generations": np.array([r["generations"]]),
+                 "populations": np.array([r["populations"]]), "trace_evals": tr[:, 1], "trace_fitness": tr[:, 2],
+                 "seed": np.array([seed], np.uint64), "base": np.array([base]), "sub": np.array([sub]),
+                 "fos_kind": np.array([fos]), "term": np.array([str(x) for x in term])}
+            d.update(O.run_ref("color", *instance_args(inst, tmp), "--fos", fos,
+                               out=os.path.join(tmp, name + ".bin")))
+            np.savez_compressed(os.path.join(HERE, name + ".npz"), **d)
+            print(f"{name}: best={r['best']} reason={r['reason']} pops={r['populations']} trace={len(tr)}")
         for name, inst, fos in COLOR_CASES:
             out = os.path.join(tmp, name + ".bin")
             d = O.run_ref("color", *instance_args(inst, tmp), "--fos", fos, out=out)

@@ -9,6 +9,6 @@ extra=""; [ -n "$pop" ] && extra="--population $pop"
 mkdir -p gpurun_out
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${tag}_launches.csv \
     python tools/prof_driver.py --config $cfg --gens $gens $extra > gpurun_out/${tag}_launches.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:gom_group_kernel -s 8 -c 2 \
+ncu --set full --clock-control none --import-source on -k regex:gom_ -s ${SKIP:-4} -c 2 \
     -o gpurun_out/${tag} -f python tools/prof_driver.py --config $cfg --gens $gens $extra > gpurun_out/${tag}_full.log 2>&1
 echo "profile $tag done"
