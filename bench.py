@@ -70,6 +70,8 @@ def parse():
     ap.add_argument("--population", type=int, default=None)
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ttt-seconds", type=float, default=20.0,
+                    help="time-to-best-known-cut leg: reference IMS budget T_ref (0 = skip)")
     return ap.parse_args()
 
 
@@ -97,8 +99,9 @@ def base_line(args, cfg, n, world):
     return {"metric": METRIC, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
             "data": "synthetic (generated Max-Cut torus, reference generator and seed)",
-            "config": {"workload": cfg["workload"], "population": n, "population_per_gpu": n,
-                       "parallelism": f"replicas{world}" if world > 1 else "single",
+            "config": {"workload": cfg["workload"], "population": n * world, "population_per_gpu": n,
+                       "parallelism": f"population sharded over {world} GPUs (NCCL all-gather of the donor pool "
+                                      f"per colour group)" if world > 1 else "single",
                        "l2": "flushed between timed steps (256 MiB write)",
                        "donors": "philox", "fos": cfg["fos"]}}
 
@@ -221,7 +224,17 @@ def bench_ours(args):
     P = G.GpuProblem(inst, fos, device=dev)
     stream = torch.cuda.Stream()  # a real stream: the legacy NULL stream would not see our kernels
     torch.cuda.set_stream(stream)
-    E = G.GpuParallelEngine(P, n, seed=1 + rank, mode="philox", stream=stream.cuda_stream)
+    if world > 1:
+        # one population of n * world members sharded over the ranks (weak
+        # scaling: n members per GPU); the NCCL id travels over the PG
+        uid = [G.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        E = G.GpuParallelEngine(P, n * world, seed=1, mode="philox", stream=stream.cuda_stream, rank=rank,
+                                world_size=world, nccl_unique_id=uid[0])
+        gen = E.run_generation          # collective per colour group: host-ordered
+    else:
+        E = G.GpuParallelEngine(P, n, seed=1, mode="philox", stream=stream.cuda_stream)
+        gen = E.run_generation_async    # one CUDA graph per generation, no host sync
 
     def barrier():
         if dist is not None:
@@ -229,7 +242,7 @@ def bench_ours(args):
 
     # warm-up
     for _ in range(max(args.warmup, 3)):
-        E.run_generation_async()
+        gen()
     E.synchronize()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MiB > 126 MB L2
 
@@ -254,7 +267,7 @@ def bench_ours(args):
     for i in range(args.steps):
         flush.zero_()
         ev0[i].record(stream)
-        E.run_generation_async()
+        gen()
         ev1[i].record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -266,7 +279,7 @@ def bench_ours(args):
     soak_t0 = time.perf_counter()
     while time.perf_counter() - soak_t0 < max(0.0, 0.6 - t_wall):
         for _ in range(20):
-            E.run_generation_async()
+            gen()
         torch.cuda.synchronize()
     E.synchronize()
     clk = clocks.stop()
@@ -278,7 +291,7 @@ def bench_ours(args):
     E.kernel_times()
     for _ in range(kern_gens):
         flush.zero_()
-        E.run_generation_async()
+        gen()
     E.synchronize()
     kern_ms = E.kernel_times()
     E.set_timing(False)
@@ -291,9 +304,9 @@ def bench_ours(args):
     if dist is not None:
         t = torch.tensor([dev_s], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        s = torch.tensor([steps, calls], dtype=torch.float64, device="cuda")
-        dist.all_reduce(s, op=dist.ReduceOp.SUM)
-        dev_s, steps, calls = float(t.item()), int(s[0].item()), int(s[1].item())
+        # sharded counters are already global (every rank accounts all ranks'
+        # steps in its epilogue): no sum over ranks
+        dev_s = float(t.item())
     value = steps / dev_s
 
     # ---- e2e through the C-ABI with host buffers ----
@@ -313,7 +326,7 @@ def bench_ours(args):
     for _ in range(e2e_steps):
         E.load_population(g_host, f_host)          # H2D: n*l genotype bytes + n fitness doubles
         E.run_generation()
-        e2e_done += int(E.last_stats.steps)
+        e2e_done += int(E.last_stats.steps)        # global steps (sharded stats are global)
         E.population(g_host, f_host)               # D2H: n*l genotype bytes + n fitness doubles
     torch.cuda.synchronize()
     barrier()
@@ -321,9 +334,7 @@ def bench_ours(args):
     if dist is not None:
         t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        s = torch.tensor([e2e_done], dtype=torch.float64, device="cuda")
-        dist.all_reduce(s, op=dist.ReduceOp.SUM)
-        e2e_s, e2e_done = float(t.item()), int(s.item())
+        e2e_s = float(t.item())
     io_bytes = n * inst.num_vertices + 8 * n
 
     if rank != 0:
@@ -376,6 +387,28 @@ def bench_ours(args):
                 cpu_baseline = {"value": None, "unit": UNIT, "cores": workers, "kind": "reference",
                                 "sample": f"failed: {exc}"}
 
+    time_to_target = None
+    if world == 1 and args.ttt_seconds > 0:
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "tools"))
+            import time_to_target as TT
+
+            ref = TT.reference_ims(cfg, 1, args.ttt_seconds, os.cpu_count() or 1)
+            gpu = TT.gpu_ims(cfg, ref["best"], 1, args.ttt_seconds)
+            time_to_target = {
+                "unit": "s", "target_cut": ref["best"],
+                "target": f"best cut of the reference IMS (base 16, sub 4, {cfg['fos']} FOS, "
+                          f"{os.cpu_count()} threads) within {args.ttt_seconds:g} s, seed 1",
+                "cpu_s": ref["seconds_to_best"], "gpu_s": gpu["seconds_to_target"],
+                "gpu_s_incl_build": gpu["seconds_to_target_incl_build"], "gpu_reached": gpu["reached"],
+                "speedup": (ref["seconds_to_best"] / gpu["seconds_to_target"]) if gpu["reached"] else None,
+                "gpu_build_s": gpu["build_seconds"], "gpu_evaluations": gpu["evaluations"],
+                "cpu_evaluations": ref["evaluations"],
+                "timing": "both from RunContext creation to the improvement reaching the cut (model prebuilt); "
+                          "gpu_s_incl_build adds the device problem build (CSR, GPU colouring)"}
+        except Exception as exc:  # noqa: BLE001
+            time_to_target = {"error": str(exc)[:300]}
+
     line = base_line(args, cfg, n, world)
     line.update({
         "value": value,
@@ -385,6 +418,7 @@ def bench_ours(args):
                 "what": "load_population + run_generation + read_population via the C-ABI, host buffers"},
         "roofline": roofline,
         "cpu_baseline": cpu_baseline,
+        "time_to_target": time_to_target,
         "clocks": clk,
         "gpu_launches": int(launches),
         "evaluator_calls_per_s": calls / dev_s,

@@ -314,6 +314,11 @@ struct gomix_gpu_engine {
   uint32_t* elit = nullptr;
   DevCtl* ctl = nullptr;
   DevCtl* h_ctl = nullptr;  // pinned
+  BeginArgs* d_begin = nullptr;  // per-call criteria read by the graph's begin kernel
+  BeginArgs* h_begin = nullptr;  // pinned staging of d_begin
+  static constexpr uint64_t kImprInline = 64;  // improvements copied back with every read_ctl
+  double* h_impr = nullptr;                    // pinned [kImprInline]
+  unsigned long long* h_impr_calls = nullptr;  // pinned [kImprInline]
   unsigned long long* gsteps = nullptr;
   unsigned long long* gcalls = nullptr;
   double* impr = nullptr;
@@ -356,6 +361,9 @@ struct gomix_gpu_engine {
     for (auto e : ev_free) cudaEventDestroy(e);
     for (void* p : allocs) cudaFree(p);
     if (h_ctl) cudaFreeHost(h_ctl);
+    if (h_begin) cudaFreeHost(h_begin);
+    if (h_impr) cudaFreeHost(h_impr);
+    if (h_impr_calls) cudaFreeHost(h_impr_calls);
     if (h_tape_pinned) cudaFreeHost(h_tape_pinned);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
@@ -476,7 +484,6 @@ struct gomix_gpu_engine {
     impr = dev_alloc<double>(allocs, impr_cap);
     impr_calls = dev_alloc<unsigned long long>(allocs, impr_cap);
     if (epi_mode == 1) part = dev_alloc<double>(allocs, (size_t)grid_cap * n);
-    tape = dev_alloc<int32_t>(allocs, max_group * n);
     d_order = dev_alloc<uint32_t>(allocs, P->k);
     d_groups = dev_alloc<GroupDesc>(allocs, P->k);
     {
@@ -493,7 +500,10 @@ struct gomix_gpu_engine {
       rec_accept = dev_alloc<uint8_t>(allocs, max_group * n);
     }
     GOMIX_CUDA(cudaMallocHost(&h_ctl, sizeof(DevCtl)));
-    GOMIX_CUDA(cudaMallocHost(&h_tape_pinned, std::max<uint64_t>(1, max_group * n) * sizeof(int32_t)));
+    GOMIX_CUDA(cudaMallocHost(&h_begin, sizeof(BeginArgs)));
+    GOMIX_CUDA(cudaMallocHost(&h_impr, kImprInline * sizeof(double)));
+    GOMIX_CUDA(cudaMallocHost(&h_impr_calls, kImprInline * sizeof(unsigned long long)));
+    d_begin = dev_alloc<BeginArgs>(allocs, 1);
     std::memset(h_ctl, 0, sizeof(DevCtl));
     h_ctl->elit_src = -1;
     h_ctl->exact = P->exact;
@@ -515,6 +525,20 @@ struct gomix_gpu_engine {
   }
 
   // ---- per-call control ------------------------------------------------------
+  BeginArgs make_begin(const gomix_stop_criteria* stop) const {
+    BeginArgs b{};
+    b.ctl = ctl;
+    b.has_budget = stop && stop->has_max_evaluations;
+    b.has_target = stop && stop->has_target;
+    b.exact = P->exact;
+    b.max_evals = stop ? stop->max_evaluations : 0.0;
+    b.q = (double)P->q;
+    b.target = stop ? stop->target_fitness : 0.0;
+    b.calls_before = stop ? stop->evaluator_calls_before : 0;
+    b.gen = (uint32_t)generation;
+    return b;
+  }
+
   void begin_call(const gomix_stop_criteria* stop) {
     BeginArgs b;
     b.ctl = ctl;
@@ -530,10 +554,6 @@ struct gomix_gpu_engine {
     ++launches;
   }
 
-  static bool no_criteria(const gomix_stop_criteria* stop) {
-    return !stop || (!stop->has_max_evaluations && !stop->has_target);
-  }
-
   // One CUDA graph per engine for a whole Philox generation: the order
   // kernel, then k GOM launches that find their group through
   // the device-side order.  Replaces ~2k launches by one graph launch.
@@ -542,12 +562,8 @@ struct gomix_gpu_engine {
       cudaStream_t cap = nullptr;
       GOMIX_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
       GOMIX_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
-      BeginArgs b{};
-      b.ctl = ctl;
-      b.exact = P->exact;
-      b.q = (double)P->q;
       OrderArgs o{ctl, d_order, (uint32_t)P->k, seed};
-      launch_order(b, o, cap);
+      launch_order(d_begin, o, cap);
       const uint64_t saved = launches;
       for (uint64_t slot = 0; slot < P->k; ++slot) launch_group(0, false, (int32_t)slot, cap);
       graph_launches = launches - saved + 1;
@@ -562,8 +578,20 @@ struct gomix_gpu_engine {
     launches += graph_launches;
   }
 
+  // Stage this call's stop criteria for the graph's begin kernel.  The pinned
+  // staging buffer is only rewritten when no earlier copy from it can be
+  // pending (sync calls wait first; async calls always stage "no criteria").
+  void stage_criteria(const gomix_stop_criteria* stop, bool sync_first) {
+    if (sync_first) GOMIX_CUDA(cudaStreamSynchronize(stream));
+    *h_begin = make_begin(stop);
+    GOMIX_CUDA(cudaMemcpyAsync(d_begin, h_begin, sizeof(BeginArgs), cudaMemcpyHostToDevice, stream));
+  }
+
   void read_ctl() {
     GOMIX_CUDA(cudaMemcpyAsync(h_ctl, ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, stream));
+    GOMIX_CUDA(cudaMemcpyAsync(h_impr, impr, std::min(kImprInline, impr_cap) * 8, cudaMemcpyDeviceToHost, stream));
+    GOMIX_CUDA(cudaMemcpyAsync(h_impr_calls, impr_calls, std::min(kImprInline, impr_cap) * 8,
+                               cudaMemcpyDeviceToHost, stream));
     GOMIX_CUDA(cudaStreamSynchronize(stream));
     ctl_stale = false;
   }
@@ -726,7 +754,16 @@ struct gomix_gpu_engine {
   // ---- replay: the reference's sequential donor draws ----------------------
   // insert_donor_genes (engine_parallel.hpp:110-120) + select_donor
   // (engine_serial.hpp:30-46) against the group-start population.
+  // donor tapes (replay mode / explicit donors) are allocated on first use:
+  // max_group * n entries is a gigabyte at 10^6 vertices and n = 512
+  void ensure_tape() {
+    if (tape) return;
+    tape = dev_alloc<int32_t>(allocs, max_group * n);
+    GOMIX_CUDA(cudaMallocHost(&h_tape_pinned, std::max<uint64_t>(1, max_group * n) * sizeof(int32_t)));
+  }
+
   void draw_replay_tape(uint64_t group) {
+    ensure_tape();
     const uint64_t nv = P->nv;
     h_pop.resize(nv * Wp);
     GOMIX_CUDA(cudaMemcpyAsync(h_pop.data(), pop, nv * Wp * 4, cudaMemcpyDeviceToHost, stream));
@@ -758,6 +795,7 @@ struct gomix_gpu_engine {
   }
 
   void upload_tape(uint64_t group, const int32_t* donor_sp) {
+    ensure_tape();
     const uint64_t g0 = P->group_off[group], G = P->group_off[group + 1] - g0;
     for (uint64_t s = 0; s < n; ++s)
       for (uint64_t p = 0; p < G; ++p) {
@@ -864,7 +902,8 @@ struct gomix_gpu_engine {
       run_generation_sharded(stop, out);
       return;
     }
-    if (mode == GOMIX_MODE_PHILOX && no_criteria(stop) && !(flags & GOMIX_FLAG_TIME_KERNELS)) {
+    if (mode == GOMIX_MODE_PHILOX && !(flags & GOMIX_FLAG_TIME_KERNELS)) {
+      stage_criteria(stop, true);
       launch_generation_graph();
       read_ctl();
       fill_stats(out);
@@ -901,6 +940,7 @@ struct gomix_gpu_engine {
       rng.permutation(order, P->k);
       for (uint64_t gi : order) launch_group(gi, false);
     } else {
+      stage_criteria(nullptr, false);
       launch_generation_graph();
     }
     ++generation;
@@ -915,7 +955,7 @@ struct gomix_gpu_engine {
   // (NULL = evaluate on the device); the elitist is kept.
   void load_population(const uint8_t* genotypes, const double* fitness) {
     if (!initialized) throw GomixError(GOMIX_E_STATE, "load_population: population not initialised");
-    if (R > 1) invalid("load_population: single-GPU engines only");
+    if (R > 1 && !nccl) invalid("load_population: in-process shards are driven by their local group");
     const uint64_t nv = P->nv;
     // the elitist snapshot may still point into the old population: finish it
     launch_finalize_elitist(snap_args(), stream);
@@ -932,6 +972,7 @@ struct gomix_gpu_engine {
     }
     launch_hash_population(snap_args(), stream);  // hashes of the new members
     ++launches;
+    if (R > 1) exchange();  // every rank's pool rows, fitness and hashes (collective)
     GOMIX_CUDA(cudaStreamSynchronize(stream));
   }
 
@@ -1377,7 +1418,10 @@ int gomix_gpu_read_improvements(gomix_gpu_engine* e, double* fitness, uint64_t* 
     const uint64_t avail = std::min<uint64_t>(e->h_ctl->n_impr, e->impr_cap);
     const bool any = fitness || evaluator_calls;
     const uint64_t take = any ? std::min(avail, capacity) : 0;
-    if (take) {
+    if (take && take <= gomix_gpu_engine::kImprInline) {  // copied back with the control block
+      if (fitness) std::memcpy(fitness, e->h_impr, take * 8);
+      if (evaluator_calls) std::memcpy(evaluator_calls, e->h_impr_calls, take * 8);
+    } else if (take) {
       if (fitness)
         GOMIX_CUDA(cudaMemcpyAsync(fitness, e->impr, take * 8, cudaMemcpyDeviceToHost, e->stream));
       if (evaluator_calls)

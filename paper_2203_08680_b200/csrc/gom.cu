@@ -807,7 +807,8 @@ constexpr uint32_t kTagOrder = 0x4F524400u;  // "ORD"
 
 // Graph path: reset the per-call block and draw this generation's group
 // order (Fisher-Yates, engine_parallel.hpp:291) from the counter-based stream.
-__global__ void begin_generation_kernel(const BeginArgs b, const OrderArgs o) {
+__global__ void begin_generation_kernel(const BeginArgs* bp, const OrderArgs o) {
+  const BeginArgs b = *bp;  // criteria uploaded before each graph launch
   DevCtl* c = b.ctl;
   c->stop = 0;
   c->stop_reason = GOMIX_STOP_NONE;
@@ -1040,8 +1041,8 @@ void launch_begin(const BeginArgs& b, cudaStream_t s) {
   GOMIX_CUDA(cudaGetLastError());
 }
 
-void launch_order(const BeginArgs& b, const OrderArgs& o, cudaStream_t s) {
-  begin_generation_kernel<<<1, 1, 0, s>>>(b, o);
+void launch_order(const BeginArgs* d_b, const OrderArgs& o, cudaStream_t s) {
+  begin_generation_kernel<<<1, 1, 0, s>>>(d_b, o);
   GOMIX_CUDA(cudaGetLastError());
 }
 

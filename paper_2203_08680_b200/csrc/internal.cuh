@@ -278,7 +278,7 @@ int univ_sliced_max_blocks_per_sm(int planes, int wp);
 void launch_univ_sliced(const GomArgs& a, int planes, int wp, int grid, cudaStream_t s);
 int gom_max_blocks_per_sm(bool univariate, bool i32, int wpt, bool team, int block, size_t smem);
 void launch_begin(const BeginArgs& b, cudaStream_t s);
-void launch_order(const BeginArgs& b, const OrderArgs& o, cudaStream_t s);
+void launch_order(const BeginArgs* d_b, const OrderArgs& o, cudaStream_t s);
 void prepare_gom(bool univariate, bool i32, int wpt, bool team, size_t smem);
 void launch_init_epilogue(const EpiArgs& a, cudaStream_t s);
 void launch_global_epilogue(const EpiArgs& a, cudaStream_t s);

@@ -283,10 +283,10 @@ class GpuParallelEngine:
         ctl = self.ctx.control
         start = ctl.calls
         end = start + int(stats.evaluator_calls)
-        fit, calls_at = self.improvements(int(stats.improvements))
+        fit, calls_at = self.improvements(int(stats.improvements)) if stats.improvements else ((), ())
         if stats.stopped and stats.stop_reason == 1:
             ctl.request_stop("evaluation-budget")
-        for f, c in zip(fit.tolist(), calls_at.tolist()):
+        for f, c in zip(list(fit), list(calls_at)):
             ctl.calls = max(ctl.calls, int(c))
             self.ctx.report_improvement(float(f), generation, self.pop_id)
         ctl.calls = end

@@ -1,0 +1,113 @@
+#!/usr/bin/env python3
+"""Time to the best-known cut: the reference's CPU IMS vs the B200 IMS.
+
+SURVEY.md §8(d): best-known = the best cut the reference's own run_parallel
+(IMS, base 16, subgenerations 4, the same FOS, every host thread) finds within
+T_ref seconds; the CPU time to it is the timestamp of that improvement in the
+reference's trace (seconds since its RunControl was created, model prebuilt).
+The GPU then runs the same IMS scheme (Philox donors) with that cut as its
+target; its time is measured the same way (RunContext creation -> the
+improvement that reaches the target), and once more including the device
+problem build (CSR upload, GPU colouring).  Repeated over seeds: success rate
+and median times.
+
+    python tools/time_to_target.py --config c2 --t-ref 20 --seeds 3 [--out profiles/ttt_c2.json]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+REF = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
+
+
+def reference_ims(cfg, seed, t_ref, workers, base=16, sub=4):
+    w = cfg["weights"]
+    wspec = "unit" if w == "unit" else f"int:{w[1]}:{w[2]}"
+    cmd = [REF, "ims", "--torus", str(cfg["width"]), str(cfg["height"]), "--weights", wspec, "--inst-seed", "1",
+           "--fos", cfg["ref_fos"], "--seed", str(seed), "--ims", "--ims-base", str(base), "--ims-sub", str(sub),
+           "--workers", str(workers), "--max-seconds", str(t_ref)]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=t_ref * 4 + 600)
+    if res.returncode != 0:
+        raise RuntimeError(res.stderr)
+    r = json.loads(res.stdout)
+    trace = r["trace"]
+    best = r["best"]
+    t_best = next(t for t, _, f in trace if f == best)
+    return {"best": best, "seconds_to_best": t_best, "run_seconds": r["seconds"], "evaluations": r["evaluations"],
+            "populations": r["populations"], "improvements": len(trace)}
+
+
+def warm_device():
+    """Create the CUDA context before anything is timed (one-time process
+    cost, not part of a run)."""
+    import paper_2203_08680_b200 as G
+
+    t = G.generate_torus(4, 4, "unit", 1)
+    G.GpuProblem(t, G.univariate_fos(16))
+
+
+def gpu_ims(cfg, target, seed, budget_s, base=16, sub=4):
+    import paper_2203_08680_b200 as G
+
+    warm_device()
+    inst = G.generate_torus(cfg["width"], cfg["height"], cfg["weights"], 1)
+    fos = G.univariate_fos(inst.num_vertices) if cfg["fos"] == "uni" else G.neighbourhood_fos(inst)
+    t0 = time.perf_counter()
+    P = G.GpuProblem(inst, fos)
+    build_s = time.perf_counter() - t0
+    sink = G.RecordingSink()
+    r = G.run_gpu(P, G.TerminationConfig(target_fitness=target, max_seconds=budget_s), seed=seed, use_ims=True,
+                  ims=G.ImsConfig(base, sub), sink=sink, mode="philox")
+    hit = r.reason == "target-reached"
+    t_hit = next((x.seconds for x in sink.rows if x.fitness >= target), None) if hit else None
+    return {"reached": hit, "seconds_to_target": t_hit, "build_seconds": build_s,
+            "seconds_to_target_incl_build": (t_hit + build_s) if hit else None, "best": r.best_fitness,
+            "evaluations": r.evaluations, "populations": r.populations, "run_seconds": r.seconds}
+
+
+def main():
+    from bench import CONFIGS
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--t-ref", type=float, default=20.0)
+    ap.add_argument("--seeds", type=int, default=1)
+    ap.add_argument("--gpu-budget", type=float, default=None, help="GPU wall budget per seed (default t_ref)")
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    cfg = CONFIGS[a.config]
+    workers = os.cpu_count() or 1
+    rows = []
+    for seed in range(1, a.seeds + 1):
+        ref = reference_ims(cfg, seed, a.t_ref, workers)
+        gpu = gpu_ims(cfg, ref["best"], seed, a.gpu_budget or a.t_ref)
+        rows.append({"seed": seed, "reference": ref, "gpu": gpu})
+        print(json.dumps(rows[-1]), flush=True)
+    ok = [r for r in rows if r["gpu"]["reached"]]
+    summ = {"config": cfg["workload"], "t_ref_s": a.t_ref, "cpu_workers": workers, "seeds": a.seeds,
+            "ims": "base 16, subgenerations 4", "success_rate": len(ok) / len(rows),
+            "cpu_median_s_to_best_known": statistics.median(r["reference"]["seconds_to_best"] for r in rows),
+            "gpu_median_s_to_target": statistics.median(r["gpu"]["seconds_to_target"] for r in ok) if ok else None,
+            "gpu_median_s_to_target_incl_build":
+                statistics.median(r["gpu"]["seconds_to_target_incl_build"] for r in ok) if ok else None,
+            "rows": rows}
+    if ok:
+        summ["speedup_median"] = summ["cpu_median_s_to_best_known"] / summ["gpu_median_s_to_target"]
+        summ["speedup_median_incl_build"] = summ["cpu_median_s_to_best_known"] / summ["gpu_median_s_to_target_incl_build"]
+    print(json.dumps({k: v for k, v in summ.items() if k != "rows"}))
+    if a.out:
+        with open(a.out, "w") as fh:
+            json.dump(summ, fh, indent=1)
+
+
+if __name__ == "__main__":
+    main()
