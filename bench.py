@@ -358,13 +358,13 @@ def bench_ours(args):
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
             tr = json.load(fh).get(args.config)
-            if tr and tr.get("population") == n:
+            if tr and tr.get("population") == n and tr.get("kernel", "gom_group_kernel") == E.kernel_name():
                 traffic = tr["dram_bytes_per_launch"]
     except (OSError, ValueError):
         pass
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak if achieved else None, "traffic": traffic,
-                "kernel": "gom_group_kernel", "bytes_per_step": b_step,
+                "kernel": E.kernel_name(), "bytes_per_step": b_step,
                 "launches": int(len(kern_ms)), "avg_launch_us": 1e6 * kern_s / max(1, len(kern_ms)),
                 "kernel_share_of_step": (kern_s / kern_gens) / (dev_s / args.steps) if dev_s else None,
                 "peak_source": peak_src,

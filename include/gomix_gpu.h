@@ -240,6 +240,9 @@ GOMIX_API int gomix_gpu_kernel_times(gomix_gpu_engine* e, float* ms, uint64_t ca
  * launch by launch (events around every GOM kernel) instead of as one CUDA
  * graph. */
 GOMIX_API int gomix_gpu_set_timing(gomix_gpu_engine* e, int32_t enable);
+/* Name of the GOM kernel this engine's Philox generations launch
+ * ("gom_univ_sliced_kernel" or "gom_group_kernel"); static storage. */
+GOMIX_API const char* gomix_gpu_engine_kernel_name(const gomix_gpu_engine* e);
 /* Number of device kernels this engine has launched so far. */
 GOMIX_API int gomix_gpu_launch_count(gomix_gpu_engine* e, uint64_t* count);
 

@@ -96,6 +96,7 @@ _SIGNATURES = {
     "gomix_gpu_generation": ([_P, C.POINTER(C.c_int64)], C.c_int),
     "gomix_gpu_kernel_times": ([_P, _P, C.c_uint64, C.POINTER(C.c_uint64)], C.c_int),
     "gomix_gpu_launch_count": ([_P, C.POINTER(C.c_uint64)], C.c_int),
+    "gomix_gpu_engine_kernel_name": ([_P], C.c_char_p),
     "gomix_gpu_set_timing": ([_P, C.c_int32], C.c_int),
     "gomix_gpu_color": ([C.POINTER(Maxcut), C.POINTER(Fos), C.c_int32, _P, C.POINTER(C.c_uint64),
                          C.POINTER(C.c_uint64)], C.c_int),

@@ -1486,6 +1486,11 @@ int gomix_gpu_set_timing(gomix_gpu_engine* e, int32_t enable) {
   });
 }
 
+const char* gomix_gpu_engine_kernel_name(const gomix_gpu_engine* e) {
+  if (!e) return "";
+  return e->univ_planes ? "gom_univ_sliced_kernel" : "gom_group_kernel";
+}
+
 int gomix_gpu_launch_count(gomix_gpu_engine* e, uint64_t* count) {
   return guarded([&] {
     if (!e || !count) invalid("launch_count: NULL argument");

@@ -414,6 +414,10 @@ class GpuParallelEngine:
     def set_timing(self, enable: bool):
         check(lib().gomix_gpu_set_timing(self.h, int(bool(enable))))
 
+    def kernel_name(self) -> str:
+        """The GOM kernel this engine's Philox generations launch."""
+        return lib().gomix_gpu_engine_kernel_name(self.h).decode()
+
     def launch_count(self) -> int:
         c = C.c_uint64()
         check(lib().gomix_gpu_launch_count(self.h, C.byref(c)))
