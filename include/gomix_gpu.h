@@ -71,7 +71,11 @@ enum {
   GOMIX_FLAG_TIME_KERNELS = 1u << 2,
   /* Univariate FOS, integer weights, PHILOX: use the lane-per-solution kernel
    * instead of the bit-sliced lane-per-set kernel (same results; A/B tests). */
-  GOMIX_FLAG_LANE_PER_SOLUTION = 1u << 3
+  GOMIX_FLAG_LANE_PER_SOLUTION = 1u << 3,
+  /* General sets, integer weights, PHILOX, n <= 256: run one kernel launch
+   * per colour group instead of the persistent whole-generation kernel
+   * (same results; A/B tests). */
+  GOMIX_FLAG_PER_GROUP_KERNELS = 1u << 4
 };
 
 enum { GOMIX_STOP_NONE = 0, GOMIX_STOP_BUDGET = 1, GOMIX_STOP_CLOCK = 2, GOMIX_STOP_TARGET = 3,

@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -289,6 +290,12 @@ struct gomix_gpu_engine {
   int grid_cap = 1;
   int univ_planes = 0;     // > 0: Philox groups run the bit-sliced lane-per-set kernel
   int univ_grid_cap = 1;
+  bool gen_ok = false;     // Philox generations run as one persistent kernel (gom_gen.cu)
+  int gen_grid = 0;
+  long long* gen_dfit = nullptr;
+  unsigned long long* gen_dh = nullptr;
+  unsigned long long* gen_cnt = nullptr;
+  unsigned int* gen_bar = nullptr;
   int sms = 148;
   uint32_t mode = GOMIX_MODE_PHILOX, flags = 0;
   int32_t pop_id = 1;
@@ -401,7 +408,9 @@ struct gomix_gpu_engine {
       // Wp warps per set, for parallelism; otherwise a warp per set with every
       // word in registers.
       const uint64_t avg_group = (P->m + P->k - 1) / P->k;
-      if (Wp > 1 && avg_group * Wp <= (uint64_t)sms * 32) {
+      const char* knob = std::getenv("GOMIX_WARP_TEAMS");  // experiment knob: 1 = always one warp per set
+      const bool force_warp = knob && knob[0] == '1';
+      if (Wp > 1 && avg_group * Wp <= (uint64_t)sms * 32 && !force_warp) {
         wpt = 1;
         tw = Wp;
         block = 32 * tw;  // one team per CTA: the whole group fits in one wave
@@ -461,6 +470,23 @@ struct gomix_gpu_engine {
     }
     for (uint64_t c = 0; c < P->k; ++c)
       max_group = std::max(max_group, P->group_off[c + 1] - P->group_off[c]);
+    if (mode == GOMIX_MODE_PHILOX && P->i32 && !P->univariate && R == 1 && n <= kGenMaxN && P->k <= kGenMaxK &&
+        !(flags & GOMIX_FLAG_RECORD_BATCH) && !(flags & GOMIX_FLAG_PER_GROUP_KERNELS)) {
+      const int per = gen_kernel_max_blocks((int)wpt, tw > 1, (int)block, smem);
+      const uint64_t want = std::max<uint64_t>(1, (max_group + teams - 1) / teams);
+      if (per >= 1) {
+        gen_grid = (int)std::min<uint64_t>(want, (uint64_t)per * sms);
+        gen_ok = true;
+        gen_dfit = dev_alloc<long long>(allocs, 3 * n);
+        gen_dh = dev_alloc<unsigned long long>(allocs, 6 * n);
+        gen_cnt = dev_alloc<unsigned long long>(allocs, 6);
+        gen_bar = dev_alloc<unsigned int>(allocs, 2);
+        GOMIX_CUDA(cudaMemset(gen_dfit, 0, 3 * n * 8));
+        GOMIX_CUDA(cudaMemset(gen_dh, 0, 6 * n * 8));
+        GOMIX_CUDA(cudaMemset(gen_cnt, 0, 6 * 8));
+        GOMIX_CUDA(cudaMemset(gen_bar, 0, 8));
+      }
+    }
 
     const uint64_t nv = P->nv;
     pool = dev_alloc<uint32_t>(allocs, (uint64_t)R * nv * Wp);
@@ -552,6 +578,25 @@ struct gomix_gpu_engine {
     b.gen = (uint32_t)generation;
     launch_begin(b, stream);
     ++launches;
+  }
+
+  // A whole Philox generation as one persistent kernel (gom_gen.cu).
+  void launch_generation_persistent() {
+    GomArgs a = gom_args(0, max_group, false, -1);
+    a.epi = epi_args(0, 0, 0);
+    GenArgs ga{d_begin, (uint32_t)P->k, d_order, gen_dfit, gen_dh, gen_cnt, gen_bar};
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (flags & GOMIX_FLAG_TIME_KERNELS) {
+      e0 = take_event();
+      e1 = take_event();
+      GOMIX_CUDA(cudaEventRecord(e0, stream));
+    }
+    launch_generation_kernel(a, ga, (int)wpt, tw > 1, gen_grid, (int)block, smem, stream);
+    ++launches;
+    if (e1) {
+      GOMIX_CUDA(cudaEventRecord(e1, stream));
+      ev_pending.push_back({e0, e1});
+    }
   }
 
   // One CUDA graph per engine for a whole Philox generation: the order
@@ -665,10 +710,7 @@ struct gomix_gpu_engine {
   }
 
   // ---- one batched group step -----------------------------------------------
-  void launch_group(uint64_t group, bool with_tape, int32_t slot = -1, cudaStream_t st = nullptr) {
-    if (!st) st = stream;
-    const uint64_t g0 = slot >= 0 ? 0 : P->group_off[group];
-    const uint64_t G = slot >= 0 ? max_group : P->group_off[group + 1] - g0;
+  GomArgs gom_args(uint64_t g0, uint64_t G, bool with_tape, int32_t slot) {
     GomArgs a;
     a.row_ptr = P->row_ptr;
     a.col = P->col;
@@ -713,8 +755,20 @@ struct gomix_gpu_engine {
     a.generation = (uint32_t)generation;
     a.seed = seed;
     a.slot = slot;
+    {
+      const char* ex = std::getenv("GOMIX_EXP");
+      a.exp_flags = ex ? (uint32_t)std::atoi(ex) : 0u;
+    }
     a.order = d_order;
     a.groups = d_groups;
+    return a;
+  }
+
+  void launch_group(uint64_t group, bool with_tape, int32_t slot = -1, cudaStream_t st = nullptr) {
+    if (!st) st = stream;
+    const uint64_t g0 = slot >= 0 ? 0 : P->group_off[group];
+    const uint64_t G = slot >= 0 ? max_group : P->group_off[group + 1] - g0;
+    GomArgs a = gom_args(g0, G, with_tape, slot);
     const uint64_t want = (G + teams - 1) / teams;
     const int grid = (int)std::min<uint64_t>(want, (uint64_t)grid_cap);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -902,9 +956,12 @@ struct gomix_gpu_engine {
       run_generation_sharded(stop, out);
       return;
     }
-    if (mode == GOMIX_MODE_PHILOX && !(flags & GOMIX_FLAG_TIME_KERNELS)) {
+    if (mode == GOMIX_MODE_PHILOX && (gen_ok || !(flags & GOMIX_FLAG_TIME_KERNELS))) {
       stage_criteria(stop, true);
-      launch_generation_graph();
+      if (gen_ok)
+        launch_generation_persistent();
+      else
+        launch_generation_graph();
       read_ctl();
       fill_stats(out);
       if (!h_ctl->stop) ++generation;
@@ -934,7 +991,10 @@ struct gomix_gpu_engine {
     if (!initialized) throw GomixError(GOMIX_E_STATE, "run_generation: population not initialised");
     if (mode != GOMIX_MODE_PHILOX) invalid("run_generation_async: needs GOMIX_MODE_PHILOX");
     if (R > 1) invalid("run_generation_async: single-GPU engines only");
-    if (flags & GOMIX_FLAG_TIME_KERNELS) {
+    if (gen_ok) {
+      stage_criteria(nullptr, false);
+      launch_generation_persistent();
+    } else if (flags & GOMIX_FLAG_TIME_KERNELS) {
       begin_call(nullptr);
       std::vector<uint64_t> order;
       rng.permutation(order, P->k);
@@ -1488,7 +1548,7 @@ int gomix_gpu_set_timing(gomix_gpu_engine* e, int32_t enable) {
 
 const char* gomix_gpu_engine_kernel_name(const gomix_gpu_engine* e) {
   if (!e) return "";
-  return e->univ_planes ? "gom_univ_sliced_kernel" : "gom_group_kernel";
+  return e->univ_planes ? "gom_univ_sliced_kernel" : e->gen_ok ? "gom_generation_kernel" : "gom_group_kernel";
 }
 
 int gomix_gpu_launch_count(gomix_gpu_engine* e, uint64_t* count) {

@@ -18,6 +18,7 @@
 #include "internal.cuh"
 
 #include "gom_common.cuh"
+#include "gom_general.cuh"
 
 namespace gomix_b200 {
 
@@ -233,9 +234,6 @@ __device__ __forceinline__ void store_words(uint32_t* row, uint32_t wit, uint32_
   }
 }
 
-__device__ __forceinline__ double shfl_d(double x, int src) {
-  return __shfl_sync(0xFFFFFFFFu, x, src);
-}
 
 // ---------------------------------------------------------------------------
 // gom_group_kernel
@@ -315,6 +313,7 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
   unsigned long long calls = 0;
 
   for (uint32_t p = blockIdx.x * teams_per_cta + team; p < G; p += gridDim.x * teams_per_cta) {
+    if (a.exp_flags & 8) break;
     if constexpr (UNIV) {
       // ---- univariate set {v}: a donor differing on v holds !x_v, so the
       // pair is present iff some member holds the other value and the move
@@ -444,258 +443,9 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
         if (lane == 0) store_words<WPT, TEAM>(a.pop + (size_t)v * Wp, wit, tw, pw, nw);
       }
     } else {
-      // ---- general set F (|F| <= 64).  Shared memory per team holds the F
-      // rows at group start (the donor pool, engine_parallel.hpp:100-103),
-      // every solution's pattern on F (so a donor test is one load), the
-      // donor-inserted rows and the committed rows.
-      const uint4 gm = gmeta[p];
-      const uint32_t sid = gm.x;
-      const uint32_t f = gm.w >> 24;
-      const uint32_t* vars = a.set_vars + gm.y;
-      const uint32_t e0 = gm.z, e1 = gm.z + (gm.w & 0xFFFFFFu);
-      // pool words: RW = R*Wp per row (every rank's shard; R == 1: the population)
-      const uint32_t RW = a.R * Wp, own = a.rank * Wp;
-      uint64_t* patt = reinterpret_cast<uint64_t*>(stage);  // pattern of every member (padded index)
-      uint32_t* rowsF = stage + 64u * RW;                    // F rows at group start, stride RW
-      uint32_t* newD = rowsF + f * RW;                       // own donor-inserted rows, stride Wp
-      uint32_t* newF = newD + f * Wp;                        // own committed rows, stride Wp
-      for (uint32_t idx = tid_team; idx < f * RW; idx += team_threads) {
-        const uint32_t jv = idx / RW, wg = idx - jv * RW;
-        rowsF[idx] = a.pool[((size_t)(wg / Wp) * a.nv + vars[jv]) * Wp + (wg % Wp)];
-      }
-      // first footprint chunk: entry per lane and its outside row, fetched
-      // now so the loads overlap the staging above
-      FpEntry E0;
-      uint32_t xw0[WPT];
-      {
-        const uint32_t e = e0 + lane;
-        if (e < e1) {
-          E0 = a.fp[e];
-        } else {
-          E0.a = kInSet;
-          E0.b = kInSet;
-          E0.w = 0.0;
-        }
-        const uint32_t ext = !(E0.a & kInSet) ? E0.a : (!(E0.b & kInSet) ? E0.b : vars[0]);
-#pragma unroll
-        for (int j = 0; j < WPT; ++j) xw0[j] = a.pop[(size_t)ext * Wp + wit + tw * j];
-      }
-      // Zobrist keys of F, 8-byte aligned: offset from the (aligned) stage is
-      // 64*RW + f*RW + 2*f*Wp, so pad by the parity of f*RW
-      unsigned long long* zF = reinterpret_cast<unsigned long long*>(newF + f * Wp + ((f * RW) & 1u));
-      for (uint32_t jv = tid_team; jv < f; jv += team_threads) zobrist(vars[jv], zF[2 * jv], zF[2 * jv + 1]);
-      const uint64_t fm = f >= 64 ? ~0ull : ((1ull << f) - 1ull);
-      team_sync(tw, teams_per_cta, team);
-      for (uint32_t wg = wit; wg < RW; wg += tw) {
-        uint64_t m = 0;
-        for (uint32_t jv = 0; jv < f; ++jv) m |= (uint64_t)((rowsF[jv * RW + wg] >> lane) & 1u) << jv;
-        patt[wg * 32u + lane] = m;
-      }
-      team_sync(tw, teams_per_cta, team);
-      uint64_t pm[WPT];
-#pragma unroll
-      for (int j = 0; j < WPT; ++j) pm[j] = patt[(own + wit + tw * j) * 32u + lane];
-
-      // phase 1: donors
-      uint64_t dm[WPT];
-      bool present[WPT];
-      int32_t dsel[WPT];
-#pragma unroll
-      for (int j = 0; j < WPT; ++j) {
-        const uint32_t w = wit + tw * j;
-        const uint32_t s = w * 32u + lane;
-        const uint32_t sg = a.rank * n + s;  // global member index (Philox counter, donors)
-        const uint64_t m = pm[j];
-        int32_t d = -1;
-        uint64_t x = m;
-        if (s < n) {
-          if (replay) {
-            d = a.tape[(size_t)p * n + s];
-            if (d >= 0) x = patt[d];
-          } else {
-            // uniform over the members that differ on F — the distribution of
-            // the lazy Fisher-Yates scan of engine_serial.hpp:30-46: rejection
-            // sampling first, exact count-and-select when it keeps failing.
-            const uint2 key = make_uint2((uint32_t)a.seed, (uint32_t)(a.seed >> 32));
-            const uint32_t ng = a.n_global, pad = 32u * Wp;
-            for (uint32_t call = 0; call < 2 && d < 0; ++call) {
-              const uint4 r = philox4x32_10(make_uint4(sg, sid, generation, kTagGom | call), key);
-              const uint32_t c0 = bounded(lo64(r), ng);
-              const uint64_t x0 = patt[(c0 / n) * pad + c0 % n];
-              if (x0 != m) {
-                d = (int32_t)c0;
-                x = x0;
-              } else {
-                const uint32_t c1 = bounded(hi64(r), ng);
-                const uint64_t x1 = patt[(c1 / n) * pad + c1 % n];
-                if (x1 != m) {
-                  d = (int32_t)c1;
-                  x = x1;
-                }
-              }
-            }
-            if (d < 0) {
-              uint32_t total = 0;
-              for (uint32_t wg = 0; wg < RW; ++wg) total += __popc(differ_word(rowsF, f, RW, wg, m, n, Wp));
-              if (total > 0) {
-                const uint4 r = philox4x32_10(make_uint4(sg, sid, generation, kTagGom | 2u), key);
-                uint32_t kth = bounded(lo64(r), total);
-                for (uint32_t wg = 0; wg < RW; ++wg) {
-                  const uint32_t dw = differ_word(rowsF, f, RW, wg, m, n, Wp);
-                  const uint32_t c = __popc(dw);
-                  if (kth < c) {
-                    const uint32_t b = select_bit(dw, kth);
-                    d = (int32_t)((wg / Wp) * n + (wg % Wp) * 32u + b);
-                    x = patt[wg * 32u + b];
-                    break;
-                  }
-                  kth -= c;
-                }
-              }
-            }
-          }
-        }
-        dm[j] = x;
-        present[j] = d >= 0;
-        dsel[j] = d;
-        uint32_t mine = 0, mine2 = 0;  // lane jv keeps the donor-inserted word of F's jv-th row
-        for (uint32_t jv = 0; jv < f; ++jv) {
-          const uint32_t word = __ballot_sync(0xFFFFFFFFu, (uint32_t)(x >> jv) & 1u);
-          if (lane == (jv & 31u)) {
-            if (jv < 32) mine = word; else mine2 = word;
-          }
-        }
-        if (lane < f) newD[lane * Wp + w] = mine;
-        if (lane + 32u < f) newD[(lane + 32u) * Wp + w] = mine2;
-      }
-      team_sync(tw, teams_per_cta, team);
-
-      // phase 2: footprint sums, ascending edge id (engine_parallel.hpp:164-173)
-      int32_t di[WPT];
-      double sn[WPT], so[WPT];
-#pragma unroll
-      for (int j = 0; j < WPT; ++j) {
-        di[j] = 0;
-        sn[j] = 0.0;
-        so[j] = 0.0;
-      }
-      for (uint32_t base = e0; base < e1; base += 32) {
-        FpEntry E;
-        uint32_t xw[WPT];
-        if (base == e0) {
-          E = E0;
-#pragma unroll
-          for (int j = 0; j < WPT; ++j) xw[j] = xw0[j];
-        } else {
-          const uint32_t e = base + lane;
-          if (e < e1) {
-            E = a.fp[e];
-          } else {
-            E.a = kInSet;
-            E.b = kInSet;
-            E.w = 0.0;
-          }
-          const uint32_t ext = !(E.a & kInSet) ? E.a : (!(E.b & kInSet) ? E.b : vars[0]);
-#pragma unroll
-          for (int j = 0; j < WPT; ++j) xw[j] = a.pop[(size_t)ext * Wp + wit + tw * j];
-        }
-        const bool ina = E.a & kInSet, inb = E.b & kInSet;
-        const uint32_t ja = (E.a & ~kInSet) * Wp, jb = (E.b & ~kInSet) * Wp;            // newD rows
-        const uint32_t jaR = (E.a & ~kInSet) * RW + own, jbR = (E.b & ~kInSet) * RW + own;  // own old rows
-        if constexpr (I32) {
-          // lane t = entry t: old / new cut words for 32 solutions at once,
-          // transposed so lane s holds its solution's entry masks, then delta
-          // = weighted popcounts over the weight bit-planes (exact integers).
-          const int32_t wt = (int32_t)E.w;
-          const uint32_t aw = wt < 0 ? (uint32_t)(-wt) : (uint32_t)wt;
-#pragma unroll
-          for (int j = 0; j < WPT; ++j) {
-            const uint32_t w = wit + tw * j;
-            const uint32_t aO = ina ? rowsF[jaR + w] : xw[j], aN = ina ? newD[ja + w] : xw[j];
-            const uint32_t bO = inb ? rowsF[jbR + w] : xw[j], bN = inb ? newD[jb + w] : xw[j];
-            const uint32_t mo = transpose32((aO ^ bO) & (E.w != 0.0 ? 0xFFFFFFFFu : 0u), lane);
-            const uint32_t mn = transpose32((aN ^ bN) & (E.w != 0.0 ? 0xFFFFFFFFu : 0u), lane);
-            int32_t d = 0;
-            for (uint32_t k = 0; k < a.wbits; ++k) {
-              const uint32_t bp = __ballot_sync(0xFFFFFFFFu, wt > 0 && ((aw >> k) & 1u));
-              const uint32_t bn = __ballot_sync(0xFFFFFFFFu, wt < 0 && ((aw >> k) & 1u));
-              d += ((int32_t)(__popc(mn & bp) - __popc(mo & bp)) - (int32_t)(__popc(mn & bn) - __popc(mo & bn))) << k;
-            }
-            di[j] += d;
-          }
-        } else {
-          const int cnt = (int)(e1 - base < 32 ? e1 - base : 32);
-          for (int t = 0; t < cnt; ++t) {
-            const uint32_t ca = __shfl_sync(0xFFFFFFFFu, E.a, t);
-            const uint32_t cb = __shfl_sync(0xFFFFFFFFu, E.b, t);
-            const bool ina_t = ca & kInSet, inb_t = cb & kInSet;
-            const uint32_t ja_t = (ca & ~kInSet) * Wp, jb_t = (cb & ~kInSet) * Wp;
-            const uint32_t jaR_t = (ca & ~kInSet) * RW + own, jbR_t = (cb & ~kInSet) * RW + own;
-            const double wt = shfl_d(E.w, t);
-#pragma unroll
-            for (int j = 0; j < WPT; ++j) {
-              const uint32_t w = wit + tw * j;
-              const uint32_t xo = (ina_t && inb_t) ? 0u : __shfl_sync(0xFFFFFFFFu, xw[j], t);
-              const uint32_t aO = ina_t ? rowsF[jaR_t + w] : xo, aN = ina_t ? newD[ja_t + w] : xo;
-              const uint32_t bO = inb_t ? rowsF[jbR_t + w] : xo, bN = inb_t ? newD[jb_t + w] : xo;
-              sn[j] += (((aN ^ bN) >> lane) & 1u) ? wt : 0.0;
-              so[j] += (((aO ^ bO) >> lane) & 1u) ? wt : 0.0;
-            }
-          }
-        }
-      }
-      const uint32_t fpl = e1 - e0;
-
-      // phases 3 + 4
-#pragma unroll
-      for (int j = 0; j < WPT; ++j) {
-        const uint32_t w = wit + tw * j;
-        const uint32_t s = w * 32u + lane;
-        const bool valid = s < n;
-        const double delta = (e1 == e0) ? 0.0 : (I32 ? (double)di[j] : sn[j] - so[j]);
-        bool accept = false;
-        if (present[j]) {
-          const bool elit = is_elit[j];
-          if (exact) {
-            accept = delta > 0.0 || (delta == 0.0 && !elit);
-          } else {
-            const double pf = pfit[j];
-            const double cand = pf + delta;
-            accept = cmp_better(false, cand, pf) || (cmp_equal(false, cand, pf) && !elit);
-          }
-        }
-        const uint32_t acc_w = __ballot_sync(0xFFFFFFFFu, accept);
-        for (uint32_t jv = lane; jv < f; jv += 32)
-          newF[jv * Wp + w] = (rowsF[jv * RW + own + w] & ~acc_w) | (newD[jv * Wp + w] & acc_w);
-        if (accept) {
-          acc[j] += I32 ? (Acc)di[j] : (Acc)delta;
-          uint64_t changed = (dm[j] ^ pm[j]) & fm;
-          const bool cap = (int32_t)(a.rank * n + s) == esrc;
-          while (changed) {
-            const uint32_t jv = (uint32_t)(__ffsll((long long)changed) - 1);
-            changed &= changed - 1;
-            dh1[j] ^= zF[2 * jv];
-            dh2[j] ^= zF[2 * jv + 1];
-            if (cap) capture_row(a.elit, a.ever, ever_cur, vars[jv], (uint32_t)(pm[j] >> jv) & 1u);
-          }
-        }
-        steps += present[j] ? 1u : 0u;
-        calls += present[j] ? fpl : 0u;
-        if (record && valid) {
-          const size_t at = (size_t)p * n + s;
-          a.rec_donor[at] = dsel[j];
-          a.rec_delta[at] = delta;
-          a.rec_present[at] = present[j];
-          a.rec_accept[at] = accept;
-        }
-      }
-      team_sync(tw, teams_per_cta, team);
-      for (uint32_t idx = tid_team; idx < f * Wp; idx += team_threads) {
-        const uint32_t jv = idx / Wp, w = idx - jv * Wp;
-        const uint32_t nw = newF[idx];
-        if (nw != rowsF[jv * RW + own + w]) a.pop[(size_t)vars[jv] * Wp + w] = nw;
-      }
-      team_sync(tw, teams_per_cta, team);
+      gom_general_set<WPT, I32, TEAM>(a, p, gmeta, generation, stage, lane, tw, wit, tid_team, team_threads,
+                                      teams_per_cta, team, exact, replay, record, is_elit, pfit, esrc, ever_cur,
+                                      acc, dh1, dh2, steps, calls);
     }
   }
 
@@ -758,9 +508,9 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
       if (s < n) {
         if (float_parts)
           a.part[(size_t)blockIdx.x * n + s] = (double)acc[j];
-        else if (a.dfit && acc[j] != 0)
+        else if (a.dfit && acc[j] != 0 && !(a.exp_flags & 2))
           atomicAdd(&a.dfit[s], (double)acc[j]);
-        if (dh1[j] | dh2[j]) {
+        if ((dh1[j] | dh2[j]) && !(a.exp_flags & 2)) {
           atomicXor(&a.dh1[s], dh1[j]);
           atomicXor(&a.dh2[s], dh2[j]);
         }
@@ -769,18 +519,18 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    if (s_steps | s_calls) {
+    if ((s_steps | s_calls) && !(a.exp_flags & 4)) {
       atomicAdd(&a.ctl->grp_steps, s_steps);
       atomicAdd(&a.ctl->grp_calls, s_calls);
     }
     // last-CTA-done ticket: everything above is visible to the last CTA
-    __threadfence();
+    if (!(a.exp_flags & 1)) __threadfence();
     s_last = atomicAdd(&a.ctl->done, 1u) == gridDim.x - 1;
   }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  epilogue_body(epi);
+  if (!(a.exp_flags & 16)) epilogue_body(epi);
   if (threadIdx.x == 0) a.ctl->done = 0;
 }
 

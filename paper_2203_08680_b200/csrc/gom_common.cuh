@@ -119,6 +119,10 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, uint32_t lane) {
   return x;
 }
 
+__device__ __forceinline__ double shfl_d(double x, int src) {
+  return __shfl_sync(0xFFFFFFFFu, x, src);
+}
+
 // Position of the k-th (0-based) set bit of x; k < popc(x).
 __device__ __forceinline__ uint32_t select_bit(uint32_t x, uint32_t k) {
   uint32_t pos = 0;

@@ -1,0 +1,341 @@
+// gom_gen.cu — a whole Philox generation (engine_parallel.hpp:283-316) in ONE
+// persistent kernel, for general linkage sets on integer weights with small
+// populations (n <= 256, the C2 shape: 10^4 sets of 5 variables, n = 64).
+//
+// Why: at that size a colour group is ~1250 (set, 64-solution) teams that
+// all fit in one wave, and the per-group kernel boundary plus its serial
+// last-CTA epilogue cost more than the GOM work itself (measured on C2: an
+// empty-bodied group kernel still takes 9.5 us of the 16 us per group).
+// Here the CTAs stay resident for all k groups:
+//
+//   for each group g (order = device Fisher-Yates on Philox, :291):
+//     work   : phases 1-4 for the group's sets (gom_general_set, shared with
+//              the per-group kernel), per-CTA sums -> global atomics into
+//              triple-buffered accumulators D[g % 3] (fitness / hash deltas,
+//              steps, calls)
+//     barrier: grid-wide (all CTAs co-resident: cooperative launch)
+//     epilogue, REDUNDANTLY in every CTA from D[g % 3]: fitness + hashes of
+//              all n members (kept in shared memory), evaluator-call
+//              accounting + budget stop (runtime.hpp:75-80), the chained
+//              elitist scan + target stop (:305-310) -> every CTA takes the
+//              same decisions without a second barrier.  CTA 0 alone writes
+//              the results back (fitness, hashes, counters, improvement log)
+//              and zeroes the accumulator of group g-1 (last read before the
+//              barrier of g, next written after the barrier of g+1).
+//
+// Results are bit-identical to the per-group path with the same device group
+// order (tests/test_gen_kernel.py).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "gom_general.cuh"
+
+namespace gomix_b200 {
+
+namespace {
+
+constexpr uint32_t kTagOrderGen = 0x4F524400u;  // same stream as begin_generation_kernel ("ORD")
+
+// Sense-by-generation grid barrier; bar[0] = arrivals, bar[1] = generation.
+// The gpu-scope fences order this CTA's writes before the arrival and, on
+// the way out, invalidate the SM's L1 so later loads see other CTAs' writes.
+__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int* vgen = bar + 1;
+    const unsigned int g = *vgen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == nblocks - 1) {
+      *(volatile unsigned int*)bar = 0u;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*vgen == g) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+}  // namespace
+
+template <int WPT, bool TEAM>
+__global__ void __launch_bounds__(512, 1) gom_generation_kernel(const GomArgs a, const GenArgs ga) {
+  extern __shared__ __align__(16) uint32_t smem[];
+  __shared__ double s_fit[kGenMaxN];
+  __shared__ unsigned long long s_h1[kGenMaxN], s_h2[kGenMaxN];
+  __shared__ uint32_t s_order[kGenMaxK];
+  __shared__ double s_chunkmax[kGenMaxN / 32];
+  __shared__ unsigned long long s_steps, s_calls;
+  // run state, identical in every CTA
+  __shared__ double s_elit_fit;
+  __shared__ int32_t s_elit_src, s_stop, s_stop_reason;
+  __shared__ unsigned long long s_eh1, s_eh2, s_calls_total, s_run_steps, s_run_calls, s_groups, s_nimpr;
+  __shared__ uint32_t s_ver;
+
+  using Acc = long long;
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const uint32_t tw = TEAM ? a.team_warps : 1u;
+  const uint32_t teams_per_cta = TEAM ? 1u : (blockDim.x >> 5);
+  const uint32_t team = TEAM ? 0u : warp, wit = TEAM ? warp : 0u;
+  const uint32_t tid_team = wit * 32u + lane, team_threads = tw * 32u;
+  const uint32_t Wp = a.Wp, n = a.n;
+  uint32_t* stage = smem + (size_t)team * a.stage_words;
+  const BeginArgs b = *ga.begin;
+  DevCtl* c = a.ctl;
+  const uint32_t gen = *(volatile unsigned int*)&c->gen_counter;
+  const uint32_t buf0 = *(volatile unsigned int*)&c->gen_buf;
+  const bool lead = blockIdx.x == 0;
+
+  if (threadIdx.x == 0) {
+    s_elit_fit = c->elit_fit;
+    s_elit_src = c->elit_src;
+    s_eh1 = c->eh1;
+    s_eh2 = c->eh2;
+    s_ver = c->elit_ver;
+    s_stop = 0;
+    s_stop_reason = GOMIX_STOP_NONE;
+    s_calls_total = b.calls_before;
+    s_run_steps = s_run_calls = s_groups = s_nimpr = 0;
+    // this generation's group order (Fisher-Yates, engine_parallel.hpp:291)
+    const uint2 key = make_uint2((uint32_t)a.seed, (uint32_t)(a.seed >> 32));
+    for (uint32_t i = 0; i < ga.k; ++i) s_order[i] = i;
+    for (uint32_t i = ga.k; i > 1; --i) {
+      const uint4 r = philox4x32_10(make_uint4(i, gen, 0u, kTagOrderGen), key);
+      const uint32_t j = bounded(lo64(r), i);
+      const uint32_t t = s_order[i - 1];
+      s_order[i - 1] = s_order[j];
+      s_order[j] = t;
+    }
+  }
+  for (uint32_t s = threadIdx.x; s < n; s += blockDim.x) {
+    s_fit[s] = a.fit[s];
+    s_h1[s] = a.h1[s];
+    s_h2[s] = a.h2[s];
+  }
+  __syncthreads();
+
+  uint32_t slot = 0;
+  for (; slot < ga.k; ++slot) {
+    const uint32_t gi = s_order[slot];
+    const GroupDesc d = a.groups[gi];
+    const uint4* gmeta = a.gmeta + d.g0;
+    const uint32_t bi = (buf0 + slot) % 3u;
+    long long* D = ga.dfit + (size_t)bi * n;
+    unsigned long long* DH1 = ga.dh + (size_t)bi * 2 * n;
+    unsigned long long* DH2 = DH1 + n;
+    unsigned long long* CNT = ga.cnt + 2 * bi;
+
+    // ---- work: phases 1-4 over this CTA's sets ------------------------------
+    const unsigned long long eh1 = s_eh1, eh2 = s_eh2;
+    const int32_t esrc = s_elit_src;
+    const uint32_t ever_cur = s_ver;
+    bool is_elit[WPT];
+    double pfit[WPT];
+    Acc acc[WPT];
+    unsigned long long dh1[WPT], dh2[WPT];
+#pragma unroll
+    for (int j = 0; j < WPT; ++j) {
+      const uint32_t s = (wit + tw * (uint32_t)j) * 32u + lane;
+      is_elit[j] = s < n && s_h1[s] == eh1 && s_h2[s] == eh2;
+      pfit[j] = 0.0;
+      acc[j] = 0;
+      dh1[j] = 0;
+      dh2[j] = 0;
+    }
+    uint32_t steps = 0;
+    unsigned long long calls = 0;
+    for (uint32_t p = blockIdx.x * teams_per_cta + team; p < d.G; p += gridDim.x * teams_per_cta)
+      gom_general_set<WPT, true, TEAM>(a, p, gmeta, gen, stage, lane, tw, wit, tid_team, team_threads,
+                                       teams_per_cta, team, true, false, false, is_elit, pfit, esrc, ever_cur,
+                                       acc, dh1, dh2, steps, calls);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      s_steps = 0;
+      s_calls = 0;
+    }
+    __syncthreads();
+    {
+      const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, steps);
+      unsigned long long wc = calls;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) wc += __shfl_xor_sync(0xFFFFFFFFu, wc, o);
+      if (lane == 0 && (ws | wc)) {
+        atomicAdd(&s_steps, (unsigned long long)ws);
+        atomicAdd(&s_calls, wc);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < WPT; ++j) {
+      const uint32_t s = (wit + tw * (uint32_t)j) * 32u + lane;
+      if (s < n) {
+        if (acc[j]) atomicAdd(reinterpret_cast<unsigned long long*>(D + s), (unsigned long long)acc[j]);
+        if (dh1[j] | dh2[j]) {
+          atomicXor(DH1 + s, dh1[j]);
+          atomicXor(DH2 + s, dh2[j]);
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && (s_steps | s_calls)) {
+      atomicAdd(CNT, s_steps);
+      atomicAdd(CNT + 1, s_calls);
+    }
+    grid_barrier(ga.bar, gridDim.x);
+
+    // ---- epilogue (every CTA): fitness / hash commit ------------------------
+    for (uint32_t s = threadIdx.x; s < n; s += blockDim.x) {
+      const double f = s_fit[s] + (double)__ldcg(D + s);
+      const unsigned long long x1 = s_h1[s] ^ __ldcg(DH1 + s), x2 = s_h2[s] ^ __ldcg(DH2 + s);
+      s_fit[s] = f;
+      s_h1[s] = x1;
+      s_h2[s] = x2;
+      if (lead) {
+        a.epi.fit[s] = f;
+        a.epi.h1[s] = x1;
+        a.epi.h2[s] = x2;
+        // accumulator of the previous group: read by every CTA before this
+        // group's barrier, written again only after the next one
+        const uint32_t zb = (bi + 2u) % 3u;
+        ga.dfit[(size_t)zb * n + s] = 0;
+        ga.dh[(size_t)zb * 2 * n + s] = 0;
+        ga.dh[(size_t)zb * 2 * n + n + s] = 0;
+      }
+    }
+    if (lead && threadIdx.x == 0) {
+      const uint32_t zb = (bi + 2u) % 3u;
+      ga.cnt[2 * zb] = 0;
+      ga.cnt[2 * zb + 1] = 0;
+    }
+    if (threadIdx.x == 0) {
+      const unsigned long long st = __ldcg(CNT), ca = __ldcg(CNT + 1);
+      s_calls_total += ca;
+      s_run_steps += st;
+      s_run_calls += ca;
+      s_groups += 1;
+      if (lead) {
+        a.epi.gsteps[gi] += st;
+        a.epi.gcalls[gi] += ca;
+      }
+      if (b.has_budget && (double)s_calls_total / b.q >= b.max_evals && !s_stop) {
+        s_stop = 1;
+        s_stop_reason = GOMIX_STOP_BUDGET;
+      }
+    }
+    __syncthreads();
+    // chained elitist scan over all members in index order (:305-310)
+    for (uint32_t ch = warp; ch * 32u < n; ch += blockDim.x >> 5) {
+      const uint32_t s = ch * 32u + lane;
+      double f = s < n ? s_fit[s] : -INFINITY;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) f = fmax(f, __shfl_xor_sync(0xFFFFFFFFu, f, o));
+      if (lane == 0) s_chunkmax[ch] = f;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double cur = s_elit_fit;
+      int32_t best = -1;
+      bool hit = false;
+      unsigned long long ni = s_nimpr;
+      const unsigned long long calls_now = s_calls_total;
+      for (uint32_t base = 0; base < n; base += 32u) {
+        if (!(s_chunkmax[base >> 5] > cur)) continue;  // better() implies >
+        const uint32_t s = base + lane;
+        const double f = s < n ? s_fit[s] : -INFINITY;
+        uint32_t m = __ballot_sync(0xFFFFFFFFu, s < n && f > cur);
+        while (m) {
+          const uint32_t l = __ffs(m) - 1;
+          cur = __shfl_sync(0xFFFFFFFFu, f, l);
+          best = (int32_t)(base + l);
+          if (lead && lane == 0 && ni < a.epi.impr_cap) {
+            a.epi.impr[ni] = cur;
+            a.epi.impr_calls[ni] = calls_now;
+          }
+          ++ni;
+          hit |= b.has_target && cur >= b.target;
+          m = __ballot_sync(0xFFFFFFFFu, s < n && lane > l && f > cur);
+        }
+      }
+      if (lane == 0) {
+        s_nimpr = ni;
+        if (hit && !s_stop) {
+          s_stop = 1;
+          s_stop_reason = GOMIX_STOP_TARGET;
+        }
+        if (best >= 0) {  // new elitist: member `best` (snapshot taken copy-on-write)
+          s_elit_fit = cur;
+          s_elit_src = best;
+          s_eh1 = s_h1[best];
+          s_eh2 = s_h2[best];
+          s_ver += 1;
+        }
+      }
+    }
+    __syncthreads();
+    if (s_stop) break;
+  }
+
+  if (lead && threadIdx.x == 0) {
+    c->elit_fit = s_elit_fit;
+    c->elit_src = s_elit_src;
+    c->eh1 = s_eh1;
+    c->eh2 = s_eh2;
+    c->elit_ver = s_ver;
+    c->stop = s_stop;
+    c->stop_reason = s_stop_reason;
+    c->has_budget = b.has_budget;
+    c->has_target = b.has_target;
+    c->max_evals = b.max_evals;
+    c->target = b.target;
+    c->calls_total = s_calls_total;
+    c->run_steps = s_run_steps;
+    c->run_calls = s_run_calls;
+    c->groups_run = s_groups;
+    c->n_impr = s_nimpr;
+    c->grp_steps = c->grp_calls = 0;
+    c->done = 0;
+    c->cur_gen = gen;
+    c->gen_counter = gen + 1;
+    c->gen_buf = buf0 + (slot < ga.k ? slot + 1 : ga.k);
+    for (uint32_t i = 0; i < ga.k; ++i) ga.order[i] = s_order[i];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+namespace {
+void* gen_kernel(int wpt, bool team) {
+  if (team) {
+    switch (wpt) {
+      case 1: return (void*)gom_generation_kernel<1, true>;
+    }
+  } else {
+    switch (wpt) {
+      case 1: return (void*)gom_generation_kernel<1, false>;
+      case 2: return (void*)gom_generation_kernel<2, false>;
+      case 4: return (void*)gom_generation_kernel<4, false>;
+      case 8: return (void*)gom_generation_kernel<8, false>;
+    }
+  }
+  return nullptr;
+}
+}  // namespace
+
+int gen_kernel_max_blocks(int wpt, bool team, int block, size_t smem) {
+  void* fn = gen_kernel(wpt, team);
+  if (!fn) return 0;
+  GOMIX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int blocks = 0;
+  GOMIX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, block, smem));
+  return blocks;
+}
+
+void launch_generation_kernel(const GomArgs& a, const GenArgs& ga, int wpt, bool team, int grid, int block,
+                              size_t smem, cudaStream_t s) {
+  void* fn = gen_kernel(wpt, team);
+  void* args[] = {(void*)&a, (void*)&ga};
+  GOMIX_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(block), args, smem, s));
+}
+
+}  // namespace gomix_b200

@@ -59,6 +59,7 @@ struct DevCtl {
   // device-owned elitist identity (never touched by the per-call reset)
   unsigned long long eh1, eh2;  // 128-bit Zobrist hash of the elitist genotype
   unsigned int elit_ver;        // snapshot version: row v is captured iff ever[v] == elit_ver
+  unsigned int gen_buf;         // persistent generation kernel: running accumulator index
 };
 
 // One colour group as the device sees it (graph path: kernels look their
@@ -177,6 +178,7 @@ struct GomArgs {
   uint64_t seed;
   EpiArgs epi;         // run by the last CTA
   int32_t slot;                 // >= 0: group = order[slot] (graph path)
+  uint32_t exp_flags;           // timing experiments only (GOMIX_EXP env): 1 no fence, 2 no fitness/hash atomics, 4 no counter atomics
   const uint32_t* order;
   const GroupDesc* groups;
 };
@@ -194,6 +196,20 @@ struct OrderArgs {
   uint32_t* order;
   uint32_t k;
   uint64_t seed;
+};
+
+// Persistent generation kernel (gom_gen.cu)
+constexpr uint32_t kGenMaxN = 256;  // members kept in shared memory by every CTA
+constexpr uint32_t kGenMaxK = 256;  // colour groups
+struct BeginArgs;
+struct GenArgs {
+  const BeginArgs* begin;
+  uint32_t k;
+  uint32_t* order;             // this generation's group order (written back for inspection)
+  long long* dfit;             // [3][n] fitness deltas
+  unsigned long long* dh;      // [3][2][n] Zobrist deltas
+  unsigned long long* cnt;     // [3][2] steps, calls
+  unsigned int* bar;           // grid barrier {arrivals, generation}
 };
 
 // Per-call control values, passed as kernel parameters (captured at launch,
@@ -270,6 +286,10 @@ class ReplayStream {
 // kernel launchers (gom.cu)
 void launch_gom(const GomArgs& a, bool univariate, bool i32, int wpt, bool team, int grid, int block,
                 size_t smem, cudaStream_t s);
+// persistent generation kernel (gom_gen.cu)
+int gen_kernel_max_blocks(int wpt, bool team, int block, size_t smem);
+void launch_generation_kernel(const GomArgs& a, const GenArgs& ga, int wpt, bool team, int grid, int block,
+                              size_t smem, cudaStream_t s);
 // bit-sliced univariate kernel (gom_univ.cu)
 int univ_sliced_planes(uint64_t max_abs_row_sum);  // 0: not representable
 int univ_sliced_block();

@@ -233,7 +233,8 @@ class GpuParallelEngine:
                  ctx: Optional[RunContext] = None, population_id: int = 1, mode: str = "replay",
                  record_batch: bool = False, ordered_float: bool = False, time_kernels: bool = False,
                  genotypes: Optional[np.ndarray] = None, stream=None, rank: int = 0, world_size: int = 1,
-                 nccl_unique_id: Optional[bytes] = None, lane_per_solution: bool = False):
+                 nccl_unique_id: Optional[bytes] = None, lane_per_solution: bool = False,
+                 per_group_kernels: bool = False):
         """world_size > 1: this process's shard of a population of
         `population_size` members over world_size GPUs (Philox mode); every
         rank passes the same nccl_unique_id (see nccl_unique_id()) and calls
@@ -249,7 +250,8 @@ class GpuParallelEngine:
                                                           problem.info.num_edges)
         flags = (_capi.FLAG_RECORD_BATCH if record_batch else 0) | (_capi.FLAG_ORDERED_FLOAT if ordered_float else 0) \
             | (_capi.FLAG_TIME_KERNELS if time_kernels else 0) \
-            | (_capi.FLAG_LANE_PER_SOLUTION if lane_per_solution else 0)
+            | (_capi.FLAG_LANE_PER_SOLUTION if lane_per_solution else 0) \
+            | (_capi.FLAG_PER_GROUP_KERNELS if per_group_kernels else 0)
         self._nid = None if nccl_unique_id is None else C.create_string_buffer(bytes(nccl_unique_id), 128)
         cfg = _capi.EngineConfig(self.n_global, seed, _capi.MODE_REPLAY if mode == "replay" else _capi.MODE_PHILOX,
                                  flags, population_id, self.rank, self.world_size,
