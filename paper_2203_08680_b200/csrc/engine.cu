@@ -12,6 +12,8 @@
 #include <nccl.h>  // types only: NCCL is resolved at run time with dlopen
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -72,6 +74,14 @@ namespace {
 // order -> ascending neighbour = ascending edge id (the reference's order).
 std::unique_ptr<Problem> create_problem(const gomix_maxcut* inst, const gomix_fos* fos,
                                         const int32_t* colour, int32_t device) {
+  const bool trace = std::getenv("GOMIX_TRACE_BUILD") != nullptr;
+  auto t_start = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!trace) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[host ] %-12s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(now - t_start).count());
+    t_start = now;
+  };
   if (!inst || !fos) invalid("problem: instance and fos are required");
   const uint64_t nv = inst->num_vertices, q = inst->num_edges, m = fos->num_sets;
   if (nv == 0) invalid("maxcut: instance needs at least one vertex");
@@ -124,6 +134,7 @@ std::unique_ptr<Problem> create_problem(const gomix_maxcut* inst, const gomix_fo
       if (colour[i] < 0) invalid("colouring: negative colour");
   }
 
+  mark("validate");
   if (device >= 0) GOMIX_CUDA(cudaSetDevice(device));
   GOMIX_CUDA(cudaGetDevice(&P->device));
 
@@ -198,7 +209,9 @@ std::unique_ptr<Problem> create_problem(const gomix_maxcut* inst, const gomix_fo
   up(P->set_off, so.data(), (m + 1) * 8);
   up(P->set_vars, P->h_set_vars.data(), entries * 4);
   up(d_eid, eid.data(), 2 * q * 4);
+  mark("csr+upload");
   build_problem_device_impl(*P, colour, d_eid);
+  mark("device");
   if (P->univariate) {
     for (uint64_t i = 0; i < m; ++i) {
       const uint32_t v = P->h_set_vars[i];

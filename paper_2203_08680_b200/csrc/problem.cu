@@ -6,15 +6,18 @@
 // (make_group_plan, engine_parallel.hpp:37-59).
 //
 // Colouring: Welsh-Powell is greedy colouring in the order (degree desc,
-// index asc).  Jones-Plassmann with exactly that order as the priority is the
-// same function computed in parallel: a set is coloured once every
-// higher-priority neighbour is, with the smallest colour they do not use —
-// which is what the sequential greedy gives it.  So the groups, and with them
-// replay parity, are identical to the reference's.
+// index asc).  Colouring every set as soon as all its higher-priority
+// neighbours are coloured, with the smallest colour they do not use, is the
+// same function computed in parallel (Jones-Plassmann with that priority);
+// here it runs as a dataflow kernel (wp_dataflow_kernel).  So the groups, and
+// with them replay parity, are identical to the reference's.
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -164,6 +167,77 @@ __global__ void jp_round_kernel(const int64_t* off, const uint32_t* adj, const u
   if (mine) atomicAdd(coloured, mine);
 }
 
+// Welsh-Powell as a dataflow: the warp holding the vertex of rank r colours
+// it as soon as every lower-ranked neighbour is coloured, with the smallest
+// colour none of them uses — exactly the sequential greedy (scheduling.hpp:
+// 85-114), but a chain link costs one shared-memory (or L2) hand-off instead
+// of a kernel launch per Jones-Plassmann round.  Warps take ranks gw, gw+W,
+// ... in increasing order, and the lowest uncoloured rank never waits, so a
+// co-resident grid cannot deadlock.  SMEM: one CTA, colours as uint16 in
+// shared memory (m <= kWpSmemMax); otherwise colours in global memory.
+constexpr uint64_t kWpSmemMax = 100000;
+constexpr int kJpBatches = 256;  // x 16 rounds before switching to the dataflow kernel
+constexpr uint32_t kWpUncoloured = 0xFFFFu;
+
+template <bool SMEM>
+__global__ void wp_dataflow_kernel(const int64_t* off, const uint32_t* adj, const uint32_t* rank,
+                                   const uint64_t* sorted_key, uint64_t m, int32_t* colour) {
+  extern __shared__ uint16_t scol[];
+  if constexpr (SMEM) {
+    for (uint64_t i = threadIdx.x; i < m; i += blockDim.x) scol[i] = (uint16_t)kWpUncoloured;
+    __syncthreads();
+  }
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  auto load_colour = [&](uint32_t j) -> uint32_t {
+    if constexpr (SMEM)
+      return *(volatile uint16_t*)&scol[j];
+    else
+      return (uint32_t)*(volatile int32_t*)&colour[j];
+  };
+  for (uint64_t r = gw; r < m; r += nw) {
+    const uint32_t v = (uint32_t)(sorted_key[r] & 0xFFFFFFFFull);
+    if constexpr (!SMEM) {
+      if (*(volatile int32_t*)&colour[v] >= 0) continue;  // coloured by the Jones-Plassmann rounds
+    }
+    const int64_t b = off[v], e = off[v + 1];
+    // the mex of the lower-ranked neighbours' colours, 32 candidates at a time
+    uint32_t c = 0xFFFFFFFFu;
+    for (uint32_t base = 0; c == 0xFFFFFFFFu; base += 32) {
+      uint32_t used = 0;
+      for (int64_t t0 = b; t0 < e; t0 += 32) {
+        const int64_t t = t0 + lane;
+        uint32_t bit = 0;
+        if (t < e) {
+          const uint32_t j = adj[t];
+          if (rank[j] < r) {
+            uint32_t cj;
+            const uint32_t unc = SMEM ? kWpUncoloured : 0xFFFFFFFFu;
+            while ((cj = load_colour(j)) == unc) {
+              if constexpr (!SMEM) __nanosleep(64);  // back off: keep L2 free for the writers
+            }
+            if (cj >= base && cj < base + 32) bit = 1u << (cj - base);
+          }
+        }
+        used |= __reduce_or_sync(0xFFFFFFFFu, bit);
+      }
+      if (~used) c = base + (uint32_t)__ffs(~used) - 1;
+    }
+    if (lane == 0) {
+      if constexpr (SMEM)
+        *(volatile uint16_t*)&scol[v] = (uint16_t)c;
+      else
+        *(volatile int32_t*)&colour[v] = (int32_t)c;
+    }
+    __syncwarp();
+  }
+  if constexpr (SMEM) {
+    __syncthreads();
+    for (uint64_t i = threadIdx.x; i < m; i += blockDim.x) colour[i] = (int32_t)scol[i];
+  }
+}
+
 __global__ void check_colouring_kernel(const int64_t* off, const uint32_t* adj,
                                        const int32_t* colour, uint64_t m, int32_t k,
                                        int* bad) {
@@ -298,8 +372,22 @@ void seg_sort_unique(Scratch& S, uint32_t* cand, const int64_t* cand_off, uint64
 // Device part of problem construction.  Expects P's CSR, edge list and FOS
 // already uploaded (row_ptr, col, eu, ev, ew, set_off, set_vars) and eid in
 // `eid` (CSR entry -> edge id).
+// GOMIX_TRACE_BUILD=1: per-phase wall times of the device build on stderr
+struct PhaseClock {
+  bool on = std::getenv("GOMIX_TRACE_BUILD") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    cudaDeviceSynchronize();
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[build] %-12s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
 void build_problem_device_impl(Problem& P, const int32_t* given_colour, const int32_t* eid) {
   Scratch S;
+  PhaseClock clk;
   const uint64_t m = P.m, nv = P.nv, entries = P.h_set_off[m];
   // 1. inverse FOS: variable -> sets (ascending set id)
   uint32_t* owner = S.get<uint32_t>(entries);
@@ -322,6 +410,7 @@ void build_problem_device_impl(Problem& P, const int32_t* given_colour, const in
   int64_t* vs_off = S.get<int64_t>(nv + 1);
   exclusive_scan(S, vs_cnt, vs_off, nv + 1);
 
+  clk.mark("fos-inverse");
   // 2. LMIG: sorted unique adjacency per set
   int64_t* bound = S.get<int64_t>(m + 1);
   GOMIX_CUDA(cudaMemset(bound, 0, (m + 1) * sizeof(int64_t)));
@@ -345,6 +434,7 @@ void build_problem_device_impl(Problem& P, const int32_t* given_colour, const in
   for (uint64_t i = 0; i < m; ++i)
     maxdeg = std::max<uint64_t>(maxdeg, (uint64_t)(h_lmig_off[i + 1] - h_lmig_off[i]));
 
+  clk.mark("lmig");
   // 3. colouring
   int32_t* colour = S.get<int32_t>(m);
   if (given_colour) {
@@ -362,15 +452,38 @@ void build_problem_device_impl(Problem& P, const int32_t* given_colour, const in
     rank_kernel<<<blocks_for(m), 256>>>(key_sorted, m, rank);
     GOMIX_CUDA(cudaGetLastError());
     GOMIX_CUDA(cudaMemset(colour, 0xFF, m * sizeof(int32_t)));
-    unsigned long long* coloured = S.get<unsigned long long>(1);
-    GOMIX_CUDA(cudaMemset(coloured, 0, sizeof(unsigned long long)));
     unsigned long long done = 0;
-    for (uint64_t round = 0; done < m; ++round) {
-      for (int r = 0; r < 16; ++r)
-        jp_round_kernel<<<blocks_for(m), 256>>>(lmig_off, lmig_adj, rank, colour, m, coloured);
+    if (m <= kWpSmemMax && maxdeg < kWpUncoloured) {
+      // one CTA, colours in shared memory: a chain link is a shared-memory hand-off
+      const size_t sm = m * sizeof(uint16_t);
+      GOMIX_CUDA(cudaFuncSetAttribute(wp_dataflow_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      wp_dataflow_kernel<true><<<1, 1024, sm>>>(lmig_off, lmig_adj, rank, key_sorted, m, colour);
       GOMIX_CUDA(cudaGetLastError());
-      GOMIX_CUDA(cudaMemcpy(&done, coloured, sizeof(done), cudaMemcpyDeviceToHost));
-      if (round > 4 * m + 16) throw GomixError(GOMIX_E_STATE, "colouring did not converge");
+    } else {
+      // Jones-Plassmann rounds while the graph is wide (grids, univariate:
+      // ~2W rounds), then the dataflow kernel for whatever long chains are
+      // left (e.g. neighbourhood sets in index order: one chain of m links)
+      unsigned long long* coloured = S.get<unsigned long long>(1);
+      GOMIX_CUDA(cudaMemset(coloured, 0, sizeof(unsigned long long)));
+      for (int batch = 0; batch < kJpBatches && done < m; ++batch) {
+        for (int r = 0; r < 16; ++r)
+          jp_round_kernel<<<blocks_for(m), 256>>>(lmig_off, lmig_adj, rank, colour, m, coloured);
+        GOMIX_CUDA(cudaGetLastError());
+        GOMIX_CUDA(cudaMemcpy(&done, coloured, sizeof(done), cudaMemcpyDeviceToHost));
+      }
+    }
+    if ((m > kWpSmemMax || maxdeg >= kWpUncoloured) && done < m) {
+      // co-resident grid (cooperative launch), colours in global memory; a
+      // warp whose vertex is already coloured moves on
+      int dev = 0, sms = 0, per = 0;
+      GOMIX_CUDA(cudaGetDevice(&dev));
+      GOMIX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      GOMIX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, wp_dataflow_kernel<false>, 256, 0));
+      const int grid = std::max(1, std::min(per * sms, blocks_for(m * 32)));
+      void* args[] = {(void*)&lmig_off, (void*)&lmig_adj, (void*)&rank, (void*)&key_sorted, (void*)&m,
+                      (void*)&colour};
+      GOMIX_CUDA(cudaLaunchCooperativeKernel((void*)wp_dataflow_kernel<false>, dim3(grid), dim3(256), args, 0,
+                                             nullptr));
     }
   }
   int* mx = S.get<int>(2);
@@ -387,6 +500,7 @@ void build_problem_device_impl(Problem& P, const int32_t* given_colour, const in
   GOMIX_CUDA(cudaMemcpy(&bad, mx + 1, sizeof(int), cudaMemcpyDeviceToHost));
   if (bad) invalid("colouring: adjacent linkage sets share a colour (groups must be independent)");
 
+  clk.mark("colouring");
   // 4. groups: sets by colour, ascending set id inside a colour (scheduling.hpp:418-422)
   {
     uint32_t* ids = S.get<uint32_t>(m);
@@ -417,6 +531,7 @@ void build_problem_device_impl(Problem& P, const int32_t* given_colour, const in
     }
   }
 
+  clk.mark("groups");
   // 5. footprint plans (multi-variable sets only; singletons read the CSR row)
   P.footprint.assign(m, 0);
   if (!P.univariate) {
@@ -457,6 +572,7 @@ void build_problem_device_impl(Problem& P, const int32_t* given_colour, const in
     GOMIX_CUDA(cudaMemcpy(P.gmeta, gm.data(), m * sizeof(uint4), cudaMemcpyHostToDevice));
   }
   GOMIX_CUDA(cudaDeviceSynchronize());
+  clk.mark("plans");
 }
 
 }  // namespace gomix_b200

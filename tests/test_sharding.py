@@ -62,8 +62,9 @@ def test_nccl_bootstrap_over_gloo_world2():
 
 def _single(P, n, seed, crit=None):
     ctx = G.RunContext(G.TerminationConfig(**(crit or {})), P.comparator(), P.info.num_edges)
-    E = G.GpuParallelEngine(P, n, seed, ctx=ctx, mode="philox")
-    E.set_timing(True)  # launch-by-launch path with the host group order, like the sharded path
+    # launch-by-launch path with the host group order, like the sharded path
+    E = G.GpuParallelEngine(P, n, seed, ctx=ctx, mode="philox", per_group_kernels=True, lane_per_solution=True)
+    E.set_timing(True)
     return E, ctx
 
 
