@@ -70,8 +70,8 @@ constexpr int kNbChunk = 4;    // neighbour (col, w) pairs fetched per round
 
 template <int B, int WP>
 __global__ void __launch_bounds__(kUnivWarps * 32, 2) gom_univ_sliced_kernel(const GomArgs a) {
-  __shared__ unsigned long long s_key[kUnivWarps][32][2];
-  __shared__ unsigned long long s_tbl[kUnivWarps][8][16][2];
+  __shared__ __align__(16) unsigned long long s_key[kUnivWarps][32][2];
+  __shared__ __align__(16) unsigned long long s_tbl[kUnivWarps][8][16][2];
   __shared__ long long s_dfit[WP * 32];
   __shared__ unsigned long long s_dh1[WP * 32], s_dh2[WP * 32];
   __shared__ uint32_t s_elit[WP];
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 2) gom_univ_sliced_kernel(con
     // ---- accept: T < h, or T == h with A even and the parent not the elitist
     const uint32_t h = (A + 1u) >> 1;
     const uint32_t aeven = (A & 1u) ? 0u : 0xFFFFFFFFu;
-    uint32_t acc[WP];
+    uint32_t acc[WP], ltw[WP];
     bool any = false;
 #pragma unroll
     for (int j = 0; j < WP; ++j) {
@@ -212,6 +212,7 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 2) gom_univ_sliced_kernel(con
         eq &= ~(T[k][j] ^ hk);
       }
       acc[j] = present ? ((lt | (eq & aeven & ~elitw[j])) & validw[j]) : 0u;
+      ltw[j] = lt;
       any |= acc[j] != 0u;
     }
     if (present) {
@@ -248,38 +249,48 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 2) gom_univ_sliced_kernel(con
       s_key[warp][lane][0] = z1;
       s_key[warp][lane][1] = z2;
       __syncwarp();
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const uint32_t e = lane + 32u * i;
-        const uint32_t c = e >> 4, m = e & 15u;
-        unsigned long long t1 = 0, t2 = 0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const unsigned long long k1 = s_key[warp][4 * c + q][0], k2 = s_key[warp][4 * c + q][1];
-          t1 ^= ((m >> q) & 1u) ? k1 : 0ull;
-          t2 ^= ((m >> q) & 1u) ? k2 : 0ull;
-        }
-        s_tbl[warp][c][m][0] = t1;
-        s_tbl[warp][c][m][1] = t2;
+      {
+        // lane = (chunk c, low bits sub): entries sub, sub+4, sub+8, sub+12 of
+        // chunk c share the XOR of keys 4c, 4c+1 selected by sub
+        const uint32_t c = lane >> 2, sub = lane & 3u;
+        const ulonglong2 k0 = *reinterpret_cast<const ulonglong2*>(s_key[warp][4 * c + 0]);
+        const ulonglong2 k1 = *reinterpret_cast<const ulonglong2*>(s_key[warp][4 * c + 1]);
+        const ulonglong2 k2 = *reinterpret_cast<const ulonglong2*>(s_key[warp][4 * c + 2]);
+        const ulonglong2 k3 = *reinterpret_cast<const ulonglong2*>(s_key[warp][4 * c + 3]);
+        const unsigned long long l1 = ((sub & 1u) ? k0.x : 0ull) ^ ((sub & 2u) ? k1.x : 0ull);
+        const unsigned long long l2 = ((sub & 1u) ? k0.y : 0ull) ^ ((sub & 2u) ? k1.y : 0ull);
+        ulonglong2* t = reinterpret_cast<ulonglong2*>(s_tbl[warp][c]);
+        t[sub] = make_ulonglong2(l1, l2);
+        t[sub + 4] = make_ulonglong2(l1 ^ k2.x, l2 ^ k2.y);
+        t[sub + 8] = make_ulonglong2(l1 ^ k3.x, l2 ^ k3.y);
+        t[sub + 12] = make_ulonglong2(l1 ^ k2.x ^ k3.x, l2 ^ k2.y ^ k3.y);
       }
       __syncwarp();
     }
 #pragma unroll
     for (int j = 0; j < WP; ++j) {
       const uint32_t accT = transpose32(acc[j], lane);  // lane b: sets l accepted by solution 32j+b
+      // fitness: only strictly improving pairs (T < h) change it; neutral
+      // accepts (delta 0) do not.  Late in a run improving moves are rare,
+      // so the plane transposes are skipped for most words.
       long long d = 0;
+      const uint32_t imp = acc[j] & ltw[j];
+      if (__any_sync(0xFFFFFFFFu, imp != 0u)) {
+        const uint32_t impT = transpose32(imp, lane);
 #pragma unroll
-      for (int k = 0; k < B; ++k) d += (long long)__popc(accT & Ab[k]) << k;
-      // accepted pairs have T <= A/2 < 2^(B-1): the top plane is zero
+        for (int k = 0; k < B; ++k) d += (long long)__popc(impT & Ab[k]) << k;
+        // improving pairs have T < A/2 < 2^(B-1): the top plane is zero
 #pragma unroll
-      for (int k = 0; k < B - 1; ++k) d -= (long long)__popc(transpose32(T[k][j] & acc[j], lane)) << (k + 1);
+        for (int k = 0; k < B - 1; ++k) d -= (long long)__popc(transpose32(T[k][j] & imp, lane)) << (k + 1);
+      }
       dfit[j] += d;
       unsigned long long x1 = 0, x2 = 0;
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         const uint32_t m = (accT >> (4 * c)) & 15u;
-        x1 ^= s_tbl[warp][c][m][0];
-        x2 ^= s_tbl[warp][c][m][1];
+        const ulonglong2 t = *reinterpret_cast<const ulonglong2*>(s_tbl[warp][c][m]);
+        x1 ^= t.x;
+        x2 ^= t.y;
       }
       dh1[j] ^= x1;
       dh2[j] ^= x2;
