@@ -69,7 +69,7 @@ constexpr int kNbChunk = 4;    // neighbour (col, w) pairs fetched per round
 }  // namespace
 
 template <int B, int WP>
-__global__ void __launch_bounds__(kUnivWarps * 32, 2) gom_univ_sliced_kernel(const GomArgs a) {
+__global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_sliced_kernel(const GomArgs a) {
   __shared__ __align__(16) unsigned long long s_key[kUnivWarps][32][2];
   __shared__ __align__(16) unsigned long long s_tbl[kUnivWarps][8][16][2];
   __shared__ long long s_dfit[WP * 32];
@@ -120,14 +120,8 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 2) gom_univ_sliced_kernel(con
     validw[j] = valid_mask((uint32_t)j, n);
   }
 
-  long long dfit[WP];
-  unsigned long long dh1[WP], dh2[WP];
-#pragma unroll
-  for (int j = 0; j < WP; ++j) {
-    dfit[j] = 0;
-    dh1[j] = 0;
-    dh2[j] = 0;
-  }
+  // per-solution fitness / hash deltas accumulate in shared memory (atomics
+  // per batch) rather than registers: 6*WP fewer registers, 3 CTAs per SM
   unsigned long long steps = 0, calls = 0;
 
   const uint32_t batches = (G + 31u) / 32u;
@@ -283,7 +277,8 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 2) gom_univ_sliced_kernel(con
 #pragma unroll
         for (int k = 0; k < B - 1; ++k) d -= (long long)__popc(transpose32(T[k][j] & imp, lane)) << (k + 1);
       }
-      dfit[j] += d;
+      const uint32_t sj = (uint32_t)j * 32u + lane;
+      if (d) atomicAdd(reinterpret_cast<unsigned long long*>(&s_dfit[sj]), (unsigned long long)d);
       unsigned long long x1 = 0, x2 = 0;
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
@@ -292,22 +287,15 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 2) gom_univ_sliced_kernel(con
         x1 ^= t.x;
         x2 ^= t.y;
       }
-      dh1[j] ^= x1;
-      dh2[j] ^= x2;
+      if (x1 | x2) {
+        atomicXor(&s_dh1[sj], x1);
+        atomicXor(&s_dh2[sj], x2);
+      }
     }
     __syncwarp();
   }
 
   // ---- per-CTA reductions, then the group epilogue in the last CTA -------
-#pragma unroll
-  for (int j = 0; j < WP; ++j) {
-    const uint32_t s = (uint32_t)j * 32u + lane;
-    if (dfit[j]) atomicAdd(reinterpret_cast<unsigned long long*>(&s_dfit[s]), (unsigned long long)dfit[j]);
-    if (dh1[j] | dh2[j]) {
-      atomicXor(&s_dh1[s], dh1[j]);
-      atomicXor(&s_dh2[s], dh2[j]);
-    }
-  }
   {
     unsigned long long ws = steps, wc = calls;
 #pragma unroll
