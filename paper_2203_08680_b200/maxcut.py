@@ -38,11 +38,14 @@ class MaxCutInstance:
             total += float(x)
         return total
 
-    def cut_values(self, genotypes: np.ndarray) -> np.ndarray:
-        """Vectorised cut values (exact for integer weights)."""
+    def cut_values(self, genotypes: np.ndarray, chunk: int = 256) -> np.ndarray:
+        """Vectorised cut values (exact for integer weights), chunk rows at a time."""
         g = np.asarray(genotypes)
-        cut = g[:, self.edge_u] != g[:, self.edge_v]
-        return cut.astype(np.float64) @ self.edge_w
+        out = np.empty(g.shape[0], np.float64)
+        for a in range(0, g.shape[0], chunk):
+            cut = g[a:a + chunk, self.edge_u] != g[a:a + chunk, self.edge_v]
+            out[a:a + chunk] = cut.astype(np.float64) @ self.edge_w
+        return out
 
     def adjacency(self):
         """VIG adjacency (graybox.hpp:305-323) as a list of sorted arrays."""
