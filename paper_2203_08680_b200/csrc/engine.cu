@@ -476,7 +476,7 @@ struct gomix_gpu_engine {
     if (per_sm < 1) invalid("engine: GOM kernel does not fit on an SM with this configuration");
     grid_cap = per_sm * sms;
     if (P->univariate && P->i32 && mode == GOMIX_MODE_PHILOX && !(flags & GOMIX_FLAG_RECORD_BATCH) &&
-        !(flags & GOMIX_FLAG_LANE_PER_SOLUTION) && Wp <= 4) {
+        !(flags & GOMIX_FLAG_LANE_PER_SOLUTION)) {
       univ_planes = univ_sliced_planes(P->max_abs_row);
       if (univ_planes) univ_grid_cap = univ_sliced_max_blocks_per_sm(univ_planes, (int)Wp) * sms;
       if (univ_grid_cap < 1) univ_planes = 0;

@@ -68,19 +68,25 @@ constexpr int kNbChunk = 4;    // neighbour (col, w) pairs fetched per round
 
 }  // namespace
 
-template <int B, int WP>
+template <int B, int WC, bool MULTI>
 __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_sliced_kernel(const GomArgs a) {
+  // WC words of a row per pass ("chunk"); MULTI: rows of Wp = a.Wp > WC words
+  // take Wp / WC passes, otherwise Wp == WC and the row is loaded once
+  extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ __align__(16) unsigned long long s_key[kUnivWarps][32][2];
   __shared__ __align__(16) unsigned long long s_tbl[kUnivWarps][8][16][2];
-  __shared__ long long s_dfit[WP * 32];
-  __shared__ unsigned long long s_dh1[WP * 32], s_dh2[WP * 32];
-  __shared__ uint32_t s_elit[WP];
   __shared__ unsigned long long s_steps, s_calls;
   __shared__ int s_last;
   if (*(volatile int32_t*)&a.ctl->stop) return;
 
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  const uint32_t n = a.n;
+  const uint32_t n = a.n, Wp = MULTI ? a.Wp : (uint32_t)WC, chunks = MULTI ? Wp / WC : 1u;
+  // per-solution fitness / hash deltas (shared-memory atomics per batch) and
+  // the group-start "parent == elitist" word masks
+  long long* s_dfit = reinterpret_cast<long long*>(dyn);
+  unsigned long long* s_dh1 = reinterpret_cast<unsigned long long*>(s_dfit + Wp * 32u);
+  unsigned long long* s_dh2 = s_dh1 + Wp * 32u;
+  uint32_t* s_elit = reinterpret_cast<uint32_t*>(s_dh2 + Wp * 32u);
   uint32_t G = a.G;
   const uint32_t* gvars = a.gvars;
   EpiArgs epi = a.epi;
@@ -97,13 +103,13 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_sliced_kernel(con
   const int32_t esrc_g = a.ctl->elit_src;
   const uint32_t ever_cur = a.ctl->elit_ver;
   const int32_t esrc = (esrc_g >= 0 && (uint32_t)esrc_g / n == a.rank) ? (int32_t)((uint32_t)esrc_g % n) : -1;
-  for (uint32_t j = warp; j < (uint32_t)WP; j += kUnivWarps) {
+  for (uint32_t j = warp; j < Wp; j += kUnivWarps) {
     const uint32_t s = j * 32u + lane;
     const bool e = s < n && a.h1[s] == eh1 && a.h2[s] == eh2;
     const uint32_t m = __ballot_sync(0xFFFFFFFFu, e);
     if (lane == 0) s_elit[j] = m;
   }
-  for (uint32_t i = threadIdx.x; i < WP * 32u; i += blockDim.x) {
+  for (uint32_t i = threadIdx.x; i < Wp * 32u; i += blockDim.x) {
     s_dfit[i] = 0;
     s_dh1[i] = 0;
     s_dh2[i] = 0;
@@ -113,15 +119,6 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_sliced_kernel(con
     s_calls = 0;
   }
   __syncthreads();
-  uint32_t elitw[WP], validw[WP];
-#pragma unroll
-  for (int j = 0; j < WP; ++j) {
-    elitw[j] = s_elit[j];
-    validw[j] = valid_mask((uint32_t)j, n);
-  }
-
-  // per-solution fitness / hash deltas accumulate in shared memory (atomics
-  // per batch) rather than registers: 6*WP fewer registers, 3 CTAs per SM
   unsigned long long steps = 0, calls = 0;
 
   const uint32_t batches = (G + 31u) / 32u;
@@ -129,167 +126,183 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_sliced_kernel(con
     const uint32_t p = bt * 32u + lane;
     const bool live = p < G;
     const uint32_t v = live ? gvars[p] : 0u;
-    uint32_t x[WP];
-#pragma unroll
-    for (int j = 0; j < WP; ++j) x[j] = 0;
+    const uint32_t* row = a.pop + (size_t)v * Wp;
     int32_t rs = 0, re = 0;
     if (live) {
-      load_row<WP>(a.pop + (size_t)v * WP, x);
       rs = a.row_ptr[v];
       re = a.row_ptr[v + 1];
     }
-    // ---- T = sum_e |w_e| b_e (bit-sliced over the row's solutions) --------
-    uint32_t T[B][WP];
+    uint32_t x0[WC];
 #pragma unroll
-    for (int k = 0; k < B; ++k)
+    for (int j = 0; j < WC; ++j) x0[j] = 0;
+    if (!MULTI && live) load_row<WC>(row, x0);
+    // ---- presence: some member (over every rank's shard) holds the other value
+    uint32_t ones = 0;
+    if (live) {
+      if (!MULTI && a.R == 1) {
 #pragma unroll
-      for (int j = 0; j < WP; ++j) T[k][j] = 0;
-    uint32_t A = 0;
-    for (int32_t base = rs; base < re; base += kNbChunk) {
-      uint32_t u[kNbChunk];
-      int32_t w[kNbChunk];
+        for (int j = 0; j < WC; ++j) ones += __popc(x0[j]);
+      } else {
+        for (uint32_t r = 0; r < a.R; ++r) {
+          const uint32_t* pr = a.R > 1 ? a.pool + ((size_t)r * a.nv + v) * Wp : row;
+          for (uint32_t c = 0; c < chunks; ++c) {
+            uint32_t y[WC];
+            load_row<WC>(pr + c * WC, y);
 #pragma unroll
-      for (int t = 0; t < kNbChunk; ++t) {
-        const bool has = base + t < re;
-        u[t] = has ? (uint32_t)__ldg(a.col + base + t) : v;
-        w[t] = has ? __ldg(a.wi + base + t) : 0;
-      }
-      uint32_t nb[kNbChunk][WP];
-#pragma unroll
-      for (int t = 0; t < kNbChunk; ++t) load_row<WP>(a.pop + (size_t)u[t] * WP, nb[t]);
-#pragma unroll
-      for (int t = 0; t < kNbChunk; ++t) {
-        const uint32_t m = (uint32_t)(w[t] < 0 ? -w[t] : w[t]);
-        const uint32_t neg = w[t] < 0 ? 0xFFFFFFFFu : 0u;
-        A += m;
-#pragma unroll
-        for (int j = 0; j < WP; ++j) {
-          const uint32_t b = (x[j] ^ nb[t][j]) ^ neg;
-          uint32_t c = 0;
-#pragma unroll
-          for (int k = 0; k < B; ++k) {
-            const uint32_t xb = ((m >> k) & 1u) ? b : 0u;
-            const uint32_t tk = T[k][j];
-            T[k][j] = tk ^ xb ^ c;
-            c = (tk & xb) | (tk & c) | (xb & c);
+            for (int j = 0; j < WC; ++j) ones += __popc(y[j]);
           }
         }
       }
     }
-    // ---- presence: some member (over every rank's shard) holds the other value
-    uint32_t ones = 0;
-    if (live) {
-      if (a.R > 1) {
-        for (uint32_t r = 0; r < a.R; ++r) {
-          const uint32_t* row = a.pool + ((size_t)r * a.nv + v) * WP;
-#pragma unroll
-          for (int j = 0; j < WP; ++j) ones += __popc(__ldg(row + j));
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < WP; ++j) ones += __popc(x[j]);
-      }
-    }
     const bool present = live && ones > 0u && ones < a.n_global;
-    // ---- accept: T < h, or T == h with A even and the parent not the elitist
-    const uint32_t h = (A + 1u) >> 1;
-    const uint32_t aeven = (A & 1u) ? 0u : 0xFFFFFFFFu;
-    uint32_t acc[WP], ltw[WP];
-    bool any = false;
-#pragma unroll
-    for (int j = 0; j < WP; ++j) {
-      uint32_t lt = 0, eq = 0xFFFFFFFFu;
-#pragma unroll
-      for (int k = B - 1; k >= 0; --k) {
-        const uint32_t hk = ((h >> k) & 1u) ? 0xFFFFFFFFu : 0u;
-        lt |= eq & ~T[k][j] & hk;
-        eq &= ~(T[k][j] ^ hk);
-      }
-      acc[j] = present ? ((lt | (eq & aeven & ~elitw[j])) & validw[j]) : 0u;
-      ltw[j] = lt;
-      any |= acc[j] != 0u;
-    }
     if (present) {
       steps += n;
       calls += (unsigned long long)n * (uint32_t)(re - rs);
     }
-    // ---- commit: accepted solutions flip v (apply_acceptance, :221-247)
-    if (any) {
-      uint32_t nx[WP];
-#pragma unroll
-      for (int j = 0; j < WP; ++j) nx[j] = x[j] ^ acc[j];
-      store_row<WP>(a.pop + (size_t)v * WP, nx);
-      if (esrc >= 0) {
-        const uint32_t ew = (uint32_t)esrc >> 5, eb = (uint32_t)esrc & 31u;
-        uint32_t aw = 0, xw = 0;
-#pragma unroll
-        for (int j = 0; j < WP; ++j)
-          if ((uint32_t)j == ew) {
-            aw = acc[j];
-            xw = x[j];
-          }
-        if ((aw >> eb) & 1u) capture_row(a.elit, a.ever, ever_cur, v, (xw >> eb) & 1u);
-      }
-    }
-    // ---- per-solution reductions over the warp's 32 sets ------------------
-    if (!__any_sync(0xFFFFFFFFu, any)) continue;
+    uint32_t A = 0, h = 0, aeven = 0;
+    bool table = false;
     uint32_t Ab[B];
+    for (uint32_t c = 0; c < chunks; ++c) {
+      uint32_t x[WC];
 #pragma unroll
-    for (int k = 0; k < B; ++k) Ab[k] = __ballot_sync(0xFFFFFFFFu, (A >> k) & 1u);
-    // Zobrist key XOR table: s_tbl[c][m] = XOR of key(v_{4c+i}) over bits i of m
-    {
-      unsigned long long z1 = 0, z2 = 0;
-      if (live && any) zobrist(v, z1, z2);
-      s_key[warp][lane][0] = z1;
-      s_key[warp][lane][1] = z2;
-      __syncwarp();
-      {
-        // lane = (chunk c, low bits sub): entries sub, sub+4, sub+8, sub+12 of
-        // chunk c share the XOR of keys 4c, 4c+1 selected by sub
-        const uint32_t c = lane >> 2, sub = lane & 3u;
-        const ulonglong2 k0 = *reinterpret_cast<const ulonglong2*>(s_key[warp][4 * c + 0]);
-        const ulonglong2 k1 = *reinterpret_cast<const ulonglong2*>(s_key[warp][4 * c + 1]);
-        const ulonglong2 k2 = *reinterpret_cast<const ulonglong2*>(s_key[warp][4 * c + 2]);
-        const ulonglong2 k3 = *reinterpret_cast<const ulonglong2*>(s_key[warp][4 * c + 3]);
-        const unsigned long long l1 = ((sub & 1u) ? k0.x : 0ull) ^ ((sub & 2u) ? k1.x : 0ull);
-        const unsigned long long l2 = ((sub & 1u) ? k0.y : 0ull) ^ ((sub & 2u) ? k1.y : 0ull);
-        ulonglong2* t = reinterpret_cast<ulonglong2*>(s_tbl[warp][c]);
-        t[sub] = make_ulonglong2(l1, l2);
-        t[sub + 4] = make_ulonglong2(l1 ^ k2.x, l2 ^ k2.y);
-        t[sub + 8] = make_ulonglong2(l1 ^ k3.x, l2 ^ k3.y);
-        t[sub + 12] = make_ulonglong2(l1 ^ k2.x ^ k3.x, l2 ^ k2.y ^ k3.y);
+      for (int j = 0; j < WC; ++j) x[j] = x0[j];
+      if (MULTI && live) load_row<WC>(row + c * WC, x);
+      // ---- T = sum_e |w_e| b_e (bit-sliced over the chunk's solutions) ------
+      uint32_t T[B][WC];
+#pragma unroll
+      for (int k = 0; k < B; ++k)
+#pragma unroll
+        for (int j = 0; j < WC; ++j) T[k][j] = 0;
+      for (int32_t base = rs; base < re; base += kNbChunk) {
+        uint32_t u[kNbChunk];
+        int32_t w[kNbChunk];
+#pragma unroll
+        for (int t = 0; t < kNbChunk; ++t) {
+          const bool has = base + t < re;
+          u[t] = has ? (uint32_t)__ldg(a.col + base + t) : v;
+          w[t] = has ? __ldg(a.wi + base + t) : 0;
+        }
+        uint32_t nb[kNbChunk][WC];
+#pragma unroll
+        for (int t = 0; t < kNbChunk; ++t) load_row<WC>(a.pop + (size_t)u[t] * Wp + c * WC, nb[t]);
+#pragma unroll
+        for (int t = 0; t < kNbChunk; ++t) {
+          const uint32_t m = (uint32_t)(w[t] < 0 ? -w[t] : w[t]);
+          const uint32_t neg = w[t] < 0 ? 0xFFFFFFFFu : 0u;
+          if (c == 0) A += m;
+#pragma unroll
+          for (int j = 0; j < WC; ++j) {
+            const uint32_t b = (x[j] ^ nb[t][j]) ^ neg;
+            uint32_t cy = 0;
+#pragma unroll
+            for (int k = 0; k < B; ++k) {
+              const uint32_t xb = ((m >> k) & 1u) ? b : 0u;
+              const uint32_t tk = T[k][j];
+              T[k][j] = tk ^ xb ^ cy;
+              cy = (tk & xb) | (tk & cy) | (xb & cy);
+            }
+          }
+        }
       }
-      __syncwarp();
-    }
-#pragma unroll
-    for (int j = 0; j < WP; ++j) {
-      const uint32_t accT = transpose32(acc[j], lane);  // lane b: sets l accepted by solution 32j+b
-      // fitness: only strictly improving pairs (T < h) change it; neutral
-      // accepts (delta 0) do not.  Late in a run improving moves are rare,
-      // so the plane transposes are skipped for most words.
-      long long d = 0;
-      const uint32_t imp = acc[j] & ltw[j];
-      if (__any_sync(0xFFFFFFFFu, imp != 0u)) {
-        const uint32_t impT = transpose32(imp, lane);
-#pragma unroll
-        for (int k = 0; k < B; ++k) d += (long long)__popc(impT & Ab[k]) << k;
-        // improving pairs have T < A/2 < 2^(B-1): the top plane is zero
-#pragma unroll
-        for (int k = 0; k < B - 1; ++k) d -= (long long)__popc(transpose32(T[k][j] & imp, lane)) << (k + 1);
+      if (c == 0) {
+        h = (A + 1u) >> 1;
+        aeven = (A & 1u) ? 0u : 0xFFFFFFFFu;
       }
-      const uint32_t sj = (uint32_t)j * 32u + lane;
-      if (d) atomicAdd(reinterpret_cast<unsigned long long*>(&s_dfit[sj]), (unsigned long long)d);
-      unsigned long long x1 = 0, x2 = 0;
+      // ---- accept: T < h, or T == h with A even and the parent not the elitist
+      uint32_t acc[WC], ltw[WC];
+      bool any = false;
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const uint32_t m = (accT >> (4 * c)) & 15u;
-        const ulonglong2 t = *reinterpret_cast<const ulonglong2*>(s_tbl[warp][c][m]);
-        x1 ^= t.x;
-        x2 ^= t.y;
+      for (int j = 0; j < WC; ++j) {
+        const uint32_t wj = c * WC + (uint32_t)j;
+        uint32_t lt = 0, eq = 0xFFFFFFFFu;
+#pragma unroll
+        for (int k = B - 1; k >= 0; --k) {
+          const uint32_t hk = ((h >> k) & 1u) ? 0xFFFFFFFFu : 0u;
+          lt |= eq & ~T[k][j] & hk;
+          eq &= ~(T[k][j] ^ hk);
+        }
+        acc[j] = present ? ((lt | (eq & aeven & ~s_elit[wj])) & valid_mask(wj, n)) : 0u;
+        ltw[j] = lt;
+        any |= acc[j] != 0u;
       }
-      if (x1 | x2) {
-        atomicXor(&s_dh1[sj], x1);
-        atomicXor(&s_dh2[sj], x2);
+      // ---- commit: accepted solutions flip v (apply_acceptance, :221-247)
+      if (any) {
+        uint32_t nx[WC];
+#pragma unroll
+        for (int j = 0; j < WC; ++j) nx[j] = x[j] ^ acc[j];
+        store_row<WC>(a.pop + (size_t)v * Wp + c * WC, nx);
+        if (esrc >= 0 && ((uint32_t)esrc >> 5) / WC == c) {
+          const uint32_t ew = ((uint32_t)esrc >> 5) - c * WC, eb = (uint32_t)esrc & 31u;
+          uint32_t aw = 0, xw = 0;
+#pragma unroll
+          for (int j = 0; j < WC; ++j)
+            if ((uint32_t)j == ew) {
+              aw = acc[j];
+              xw = x[j];
+            }
+          if ((aw >> eb) & 1u) capture_row(a.elit, a.ever, ever_cur, v, (xw >> eb) & 1u);
+        }
+      }
+      // ---- per-solution reductions over the warp's 32 sets ----------------
+      if (!__any_sync(0xFFFFFFFFu, any)) continue;
+      if (!table) {  // first accepting chunk of this batch (warp-uniform)
+        table = true;
+#pragma unroll
+        for (int k = 0; k < B; ++k) Ab[k] = __ballot_sync(0xFFFFFFFFu, (A >> k) & 1u);
+        // Zobrist key XOR table: s_tbl[c][m] = XOR of key(v_{4c+i}) over bits i of m
+        unsigned long long z1 = 0, z2 = 0;
+        if (present) zobrist(v, z1, z2);
+        s_key[warp][lane][0] = z1;
+        s_key[warp][lane][1] = z2;
+        __syncwarp();
+        {
+          // lane = (chunk q, low bits sub): entries sub, sub+4, sub+8, sub+12 of
+          // chunk q share the XOR of keys 4q, 4q+1 selected by sub
+          const uint32_t q = lane >> 2, sub = lane & 3u;
+          const ulonglong2 k0 = *reinterpret_cast<const ulonglong2*>(s_key[warp][4 * q + 0]);
+          const ulonglong2 k1 = *reinterpret_cast<const ulonglong2*>(s_key[warp][4 * q + 1]);
+          const ulonglong2 k2 = *reinterpret_cast<const ulonglong2*>(s_key[warp][4 * q + 2]);
+          const ulonglong2 k3 = *reinterpret_cast<const ulonglong2*>(s_key[warp][4 * q + 3]);
+          const unsigned long long l1 = ((sub & 1u) ? k0.x : 0ull) ^ ((sub & 2u) ? k1.x : 0ull);
+          const unsigned long long l2 = ((sub & 1u) ? k0.y : 0ull) ^ ((sub & 2u) ? k1.y : 0ull);
+          ulonglong2* t = reinterpret_cast<ulonglong2*>(s_tbl[warp][q]);
+          t[sub] = make_ulonglong2(l1, l2);
+          t[sub + 4] = make_ulonglong2(l1 ^ k2.x, l2 ^ k2.y);
+          t[sub + 8] = make_ulonglong2(l1 ^ k3.x, l2 ^ k3.y);
+          t[sub + 12] = make_ulonglong2(l1 ^ k2.x ^ k3.x, l2 ^ k2.y ^ k3.y);
+        }
+        __syncwarp();
+      }
+#pragma unroll
+      for (int j = 0; j < WC; ++j) {
+        const uint32_t accT = transpose32(acc[j], lane);  // lane b: sets l accepted by solution 32j+b
+        // fitness: only strictly improving pairs (T < h) change it; neutral
+        // accepts (delta 0) do not.  Late in a run improving moves are rare,
+        // so the plane transposes are skipped for most words.
+        long long d = 0;
+        const uint32_t imp = acc[j] & ltw[j];
+        if (__any_sync(0xFFFFFFFFu, imp != 0u)) {
+          const uint32_t impT = transpose32(imp, lane);
+#pragma unroll
+          for (int k = 0; k < B; ++k) d += (long long)__popc(impT & Ab[k]) << k;
+          // improving pairs have T < A/2 < 2^(B-1): the top plane is zero
+#pragma unroll
+          for (int k = 0; k < B - 1; ++k) d -= (long long)__popc(transpose32(T[k][j] & imp, lane)) << (k + 1);
+        }
+        const uint32_t sj = (c * WC + (uint32_t)j) * 32u + lane;
+        if (d) atomicAdd(reinterpret_cast<unsigned long long*>(&s_dfit[sj]), (unsigned long long)d);
+        unsigned long long x1 = 0, x2 = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const uint32_t m = (accT >> (4 * q)) & 15u;
+          const ulonglong2 t = *reinterpret_cast<const ulonglong2*>(s_tbl[warp][q][m]);
+          x1 ^= t.x;
+          x2 ^= t.y;
+        }
+        if (x1 | x2) {
+          atomicXor(&s_dh1[sj], x1);
+          atomicXor(&s_dh2[sj], x2);
+        }
       }
     }
     __syncwarp();
@@ -309,7 +322,7 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_sliced_kernel(con
     }
   }
   __syncthreads();
-  for (uint32_t s = threadIdx.x; s < n && s < WP * 32u; s += blockDim.x) {
+  for (uint32_t s = threadIdx.x; s < n && s < Wp * 32u; s += blockDim.x) {
     if (s_dfit[s]) atomicAdd(&a.dfit[s], (double)s_dfit[s]);
     if (s_dh1[s] | s_dh2[s]) {
       atomicXor(&a.dh1[s], s_dh1[s]);
@@ -338,26 +351,32 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_sliced_kernel(con
 // launchers
 // ---------------------------------------------------------------------------
 namespace {
-template <int WP>
-void* univ_kernel_wp(int planes) {
+template <int WC, bool MULTI>
+void* univ_kernel_wc(int planes) {
   switch (planes) {
-    case 4: return (void*)gom_univ_sliced_kernel<4, WP>;
-    case 6: return (void*)gom_univ_sliced_kernel<6, WP>;
-    case 8: return (void*)gom_univ_sliced_kernel<8, WP>;
-    case 12: return (void*)gom_univ_sliced_kernel<12, WP>;
-    case 16: return (void*)gom_univ_sliced_kernel<16, WP>;
+    case 4: return (void*)gom_univ_sliced_kernel<4, WC, MULTI>;
+    case 6: return (void*)gom_univ_sliced_kernel<6, WC, MULTI>;
+    case 8: return (void*)gom_univ_sliced_kernel<8, WC, MULTI>;
+    case 12: return (void*)gom_univ_sliced_kernel<12, WC, MULTI>;
+    case 16: return (void*)gom_univ_sliced_kernel<16, WC, MULTI>;
   }
   throw GomixError(GOMIX_E_INVALID, "univariate sliced kernel: unsupported plane count");
 }
 
+// rows of up to 4 words in one pass, wider rows in passes of 4 words
+int words_per_chunk(int wp) { return wp >= 4 ? 4 : wp; }
+
 void* univ_kernel(int planes, int wp) {
-  switch (wp) {
-    case 1: return univ_kernel_wp<1>(planes);
-    case 2: return univ_kernel_wp<2>(planes);
-    case 4: return univ_kernel_wp<4>(planes);
+  if (wp > 4) return univ_kernel_wc<4, true>(planes);
+  switch (words_per_chunk(wp)) {
+    case 1: return univ_kernel_wc<1, false>(planes);
+    case 2: return univ_kernel_wc<2, false>(planes);
+    case 4: return univ_kernel_wc<4, false>(planes);
   }
   throw GomixError(GOMIX_E_INVALID, "univariate sliced kernel: unsupported row width");
 }
+
+size_t univ_smem(int wp) { return (size_t)wp * 32 * 24 + (size_t)wp * 4; }
 }  // namespace
 
 int univ_sliced_planes(uint64_t max_abs_row_sum) {
@@ -372,15 +391,17 @@ int univ_sliced_block() { return kUnivWarps * 32; }
 int univ_sliced_sets_per_cta() { return kUnivWarps * 32; }
 
 int univ_sliced_max_blocks_per_sm(int planes, int wp) {
+  void* fn = univ_kernel(planes, wp);
+  GOMIX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)univ_smem(wp)));
   int blocks = 0;
-  GOMIX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, univ_kernel(planes, wp), kUnivWarps * 32, 0));
+  GOMIX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, kUnivWarps * 32, univ_smem(wp)));
   return blocks;
 }
 
 void launch_univ_sliced(const GomArgs& a, int planes, int wp, int grid, cudaStream_t s) {
   void* fn = univ_kernel(planes, wp);
   void* args[] = {(void*)&a};
-  GOMIX_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kUnivWarps * 32), args, 0, s));
+  GOMIX_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kUnivWarps * 32), args, univ_smem(wp), s));
 }
 
 }  // namespace gomix_b200

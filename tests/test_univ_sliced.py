@@ -6,8 +6,9 @@ For a univariate FOS the Philox outcome does not depend on the donor draw
 bit-identical populations, fitness, elitists, counters and stop decisions —
 and fitness must equal the cut value of every genotype (the checksum the
 full-size runs use).  Cases cover signed and zero weights, isolated vertices,
-populations that are not multiples of 32, every row width (1/2/4 words) and
-every plane count the kernel instantiates (4..16).
+populations that are not multiples of 32, every row width (1/2/4 words in one pass, up to
+128 words in 4-word passes) and every plane count the kernel instantiates
+(4..16).
 """
 import numpy as np
 import pytest
@@ -54,6 +55,9 @@ def _sparse_graph(nv, avg_deg, wlo, whi, seed, isolated=0):
     ((10, 10), ("int", 1, 10), 32, 8),    # C1 shape, 1 word
     ((14, 9), ("int", -3, 3), 64, 6),     # zero weights, 2 words
     ((9, 7), ("int", 1, 10), 20, 6),      # odd torus (3 colours), 20 members
+    ((20, 20), ("int", 1, 10), 256, 4),   # 8 words: two 4-word passes per row
+    ((16, 12), ("int", -5, 9), 1000, 3),  # 32 words, last word partial
+    ((10, 10), ("int", 1, 10), 4096, 3),  # 128 words, the largest population
 ])
 def test_sliced_equals_lane_per_solution_torus(shape, weights, n, gens):
     inst = G.generate_torus(shape[0], shape[1], weights, 3)
