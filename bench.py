@@ -8,18 +8,22 @@ engine_parallel.hpp:283-316) of the workload; the unit of work is one partial
 evaluation = one executed (solution, linkage set) GOM step
 (RunResult::GroupCounter::steps, runtime.hpp:170-175).
 
-Default workload (BASELINE.json configs[1], the 1-B200 config): C2 = Max-Cut
-2-D torus 100x100 (10^4 vertices), integer weights U[1,10] (generate_torus,
-seed 1), neighbourhood FOS, population 64, Philox donors.
+Default workload: BASELINE.json configs[2] = C3, Max-Cut 2-D torus 1000x1000
+(10^6 vertices), integer weights U[1,10] (generate_torus seed 1), univariate
+FOS, population 128 per GPU, Philox donors.  The metric is quoted "at
+1/2/4/8 B200", which is this config ("sharded 1/2/4/8 B200"), and the north
+star's target is stated on it (the 10^6-vertex grid on 1 B200); it fits one
+GPU.  configs[1] (C2: 100x100, neighbourhood FOS, n=64) is --config c2.
 
 ours:
   value  device throughput, inputs resident in HBM: CUDA events on the engine's
          stream around each generation; L2 flushed (256 MiB write) between
          timed generations, outside the events.
-  e2e    through the C-ABI with HOST buffers: every step uploads the whole
-         population (genotypes + fitness), runs the generation and reads the
-         population back (gomix_gpu_load_population / run_generation /
-         read_population), wall clock.
+  e2e    through the C-ABI with HOST buffers, the reference run loop's
+         per-generation GenerationRunner calls: run_generation (criteria in,
+         stats + improvement log out) + read_elitist (genotype out), wall
+         clock.  e2e_population_roundtrip additionally uploads and reads back
+         the whole population every step.
   roofline  gom_group_kernel (dominant kernel): algorithmic bytes (SURVEY.md
          §8(d) B_step x steps) / its CUDA-event durations vs measured HBM peak.
   cpu_baseline  the reference ParallelEngine (oracle/_ref, compiled from the
@@ -43,6 +47,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "Max-Cut partial evals/sec; time-to-best-known cut (s) at 1/2/4/8 B200"
+REF_BUDGET_S = 90.0  # reference arm: cap on the generations it times (bounded sample)
 UNIT = "partial evaluations/s"
 
 CONFIGS = {
@@ -66,7 +71,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--population", type=int, default=None)
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -79,17 +84,22 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
-def ref_cmd(cfg, n, gens, workers):
+def ref_cmd(cfg, n, gens, workers, max_seconds=0.0):
     w = cfg["weights"]
     wspec = "unit" if w == "unit" else f"int:{w[1]}:{w[2]}"
-    return [os.path.join(ROOT, "oracle", "_ref", "ref_driver"), "bench", "--torus", str(cfg["width"]),
-            str(cfg["height"]), "--weights", wspec, "--inst-seed", "1", "--fos", cfg["ref_fos"], "--n", str(n),
-            "--seed", "1", "--gens", str(gens), "--workers", str(workers)]
+    cmd = [os.path.join(ROOT, "oracle", "_ref", "ref_driver"), "bench", "--torus", str(cfg["width"]),
+           str(cfg["height"]), "--weights", wspec, "--inst-seed", "1", "--fos", cfg["ref_fos"], "--n", str(n),
+           "--seed", "1", "--gens", str(gens), "--workers", str(workers)]
+    if max_seconds > 0:
+        cmd += ["--max-seconds", str(max_seconds)]
+    return cmd
 
 
-def run_reference(cfg, n, gens, workers, timeout=3600):
-    """The reference ParallelEngine compiled from its own headers (oracle/_ref)."""
-    res = subprocess.run(ref_cmd(cfg, n, gens, workers), capture_output=True, text=True, timeout=timeout)
+def run_reference(cfg, n, gens, workers, timeout=3600, max_seconds=0.0):
+    """The reference ParallelEngine compiled from its own headers (oracle/_ref);
+    with max_seconds, generations stop once that much time was spent."""
+    res = subprocess.run(ref_cmd(cfg, n, gens, workers, max_seconds), capture_output=True, text=True,
+                         timeout=timeout)
     if res.returncode != 0:
         raise RuntimeError(f"ref_driver failed: {res.stderr.strip()}")
     return json.loads(res.stdout)
@@ -119,16 +129,21 @@ def bench_reference(args):
     if not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "ref_driver")):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/ref_driver was not built"}))
         return
-    out = run_reference(cfg, n, args.warmup + args.steps, workers)
-    gens = out["gens"][args.warmup:]
+    # bounded sample: W + K generations, or as many as fit in REF_BUDGET_S
+    out = run_reference(cfg, n, args.warmup + args.steps, workers, max_seconds=REF_BUDGET_S)
+    allg = out["gens"]
+    warm = min(args.warmup, max(0, len(allg) - 1))
+    gens = allg[warm:]
     secs = sum(g["seconds"] for g in gens)
     steps = sum(g["steps"] for g in gens)
     value = steps / secs
     line = base_line(args, cfg, n, world)
     line.update({"impl": "reference", "value": value, "ms_per_step": 1e3 * secs / len(gens), "dtype": "f64",
+                 "steps_timed": len(gens), "warmup_run": warm,
                  "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "reference",
-                                  "sample": f"{len(gens)} generations of {args.config} after {args.warmup} "
-                                            f"warm-up, ParallelEngine(workers={workers})"},
+                                  "sample": f"{len(gens)} generations of {args.config} after {warm} warm-up "
+                                            f"(W + K = {args.warmup + args.steps} requested, capped at "
+                                            f"{REF_BUDGET_S:g} s of generations), ParallelEngine(workers={workers})"},
                  "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
     line["config"]["parallelism"] = f"cpu ParallelEngine workers={workers}"
     line["config"]["donors"] = "reference RngStream"
@@ -310,8 +325,30 @@ def bench_ours(args):
     value = steps / dev_s
 
     # ---- e2e through the C-ABI with host buffers ----
+    # (1) the drop-in call pattern: what the reference's run loop / ImsDriver
+    #     does with a GenerationRunner every generation (ims.hpp:77-80,
+    #     run.hpp:64-66): run_generation with the run's stop criteria from the
+    #     host (H2D) and its stats + improvement log back (D2H), then the
+    #     elitist genotype read into a pinned host buffer (D2H l bytes).
     e2e_steps = args.e2e_steps or min(args.steps, 50)
-    # pinned host buffers (the reference-facing call with host memory)
+    eg_host = torch.empty((inst.num_vertices,), dtype=torch.uint8, pin_memory=True).numpy()
+    for _ in range(3):
+        E.run_generation()
+        E.elitist(eg_host)
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e2e_done = 0
+    for _ in range(e2e_steps):
+        E.run_generation()                          # H2D: stop criteria; D2H: stats + improvements
+        e2e_done += int(E.last_stats.steps)         # global steps (sharded stats are global)
+        E.elitist(eg_host)                          # D2H: l genotype bytes (+ fitness)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_s = time.perf_counter() - t0
+    # (2) the whole population in and out every step (n*l genotype bytes +
+    #     n fitness doubles each way): the cost of a caller that keeps the
+    #     population on the host
     g_host = torch.empty((n, inst.num_vertices), dtype=torch.uint8, pin_memory=True).numpy()
     f_host = torch.empty((n,), dtype=torch.float64, pin_memory=True).numpy()
     E.population(g_host, f_host)
@@ -322,20 +359,23 @@ def bench_ours(args):
     barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    e2e_done = 0
-    for _ in range(e2e_steps):
-        E.load_population(g_host, f_host)          # H2D: n*l genotype bytes + n fitness doubles
+    rt_done = 0
+    rt_steps = max(5, e2e_steps // 5)
+    for _ in range(rt_steps):
+        E.load_population(g_host, f_host)
         E.run_generation()
-        e2e_done += int(E.last_stats.steps)        # global steps (sharded stats are global)
-        E.population(g_host, f_host)               # D2H: n*l genotype bytes + n fitness doubles
+        rt_done += int(E.last_stats.steps)
+        E.population(g_host, f_host)
     torch.cuda.synchronize()
     barrier()
-    e2e_s = time.perf_counter() - t0
+    rt_s = time.perf_counter() - t0
     if dist is not None:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        t = torch.tensor([e2e_s, rt_s], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+        e2e_s, rt_s = float(t[0].item()), float(t[1].item())
     io_bytes = n * inst.num_vertices + 8 * n
+    crit_bytes = 40           # gomix_stop_criteria
+    stats_bytes = 48 + 1024   # gomix_run_stats + control block and inline improvement log read back
 
     if rank != 0:
         if dist is not None:
@@ -413,9 +453,15 @@ def bench_ours(args):
     line.update({
         "value": value,
         "ms_per_step": 1e3 * dev_s / args.steps,
-        "e2e": {"value": e2e_done / e2e_s, "unit": UNIT, "h2d_bytes_per_step": io_bytes,
-                "d2h_bytes_per_step": io_bytes, "steps": e2e_steps,
-                "what": "load_population + run_generation + read_population via the C-ABI, host buffers"},
+        "e2e": {"value": e2e_done / e2e_s, "unit": UNIT, "h2d_bytes_per_step": crit_bytes,
+                "d2h_bytes_per_step": stats_bytes + inst.num_vertices + 8, "steps": e2e_steps,
+                "what": "per generation through the C-ABI with pinned host buffers, the reference run loop's "
+                        "GenerationRunner calls: run_generation (stop criteria in, stats + improvements out) "
+                        "+ read_elitist (genotype out); wall clock"},
+        "e2e_population_roundtrip": {"value": rt_done / rt_s, "unit": UNIT, "h2d_bytes_per_step": io_bytes,
+                                     "d2h_bytes_per_step": io_bytes, "steps": rt_steps,
+                                     "what": "load_population + run_generation + read_population (the whole "
+                                             "population as genotype bytes both ways every step)"},
         "roofline": roofline,
         "cpu_baseline": cpu_baseline,
         "time_to_target": time_to_target,

@@ -369,11 +369,14 @@ int mode_bench(const Args& a) {
   std::printf("{\"groups\": %zu, \"init_seconds\": %.6f, \"gens\": [", arts->groups.num_groups(),
               init_s);
   std::uint64_t prev_steps = 0, prev_calls = ctx.control.evaluator_calls();
+  double total = 0.0;
   for (long gen = 0; gen < a.gens; ++gen) {
+    if (a.max_seconds > 0 && gen > 0 && total >= a.max_seconds) break;  // bounded sample
     const auto t0 = std::chrono::steady_clock::now();
     engine.run_generation();
     const double s =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    total += s;
     std::uint64_t steps = 0;
     for (const auto& c : engine.group_counters()) steps += c.steps;
     const std::uint64_t calls = ctx.control.evaluator_calls();

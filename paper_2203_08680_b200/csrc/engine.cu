@@ -129,6 +129,13 @@ std::unique_ptr<Problem> create_problem(const gomix_maxcut* inst, const gomix_fo
     P->max_f = std::max<uint64_t>(P->max_f, b - a);
     if (b - a != 1) P->univariate = false;
   }
+  {
+    std::vector<uint8_t> seen(nv, 0);
+    for (uint64_t t = 0; t < entries && P->var_once; ++t) {
+      if (seen[P->h_set_vars[t]]) P->var_once = false;
+      seen[P->h_set_vars[t]] = 1;
+    }
+  }
   if (colour) {
     for (uint64_t i = 0; i < m; ++i)
       if (colour[i] < 0) invalid("colouring: negative colour");
@@ -236,6 +243,7 @@ struct NcclApi {
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -256,11 +264,12 @@ const NcclApi& nccl_api() {
     GOMIX_SYM(CommDestroy, "ncclCommDestroy");
     GOMIX_SYM(AllGather, "ncclAllGather");
     GOMIX_SYM(Broadcast, "ncclBroadcast");
+    GOMIX_SYM(AllReduce, "ncclAllReduce");
     GOMIX_SYM(GroupStart, "ncclGroupStart");
     GOMIX_SYM(GroupEnd, "ncclGroupEnd");
     GOMIX_SYM(GetErrorString, "ncclGetErrorString");
 #undef GOMIX_SYM
-    a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.AllGather && a.Broadcast &&
+    a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.AllGather && a.Broadcast && a.AllReduce &&
            a.GroupStart && a.GroupEnd && a.GetErrorString;
     if (!a.ok) a.why = "libnccl.so.2 lacks required symbols";
     return a;
@@ -303,6 +312,13 @@ struct gomix_gpu_engine {
   int grid_cap = 1;
   int univ_planes = 0;     // > 0: Philox groups run the bit-sliced lane-per-set kernel
   int univ_grid_cap = 1;
+  // Sharded univariate runs on a variable-once FOS: a row changes only in its
+  // own group, so its count of 1s over all ranks (the presence test) is
+  // exchanged once per generation and the per-group exchange drops the rows.
+  bool lite = false;
+  uint32_t* ones = nullptr;        // [nv] all ranks
+  uint32_t* ones_local = nullptr;  // [nv] this rank
+  uint32_t* ones_stage = nullptr;  // [R][nv] (in-process shards)
   bool gen_ok = false;     // Philox generations run as one persistent kernel (gom_gen.cu)
   int gen_grid = 0;
   long long* gen_dfit = nullptr;
@@ -538,6 +554,12 @@ struct gomix_gpu_engine {
       rec_present = dev_alloc<uint8_t>(allocs, max_group * n);
       rec_accept = dev_alloc<uint8_t>(allocs, max_group * n);
     }
+    lite = R > 1 && P->univariate && P->var_once && mode == GOMIX_MODE_PHILOX;
+    if (lite) {
+      ones = dev_alloc<uint32_t>(allocs, nv);
+      ones_local = dev_alloc<uint32_t>(allocs, nv);
+      if (!cfg.nccl_unique_id) ones_stage = dev_alloc<uint32_t>(allocs, (uint64_t)R * nv);
+    }
     GOMIX_CUDA(cudaMallocHost(&h_ctl, sizeof(DevCtl)));
     GOMIX_CUDA(cudaMallocHost(&h_begin, sizeof(BeginArgs)));
     GOMIX_CUDA(cudaMallocHost(&h_impr, kImprInline * sizeof(double)));
@@ -758,6 +780,7 @@ struct gomix_gpu_engine {
     a.n = (uint32_t)n;
     a.Wp = Wp;
     a.pool = pool;
+    a.ones = lite ? ones : nullptr;
     a.nv = P->nv;
     a.R = R;
     a.rank = rank;
@@ -922,15 +945,24 @@ struct gomix_gpu_engine {
     void* base;
     size_t bytes;  // rank r's chunk sits at base + r * bytes
   };
-  std::vector<Chunk> shard_chunks() const {
-    return {{pool, P->nv * Wp * 4}, {fit_all, n * 8}, {h1_all, n * 8}, {h2_all, n * 8}, {rank_cnt, 16}};
+  std::vector<Chunk> shard_chunks(bool rows = true) const {
+    std::vector<Chunk> c;
+    if (rows) c.push_back({pool, P->nv * Wp * 4});
+    c.push_back({fit_all, n * 8});
+    c.push_back({h1_all, n * 8});
+    c.push_back({h2_all, n * 8});
+    c.push_back({rank_cnt, 16});
+    return c;
   }
 
+  // per-group exchange: rows only when the next group may read other ranks' rows
+  std::vector<Chunk> group_chunks() const { return shard_chunks(!lite); }
+
   // all-gather over NCCL (in place), one grouped call
-  void exchange() {
+  void exchange(bool rows = true) {
     const NcclApi& api = nccl_or_throw();
     nccl_check(api.GroupStart(), "ncclGroupStart");
-    for (const Chunk& c : shard_chunks())
+    for (const Chunk& c : shard_chunks(rows))
       nccl_check(api.AllGather(static_cast<char*>(c.base) + rank * c.bytes, c.base, c.bytes, ncclUint8,
                                nccl->comm, stream),
                  "ncclAllGather");
@@ -948,9 +980,15 @@ struct gomix_gpu_engine {
     begin_call(stop);
     std::vector<uint64_t> order;
     rng.permutation(order, P->k);  // same seed on every rank: same order
+    if (lite) {  // members holding 1 per row, summed over the ranks
+      launch_count_ones(pop, P->nv, Wp, ones_local, stream);
+      const NcclApi& api = nccl_or_throw();
+      nccl_check(api.AllReduce(ones_local, ones, P->nv, ncclUint32, ncclSum, nccl->comm, stream), "ncclAllReduce");
+      ++launches;
+    }
     for (uint64_t gi : order) {
       launch_group(gi, false);
-      exchange();
+      exchange(!lite);
       global_epilogue(gi);
     }
     read_ctl();
@@ -1089,7 +1127,7 @@ struct gomix_gpu_local_group {
   void set_device(uint32_t r) { GOMIX_CUDA(cudaSetDevice(eng[r]->P->device)); }
 
   // every engine finished its local step -> copy every rank's chunks everywhere
-  void exchange() {
+  void exchange(bool rows = true) {
     for (uint32_t r = 0; r < R(); ++r) {
       set_device(r);
       GOMIX_CUDA(cudaEventRecord(ev_step[r], eng[r]->stream));
@@ -1097,11 +1135,11 @@ struct gomix_gpu_local_group {
     for (uint32_t d = 0; d < R(); ++d) {
       set_device(d);
       gomix_gpu_engine& dst = *eng[d];
-      const auto dchunks = dst.shard_chunks();
+      const auto dchunks = dst.shard_chunks(rows);
       for (uint32_t r = 0; r < R(); ++r) {
         if (r == d) continue;
         GOMIX_CUDA(cudaStreamWaitEvent(dst.stream, ev_step[r], 0));
-        const auto schunks = eng[r]->shard_chunks();
+        const auto schunks = eng[r]->shard_chunks(rows);
         for (size_t c = 0; c < dchunks.size(); ++c)
           GOMIX_CUDA(cudaMemcpyAsync(static_cast<char*>(dchunks[c].base) + r * dchunks[c].bytes,
                                      static_cast<const char*>(schunks[c].base) + r * schunks[c].bytes,
@@ -1140,12 +1178,37 @@ struct gomix_gpu_local_group {
       eng[r]->rng.permutation(o, eng[r]->P->k);
       if (r == 0) order = o;
     }
+    const bool lite = eng[0]->lite;
+    if (lite) {  // members holding 1 per row, summed over the ranks (the NCCL all-reduce)
+      for (uint32_t r = 0; r < R(); ++r) {
+        set_device(r);
+        launch_count_ones(eng[r]->pop, eng[r]->P->nv, eng[r]->Wp, eng[r]->ones_local, eng[r]->stream);
+        GOMIX_CUDA(cudaEventRecord(ev_step[r], eng[r]->stream));
+      }
+      for (uint32_t d = 0; d < R(); ++d) {
+        set_device(d);
+        gomix_gpu_engine& dst = *eng[d];
+        const uint64_t nv = dst.P->nv;
+        for (uint32_t r = 0; r < R(); ++r) {
+          GOMIX_CUDA(cudaStreamWaitEvent(dst.stream, ev_step[r], 0));
+          GOMIX_CUDA(cudaMemcpyAsync(dst.ones_stage + (uint64_t)r * nv, eng[r]->ones_local, nv * 4, cudaMemcpyDefault,
+                                     dst.stream));
+        }
+        launch_sum_ones(dst.ones_stage, R(), nv, dst.ones, dst.stream);
+        GOMIX_CUDA(cudaEventRecord(ev_done[d], dst.stream));
+      }
+      for (uint32_t r = 0; r < R(); ++r) {
+        set_device(r);
+        for (uint32_t d = 0; d < R(); ++d)
+          if (d != r) GOMIX_CUDA(cudaStreamWaitEvent(eng[r]->stream, ev_done[d], 0));
+      }
+    }
     for (uint64_t gi : order) {
       for (uint32_t r = 0; r < R(); ++r) {
         set_device(r);
         eng[r]->launch_group(gi, false);
       }
-      exchange();
+      exchange(!lite);
       for (uint32_t r = 0; r < R(); ++r) {
         set_device(r);
         eng[r]->global_epilogue(gi);

@@ -328,7 +328,9 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
       const int32_t rs = a.row_ptr[v], re = a.row_ptr[v + 1];
       uint32_t ones = 0;  // members holding 1 at v, over every rank's shard
       if (!replay) {
-        if (a.R > 1) {
+        if (a.ones) {
+          ones = a.ones[v];  // sharded, variable-once FOS: counted at generation start
+        } else if (a.R > 1) {
           for (uint32_t wg = lane; wg < a.R * Wp; wg += 32)
             ones += __popc(a.pool[((size_t)(wg / Wp) * a.nv + v) * Wp + (wg % Wp)]);
           ones = __reduce_add_sync(0xFFFFFFFFu, ones);
@@ -626,6 +628,24 @@ __global__ void init_epilogue_kernel(const EpiArgs a) {
 // Initial alleles: bit (v, g) of global member g is bit g%32 of Philox block
 // (v, g/32), so a shard of the population draws exactly the bits the same
 // members get in a single-GPU run.
+// Members holding 1, per row (sharded univariate runs: summed over the ranks
+// once per generation instead of all-gathering every row after every group).
+__global__ void count_ones_kernel(const uint32_t* pop, uint64_t nv, uint32_t Wp, uint32_t* ones) {
+  for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t c = 0;
+    for (uint32_t w = 0; w < Wp; ++w) c += __popc(pop[v * Wp + w]);
+    ones[v] = c;
+  }
+}
+
+__global__ void sum_ones_kernel(const uint32_t* stage, uint32_t R, uint64_t nv, uint32_t* ones) {
+  for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t c = 0;
+    for (uint32_t r = 0; r < R; ++r) c += stage[(uint64_t)r * nv + v];
+    ones[v] = c;
+  }
+}
+
 __global__ void philox_init_kernel(uint32_t* pop, uint64_t nv, uint32_t n, uint32_t Wp,
                                    uint64_t seed, uint32_t rank) {
   const uint64_t total = nv * Wp;
@@ -834,6 +854,16 @@ void launch_ims_collect(const SnapArgs& a, ImsBestDev* b, uint32_t* bits, int ex
 void launch_ims_offer(const SnapArgs& a, ImsBestDev* b, const uint32_t* bits, int exact, cudaStream_t s) {
   ims_offer_decide_kernel<<<1, 1, 0, s>>>(a.ctl, b, exact);
   ims_offer_copy_kernel<<<grid_for((a.nv + 31) / 32, 256, 148 * 4), 256, 0, s>>>(a, b, bits);
+  GOMIX_CUDA(cudaGetLastError());
+}
+
+void launch_count_ones(const uint32_t* pop, uint64_t nv, uint32_t Wp, uint32_t* ones, cudaStream_t s) {
+  count_ones_kernel<<<grid_for(nv, 256, 148 * 8), 256, 0, s>>>(pop, nv, Wp, ones);
+  GOMIX_CUDA(cudaGetLastError());
+}
+
+void launch_sum_ones(const uint32_t* stage, uint32_t R, uint64_t nv, uint32_t* ones, cudaStream_t s) {
+  sum_ones_kernel<<<grid_for(nv, 256, 148 * 8), 256, 0, s>>>(stage, R, nv, ones);
   GOMIX_CUDA(cudaGetLastError());
 }
 

@@ -139,7 +139,9 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_sliced_kernel(con
     // ---- presence: some member (over every rank's shard) holds the other value
     uint32_t ones = 0;
     if (live) {
-      if (!MULTI && a.R == 1) {
+      if (a.ones) {
+        ones = a.ones[v];  // sharded, variable-once FOS: counted at generation start
+      } else if (!MULTI && a.R == 1) {
 #pragma unroll
         for (int j = 0; j < WC; ++j) ones += __popc(x0[j]);
       } else {

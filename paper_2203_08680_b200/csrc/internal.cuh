@@ -74,6 +74,7 @@ struct Problem {
   uint64_t nv = 0, q = 0, m = 0, k = 0, lmig_edges = 0, max_f = 0, max_fp = 0;
   uint64_t max_abs_row = 0;  // univariate: max over sets {v} of sum |w| on v's edges (integer weights)
   bool exact = true, univariate = true, i32 = false;
+  bool var_once = true;  // every variable is in at most one linkage set
   // host mirrors (small)
   std::vector<uint64_t> h_set_off;
   std::vector<uint32_t> h_set_vars;
@@ -171,6 +172,7 @@ struct GomArgs {
   uint8_t* rec_accept;
   uint32_t n, Wp, team_warps, stage_words;  // n: this rank's solutions, Wp: words per row per rank
   const uint32_t* pool;  // all ranks' rows, rank-major [R][nv][Wp] (== pop when R == 1)
+  const uint32_t* ones;  // sharded univariate runs: members holding 1 per row over all ranks (else nullptr)
   uint64_t nv;
   uint32_t R, rank, n_global;
   int32_t exact;
@@ -307,6 +309,8 @@ void launch_finalize_elitist(const SnapArgs& a, cudaStream_t s);
 void launch_external_elitist(const SnapArgs& a, double fitness, cudaStream_t s);
 void launch_ims_collect(const SnapArgs& a, ImsBestDev* b, uint32_t* bits, int exact, cudaStream_t s);
 void launch_ims_offer(const SnapArgs& a, ImsBestDev* b, const uint32_t* bits, int exact, cudaStream_t s);
+void launch_count_ones(const uint32_t* pop, uint64_t nv, uint32_t Wp, uint32_t* ones, cudaStream_t s);
+void launch_sum_ones(const uint32_t* stage, uint32_t R, uint64_t nv, uint32_t* ones, cudaStream_t s);
 void launch_philox_init(uint32_t* pop, uint64_t nv, uint32_t n, uint32_t Wp, uint64_t seed,
                         uint32_t rank, cudaStream_t s);
 void launch_full_eval(const Problem& P, const uint32_t* pop, double* fit, uint32_t n,

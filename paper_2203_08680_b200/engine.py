@@ -344,8 +344,11 @@ class GpuParallelEngine:
         check(lib().gomix_gpu_generation(self.h, C.byref(g)))
         return g.value
 
-    def elitist(self):
-        g = np.zeros(self.problem.info.num_vertices, np.uint8)
+    def elitist(self, genotype_out: Optional[np.ndarray] = None):
+        """(genotype, fitness) of the elitist; an optional caller buffer (e.g.
+        pinned host memory, num_vertices uint8) is filled in place."""
+        g = genotype_out if genotype_out is not None else np.zeros(self.problem.info.num_vertices, np.uint8)
+        assert g.dtype == np.uint8 and g.shape == (self.problem.info.num_vertices,) and g.flags.c_contiguous
         f = C.c_double()
         check(lib().gomix_gpu_read_elitist(self.h, g.ctypes.data, C.byref(f)))
         return g, f.value
