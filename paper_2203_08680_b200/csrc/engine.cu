@@ -342,6 +342,8 @@ struct gomix_gpu_engine {
   double* fit = nullptr;
   double* dfit = nullptr;
   double* part = nullptr;
+  double* part1 = nullptr;
+  unsigned int* part_cnt = nullptr;
   unsigned long long* h1 = nullptr;  // per-solution Zobrist hashes
   unsigned long long* h2 = nullptr;
   unsigned long long* dh1 = nullptr;
@@ -538,7 +540,13 @@ struct gomix_gpu_engine {
     impr_cap = std::min<uint64_t>(std::max<uint64_t>(4096, n_global * (P->k + 1)), 1ull << 22);
     impr = dev_alloc<double>(allocs, impr_cap);
     impr_calls = dev_alloc<unsigned long long>(allocs, impr_cap);
-    if (epi_mode == 1) part = dev_alloc<double>(allocs, (size_t)grid_cap * n);
+    if (epi_mode == 1) {
+      part = dev_alloc<double>(allocs, (size_t)grid_cap * n);
+      const uint64_t nblk = ((uint64_t)grid_cap + kPartBlock - 1) / kPartBlock;
+      part1 = dev_alloc<double>(allocs, nblk * n);
+      part_cnt = dev_alloc<unsigned int>(allocs, nblk);
+      GOMIX_CUDA(cudaMemset(part_cnt, 0, nblk * sizeof(unsigned int)));
+    }
     d_order = dev_alloc<uint32_t>(allocs, P->k);
     d_groups = dev_alloc<GroupDesc>(allocs, P->k);
     {
@@ -768,6 +776,8 @@ struct gomix_gpu_engine {
     a.elit = elit;
     a.dfit = epi_mode == 0 ? dfit : nullptr;
     a.part = epi_mode == 1 ? part : nullptr;
+    a.part1 = epi_mode == 1 ? part1 : nullptr;
+    a.part_cnt = part_cnt;
     a.dh1 = dh1;
     a.dh2 = dh2;
     a.ctl = ctl;
@@ -921,7 +931,7 @@ struct gomix_gpu_engine {
       launch_philox_init(pop, nv, (uint32_t)n, Wp, seed, rank, stream);
       ++launches;
     }
-    launch_full_eval(*P, pop, fit, (uint32_t)n, Wp, !P->exact, stream);
+    launch_full_eval(*P, pop, fit, (uint32_t)n, Wp, epi_mode == 2, stream);
     launch_hash_population(snap_args(), stream);
     launches += 2;
     if (R > 1 && nccl) exchange();
@@ -1078,7 +1088,7 @@ struct gomix_gpu_engine {
     if (fitness) {
       GOMIX_CUDA(cudaMemcpyAsync(fit, fitness, n * 8, cudaMemcpyHostToDevice, stream));
     } else {
-      launch_full_eval(*P, pop, fit, (uint32_t)n, Wp, !P->exact, stream);
+      launch_full_eval(*P, pop, fit, (uint32_t)n, Wp, epi_mode == 2, stream);
       ++launches;
     }
     launch_hash_population(snap_args(), stream);  // hashes of the new members

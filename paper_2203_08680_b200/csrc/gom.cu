@@ -520,14 +520,40 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    if ((s_steps | s_calls) && !(a.exp_flags & 4)) {
-      atomicAdd(&a.ctl->grp_steps, s_steps);
-      atomicAdd(&a.ctl->grp_calls, s_calls);
+  if (threadIdx.x == 0 && (s_steps | s_calls) && !(a.exp_flags & 4)) {
+    atomicAdd(&a.ctl->grp_steps, s_steps);
+    atomicAdd(&a.ctl->grp_calls, s_calls);
+  }
+  uint32_t parties = gridDim.x;
+  if (float_parts && a.part1 && gridDim.x > kPartBlock) {
+    // two-level deterministic sum of the float partials: the last CTA of each
+    // block of kPartBlock CTAs adds that block's rows in CTA order into one
+    // level-1 row, so the epilogue adds ceil(grid / kPartBlock) rows instead
+    // of one per CTA (the serial tail of float launches)
+    const uint32_t blk = blockIdx.x / kPartBlock;
+    const uint32_t b0 = blk * kPartBlock, members = min(kPartBlock, gridDim.x - b0);
+    if (threadIdx.x == 0) {
+      __threadfence();
+      s_last = atomicAdd(&a.part_cnt[blk], 1u) == members - 1;
     }
-    // last-CTA-done ticket: everything above is visible to the last CTA
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    for (uint32_t s = threadIdx.x; s < n; s += blockDim.x) {
+      double sum = 0.0;
+      for (uint32_t b = b0; b < b0 + members; ++b) sum += __ldcg(a.part + (size_t)b * n + s);
+      a.part1[(size_t)blk * n + s] = sum;
+    }
+    if (threadIdx.x == 0) a.part_cnt[blk] = 0;
+    parties = (gridDim.x + kPartBlock - 1) / kPartBlock;
+    epi.part = a.part1;
+    epi.nparts = parties;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    // last-party ticket: everything above is visible to the last one
     if (!(a.exp_flags & 1)) __threadfence();
-    s_last = atomicAdd(&a.ctl->done, 1u) == gridDim.x - 1;
+    s_last = atomicAdd(&a.ctl->done, 1u) == parties - 1;
   }
   __syncthreads();
   if (!s_last) return;
@@ -687,6 +713,24 @@ __global__ void full_eval_parallel_kernel(const uint32_t* eu, const uint32_t* ev
     const uint32_t s = w * 32u + lane;
     if (s < n && sum != 0.0) atomicAdd(&fit[s], sum);
   }
+}
+
+// Float fitness, deterministic and parallel (production mode): a warp per
+// solution, lane-strided partial sums combined by an xor butterfly.
+__global__ void full_eval_warp_kernel(const uint32_t* eu, const uint32_t* ev, const double* ew, uint64_t q,
+                                      const uint32_t* pop, double* fit, uint32_t n, uint32_t Wp) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (s >= n) return;
+  const uint32_t w = s >> 5, b = s & 31u;
+  double sum = 0.0;
+  for (uint64_t e = lane; e < q; e += 32) {
+    const uint32_t x = pop[(uint64_t)eu[e] * Wp + w] ^ pop[(uint64_t)ev[e] * Wp + w];
+    sum += ((x >> b) & 1u) ? ew[e] : 0.0;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
+  if (lane == 0) fit[s] = sum;
 }
 
 // Float fitness in the reference's left-to-right edge order (graybox.hpp:139-144).
@@ -877,6 +921,8 @@ void launch_full_eval(const Problem& P, const uint32_t* pop, double* fit, uint32
                       uint32_t Wp, bool ordered, cudaStream_t s) {
   if (ordered) {
     full_eval_ordered_kernel<<<(n + 127) / 128, 128, 0, s>>>(P.eu, P.ev, P.ew, P.q, pop, fit, n, Wp);
+  } else if (!P.exact) {
+    full_eval_warp_kernel<<<(n + 7) / 8, 256, 0, s>>>(P.eu, P.ev, P.ew, P.q, pop, fit, n, Wp);
   } else {
     GOMIX_CUDA(cudaMemsetAsync(fit, 0, n * sizeof(double), s));
     const uint64_t chunk = 1024;

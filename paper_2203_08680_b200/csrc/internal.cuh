@@ -30,6 +30,7 @@ namespace gomix_b200 {
 constexpr uint32_t kInSet = 0x80000000u;
 constexpr int kMaxSetSize = 64;     // per-lane set patterns are uint64 masks
 constexpr int kEpilogueThreads = 1024;
+constexpr uint32_t kPartBlock = 32;  // CTAs whose float partials one level-1 reducer adds
 
 struct FpEntry {
   uint32_t a, b;  // endpoint vertex id, or kInSet | index within the set
@@ -173,6 +174,8 @@ struct GomArgs {
   uint32_t n, Wp, team_warps, stage_words;  // n: this rank's solutions, Wp: words per row per rank
   const uint32_t* pool;  // all ranks' rows, rank-major [R][nv][Wp] (== pop when R == 1)
   const uint32_t* ones;  // sharded univariate runs: members holding 1 per row over all ranks (else nullptr)
+  double* part1;           // float partials, level 1: [ceil(grid / kPartBlock)][n] (nullptr: one level)
+  unsigned int* part_cnt;  // per level-1 block arrival counters
   uint64_t nv;
   uint32_t R, rank, n_global;
   int32_t exact;
