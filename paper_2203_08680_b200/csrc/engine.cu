@@ -508,14 +508,14 @@ struct gomix_gpu_engine {
       if (per >= 1) {
         gen_grid = (int)std::min<uint64_t>(want, (uint64_t)per * sms);
         gen_ok = true;
-        gen_dfit = dev_alloc<long long>(allocs, 3 * n);
-        gen_dh = dev_alloc<unsigned long long>(allocs, 6 * n);
+        gen_dfit = dev_alloc<long long>(allocs, 3 * n * kAccStride);
+        gen_dh = dev_alloc<unsigned long long>(allocs, 6 * n * kAccStride);
         gen_cnt = dev_alloc<unsigned long long>(allocs, 6);
-        gen_bar = dev_alloc<unsigned int>(allocs, 2);
-        GOMIX_CUDA(cudaMemset(gen_dfit, 0, 3 * n * 8));
-        GOMIX_CUDA(cudaMemset(gen_dh, 0, 6 * n * 8));
+        gen_bar = dev_alloc<unsigned int>(allocs, 2048);  // two-level barrier (gom_gen.cu)
+        GOMIX_CUDA(cudaMemset(gen_dfit, 0, 3 * n * kAccStride * 8));
+        GOMIX_CUDA(cudaMemset(gen_dh, 0, 6 * n * kAccStride * 8));
         GOMIX_CUDA(cudaMemset(gen_cnt, 0, 6 * 8));
-        GOMIX_CUDA(cudaMemset(gen_bar, 0, 8));
+        GOMIX_CUDA(cudaMemset(gen_bar, 0, 2048 * 4));
       }
     }
 
@@ -1239,6 +1239,21 @@ struct gomix_gpu_local_group {
 extern "C" {
 
 int gomix_gpu_abi_version(void) { return GOMIX_GPU_ABI_VERSION; }
+
+GOMIX_API int gomix_debug_cta_probes(unsigned long long* out) {
+  return guarded([&] { debug_cta_probes(out); });
+}
+
+// latency-study probes (GOMIX_EXP bit 32), not part of the public header
+GOMIX_API int gomix_debug_probes(unsigned long long* out, int32_t reset) {
+  return guarded([&] {
+    unsigned long long b[64];
+    debug_probes(out, reset != 0);
+    debug_probes_gen(b, reset != 0);
+    for (int i = 0; i < 64; ++i)
+      if (!out[i]) out[i] = b[i];
+  });
+}
 
 const char* gomix_gpu_last_error(void) { return g_last_error.c_str(); }
 

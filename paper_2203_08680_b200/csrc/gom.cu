@@ -911,6 +911,15 @@ void launch_sum_ones(const uint32_t* stage, uint32_t R, uint64_t nv, uint32_t* o
   GOMIX_CUDA(cudaGetLastError());
 }
 
+void debug_probes(unsigned long long* out, bool reset) {
+  GOMIX_CUDA(cudaDeviceSynchronize());
+  GOMIX_CUDA(cudaMemcpyFromSymbol(out, g_probe, sizeof(unsigned long long) * 64));
+  if (reset) {
+    unsigned long long z[64] = {};
+    GOMIX_CUDA(cudaMemcpyToSymbol(g_probe, z, sizeof(z)));
+  }
+}
+
 void launch_philox_init(uint32_t* pop, uint64_t nv, uint32_t n, uint32_t Wp, uint64_t seed,
                         uint32_t rank, cudaStream_t s) {
   philox_init_kernel<<<grid_for(nv * Wp, 256, 4096), 256, 0, s>>>(pop, nv, n, Wp, seed, rank);

@@ -14,6 +14,17 @@ namespace gomix_b200 {
 
 constexpr uint32_t kEpiSmemFit = 256;  // fitness values the epilogue keeps in shared memory
 
+// Timing probes for latency studies (GOMIX_EXP bit 32): CTA 0 / thread 0
+// records %globaltimer at numbered points of its first set.
+static __device__ unsigned long long g_probe[64];  // one copy per translation unit
+__device__ __forceinline__ void probe(uint32_t flags, uint32_t i) {
+  if ((flags & 32u) && blockIdx.x == 0 && threadIdx.x == 0 && i < 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (g_probe[i] == 0) g_probe[i] = t;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Philox4x32-10 (Salmon et al., SC'11), counter-based: every (generation, set,
 // solution, call) has its own counter, so draws need no state and no order.
@@ -103,7 +114,7 @@ __device__ __forceinline__ uint32_t differ_word(const uint32_t* rowsF, uint32_t 
   uint32_t dw = 0;
   for (uint32_t jv = 0; jv < f; ++jv)
     dw |= rowsF[jv * RW + wg] ^ (((m >> jv) & 1ull) ? 0xFFFFFFFFu : 0u);
-  return dw & valid_mask(wg % Wp, n);
+  return dw & valid_mask(wg & (Wp - 1u), n);  // Wp is a power of two
 }
 
 // 32x32 bit-matrix transpose across a warp: lane r holds row r on entry;

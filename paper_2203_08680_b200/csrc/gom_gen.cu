@@ -34,24 +34,41 @@ namespace gomix_b200 {
 
 namespace {
 
-constexpr uint32_t kTagOrderGen = 0x4F524400u;  // same stream as begin_generation_kernel ("ORD")
+constexpr uint32_t kTagOrderGen = 0x4F524400u;
+__device__ unsigned long long g_cta_probe[8192];  // latency study: per-CTA arrival time and SM id  // same stream as begin_generation_kernel ("ORD")
 
-// Sense-by-generation grid barrier; bar[0] = arrivals, bar[1] = generation.
-// The gpu-scope fences order this CTA's writes before the arrival and, on
-// the way out, invalidate the SM's L1 so later loads see other CTAs' writes.
+// Two-level grid barrier.  ~1,250 single-team CTAs arriving on one counter
+// serialise in one L2 slice (measured ~4 us per barrier on C2), so CTAs
+// arrive on kBarSub counters (one 128-byte line each), the last arriver of
+// each sub-group arrives on the top counter, and the last of those bumps the
+// generation word every CTA polls.  Layout (uint32): [0] generation,
+// [32] top arrivals, [64 + 32 g] arrivals of sub-group g.  The gpu-scope
+// fences order each CTA's writes before its arrival and, on the way out,
+// invalidate the SM's L1 so later loads see other CTAs' writes.
+constexpr uint32_t kBarSub = 32;
+
 __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nblocks) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile unsigned int* vgen = bar + 1;
+    volatile unsigned int* vgen = bar;
     const unsigned int g = *vgen;
     __threadfence();
-    if (atomicAdd(bar, 1u) == nblocks - 1) {
-      *(volatile unsigned int*)bar = 0u;
+    const uint32_t subs = min(kBarSub, nblocks);
+    const uint32_t grp = blockIdx.x % subs;
+    const uint32_t members = nblocks / subs + (grp < nblocks % subs ? 1u : 0u);
+    bool released = false;
+    if (atomicAdd(bar + 64 + 32 * grp, 1u) == members - 1) {
+      *(volatile unsigned int*)(bar + 64 + 32 * grp) = 0u;
       __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      while (*vgen == g) __nanosleep(20);
+      if (atomicAdd(bar + 32, 1u) == subs - 1) {
+        *(volatile unsigned int*)(bar + 32) = 0u;
+        __threadfence();
+        atomicAdd(bar, 1u);
+        released = true;
+      }
     }
+    if (!released)
+      while (*vgen == g) __nanosleep(64);
     __threadfence();
   }
   __syncthreads();
@@ -59,8 +76,14 @@ __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nbl
 
 }  // namespace
 
-template <int WPT, bool TEAM>
-__global__ void __launch_bounds__(512, 1) gom_generation_kernel(const GomArgs a, const GenArgs ga) {
+// Every set of a group should get its own team in ONE wave (a second set per
+// team doubles the group's critical path), so team kernels are register-
+// capped for that: 2-warp teams (n <= 64) at 11 CTAs per SM = 1,628 teams.
+constexpr int gen_min_blocks(bool team, int tw) { return team ? (tw == 2 ? 11 : (tw == 4 ? 5 : 2)) : 2; }
+
+template <int WPT, bool TEAM, int TW>
+__global__ void __launch_bounds__(TEAM ? 32 * TW : 256, gen_min_blocks(TEAM, TW))
+    gom_generation_kernel(const GomArgs a, const GenArgs ga) {
   extern __shared__ __align__(16) uint32_t smem[];
   __shared__ double s_fit[kGenMaxN];
   __shared__ unsigned long long s_h1[kGenMaxN], s_h2[kGenMaxN];
@@ -75,7 +98,7 @@ __global__ void __launch_bounds__(512, 1) gom_generation_kernel(const GomArgs a,
 
   using Acc = long long;
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  const uint32_t tw = TEAM ? a.team_warps : 1u;
+  const uint32_t tw = TEAM ? (uint32_t)TW : 1u;
   const uint32_t teams_per_cta = TEAM ? 1u : (blockDim.x >> 5);
   const uint32_t team = TEAM ? 0u : warp, wit = TEAM ? warp : 0u;
   const uint32_t tid_team = wit * 32u + lane, team_threads = tw * 32u;
@@ -121,9 +144,11 @@ __global__ void __launch_bounds__(512, 1) gom_generation_kernel(const GomArgs a,
     const GroupDesc d = a.groups[gi];
     const uint4* gmeta = a.gmeta + d.g0;
     const uint32_t bi = (buf0 + slot) % 3u;
-    long long* D = ga.dfit + (size_t)bi * n;
-    unsigned long long* DH1 = ga.dh + (size_t)bi * 2 * n;
-    unsigned long long* DH2 = DH1 + n;
+    // accumulators spread one per 256-byte line: ~1,250 CTAs add into the same
+    // n solutions, so neighbouring solutions must not share an L2 line
+    long long* D = ga.dfit + (size_t)bi * n * kAccStride;
+    unsigned long long* DH1 = ga.dh + (size_t)bi * 2 * n * kAccStride;
+    unsigned long long* DH2 = DH1 + (size_t)n * kAccStride;
     unsigned long long* CNT = ga.cnt + 2 * bi;
 
     // ---- work: phases 1-4 over this CTA's sets ------------------------------
@@ -169,10 +194,10 @@ __global__ void __launch_bounds__(512, 1) gom_generation_kernel(const GomArgs a,
     for (int j = 0; j < WPT; ++j) {
       const uint32_t s = (wit + tw * (uint32_t)j) * 32u + lane;
       if (s < n) {
-        if (acc[j]) atomicAdd(reinterpret_cast<unsigned long long*>(D + s), (unsigned long long)acc[j]);
+        if (acc[j]) atomicAdd(reinterpret_cast<unsigned long long*>(D + s * kAccStride), (unsigned long long)acc[j]);
         if (dh1[j] | dh2[j]) {
-          atomicXor(DH1 + s, dh1[j]);
-          atomicXor(DH2 + s, dh2[j]);
+          atomicXor(DH1 + s * kAccStride, dh1[j]);
+          atomicXor(DH2 + s * kAccStride, dh2[j]);
         }
       }
     }
@@ -181,12 +206,22 @@ __global__ void __launch_bounds__(512, 1) gom_generation_kernel(const GomArgs a,
       atomicAdd(CNT, s_steps);
       atomicAdd(CNT + 1, s_calls);
     }
+    probe(a.exp_flags, 16 + 4 * slot);
+    if ((a.exp_flags & 32u) && slot == 0 && threadIdx.x == 0 && blockIdx.x < 4096) {
+      unsigned long long t;
+      uint32_t smid;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      g_cta_probe[2 * blockIdx.x] = t;
+      g_cta_probe[2 * blockIdx.x + 1] = smid;
+    }
     grid_barrier(ga.bar, gridDim.x);
+    probe(a.exp_flags, 17 + 4 * slot);
 
     // ---- epilogue (every CTA): fitness / hash commit ------------------------
     for (uint32_t s = threadIdx.x; s < n; s += blockDim.x) {
-      const double f = s_fit[s] + (double)__ldcg(D + s);
-      const unsigned long long x1 = s_h1[s] ^ __ldcg(DH1 + s), x2 = s_h2[s] ^ __ldcg(DH2 + s);
+      const double f = s_fit[s] + (double)__ldcg(D + s * kAccStride);
+      const unsigned long long x1 = s_h1[s] ^ __ldcg(DH1 + s * kAccStride), x2 = s_h2[s] ^ __ldcg(DH2 + s * kAccStride);
       s_fit[s] = f;
       s_h1[s] = x1;
       s_h2[s] = x2;
@@ -197,9 +232,9 @@ __global__ void __launch_bounds__(512, 1) gom_generation_kernel(const GomArgs a,
         // accumulator of the previous group: read by every CTA before this
         // group's barrier, written again only after the next one
         const uint32_t zb = (bi + 2u) % 3u;
-        ga.dfit[(size_t)zb * n + s] = 0;
-        ga.dh[(size_t)zb * 2 * n + s] = 0;
-        ga.dh[(size_t)zb * 2 * n + n + s] = 0;
+        ga.dfit[((size_t)zb * n + s) * kAccStride] = 0;
+        ga.dh[((size_t)zb * 2 * n + s) * kAccStride] = 0;
+        ga.dh[((size_t)zb * 2 * n + n + s) * kAccStride] = 0;
       }
     }
     if (lead && threadIdx.x == 0) {
@@ -272,6 +307,7 @@ __global__ void __launch_bounds__(512, 1) gom_generation_kernel(const GomArgs a,
       }
     }
     __syncthreads();
+    probe(a.exp_flags, 18 + 4 * slot);
     if (s_stop) break;
   }
 
@@ -305,25 +341,42 @@ __global__ void __launch_bounds__(512, 1) gom_generation_kernel(const GomArgs a,
 // launchers
 // ---------------------------------------------------------------------------
 namespace {
-void* gen_kernel(int wpt, bool team) {
+void* gen_kernel(int wpt, bool team, int tw) {
   if (team) {
-    switch (wpt) {
-      case 1: return (void*)gom_generation_kernel<1, true>;
+    if (wpt != 1) return nullptr;
+    switch (tw) {
+      case 2: return (void*)gom_generation_kernel<1, true, 2>;
+      case 4: return (void*)gom_generation_kernel<1, true, 4>;
+      case 8: return (void*)gom_generation_kernel<1, true, 8>;
     }
   } else {
     switch (wpt) {
-      case 1: return (void*)gom_generation_kernel<1, false>;
-      case 2: return (void*)gom_generation_kernel<2, false>;
-      case 4: return (void*)gom_generation_kernel<4, false>;
-      case 8: return (void*)gom_generation_kernel<8, false>;
+      case 1: return (void*)gom_generation_kernel<1, false, 1>;
+      case 2: return (void*)gom_generation_kernel<2, false, 1>;
+      case 4: return (void*)gom_generation_kernel<4, false, 1>;
+      case 8: return (void*)gom_generation_kernel<8, false, 1>;
     }
   }
   return nullptr;
 }
 }  // namespace
 
+void debug_cta_probes(unsigned long long* out) {
+  GOMIX_CUDA(cudaDeviceSynchronize());
+  GOMIX_CUDA(cudaMemcpyFromSymbol(out, g_cta_probe, sizeof(unsigned long long) * 8192));
+}
+
+void debug_probes_gen(unsigned long long* out, bool reset) {
+  GOMIX_CUDA(cudaDeviceSynchronize());
+  GOMIX_CUDA(cudaMemcpyFromSymbol(out, g_probe, sizeof(unsigned long long) * 64));
+  if (reset) {
+    unsigned long long z[64] = {};
+    GOMIX_CUDA(cudaMemcpyToSymbol(g_probe, z, sizeof(z)));
+  }
+}
+
 int gen_kernel_max_blocks(int wpt, bool team, int block, size_t smem) {
-  void* fn = gen_kernel(wpt, team);
+  void* fn = gen_kernel(wpt, team, team ? block / 32 : 1);
   if (!fn) return 0;
   GOMIX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int blocks = 0;
@@ -333,7 +386,7 @@ int gen_kernel_max_blocks(int wpt, bool team, int block, size_t smem) {
 
 void launch_generation_kernel(const GomArgs& a, const GenArgs& ga, int wpt, bool team, int grid, int block,
                               size_t smem, cudaStream_t s) {
-  void* fn = gen_kernel(wpt, team);
+  void* fn = gen_kernel(wpt, team, team ? block / 32 : 1);
   void* args[] = {(void*)&a, (void*)&ga};
   GOMIX_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(block), args, smem, s));
 }

@@ -23,6 +23,7 @@ __device__ __forceinline__ void gom_general_set(
   // rows at group start (the donor pool, engine_parallel.hpp:100-103),
   // every solution's pattern on F (so a donor test is one load), the
   // donor-inserted rows and the committed rows.
+  probe(a.exp_flags, 0);
   const uint4 gm = gmeta[p];
   const uint32_t sid = gm.x;
   const uint32_t f = gm.w >> 24;
@@ -30,6 +31,7 @@ __device__ __forceinline__ void gom_general_set(
   const uint32_t e0 = gm.z, e1 = gm.z + (gm.w & 0xFFFFFFu);
   // pool words: RW = R*Wp per row (every rank's shard; R == 1: the population)
   const uint32_t RW = a.R * Wp, own = a.rank * Wp;
+  probe(a.exp_flags, 1);
   uint64_t* patt = reinterpret_cast<uint64_t*>(stage);  // pattern of every member (padded index)
   uint32_t* rowsF = stage + 64u * RW;                    // F rows at group start, stride RW
   uint32_t* newD = rowsF + f * RW;                       // own donor-inserted rows, stride Wp
@@ -63,12 +65,14 @@ __device__ __forceinline__ void gom_general_set(
   for (uint32_t jv = tid_team; jv < f; jv += team_threads) zobrist(vars[jv], zF[2 * jv], zF[2 * jv + 1]);
   const uint64_t fm = f >= 64 ? ~0ull : ((1ull << f) - 1ull);
   team_sync(tw, teams_per_cta, team);
+  probe(a.exp_flags, 2);
   for (uint32_t wg = wit; wg < RW; wg += tw) {
     uint64_t m = 0;
     for (uint32_t jv = 0; jv < f; ++jv) m |= (uint64_t)((rowsF[jv * RW + wg] >> lane) & 1u) << jv;
     patt[wg * 32u + lane] = m;
   }
   team_sync(tw, teams_per_cta, team);
+  probe(a.exp_flags, 3);
   uint64_t pm[WPT];
 #pragma unroll
   for (int j = 0; j < WPT; ++j) pm[j] = patt[(own + wit + tw * j) * 32u + lane];
@@ -91,40 +95,32 @@ __device__ __forceinline__ void gom_general_set(
         if (d >= 0) x = patt[d];
       } else {
         // uniform over the members that differ on F — the distribution of
-        // the lazy Fisher-Yates scan of engine_serial.hpp:30-46: rejection
-        // sampling first, exact count-and-select when it keeps failing.
-        // (Counting first was measured slower on C2: most draws succeed at
-        // the first candidate.)
+        // the lazy Fisher-Yates scan of engine_serial.hpp:30-46 — from ONE
+        // Philox call: candidate c0 uniform over all members is taken when it
+        // differs; otherwise the k-th differing member, k uniform from the
+        // call's other 64 bits.  P(d) = 1/n + (n_same/n)(1/n_diff) = 1/n_diff
+        // for every differing d, and a warp diverges for at most one
+        // count-and-select (instead of more draws).
         const uint2 key = make_uint2((uint32_t)a.seed, (uint32_t)(a.seed >> 32));
-        const uint32_t ng = a.n_global, pad = 32u * Wp;
-        for (uint32_t call = 0; call < 2 && d < 0; ++call) {
-          const uint4 r = philox4x32_10(make_uint4(sg, sid, generation, kTagGom | call), key);
-          const uint32_t c0 = bounded(lo64(r), ng);
-          const uint64_t x0 = patt[(c0 / n) * pad + c0 % n];
-          if (x0 != m) {
-            d = (int32_t)c0;
-            x = x0;
-          } else {
-            const uint32_t c1 = bounded(hi64(r), ng);
-            const uint64_t x1 = patt[(c1 / n) * pad + c1 % n];
-            if (x1 != m) {
-              d = (int32_t)c1;
-              x = x1;
-            }
-          }
-        }
-        if (d < 0) {
+        const uint32_t ng = a.n_global;
+        const uint4 r = philox4x32_10(make_uint4(sg, sid, generation, kTagGom), key);
+        const uint32_t c0 = bounded(lo64(r), ng);
+        const uint32_t i0 = a.R == 1 ? c0 : (c0 / n) * (32u * Wp) + c0 % n;
+        const uint64_t x0 = patt[i0];
+        if (x0 != m) {
+          d = (int32_t)c0;
+          x = x0;
+        } else {
           uint32_t total = 0;
           for (uint32_t wg = 0; wg < RW; ++wg) total += __popc(differ_word(rowsF, f, RW, wg, m, n, Wp));
           if (total > 0) {
-            const uint4 r = philox4x32_10(make_uint4(sg, sid, generation, kTagGom | 2u), key);
-            uint32_t kth = bounded(lo64(r), total);
+            uint32_t kth = bounded(hi64(r), total);
             for (uint32_t wg = 0; wg < RW; ++wg) {
               const uint32_t dw = differ_word(rowsF, f, RW, wg, m, n, Wp);
               const uint32_t c = __popc(dw);
               if (kth < c) {
                 const uint32_t b = select_bit(dw, kth);
-                d = (int32_t)((wg / Wp) * n + (wg % Wp) * 32u + b);
+                d = (int32_t)((wg >> lwp) * n + (wg & (Wp - 1u)) * 32u + b);
                 x = patt[wg * 32u + b];
                 break;
               }
@@ -148,6 +144,7 @@ __device__ __forceinline__ void gom_general_set(
     if (lane + 32u < f) newD[(lane + 32u) * Wp + w] = mine2;
   }
   team_sync(tw, teams_per_cta, team);
+  probe(a.exp_flags, 4);
 
   // phase 2: footprint sums, ascending edge id (engine_parallel.hpp:164-173)
   int32_t di[WPT];
@@ -226,6 +223,7 @@ __device__ __forceinline__ void gom_general_set(
   const uint32_t fpl = e1 - e0;
 
   // phases 3 + 4
+  probe(a.exp_flags, 5);
 #pragma unroll
   for (int j = 0; j < WPT; ++j) {
     const uint32_t w = wit + tw * j;
@@ -269,12 +267,14 @@ __device__ __forceinline__ void gom_general_set(
     }
   }
   team_sync(tw, teams_per_cta, team);
+  probe(a.exp_flags, 6);
   for (uint32_t idx = tid_team; idx < f * Wp; idx += team_threads) {
     const uint32_t jv = idx / Wp, w = idx - jv * Wp;
     const uint32_t nw = newF[idx];
     if (nw != rowsF[jv * RW + own + w]) a.pop[(size_t)vars[jv] * Wp + w] = nw;
   }
   team_sync(tw, teams_per_cta, team);
+  probe(a.exp_flags, 7);
 }
 
 }  // namespace gomix_b200

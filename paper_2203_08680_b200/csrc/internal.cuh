@@ -206,6 +206,7 @@ struct OrderArgs {
 // Persistent generation kernel (gom_gen.cu)
 constexpr uint32_t kGenMaxN = 256;  // members kept in shared memory by every CTA
 constexpr uint32_t kGenMaxK = 256;  // colour groups
+constexpr uint32_t kAccStride = 32;  // persistent kernel accumulators: one per 256-byte line
 struct BeginArgs;
 struct GenArgs {
   const BeginArgs* begin;
@@ -314,6 +315,9 @@ void launch_ims_collect(const SnapArgs& a, ImsBestDev* b, uint32_t* bits, int ex
 void launch_ims_offer(const SnapArgs& a, ImsBestDev* b, const uint32_t* bits, int exact, cudaStream_t s);
 void launch_count_ones(const uint32_t* pop, uint64_t nv, uint32_t Wp, uint32_t* ones, cudaStream_t s);
 void launch_sum_ones(const uint32_t* stage, uint32_t R, uint64_t nv, uint32_t* ones, cudaStream_t s);
+void debug_probes(unsigned long long* out, bool reset);
+void debug_probes_gen(unsigned long long* out, bool reset);
+void debug_cta_probes(unsigned long long* out);
 void launch_philox_init(uint32_t* pop, uint64_t nv, uint32_t n, uint32_t Wp, uint64_t seed,
                         uint32_t rank, cudaStream_t s);
 void launch_full_eval(const Problem& P, const uint32_t* pop, double* fit, uint32_t n,
