@@ -439,9 +439,7 @@ struct gomix_gpu_engine {
       // Wp warps per set, for parallelism; otherwise a warp per set with every
       // word in registers.
       const uint64_t avg_group = (P->m + P->k - 1) / P->k;
-      const char* knob = std::getenv("GOMIX_WARP_TEAMS");  // experiment knob: 1 = always one warp per set
-      const bool force_warp = knob && knob[0] == '1';
-      if (Wp > 1 && avg_group * Wp <= (uint64_t)sms * 32 && !force_warp) {
+      if (Wp > 1 && avg_group * Wp <= (uint64_t)sms * 32) {
         wpt = 1;
         tw = Wp;
         block = 32 * tw;  // one team per CTA: the whole group fits in one wave

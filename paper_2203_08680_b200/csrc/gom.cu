@@ -313,7 +313,6 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
   unsigned long long calls = 0;
 
   for (uint32_t p = blockIdx.x * teams_per_cta + team; p < G; p += gridDim.x * teams_per_cta) {
-    if (a.exp_flags & 8) break;
     if constexpr (UNIV) {
       // ---- univariate set {v}: a donor differing on v holds !x_v, so the
       // pair is present iff some member holds the other value and the move
@@ -510,9 +509,9 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
       if (s < n) {
         if (float_parts)
           a.part[(size_t)blockIdx.x * n + s] = (double)acc[j];
-        else if (a.dfit && acc[j] != 0 && !(a.exp_flags & 2))
+        else if (a.dfit && acc[j] != 0)
           atomicAdd(&a.dfit[s], (double)acc[j]);
-        if ((dh1[j] | dh2[j]) && !(a.exp_flags & 2)) {
+        if (dh1[j] | dh2[j]) {
           atomicXor(&a.dh1[s], dh1[j]);
           atomicXor(&a.dh2[s], dh2[j]);
         }
@@ -520,7 +519,7 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0 && (s_steps | s_calls) && !(a.exp_flags & 4)) {
+  if (threadIdx.x == 0 && (s_steps | s_calls)) {
     atomicAdd(&a.ctl->grp_steps, s_steps);
     atomicAdd(&a.ctl->grp_calls, s_calls);
   }
@@ -552,13 +551,13 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
   }
   if (threadIdx.x == 0) {
     // last-party ticket: everything above is visible to the last one
-    if (!(a.exp_flags & 1)) __threadfence();
+    __threadfence();
     s_last = atomicAdd(&a.ctl->done, 1u) == parties - 1;
   }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  if (!(a.exp_flags & 16)) epilogue_body(epi);
+  epilogue_body(epi);
   if (threadIdx.x == 0) a.ctl->done = 0;
 }
 

@@ -183,7 +183,7 @@ struct GomArgs {
   uint64_t seed;
   EpiArgs epi;         // run by the last CTA
   int32_t slot;                 // >= 0: group = order[slot] (graph path)
-  uint32_t exp_flags;           // timing experiments only (GOMIX_EXP env): 1 no fence, 2 no fitness/hash atomics, 4 no counter atomics
+  uint32_t exp_flags;           // latency studies only (GOMIX_EXP env): 32 = %globaltimer probes
   const uint32_t* order;
   const GroupDesc* groups;
 };
