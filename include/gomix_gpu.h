@@ -303,6 +303,21 @@ GOMIX_API int gomix_generate_torus(uint64_t width, uint64_t height, int32_t weig
 GOMIX_API int gomix_generate_regular(uint64_t num_vertices, uint32_t degree, int32_t weight_kind, int64_t lo,
                            int64_t hi, uint64_t seed, uint32_t* eu, uint32_t* ev, double* ew);
 
+/* ---- linkage model (host only) -------------------------------------------------- */
+
+/* build_fixed_model's FOS (model.hpp:31-52): learn_tree_upgma (linkage.hpp:
+ * 133-264) over vig_similarity (weighted = 0: 1 per edge) or weight_similarity
+ * (weighted != 0: |w| per edge), size bound `bound` (0 = unbounded FLT),
+ * computed without the n x n matrix (sparse similarity, O((n+q) log n)).
+ * Same sets in the same order as the reference: singletons in variable
+ * order, then merged sets in merge order, the full set never emitted.
+ * With set_offset or set_vars NULL only num_sets and total_vars are returned;
+ * otherwise set_offset holds num_sets + 1 entries and set_vars total_vars. */
+GOMIX_API int gomix_fos_bounded_flt(uint64_t num_vertices, uint64_t num_edges, const uint32_t* edge_u,
+                                    const uint32_t* edge_v, const double* edge_w, uint64_t bound,
+                                    int32_t weighted, uint64_t* num_sets, uint64_t* total_vars,
+                                    uint64_t* set_offset, uint32_t* set_vars);
+
 /* ---- misc ------------------------------------------------------------------- */
 
 /* Standalone GPU colouring (the color-stats path, gomix_main.cpp:319-351). */

@@ -113,6 +113,8 @@ _SIGNATURES = {
     "gomix_gpu_local_group_init_population": ([_P, C.POINTER(StopCriteria), C.POINTER(RunStats)], C.c_int),
     "gomix_gpu_local_group_run_generation": ([_P, C.POINTER(StopCriteria), C.POINTER(RunStats)], C.c_int),
     "gomix_gpu_local_group_read_elitist": ([_P, _P, C.POINTER(C.c_double)], C.c_int),
+    "gomix_fos_bounded_flt": ([C.c_uint64, C.c_uint64, _P, _P, _P, C.c_uint64, C.c_int32, C.POINTER(C.c_uint64),
+                               C.POINTER(C.c_uint64), _P, _P], C.c_int),
     "gomix_generate_torus": ([C.c_uint64, C.c_uint64, C.c_int32, C.c_int64, C.c_int64, C.c_uint64,
                               _P, _P, _P], C.c_int),
     "gomix_generate_regular": ([C.c_uint64, C.c_uint32, C.c_int32, C.c_int64, C.c_int64, C.c_uint64,

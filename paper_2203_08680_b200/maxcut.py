@@ -10,6 +10,9 @@ from __future__ import annotations
 import math
 from dataclasses import dataclass
 
+import ctypes as C
+from typing import Optional
+
 import numpy as np
 
 from . import _capi
@@ -163,6 +166,27 @@ def univariate_fos(num_variables: int) -> Fos:
     """Singletons in variable order (the CLI's `univariate` = bound 1)."""
     return Fos(num_variables, np.arange(num_variables + 1, dtype=np.uint64),
                np.arange(num_variables, dtype=np.uint32))
+
+
+def bounded_flt_fos(inst: MaxCutInstance, bound: Optional[int] = None, weighted: bool = False) -> Fos:
+    """The reference's fixed linkage tree (build_fixed_model, model.hpp:31-52):
+    UPGMA over the VIG similarity (or |w| with weighted=True), merged sets of
+    at most `bound` variables (None: unbounded FLT).  Computed on sparse
+    similarities (no n x n matrix), same sets in the same order."""
+    if bound is not None and bound <= 0:
+        raise ValueError("linkage: size bound must be positive")
+    L = _capi.lib()
+    eu = np.ascontiguousarray(inst.edge_u, np.uint32)
+    ev = np.ascontiguousarray(inst.edge_v, np.uint32)
+    ew = np.ascontiguousarray(inst.edge_w, np.float64)
+    m, tv = C.c_uint64(), C.c_uint64()
+    args = (inst.num_vertices, inst.num_edges, eu.ctypes.data, ev.ctypes.data, ew.ctypes.data, bound or 0,
+            int(weighted))
+    _capi.check(L.gomix_fos_bounded_flt(*args, C.byref(m), C.byref(tv), None, None))
+    off = np.zeros(m.value + 1, np.uint64)
+    vars_ = np.zeros(tv.value, np.uint32)
+    _capi.check(L.gomix_fos_bounded_flt(*args, C.byref(m), C.byref(tv), off.ctypes.data, vars_.ctypes.data))
+    return Fos(inst.num_vertices, off, vars_)
 
 
 def neighbourhood_fos(inst: MaxCutInstance) -> Fos:

@@ -44,6 +44,14 @@ COLOR_CASES = [
     ("col_torus40_bflt10", ["--torus", 40, 40, "--weights", "unit"], "bflt:10"),
     ("col_reg8", ["@reg", 200, 8, 31], "univariate"),
     ("col_reg5odd", ["@reg", 64, 5, 32], "neigh"),
+    # bounded / unbounded FLT (build_fixed_model over vig_similarity): pins
+    # the sparse UPGMA of csrc/linkage.cu
+    ("col_torus10_bflt3", ["--torus", 10, 10, "--weights", "unit"], "bflt:3"),
+    ("col_torus10_bflt7", ["--torus", 10, 10, "--weights", "int:1:10"], "bflt:7"),
+    ("col_reg64_bflt6", ["@reg", 64, 5, 33], "bflt:6"),
+    ("col_reg50_bflt2", ["@reg", 50, 3, 34], "bflt:2"),
+    ("col_torus7x5_flt", ["--torus", 7, 5, "--weights", "unit"], "flt"),
+    ("col_torus12x9_bflt16", ["--torus", 12, 9, "--weights", "unit"], "bflt:16"),
 ]
 
 
