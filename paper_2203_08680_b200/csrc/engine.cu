@@ -320,6 +320,7 @@ struct gomix_gpu_engine {
   uint32_t* ones_local = nullptr;  // [nv] this rank
   uint32_t* ones_stage = nullptr;  // [R][nv] (in-process shards)
   bool gen_ok = false;     // Philox generations run as one persistent kernel (gom_gen.cu)
+  bool gen_lean = false;   // ... with one warp per (set, population word)
   int gen_grid = 0;
   long long* gen_dfit = nullptr;
   unsigned long long* gen_dh = nullptr;
@@ -501,8 +502,13 @@ struct gomix_gpu_engine {
       max_group = std::max(max_group, P->group_off[c + 1] - P->group_off[c]);
     if (mode == GOMIX_MODE_PHILOX && P->i32 && !P->univariate && R == 1 && n <= kGenMaxN && P->k <= kGenMaxK &&
         !(flags & GOMIX_FLAG_RECORD_BATCH) && !(flags & GOMIX_FLAG_PER_GROUP_KERNELS)) {
-      const int per = gen_kernel_max_blocks((int)wpt, tw > 1, (int)block, smem);
-      const uint64_t want = std::max<uint64_t>(1, (max_group + teams - 1) / teams);
+      // lean layout (one warp per set and population word, gom_lean.cuh) for sets of <= 32 variables
+      gen_lean = P->max_f <= 32 && !(flags & GOMIX_FLAG_LANE_PER_SOLUTION);
+      const int gblock = gen_lean ? 256 : (int)block;
+      const size_t gsmem = gen_lean ? (size_t)gen_lean_smem() : smem;
+      const int per = gen_kernel_max_blocks((int)wpt, tw > 1, gblock, gsmem, gen_lean);
+      const uint64_t want = gen_lean ? std::max<uint64_t>(1, (max_group * Wp + 7) / 8)
+                                     : std::max<uint64_t>(1, (max_group + teams - 1) / teams);
       if (per >= 1) {
         gen_grid = (int)std::min<uint64_t>(want, (uint64_t)per * sms);
         gen_ok = true;
@@ -632,7 +638,8 @@ struct gomix_gpu_engine {
       e1 = take_event();
       GOMIX_CUDA(cudaEventRecord(e0, stream));
     }
-    launch_generation_kernel(a, ga, (int)wpt, tw > 1, gen_grid, (int)block, smem, stream);
+    launch_generation_kernel(a, ga, (int)wpt, tw > 1, gen_grid, gen_lean ? 256 : (int)block,
+                             gen_lean ? (size_t)gen_lean_smem() : smem, stream, gen_lean);
     ++launches;
     if (e1) {
       GOMIX_CUDA(cudaEventRecord(e1, stream));

@@ -29,6 +29,7 @@
 #include <stdint.h>
 
 #include "gom_general.cuh"
+#include "gom_lean.cuh"
 
 namespace gomix_b200 {
 
@@ -81,8 +82,10 @@ __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nbl
 // capped for that: 2-warp teams (n <= 64) at 11 CTAs per SM = 1,628 teams.
 constexpr int gen_min_blocks(bool team, int tw) { return team ? (tw == 2 ? 11 : (tw == 4 ? 5 : 2)) : 2; }
 
-template <int WPT, bool TEAM, int TW>
-__global__ void __launch_bounds__(TEAM ? 32 * TW : 256, gen_min_blocks(TEAM, TW))
+// LEAN: every warp owns one population word of the sets it processes
+// (gom_lean_unit, |F| <= 32); otherwise teams run gom_general_set.
+template <int WPT, bool TEAM, int TW, bool LEAN>
+__global__ void __launch_bounds__(LEAN ? 256 : (TEAM ? 32 * TW : 256), LEAN ? 3 : gen_min_blocks(TEAM, TW))
     gom_generation_kernel(const GomArgs a, const GenArgs ga) {
   extern __shared__ __align__(16) uint32_t smem[];
   __shared__ double s_fit[kGenMaxN];
@@ -104,6 +107,10 @@ __global__ void __launch_bounds__(TEAM ? 32 * TW : 256, gen_min_blocks(TEAM, TW)
   const uint32_t tid_team = wit * 32u + lane, team_threads = tw * 32u;
   const uint32_t Wp = a.Wp, n = a.n;
   uint32_t* stage = smem + (size_t)team * a.stage_words;
+  const uint32_t gwarp = blockIdx.x * (blockDim.x >> 5) + warp;
+  const uint32_t lean_w = LEAN ? gwarp % Wp : 0u;  // the grid's warp count is a multiple of Wp
+  // solution of this thread's word j
+  auto sol = [&](int j) -> uint32_t { return LEAN ? lean_w * 32u + lane : (wit + tw * (uint32_t)j) * 32u + lane; };
   const BeginArgs b = *ga.begin;
   DevCtl* c = a.ctl;
   const uint32_t gen = *(volatile unsigned int*)&c->gen_counter;
@@ -161,7 +168,7 @@ __global__ void __launch_bounds__(TEAM ? 32 * TW : 256, gen_min_blocks(TEAM, TW)
     unsigned long long dh1[WPT], dh2[WPT];
 #pragma unroll
     for (int j = 0; j < WPT; ++j) {
-      const uint32_t s = (wit + tw * (uint32_t)j) * 32u + lane;
+      const uint32_t s = sol(j);
       is_elit[j] = s < n && s_h1[s] == eh1 && s_h2[s] == eh2;
       pfit[j] = 0.0;
       acc[j] = 0;
@@ -170,10 +177,18 @@ __global__ void __launch_bounds__(TEAM ? 32 * TW : 256, gen_min_blocks(TEAM, TW)
     }
     uint32_t steps = 0;
     unsigned long long calls = 0;
-    for (uint32_t p = blockIdx.x * teams_per_cta + team; p < d.G; p += gridDim.x * teams_per_cta)
-      gom_general_set<WPT, true, TEAM>(a, p, gmeta, gen, stage, lane, tw, wit, tid_team, team_threads,
-                                       teams_per_cta, team, true, false, false, is_elit, pfit, esrc, ever_cur,
-                                       acc, dh1, dh2, steps, calls);
+    if constexpr (LEAN) {
+      uint32_t* wsm = smem + (size_t)warp * kLeanSmemWords;
+      const uint32_t per_round = (gridDim.x * (blockDim.x >> 5)) / Wp;
+      for (uint32_t p = gwarp / Wp; p < d.G; p += per_round)
+        gom_lean_unit(a, p, gmeta, lean_w, gen, wsm, lane, is_elit[0], esrc, ever_cur, false, acc[0], dh1[0],
+                      dh2[0], steps, calls);
+    } else {
+      for (uint32_t p = blockIdx.x * teams_per_cta + team; p < d.G; p += gridDim.x * teams_per_cta)
+        gom_general_set<WPT, true, TEAM>(a, p, gmeta, gen, stage, lane, tw, wit, tid_team, team_threads,
+                                         teams_per_cta, team, true, false, false, is_elit, pfit, esrc, ever_cur,
+                                         acc, dh1, dh2, steps, calls);
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
       s_steps = 0;
@@ -192,7 +207,7 @@ __global__ void __launch_bounds__(TEAM ? 32 * TW : 256, gen_min_blocks(TEAM, TW)
     }
 #pragma unroll
     for (int j = 0; j < WPT; ++j) {
-      const uint32_t s = (wit + tw * (uint32_t)j) * 32u + lane;
+      const uint32_t s = sol(j);
       if (s < n) {
         if (acc[j]) atomicAdd(reinterpret_cast<unsigned long long*>(D + s * kAccStride), (unsigned long long)acc[j]);
         if (dh1[j] | dh2[j]) {
@@ -341,20 +356,21 @@ __global__ void __launch_bounds__(TEAM ? 32 * TW : 256, gen_min_blocks(TEAM, TW)
 // launchers
 // ---------------------------------------------------------------------------
 namespace {
-void* gen_kernel(int wpt, bool team, int tw) {
+void* gen_kernel(int wpt, bool team, int tw, bool lean) {
+  if (lean) return (void*)gom_generation_kernel<1, false, 1, true>;
   if (team) {
     if (wpt != 1) return nullptr;
     switch (tw) {
-      case 2: return (void*)gom_generation_kernel<1, true, 2>;
-      case 4: return (void*)gom_generation_kernel<1, true, 4>;
-      case 8: return (void*)gom_generation_kernel<1, true, 8>;
+      case 2: return (void*)gom_generation_kernel<1, true, 2, false>;
+      case 4: return (void*)gom_generation_kernel<1, true, 4, false>;
+      case 8: return (void*)gom_generation_kernel<1, true, 8, false>;
     }
   } else {
     switch (wpt) {
-      case 1: return (void*)gom_generation_kernel<1, false, 1>;
-      case 2: return (void*)gom_generation_kernel<2, false, 1>;
-      case 4: return (void*)gom_generation_kernel<4, false, 1>;
-      case 8: return (void*)gom_generation_kernel<8, false, 1>;
+      case 1: return (void*)gom_generation_kernel<1, false, 1, false>;
+      case 2: return (void*)gom_generation_kernel<2, false, 1, false>;
+      case 4: return (void*)gom_generation_kernel<4, false, 1, false>;
+      case 8: return (void*)gom_generation_kernel<8, false, 1, false>;
     }
   }
   return nullptr;
@@ -375,8 +391,10 @@ void debug_probes_gen(unsigned long long* out, bool reset) {
   }
 }
 
-int gen_kernel_max_blocks(int wpt, bool team, int block, size_t smem) {
-  void* fn = gen_kernel(wpt, team, team ? block / 32 : 1);
+int gen_lean_smem() { return 8 * (int)kLeanSmemWords * 4; }
+
+int gen_kernel_max_blocks(int wpt, bool team, int block, size_t smem, bool lean) {
+  void* fn = gen_kernel(wpt, team, team ? block / 32 : 1, lean);
   if (!fn) return 0;
   GOMIX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int blocks = 0;
@@ -385,8 +403,8 @@ int gen_kernel_max_blocks(int wpt, bool team, int block, size_t smem) {
 }
 
 void launch_generation_kernel(const GomArgs& a, const GenArgs& ga, int wpt, bool team, int grid, int block,
-                              size_t smem, cudaStream_t s) {
-  void* fn = gen_kernel(wpt, team, team ? block / 32 : 1);
+                              size_t smem, cudaStream_t s, bool lean) {
+  void* fn = gen_kernel(wpt, team, team ? block / 32 : 1, lean);
   void* args[] = {(void*)&a, (void*)&ga};
   GOMIX_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(block), args, smem, s));
 }

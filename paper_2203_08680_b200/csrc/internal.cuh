@@ -293,9 +293,10 @@ class ReplayStream {
 void launch_gom(const GomArgs& a, bool univariate, bool i32, int wpt, bool team, int grid, int block,
                 size_t smem, cudaStream_t s);
 // persistent generation kernel (gom_gen.cu)
-int gen_kernel_max_blocks(int wpt, bool team, int block, size_t smem);
+int gen_kernel_max_blocks(int wpt, bool team, int block, size_t smem, bool lean);
+int gen_lean_smem();  // dynamic shared memory of a lean launch (8 warps)
 void launch_generation_kernel(const GomArgs& a, const GenArgs& ga, int wpt, bool team, int grid, int block,
-                              size_t smem, cudaStream_t s);
+                              size_t smem, cudaStream_t s, bool lean);
 // bit-sliced univariate kernel (gom_univ.cu)
 int univ_sliced_planes(uint64_t max_abs_row_sum);  // 0: not representable
 int univ_sliced_block();
