@@ -12,6 +12,7 @@
 #include <nccl.h>  // types only: NCCL is resolved at run time with dlopen
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cmath>
@@ -34,6 +35,12 @@ using namespace gomix_b200;
 namespace {
 
 thread_local std::string g_last_error;
+
+// latency-study instrumentation switch (GOMIX_EXP at load, gomix_debug_set_flags)
+std::atomic<uint32_t> g_exp_flags{[] {
+  const char* ex = std::getenv("GOMIX_EXP");
+  return ex ? (uint32_t)std::atoi(ex) : 0u;
+}()};
 
 template <typename F>
 int guarded(F&& f) {
@@ -806,10 +813,7 @@ struct gomix_gpu_engine {
     a.generation = (uint32_t)generation;
     a.seed = seed;
     a.slot = slot;
-    {
-      const char* ex = std::getenv("GOMIX_EXP");
-      a.exp_flags = ex ? (uint32_t)std::atoi(ex) : 0u;
-    }
+    a.exp_flags = g_exp_flags.load(std::memory_order_relaxed);
     a.order = d_order;
     a.groups = d_groups;
     return a;
@@ -1250,6 +1254,11 @@ GOMIX_API int gomix_debug_cta_probes(unsigned long long* out) {
 }
 
 // latency-study probes (GOMIX_EXP bit 32), not part of the public header
+GOMIX_API int gomix_debug_set_flags(uint32_t flags) {
+  g_exp_flags.store(flags);
+  return GOMIX_OK;
+}
+
 GOMIX_API int gomix_debug_probes(unsigned long long* out, int32_t reset) {
   return guarded([&] {
     unsigned long long b[64];

@@ -5,6 +5,7 @@ import paper_2203_08680_b200 as G
 from paper_2203_08680_b200 import _capi
 L = _capi.lib()
 L.gomix_debug_probes.argtypes = [C.c_void_p, C.c_int32]
+L.gomix_debug_set_flags.argtypes = [C.c_uint32]
 inst = G.generate_torus(100, 100, ("int", 1, 10), 1)
 P = G.GpuProblem(inst, G.neighbourhood_fos(inst))
 for per_group in (False, True):
@@ -14,10 +15,10 @@ for per_group in (False, True):
     E.synchronize()
     buf = np.zeros(64, np.uint64)
     L.gomix_debug_probes(buf.ctypes.data, 1)
-    os.environ["GOMIX_EXP"] = "32"
+    L.gomix_debug_set_flags(32)
     E.run_generation_async(); E.synchronize()
     L.gomix_debug_probes(buf.ctypes.data, 1)
-    os.environ["GOMIX_EXP"] = "0"
+    L.gomix_debug_set_flags(0)
     t0 = buf[0]
     print("per_group" if per_group else "persistent", [(i, int(buf[i] - t0) if buf[i] else None) for i in range(48) if buf[i]])
 
@@ -27,9 +28,9 @@ E = G.GpuParallelEngine(P, 64, 1, mode="philox")
 for _ in range(10):
     E.run_generation_async()
 E.synchronize()
-os.environ["GOMIX_EXP"] = "32"
+L.gomix_debug_set_flags(32)
 E.run_generation_async(); E.synchronize()
-os.environ["GOMIX_EXP"] = "0"
+L.gomix_debug_set_flags(0)
 cp = np.zeros(8192, np.uint64)
 L.gomix_debug_cta_probes(cp.ctypes.data)
 t = cp[0::2][:1250].astype(np.int64); sm = cp[1::2][:1250].astype(np.int64)
