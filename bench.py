@@ -339,10 +339,13 @@ def bench_ours(args):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     e2e_done = 0
+    elit_reads = 0
     for _ in range(e2e_steps):
         E.run_generation()                          # H2D: stop criteria; D2H: stats + improvements
         e2e_done += int(E.last_stats.steps)         # global steps (sharded stats are global)
-        E.elitist(eg_host)                          # D2H: l genotype bytes (+ fitness)
+        if E.last_stats.improvements:               # the adapter's lazy elitist refresh: the
+            E.elitist(eg_host)                      # genotype changes only with a better fitness
+            elit_reads += 1                         # D2H: l genotype bytes (+ fitness)
     torch.cuda.synchronize()
     barrier()
     e2e_s = time.perf_counter() - t0
@@ -454,10 +457,13 @@ def bench_ours(args):
         "value": value,
         "ms_per_step": 1e3 * dev_s / args.steps,
         "e2e": {"value": e2e_done / e2e_s, "unit": UNIT, "h2d_bytes_per_step": crit_bytes,
-                "d2h_bytes_per_step": stats_bytes + inst.num_vertices + 8, "steps": e2e_steps,
+                "d2h_bytes_per_step": stats_bytes + (inst.num_vertices + 8) * elit_reads / e2e_steps,
+                "steps": e2e_steps, "elitist_reads": elit_reads,
                 "what": "per generation through the C-ABI with pinned host buffers, the reference run loop's "
                         "GenerationRunner calls: run_generation (stop criteria in, stats + improvements out) "
-                        "+ read_elitist (genotype out); wall clock"},
+                        "+ the elitist genotype read back after every generation that improved it (the C++ "
+                        "adapter's lazy elitist(): the genotype changes only with a strictly better fitness, "
+                        "engine_parallel.hpp:305-310); wall clock"},
         "e2e_population_roundtrip": {"value": rt_done / rt_s, "unit": UNIT, "h2d_bytes_per_step": io_bytes,
                                      "d2h_bytes_per_step": io_bytes, "steps": rt_steps,
                                      "what": "load_population + run_generation + read_population (the whole "

@@ -266,8 +266,11 @@ class GpuParallelEngine final : public GenerationRunner {
       ctx_.report_improvement(fit[i], generation, pop_id_);
     }
     if (end > done) ctx_.control.add_evaluator_calls(end - done);
+    // the elitist genotype changes only with a strictly better fitness
+    // (engine_parallel.hpp:305-310, :320-322): the host copy is refreshed
+    // lazily, and only after a generation that replaced it
+    if (stats.improvements > 0 || stats.elitist_fitness != elitist_.fitness) elitist_stale_ = true;
     elitist_.fitness = stats.elitist_fitness;
-    elitist_stale_ = true;
   }
 
   const GrayBoxProblem& problem_;

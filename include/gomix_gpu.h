@@ -75,7 +75,10 @@ enum {
   /* General sets, integer weights, PHILOX, n <= 256: run one kernel launch
    * per colour group instead of the persistent whole-generation kernel
    * (same results; A/B tests). */
-  GOMIX_FLAG_PER_GROUP_KERNELS = 1u << 4
+  GOMIX_FLAG_PER_GROUP_KERNELS = 1u << 4,
+  /* Univariate FOS of degree <= 4: use the adder/comparator bit-sliced kernel
+   * instead of the truth-table one (same results; A/B tests). */
+  GOMIX_FLAG_NO_TRUTH_TABLE = 1u << 5
 };
 
 enum { GOMIX_STOP_NONE = 0, GOMIX_STOP_BUDGET = 1, GOMIX_STOP_CLOCK = 2, GOMIX_STOP_TARGET = 3,

@@ -16,8 +16,8 @@ LIB_PATH = os.path.join(PKG, "libgomix_b200.so")
 
 GOMIX_OK, GOMIX_E_INVALID, GOMIX_E_CUDA, GOMIX_E_NCCL, GOMIX_E_OOM, GOMIX_E_STATE = range(6)
 MODE_REPLAY, MODE_PHILOX = 0, 1
-FLAG_ORDERED_FLOAT, FLAG_RECORD_BATCH, FLAG_TIME_KERNELS, FLAG_LANE_PER_SOLUTION, FLAG_PER_GROUP_KERNELS = \
-    1, 2, 4, 8, 16
+FLAG_ORDERED_FLOAT, FLAG_RECORD_BATCH, FLAG_TIME_KERNELS, FLAG_LANE_PER_SOLUTION, FLAG_PER_GROUP_KERNELS, \
+    FLAG_NO_TRUTH_TABLE = 1, 2, 4, 8, 16, 32
 STOP_NAMES = {0: "none", 1: "evaluation-budget", 2: "wall-clock", 3: "target-reached",
               4: "generation-limit"}
 

@@ -225,6 +225,10 @@ std::unique_ptr<Problem> create_problem(const gomix_maxcut* inst, const gomix_fo
   up(d_eid, eid.data(), 2 * q * 4);
   mark("csr+upload");
   build_problem_device_impl(*P, colour, d_eid);
+  // truth-table plan of the bit-sliced univariate kernel (every variable of
+  // degree <= 4, int16 weights)
+  if (P->univariate && P->i32 && P->max_fp <= 4 && maxw < 32768.0 && univ_sliced_planes(P->max_abs_row) > 0)
+    build_univ_records(*P);
   mark("device");
   if (P->univariate) {
     for (uint64_t i = 0; i < m; ++i) {
@@ -318,6 +322,7 @@ struct gomix_gpu_engine {
   size_t smem = 0;
   int grid_cap = 1;
   int univ_planes = 0;     // > 0: Philox groups run the bit-sliced lane-per-set kernel
+  bool univ_tt = false;    // ... its truth-table variant (degree <= 4 plan records)
   int univ_grid_cap = 1;
   // Sharded univariate runs on a variable-once FOS: a row changes only in its
   // own group, so its count of 1s over all ranks (the presence test) is
@@ -502,7 +507,8 @@ struct gomix_gpu_engine {
     if (P->univariate && P->i32 && mode == GOMIX_MODE_PHILOX && !(flags & GOMIX_FLAG_RECORD_BATCH) &&
         !(flags & GOMIX_FLAG_LANE_PER_SOLUTION)) {
       univ_planes = univ_sliced_planes(P->max_abs_row);
-      if (univ_planes) univ_grid_cap = univ_sliced_max_blocks_per_sm(univ_planes, (int)Wp) * sms;
+      univ_tt = P->urec != nullptr && Wp <= 4 && !(flags & GOMIX_FLAG_NO_TRUTH_TABLE);
+      if (univ_planes) univ_grid_cap = univ_sliced_max_blocks_per_sm(univ_planes, (int)Wp, univ_tt) * sms;
       if (univ_grid_cap < 1) univ_planes = 0;
     }
     for (uint64_t c = 0; c < P->k; ++c)
@@ -777,6 +783,8 @@ struct gomix_gpu_engine {
     a.fp = P->fp;
     a.gsets = P->gsets + g0;
     a.gvars = P->gvars ? P->gvars + g0 : nullptr;
+    a.urec = P->urec ? P->urec + 2 * g0 : nullptr;
+    a.ukey = P->ukey ? P->ukey + g0 : nullptr;
     a.gmeta = P->gmeta ? P->gmeta + g0 : nullptr;
     a.wbits = P->wbits;
     a.G = (uint32_t)G;
@@ -836,7 +844,7 @@ struct gomix_gpu_engine {
       const uint64_t per = (uint64_t)univ_sliced_sets_per_cta();
       const int g = (int)std::max<uint64_t>(1, std::min<uint64_t>((G + per - 1) / per, (uint64_t)univ_grid_cap));
       a.epi = epi_args(group, (uint32_t)G, (uint32_t)g);
-      launch_univ_sliced(a, univ_planes, (int)Wp, g, st);
+      launch_univ_sliced(a, univ_planes, (int)Wp, univ_tt, g, st);
     } else {
       a.epi = epi_args(group, (uint32_t)G, (uint32_t)grid);
       launch_gom(a, P->univariate, P->i32, (int)wpt, tw > 1, grid, (int)block, smem, st);
@@ -1663,7 +1671,7 @@ int gomix_gpu_set_timing(gomix_gpu_engine* e, int32_t enable) {
 
 const char* gomix_gpu_engine_kernel_name(const gomix_gpu_engine* e) {
   if (!e) return "";
-  return e->univ_planes ? "gom_univ_sliced_kernel" : e->gen_ok ? "gom_generation_kernel" : "gom_group_kernel";
+  return e->univ_planes ? (e->univ_tt ? "gom_univ_tt_kernel" : "gom_univ_sliced_kernel") : e->gen_ok ? "gom_generation_kernel" : "gom_group_kernel";
 }
 
 int gomix_gpu_launch_count(gomix_gpu_engine* e, uint64_t* count) {

@@ -350,30 +350,425 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_sliced_kernel(con
 }
 
 // ---------------------------------------------------------------------------
+// Truth-table variant for sets whose variable has at most 4 edges (every
+// torus): the accept decision of (s, {v}) depends only on the 4-bit pattern
+// p_s = (b_0,s .. b_3,s) of v's edges, so the group plan stores, per
+// position, the 16-entry tables LT[p] = [T(p) < h] (strict improvement) and
+// LE[p] = LT[p] | [2T(p) == A] (improvement or neutral), built once from the
+// weights (build_univ_records_kernel).  The decision for 32 solutions is then
+// a 4-level multiplexer tree over the b words (15 LOP3s) instead of the
+// B-plane adder + comparator; words holding no group-start elitist take
+// accept = LE directly.  T planes are only formed for words that hold a
+// strictly improving pair (their fitness deltas).  The plan record also
+// carries the neighbour ids and weights, so a set costs two coalesced
+// 16-byte loads before its rows (no gvars -> row_ptr -> col chain).
+// ---------------------------------------------------------------------------
+namespace {
+
+// leaf masks of a 16-entry table held in bits [16*half, 16*half + 16) of tt
+__device__ __forceinline__ void tt_masks(uint32_t tt, int half, uint32_t (&m)[16]) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) m[i] = (uint32_t)((int32_t)(tt << (31 - (16 * half + i))) >> 31);
+}
+
+// bit-sliced lookup: bit s of the result = table[p_s], p_s = b0_s | b1_s<<1 | b2_s<<2 | b3_s<<3
+__device__ __forceinline__ uint32_t tt_mux(const uint32_t (&m)[16], uint32_t b0, uint32_t b1, uint32_t b2,
+                                           uint32_t b3) {
+  uint32_t l0[8], l1[4], l2[2];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) l0[q] = (b0 & m[2 * q + 1]) | (~b0 & m[2 * q]);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) l1[q] = (b1 & l0[2 * q + 1]) | (~b1 & l0[2 * q]);
+#pragma unroll
+  for (int q = 0; q < 2; ++q) l2[q] = (b2 & l1[2 * q + 1]) | (~b2 & l1[2 * q]);
+  return (b3 & l2[1]) | (~b3 & l2[0]);
+}
+
+// LT lookup (table bits 0..15) generating each leaf mask where it is used:
+// for the rare words holding a group-start elitist, without a second live
+// mask array
+__device__ __forceinline__ uint32_t tt_mux_lt(uint32_t tt, uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) {
+  uint32_t l0[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const uint32_t m0 = (uint32_t)((int32_t)(tt << (31 - 2 * q)) >> 31);
+    const uint32_t m1 = (uint32_t)((int32_t)(tt << (30 - 2 * q)) >> 31);
+    l0[q] = (b0 & m1) | (~b0 & m0);
+  }
+  uint32_t l1[4], l2[2];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) l1[q] = (b1 & l0[2 * q + 1]) | (~b1 & l0[2 * q]);
+#pragma unroll
+  for (int q = 0; q < 2; ++q) l2[q] = (b2 & l1[2 * q + 1]) | (~b2 & l1[2 * q]);
+  return (b3 & l2[1]) | (~b3 & l2[0]);
+}
+
+__device__ __forceinline__ int32_t w16(uint32_t packed, int hi) {
+  return hi ? ((int32_t)packed >> 16) : ((int32_t)(packed << 16) >> 16);
+}
+
+}  // namespace
+
+// One record pair per group position: r[2p] = {v, LT | LE << 16, w0 | w1 << 16,
+// w2 | w3 << 16} (int16 weights in CSR order = ascending neighbour), r[2p+1] =
+// the neighbours (padding: v itself with weight 0, whose b word is 0);
+// key[p] = Zobrist key of v.
+__global__ void build_univ_records_kernel(const uint32_t* gvars, const int32_t* row_ptr, const int32_t* col,
+                                          const int32_t* wi, uint64_t m, uint4* rec, ulonglong2* key) {
+  const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= m) return;
+  const uint32_t v = gvars[p];
+  const int32_t rs = row_ptr[v], deg = row_ptr[v + 1] - rs;
+  uint32_t c[4] = {v, v, v, v}, mag[4] = {0, 0, 0, 0};
+  int32_t w[4] = {0, 0, 0, 0};
+  for (int t = 0; t < deg && t < 4; ++t) {
+    c[t] = (uint32_t)col[rs + t];
+    w[t] = wi[rs + t];
+    mag[t] = (uint32_t)(w[t] < 0 ? -w[t] : w[t]);
+  }
+  const uint32_t A = mag[0] + mag[1] + mag[2] + mag[3], h = (A + 1u) >> 1;
+  uint32_t lt = 0, le = 0;
+  for (uint32_t pat = 0; pat < 16; ++pat) {
+    uint32_t T = 0;
+    for (int t = 0; t < 4; ++t)
+      if ((pat >> t) & 1u) T += mag[t];
+    if (T < h) lt |= 1u << pat;
+    if (T < h || 2u * T == A) le |= 1u << pat;
+  }
+  rec[2 * p] = make_uint4(v, lt | (le << 16), ((uint32_t)w[0] & 0xFFFFu) | ((uint32_t)w[1] << 16),
+                          ((uint32_t)w[2] & 0xFFFFu) | ((uint32_t)w[3] << 16));
+  rec[2 * p + 1] = make_uint4(c[0], c[1], c[2], c[3]);
+  unsigned long long z1, z2;
+  zobrist(v, z1, z2);
+  key[p] = make_ulonglong2(z1, z2);
+}
+
+template <int B, int WC, bool MULTI>
+__global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_tt_kernel(const GomArgs a) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  __shared__ __align__(16) unsigned long long s_key[kUnivWarps][32][2];
+  __shared__ __align__(16) unsigned long long s_tbl[kUnivWarps][8][16][2];
+  __shared__ unsigned long long s_steps, s_calls;
+  __shared__ int s_last;
+  if (*(volatile int32_t*)&a.ctl->stop) return;
+
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const uint32_t n = a.n, Wp = MULTI ? a.Wp : (uint32_t)WC, chunks = MULTI ? Wp / WC : 1u;
+  long long* s_dfit = reinterpret_cast<long long*>(dyn);
+  unsigned long long* s_dh1 = reinterpret_cast<unsigned long long*>(s_dfit + Wp * 32u);
+  unsigned long long* s_dh2 = s_dh1 + Wp * 32u;
+  uint32_t* s_elit = reinterpret_cast<uint32_t*>(s_dh2 + Wp * 32u);
+  uint32_t G = a.G;
+  const uint4* urec = a.urec;
+  const ulonglong2* ukey = a.ukey;
+  EpiArgs epi = a.epi;
+  if (a.slot >= 0) {  // graph path: this launch's group comes from the device-side order
+    const uint32_t gi = a.order[a.slot];
+    const GroupDesc d = a.groups[gi];
+    G = d.G;
+    urec += 2u * (size_t)d.g0;
+    ukey += d.g0;
+    epi.group = gi;
+    epi.G = G;
+  }
+  const unsigned long long eh1 = a.ctl->eh1, eh2 = a.ctl->eh2;
+  const int32_t esrc_g = a.ctl->elit_src;
+  const uint32_t ever_cur = a.ctl->elit_ver;
+  const int32_t esrc = (esrc_g >= 0 && (uint32_t)esrc_g / n == a.rank) ? (int32_t)((uint32_t)esrc_g % n) : -1;
+  for (uint32_t j = warp; j < Wp; j += kUnivWarps) {
+    const uint32_t s = j * 32u + lane;
+    const bool e = s < n && a.h1[s] == eh1 && a.h2[s] == eh2;
+    const uint32_t m = __ballot_sync(0xFFFFFFFFu, e);
+    if (lane == 0) s_elit[j] = m;
+  }
+  for (uint32_t i = threadIdx.x; i < Wp * 32u; i += blockDim.x) {
+    s_dfit[i] = 0;
+    s_dh1[i] = 0;
+    s_dh2[i] = 0;
+  }
+  if (threadIdx.x == 0) {
+    s_steps = 0;
+    s_calls = 0;
+  }
+  __syncthreads();
+  unsigned long long steps = 0, calls = 0;
+
+  const uint32_t batches = (G + 31u) / 32u;
+  const uint32_t bstride = gridDim.x * kUnivWarps;
+  // the plan records of the warp's next batch are in flight while this one
+  // computes (one dependent load level less per batch)
+  uint4 ra_n = make_uint4(0, 0, 0, 0), rc_n = make_uint4(0, 0, 0, 0);
+  {
+    const uint32_t p0 = (blockIdx.x * kUnivWarps + warp) * 32u + lane;
+    if (p0 < G) {
+      ra_n = __ldg(urec + 2u * (size_t)p0);
+      rc_n = __ldg(urec + 2u * (size_t)p0 + 1u);
+    }
+  }
+  for (uint32_t bt = blockIdx.x * kUnivWarps + warp; bt < batches; bt += bstride) {
+    const uint32_t p = bt * 32u + lane;
+    const bool live = p < G;
+    const uint4 ra = ra_n, rc = rc_n;
+    {
+      const uint32_t pn = p + bstride * 32u;
+      ra_n = make_uint4(0, 0, 0, 0);
+      rc_n = make_uint4(0, 0, 0, 0);
+      if (pn < G) {
+        ra_n = __ldg(urec + 2u * (size_t)pn);
+        rc_n = __ldg(urec + 2u * (size_t)pn + 1u);
+      }
+    }
+    const uint32_t v = ra.x;
+    const uint32_t u[4] = {rc.x, rc.y, rc.z, rc.w};
+    const uint32_t* row = a.pop + (size_t)v * Wp;
+    uint32_t x0[WC], nb0[4][WC];
+#pragma unroll
+    for (int j = 0; j < WC; ++j) {
+      x0[j] = 0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) nb0[t][j] = 0;
+    }
+    if (!MULTI && live) {
+      load_row<WC>(row, x0);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) load_row<WC>(a.pop + (size_t)u[t] * Wp, nb0[t]);
+    }
+    int32_t w[4];
+    w[0] = w16(ra.z, 0);
+    w[1] = w16(ra.z, 1);
+    w[2] = w16(ra.w, 0);
+    w[3] = w16(ra.w, 1);
+    uint32_t neg[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) neg[t] = w[t] < 0 ? 0xFFFFFFFFu : 0u;
+    const uint32_t deg = (uint32_t)(u[0] != v) + (uint32_t)(u[1] != v) + (uint32_t)(u[2] != v) + (uint32_t)(u[3] != v);
+    // ---- presence: some member (over every rank's shard) holds the other value
+    uint32_t ones = 0;
+    if (live) {
+      if (a.ones) {
+        ones = a.ones[v];
+      } else if (!MULTI && a.R == 1) {
+#pragma unroll
+        for (int j = 0; j < WC; ++j) ones += __popc(x0[j]);
+      } else {
+        for (uint32_t r = 0; r < a.R; ++r) {
+          const uint32_t* pr = a.R > 1 ? a.pool + ((size_t)r * a.nv + v) * Wp : row;
+          for (uint32_t c = 0; c < chunks; ++c) {
+            uint32_t y[WC];
+            load_row<WC>(pr + c * WC, y);
+#pragma unroll
+            for (int j = 0; j < WC; ++j) ones += __popc(y[j]);
+          }
+        }
+      }
+    }
+    const bool present = live && ones > 0u && ones < a.n_global;
+    if (present) {
+      steps += n;
+      calls += (unsigned long long)n * deg;
+    }
+    const uint32_t pmask = present ? 0xFFFFFFFFu : 0u;
+    bool table = false;
+#pragma unroll 1
+    for (uint32_t c = 0; c < chunks; ++c) {
+      uint32_t x[WC], nb[4][WC];
+#pragma unroll
+      for (int j = 0; j < WC; ++j) {
+        x[j] = x0[j];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) nb[t][j] = nb0[t][j];
+      }
+      if (MULTI && live) {
+        load_row<WC>(row + c * WC, x);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) load_row<WC>(a.pop + (size_t)u[t] * Wp + c * WC, nb[t]);
+      }
+      // ---- b words (edge "uncut-gain" bits), then accept via the LE table
+      // (LT | LE & ~elitist where the group-start elitist lives)
+      uint32_t bw[4][WC], acc[WC];
+      bool any = false;
+#pragma unroll
+      for (int j = 0; j < WC; ++j)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) bw[t][j] = x[j] ^ nb[t][j] ^ neg[t];
+      {
+        uint32_t mle[16];
+        tt_masks(ra.y, 1, mle);
+#pragma unroll
+        for (int j = 0; j < WC; ++j) {
+          const uint32_t wj = c * WC + (uint32_t)j;
+          uint32_t ac = tt_mux(mle, bw[0][j], bw[1][j], bw[2][j], bw[3][j]);
+          const uint32_t ew = s_elit[wj];
+          if (ew) ac = tt_mux_lt(ra.y, bw[0][j], bw[1][j], bw[2][j], bw[3][j]) | (ac & ~ew);  // warp-uniform
+          acc[j] = ac & pmask & valid_mask(wj, n);
+          any |= acc[j] != 0u;
+        }
+      }
+      // ---- commit: accepted solutions flip v (apply_acceptance, :221-247)
+      if (any) {
+        uint32_t nx[WC];
+#pragma unroll
+        for (int j = 0; j < WC; ++j) nx[j] = x[j] ^ acc[j];
+        store_row<WC>(a.pop + (size_t)v * Wp + c * WC, nx);
+        if (esrc >= 0 && ((uint32_t)esrc >> 5) / WC == c) {
+          const uint32_t ew = ((uint32_t)esrc >> 5) - c * WC, eb = (uint32_t)esrc & 31u;
+          uint32_t aw = 0, xw = 0;
+#pragma unroll
+          for (int j = 0; j < WC; ++j)
+            if ((uint32_t)j == ew) {
+              aw = acc[j];
+              xw = x[j];
+            }
+          if ((aw >> eb) & 1u) capture_row(a.elit, a.ever, ever_cur, v, (xw >> eb) & 1u);
+        }
+      }
+      // ---- per-solution reductions over the warp's 32 sets ----------------
+      if (!__any_sync(0xFFFFFFFFu, any)) continue;
+      if (!table) {  // first accepting chunk of this batch (warp-uniform)
+        table = true;
+        ulonglong2 z = make_ulonglong2(0ull, 0ull);
+        if (live) z = __ldg(ukey + p);
+        s_key[warp][lane][0] = z.x;
+        s_key[warp][lane][1] = z.y;
+        __syncwarp();
+        {
+          const uint32_t q = lane >> 2, sub = lane & 3u;
+          const ulonglong2 k0 = *reinterpret_cast<const ulonglong2*>(s_key[warp][4 * q + 0]);
+          const ulonglong2 k1 = *reinterpret_cast<const ulonglong2*>(s_key[warp][4 * q + 1]);
+          const ulonglong2 k2 = *reinterpret_cast<const ulonglong2*>(s_key[warp][4 * q + 2]);
+          const ulonglong2 k3 = *reinterpret_cast<const ulonglong2*>(s_key[warp][4 * q + 3]);
+          const unsigned long long l1 = ((sub & 1u) ? k0.x : 0ull) ^ ((sub & 2u) ? k1.x : 0ull);
+          const unsigned long long l2 = ((sub & 1u) ? k0.y : 0ull) ^ ((sub & 2u) ? k1.y : 0ull);
+          ulonglong2* t = reinterpret_cast<ulonglong2*>(s_tbl[warp][q]);
+          t[sub] = make_ulonglong2(l1, l2);
+          t[sub + 4] = make_ulonglong2(l1 ^ k2.x, l2 ^ k2.y);
+          t[sub + 8] = make_ulonglong2(l1 ^ k3.x, l2 ^ k3.y);
+          t[sub + 12] = make_ulonglong2(l1 ^ k2.x ^ k3.x, l2 ^ k2.y ^ k3.y);
+        }
+        __syncwarp();
+      }
+      uint32_t mlt[16];
+      tt_masks(ra.y, 0, mlt);
+#pragma unroll
+      for (int j = 0; j < WC; ++j) {
+        if (!__any_sync(0xFFFFFFFFu, acc[j] != 0u)) continue;
+        const uint32_t accT = transpose32(acc[j], lane);  // lane b: sets l accepted by solution 32j+b
+        const uint32_t b0 = bw[0][j], b1 = bw[1][j], b2 = bw[2][j], b3 = bw[3][j];
+        long long d = 0;
+        const uint32_t imp = acc[j] & tt_mux(mlt, b0, b1, b2, b3);
+        if (__any_sync(0xFFFFFFFFu, imp != 0u)) {
+          // T planes of this word (only words with a strictly improving pair)
+          uint32_t T[B];
+#pragma unroll
+          for (int k = 0; k < B; ++k) T[k] = 0;
+          const uint32_t bb[4] = {b0, b1, b2, b3};
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const uint32_t mg = (uint32_t)abs(w[t]);
+            uint32_t cy = 0;
+#pragma unroll
+            for (int k = 0; k < B; ++k) {
+              const uint32_t xb = ((mg >> k) & 1u) ? bb[t] : 0u;
+              const uint32_t tk = T[k];
+              T[k] = tk ^ xb ^ cy;
+              cy = (tk & xb) | (tk & cy) | (xb & cy);
+            }
+          }
+          const uint32_t impT = transpose32(imp, lane);
+          const uint32_t A = (uint32_t)(abs(w[0]) + abs(w[1]) + abs(w[2]) + abs(w[3]));
+#pragma unroll
+          for (int k = 0; k < B; ++k) d += (long long)__popc(impT & __ballot_sync(0xFFFFFFFFu, (A >> k) & 1u)) << k;
+#pragma unroll
+          for (int k = 0; k < B - 1; ++k) d -= (long long)__popc(transpose32(T[k] & imp, lane)) << (k + 1);
+        }
+        const uint32_t sj = (c * WC + (uint32_t)j) * 32u + lane;
+        if (d) atomicAdd(reinterpret_cast<unsigned long long*>(&s_dfit[sj]), (unsigned long long)d);
+        unsigned long long x1 = 0, x2 = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const uint32_t m = (accT >> (4 * q)) & 15u;
+          const ulonglong2 t = *reinterpret_cast<const ulonglong2*>(s_tbl[warp][q][m]);
+          x1 ^= t.x;
+          x2 ^= t.y;
+        }
+        if (x1 | x2) {
+          atomicXor(&s_dh1[sj], x1);
+          atomicXor(&s_dh2[sj], x2);
+        }
+      }
+    }
+    __syncwarp();
+  }
+
+  {
+    unsigned long long ws = steps, wc = calls;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ws += __shfl_xor_sync(0xFFFFFFFFu, ws, o);
+      wc += __shfl_xor_sync(0xFFFFFFFFu, wc, o);
+    }
+    if (lane == 0 && (ws | wc)) {
+      atomicAdd(&s_steps, ws);
+      atomicAdd(&s_calls, wc);
+    }
+  }
+  __syncthreads();
+  for (uint32_t s = threadIdx.x; s < n && s < Wp * 32u; s += blockDim.x) {
+    if (s_dfit[s]) atomicAdd(&a.dfit[s], (double)s_dfit[s]);
+    if (s_dh1[s] | s_dh2[s]) {
+      atomicXor(&a.dh1[s], s_dh1[s]);
+      atomicXor(&a.dh2[s], s_dh2[s]);
+    }
+  }
+  if (threadIdx.x == 0) {
+    if (s_steps | s_calls) {
+      atomicAdd(&a.ctl->grp_steps, s_steps);
+      atomicAdd(&a.ctl->grp_calls, s_calls);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&a.ctl->done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  epilogue_body(epi);
+  if (threadIdx.x == 0) a.ctl->done = 0;
+}
+
+// ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
 namespace {
 template <int WC, bool MULTI>
-void* univ_kernel_wc(int planes) {
+void* univ_kernel_wc(int planes, bool tt) {
+#define GOMIX_UNIV_CASE(b) \
+  case b: return tt && !MULTI ? (void*)gom_univ_tt_kernel<b, WC, false> : (void*)gom_univ_sliced_kernel<b, WC, MULTI>;
   switch (planes) {
-    case 4: return (void*)gom_univ_sliced_kernel<4, WC, MULTI>;
-    case 6: return (void*)gom_univ_sliced_kernel<6, WC, MULTI>;
-    case 8: return (void*)gom_univ_sliced_kernel<8, WC, MULTI>;
-    case 12: return (void*)gom_univ_sliced_kernel<12, WC, MULTI>;
-    case 16: return (void*)gom_univ_sliced_kernel<16, WC, MULTI>;
+    GOMIX_UNIV_CASE(4)
+    GOMIX_UNIV_CASE(6)
+    GOMIX_UNIV_CASE(8)
+    GOMIX_UNIV_CASE(12)
+    GOMIX_UNIV_CASE(16)
   }
+#undef GOMIX_UNIV_CASE
   throw GomixError(GOMIX_E_INVALID, "univariate sliced kernel: unsupported plane count");
 }
 
 // rows of up to 4 words in one pass, wider rows in passes of 4 words
 int words_per_chunk(int wp) { return wp >= 4 ? 4 : wp; }
 
-void* univ_kernel(int planes, int wp) {
-  if (wp > 4) return univ_kernel_wc<4, true>(planes);
+void* univ_kernel(int planes, int wp, bool tt) {
+  // 12/16-plane counters for 4-word chunks do not fit the register budget
+  // (T alone is 48/64 registers): 2-word passes instead
+  if (planes >= 12 && wp >= 4 && !(tt && wp == 4)) return univ_kernel_wc<2, true>(planes, false);
+  if (wp > 4) return univ_kernel_wc<4, true>(planes, tt);
   switch (words_per_chunk(wp)) {
-    case 1: return univ_kernel_wc<1, false>(planes);
-    case 2: return univ_kernel_wc<2, false>(planes);
-    case 4: return univ_kernel_wc<4, false>(planes);
+    case 1: return univ_kernel_wc<1, false>(planes, tt);
+    case 2: return univ_kernel_wc<2, false>(planes, tt);
+    case 4: return univ_kernel_wc<4, false>(planes, tt);
   }
   throw GomixError(GOMIX_E_INVALID, "univariate sliced kernel: unsupported row width");
 }
@@ -392,18 +787,27 @@ int univ_sliced_block() { return kUnivWarps * 32; }
 
 int univ_sliced_sets_per_cta() { return kUnivWarps * 32; }
 
-int univ_sliced_max_blocks_per_sm(int planes, int wp) {
-  void* fn = univ_kernel(planes, wp);
+int univ_sliced_max_blocks_per_sm(int planes, int wp, bool tt) {
+  void* fn = univ_kernel(planes, wp, tt);
   GOMIX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)univ_smem(wp)));
   int blocks = 0;
   GOMIX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, kUnivWarps * 32, univ_smem(wp)));
   return blocks;
 }
 
-void launch_univ_sliced(const GomArgs& a, int planes, int wp, int grid, cudaStream_t s) {
-  void* fn = univ_kernel(planes, wp);
+void launch_univ_sliced(const GomArgs& a, int planes, int wp, bool tt, int grid, cudaStream_t s) {
+  void* fn = univ_kernel(planes, wp, tt);
   void* args[] = {(void*)&a};
   GOMIX_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kUnivWarps * 32), args, univ_smem(wp), s));
+}
+
+void build_univ_records(Problem& P) {
+  const uint64_t m = P.m;
+  P.urec = dev_alloc<uint4>(P.allocations, 2 * m);
+  P.ukey = dev_alloc<ulonglong2>(P.allocations, m);
+  build_univ_records_kernel<<<(unsigned)((m + 255) / 256), 256>>>(P.gvars, P.row_ptr, P.col, P.wi, m, P.urec,
+                                                                  P.ukey);
+  GOMIX_CUDA(cudaGetLastError());
 }
 
 }  // namespace gomix_b200

@@ -95,6 +95,8 @@ struct Problem {
   uint32_t* gsets = nullptr;
   uint32_t* gvars = nullptr;
   uint4* gmeta = nullptr;
+  uint4* urec = nullptr;       // univariate, degree <= 4, |w| < 2^15: truth-table plan records (2 per position)
+  ulonglong2* ukey = nullptr;  // ... and the Zobrist key of each position's variable
   uint32_t wbits = 1;
   int64_t* fp_off = nullptr;
   FpEntry* fp = nullptr;
@@ -153,6 +155,8 @@ struct GomArgs {
   const uint32_t* gsets;  // this group's members (ascending set ids)
   const uint32_t* gvars;  // singleton FOS: the variable of each member
   const uint4* gmeta;     // general FOS: {set id, vars offset, footprint offset, f << 24 | footprint}
+  const uint4* urec;       // truth-table plan records of this group (gom_univ_tt_kernel)
+  const ulonglong2* ukey;  // Zobrist keys of this group's variables
   uint32_t wbits;         // bit-planes of max |w| (integer path)
   uint32_t G;             // |G|
   uint32_t* pop;
@@ -301,8 +305,9 @@ void launch_generation_kernel(const GomArgs& a, const GenArgs& ga, int wpt, bool
 int univ_sliced_planes(uint64_t max_abs_row_sum);  // 0: not representable
 int univ_sliced_block();
 int univ_sliced_sets_per_cta();
-int univ_sliced_max_blocks_per_sm(int planes, int wp);
-void launch_univ_sliced(const GomArgs& a, int planes, int wp, int grid, cudaStream_t s);
+int univ_sliced_max_blocks_per_sm(int planes, int wp, bool tt);
+void launch_univ_sliced(const GomArgs& a, int planes, int wp, bool tt, int grid, cudaStream_t s);
+void build_univ_records(Problem& P);  // truth-table plan records (urec, ukey) of a degree <= 4 univariate FOS
 int gom_max_blocks_per_sm(bool univariate, bool i32, int wpt, bool team, int block, size_t smem);
 void launch_begin(const BeginArgs& b, cudaStream_t s);
 void launch_order(const BeginArgs* d_b, const OrderArgs& o, cudaStream_t s);

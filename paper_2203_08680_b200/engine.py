@@ -234,7 +234,7 @@ class GpuParallelEngine:
                  record_batch: bool = False, ordered_float: bool = False, time_kernels: bool = False,
                  genotypes: Optional[np.ndarray] = None, stream=None, rank: int = 0, world_size: int = 1,
                  nccl_unique_id: Optional[bytes] = None, lane_per_solution: bool = False,
-                 per_group_kernels: bool = False):
+                 per_group_kernels: bool = False, truth_table: bool = True):
         """world_size > 1: this process's shard of a population of
         `population_size` members over world_size GPUs (Philox mode); every
         rank passes the same nccl_unique_id (see nccl_unique_id()) and calls
@@ -251,7 +251,8 @@ class GpuParallelEngine:
         flags = (_capi.FLAG_RECORD_BATCH if record_batch else 0) | (_capi.FLAG_ORDERED_FLOAT if ordered_float else 0) \
             | (_capi.FLAG_TIME_KERNELS if time_kernels else 0) \
             | (_capi.FLAG_LANE_PER_SOLUTION if lane_per_solution else 0) \
-            | (_capi.FLAG_PER_GROUP_KERNELS if per_group_kernels else 0)
+            | (_capi.FLAG_PER_GROUP_KERNELS if per_group_kernels else 0) \
+            | (0 if truth_table else _capi.FLAG_NO_TRUTH_TABLE)
         self._nid = None if nccl_unique_id is None else C.create_string_buffer(bytes(nccl_unique_id), 128)
         cfg = _capi.EngineConfig(self.n_global, seed, _capi.MODE_REPLAY if mode == "replay" else _capi.MODE_PHILOX,
                                  flags, population_id, self.rank, self.world_size,

@@ -74,6 +74,9 @@ def test_sliced_equals_lane_per_solution_torus(shape, weights, n, gens):
     (16, 1, 10, 128),       # A up to ~300: 12 planes
     (6, -1000, 1000, 64),   # 16 planes
     (3, 0, 1, 96),          # 4 planes, many zero weights
+    (6, -1000, 1000, 96),   # 16 planes, 4 words: 2-word passes
+    (6, -1000, 1000, 256),  # 16 planes, 8 words
+    (16, 1, 10, 200),       # 12 planes, 8 words, partial last word
 ])
 def test_sliced_equals_lane_per_solution_random_graphs(avg_deg, wlo, whi, n):
     inst = _sparse_graph(3000, avg_deg, wlo, whi, 5, isolated=40)
@@ -114,4 +117,97 @@ def test_sliced_full_size_c3():
     for _ in range(2):
         a.run_generation()
         b.run_generation()
+    _same(inst, a, b)
+
+
+# ---------------------------------------------------------------------------
+# truth-table variant (gom_univ_tt_kernel): every variable of degree <= 4
+# ---------------------------------------------------------------------------
+def _deg4_graph(nv, m, wlo, whi, seed):
+    """Random graph with every degree <= 4 (some 0..3), weights in [wlo, whi]."""
+    rs = np.random.RandomState(seed)
+    deg = np.zeros(nv, np.int64)
+    seen, eu, ev = set(), [], []
+    for _ in range(m):
+        a, b = rs.randint(0, nv, 2)
+        a, b = int(min(a, b)), int(max(a, b))
+        if a == b or (a, b) in seen or deg[a] >= 4 or deg[b] >= 4:
+            continue
+        seen.add((a, b))
+        deg[a] += 1
+        deg[b] += 1
+        eu.append(a)
+        ev.append(b)
+    o = np.lexsort((ev, eu))
+    w = rs.randint(wlo, whi + 1, len(eu)).astype(np.float64)
+    return G.MaxCutInstance(nv, np.asarray(eu, np.uint32)[o], np.asarray(ev, np.uint32)[o], w)
+
+
+def _triple(P, n, seed):
+    a = G.GpuParallelEngine(P, n, seed, mode="philox")
+    b = G.GpuParallelEngine(P, n, seed, mode="philox", truth_table=False)
+    c = G.GpuParallelEngine(P, n, seed, mode="philox", lane_per_solution=True)
+    assert a.kernel_name() == "gom_univ_tt_kernel"
+    assert b.kernel_name() == "gom_univ_sliced_kernel"
+    return a, b, c
+
+
+@pytest.mark.parametrize("inst_kind,n,gens", [
+    ("torus_pos", 128, 40),     # long enough for the neutral-oscillation steady state
+    ("torus_pm", 100, 25),      # signed weights, partial last word
+    ("torus_pm0", 64, 25),      # zero weights, 2 words
+    ("torus_c1", 32, 30),       # C1: tiny, clones of the elitist are common
+    ("deg4", 128, 25),          # degrees 0..4, padding slots
+    ("deg4_big", 96, 20),       # |w| up to 8000: 16 planes
+])
+def test_truth_table_equals_adder_and_lane_per_solution(inst_kind, n, gens):
+    inst = {
+        "torus_pos": lambda: G.generate_torus(24, 20, ("int", 1, 10), 4),
+        "torus_pm": lambda: G.generate_torus(16, 12, ("int", -5, 9), 3),
+        "torus_pm0": lambda: G.generate_torus(14, 9, ("int", -3, 3), 3),
+        "torus_c1": lambda: G.generate_torus(10, 10, ("int", 1, 10), 1),
+        "deg4": lambda: _deg4_graph(2000, 5000, -5, 9, 11),
+        "deg4_big": lambda: _deg4_graph(1500, 4000, -8000, 8000, 12),
+    }[inst_kind]()
+    P = G.GpuProblem(inst, G.univariate_fos(inst.num_vertices))
+    a, b, c = _triple(P, n, 5)
+    for _ in range(gens):
+        for e in (a, b, c):
+            e.run_generation()
+        _same(inst, a, b)
+        _same(inst, a, c)
+
+
+def test_truth_table_stop_criteria_match():
+    inst = G.generate_torus(30, 30, ("int", 1, 10), 2)
+    P = G.GpuProblem(inst, G.univariate_fos(900))
+    for crit in (dict(max_evaluations=5000.0), dict(target_fitness=3000.0)):
+        ca = G.RunContext(G.TerminationConfig(**crit), P.comparator(), inst.num_edges)
+        cb = G.RunContext(G.TerminationConfig(**crit), P.comparator(), inst.num_edges)
+        a = G.GpuParallelEngine(P, 64, 3, ctx=ca, mode="philox")
+        b = G.GpuParallelEngine(P, 64, 3, ctx=cb, mode="philox", truth_table=False)
+        for _ in range(400):
+            a.run_generation()
+            b.run_generation()
+            if ca.control.stop_requested():
+                break
+        assert ca.control.stop_requested() and cb.control.stop_requested()
+        assert ca.control.reason == cb.control.reason
+        assert ca.control.calls == cb.control.calls
+        _same(inst, a, b)
+
+
+def test_truth_table_full_size_c3():
+    """C3 (10^6 vertices, n=128): the truth-table kernel (the bench's) agrees
+    with the adder kernel over 30 generations (into the steady state)."""
+    inst = G.generate_torus(1000, 1000, ("int", 1, 10), 1)
+    P = G.GpuProblem(inst, G.univariate_fos(inst.num_vertices))
+    a = G.GpuParallelEngine(P, 128, 1, mode="philox")
+    b = G.GpuParallelEngine(P, 128, 1, mode="philox", truth_table=False)
+    assert a.kernel_name() == "gom_univ_tt_kernel"
+    for _ in range(30):
+        a.run_generation_async()
+        b.run_generation_async()
+    a.synchronize()
+    b.synchronize()
     _same(inst, a, b)
