@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libgomix_b200.so")
+LIB_PATH = os.environ.get("GOMIX_LIB") or os.path.join(PKG, "libgomix_b200.so")  # GOMIX_LIB: an alternative in-tree build (A/B experiments)
 
 GOMIX_OK, GOMIX_E_INVALID, GOMIX_E_CUDA, GOMIX_E_NCCL, GOMIX_E_OOM, GOMIX_E_STATE = range(6)
 MODE_REPLAY, MODE_PHILOX = 0, 1

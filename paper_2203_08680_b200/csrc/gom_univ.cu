@@ -64,6 +64,16 @@ __device__ __forceinline__ void store_row(uint32_t* row, const uint32_t (&x)[WP]
 }
 
 constexpr int kUnivWarps = 8;  // warps per CTA
+constexpr uint32_t kSparseKeys = 6;  // hash deltas key by key up to this many accepted sets per solution
+
+// 64-bit XOR into shared memory as two native 32-bit atomics (a 64-bit
+// shared atomic XOR compiles to a compare-and-swap loop)
+__device__ __forceinline__ void xor_shared64(unsigned long long* p, unsigned long long v) {
+  unsigned int* q = reinterpret_cast<unsigned int*>(p);
+  const unsigned int lo = (unsigned int)v, hi = (unsigned int)(v >> 32);
+  if (lo) atomicXor(q, lo);
+  if (hi) atomicXor(q + 1, hi);
+}
 constexpr int kNbChunk = 4;    // neighbour (col, w) pairs fetched per round
 
 }  // namespace
@@ -302,8 +312,8 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_sliced_kernel(con
           x2 ^= t.y;
         }
         if (x1 | x2) {
-          atomicXor(&s_dh1[sj], x1);
-          atomicXor(&s_dh2[sj], x2);
+          xor_shared64(&s_dh1[sj], x1);
+          xor_shared64(&s_dh2[sj], x2);
         }
       }
     }
@@ -498,24 +508,29 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_tt_kernel(const G
   // the plan records of the warp's next batch are in flight while this one
   // computes (one dependent load level less per batch)
   uint4 ra_n = make_uint4(0, 0, 0, 0), rc_n = make_uint4(0, 0, 0, 0);
+  ulonglong2 zk_n = make_ulonglong2(0ull, 0ull);
   {
     const uint32_t p0 = (blockIdx.x * kUnivWarps + warp) * 32u + lane;
     if (p0 < G) {
       ra_n = __ldg(urec + 2u * (size_t)p0);
       rc_n = __ldg(urec + 2u * (size_t)p0 + 1u);
+      zk_n = __ldg(ukey + p0);
     }
   }
   for (uint32_t bt = blockIdx.x * kUnivWarps + warp; bt < batches; bt += bstride) {
     const uint32_t p = bt * 32u + lane;
     const bool live = p < G;
     const uint4 ra = ra_n, rc = rc_n;
+    const ulonglong2 zk = zk_n;
     {
       const uint32_t pn = p + bstride * 32u;
       ra_n = make_uint4(0, 0, 0, 0);
       rc_n = make_uint4(0, 0, 0, 0);
+      zk_n = make_ulonglong2(0ull, 0ull);
       if (pn < G) {
         ra_n = __ldg(urec + 2u * (size_t)pn);
         rc_n = __ldg(urec + 2u * (size_t)pn + 1u);
+        zk_n = __ldg(ukey + pn);
       }
     }
     const uint32_t v = ra.x;
@@ -568,7 +583,7 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_tt_kernel(const G
       calls += (unsigned long long)n * deg;
     }
     const uint32_t pmask = present ? 0xFFFFFFFFu : 0u;
-    bool table = false;
+    bool keys = false, tbl = false;
 #pragma unroll 1
     for (uint32_t c = 0; c < chunks; ++c) {
       uint32_t x[WC], nb[4][WC];
@@ -624,27 +639,10 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_tt_kernel(const G
       }
       // ---- per-solution reductions over the warp's 32 sets ----------------
       if (!__any_sync(0xFFFFFFFFu, any)) continue;
-      if (!table) {  // first accepting chunk of this batch (warp-uniform)
-        table = true;
-        ulonglong2 z = make_ulonglong2(0ull, 0ull);
-        if (live) z = __ldg(ukey + p);
-        s_key[warp][lane][0] = z.x;
-        s_key[warp][lane][1] = z.y;
-        __syncwarp();
-        {
-          const uint32_t q = lane >> 2, sub = lane & 3u;
-          const ulonglong2 k0 = *reinterpret_cast<const ulonglong2*>(s_key[warp][4 * q + 0]);
-          const ulonglong2 k1 = *reinterpret_cast<const ulonglong2*>(s_key[warp][4 * q + 1]);
-          const ulonglong2 k2 = *reinterpret_cast<const ulonglong2*>(s_key[warp][4 * q + 2]);
-          const ulonglong2 k3 = *reinterpret_cast<const ulonglong2*>(s_key[warp][4 * q + 3]);
-          const unsigned long long l1 = ((sub & 1u) ? k0.x : 0ull) ^ ((sub & 2u) ? k1.x : 0ull);
-          const unsigned long long l2 = ((sub & 1u) ? k0.y : 0ull) ^ ((sub & 2u) ? k1.y : 0ull);
-          ulonglong2* t = reinterpret_cast<ulonglong2*>(s_tbl[warp][q]);
-          t[sub] = make_ulonglong2(l1, l2);
-          t[sub + 4] = make_ulonglong2(l1 ^ k2.x, l2 ^ k2.y);
-          t[sub + 8] = make_ulonglong2(l1 ^ k3.x, l2 ^ k3.y);
-          t[sub + 12] = make_ulonglong2(l1 ^ k2.x ^ k3.x, l2 ^ k2.y ^ k3.y);
-        }
+      if (!keys) {  // first accepting chunk of this batch (warp-uniform): the sets' keys
+        keys = true;
+        s_key[warp][lane][0] = zk.x;
+        s_key[warp][lane][1] = zk.y;
         __syncwarp();
       }
       uint32_t mlt[16];
@@ -683,17 +681,48 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_tt_kernel(const G
         }
         const uint32_t sj = (c * WC + (uint32_t)j) * 32u + lane;
         if (d) atomicAdd(reinterpret_cast<unsigned long long*>(&s_dfit[sj]), (unsigned long long)d);
+        // hash delta of solution 32j+lane: XOR of the keys of its accepted
+        // sets — key by key when every solution of the word accepted few
+        // sets (the steady state: neutral flips are sparse), else through the
+        // 4-bit-chunk table of key XORs
         unsigned long long x1 = 0, x2 = 0;
+        if (__reduce_max_sync(0xFFFFFFFFu, (uint32_t)__popc(accT)) <= kSparseKeys) {
+          uint32_t r = accT;
+          while (r) {
+            const uint32_t l = (uint32_t)(__ffs(r) - 1);
+            r &= r - 1u;
+            const ulonglong2 k = *reinterpret_cast<const ulonglong2*>(s_key[warp][l]);
+            x1 ^= k.x;
+            x2 ^= k.y;
+          }
+        } else {
+          if (!tbl) {
+            tbl = true;
+            const uint32_t q = lane >> 2, sub = lane & 3u;
+            const ulonglong2 k0 = *reinterpret_cast<const ulonglong2*>(s_key[warp][4 * q + 0]);
+            const ulonglong2 k1 = *reinterpret_cast<const ulonglong2*>(s_key[warp][4 * q + 1]);
+            const ulonglong2 k2 = *reinterpret_cast<const ulonglong2*>(s_key[warp][4 * q + 2]);
+            const ulonglong2 k3 = *reinterpret_cast<const ulonglong2*>(s_key[warp][4 * q + 3]);
+            const unsigned long long l1 = ((sub & 1u) ? k0.x : 0ull) ^ ((sub & 2u) ? k1.x : 0ull);
+            const unsigned long long l2 = ((sub & 1u) ? k0.y : 0ull) ^ ((sub & 2u) ? k1.y : 0ull);
+            ulonglong2* tb = reinterpret_cast<ulonglong2*>(s_tbl[warp][q]);
+            tb[sub] = make_ulonglong2(l1, l2);
+            tb[sub + 4] = make_ulonglong2(l1 ^ k2.x, l2 ^ k2.y);
+            tb[sub + 8] = make_ulonglong2(l1 ^ k3.x, l2 ^ k3.y);
+            tb[sub + 12] = make_ulonglong2(l1 ^ k2.x ^ k3.x, l2 ^ k2.y ^ k3.y);
+            __syncwarp();
+          }
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const uint32_t m = (accT >> (4 * q)) & 15u;
-          const ulonglong2 t = *reinterpret_cast<const ulonglong2*>(s_tbl[warp][q][m]);
-          x1 ^= t.x;
-          x2 ^= t.y;
+          for (int q = 0; q < 8; ++q) {
+            const uint32_t m = (accT >> (4 * q)) & 15u;
+            const ulonglong2 tq = *reinterpret_cast<const ulonglong2*>(s_tbl[warp][q][m]);
+            x1 ^= tq.x;
+            x2 ^= tq.y;
+          }
         }
         if (x1 | x2) {
-          atomicXor(&s_dh1[sj], x1);
-          atomicXor(&s_dh2[sj], x2);
+          xor_shared64(&s_dh1[sj], x1);
+          xor_shared64(&s_dh2[sj], x2);
         }
       }
     }
