@@ -394,25 +394,6 @@ __device__ __forceinline__ uint32_t tt_mux(const uint32_t (&m)[16], uint32_t b0,
   return (b3 & l2[1]) | (~b3 & l2[0]);
 }
 
-// LT lookup (table bits 0..15) generating each leaf mask where it is used:
-// for the rare words holding a group-start elitist, without a second live
-// mask array
-__device__ __forceinline__ uint32_t tt_mux_lt(uint32_t tt, uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) {
-  uint32_t l0[8];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const uint32_t m0 = (uint32_t)((int32_t)(tt << (31 - 2 * q)) >> 31);
-    const uint32_t m1 = (uint32_t)((int32_t)(tt << (30 - 2 * q)) >> 31);
-    l0[q] = (b0 & m1) | (~b0 & m0);
-  }
-  uint32_t l1[4], l2[2];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) l1[q] = (b1 & l0[2 * q + 1]) | (~b1 & l0[2 * q]);
-#pragma unroll
-  for (int q = 0; q < 2; ++q) l2[q] = (b2 & l1[2 * q + 1]) | (~b2 & l1[2 * q]);
-  return (b3 & l2[1]) | (~b3 & l2[0]);
-}
-
 __device__ __forceinline__ int32_t w16(uint32_t packed, int hi) {
   return hi ? ((int32_t)packed >> 16) : ((int32_t)(packed << 16) >> 16);
 }
@@ -458,6 +439,7 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_tt_kernel(const G
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ __align__(16) unsigned long long s_key[kUnivWarps][32][2];
   __shared__ __align__(16) unsigned long long s_tbl[kUnivWarps][8][16][2];
+  __shared__ __align__(16) ulonglong2 s_wh[kUnivWarps][4 * 32];  // per-warp hash deltas (Wp <= 4)
   __shared__ unsigned long long s_steps, s_calls;
   __shared__ int s_last;
   if (*(volatile int32_t*)&a.ctl->stop) return;
@@ -493,8 +475,8 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_tt_kernel(const G
   }
   for (uint32_t i = threadIdx.x; i < Wp * 32u; i += blockDim.x) {
     s_dfit[i] = 0;
-    s_dh1[i] = 0;
-    s_dh2[i] = 0;
+#pragma unroll
+    for (int q = 0; q < kUnivWarps; ++q) s_wh[q][i] = make_ulonglong2(0ull, 0ull);
   }
   if (threadIdx.x == 0) {
     s_steps = 0;
@@ -510,14 +492,16 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_tt_kernel(const G
   uint4 ra_n = make_uint4(0, 0, 0, 0), rc_n = make_uint4(0, 0, 0, 0);
   ulonglong2 zk_n = make_ulonglong2(0ull, 0ull);
   {
-    const uint32_t p0 = (blockIdx.x * kUnivWarps + warp) * 32u + lane;
+    const uint32_t p0 = (warp * gridDim.x + blockIdx.x) * 32u + lane;
     if (p0 < G) {
       ra_n = __ldg(urec + 2u * (size_t)p0);
       rc_n = __ldg(urec + 2u * (size_t)p0 + 1u);
       zk_n = __ldg(ukey + p0);
     }
   }
-  for (uint32_t bt = blockIdx.x * kUnivWarps + warp; bt < batches; bt += bstride) {
+  // warp-major batch order: the warps that get one batch more than the
+  // others are spread over every CTA (and SM) instead of the first CTAs
+  for (uint32_t bt = warp * gridDim.x + blockIdx.x; bt < batches; bt += bstride) {
     const uint32_t p = bt * 32u + lane;
     const bool live = p < G;
     const uint4 ra = ra_n, rc = rc_n;
@@ -614,7 +598,17 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_tt_kernel(const G
           const uint32_t wj = c * WC + (uint32_t)j;
           uint32_t ac = tt_mux(mle, bw[0][j], bw[1][j], bw[2][j], bw[3][j]);
           const uint32_t ew = s_elit[wj];
-          if (ew) ac = tt_mux_lt(ra.y, bw[0][j], bw[1][j], bw[2][j], bw[3][j]) | (ac & ~ew);  // warp-uniform
+          if (ew) {  // warp-uniform: group-start elitist copies take strict improvements only
+            uint32_t e = ew, keep = 0xFFFFFFFFu;
+            while (e) {
+              const uint32_t b = (uint32_t)(__ffs(e) - 1);
+              e &= e - 1u;
+              const uint32_t pat = ((bw[0][j] >> b) & 1u) | (((bw[1][j] >> b) & 1u) << 1) |
+                                   (((bw[2][j] >> b) & 1u) << 2) | (((bw[3][j] >> b) & 1u) << 3);
+              if (!((ra.y >> pat) & 1u)) keep &= ~(1u << b);  // LT[p] bit of the table
+            }
+            ac &= keep;
+          }
           acc[j] = ac & pmask & valid_mask(wj, n);
           any |= acc[j] != 0u;
         }
@@ -720,9 +714,12 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_tt_kernel(const G
             x2 ^= tq.y;
           }
         }
-        if (x1 | x2) {
-          xor_shared64(&s_dh1[sj], x1);
-          xor_shared64(&s_dh2[sj], x2);
+        if (x1 | x2) {  // the warp's own running hash deltas: no atomics
+          ulonglong2* q = &s_wh[warp][j * 32 + lane];
+          ulonglong2 o = *q;
+          o.x ^= x1;
+          o.y ^= x2;
+          *q = o;
         }
       }
     }
@@ -743,6 +740,14 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_tt_kernel(const G
   }
   __syncthreads();
   for (uint32_t s = threadIdx.x; s < n && s < Wp * 32u; s += blockDim.x) {
+    unsigned long long x1 = 0, x2 = 0;
+#pragma unroll
+    for (int q = 0; q < kUnivWarps; ++q) {
+      x1 ^= s_wh[q][s].x;
+      x2 ^= s_wh[q][s].y;
+    }
+    s_dh1[s] = x1;
+    s_dh2[s] = x2;
     if (s_dfit[s]) atomicAdd(&a.dfit[s], (double)s_dfit[s]);
     if (s_dh1[s] | s_dh2[s]) {
       atomicXor(&a.dh1[s], s_dh1[s]);
