@@ -1274,6 +1274,9 @@ GOMIX_API int gomix_debug_probes(unsigned long long* out, int32_t reset) {
     debug_probes_gen(b, reset != 0);
     for (int i = 0; i < 64; ++i)
       if (!out[i]) out[i] = b[i];
+    debug_probes_univ(b, reset != 0);
+    for (int i = 0; i < 64; ++i)
+      if (!out[i]) out[i] = b[i];
   });
 }
 

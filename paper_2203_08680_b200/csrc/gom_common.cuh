@@ -24,6 +24,14 @@ __device__ __forceinline__ void probe(uint32_t flags, uint32_t i) {
     if (g_probe[i] == 0) g_probe[i] = t;
   }
 }
+// the same from thread 0 of whichever CTA calls it (the last-CTA epilogue)
+__device__ __forceinline__ void probe_last(uint32_t flags, uint32_t i) {
+  if ((flags & 32u) && threadIdx.x == 0 && i < 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (g_probe[i] == 0) g_probe[i] = t;
+  }
+}
 
 // ---------------------------------------------------------------------------
 // Philox4x32-10 (Salmon et al., SC'11), counter-based: every (generation, set,

@@ -442,6 +442,7 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_tt_kernel(const G
   __shared__ __align__(16) ulonglong2 s_wh[kUnivWarps][4 * 32];  // per-warp hash deltas (Wp <= 4)
   __shared__ unsigned long long s_steps, s_calls;
   __shared__ int s_last;
+  probe(a.exp_flags, 40);
   if (*(volatile int32_t*)&a.ctl->stop) return;
 
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
@@ -483,6 +484,7 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_tt_kernel(const G
     s_calls = 0;
   }
   __syncthreads();
+  probe(a.exp_flags, 41);
   unsigned long long steps = 0, calls = 0;
 
   const uint32_t batches = (G + 31u) / 32u;
@@ -726,6 +728,7 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_tt_kernel(const G
     __syncwarp();
   }
 
+  probe(a.exp_flags, 42);
   {
     unsigned long long ws = steps, wc = calls;
 #pragma unroll
@@ -766,9 +769,12 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_tt_kernel(const G
     s_last = atomicAdd(&a.ctl->done, 1u) == gridDim.x - 1;
   }
   __syncthreads();
+  probe(a.exp_flags, 43);
   if (!s_last) return;
   __threadfence();
+  probe_last(a.exp_flags, 44);
   epilogue_body(epi);
+  probe_last(a.exp_flags, 45);
   if (threadIdx.x == 0) a.ctl->done = 0;
 }
 
@@ -833,6 +839,15 @@ void launch_univ_sliced(const GomArgs& a, int planes, int wp, bool tt, int grid,
   void* fn = univ_kernel(planes, wp, tt);
   void* args[] = {(void*)&a};
   GOMIX_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kUnivWarps * 32), args, univ_smem(wp), s));
+}
+
+void debug_probes_univ(unsigned long long* out, bool reset) {
+  GOMIX_CUDA(cudaDeviceSynchronize());
+  GOMIX_CUDA(cudaMemcpyFromSymbol(out, g_probe, sizeof(unsigned long long) * 64));
+  if (reset) {
+    unsigned long long z[64] = {};
+    GOMIX_CUDA(cudaMemcpyToSymbol(g_probe, z, sizeof(z)));
+  }
 }
 
 void build_univ_records(Problem& P) {
