@@ -196,13 +196,13 @@ __global__ void __launch_bounds__(LEAN ? 256 : (TEAM ? 32 * TW : 256), LEAN ? 3 
     }
     __syncthreads();
     {
+      // per-CTA group counts fit 32 bits (units per CTA x n x footprint):
+      // native 32-bit shared atomics (64-bit ones are compare-and-swap loops)
       const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, steps);
-      unsigned long long wc = calls;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) wc += __shfl_xor_sync(0xFFFFFFFFu, wc, o);
+      const uint32_t wc = __reduce_add_sync(0xFFFFFFFFu, (uint32_t)calls);
       if (lane == 0 && (ws | wc)) {
-        atomicAdd(&s_steps, (unsigned long long)ws);
-        atomicAdd(&s_calls, wc);
+        atomicAdd(reinterpret_cast<unsigned int*>(&s_steps), ws);
+        atomicAdd(reinterpret_cast<unsigned int*>(&s_calls), wc);
       }
     }
 #pragma unroll

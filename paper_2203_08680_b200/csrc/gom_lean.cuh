@@ -91,27 +91,36 @@ __device__ __forceinline__ void gom_lean_unit(const GomArgs& a, uint32_t p, cons
       d = (int32_t)c0;
       x = x0;
     } else {
+      // k-th member (k uniform) among those differing from m on F, in one
+      // pass over F's rows: dwa[wg] = members of pool word wg that differ
+      uint32_t dwa[kLeanMaxWords];
+#pragma unroll
+      for (uint32_t wg = 0; wg < kLeanMaxWords; ++wg) dwa[wg] = 0;
+      for (uint32_t jv = 0; jv < f; ++jv) {
+        const uint32_t mk = 0u - ((m >> jv) & 1u);
+#pragma unroll
+        for (uint32_t wg = 0; wg < kLeanMaxWords; ++wg)
+          if (wg < Wp) dwa[wg] |= rowsW[jv * Wp + wg] ^ mk;
+      }
       uint32_t total = 0;
-      for (uint32_t wg = 0; wg < Wp; ++wg) {
-        uint32_t dw = 0;
-        for (uint32_t jv = 0; jv < f; ++jv) dw |= rowsW[jv * Wp + wg] ^ (((m >> jv) & 1u) ? FULL : 0u);
-        total += __popc(dw & valid_mask(wg, n));
+#pragma unroll
+      for (uint32_t wg = 0; wg < kLeanMaxWords; ++wg) {
+        if (wg < Wp) dwa[wg] &= valid_mask(wg, n);
+        total += __popc(dwa[wg]);
       }
       if (total > 0) {
         uint32_t kth = bounded(hi64(rr), total);
-        for (uint32_t wg = 0; wg < Wp; ++wg) {
-          uint32_t dw = 0;
-          for (uint32_t jv = 0; jv < f; ++jv) dw |= rowsW[jv * Wp + wg] ^ (((m >> jv) & 1u) ? FULL : 0u);
-          dw &= valid_mask(wg, n);
-          const uint32_t c = __popc(dw);
-          if (kth < c) {
-            const uint32_t b = select_bit(dw, kth);
-            d = (int32_t)(wg * 32u + b);
-            x = pattW[d];
-            break;
+#pragma unroll
+        for (uint32_t wg = 0; wg < kLeanMaxWords; ++wg) {
+          const uint32_t c = __popc(dwa[wg]);
+          if (d < 0) {
+            if (kth < c)
+              d = (int32_t)(wg * 32u + select_bit(dwa[wg], kth));
+            else
+              kth -= c;
           }
-          kth -= c;
         }
+        x = pattW[d];
       }
     }
   }
