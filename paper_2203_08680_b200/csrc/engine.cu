@@ -524,6 +524,10 @@ struct gomix_gpu_engine {
                                      : std::max<uint64_t>(1, (max_group + teams - 1) / teams);
       if (per >= 1) {
         gen_grid = (int)std::min<uint64_t>(want, (uint64_t)per * sms);
+        // lean units: whole waves of CTAs per SM (every SM holds the same
+        // number of CTAs; units spread warp-major over them)
+        if (gen_lean && want > (uint64_t)sms)
+          gen_grid = (int)std::min<uint64_t>((uint64_t)sms * ((want + sms - 1) / sms), (uint64_t)per * sms);
         gen_ok = true;
         gen_dfit = dev_alloc<long long>(allocs, 3 * n * kAccStride);
         gen_dh = dev_alloc<unsigned long long>(allocs, 6 * n * kAccStride);

@@ -107,7 +107,9 @@ __global__ void __launch_bounds__(LEAN ? 256 : (TEAM ? 32 * TW : 256), LEAN ? 3 
   const uint32_t tid_team = wit * 32u + lane, team_threads = tw * 32u;
   const uint32_t Wp = a.Wp, n = a.n;
   uint32_t* stage = smem + (size_t)team * a.stage_words;
-  const uint32_t gwarp = blockIdx.x * (blockDim.x >> 5) + warp;
+  // LEAN units go to warps in warp-major order (slot w of every CTA before
+  // slot w + 1), so every SM gets the same number of busy warps
+  const uint32_t gwarp = LEAN ? warp * gridDim.x + blockIdx.x : blockIdx.x * (blockDim.x >> 5) + warp;
   const uint32_t lean_w = LEAN ? gwarp % Wp : 0u;  // the grid's warp count is a multiple of Wp
   // solution of this thread's word j
   auto sol = [&](int j) -> uint32_t { return LEAN ? lean_w * 32u + lane : (wit + tw * (uint32_t)j) * 32u + lane; };
