@@ -148,9 +148,11 @@ __global__ void __launch_bounds__(LEAN ? 256 : (TEAM ? 32 * TW : 256), LEAN ? 3 
   __syncthreads();
 
   uint32_t slot = 0;
+  LeanPre pre{};     // LEAN: the next group's first unit, prefetched before the barrier
+  GroupDesc dnext{};  // the next group's descriptor, loaded before the barrier
   for (; slot < ga.k; ++slot) {
     const uint32_t gi = s_order[slot];
-    const GroupDesc d = a.groups[gi];
+    const GroupDesc d = slot == 0 ? a.groups[gi] : dnext;
     const uint4* gmeta = a.gmeta + d.g0;
     const uint32_t bi = (buf0 + slot) % 3u;
     // accumulators spread one per 256-byte line: ~1,250 CTAs add into the same
@@ -182,14 +184,22 @@ __global__ void __launch_bounds__(LEAN ? 256 : (TEAM ? 32 * TW : 256), LEAN ? 3 
     if constexpr (LEAN) {
       uint32_t* wsm = smem + (size_t)warp * kLeanSmemWords;
       const uint32_t per_round = (gridDim.x * (blockDim.x >> 5)) / Wp;
-      for (uint32_t p = gwarp / Wp; p < d.G; p += per_round)
-        gom_lean_unit(a, p, gmeta, lean_w, gen, wsm, lane, is_elit[0], esrc, ever_cur, false, acc[0], dh1[0],
+      for (uint32_t p = gwarp / Wp; p < d.G; p += per_round) {
+        const LeanPre cur = (p == gwarp / Wp && slot > 0) ? pre : lean_prefetch(a, gmeta, p, lane);
+        gom_lean_unit(a, p, cur, lean_w, gen, wsm, lane, is_elit[0], esrc, ever_cur, false, acc[0], dh1[0],
                       dh2[0], steps, calls);
+      }
+      // the next group's first unit: plan inputs in flight during the barrier
+      if (slot + 1 < ga.k) {
+        dnext = a.groups[s_order[slot + 1]];
+        if (gwarp / Wp < dnext.G) pre = lean_prefetch(a, a.gmeta + dnext.g0, gwarp / Wp, lane);
+      }
     } else {
       for (uint32_t p = blockIdx.x * teams_per_cta + team; p < d.G; p += gridDim.x * teams_per_cta)
         gom_general_set<WPT, true, TEAM>(a, p, gmeta, gen, stage, lane, tw, wit, tid_team, team_threads,
                                          teams_per_cta, team, true, false, false, is_elit, pfit, esrc, ever_cur,
                                          acc, dh1, dh2, steps, calls);
+      if (slot + 1 < ga.k) dnext = a.groups[s_order[slot + 1]];
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -236,6 +246,11 @@ __global__ void __launch_bounds__(LEAN ? 256 : (TEAM ? 32 * TW : 256), LEAN ? 3 
     probe(a.exp_flags, 17 + 4 * slot);
 
     // ---- epilogue (every CTA): fitness / hash commit ------------------------
+    unsigned long long cnt_st = 0, cnt_ca = 0;
+    if (threadIdx.x == 0) {  // issued with the accumulator loads below (one round trip)
+      cnt_st = __ldcg(CNT);
+      cnt_ca = __ldcg(CNT + 1);
+    }
     for (uint32_t s = threadIdx.x; s < n; s += blockDim.x) {
       const double f = s_fit[s] + (double)__ldcg(D + s * kAccStride);
       const unsigned long long x1 = s_h1[s] ^ __ldcg(DH1 + s * kAccStride), x2 = s_h2[s] ^ __ldcg(DH2 + s * kAccStride);
@@ -260,7 +275,7 @@ __global__ void __launch_bounds__(LEAN ? 256 : (TEAM ? 32 * TW : 256), LEAN ? 3 
       ga.cnt[2 * zb + 1] = 0;
     }
     if (threadIdx.x == 0) {
-      const unsigned long long st = __ldcg(CNT), ca = __ldcg(CNT + 1);
+      const unsigned long long st = cnt_st, ca = cnt_ca;
       s_calls_total += ca;
       s_run_steps += st;
       s_run_calls += ca;

@@ -26,21 +26,46 @@ constexpr uint32_t kLeanMaxF = 32;       // set size (variables per lane view)
 constexpr uint32_t kLeanMaxWords = 8;    // pool words (n <= 256)
 constexpr uint32_t kLeanSmemWords = kLeanMaxF * kLeanMaxWords + kLeanMaxWords * 32 + 2 * 2 * kLeanMaxF;
 
-__device__ __forceinline__ void gom_lean_unit(const GomArgs& a, uint32_t p, const uint4* gmeta, uint32_t w,
+// The unit's population-independent inputs (plan record, F's variables, its
+// first footprint chunk): loaded ahead, e.g. during the grid barrier before
+// the unit's group, so the group's critical path starts at the row loads.
+struct LeanPre {
+  uint4 gm;    // {set id, vars offset, footprint offset, f << 24 | footprint}
+  uint32_t vj; // lane jv: variable jv of F
+  FpEntry e0;  // lane t: footprint entry t
+};
+
+__device__ __forceinline__ LeanPre lean_prefetch(const GomArgs& a, const uint4* gmeta, uint32_t p, uint32_t lane) {
+  LeanPre r;
+  r.gm = gmeta[p];
+  const uint32_t f = r.gm.w >> 24;
+  r.vj = lane < f ? a.set_vars[r.gm.y + lane] : 0u;
+  const uint32_t e = r.gm.z + lane, e1 = r.gm.z + (r.gm.w & 0xFFFFFFu);
+  if (e < e1) {
+    r.e0 = a.fp[e];
+  } else {
+    r.e0.a = kInSet;
+    r.e0.b = kInSet;
+    r.e0.w = 0.0;
+  }
+  return r;
+}
+
+__device__ __forceinline__ void gom_lean_unit(const GomArgs& a, uint32_t p, const LeanPre& pre, uint32_t w,
                                               uint32_t generation, uint32_t* wsm, uint32_t lane, bool is_elit,
                                               int32_t esrc, uint32_t ever_cur, bool record, long long& acc,
                                               unsigned long long& dh1, unsigned long long& dh2, uint32_t& steps,
                                               unsigned long long& calls) {
   constexpr uint32_t FULL = 0xFFFFFFFFu;
   const uint32_t Wp = a.Wp, n = a.n, lwp = 31u - __clz(Wp);
-  const uint4 gm = gmeta[p];
+  const uint4 gm = pre.gm;
   const uint32_t sid = gm.x, f = gm.w >> 24;
   const uint32_t* vars = a.set_vars + gm.y;
   const uint32_t e0 = gm.z, e1 = gm.z + (gm.w & 0xFFFFFFu);
   uint32_t* rowsW = wsm;                                         // [jv * Wp + wg]
   uint32_t* pattW = wsm + kLeanMaxF * kLeanMaxWords;             // [member]
   unsigned long long* zW = reinterpret_cast<unsigned long long*>(pattW + kLeanMaxWords * 32);  // [2 jv + {0,1}]
-  const uint32_t vj = lane < f ? vars[lane] : 0u;  // lane jv: variable jv of F
+  const uint32_t vj = pre.vj;  // lane jv: variable jv of F
   // ---- F's rows at group start (the donor pool, engine_parallel.hpp:100-103)
   for (uint32_t base = 0; base < f * Wp; base += 32) {
     const uint32_t idx = base + lane;
@@ -48,18 +73,8 @@ __device__ __forceinline__ void gom_lean_unit(const GomArgs& a, uint32_t p, cons
     const uint32_t v = __shfl_sync(FULL, vj, jv);
     if (idx < f * Wp) rowsW[idx] = a.pop[(size_t)v * Wp + (idx & (Wp - 1u))];
   }
-  // first footprint chunk: entry per lane and its outside row word (word w)
-  FpEntry E0;
-  {
-    const uint32_t e = e0 + lane;
-    if (e < e1) {
-      E0 = a.fp[e];
-    } else {
-      E0.a = kInSet;
-      E0.b = kInSet;
-      E0.w = 0.0;
-    }
-  }
+  // first footprint chunk: entry per lane (prefetched) and its outside row word (word w)
+  const FpEntry E0 = pre.e0;
   const uint32_t v0 = __shfl_sync(FULL, vj, 0);
   uint32_t xo0;
   {
