@@ -78,7 +78,12 @@ enum {
   GOMIX_FLAG_PER_GROUP_KERNELS = 1u << 4,
   /* Univariate FOS of degree <= 4: use the adder/comparator bit-sliced kernel
    * instead of the truth-table one (same results; A/B tests). */
-  GOMIX_FLAG_NO_TRUTH_TABLE = 1u << 5
+  GOMIX_FLAG_NO_TRUTH_TABLE = 1u << 5,
+  /* Parallel-friendly Forced Improvement after every generation (single GPU):
+   * triggered solutions take the elitist as donor group by group, halt after
+   * the first group that strictly improved them, else become elitist copies
+   * (engine_serial.hpp:98-128 restated group-wise; see gom_fi.cu). */
+  GOMIX_FLAG_FORCED_IMPROVEMENT = 1u << 6
 };
 
 enum { GOMIX_STOP_NONE = 0, GOMIX_STOP_BUDGET = 1, GOMIX_STOP_CLOCK = 2, GOMIX_STOP_TARGET = 3,
@@ -213,6 +218,15 @@ GOMIX_API int gomix_gpu_load_population(gomix_gpu_engine* e, const uint8_t* geno
  * donor_tape == NULL draws donors with the engine's mode. */
 GOMIX_API int gomix_gpu_run_group(gomix_gpu_engine* e, uint64_t group, const int32_t* donor_tape,
                         const gomix_stop_criteria* stop, gomix_run_stats* out);
+
+/* One Forced-Improvement pass now (see GOMIX_FLAG_FORCED_IMPROVEMENT) over the
+ * solutions with flags[s] != 0 (flags NULL: the engine's own trigger —
+ * unchanged genotype or stagnation since the last generation started), the
+ * colour groups in group_order (k entries; NULL: a fresh permutation from the
+ * engine's stream).  Counts toward the run's evaluator calls and stop
+ * criteria like a generation's groups.  Single-GPU engines. */
+GOMIX_API int gomix_gpu_forced_improvement(gomix_gpu_engine* e, const uint8_t* flags, const uint32_t* group_order,
+                                           const gomix_stop_criteria* stop, gomix_run_stats* out);
 
 /* Last group's GroupBatch arrays, each n*|G| in s*|G| + p order (needs
  * GOMIX_FLAG_RECORD_BATCH).  Any pointer may be NULL. */

@@ -16,6 +16,11 @@
 //   color  : FOS + LMIG + Welsh-Powell groups (scheduling.hpp:35,85).
 //   bench  : wall time of ParallelEngine::run_generation with W workers.
 //   ims    : run_parallel (run.hpp:106) with IMS and a target / budget.
+//   fi     : the reference's forced_improvement (engine_serial.hpp:98-128) on
+//            one solution of a given population (--pop: int64 header
+//            [n, nv, o, e] then n*nv genotype bytes; o = the solution, e =
+//            the elitist) with RngStream(--seed); dumps the set order it
+//            draws, the result genotype / fitness, calls and the outcome.
 #include <chrono>
 #include <cstdio>
 #include <cstring>
@@ -56,6 +61,7 @@ struct Args {
   double max_seconds = 0, target = 0, max_evals = 0;
   bool has_target = false, has_evals = false, use_ims = false, serial = false;
   std::size_t ims_base = 16, ims_sub = 4;
+  std::string pop;
 };
 
 Args parse(int argc, char** argv) {
@@ -84,6 +90,7 @@ Args parse(int argc, char** argv) {
     else if (k == "--serial") a.serial = true;
     else if (k == "--ims-base") a.ims_base = std::stoull(next());
     else if (k == "--ims-sub") a.ims_sub = std::stoull(next());
+    else if (k == "--pop") a.pop = next();
     else throw std::invalid_argument("unknown flag " + k);
   }
   return a;
@@ -422,20 +429,51 @@ int mode_ims(const Args& a) {
 
 }  // namespace
 
+int mode_fi(const Args& a) {
+  const MaxCutInstance inst = make_instance(a);
+  const GrayBoxProblem problem = as_graybox(inst);
+  auto arts = build_model(a, problem);
+  std::ifstream in(a.pop, std::ios::binary);
+  if (!in) throw std::runtime_error("cannot open " + a.pop);
+  std::int64_t hdr[4];
+  in.read(reinterpret_cast<char*>(hdr), sizeof(hdr));
+  const std::size_t n = (std::size_t)hdr[0], nv = (std::size_t)hdr[1];
+  if (nv != problem.num_variables()) throw std::invalid_argument("fi: genotype length mismatch");
+  std::vector<std::uint8_t> g(n * nv);
+  in.read(reinterpret_cast<char*>(g.data()), (std::streamsize)g.size());
+  auto row = [&](std::int64_t s) { return Genotype(g.begin() + s * (std::int64_t)nv, g.begin() + (s + 1) * (std::int64_t)nv); };
+  EvaluatedSolution o = full_evaluate(problem, row(hdr[2]));
+  const EvaluatedSolution elitist = full_evaluate(problem, row(hdr[3]));
+  RngStream rng(a.seed);
+  RngStream peek = rng;
+  std::vector<std::size_t> order;
+  peek.permutation(order, arts->fos.sets.size());
+  EvalWorkspace ws;
+  ws.bind(problem);
+  const FiOutcome r = forced_improvement(problem, o, elitist, arts->fos, rng, problem.comparator(), ws);
+  write_u64("set_order", std::vector<std::uint64_t>(order.begin(), order.end()));
+  write_u8("genotype", std::vector<std::uint8_t>(o.genotype.begin(), o.genotype.end()));
+  write_f64("fitness", {o.fitness});
+  write_u64("evaluator_calls", {r.evaluator_calls});
+  write_u64("strict_improvement", {r.strict_improvement ? 1u : 0u});
+  write_u64("replaced_by_elitist", {r.replaced_by_elitist ? 1u : 0u});
+  return 0;
+}
+
 int main(int argc, char** argv) {
   try {
     const Args a = parse(argc, argv);
-    if (a.mode == "run" || a.mode == "color") {
+    if (a.mode == "run" || a.mode == "color" || a.mode == "fi") {
       if (a.out.empty()) throw std::invalid_argument("--out required");
       g_out = std::fopen(a.out.c_str(), "wb");
       if (!g_out) throw std::runtime_error("cannot write " + a.out);
-      const int rc = a.mode == "run" ? mode_run(a) : mode_color(a);
+      const int rc = a.mode == "run" ? mode_run(a) : (a.mode == "color" ? mode_color(a) : mode_fi(a));
       std::fclose(g_out);
       return rc;
     }
     if (a.mode == "bench") return mode_bench(a);
     if (a.mode == "ims") return mode_ims(a);
-    throw std::invalid_argument("mode: run | color | bench | ims");
+    throw std::invalid_argument("mode: run | color | bench | ims | fi");
   } catch (const std::exception& e) {
     std::fprintf(stderr, "ref_driver: %s\n", e.what());
     return 2;

@@ -17,7 +17,7 @@ LIB_PATH = os.environ.get("GOMIX_LIB") or os.path.join(PKG, "libgomix_b200.so") 
 GOMIX_OK, GOMIX_E_INVALID, GOMIX_E_CUDA, GOMIX_E_NCCL, GOMIX_E_OOM, GOMIX_E_STATE = range(6)
 MODE_REPLAY, MODE_PHILOX = 0, 1
 FLAG_ORDERED_FLOAT, FLAG_RECORD_BATCH, FLAG_TIME_KERNELS, FLAG_LANE_PER_SOLUTION, FLAG_PER_GROUP_KERNELS, \
-    FLAG_NO_TRUTH_TABLE = 1, 2, 4, 8, 16, 32
+    FLAG_NO_TRUTH_TABLE, FLAG_FORCED_IMPROVEMENT = 1, 2, 4, 8, 16, 32, 64
 STOP_NAMES = {0: "none", 1: "evaluation-budget", 2: "wall-clock", 3: "target-reached",
               4: "generation-limit"}
 
@@ -87,6 +87,7 @@ _SIGNATURES = {
     "gomix_gpu_synchronize": ([_P, C.POINTER(RunStats)], C.c_int),
     "gomix_gpu_load_population": ([_P, _P, _P], C.c_int),
     "gomix_gpu_run_group": ([_P, C.c_uint64, _P, C.POINTER(StopCriteria), C.POINTER(RunStats)], C.c_int),
+    "gomix_gpu_forced_improvement": ([_P, _P, _P, C.POINTER(StopCriteria), C.POINTER(RunStats)], C.c_int),
     "gomix_gpu_read_batch": ([_P, _P, _P, _P, _P], C.c_int),
     "gomix_gpu_read_population": ([_P, _P, _P], C.c_int),
     "gomix_gpu_read_population_packed": ([_P, _P, C.POINTER(C.c_uint64)], C.c_int),

@@ -377,6 +377,15 @@ struct gomix_gpu_engine {
   uint64_t impr_cap = 0;
   int32_t* tape = nullptr;
   int32_t* h_tape_pinned = nullptr;
+  // forced improvement (GOMIX_FLAG_FORCED_IMPROVEMENT / gomix_gpu_forced_improvement, gom_fi.cu)
+  bool fi_on = false;
+  double* fi_fit_start = nullptr;
+  unsigned long long* fi_h1s = nullptr;
+  unsigned long long* fi_h2s = nullptr;
+  int32_t* fi_stag = nullptr;
+  uint8_t* fi_flag = nullptr;
+  double* fi_fit0 = nullptr;
+  uint32_t* fi_mask = nullptr;
   int32_t* rec_donor = nullptr;
   double* rec_delta = nullptr;
   uint8_t* rec_present = nullptr;
@@ -561,6 +570,8 @@ struct gomix_gpu_engine {
     impr_cap = std::min<uint64_t>(std::max<uint64_t>(4096, n_global * (P->k + 1)), 1ull << 22);
     impr = dev_alloc<double>(allocs, impr_cap);
     impr_calls = dev_alloc<unsigned long long>(allocs, impr_cap);
+    fi_on = (flags & GOMIX_FLAG_FORCED_IMPROVEMENT) != 0;
+    if (fi_on && R > 1) invalid("engine: forced improvement needs a single-GPU engine");
     if (epi_mode == 1) {
       part = dev_alloc<double>(allocs, (size_t)grid_cap * n);
       const uint64_t nblk = ((uint64_t)grid_cap + kPartBlock - 1) / kPartBlock;
@@ -877,10 +888,105 @@ struct gomix_gpu_engine {
   // (engine_serial.hpp:30-46) against the group-start population.
   // donor tapes (replay mode / explicit donors) are allocated on first use:
   // max_group * n entries is a gigabyte at 10^6 vertices and n = 512
-  void ensure_tape() {
-    if (tape) return;
-    tape = dev_alloc<int32_t>(allocs, max_group * n);
-    GOMIX_CUDA(cudaMallocHost(&h_tape_pinned, std::max<uint64_t>(1, max_group * n) * sizeof(int32_t)));
+  void ensure_tape(bool host = true) {
+    if (!tape) tape = dev_alloc<int32_t>(allocs, max_group * n);
+    if (host && !h_tape_pinned)
+      GOMIX_CUDA(cudaMallocHost(&h_tape_pinned, std::max<uint64_t>(1, max_group * n) * sizeof(int32_t)));
+  }
+
+  // ---- forced improvement (gom_fi.cu) ----------------------------------------
+  void ensure_fi() {
+    if (fi_fit_start) return;
+    fi_fit_start = dev_alloc<double>(allocs, n);
+    fi_h1s = dev_alloc<unsigned long long>(allocs, n);
+    fi_h2s = dev_alloc<unsigned long long>(allocs, n);
+    fi_stag = dev_alloc<int32_t>(allocs, n);
+    fi_flag = dev_alloc<uint8_t>(allocs, n);
+    fi_fit0 = dev_alloc<double>(allocs, n);
+    fi_mask = dev_alloc<uint32_t>(allocs, Wp);
+    GOMIX_CUDA(cudaMemsetAsync(fi_stag, 0, n * sizeof(int32_t), stream));
+    GOMIX_CUDA(cudaMemsetAsync(fi_flag, 0, n, stream));
+  }
+
+  FiArgs fi_args() {
+    FiArgs a;
+    a.pop = pop;
+    a.fit = fit;
+    a.h1 = h1;
+    a.h2 = h2;
+    a.fit_start = fi_fit_start;
+    a.h1s = fi_h1s;
+    a.h2s = fi_h2s;
+    a.stag = fi_stag;
+    a.flag = fi_flag;
+    a.fit0 = fi_fit0;
+    a.mask = fi_mask;
+    a.ctl = ctl;
+    a.gsets = P->gsets;
+    a.set_off = P->set_off;
+    a.set_vars = P->set_vars;
+    a.nv = P->nv;
+    a.n = (uint32_t)n;
+    a.Wp = Wp;
+    a.threshold = 1 + (int32_t)std::floor(std::log10((double)n));  // engine_serial.hpp:153-155
+    return a;
+  }
+
+  // generation start (before its GOM groups)
+  void fi_snapshot() {
+    ensure_fi();
+    launch_fi_snapshot(fi_args(), stream);
+    ++launches;
+  }
+
+  // The pass itself: trigger (or given flags), then every colour group in
+  // `order` as one batched GOM step with the elitist as donor, then the
+  // elitist copies.  Runs after the generation's groups, on the same stream,
+  // against the same control block (calls, stop criteria, elitist scan).
+  void fi_pass(const uint8_t* given, const std::vector<uint64_t>& order, bool update_stag) {
+    ensure_fi();
+    ensure_tape(false);
+    const FiArgs fa = fi_args();
+    if (given) GOMIX_CUDA(cudaMemcpyAsync(fi_flag, given, n, cudaMemcpyHostToDevice, stream));
+    launch_fi_flags(fa, given != nullptr, stream);
+    ++launches;
+    for (uint64_t gi : order) {
+      const uint64_t g0 = P->group_off[gi], G = P->group_off[gi + 1] - g0;
+      launch_fi_tape(fa, g0, G, tape, stream);
+      launch_group(gi, true);
+      ++launches;
+    }
+    launch_fi_finish(fa, update_stag, stream);
+    launches += 3;
+  }
+
+  // the engine's own trigger after a generation, groups in a fresh order
+  void fi_after_generation() {
+    std::vector<uint64_t> order;
+    rng.permutation(order, P->k);
+    fi_pass(nullptr, order, true);
+  }
+
+  void forced_improvement(const uint8_t* flags_in, const uint32_t* group_order, const gomix_stop_criteria* stop,
+                          gomix_run_stats* out) {
+    if (!initialized) throw GomixError(GOMIX_E_STATE, "forced_improvement: population not initialised");
+    if (R > 1) invalid("forced_improvement: single-GPU engines only");
+    std::vector<uint64_t> order;
+    if (group_order) {
+      std::vector<uint8_t> seen(P->k, 0);
+      for (uint64_t i = 0; i < P->k; ++i) {
+        if (group_order[i] >= P->k || seen[group_order[i]]) invalid("forced_improvement: group_order is not a permutation");
+        seen[group_order[i]] = 1;
+        order.push_back(group_order[i]);
+      }
+    } else {
+      rng.permutation(order, P->k);
+    }
+    if (!flags_in && !fi_fit_start) invalid("forced_improvement: no generation has set the trigger (pass flags)");
+    begin_call(stop);
+    fi_pass(flags_in, order, false);
+    read_ctl();
+    fill_stats(out);
   }
 
   void draw_replay_tape(uint64_t group) {
@@ -1040,16 +1146,19 @@ struct gomix_gpu_engine {
     }
     if (mode == GOMIX_MODE_PHILOX && (gen_ok || !(flags & GOMIX_FLAG_TIME_KERNELS))) {
       stage_criteria(stop, true);
+      if (fi_on) fi_snapshot();
       if (gen_ok)
         launch_generation_persistent();
       else
         launch_generation_graph();
+      if (fi_on) fi_after_generation();
       read_ctl();
       fill_stats(out);
       if (!h_ctl->stop) ++generation;
       return;
     }
     begin_call(stop);
+    if (fi_on) fi_snapshot();
     std::vector<uint64_t> order;
     rng.permutation(order, P->k);  // engine_parallel.hpp:291
     for (uint64_t gi : order) {
@@ -1062,6 +1171,7 @@ struct gomix_gpu_engine {
       }
       launch_group(gi, mode == GOMIX_MODE_REPLAY);
     }
+    if (fi_on) fi_after_generation();
     read_ctl();
     fill_stats(out);
     if (!h_ctl->stop) ++generation;  // engine_parallel.hpp:311-314
@@ -1075,16 +1185,20 @@ struct gomix_gpu_engine {
     if (R > 1) invalid("run_generation_async: single-GPU engines only");
     if (gen_ok) {
       stage_criteria(nullptr, false);
+      if (fi_on) fi_snapshot();
       launch_generation_persistent();
     } else if (flags & GOMIX_FLAG_TIME_KERNELS) {
       begin_call(nullptr);
+      if (fi_on) fi_snapshot();
       std::vector<uint64_t> order;
       rng.permutation(order, P->k);
       for (uint64_t gi : order) launch_group(gi, false);
     } else {
       stage_criteria(nullptr, false);
+      if (fi_on) fi_snapshot();
       launch_generation_graph();
     }
+    if (fi_on) fi_after_generation();
     ++generation;
   }
 
@@ -1407,6 +1521,14 @@ int gomix_gpu_run_group(gomix_gpu_engine* e, uint64_t group, const int32_t* dono
   return guarded([&] {
     if (!e) invalid("run_group: NULL engine");
     e->run_group(group, donor_tape, stop, out);
+  });
+}
+
+int gomix_gpu_forced_improvement(gomix_gpu_engine* e, const uint8_t* flags, const uint32_t* group_order,
+                                 const gomix_stop_criteria* stop, gomix_run_stats* out) {
+  return guarded([&] {
+    if (!e) invalid("forced_improvement: NULL engine");
+    e->forced_improvement(flags, group_order, stop, out);
   });
 }
 

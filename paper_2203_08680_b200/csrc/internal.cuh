@@ -192,6 +192,28 @@ struct GomArgs {
   const GroupDesc* groups;
 };
 
+// Forced-improvement phase (gom_fi.cu)
+struct FiArgs {
+  uint32_t* pop;
+  double* fit;
+  unsigned long long* h1;
+  unsigned long long* h2;
+  double* fit_start;  // generation start
+  unsigned long long* h1s;
+  unsigned long long* h2s;
+  int32_t* stag;      // generations without strict improvement (SerialEngine::stagnation_)
+  uint8_t* flag;      // triggered this generation
+  double* fit0;       // fitness at the start of the pass
+  uint32_t* mask;     // Wp words: still in the pass after every group
+  const DevCtl* ctl;
+  const uint32_t* gsets;
+  const int64_t* set_off;
+  const uint32_t* set_vars;
+  uint64_t nv;
+  uint32_t n, Wp;
+  int32_t threshold;  // 1 + floor(log10 n) (engine_serial.hpp:153-155)
+};
+
 // Run-wide best of an IMS run (ImsDriver::best_, ims.hpp:98-99), device-resident.
 struct ImsBestDev {
   double fit;
@@ -307,7 +329,11 @@ int univ_sliced_block();
 int univ_sliced_sets_per_cta();
 int univ_sliced_max_blocks_per_sm(int planes, int wp, bool tt);
 void launch_univ_sliced(const GomArgs& a, int planes, int wp, bool tt, int grid, cudaStream_t s);
-void build_univ_records(Problem& P);  // truth-table plan records (urec, ukey) of a degree <= 4 univariate FOS
+void build_univ_records(Problem& P);
+void launch_fi_snapshot(const FiArgs& a, cudaStream_t s);
+void launch_fi_flags(const FiArgs& a, bool given, cudaStream_t s);
+void launch_fi_tape(const FiArgs& a, uint64_t g0, uint64_t G, int32_t* tape, cudaStream_t s);
+void launch_fi_finish(const FiArgs& a, bool update_stag, cudaStream_t s);  // truth-table plan records (urec, ukey) of a degree <= 4 univariate FOS
 int gom_max_blocks_per_sm(bool univariate, bool i32, int wpt, bool team, int block, size_t smem);
 void launch_begin(const BeginArgs& b, cudaStream_t s);
 void launch_order(const BeginArgs* d_b, const OrderArgs& o, cudaStream_t s);

@@ -234,7 +234,8 @@ class GpuParallelEngine:
                  record_batch: bool = False, ordered_float: bool = False, time_kernels: bool = False,
                  genotypes: Optional[np.ndarray] = None, stream=None, rank: int = 0, world_size: int = 1,
                  nccl_unique_id: Optional[bytes] = None, lane_per_solution: bool = False,
-                 per_group_kernels: bool = False, truth_table: bool = True):
+                 per_group_kernels: bool = False, truth_table: bool = True,
+                 forced_improvement: bool = False):
         """world_size > 1: this process's shard of a population of
         `population_size` members over world_size GPUs (Philox mode); every
         rank passes the same nccl_unique_id (see nccl_unique_id()) and calls
@@ -252,7 +253,8 @@ class GpuParallelEngine:
             | (_capi.FLAG_TIME_KERNELS if time_kernels else 0) \
             | (_capi.FLAG_LANE_PER_SOLUTION if lane_per_solution else 0) \
             | (_capi.FLAG_PER_GROUP_KERNELS if per_group_kernels else 0) \
-            | (0 if truth_table else _capi.FLAG_NO_TRUTH_TABLE)
+            | (0 if truth_table else _capi.FLAG_NO_TRUTH_TABLE) \
+            | (_capi.FLAG_FORCED_IMPROVEMENT if forced_improvement else 0)
         self._nid = None if nccl_unique_id is None else C.create_string_buffer(bytes(nccl_unique_id), 128)
         cfg = _capi.EngineConfig(self.n_global, seed, _capi.MODE_REPLAY if mode == "replay" else _capi.MODE_PHILOX,
                                  flags, population_id, self.rank, self.world_size,
@@ -374,6 +376,22 @@ class GpuParallelEngine:
         stats = _capi.RunStats()
         crit = self.ctx.control.criteria()
         check(lib().gomix_gpu_run_group(self.h, group, _capi.ptr(d), C.byref(crit), C.byref(stats)))
+        self._absorb(stats, self.generation())
+        return stats
+
+    def forced_improvement(self, flags=None, group_order=None):
+        """One parallel-friendly Forced-Improvement pass now (csrc/gom_fi.cu):
+        solutions with flags[s] (None: the engine's own trigger) take the
+        elitist as donor group by group in group_order (None: a fresh
+        permutation), leave after the first group that strictly improved
+        them, else become elitist copies."""
+        f = None if flags is None else np.ascontiguousarray(np.asarray(flags) != 0, np.uint8)
+        if f is not None and f.shape != (self.n,):
+            raise ValueError("forced_improvement: flags must have one entry per solution")
+        o = None if group_order is None else np.ascontiguousarray(group_order, np.uint32)
+        stats = _capi.RunStats()
+        crit = self.ctx.control.criteria()
+        check(lib().gomix_gpu_forced_improvement(self.h, _capi.ptr(f), _capi.ptr(o), C.byref(crit), C.byref(stats)))
         self._absorb(stats, self.generation())
         return stats
 
