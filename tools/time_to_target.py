@@ -55,7 +55,7 @@ def warm_device():
     G.GpuProblem(t, G.univariate_fos(16))
 
 
-def gpu_ims(cfg, target, seed, budget_s, base=16, sub=4):
+def gpu_ims(cfg, target, seed, budget_s, base=16, sub=4, **engine_kw):
     import paper_2203_08680_b200 as G
 
     warm_device()
@@ -67,7 +67,7 @@ def gpu_ims(cfg, target, seed, budget_s, base=16, sub=4):
     build_s = time.perf_counter() - t0
     sink = G.RecordingSink()
     r = G.run_gpu(P, G.TerminationConfig(target_fitness=target, max_seconds=budget_s), seed=seed, use_ims=True,
-                  ims=G.ImsConfig(base, sub), sink=sink, mode="philox")
+                  ims=G.ImsConfig(base, sub), sink=sink, mode="philox", **engine_kw)
     hit = r.reason == "target-reached"
     t_hit = next((x.seconds for x in sink.rows if x.fitness >= target), None) if hit else None
     return {"reached": hit, "seconds_to_target": t_hit, "build_seconds": build_s,
@@ -84,6 +84,8 @@ def main():
     ap.add_argument("--seeds", type=int, default=1)
     ap.add_argument("--gpu-budget", type=float, default=None, help="GPU wall budget per seed (default t_ref)")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--fi", action="store_true",
+                    help="also run the GPU IMS with the parallel forced improvement (csrc/gom_fi.cu)")
     a = ap.parse_args()
     cfg = CONFIGS[a.config]
     workers = os.cpu_count() or 1
@@ -92,6 +94,8 @@ def main():
         ref = reference_ims(cfg, seed, a.t_ref, workers)
         gpu = gpu_ims(cfg, ref["best"], seed, a.gpu_budget or a.t_ref)
         rows.append({"seed": seed, "reference": ref, "gpu": gpu})
+        if a.fi:
+            rows[-1]["gpu_fi"] = gpu_ims(cfg, ref["best"], seed, a.gpu_budget or a.t_ref, forced_improvement=True)
         print(json.dumps(rows[-1]), flush=True)
     ok = [r for r in rows if r["gpu"]["reached"]]
     summ = {"config": cfg["workload"], "t_ref_s": a.t_ref, "cpu_workers": workers, "seeds": a.seeds,
@@ -101,6 +105,11 @@ def main():
             "gpu_median_s_to_target_incl_build":
                 statistics.median(r["gpu"]["seconds_to_target_incl_build"] for r in ok) if ok else None,
             "rows": rows}
+    if a.fi:
+        okf = [r for r in rows if r["gpu_fi"]["reached"]]
+        summ["fi_success_rate"] = len(okf) / len(rows)
+        summ["fi_gpu_median_s_to_target"] = \
+            statistics.median(r["gpu_fi"]["seconds_to_target"] for r in okf) if okf else None
     if ok:
         summ["speedup_median"] = summ["cpu_median_s_to_best_known"] / summ["gpu_median_s_to_target"]
         summ["speedup_median_incl_build"] = summ["cpu_median_s_to_best_known"] / summ["gpu_median_s_to_target_incl_build"]
