@@ -419,7 +419,8 @@ struct gomix_gpu_engine {
       cudaEventDestroy(pr.second);
     }
     for (auto e : ev_free) cudaEventDestroy(e);
-    for (void* p : allocs) cudaFree(p);
+    cudaDeviceSynchronize();
+    cached_free_all(allocs);
     if (h_ctl) cudaFreeHost(h_ctl);
     if (h_begin) cudaFreeHost(h_begin);
     if (h_impr) cudaFreeHost(h_impr);
@@ -1647,7 +1648,8 @@ struct gomix_gpu_ims_best {
   std::vector<void*> allocs;
   ~gomix_gpu_ims_best() {
     if (ev) cudaEventSynchronize(ev), cudaEventDestroy(ev);
-    for (void* p : allocs) cudaFree(p);
+    cudaDeviceSynchronize();
+    cached_free_all(allocs);
     if (host) cudaFreeHost(host);
   }
   void order_before(gomix_gpu_engine* e) {

@@ -273,11 +273,20 @@ struct GomixError : std::runtime_error {
 
 inline void invalid(const std::string& m) { throw GomixError(GOMIX_E_INVALID, m); }
 
+// Process-wide caching device allocator (problem.cu): blocks go back to a
+// per-device free list instead of cudaFree (which synchronises the device
+// and, for large blocks, costs milliseconds), so repeated problem / engine
+// builds of similar sizes reuse memory.  Callers synchronise before freeing
+// (the cache does not track stream use).  Sizes are rounded up (1 MiB
+// granules above 1 MiB, powers of two below); at most 8 GiB stay cached.
+void* cached_malloc(size_t bytes);
+void cached_free(void* p);
+void cached_free_all(std::vector<void*>& blocks);
+
 template <typename T>
 T* dev_alloc(std::vector<void*>& owner, size_t count) {
-  void* p = nullptr;
   if (count == 0) count = 1;
-  GOMIX_CUDA(cudaMalloc(&p, count * sizeof(T)));
+  void* p = cached_malloc(count * sizeof(T));
   owner.push_back(p);
   return static_cast<T*>(p);
 }

@@ -22,12 +22,95 @@
 #include <cstring>
 #include <numeric>
 
+#include <map>
+#include <mutex>
+#include <unordered_map>
+
 #include "internal.cuh"
 
 namespace gomix_b200 {
 
+// ---- caching device allocator (internal.cuh) ---------------------------------
+namespace {
+struct DeviceCache {
+  std::mutex mu;
+  std::map<std::pair<int, size_t>, std::vector<void*>> free_blocks;  // (device, rounded size)
+  std::unordered_map<void*, std::pair<int, size_t>> live;
+  size_t cached_bytes = 0;
+  static constexpr size_t kCap = 8ull << 30;
+};
+DeviceCache& cache() {
+  static DeviceCache* c = new DeviceCache;  // never destroyed: frees may run during process exit
+  return *c;
+}
+size_t round_block(size_t b) {
+  if (b >= (1u << 20)) return (b + (1u << 20) - 1) & ~((size_t)(1u << 20) - 1);
+  size_t r = 256;
+  while (r < b) r <<= 1;
+  return r;
+}
+}  // namespace
+
+void* cached_malloc(size_t bytes) {
+  int dev = 0;
+  GOMIX_CUDA(cudaGetDevice(&dev));
+  const size_t sz = round_block(std::max<size_t>(bytes, 1));
+  DeviceCache& c = cache();
+  {
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto it = c.free_blocks.find({dev, sz});
+    if (it != c.free_blocks.end() && !it->second.empty()) {
+      void* p = it->second.back();
+      it->second.pop_back();
+      c.cached_bytes -= sz;
+      c.live[p] = {dev, sz};
+      return p;
+    }
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, sz);
+  if (e == cudaErrorMemoryAllocation) {  // give the cached blocks back and retry once
+    cudaGetLastError();
+    std::lock_guard<std::mutex> lk(c.mu);
+    for (auto& kv : c.free_blocks)
+      for (void* q : kv.second) cudaFree(q);
+    c.free_blocks.clear();
+    c.cached_bytes = 0;
+    e = cudaMalloc(&p, sz);
+  }
+  GOMIX_CUDA(e);
+  std::lock_guard<std::mutex> lk(c.mu);
+  c.live[p] = {dev, sz};
+  return p;
+}
+
+void cached_free(void* p) {
+  if (!p) return;
+  DeviceCache& c = cache();
+  std::lock_guard<std::mutex> lk(c.mu);
+  auto it = c.live.find(p);
+  if (it == c.live.end()) {
+    cudaFree(p);
+    return;
+  }
+  const auto key = it->second;
+  c.live.erase(it);
+  if (c.cached_bytes + key.second > DeviceCache::kCap) {
+    cudaFree(p);
+    return;
+  }
+  c.free_blocks[key].push_back(p);
+  c.cached_bytes += key.second;
+}
+
+void cached_free_all(std::vector<void*>& blocks) {
+  for (void* p : blocks) cached_free(p);
+  blocks.clear();
+}
+
 Problem::~Problem() {
-  for (void* p : allocations) cudaFree(p);
+  cudaDeviceSynchronize();  // engines' streams may still read the problem (cudaFree used to wait)
+  cached_free_all(allocations);
 }
 
 namespace {
@@ -317,13 +400,13 @@ struct Scratch {
   std::vector<void*> bufs;
   template <typename T>
   T* get(size_t count) {
-    void* p = nullptr;
-    GOMIX_CUDA(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+    void* p = cached_malloc(std::max<size_t>(count, 1) * sizeof(T));
     bufs.push_back(p);
     return static_cast<T*>(p);
   }
   ~Scratch() {
-    for (void* p : bufs) cudaFree(p);
+    cudaDeviceSynchronize();
+    cached_free_all(bufs);
   }
 };
 
