@@ -368,12 +368,11 @@ struct gomix_gpu_engine {
   BeginArgs* d_begin = nullptr;  // per-call criteria read by the graph's begin kernel
   BeginArgs* h_begin = nullptr;  // pinned staging of d_begin
   static constexpr uint64_t kImprInline = 64;  // improvements copied back with every read_ctl
-  double* h_impr = nullptr;                    // pinned [kImprInline]
-  unsigned long long* h_impr_calls = nullptr;  // pinned [kImprInline]
+  static constexpr size_t kCtlBytes = (sizeof(DevCtl) + 63) / 64 * 64;  // control block, then the log
+  ImprRec* h_impr = nullptr;                   // pinned [kImprInline], right after *h_ctl
   unsigned long long* gsteps = nullptr;
   unsigned long long* gcalls = nullptr;
-  double* impr = nullptr;
-  unsigned long long* impr_calls = nullptr;
+  ImprRec* impr = nullptr;  // right after *ctl
   uint64_t impr_cap = 0;
   int32_t* tape = nullptr;
   int32_t* h_tape_pinned = nullptr;
@@ -423,8 +422,6 @@ struct gomix_gpu_engine {
     cached_free_all(allocs);
     if (h_ctl) cudaFreeHost(h_ctl);
     if (h_begin) cudaFreeHost(h_begin);
-    if (h_impr) cudaFreeHost(h_impr);
-    if (h_impr_calls) cudaFreeHost(h_impr_calls);
     if (h_tape_pinned) cudaFreeHost(h_tape_pinned);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
@@ -565,12 +562,14 @@ struct gomix_gpu_engine {
     dh2 = dev_alloc<unsigned long long>(allocs, n);
     ever = dev_alloc<uint32_t>(allocs, nv);
     elit = dev_alloc<uint32_t>(allocs, (nv + 31) / 32);
-    ctl = dev_alloc<DevCtl>(allocs, 1);
+    impr_cap = std::min<uint64_t>(std::max<uint64_t>(4096, n_global * (P->k + 1)), 1ull << 22);
+    {  // control block + improvement log in one block (read back with one copy)
+      char* blk = dev_alloc<char>(allocs, kCtlBytes + impr_cap * sizeof(ImprRec));
+      ctl = reinterpret_cast<DevCtl*>(blk);
+      impr = reinterpret_cast<ImprRec*>(blk + kCtlBytes);
+    }
     gsteps = dev_alloc<unsigned long long>(allocs, P->k);
     gcalls = dev_alloc<unsigned long long>(allocs, P->k);
-    impr_cap = std::min<uint64_t>(std::max<uint64_t>(4096, n_global * (P->k + 1)), 1ull << 22);
-    impr = dev_alloc<double>(allocs, impr_cap);
-    impr_calls = dev_alloc<unsigned long long>(allocs, impr_cap);
     fi_on = (flags & GOMIX_FLAG_FORCED_IMPROVEMENT) != 0;
     if (fi_on && R > 1) invalid("engine: forced improvement needs a single-GPU engine");
     if (epi_mode == 1) {
@@ -601,10 +600,9 @@ struct gomix_gpu_engine {
       ones_local = dev_alloc<uint32_t>(allocs, nv);
       if (!cfg.nccl_unique_id) ones_stage = dev_alloc<uint32_t>(allocs, (uint64_t)R * nv);
     }
-    GOMIX_CUDA(cudaMallocHost(&h_ctl, sizeof(DevCtl)));
+    GOMIX_CUDA(cudaMallocHost(&h_ctl, kCtlBytes + kImprInline * sizeof(ImprRec)));
+    h_impr = reinterpret_cast<ImprRec*>(reinterpret_cast<char*>(h_ctl) + kCtlBytes);
     GOMIX_CUDA(cudaMallocHost(&h_begin, sizeof(BeginArgs)));
-    GOMIX_CUDA(cudaMallocHost(&h_impr, kImprInline * sizeof(double)));
-    GOMIX_CUDA(cudaMallocHost(&h_impr_calls, kImprInline * sizeof(unsigned long long)));
     d_begin = dev_alloc<BeginArgs>(allocs, 1);
     std::memset(h_ctl, 0, sizeof(DevCtl));
     h_ctl->elit_src = -1;
@@ -710,9 +708,8 @@ struct gomix_gpu_engine {
   }
 
   void read_ctl() {
-    GOMIX_CUDA(cudaMemcpyAsync(h_ctl, ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, stream));
-    GOMIX_CUDA(cudaMemcpyAsync(h_impr, impr, std::min(kImprInline, impr_cap) * 8, cudaMemcpyDeviceToHost, stream));
-    GOMIX_CUDA(cudaMemcpyAsync(h_impr_calls, impr_calls, std::min(kImprInline, impr_cap) * 8,
+    // one copy: the control block and the first log entries behind it
+    GOMIX_CUDA(cudaMemcpyAsync(h_ctl, ctl, kCtlBytes + std::min(kImprInline, impr_cap) * sizeof(ImprRec),
                                cudaMemcpyDeviceToHost, stream));
     GOMIX_CUDA(cudaStreamSynchronize(stream));
     ctl_stale = false;
@@ -769,7 +766,6 @@ struct gomix_gpu_engine {
     e.gsteps = gsteps;
     e.gcalls = gcalls;
     e.impr = impr;
-    e.impr_calls = impr_calls;
     e.impr_cap = impr_cap;
     e.fit_all = fit_all;
     e.h1_all = h1_all;
@@ -1732,16 +1728,17 @@ int gomix_gpu_read_improvements(gomix_gpu_engine* e, double* fitness, uint64_t* 
     const uint64_t avail = std::min<uint64_t>(e->h_ctl->n_impr, e->impr_cap);
     const bool any = fitness || evaluator_calls;
     const uint64_t take = any ? std::min(avail, capacity) : 0;
-    if (take && take <= gomix_gpu_engine::kImprInline) {  // copied back with the control block
-      if (fitness) std::memcpy(fitness, e->h_impr, take * 8);
-      if (evaluator_calls) std::memcpy(evaluator_calls, e->h_impr_calls, take * 8);
-    } else if (take) {
-      if (fitness)
-        GOMIX_CUDA(cudaMemcpyAsync(fitness, e->impr, take * 8, cudaMemcpyDeviceToHost, e->stream));
-      if (evaluator_calls)
-        GOMIX_CUDA(cudaMemcpyAsync(evaluator_calls, e->impr_calls, take * 8, cudaMemcpyDeviceToHost,
-                                   e->stream));
+    std::vector<ImprRec> far;
+    const ImprRec* src = e->h_impr;  // copied back with the control block
+    if (take > gomix_gpu_engine::kImprInline) {
+      far.resize(take);
+      GOMIX_CUDA(cudaMemcpyAsync(far.data(), e->impr, take * sizeof(ImprRec), cudaMemcpyDeviceToHost, e->stream));
       GOMIX_CUDA(cudaStreamSynchronize(e->stream));
+      src = far.data();
+    }
+    for (uint64_t i = 0; i < take; ++i) {
+      if (fitness) fitness[i] = src[i].fit;
+      if (evaluator_calls) evaluator_calls[i] = src[i].calls;
     }
     if (count) *count = any ? take : avail;
   });

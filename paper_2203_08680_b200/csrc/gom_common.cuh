@@ -177,8 +177,8 @@ static __device__ void note_improvement(const EpiArgs& a, double f) {
   DevCtl* c = a.ctl;
   const unsigned long long i = c->n_impr++;
   if (i < a.impr_cap) {
-    a.impr[i] = f;
-    a.impr_calls[i] = c->calls_total;
+    a.impr[i].fit = f;
+    a.impr[i].calls = c->calls_total;
   }
   if (c->has_target && (cmp_better(c->exact, f, c->target) || cmp_equal(c->exact, f, c->target)))
     request_stop(c, GOMIX_STOP_TARGET);
@@ -311,8 +311,8 @@ static __device__ void elitist_scan(const EpiArgs& a, const double* s_fit) {
         cur = __shfl_sync(0xFFFFFFFFu, f, l);
         best = (int32_t)(base + l);
         if (lane == 0 && ni < a.impr_cap) {
-          a.impr[ni] = cur;
-          a.impr_calls[ni] = calls_now;
+          a.impr[ni].fit = cur;
+          a.impr[ni].calls = calls_now;
         }
         ++ni;
         hit |= has_target && (cmp_better(exact, cur, target) || cmp_equal(exact, cur, target));

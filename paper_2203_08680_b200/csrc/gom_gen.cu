@@ -315,8 +315,8 @@ __global__ void __launch_bounds__(LEAN ? 256 : (TEAM ? 32 * TW : 256), LEAN ? 3 
           cur = __shfl_sync(0xFFFFFFFFu, f, l);
           best = (int32_t)(base + l);
           if (lead && lane == 0 && ni < a.epi.impr_cap) {
-            a.epi.impr[ni] = cur;
-            a.epi.impr_calls[ni] = calls_now;
+            a.epi.impr[ni].fit = cur;
+            a.epi.impr[ni].calls = calls_now;
           }
           ++ni;
           hit |= b.has_target && cur >= b.target;

@@ -104,6 +104,14 @@ struct Problem {
   ~Problem();
 };
 
+// One elitist improvement (TraceSink::improvement, runtime.hpp:24-29); the log
+// directly follows the control block in device memory, so one copy returns
+// the control block and the first log entries.
+struct ImprRec {
+  double fit;
+  unsigned long long calls;
+};
+
 struct EpiArgs {
   double* fit;
   const double* part;
@@ -117,8 +125,7 @@ struct EpiArgs {
   DevCtl* ctl;
   unsigned long long* gsteps;
   unsigned long long* gcalls;
-  double* impr;
-  unsigned long long* impr_calls;  // RunControl call count when the improvement was reported
+  ImprRec* impr;  // improvement log: fitness + RunControl call count when it was reported
   uint64_t impr_cap;
   uint32_t n, G, nparts, group;  // n: this rank's solutions
   int32_t mode;  // 0 exact atomics, 1 float partials, 2 ordered
