@@ -856,7 +856,10 @@ struct gomix_gpu_engine {
       const uint64_t per = (uint64_t)univ_sliced_sets_per_cta();
       const int g = (int)std::max<uint64_t>(1, std::min<uint64_t>((G + per - 1) / per, (uint64_t)univ_grid_cap));
       a.epi = epi_args(group, (uint32_t)G, (uint32_t)g);
-      launch_univ_sliced(a, univ_planes, (int)Wp, univ_tt, g, st);
+      // graph path, groups after the first: programmatic dependent launch
+      // (truth-table kernel only: it waits on griddepcontrol before reading
+      // the previous group's results)
+      launch_univ_sliced(a, univ_planes, (int)Wp, univ_tt, g, st, univ_tt && slot > 0);
     } else {
       a.epi = epi_args(group, (uint32_t)G, (uint32_t)grid);
       launch_gom(a, P->univariate, P->i32, (int)wpt, tw > 1, grid, (int)block, smem, st);

@@ -443,7 +443,6 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_tt_kernel(const G
   __shared__ unsigned long long s_steps, s_calls;
   __shared__ int s_last;
   probe(a.exp_flags, 40);
-  if (*(volatile int32_t*)&a.ctl->stop) return;
 
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   const uint32_t n = a.n, Wp = MULTI ? a.Wp : (uint32_t)WC, chunks = MULTI ? Wp / WC : 1u;
@@ -464,6 +463,24 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_tt_kernel(const G
     epi.group = gi;
     epi.G = G;
   }
+  // the plan records of the warp's first batch (static data, like the group
+  // order read above, which the generation's begin kernel wrote before the
+  // previous launch started): in flight before the dependency wait.  The
+  // next batch's records are always in flight while one computes.
+  uint4 ra_n = make_uint4(0, 0, 0, 0), rc_n = make_uint4(0, 0, 0, 0);
+  ulonglong2 zk_n = make_ulonglong2(0ull, 0ull);
+  {
+    const uint32_t p0 = (warp * gridDim.x + blockIdx.x) * 32u + lane;
+    if (p0 < G) {
+      ra_n = __ldg(urec + 2u * (size_t)p0);
+      rc_n = __ldg(urec + 2u * (size_t)p0 + 1u);
+      zk_n = __ldg(ukey + p0);
+    }
+  }
+  // programmatic dependent launch (graph path): everything below reads what
+  // the previous group's launch wrote (population, control block, hashes)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (*(volatile int32_t*)&a.ctl->stop) return;
   const unsigned long long eh1 = a.ctl->eh1, eh2 = a.ctl->eh2;
   const int32_t esrc_g = a.ctl->elit_src;
   const uint32_t ever_cur = a.ctl->elit_ver;
@@ -489,18 +506,6 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_tt_kernel(const G
 
   const uint32_t batches = (G + 31u) / 32u;
   const uint32_t bstride = gridDim.x * kUnivWarps;
-  // the plan records of the warp's next batch are in flight while this one
-  // computes (one dependent load level less per batch)
-  uint4 ra_n = make_uint4(0, 0, 0, 0), rc_n = make_uint4(0, 0, 0, 0);
-  ulonglong2 zk_n = make_ulonglong2(0ull, 0ull);
-  {
-    const uint32_t p0 = (warp * gridDim.x + blockIdx.x) * 32u + lane;
-    if (p0 < G) {
-      ra_n = __ldg(urec + 2u * (size_t)p0);
-      rc_n = __ldg(urec + 2u * (size_t)p0 + 1u);
-      zk_n = __ldg(ukey + p0);
-    }
-  }
   // warp-major batch order: the warps that get one batch more than the
   // others are spread over every CTA (and SM) instead of the first CTAs
   for (uint32_t bt = warp * gridDim.x + blockIdx.x; bt < batches; bt += bstride) {
@@ -729,6 +734,9 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_tt_kernel(const G
   }
 
   probe(a.exp_flags, 42);
+  // the next group's launch may start its prologue (it waits for this grid's
+  // completion before touching anything written here)
+  asm volatile("griddepcontrol.launch_dependents;");
   {
     unsigned long long ws = steps, wc = calls;
 #pragma unroll
@@ -835,10 +843,26 @@ int univ_sliced_max_blocks_per_sm(int planes, int wp, bool tt) {
   return blocks;
 }
 
-void launch_univ_sliced(const GomArgs& a, int planes, int wp, bool tt, int grid, cudaStream_t s) {
+void launch_univ_sliced(const GomArgs& a, int planes, int wp, bool tt, int grid, cudaStream_t s, bool pdl) {
   void* fn = univ_kernel(planes, wp, tt);
   void* args[] = {(void*)&a};
-  GOMIX_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kUnivWarps * 32), args, univ_smem(wp), s));
+  if (!pdl) {
+    GOMIX_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kUnivWarps * 32), args, univ_smem(wp), s));
+    return;
+  }
+  // programmatic dependent launch: may begin while the previous kernel on the
+  // stream finishes (the kernel waits with griddepcontrol.wait)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kUnivWarps * 32);
+  cfg.dynamicSmemBytes = univ_smem(wp);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  GOMIX_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
 }
 
 void debug_probes_univ(unsigned long long* out, bool reset) {

@@ -344,7 +344,8 @@ int univ_sliced_planes(uint64_t max_abs_row_sum);  // 0: not representable
 int univ_sliced_block();
 int univ_sliced_sets_per_cta();
 int univ_sliced_max_blocks_per_sm(int planes, int wp, bool tt);
-void launch_univ_sliced(const GomArgs& a, int planes, int wp, bool tt, int grid, cudaStream_t s);
+void launch_univ_sliced(const GomArgs& a, int planes, int wp, bool tt, int grid, cudaStream_t s,
+                        bool pdl = false);
 void build_univ_records(Problem& P);
 void launch_fi_snapshot(const FiArgs& a, cudaStream_t s);
 void launch_fi_flags(const FiArgs& a, bool given, cudaStream_t s);
