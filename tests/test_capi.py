@@ -123,3 +123,15 @@ def test_null_arguments():
     assert L.gomix_gpu_engine_destroy(None) == 0  # delete nullptr is a no-op
     assert L.gomix_gpu_run_generation(None, None, None) == _capi.GOMIX_E_INVALID
     assert L.gomix_gpu_problem_info(None, None) == _capi.GOMIX_E_INVALID
+
+
+def test_flag_constants_match_the_header():
+    """The Python mirror's engine flags are the header's GOMIX_FLAG_* values."""
+    import re
+
+    hdr = open(os.path.join(ROOT, "include", "gomix_gpu.h")).read()
+    vals = {m.group(1): 1 << int(m.group(2)) for m in re.finditer(r"GOMIX_FLAG_(\w+)\s*=\s*1u\s*<<\s*(\d+)", hdr)}
+    from paper_2203_08680_b200 import _capi as K
+    for name, v in vals.items():
+        assert getattr(K, "FLAG_" + name) == v, name
+    assert "FORCED_IMPROVEMENT" in vals and "NO_TRUTH_TABLE" in vals
