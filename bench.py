@@ -290,12 +290,15 @@ def bench_ours(args):
     _, steps1, calls1 = E.group_counters()
     launches = E.launch_count() - launches0
     step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
-    # keep the GPU busy for the clock record when the timed region was short
-    soak_t0 = time.perf_counter()
-    while time.perf_counter() - soak_t0 < max(0.0, 0.6 - t_wall):
-        for _ in range(20):
-            gen()
-        torch.cuda.synchronize()
+    # keep the GPU busy for the clock record when the timed region was short;
+    # the generation count is fixed up front (rank 0's estimate, broadcast):
+    # sharded generations are collectives, so every rank must run the same number
+    soak = [int(max(0.0, 0.6 - t_wall) / max(t_wall / max(1, args.steps), 1e-6))]
+    if dist is not None:
+        dist.broadcast_object_list(soak, src=0)
+    for _ in range(min(soak[0], 20000)):
+        gen()
+    torch.cuda.synchronize()
     E.synchronize()
     clk = clocks.stop()
     # dominant-kernel durations (roofline): the same generations issued launch
