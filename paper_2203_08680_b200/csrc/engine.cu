@@ -152,52 +152,9 @@ std::unique_ptr<Problem> create_problem(const gomix_maxcut* inst, const gomix_fo
   if (device >= 0) GOMIX_CUDA(cudaSetDevice(device));
   GOMIX_CUDA(cudaGetDevice(&P->device));
 
-  // CSR
-  std::vector<int32_t> row_ptr(nv + 1, 0), col(2 * q), eid(2 * q), wi(2 * q);
-  std::vector<double> w(2 * q);
-  std::vector<int64_t> indeg(nv, 0);
-  for (uint64_t i = 0; i < q; ++i) {
-    row_ptr[inst->edge_u[i] + 1]++;
-    row_ptr[inst->edge_v[i] + 1]++;
-    indeg[inst->edge_v[i]]++;
-  }
-  for (uint64_t v = 0; v < nv; ++v) row_ptr[v + 1] += row_ptr[v];
-  std::vector<int64_t> rev(nv), fwd(nv);
-  for (uint64_t v = 0; v < nv; ++v) {
-    rev[v] = row_ptr[v];
-    fwd[v] = row_ptr[v] + indeg[v];
-  }
-  uint64_t max_deg_sum = 0;
-  for (uint64_t i = 0; i < q; ++i) {
-    const uint32_t u = inst->edge_u[i], v = inst->edge_v[i];
-    const double x = inst->edge_w[i];
-    const int64_t a = fwd[u]++, b = rev[v]++;
-    col[a] = (int32_t)v;
-    col[b] = (int32_t)u;
-    eid[a] = eid[b] = (int32_t)i;
-    w[a] = w[b] = x;
-    wi[a] = wi[b] = exact && std::fabs(x) < 2147483648.0 ? (int32_t)x : 0;
-  }
-  for (uint64_t i = 0; i < m; ++i) {
-    uint64_t s = 0;
-    for (uint64_t t = P->h_set_off[i]; t < P->h_set_off[i + 1]; ++t)
-      s += (uint64_t)(row_ptr[P->h_set_vars[t] + 1] - row_ptr[P->h_set_vars[t]]);
-    max_deg_sum = std::max(max_deg_sum, s);
-  }
-  // int32 per-pair arithmetic is exact when |delta| <= max|w| * footprint < 2^30
-  P->i32 = exact && maxw * (double)std::max<uint64_t>(max_deg_sum, 1) < 1073741824.0;
-  P->wbits = 1;
-  while (P->i32 && P->wbits < 31 && (double)(1u << P->wbits) <= maxw) ++P->wbits;
-  if (P->univariate) {
-    for (uint64_t i = 0; i < m; ++i) {
-      const uint32_t v = P->h_set_vars[i];
-      P->max_fp = std::max<uint64_t>(P->max_fp, (uint64_t)(row_ptr[v + 1] - row_ptr[v]));
-      uint64_t a = 0;
-      for (int32_t e = row_ptr[v]; e < row_ptr[v + 1]; ++e) a += (uint64_t)std::llabs((long long)wi[e]);
-      P->max_abs_row = std::max(P->max_abs_row, a);
-    }
-  }
-
+  // CSR, built on the device from the uploaded edge list (build_csr_device):
+  // row v = v's neighbours ascending = its edges in ascending edge id (the
+  // reference's summation order for sorted edge lists)
   auto& A = P->allocations;
   P->row_ptr = dev_alloc<int32_t>(A, nv + 1);
   P->col = dev_alloc<int32_t>(A, 2 * q);
@@ -212,17 +169,34 @@ std::unique_ptr<Problem> create_problem(const gomix_maxcut* inst, const gomix_fo
   auto up = [](void* dst, const void* src, size_t bytes) {
     if (bytes) GOMIX_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
   };
-  up(P->row_ptr, row_ptr.data(), (nv + 1) * 4);
-  up(P->col, col.data(), 2 * q * 4);
-  up(P->w, w.data(), 2 * q * 8);
-  up(P->wi, wi.data(), 2 * q * 4);
   up(P->eu, inst->edge_u, q * 4);
   up(P->ev, inst->edge_v, q * 4);
   up(P->ew, inst->edge_w, q * 8);
   std::vector<int64_t> so(P->h_set_off.begin(), P->h_set_off.end());
   up(P->set_off, so.data(), (m + 1) * 8);
   up(P->set_vars, P->h_set_vars.data(), entries * 4);
-  up(d_eid, eid.data(), 2 * q * 4);
+  uint64_t max_abs_row = 0;
+  build_csr_device(*P, exact, d_eid, &max_abs_row);
+  std::vector<int32_t> row_ptr(nv + 1);
+  GOMIX_CUDA(cudaMemcpy(row_ptr.data(), P->row_ptr, (nv + 1) * 4, cudaMemcpyDeviceToHost));
+  uint64_t max_deg_sum = 0;
+  for (uint64_t i = 0; i < m; ++i) {
+    uint64_t s = 0;
+    for (uint64_t t = P->h_set_off[i]; t < P->h_set_off[i + 1]; ++t)
+      s += (uint64_t)(row_ptr[P->h_set_vars[t] + 1] - row_ptr[P->h_set_vars[t]]);
+    max_deg_sum = std::max(max_deg_sum, s);
+  }
+  // int32 per-pair arithmetic is exact when |delta| <= max|w| * footprint < 2^30
+  P->i32 = exact && maxw * (double)std::max<uint64_t>(max_deg_sum, 1) < 1073741824.0;
+  P->wbits = 1;
+  while (P->i32 && P->wbits < 31 && (double)(1u << P->wbits) <= maxw) ++P->wbits;
+  if (P->univariate) {
+    for (uint64_t i = 0; i < m; ++i) {
+      const uint32_t v = P->h_set_vars[i];
+      P->max_fp = std::max<uint64_t>(P->max_fp, (uint64_t)(row_ptr[v + 1] - row_ptr[v]));
+    }
+    P->max_abs_row = max_abs_row;  // over every vertex: univariate sets cover a subset of them
+  }
   mark("csr+upload");
   build_problem_device_impl(*P, colour, d_eid);
   // truth-table plan of the bit-sliced univariate kernel (every variable of

@@ -347,6 +347,7 @@ int univ_sliced_max_blocks_per_sm(int planes, int wp, bool tt);
 void launch_univ_sliced(const GomArgs& a, int planes, int wp, bool tt, int grid, cudaStream_t s,
                         bool pdl = false);
 void build_univ_records(Problem& P);
+void build_csr_device(Problem& P, bool exact, int32_t* d_eid, uint64_t* max_abs_row);  // problem.cu
 void launch_fi_snapshot(const FiArgs& a, cudaStream_t s);
 void launch_fi_flags(const FiArgs& a, bool given, cudaStream_t s);
 void launch_fi_tape(const FiArgs& a, uint64_t g0, uint64_t G, int32_t* tape, cudaStream_t s);

@@ -452,6 +452,84 @@ void seg_sort_unique(Scratch& S, uint32_t* cand, const int64_t* cand_off, uint64
 
 }  // namespace
 
+// ---- CSR from the edge list (create_problem) ---------------------------------
+namespace {
+__global__ void csr_count_kernel(const uint32_t* eu, const uint32_t* ev, uint64_t q, int32_t* cnt) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < q; i += (uint64_t)gridDim.x * blockDim.x) {
+    atomicAdd(&cnt[eu[i] + 1], 1);
+    atomicAdd(&cnt[ev[i] + 1], 1);
+  }
+}
+// key = (row << 32) | neighbour: sorting makes every row contiguous and ascending
+__global__ void csr_keys_kernel(const uint32_t* eu, const uint32_t* ev, uint64_t q, unsigned long long* key,
+                                int32_t* val) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < q; i += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned long long u = eu[i], v = ev[i];
+    key[2 * i] = (u << 32) | v;
+    key[2 * i + 1] = (v << 32) | u;
+    val[2 * i] = val[2 * i + 1] = (int32_t)i;
+  }
+}
+__global__ void csr_fill_kernel(const unsigned long long* key, const int32_t* eidv, const double* ew, uint64_t cnt,
+                                int32_t exact, int32_t* col, int32_t* eid, double* w, int32_t* wi) {
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cnt; j += (uint64_t)gridDim.x * blockDim.x) {
+    const int32_t e = eidv[j];
+    const double x = ew[e];
+    col[j] = (int32_t)(uint32_t)(key[j] & 0xFFFFFFFFull);
+    eid[j] = e;
+    w[j] = x;
+    wi[j] = exact && fabs(x) < 2147483648.0 ? (int32_t)x : 0;
+  }
+}
+// max over rows of sum |wi| (the univariate kernels' plane count)
+__global__ void csr_row_abs_kernel(const int32_t* row_ptr, const int32_t* wi, uint64_t nv, unsigned long long* mx) {
+  for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += (uint64_t)gridDim.x * blockDim.x) {
+    unsigned long long a = 0;
+    for (int32_t e = row_ptr[v]; e < row_ptr[v + 1]; ++e) a += (unsigned long long)llabs((long long)wi[e]);
+    atomicMax(mx, a);
+  }
+}
+unsigned grid_for(uint64_t work) { return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((work + 255) / 256, 65535)); }
+}  // namespace
+
+void build_csr_device(Problem& P, bool exact, int32_t* d_eid, uint64_t* max_abs_row) {
+  Scratch S;
+  const uint64_t nv = P.nv, q = P.q, cnt2 = 2 * q;
+  int32_t* cnt = S.get<int32_t>(nv + 1);
+  GOMIX_CUDA(cudaMemset(cnt, 0, (nv + 1) * sizeof(int32_t)));
+  if (q) csr_count_kernel<<<grid_for(q), 256>>>(P.eu, P.ev, q, cnt);
+  GOMIX_CUDA(cudaGetLastError());
+  {
+    size_t bytes = 0;
+    GOMIX_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, cnt, P.row_ptr, (int64_t)(nv + 1)));
+    void* tmp = S.get<char>(bytes);
+    GOMIX_CUDA(cub::DeviceScan::InclusiveSum(tmp, bytes, cnt, P.row_ptr, (int64_t)(nv + 1)));
+  }
+  if (q) {
+    unsigned long long* key = S.get<unsigned long long>(cnt2);
+    unsigned long long* key_s = S.get<unsigned long long>(cnt2);
+    int32_t* val = S.get<int32_t>(cnt2);
+    int32_t* val_s = S.get<int32_t>(cnt2);
+    csr_keys_kernel<<<grid_for(q), 256>>>(P.eu, P.ev, q, key, val);
+    GOMIX_CUDA(cudaGetLastError());
+    int end_bit = 64;  // only the bits a vertex id can occupy
+    while (end_bit > 33 && !((nv - 1) >> (end_bit - 33))) --end_bit;
+    size_t bytes = 0;
+    GOMIX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, key, key_s, val, val_s, (int64_t)cnt2, 0, end_bit));
+    void* tmp = S.get<char>(bytes);
+    GOMIX_CUDA(cub::DeviceRadixSort::SortPairs(tmp, bytes, key, key_s, val, val_s, (int64_t)cnt2, 0, end_bit));
+    csr_fill_kernel<<<grid_for(cnt2), 256>>>(key_s, val_s, P.ew, cnt2, exact ? 1 : 0, P.col, d_eid, P.w, P.wi);
+    GOMIX_CUDA(cudaGetLastError());
+  }
+  unsigned long long* mx = S.get<unsigned long long>(1);
+  GOMIX_CUDA(cudaMemset(mx, 0, sizeof(unsigned long long)));
+  csr_row_abs_kernel<<<grid_for(nv), 256>>>(P.row_ptr, P.wi, nv, mx);
+  GOMIX_CUDA(cudaGetLastError());
+  unsigned long long h = 0;
+  GOMIX_CUDA(cudaMemcpy(&h, mx, sizeof(h), cudaMemcpyDeviceToHost));
+  *max_abs_row = h;
+}
+
 // Device part of problem construction.  Expects P's CSR, edge list and FOS
 // already uploaded (row_ptr, col, eu, ev, ew, set_off, set_vars) and eid in
 // `eid` (CSR entry -> edge id).
