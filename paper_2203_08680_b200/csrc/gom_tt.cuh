@@ -1,0 +1,309 @@
+// gom_tt.cuh — the truth-table univariate GOM step (degree <= 4, Philox,
+// rows of WC <= 4 words) as a device function: the batch loop shared by the
+// per-group kernel (gom_univ_tt_kernel, gom_univ.cu) and the persistent
+// whole-generation kernel (gom_generation_kernel's truth-table mode,
+// gom_gen.cu).  Semantics and layout: gom_univ.cu's header and DESIGN.md §4.
+#pragma once
+
+#include "gom_common.cuh"
+
+namespace gomix_b200 {
+
+constexpr int kUnivWarps = 8;        // warps per CTA of the univariate kernels
+constexpr uint32_t kSparseKeys = 6;  // hash deltas key by key up to this many accepted sets per solution
+
+template <int WP>
+__device__ __forceinline__ void load_row(const uint32_t* row, uint32_t (&x)[WP]) {
+  if constexpr (WP == 4) {
+    const uint4 t = __ldg(reinterpret_cast<const uint4*>(row));
+    x[0] = t.x; x[1] = t.y; x[2] = t.z; x[3] = t.w;
+  } else if constexpr (WP == 2) {
+    const uint2 t = __ldg(reinterpret_cast<const uint2*>(row));
+    x[0] = t.x; x[1] = t.y;
+  } else {
+    x[0] = __ldg(row);
+  }
+}
+
+// neighbour rows are written by no lane of this launch (same-colour sets are
+// not adjacent), so the read-only path is safe for them too
+template <int WP>
+__device__ __forceinline__ void store_row(uint32_t* row, const uint32_t (&x)[WP]) {
+  if constexpr (WP == 4) {
+    *reinterpret_cast<uint4*>(row) = make_uint4(x[0], x[1], x[2], x[3]);
+  } else if constexpr (WP == 2) {
+    *reinterpret_cast<uint2*>(row) = make_uint2(x[0], x[1]);
+  } else {
+    row[0] = x[0];
+  }
+}
+
+// 64-bit XOR into shared memory as two native 32-bit atomics (a 64-bit
+// shared atomic XOR compiles to a compare-and-swap loop)
+__device__ __forceinline__ void xor_shared64(unsigned long long* p, unsigned long long v) {
+  unsigned int* q = reinterpret_cast<unsigned int*>(p);
+  const unsigned int lo = (unsigned int)v, hi = (unsigned int)(v >> 32);
+  if (lo) atomicXor(q, lo);
+  if (hi) atomicXor(q + 1, hi);
+}
+
+// leaf masks of a 16-entry table held in bits [16*half, 16*half + 16) of tt
+__device__ __forceinline__ void tt_masks(uint32_t tt, int half, uint32_t (&m)[16]) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) m[i] = (uint32_t)((int32_t)(tt << (31 - (16 * half + i))) >> 31);
+}
+
+// bit-sliced lookup: bit s of the result = table[p_s], p_s = b0_s | b1_s<<1 | b2_s<<2 | b3_s<<3
+__device__ __forceinline__ uint32_t tt_mux(const uint32_t (&m)[16], uint32_t b0, uint32_t b1, uint32_t b2,
+                                           uint32_t b3) {
+  uint32_t l0[8], l1[4], l2[2];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) l0[q] = (b0 & m[2 * q + 1]) | (~b0 & m[2 * q]);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) l1[q] = (b1 & l0[2 * q + 1]) | (~b1 & l0[2 * q]);
+#pragma unroll
+  for (int q = 0; q < 2; ++q) l2[q] = (b2 & l1[2 * q + 1]) | (~b2 & l1[2 * q]);
+  return (b3 & l2[1]) | (~b3 & l2[0]);
+}
+
+__device__ __forceinline__ int32_t w16(uint32_t packed, int hi) {
+  return hi ? ((int32_t)packed >> 16) : ((int32_t)(packed << 16) >> 16);
+}
+
+// per-CTA scratch of the batch loop
+struct TtShared {
+  unsigned long long key[kUnivWarps][32][2];      // the warp's sets' Zobrist keys
+  unsigned long long tbl[kUnivWarps][8][16][2];   // 4-bit-chunk key XOR tables
+  ulonglong2 wh[kUnivWarps][4 * 32];              // per-warp hash deltas of the CTA's solutions
+};
+
+// The plan records of a warp's next batch, in flight while a batch computes.
+struct TtNext {
+  uint4 ra, rc;
+  ulonglong2 zk;
+};
+
+__device__ __forceinline__ TtNext tt_fetch(const uint4* urec, const ulonglong2* ukey, uint32_t G, uint32_t p) {
+  TtNext r;
+  r.ra = make_uint4(0, 0, 0, 0);
+  r.rc = make_uint4(0, 0, 0, 0);
+  r.zk = make_ulonglong2(0ull, 0ull);
+  if (p < G) {
+    r.ra = __ldg(urec + 2u * (size_t)p);
+    r.rc = __ldg(urec + 2u * (size_t)p + 1u);
+    r.zk = __ldg(ukey + p);
+  }
+  return r;
+}
+
+// The batches of one colour group handled by this warp: warp-major batch
+// order (bt = warp * gridDim.x + blockIdx.x, then + gridDim.x * kUnivWarps),
+// `nx` = the first batch's records (fetched by the caller).  Commits the
+// accepted flips in place, records the elitist's old bits copy-on-write,
+// accumulates fitness deltas into s_dfit (per solution, shared atomics) and
+// hash deltas into sh.wh[warp] (this warp's own slice), counts steps/calls.
+// s_elit: group-start "parent == elitist" mask per word.
+template <int B, int WC>
+__device__ __forceinline__ void tt_batches(const GomArgs& a, const uint4* urec, const ulonglong2* ukey, uint32_t G,
+                                           TtNext nx, const uint32_t* s_elit, long long* s_dfit, TtShared& sh,
+                                           int32_t esrc, uint32_t ever_cur, uint32_t lane, uint32_t warp,
+                                           unsigned long long& steps, unsigned long long& calls) {
+  constexpr uint32_t Wp = (uint32_t)WC;
+  const uint32_t n = a.n;
+  const uint32_t batches = (G + 31u) / 32u;
+  const uint32_t bstride = gridDim.x * kUnivWarps;
+  for (uint32_t bt = warp * gridDim.x + blockIdx.x; bt < batches; bt += bstride) {
+    const uint32_t p = bt * 32u + lane;
+    const bool live = p < G;
+    const uint4 ra = nx.ra, rc = nx.rc;
+    const ulonglong2 zk = nx.zk;
+    nx = tt_fetch(urec, ukey, G, p + bstride * 32u);
+    const uint32_t v = ra.x;
+    const uint32_t u[4] = {rc.x, rc.y, rc.z, rc.w};
+    uint32_t x[WC], nb[4][WC];
+#pragma unroll
+    for (int j = 0; j < WC; ++j) {
+      x[j] = 0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) nb[t][j] = 0;
+    }
+    if (live) {
+      load_row<WC>(a.pop + (size_t)v * Wp, x);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) load_row<WC>(a.pop + (size_t)u[t] * Wp, nb[t]);
+    }
+    int32_t w[4];
+    w[0] = w16(ra.z, 0);
+    w[1] = w16(ra.z, 1);
+    w[2] = w16(ra.w, 0);
+    w[3] = w16(ra.w, 1);
+    uint32_t neg[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) neg[t] = w[t] < 0 ? 0xFFFFFFFFu : 0u;
+    const uint32_t deg = (uint32_t)(u[0] != v) + (uint32_t)(u[1] != v) + (uint32_t)(u[2] != v) + (uint32_t)(u[3] != v);
+    // ---- presence: some member (over every rank's shard) holds the other value
+    uint32_t ones = 0;
+    if (live) {
+      if (a.ones) {
+        ones = a.ones[v];
+      } else if (a.R == 1) {
+#pragma unroll
+        for (int j = 0; j < WC; ++j) ones += __popc(x[j]);
+      } else {
+        for (uint32_t r = 0; r < a.R; ++r) {
+          uint32_t y[WC];
+          load_row<WC>(a.pool + ((size_t)r * a.nv + v) * Wp, y);
+#pragma unroll
+          for (int j = 0; j < WC; ++j) ones += __popc(y[j]);
+        }
+      }
+    }
+    const bool present = live && ones > 0u && ones < a.n_global;
+    if (present) {
+      steps += n;
+      calls += (unsigned long long)n * deg;
+    }
+    const uint32_t pmask = present ? 0xFFFFFFFFu : 0u;
+    // ---- b words (edge "uncut-gain" bits), then accept via the LE table
+    // (LT | LE & ~elitist where the group-start elitist lives)
+    uint32_t bw[4][WC], acc[WC];
+    bool any = false;
+#pragma unroll
+    for (int j = 0; j < WC; ++j)
+#pragma unroll
+      for (int t = 0; t < 4; ++t) bw[t][j] = x[j] ^ nb[t][j] ^ neg[t];
+    {
+      uint32_t mle[16];
+      tt_masks(ra.y, 1, mle);
+#pragma unroll
+      for (int j = 0; j < WC; ++j) {
+        uint32_t ac = tt_mux(mle, bw[0][j], bw[1][j], bw[2][j], bw[3][j]);
+        const uint32_t ew = s_elit[j];
+        if (ew) {  // warp-uniform: group-start elitist copies take strict improvements only
+          uint32_t e = ew, keep = 0xFFFFFFFFu;
+          while (e) {
+            const uint32_t b = (uint32_t)(__ffs(e) - 1);
+            e &= e - 1u;
+            const uint32_t pat = ((bw[0][j] >> b) & 1u) | (((bw[1][j] >> b) & 1u) << 1) |
+                                 (((bw[2][j] >> b) & 1u) << 2) | (((bw[3][j] >> b) & 1u) << 3);
+            if (!((ra.y >> pat) & 1u)) keep &= ~(1u << b);  // LT[p] bit of the table
+          }
+          ac &= keep;
+        }
+        acc[j] = ac & pmask & valid_mask((uint32_t)j, n);
+        any |= acc[j] != 0u;
+      }
+    }
+    // ---- commit: accepted solutions flip v (apply_acceptance, :221-247)
+    if (any) {
+      uint32_t nw[WC];
+#pragma unroll
+      for (int j = 0; j < WC; ++j) nw[j] = x[j] ^ acc[j];
+      store_row<WC>(a.pop + (size_t)v * Wp, nw);
+      if (esrc >= 0) {
+        const uint32_t ew = (uint32_t)esrc >> 5, eb = (uint32_t)esrc & 31u;
+        uint32_t aw = 0, xw = 0;
+#pragma unroll
+        for (int j = 0; j < WC; ++j)
+          if ((uint32_t)j == ew) {
+            aw = acc[j];
+            xw = x[j];
+          }
+        if ((aw >> eb) & 1u) capture_row(a.elit, a.ever, ever_cur, v, (xw >> eb) & 1u);
+      }
+    }
+    // ---- per-solution reductions over the warp's 32 sets ----------------
+    if (__any_sync(0xFFFFFFFFu, any)) {
+      sh.key[warp][lane][0] = zk.x;
+      sh.key[warp][lane][1] = zk.y;
+      __syncwarp();
+      bool tbl = false;
+      uint32_t mlt[16];
+      tt_masks(ra.y, 0, mlt);
+#pragma unroll
+      for (int j = 0; j < WC; ++j) {
+        if (!__any_sync(0xFFFFFFFFu, acc[j] != 0u)) continue;
+        const uint32_t accT = transpose32(acc[j], lane);  // lane b: sets l accepted by solution 32j+b
+        const uint32_t b0 = bw[0][j], b1 = bw[1][j], b2 = bw[2][j], b3 = bw[3][j];
+        long long d = 0;
+        const uint32_t imp = acc[j] & tt_mux(mlt, b0, b1, b2, b3);
+        if (__any_sync(0xFFFFFFFFu, imp != 0u)) {
+          // T planes of this word (only words with a strictly improving pair)
+          uint32_t T[B];
+#pragma unroll
+          for (int k = 0; k < B; ++k) T[k] = 0;
+          const uint32_t bb[4] = {b0, b1, b2, b3};
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const uint32_t mg = (uint32_t)abs(w[t]);
+            uint32_t cy = 0;
+#pragma unroll
+            for (int k = 0; k < B; ++k) {
+              const uint32_t xb = ((mg >> k) & 1u) ? bb[t] : 0u;
+              const uint32_t tk = T[k];
+              T[k] = tk ^ xb ^ cy;
+              cy = (tk & xb) | (tk & cy) | (xb & cy);
+            }
+          }
+          const uint32_t impT = transpose32(imp, lane);
+          const uint32_t A = (uint32_t)(abs(w[0]) + abs(w[1]) + abs(w[2]) + abs(w[3]));
+#pragma unroll
+          for (int k = 0; k < B; ++k) d += (long long)__popc(impT & __ballot_sync(0xFFFFFFFFu, (A >> k) & 1u)) << k;
+#pragma unroll
+          for (int k = 0; k < B - 1; ++k) d -= (long long)__popc(transpose32(T[k] & imp, lane)) << (k + 1);
+        }
+        const uint32_t sj = (uint32_t)j * 32u + lane;
+        if (d) atomicAdd(reinterpret_cast<unsigned long long*>(&s_dfit[sj]), (unsigned long long)d);
+        // hash delta of solution 32j+lane: XOR of the keys of its accepted
+        // sets — key by key when every solution of the word accepted few
+        // sets (the steady state: neutral flips are sparse), else through the
+        // 4-bit-chunk table of key XORs
+        unsigned long long x1 = 0, x2 = 0;
+        if (__reduce_max_sync(0xFFFFFFFFu, (uint32_t)__popc(accT)) <= kSparseKeys) {
+          uint32_t r = accT;
+          while (r) {
+            const uint32_t l = (uint32_t)(__ffs(r) - 1);
+            r &= r - 1u;
+            const ulonglong2 k = *reinterpret_cast<const ulonglong2*>(sh.key[warp][l]);
+            x1 ^= k.x;
+            x2 ^= k.y;
+          }
+        } else {
+          if (!tbl) {
+            tbl = true;
+            const uint32_t q = lane >> 2, sub = lane & 3u;
+            const ulonglong2 k0 = *reinterpret_cast<const ulonglong2*>(sh.key[warp][4 * q + 0]);
+            const ulonglong2 k1 = *reinterpret_cast<const ulonglong2*>(sh.key[warp][4 * q + 1]);
+            const ulonglong2 k2 = *reinterpret_cast<const ulonglong2*>(sh.key[warp][4 * q + 2]);
+            const ulonglong2 k3 = *reinterpret_cast<const ulonglong2*>(sh.key[warp][4 * q + 3]);
+            const unsigned long long l1 = ((sub & 1u) ? k0.x : 0ull) ^ ((sub & 2u) ? k1.x : 0ull);
+            const unsigned long long l2 = ((sub & 1u) ? k0.y : 0ull) ^ ((sub & 2u) ? k1.y : 0ull);
+            ulonglong2* tb = reinterpret_cast<ulonglong2*>(sh.tbl[warp][q]);
+            tb[sub] = make_ulonglong2(l1, l2);
+            tb[sub + 4] = make_ulonglong2(l1 ^ k2.x, l2 ^ k2.y);
+            tb[sub + 8] = make_ulonglong2(l1 ^ k3.x, l2 ^ k3.y);
+            tb[sub + 12] = make_ulonglong2(l1 ^ k2.x ^ k3.x, l2 ^ k2.y ^ k3.y);
+            __syncwarp();
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const uint32_t m = (accT >> (4 * q)) & 15u;
+            const ulonglong2 tq = *reinterpret_cast<const ulonglong2*>(sh.tbl[warp][q][m]);
+            x1 ^= tq.x;
+            x2 ^= tq.y;
+          }
+        }
+        if (x1 | x2) {  // the warp's own running hash deltas: no atomics
+          ulonglong2* q = &sh.wh[warp][j * 32 + lane];
+          ulonglong2 o = *q;
+          o.x ^= x1;
+          o.y ^= x2;
+          *q = o;
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace gomix_b200

@@ -32,50 +32,12 @@
 #include <stdint.h>
 
 #include "gom_common.cuh"
+#include "gom_tt.cuh"
 
 namespace gomix_b200 {
 
 namespace {
-
-template <int WP>
-__device__ __forceinline__ void load_row(const uint32_t* row, uint32_t (&x)[WP]) {
-  if constexpr (WP == 4) {
-    const uint4 t = __ldg(reinterpret_cast<const uint4*>(row));
-    x[0] = t.x; x[1] = t.y; x[2] = t.z; x[3] = t.w;
-  } else if constexpr (WP == 2) {
-    const uint2 t = __ldg(reinterpret_cast<const uint2*>(row));
-    x[0] = t.x; x[1] = t.y;
-  } else {
-    x[0] = __ldg(row);
-  }
-}
-
-// neighbour rows are written by no lane of this launch (same-colour sets are
-// not adjacent), so the read-only path is safe for them too
-template <int WP>
-__device__ __forceinline__ void store_row(uint32_t* row, const uint32_t (&x)[WP]) {
-  if constexpr (WP == 4) {
-    *reinterpret_cast<uint4*>(row) = make_uint4(x[0], x[1], x[2], x[3]);
-  } else if constexpr (WP == 2) {
-    *reinterpret_cast<uint2*>(row) = make_uint2(x[0], x[1]);
-  } else {
-    row[0] = x[0];
-  }
-}
-
-constexpr int kUnivWarps = 8;  // warps per CTA
-constexpr uint32_t kSparseKeys = 6;  // hash deltas key by key up to this many accepted sets per solution
-
-// 64-bit XOR into shared memory as two native 32-bit atomics (a 64-bit
-// shared atomic XOR compiles to a compare-and-swap loop)
-__device__ __forceinline__ void xor_shared64(unsigned long long* p, unsigned long long v) {
-  unsigned int* q = reinterpret_cast<unsigned int*>(p);
-  const unsigned int lo = (unsigned int)v, hi = (unsigned int)(v >> 32);
-  if (lo) atomicXor(q, lo);
-  if (hi) atomicXor(q + 1, hi);
-}
-constexpr int kNbChunk = 4;    // neighbour (col, w) pairs fetched per round
-
+constexpr int kNbChunk = 4;  // neighbour (col, w) pairs fetched per round
 }  // namespace
 
 template <int B, int WC, bool MULTI>
@@ -373,32 +335,7 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_sliced_kernel(con
 // carries the neighbour ids and weights, so a set costs two coalesced
 // 16-byte loads before its rows (no gvars -> row_ptr -> col chain).
 // ---------------------------------------------------------------------------
-namespace {
 
-// leaf masks of a 16-entry table held in bits [16*half, 16*half + 16) of tt
-__device__ __forceinline__ void tt_masks(uint32_t tt, int half, uint32_t (&m)[16]) {
-#pragma unroll
-  for (int i = 0; i < 16; ++i) m[i] = (uint32_t)((int32_t)(tt << (31 - (16 * half + i))) >> 31);
-}
-
-// bit-sliced lookup: bit s of the result = table[p_s], p_s = b0_s | b1_s<<1 | b2_s<<2 | b3_s<<3
-__device__ __forceinline__ uint32_t tt_mux(const uint32_t (&m)[16], uint32_t b0, uint32_t b1, uint32_t b2,
-                                           uint32_t b3) {
-  uint32_t l0[8], l1[4], l2[2];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) l0[q] = (b0 & m[2 * q + 1]) | (~b0 & m[2 * q]);
-#pragma unroll
-  for (int q = 0; q < 4; ++q) l1[q] = (b1 & l0[2 * q + 1]) | (~b1 & l0[2 * q]);
-#pragma unroll
-  for (int q = 0; q < 2; ++q) l2[q] = (b2 & l1[2 * q + 1]) | (~b2 & l1[2 * q]);
-  return (b3 & l2[1]) | (~b3 & l2[0]);
-}
-
-__device__ __forceinline__ int32_t w16(uint32_t packed, int hi) {
-  return hi ? ((int32_t)packed >> 16) : ((int32_t)(packed << 16) >> 16);
-}
-
-}  // namespace
 
 // One record pair per group position: r[2p] = {v, LT | LE << 16, w0 | w1 << 16,
 // w2 | w3 << 16} (int16 weights in CSR order = ascending neighbour), r[2p+1] =
@@ -434,22 +371,19 @@ __global__ void build_univ_records_kernel(const uint32_t* gvars, const int32_t* 
   key[p] = make_ulonglong2(z1, z2);
 }
 
-template <int B, int WC, bool MULTI>
+template <int B, int WC>
 __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_tt_kernel(const GomArgs a) {
-  extern __shared__ __align__(16) unsigned char dyn[];
-  __shared__ __align__(16) unsigned long long s_key[kUnivWarps][32][2];
-  __shared__ __align__(16) unsigned long long s_tbl[kUnivWarps][8][16][2];
-  __shared__ __align__(16) ulonglong2 s_wh[kUnivWarps][4 * 32];  // per-warp hash deltas (Wp <= 4)
+  __shared__ __align__(16) TtShared sh;
+  __shared__ long long s_dfit[WC * 32];
+  __shared__ unsigned long long s_dh1[WC * 32], s_dh2[WC * 32];
+  __shared__ uint32_t s_elit[WC];
   __shared__ unsigned long long s_steps, s_calls;
   __shared__ int s_last;
   probe(a.exp_flags, 40);
 
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  const uint32_t n = a.n, Wp = MULTI ? a.Wp : (uint32_t)WC, chunks = MULTI ? Wp / WC : 1u;
-  long long* s_dfit = reinterpret_cast<long long*>(dyn);
-  unsigned long long* s_dh1 = reinterpret_cast<unsigned long long*>(s_dfit + Wp * 32u);
-  unsigned long long* s_dh2 = s_dh1 + Wp * 32u;
-  uint32_t* s_elit = reinterpret_cast<uint32_t*>(s_dh2 + Wp * 32u);
+  constexpr uint32_t Wp = (uint32_t)WC;
+  const uint32_t n = a.n;
   uint32_t G = a.G;
   const uint4* urec = a.urec;
   const ulonglong2* ukey = a.ukey;
@@ -465,18 +399,8 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_tt_kernel(const G
   }
   // the plan records of the warp's first batch (static data, like the group
   // order read above, which the generation's begin kernel wrote before the
-  // previous launch started): in flight before the dependency wait.  The
-  // next batch's records are always in flight while one computes.
-  uint4 ra_n = make_uint4(0, 0, 0, 0), rc_n = make_uint4(0, 0, 0, 0);
-  ulonglong2 zk_n = make_ulonglong2(0ull, 0ull);
-  {
-    const uint32_t p0 = (warp * gridDim.x + blockIdx.x) * 32u + lane;
-    if (p0 < G) {
-      ra_n = __ldg(urec + 2u * (size_t)p0);
-      rc_n = __ldg(urec + 2u * (size_t)p0 + 1u);
-      zk_n = __ldg(ukey + p0);
-    }
-  }
+  // previous launch started): in flight before the dependency wait
+  const TtNext first = tt_fetch(urec, ukey, G, (warp * gridDim.x + blockIdx.x) * 32u + lane);
   // programmatic dependent launch (graph path): everything below reads what
   // the previous group's launch wrote (population, control block, hashes)
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -494,7 +418,7 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_tt_kernel(const G
   for (uint32_t i = threadIdx.x; i < Wp * 32u; i += blockDim.x) {
     s_dfit[i] = 0;
 #pragma unroll
-    for (int q = 0; q < kUnivWarps; ++q) s_wh[q][i] = make_ulonglong2(0ull, 0ull);
+    for (int q = 0; q < kUnivWarps; ++q) sh.wh[q][i] = make_ulonglong2(0ull, 0ull);
   }
   if (threadIdx.x == 0) {
     s_steps = 0;
@@ -503,235 +427,7 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_tt_kernel(const G
   __syncthreads();
   probe(a.exp_flags, 41);
   unsigned long long steps = 0, calls = 0;
-
-  const uint32_t batches = (G + 31u) / 32u;
-  const uint32_t bstride = gridDim.x * kUnivWarps;
-  // warp-major batch order: the warps that get one batch more than the
-  // others are spread over every CTA (and SM) instead of the first CTAs
-  for (uint32_t bt = warp * gridDim.x + blockIdx.x; bt < batches; bt += bstride) {
-    const uint32_t p = bt * 32u + lane;
-    const bool live = p < G;
-    const uint4 ra = ra_n, rc = rc_n;
-    const ulonglong2 zk = zk_n;
-    {
-      const uint32_t pn = p + bstride * 32u;
-      ra_n = make_uint4(0, 0, 0, 0);
-      rc_n = make_uint4(0, 0, 0, 0);
-      zk_n = make_ulonglong2(0ull, 0ull);
-      if (pn < G) {
-        ra_n = __ldg(urec + 2u * (size_t)pn);
-        rc_n = __ldg(urec + 2u * (size_t)pn + 1u);
-        zk_n = __ldg(ukey + pn);
-      }
-    }
-    const uint32_t v = ra.x;
-    const uint32_t u[4] = {rc.x, rc.y, rc.z, rc.w};
-    const uint32_t* row = a.pop + (size_t)v * Wp;
-    uint32_t x0[WC], nb0[4][WC];
-#pragma unroll
-    for (int j = 0; j < WC; ++j) {
-      x0[j] = 0;
-#pragma unroll
-      for (int t = 0; t < 4; ++t) nb0[t][j] = 0;
-    }
-    if (!MULTI && live) {
-      load_row<WC>(row, x0);
-#pragma unroll
-      for (int t = 0; t < 4; ++t) load_row<WC>(a.pop + (size_t)u[t] * Wp, nb0[t]);
-    }
-    int32_t w[4];
-    w[0] = w16(ra.z, 0);
-    w[1] = w16(ra.z, 1);
-    w[2] = w16(ra.w, 0);
-    w[3] = w16(ra.w, 1);
-    uint32_t neg[4];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) neg[t] = w[t] < 0 ? 0xFFFFFFFFu : 0u;
-    const uint32_t deg = (uint32_t)(u[0] != v) + (uint32_t)(u[1] != v) + (uint32_t)(u[2] != v) + (uint32_t)(u[3] != v);
-    // ---- presence: some member (over every rank's shard) holds the other value
-    uint32_t ones = 0;
-    if (live) {
-      if (a.ones) {
-        ones = a.ones[v];
-      } else if (!MULTI && a.R == 1) {
-#pragma unroll
-        for (int j = 0; j < WC; ++j) ones += __popc(x0[j]);
-      } else {
-        for (uint32_t r = 0; r < a.R; ++r) {
-          const uint32_t* pr = a.R > 1 ? a.pool + ((size_t)r * a.nv + v) * Wp : row;
-          for (uint32_t c = 0; c < chunks; ++c) {
-            uint32_t y[WC];
-            load_row<WC>(pr + c * WC, y);
-#pragma unroll
-            for (int j = 0; j < WC; ++j) ones += __popc(y[j]);
-          }
-        }
-      }
-    }
-    const bool present = live && ones > 0u && ones < a.n_global;
-    if (present) {
-      steps += n;
-      calls += (unsigned long long)n * deg;
-    }
-    const uint32_t pmask = present ? 0xFFFFFFFFu : 0u;
-    bool keys = false, tbl = false;
-#pragma unroll 1
-    for (uint32_t c = 0; c < chunks; ++c) {
-      uint32_t x[WC], nb[4][WC];
-#pragma unroll
-      for (int j = 0; j < WC; ++j) {
-        x[j] = x0[j];
-#pragma unroll
-        for (int t = 0; t < 4; ++t) nb[t][j] = nb0[t][j];
-      }
-      if (MULTI && live) {
-        load_row<WC>(row + c * WC, x);
-#pragma unroll
-        for (int t = 0; t < 4; ++t) load_row<WC>(a.pop + (size_t)u[t] * Wp + c * WC, nb[t]);
-      }
-      // ---- b words (edge "uncut-gain" bits), then accept via the LE table
-      // (LT | LE & ~elitist where the group-start elitist lives)
-      uint32_t bw[4][WC], acc[WC];
-      bool any = false;
-#pragma unroll
-      for (int j = 0; j < WC; ++j)
-#pragma unroll
-        for (int t = 0; t < 4; ++t) bw[t][j] = x[j] ^ nb[t][j] ^ neg[t];
-      {
-        uint32_t mle[16];
-        tt_masks(ra.y, 1, mle);
-#pragma unroll
-        for (int j = 0; j < WC; ++j) {
-          const uint32_t wj = c * WC + (uint32_t)j;
-          uint32_t ac = tt_mux(mle, bw[0][j], bw[1][j], bw[2][j], bw[3][j]);
-          const uint32_t ew = s_elit[wj];
-          if (ew) {  // warp-uniform: group-start elitist copies take strict improvements only
-            uint32_t e = ew, keep = 0xFFFFFFFFu;
-            while (e) {
-              const uint32_t b = (uint32_t)(__ffs(e) - 1);
-              e &= e - 1u;
-              const uint32_t pat = ((bw[0][j] >> b) & 1u) | (((bw[1][j] >> b) & 1u) << 1) |
-                                   (((bw[2][j] >> b) & 1u) << 2) | (((bw[3][j] >> b) & 1u) << 3);
-              if (!((ra.y >> pat) & 1u)) keep &= ~(1u << b);  // LT[p] bit of the table
-            }
-            ac &= keep;
-          }
-          acc[j] = ac & pmask & valid_mask(wj, n);
-          any |= acc[j] != 0u;
-        }
-      }
-      // ---- commit: accepted solutions flip v (apply_acceptance, :221-247)
-      if (any) {
-        uint32_t nx[WC];
-#pragma unroll
-        for (int j = 0; j < WC; ++j) nx[j] = x[j] ^ acc[j];
-        store_row<WC>(a.pop + (size_t)v * Wp + c * WC, nx);
-        if (esrc >= 0 && ((uint32_t)esrc >> 5) / WC == c) {
-          const uint32_t ew = ((uint32_t)esrc >> 5) - c * WC, eb = (uint32_t)esrc & 31u;
-          uint32_t aw = 0, xw = 0;
-#pragma unroll
-          for (int j = 0; j < WC; ++j)
-            if ((uint32_t)j == ew) {
-              aw = acc[j];
-              xw = x[j];
-            }
-          if ((aw >> eb) & 1u) capture_row(a.elit, a.ever, ever_cur, v, (xw >> eb) & 1u);
-        }
-      }
-      // ---- per-solution reductions over the warp's 32 sets ----------------
-      if (!__any_sync(0xFFFFFFFFu, any)) continue;
-      if (!keys) {  // first accepting chunk of this batch (warp-uniform): the sets' keys
-        keys = true;
-        s_key[warp][lane][0] = zk.x;
-        s_key[warp][lane][1] = zk.y;
-        __syncwarp();
-      }
-      uint32_t mlt[16];
-      tt_masks(ra.y, 0, mlt);
-#pragma unroll
-      for (int j = 0; j < WC; ++j) {
-        if (!__any_sync(0xFFFFFFFFu, acc[j] != 0u)) continue;
-        const uint32_t accT = transpose32(acc[j], lane);  // lane b: sets l accepted by solution 32j+b
-        const uint32_t b0 = bw[0][j], b1 = bw[1][j], b2 = bw[2][j], b3 = bw[3][j];
-        long long d = 0;
-        const uint32_t imp = acc[j] & tt_mux(mlt, b0, b1, b2, b3);
-        if (__any_sync(0xFFFFFFFFu, imp != 0u)) {
-          // T planes of this word (only words with a strictly improving pair)
-          uint32_t T[B];
-#pragma unroll
-          for (int k = 0; k < B; ++k) T[k] = 0;
-          const uint32_t bb[4] = {b0, b1, b2, b3};
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const uint32_t mg = (uint32_t)abs(w[t]);
-            uint32_t cy = 0;
-#pragma unroll
-            for (int k = 0; k < B; ++k) {
-              const uint32_t xb = ((mg >> k) & 1u) ? bb[t] : 0u;
-              const uint32_t tk = T[k];
-              T[k] = tk ^ xb ^ cy;
-              cy = (tk & xb) | (tk & cy) | (xb & cy);
-            }
-          }
-          const uint32_t impT = transpose32(imp, lane);
-          const uint32_t A = (uint32_t)(abs(w[0]) + abs(w[1]) + abs(w[2]) + abs(w[3]));
-#pragma unroll
-          for (int k = 0; k < B; ++k) d += (long long)__popc(impT & __ballot_sync(0xFFFFFFFFu, (A >> k) & 1u)) << k;
-#pragma unroll
-          for (int k = 0; k < B - 1; ++k) d -= (long long)__popc(transpose32(T[k] & imp, lane)) << (k + 1);
-        }
-        const uint32_t sj = (c * WC + (uint32_t)j) * 32u + lane;
-        if (d) atomicAdd(reinterpret_cast<unsigned long long*>(&s_dfit[sj]), (unsigned long long)d);
-        // hash delta of solution 32j+lane: XOR of the keys of its accepted
-        // sets — key by key when every solution of the word accepted few
-        // sets (the steady state: neutral flips are sparse), else through the
-        // 4-bit-chunk table of key XORs
-        unsigned long long x1 = 0, x2 = 0;
-        if (__reduce_max_sync(0xFFFFFFFFu, (uint32_t)__popc(accT)) <= kSparseKeys) {
-          uint32_t r = accT;
-          while (r) {
-            const uint32_t l = (uint32_t)(__ffs(r) - 1);
-            r &= r - 1u;
-            const ulonglong2 k = *reinterpret_cast<const ulonglong2*>(s_key[warp][l]);
-            x1 ^= k.x;
-            x2 ^= k.y;
-          }
-        } else {
-          if (!tbl) {
-            tbl = true;
-            const uint32_t q = lane >> 2, sub = lane & 3u;
-            const ulonglong2 k0 = *reinterpret_cast<const ulonglong2*>(s_key[warp][4 * q + 0]);
-            const ulonglong2 k1 = *reinterpret_cast<const ulonglong2*>(s_key[warp][4 * q + 1]);
-            const ulonglong2 k2 = *reinterpret_cast<const ulonglong2*>(s_key[warp][4 * q + 2]);
-            const ulonglong2 k3 = *reinterpret_cast<const ulonglong2*>(s_key[warp][4 * q + 3]);
-            const unsigned long long l1 = ((sub & 1u) ? k0.x : 0ull) ^ ((sub & 2u) ? k1.x : 0ull);
-            const unsigned long long l2 = ((sub & 1u) ? k0.y : 0ull) ^ ((sub & 2u) ? k1.y : 0ull);
-            ulonglong2* tb = reinterpret_cast<ulonglong2*>(s_tbl[warp][q]);
-            tb[sub] = make_ulonglong2(l1, l2);
-            tb[sub + 4] = make_ulonglong2(l1 ^ k2.x, l2 ^ k2.y);
-            tb[sub + 8] = make_ulonglong2(l1 ^ k3.x, l2 ^ k3.y);
-            tb[sub + 12] = make_ulonglong2(l1 ^ k2.x ^ k3.x, l2 ^ k2.y ^ k3.y);
-            __syncwarp();
-          }
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const uint32_t m = (accT >> (4 * q)) & 15u;
-            const ulonglong2 tq = *reinterpret_cast<const ulonglong2*>(s_tbl[warp][q][m]);
-            x1 ^= tq.x;
-            x2 ^= tq.y;
-          }
-        }
-        if (x1 | x2) {  // the warp's own running hash deltas: no atomics
-          ulonglong2* q = &s_wh[warp][j * 32 + lane];
-          ulonglong2 o = *q;
-          o.x ^= x1;
-          o.y ^= x2;
-          *q = o;
-        }
-      }
-    }
-    __syncwarp();
-  }
+  tt_batches<B, WC>(a, urec, ukey, G, first, s_elit, s_dfit, sh, esrc, ever_cur, lane, warp, steps, calls);
 
   probe(a.exp_flags, 42);
   // the next group's launch may start its prologue (it waits for this grid's
@@ -754,15 +450,15 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_tt_kernel(const G
     unsigned long long x1 = 0, x2 = 0;
 #pragma unroll
     for (int q = 0; q < kUnivWarps; ++q) {
-      x1 ^= s_wh[q][s].x;
-      x2 ^= s_wh[q][s].y;
+      x1 ^= sh.wh[q][s].x;
+      x2 ^= sh.wh[q][s].y;
     }
     s_dh1[s] = x1;
     s_dh2[s] = x2;
     if (s_dfit[s]) atomicAdd(&a.dfit[s], (double)s_dfit[s]);
-    if (s_dh1[s] | s_dh2[s]) {
-      atomicXor(&a.dh1[s], s_dh1[s]);
-      atomicXor(&a.dh2[s], s_dh2[s]);
+    if (x1 | x2) {
+      atomicXor(&a.dh1[s], x1);
+      atomicXor(&a.dh2[s], x2);
     }
   }
   if (threadIdx.x == 0) {
@@ -793,7 +489,7 @@ namespace {
 template <int WC, bool MULTI>
 void* univ_kernel_wc(int planes, bool tt) {
 #define GOMIX_UNIV_CASE(b) \
-  case b: return tt && !MULTI ? (void*)gom_univ_tt_kernel<b, WC, false> : (void*)gom_univ_sliced_kernel<b, WC, MULTI>;
+  case b: return tt && !MULTI ? (void*)gom_univ_tt_kernel<b, WC> : (void*)gom_univ_sliced_kernel<b, WC, MULTI>;
   switch (planes) {
     GOMIX_UNIV_CASE(4)
     GOMIX_UNIV_CASE(6)
