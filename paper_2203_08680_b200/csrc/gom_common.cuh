@@ -186,7 +186,7 @@ static __device__ void note_improvement(const EpiArgs& a, double f) {
 
 // Commit this rank's group deltas: fitness (exact atomics / float partials /
 // reference-ordered recorded deltas) and Zobrist hashes of its n solutions.
-static __device__ void commit_local(const EpiArgs& a, double* s_fit) {
+static __device__ void commit_local(const EpiArgs& a, double* s_fit, unsigned long long* s_h = nullptr) {
   const uint32_t n = a.n;
   if (a.mode == 1) {
     // float partials, one per CTA of the launch: thread t adds the partials
@@ -230,8 +230,13 @@ static __device__ void commit_local(const EpiArgs& a, double* s_fit) {
     }
     a.fit[s] = f;
     if (s_fit && s < kEpiSmemFit) s_fit[s] = f;
-    a.h1[s] ^= a.dh1[s];
-    a.h2[s] ^= a.dh2[s];
+    const unsigned long long x1 = a.h1[s] ^ a.dh1[s], x2 = a.h2[s] ^ a.dh2[s];
+    a.h1[s] = x1;
+    a.h2[s] = x2;
+    if (s_h && s < kEpiSmemFit) {  // the scan takes a new elitist's hash from here
+      s_h[2 * s] = x1;
+      s_h[2 * s + 1] = x2;
+    }
     a.dh1[s] = 0;
     a.dh2[s] = 0;
   }
@@ -251,12 +256,18 @@ static __device__ void commit_local(const EpiArgs& a, double* s_fit) {
 // improvement with the call count at that moment and latching the target stop
 // (runtime.hpp:88-93,136-143).  Sharded runs execute it on every rank from the
 // gathered state, so all ranks take identical decisions.
-static __device__ void elitist_scan(const EpiArgs& a, const double* s_fit) {
+static __device__ void elitist_scan(const EpiArgs& a, const double* s_fit,
+                                    const unsigned long long* s_h = nullptr) {
   DevCtl* c = a.ctl;
   const uint32_t n = a.n_global;
   __shared__ double s_chunkmax[32];
-  __shared__ int32_t s_best;
+  __shared__ double s_cur, s_target;
+  __shared__ unsigned long long s_ni, s_calls_now;
+  __shared__ int32_t s_exact, s_has_target, s_stopped;
+  __shared__ uint32_t s_ver;
   if (threadIdx.x == 0) {
+    // every control-block load first (independent of each other: one memory
+    // round trip), then the updates
     unsigned long long st = 0, ca = 0;
     if (a.R > 1) {
       for (uint32_t r = 0; r < a.R; ++r) {
@@ -266,18 +277,38 @@ static __device__ void elitist_scan(const EpiArgs& a, const double* s_fit) {
     } else {
       st = c->grp_steps;
       ca = c->grp_calls;
+    }
+    const unsigned long long calls_total = c->calls_total, run_steps = c->run_steps, run_calls = c->run_calls;
+    const unsigned long long groups_run = c->groups_run, n_impr = c->n_impr;
+    const unsigned long long gst = a.gsteps[a.group], gca = a.gcalls[a.group];
+    const int32_t has_budget = c->has_budget, has_target = c->has_target, exact = c->exact;
+    int32_t stop = c->stop;
+    const uint32_t ver = c->elit_ver;
+    const double max_evals = c->max_evals, q = c->q, target = c->target, elit_fit = c->elit_fit;
+    if (a.R == 1) {
       c->grp_steps = 0;
       c->grp_calls = 0;
     }
-    c->calls_total += ca;
-    c->run_steps += st;
-    c->run_calls += ca;
-    c->groups_run += 1;
-    a.gsteps[a.group] += st;
-    a.gcalls[a.group] += ca;
-    if (c->has_budget && (double)c->calls_total / c->q >= c->max_evals)
-      request_stop(c, GOMIX_STOP_BUDGET);
-    s_best = -1;
+    const unsigned long long ct = calls_total + ca;
+    c->calls_total = ct;
+    c->run_steps = run_steps + st;
+    c->run_calls = run_calls + ca;
+    c->groups_run = groups_run + 1;
+    a.gsteps[a.group] = gst + st;
+    a.gcalls[a.group] = gca + ca;
+    if (has_budget && (double)ct / q >= max_evals && !stop) {  // request_stop(budget)
+      c->stop = 1;
+      c->stop_reason = GOMIX_STOP_BUDGET;
+      stop = 1;
+    }
+    s_stopped = stop;
+    s_ver = ver;
+    s_cur = elit_fit;
+    s_target = target;
+    s_ni = n_impr;
+    s_calls_now = ct;
+    s_exact = exact;
+    s_has_target = has_target;
   }
   __syncthreads();
   // chunk maxima let the serial scan skip chunks that cannot hold a record
@@ -292,12 +323,12 @@ static __device__ void elitist_scan(const EpiArgs& a, const double* s_fit) {
   }
   __syncthreads();
   if (warp == 0) {
-    const bool exact = c->exact != 0;
-    const int32_t has_target = c->has_target;
-    const double target = c->target;
-    unsigned long long ni = c->n_impr;
-    const unsigned long long calls_now = c->calls_total;
-    double cur = c->elit_fit;
+    const bool exact = s_exact != 0;
+    const int32_t has_target = s_has_target;
+    const double target = s_target;
+    unsigned long long ni = s_ni;
+    const unsigned long long calls_now = s_calls_now;
+    double cur = s_cur;
     int32_t best = -1;
     bool hit = false;
     for (uint32_t base = 0; base < n; base += 32u) {
@@ -321,25 +352,33 @@ static __device__ void elitist_scan(const EpiArgs& a, const double* s_fit) {
     }
     if (lane == 0) {
       c->n_impr = ni;
-      if (hit) request_stop(c, GOMIX_STOP_TARGET);
+      if (hit && !s_stopped) {  // request_stop(target): the budget stop, if any, came first
+        c->stop = 1;
+        c->stop_reason = GOMIX_STOP_TARGET;
+      }
       if (best >= 0) {  // new elitist: member `best` (snapshot taken copy-on-write)
         c->elit_fit = cur;
         c->elit_src = best;
-        c->eh1 = a.h1_all[best];
-        c->eh2 = a.h2_all[best];
-        c->elit_ver += 1;
+        if (s_h && (uint32_t)best < kEpiSmemFit) {
+          c->eh1 = s_h[2 * best];
+          c->eh2 = s_h[2 * best + 1];
+        } else {
+          c->eh1 = a.h1_all[best];
+          c->eh2 = a.h2_all[best];
+        }
+        c->elit_ver = s_ver + 1;
       }
-      s_best = best;
     }
   }
   __syncthreads();
 }
 
 static __device__ void epilogue_body(const EpiArgs& a) {
-  __shared__ double s_fit[kEpiSmemFit];  // this group's fitness, scanned without global loads
-  commit_local(a, a.R == 1 ? s_fit : nullptr);
+  __shared__ double s_fit[kEpiSmemFit];              // this group's fitness, scanned without global loads
+  __shared__ unsigned long long s_h[2 * kEpiSmemFit];  // ... and hashes (a new elitist's)
+  commit_local(a, a.R == 1 ? s_fit : nullptr, a.R == 1 ? s_h : nullptr);
   __syncthreads();
-  if (a.R == 1) elitist_scan(a, s_fit);
+  if (a.R == 1) elitist_scan(a, s_fit, s_h);
 }
 
 }  // namespace gomix_b200
