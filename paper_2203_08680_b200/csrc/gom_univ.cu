@@ -404,16 +404,22 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_tt_kernel(const G
   // programmatic dependent launch (graph path): everything below reads what
   // the previous group's launch wrote (population, control block, hashes)
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (*(volatile int32_t*)&a.ctl->stop) return;
+  // the control block and this warp's hashes in one round trip, then the stop check
+  const int32_t stopped = *(volatile int32_t*)&a.ctl->stop;
   const unsigned long long eh1 = a.ctl->eh1, eh2 = a.ctl->eh2;
   const int32_t esrc_g = a.ctl->elit_src;
   const uint32_t ever_cur = a.ctl->elit_ver;
+  const uint32_t sw = warp * 32u + lane;
+  unsigned long long hs1 = 0, hs2 = 0;
+  if (warp < Wp && sw < n) {
+    hs1 = a.h1[sw];
+    hs2 = a.h2[sw];
+  }
+  if (stopped) return;
   const int32_t esrc = (esrc_g >= 0 && (uint32_t)esrc_g / n == a.rank) ? (int32_t)((uint32_t)esrc_g % n) : -1;
-  for (uint32_t j = warp; j < Wp; j += kUnivWarps) {
-    const uint32_t s = j * 32u + lane;
-    const bool e = s < n && a.h1[s] == eh1 && a.h2[s] == eh2;
-    const uint32_t m = __ballot_sync(0xFFFFFFFFu, e);
-    if (lane == 0) s_elit[j] = m;
+  if (warp < Wp) {  // group-start "parent == elitist" (engine_parallel.hpp:202) as word masks
+    const uint32_t m = __ballot_sync(0xFFFFFFFFu, sw < n && hs1 == eh1 && hs2 == eh2);
+    if (lane == 0) s_elit[warp] = m;
   }
   for (uint32_t i = threadIdx.x; i < Wp * 32u; i += blockDim.x) {
     s_dfit[i] = 0;
