@@ -483,11 +483,18 @@ __global__ void csr_fill_kernel(const unsigned long long* key, const int32_t* ei
 }
 // max over rows of sum |wi| (the univariate kernels' plane count)
 __global__ void csr_row_abs_kernel(const int32_t* row_ptr, const int32_t* wi, uint64_t nv, unsigned long long* mx) {
+  unsigned long long best = 0;
   for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += (uint64_t)gridDim.x * blockDim.x) {
     unsigned long long a = 0;
     for (int32_t e = row_ptr[v]; e < row_ptr[v + 1]; ++e) a += (unsigned long long)llabs((long long)wi[e]);
-    atomicMax(mx, a);
+    best = a > best ? a : best;
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {  // one atomic per warp, not per row
+    const unsigned long long y = __shfl_xor_sync(0xFFFFFFFFu, best, o);
+    best = y > best ? y : best;
+  }
+  if ((threadIdx.x & 31u) == 0 && best) atomicMax(mx, best);
 }
 unsigned grid_for(uint64_t work) { return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((work + 255) / 256, 65535)); }
 }  // namespace
