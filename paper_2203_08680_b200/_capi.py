@@ -12,7 +12,15 @@ import os
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("GOMIX_LIB") or os.path.join(PKG, "libgomix_b200.so")  # GOMIX_LIB: an alternative in-tree build (A/B experiments)
+LIB_PATH = os.path.join(PKG, "libgomix_b200.so")
+# GOMIX_LIB: an alternative in-tree build for A/B timing experiments; only a
+# library inside this package directory is accepted
+_alt = os.environ.get("GOMIX_LIB")
+if _alt:
+    _alt = os.path.realpath(_alt)
+    if os.path.dirname(_alt) != os.path.realpath(PKG) or not os.path.basename(_alt).endswith(".so"):
+        raise ImportError("GOMIX_LIB must name a .so inside " + PKG)
+    LIB_PATH = _alt
 
 GOMIX_OK, GOMIX_E_INVALID, GOMIX_E_CUDA, GOMIX_E_NCCL, GOMIX_E_OOM, GOMIX_E_STATE = range(6)
 MODE_REPLAY, MODE_PHILOX = 0, 1
