@@ -1,0 +1,87 @@
+#!/usr/bin/env python3
+"""BASELINE config C5 as the time-to-target sweep it names: "population-size
+sweep 16..4096 on n=10^5 grid, time-to-target vs host-CPU reference".
+
+Per population size n (single population, no IMS — the population size is
+the swept variable): the reference's own run_parallel (ParallelEngine, every
+host thread, univariate FOS, seed s) runs for T_ref seconds; its best cut is
+the target; the B200 engine (Philox donors, same n, same instance) then runs
+to that target.  Both clocks start at RunContext creation with the model
+prebuilt (runtime.hpp:62-68).  A population that stalls below the target
+within the GPU budget counts as a miss.
+
+    python tools/ttt_population_sweep.py [--t-ref 10] [--sizes 16,64,256,1024,4096] [--out ...]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+REF = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
+W, H = 316, 316
+
+
+def reference_run(n, seed, t_ref, workers):
+    cmd = [REF, "ims", "--torus", str(W), str(H), "--weights", "int:1:10", "--inst-seed", "1", "--fos",
+           "univariate", "--n", str(n), "--seed", str(seed), "--workers", str(workers), "--max-seconds", str(t_ref)]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=t_ref * 4 + 600)
+    if res.returncode != 0:
+        raise RuntimeError(res.stderr)
+    r = json.loads(res.stdout)
+    best = r["best"]
+    t_best = next(t for t, _, f in r["trace"] if f == best)
+    return {"best": best, "seconds_to_best": t_best, "evaluations": r["evaluations"],
+            "generations": r["generations"]}
+
+
+def gpu_run(P, n, seed, target, budget_s):
+    import paper_2203_08680_b200 as G
+
+    sink = G.RecordingSink()
+    r = G.run_gpu(P, G.TerminationConfig(target_fitness=target, max_seconds=budget_s), seed=seed,
+                  population_size=n, use_ims=False, sink=sink, mode="philox")
+    hit = r.reason == "target-reached"
+    t_hit = next((x.seconds for x in sink.rows if x.fitness >= target), None) if hit else None
+    return {"reached": hit, "seconds_to_target": t_hit, "best": r.best_fitness, "evaluations": r.evaluations,
+            "generations": r.generations}
+
+
+def main():
+    import paper_2203_08680_b200 as G
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--t-ref", type=float, default=10.0)
+    ap.add_argument("--sizes", default="16,64,256,1024,4096")
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    workers = os.cpu_count() or 1
+    inst = G.generate_torus(W, H, ("int", 1, 10), 1)
+    fos = G.univariate_fos(inst.num_vertices)
+    P = G.GpuProblem(inst, fos)  # built once: the sweep compares run times
+    rows = []
+    for n in (int(x) for x in a.sizes.split(",")):
+        ref = reference_run(n, a.seed, a.t_ref, workers)
+        gpu = gpu_run(P, n, a.seed, ref["best"], a.t_ref)
+        row = {"population": n, "reference": ref, "gpu": gpu,
+               "speedup": (ref["seconds_to_best"] / gpu["seconds_to_target"]) if gpu["reached"] else None}
+        rows.append(row)
+        print(json.dumps(row), flush=True)
+    out = {"config": f"C5: Max-Cut 2-D torus {W}x{H} (~1e5 vertices), integer weights U[1,10], univariate FOS",
+           "t_ref_s": a.t_ref, "cpu_workers": workers, "seed": a.seed,
+           "method": "single population per size; target = the reference run_parallel's best within T_ref",
+           "rows": rows}
+    if a.out:
+        with open(a.out, "w") as fh:
+            json.dump(out, fh, indent=1)
+
+
+if __name__ == "__main__":
+    main()
