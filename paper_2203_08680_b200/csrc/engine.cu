@@ -369,6 +369,8 @@ struct gomix_gpu_engine {
   GroupDesc* d_groups = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   uint64_t graph_launches = 0;
+  static constexpr int kGraphAfter = 4;  // generations issued directly before the graph is captured
+  int graph_warm = 0;
 
   cudaStream_t stream = nullptr;
   bool own_stream = false;
@@ -652,6 +654,18 @@ struct gomix_gpu_engine {
   // kernel, then k GOM launches that find their group through
   // the device-side order.  Replaces ~2k launches by one graph launch.
   void launch_generation_graph() {
+    // The first generations of an engine (IMS creates short-lived ones) are
+    // issued launch by launch — the same kernels in the same order as the
+    // captured graph — so a population that reaches the target early never
+    // pays the capture and instantiation.
+    if (!graph_exec && graph_warm < kGraphAfter) {
+      ++graph_warm;
+      OrderArgs o{ctl, d_order, (uint32_t)P->k, seed};
+      launch_order(d_begin, o, stream);
+      for (uint64_t slot = 0; slot < P->k; ++slot) launch_group(0, false, (int32_t)slot, stream);
+      ++launches;
+      return;
+    }
     if (!graph_exec) {
       cudaStream_t cap = nullptr;
       GOMIX_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
