@@ -53,6 +53,12 @@ def warm_device():
 
     t = G.generate_torus(4, 4, "unit", 1)
     G.GpuProblem(t, G.univariate_fos(16))
+    # and the GOM kernels' first-use loading (lazy module loading), also untimed
+    for fos in (G.univariate_fos(16), G.neighbourhood_fos(t)):
+        E = G.GpuParallelEngine(G.GpuProblem(t, fos), 16, 1, mode="philox")
+        for _ in range(6):
+            E.run_generation()
+        del E
 
 
 def gpu_ims(cfg, target, seed, budget_s, base=16, sub=4, **engine_kw):

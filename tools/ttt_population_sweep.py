@@ -66,6 +66,10 @@ def main():
     inst = G.generate_torus(W, H, ("int", 1, 10), 1)
     fos = G.univariate_fos(inst.num_vertices)
     P = G.GpuProblem(inst, fos)  # built once: the sweep compares run times
+    warm = G.GpuParallelEngine(P, 16, 99, mode="philox")  # untimed: first-use kernel loading (one-time process cost)
+    for _ in range(6):
+        warm.run_generation()
+    del warm
     rows = []
     for n in (int(x) for x in a.sizes.split(",")):
         ref = reference_run(n, a.seed, a.t_ref, workers)
