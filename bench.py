@@ -293,10 +293,10 @@ def bench_ours(args):
     # keep the GPU busy for the clock record when the timed region was short;
     # the generation count is fixed up front (rank 0's estimate, broadcast):
     # sharded generations are collectives, so every rank must run the same number
-    soak = [int(max(0.0, 0.6 - t_wall) / max(t_wall / max(1, args.steps), 1e-6))]
+    soak = [int(max(0.0, 1.5 - t_wall) / max(t_wall / max(1, args.steps), 1e-6))]
     if dist is not None:
         dist.broadcast_object_list(soak, src=0)
-    for _ in range(min(soak[0], 20000)):
+    for _ in range(min(soak[0], 50000)):
         gen()
     torch.cuda.synchronize()
     E.synchronize()
