@@ -293,7 +293,8 @@ def bench_ours(args):
     # keep the GPU busy for the clock record when the timed region was short;
     # the generation count is fixed up front (rank 0's estimate, broadcast):
     # sharded generations are collectives, so every rank must run the same number
-    soak = [int(max(0.0, 1.5 - t_wall) / max(t_wall / max(1, args.steps), 1e-6))]
+    per_gen_s = max(sum(step_ms) / 1e3 / max(1, args.steps), 1e-6)  # device time per generation
+    soak = [int(max(0.0, 1.5 - t_wall) / per_gen_s)]
     if dist is not None:
         dist.broadcast_object_list(soak, src=0)
     for _ in range(min(soak[0], 50000)):
