@@ -66,12 +66,14 @@ def main():
     inst = G.generate_torus(W, H, ("int", 1, 10), 1)
     fos = G.univariate_fos(inst.num_vertices)
     P = G.GpuProblem(inst, fos)  # built once: the sweep compares run times
-    warm = G.GpuParallelEngine(P, 16, 99, mode="philox")  # untimed: first-use kernel loading (one-time process cost)
-    for _ in range(6):
-        warm.run_generation()
-    del warm
+    sizes = [int(x) for x in a.sizes.split(",")]
+    for n in sizes:  # untimed: first-use kernel loading of every size's variants (one-time process cost)
+        warm = G.GpuParallelEngine(P, n, 99, mode="philox")
+        for _ in range(6):
+            warm.run_generation()
+        del warm
     rows = []
-    for n in (int(x) for x in a.sizes.split(",")):
+    for n in sizes:
         ref = reference_run(n, a.seed, a.t_ref, workers)
         gpu = gpu_run(P, n, a.seed, ref["best"], a.t_ref)
         row = {"population": n, "reference": ref, "gpu": gpu,
