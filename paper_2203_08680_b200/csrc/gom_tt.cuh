@@ -1,8 +1,8 @@
 // gom_tt.cuh — the truth-table univariate GOM step (degree <= 4, Philox,
-// rows of WC <= 4 words) as a device function: the batch loop shared by the
-// per-group kernel (gom_univ_tt_kernel, gom_univ.cu) and the persistent
-// whole-generation kernel (gom_generation_kernel's truth-table mode,
-// gom_gen.cu).  Semantics and layout: gom_univ.cu's header and DESIGN.md §4.
+// rows of WC <= 4 words) as a device function: the batch loop of
+// gom_univ_tt_kernel (gom_univ.cu; a persistent whole-generation variant was
+// measured and not kept).  Semantics and layout: gom_univ.cu's
+// header and DESIGN.md §4.
 #pragma once
 
 #include "gom_common.cuh"
