@@ -29,12 +29,12 @@ sys.path.insert(0, ROOT)
 REF = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
 
 
-def reference_ims(cfg, seed, t_ref, workers, base=16, sub=4):
+def reference_ims(cfg, seed, t_ref, workers, base=16, sub=4, serial=False):
     w = cfg["weights"]
     wspec = "unit" if w == "unit" else f"int:{w[1]}:{w[2]}"
     cmd = [REF, "ims", "--torus", str(cfg["width"]), str(cfg["height"]), "--weights", wspec, "--inst-seed", "1",
            "--fos", cfg["ref_fos"], "--seed", str(seed), "--ims", "--ims-base", str(base), "--ims-sub", str(sub),
-           "--workers", str(workers), "--max-seconds", str(t_ref)]
+           "--workers", str(workers), "--max-seconds", str(t_ref)] + (["--serial"] if serial else [])
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=t_ref * 4 + 600)
     if res.returncode != 0:
         raise RuntimeError(res.stderr)
@@ -90,14 +90,17 @@ def main():
     ap.add_argument("--seeds", type=int, default=1)
     ap.add_argument("--gpu-budget", type=float, default=None, help="GPU wall budget per seed (default t_ref)")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--serial", action="store_true",
+                    help="reference = SerialEngine on one core (the paper's baseline, PAPER.md:502) instead of "
+                         "ParallelEngine on every host thread")
     ap.add_argument("--fi", action="store_true",
                     help="also run the GPU IMS with the parallel forced improvement (csrc/gom_fi.cu)")
     a = ap.parse_args()
     cfg = CONFIGS[a.config]
-    workers = os.cpu_count() or 1
+    workers = 1 if a.serial else (os.cpu_count() or 1)
     rows = []
     for seed in range(1, a.seeds + 1):
-        ref = reference_ims(cfg, seed, a.t_ref, workers)
+        ref = reference_ims(cfg, seed, a.t_ref, workers, serial=a.serial)
         gpu = gpu_ims(cfg, ref["best"], seed, a.gpu_budget or a.t_ref)
         rows.append({"seed": seed, "reference": ref, "gpu": gpu})
         if a.fi:
@@ -105,7 +108,8 @@ def main():
         print(json.dumps(rows[-1]), flush=True)
     ok = [r for r in rows if r["gpu"]["reached"]]
     summ = {"config": cfg["workload"], "t_ref_s": a.t_ref, "cpu_workers": workers, "seeds": a.seeds,
-            "ims": "base 16, subgenerations 4", "success_rate": len(ok) / len(rows),
+            "ims": "base 16, subgenerations 4", "reference_engine": "SerialEngine, 1 core" if a.serial else
+            f"ParallelEngine, {workers} threads", "success_rate": len(ok) / len(rows),
             "cpu_median_s_to_best_known": statistics.median(r["reference"]["seconds_to_best"] for r in rows),
             "gpu_median_s_to_target": statistics.median(r["gpu"]["seconds_to_target"] for r in ok) if ok else None,
             "gpu_median_s_to_target_incl_build":
