@@ -66,6 +66,20 @@ __device__ __forceinline__ uint32_t tt_mux(const uint32_t (&m)[16], uint32_t b0,
   return (b3 & l2[1]) | (~b3 & l2[0]);
 }
 
+// the same lookup at the complemented pattern: bit s = table[~p_s & 15]
+// (complementing every input swaps the two leaves of every multiplexer)
+__device__ __forceinline__ uint32_t tt_mux_not(const uint32_t (&m)[16], uint32_t b0, uint32_t b1, uint32_t b2,
+                                               uint32_t b3) {
+  uint32_t l0[8], l1[4], l2[2];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) l0[q] = (b0 & m[2 * q]) | (~b0 & m[2 * q + 1]);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) l1[q] = (b1 & l0[2 * q]) | (~b1 & l0[2 * q + 1]);
+#pragma unroll
+  for (int q = 0; q < 2; ++q) l2[q] = (b2 & l1[2 * q]) | (~b2 & l1[2 * q + 1]);
+  return (b3 & l2[0]) | (~b3 & l2[1]);
+}
+
 __device__ __forceinline__ int32_t w16(uint32_t packed, int hi) {
   return hi ? ((int32_t)packed >> 16) : ((int32_t)(packed << 16) >> 16);
 }
@@ -172,9 +186,9 @@ __device__ __forceinline__ void tt_batches(const GomArgs& a, const uint4* urec, 
     for (int j = 0; j < WC; ++j)
 #pragma unroll
       for (int t = 0; t < 4; ++t) bw[t][j] = x[j] ^ nb[t][j] ^ neg[t];
+    uint32_t mle[16];
+    tt_masks(ra.y, 1, mle);
     {
-      uint32_t mle[16];
-      tt_masks(ra.y, 1, mle);
 #pragma unroll
       for (int j = 0; j < WC; ++j) {
         uint32_t ac = tt_mux(mle, bw[0][j], bw[1][j], bw[2][j], bw[3][j]);
@@ -218,15 +232,15 @@ __device__ __forceinline__ void tt_batches(const GomArgs& a, const uint4* urec, 
       sh.key[warp][lane][1] = zk.y;
       __syncwarp();
       bool tbl = false;
-      uint32_t mlt[16];
-      tt_masks(ra.y, 0, mlt);
 #pragma unroll
       for (int j = 0; j < WC; ++j) {
         if (!__any_sync(0xFFFFFFFFu, acc[j] != 0u)) continue;
         const uint32_t accT = transpose32(acc[j], lane);  // lane b: sets l accepted by solution 32j+b
         const uint32_t b0 = bw[0][j], b1 = bw[1][j], b2 = bw[2][j], b3 = bw[3][j];
         long long d = 0;
-        const uint32_t imp = acc[j] & tt_mux(mlt, b0, b1, b2, b3);
+        // strict improvements: T(p) < A/2  <=>  T(~p) = A - T(p) > A/2  <=>
+        // ~p is not in LE — the LE table at the complemented pattern, no LT masks
+        const uint32_t imp = acc[j] & ~tt_mux_not(mle, b0, b1, b2, b3);
         if (__any_sync(0xFFFFFFFFu, imp != 0u)) {
           // T planes of this word (only words with a strictly improving pair)
           uint32_t T[B];
