@@ -95,7 +95,9 @@ def test_largest_linkage_set_64_variables():
 def test_sets_of_65_variables_are_rejected():
     t = G.generate_torus(12, 12, ("int", 1, 3), 3)
     fos = G.Fos.from_sets(t.num_vertices, [list(range(65))] + [[v] for v in range(65, t.num_vertices)])
-    with pytest.raises(Exception):
+    from paper_2203_08680_b200._capi import InvalidArgument
+
+    with pytest.raises(InvalidArgument, match="64 variables"):
         G.GpuProblem(t, fos)
 
 
