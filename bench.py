@@ -129,8 +129,9 @@ def bench_reference(args):
     if not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "ref_driver")):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/ref_driver was not built"}))
         return
+    # the same population as our arm at N GPUs (n per GPU, weak scaling);
     # bounded sample: W + K generations, or as many as fit in REF_BUDGET_S
-    out = run_reference(cfg, n, args.warmup + args.steps, workers, max_seconds=REF_BUDGET_S)
+    out = run_reference(cfg, n * world, args.warmup + args.steps, workers, max_seconds=REF_BUDGET_S)
     allg = out["gens"]
     warm = min(args.warmup, max(0, len(allg) - 1))
     gens = allg[warm:]
