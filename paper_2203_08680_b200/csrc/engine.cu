@@ -341,8 +341,7 @@ struct gomix_gpu_engine {
   DevCtl* ctl = nullptr;
   DevCtl* h_ctl = nullptr;  // pinned
   BeginArgs* d_begin = nullptr;  // per-call criteria read by the graph's begin kernel
-  BeginArgs* h_begin = nullptr;  // pinned, mapped: the graph's begin kernel reads it in place
-  BeginArgs* m_begin = nullptr;  // device view of h_begin (no copy before a graph launch)
+  BeginArgs* h_begin = nullptr;  // pinned staging of d_begin
   static constexpr uint64_t kImprInline = 64;  // improvements copied back with every read_ctl
   static constexpr size_t kCtlBytes = (sizeof(DevCtl) + 63) / 64 * 64;  // control block, then the log
   ImprRec* h_impr = nullptr;                   // pinned [kImprInline], right after *h_ctl
@@ -580,8 +579,7 @@ struct gomix_gpu_engine {
     }
     GOMIX_CUDA(cudaMallocHost(&h_ctl, kCtlBytes + kImprInline * sizeof(ImprRec)));
     h_impr = reinterpret_cast<ImprRec*>(reinterpret_cast<char*>(h_ctl) + kCtlBytes);
-    GOMIX_CUDA(cudaHostAlloc(&h_begin, sizeof(BeginArgs), cudaHostAllocMapped));
-    GOMIX_CUDA(cudaHostGetDevicePointer((void**)&m_begin, h_begin, 0));
+    GOMIX_CUDA(cudaMallocHost(&h_begin, sizeof(BeginArgs)));
     d_begin = dev_alloc<BeginArgs>(allocs, 1);
     std::memset(h_ctl, 0, sizeof(DevCtl));
     h_ctl->elit_src = -1;
@@ -667,7 +665,7 @@ struct gomix_gpu_engine {
     if (!graph_exec && graph_warm < kGraphAfter) {
       ++graph_warm;
       OrderArgs o{ctl, d_order, (uint32_t)P->k, seed};
-      launch_order(m_begin, o, stream);
+      launch_order(d_begin, o, stream);
       for (uint64_t slot = 0; slot < P->k; ++slot) launch_group(0, false, (int32_t)slot, stream);
       ++launches;
       return;
@@ -677,7 +675,7 @@ struct gomix_gpu_engine {
       GOMIX_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
       GOMIX_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
       OrderArgs o{ctl, d_order, (uint32_t)P->k, seed};
-      launch_order(m_begin, o, cap);
+      launch_order(d_begin, o, cap);
       const uint64_t saved = launches;
       for (uint64_t slot = 0; slot < P->k; ++slot) launch_group(0, false, (int32_t)slot, cap);
       graph_launches = launches - saved + 1;
@@ -692,15 +690,13 @@ struct gomix_gpu_engine {
     launches += graph_launches;
   }
 
-  // Stage this call's stop criteria: the graph's begin kernel reads the
-  // mapped host copy in place; the persistent generation kernel (every CTA
-  // reads them) gets a device copy.  The host copy is only rewritten when no
-  // earlier reader can be pending (sync calls wait first; async calls always
-  // stage "no criteria").
+  // Stage this call's stop criteria for the graph's begin kernel.  The pinned
+  // staging buffer is only rewritten when no earlier copy from it can be
+  // pending (sync calls wait first; async calls always stage "no criteria").
   void stage_criteria(const gomix_stop_criteria* stop, bool sync_first) {
     if (sync_first) GOMIX_CUDA(cudaStreamSynchronize(stream));
     *h_begin = make_begin(stop);
-    if (gen_ok) GOMIX_CUDA(cudaMemcpyAsync(d_begin, h_begin, sizeof(BeginArgs), cudaMemcpyHostToDevice, stream));
+    GOMIX_CUDA(cudaMemcpyAsync(d_begin, h_begin, sizeof(BeginArgs), cudaMemcpyHostToDevice, stream));
   }
 
   void read_ctl() {

@@ -51,11 +51,31 @@ size_t round_block(size_t b) {
 }
 }  // namespace
 
+// The cache is opt-in (GOMIX_ALLOC_CACHE=1): with it, one stop-criteria
+// comparison test (tests/test_gen_kernel.py, budget stop inside a generation)
+// fails intermittently in full-suite runs — recycled block addresses, not
+// their contents or the missing implicit synchronisation (both ruled out) —
+// and the cause is not found yet.  Plain cudaMalloc / cudaFree by default.
+bool cache_disabled() {
+  static const bool off = std::getenv("GOMIX_ALLOC_CACHE") == nullptr;
+  return off;
+}
+
 void* cached_malloc(size_t bytes) {
+  if (cache_disabled()) {
+    void* p = nullptr;
+    GOMIX_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 1)));
+    return p;
+  }
+  // cudaMalloc / cudaFree synchronise the device implicitly and callers
+  // have come to rely on it (a stop-criteria test turned flaky without): keep
+  // that, minus the allocation itself
+  GOMIX_CUDA(cudaDeviceSynchronize());
   int dev = 0;
   GOMIX_CUDA(cudaGetDevice(&dev));
   const size_t sz = round_block(std::max<size_t>(bytes, 1));
   DeviceCache& c = cache();
+  void* reused = nullptr;
   {
     std::lock_guard<std::mutex> lk(c.mu);
     auto it = c.free_blocks.find({dev, sz});
@@ -64,9 +84,10 @@ void* cached_malloc(size_t bytes) {
       it->second.pop_back();
       c.cached_bytes -= sz;
       c.live[p] = {dev, sz};
-      return p;
+      reused = p;
     }
   }
+  if (reused) return reused;
   void* p = nullptr;
   cudaError_t e = cudaMalloc(&p, sz);
   if (e == cudaErrorMemoryAllocation) {  // give the cached blocks back and retry once
@@ -86,6 +107,11 @@ void* cached_malloc(size_t bytes) {
 
 void cached_free(void* p) {
   if (!p) return;
+  if (cache_disabled()) {
+    cudaFree(p);
+    return;
+  }
+  cudaDeviceSynchronize();  // as cudaFree would
   DeviceCache& c = cache();
   std::lock_guard<std::mutex> lk(c.mu);
   auto it = c.live.find(p);
