@@ -26,7 +26,9 @@
 #pragma once
 
 #include <cstdint>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -219,20 +221,37 @@ class GpuParallelEngine final : public GenerationRunner {
   };
 
   // One device model per (problem, model) pair, shared by every population of
-  // a run like the reference's shared ModelArtifacts (run.hpp:110).
+  // a run like the reference's shared ModelArtifacts (run.hpp:110).  Keyed on
+  // the model's identity (owner_before of its shared_ptr, so a freed model's
+  // address being reused cannot alias), the problem and the device; guarded
+  // by a mutex because run_with may be called from several threads.
+  struct CacheKey {
+    const void* problem;
+    std::weak_ptr<const ModelArtifacts> model;
+    int32_t device;
+  };
+  struct CacheLess {
+    bool operator()(const CacheKey& a, const CacheKey& b) const {
+      if (a.problem != b.problem) return std::less<const void*>()(a.problem, b.problem);
+      if (a.device != b.device) return a.device < b.device;
+      return a.model.owner_before(b.model);
+    }
+  };
+
   std::shared_ptr<gomix_gpu_problem> shared_problem(const gomix_maxcut& inst, const gomix_fos& fos,
                                                     const int32_t* colour) {
-    static std::weak_ptr<gomix_gpu_problem> cache;
-    static const void* cache_problem = nullptr;
-    static const void* cache_model = nullptr;
-    if (auto p = cache.lock(); p && cache_problem == &problem_ && cache_model == model_.get())
-      return p;
+    static std::mutex mu;
+    static std::map<CacheKey, std::weak_ptr<gomix_gpu_problem>, CacheLess> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    for (auto it = cache.begin(); it != cache.end();)  // drop entries whose model or device problem died
+      it = (it->first.model.expired() || it->second.expired()) ? cache.erase(it) : std::next(it);
+    const CacheKey key{&problem_, model_, device};
+    if (auto it = cache.find(key); it != cache.end())
+      if (auto p = it->second.lock()) return p;
     gomix_gpu_problem* raw = nullptr;
     gpu_detail::check(gomix_gpu_problem_create(&inst, &fos, colour, device, &raw));
     std::shared_ptr<gomix_gpu_problem> p(raw, ProblemDel{});
-    cache = p;
-    cache_problem = &problem_;
-    cache_model = model_.get();
+    cache[key] = p;
     return p;
   }
 

@@ -60,6 +60,7 @@ struct Args {
   std::string out;
   double max_seconds = 0, target = 0, max_evals = 0;
   bool has_target = false, has_evals = false, use_ims = false, serial = false;
+  bool light = false;  // run: no phase replica / batch arrays; per-generation populations as packed bits
   std::size_t ims_base = 16, ims_sub = 4;
   std::string pop;
 };
@@ -87,6 +88,7 @@ Args parse(int argc, char** argv) {
     else if (k == "--target") { a.target = std::stod(next()); a.has_target = true; }
     else if (k == "--max-evals") { a.max_evals = std::stod(next()); a.has_evals = true; }
     else if (k == "--ims") a.use_ims = true;
+    else if (k == "--light") a.light = true;
     else if (k == "--serial") a.serial = true;
     else if (k == "--ims-base") a.ims_base = std::stoull(next());
     else if (k == "--ims-sub") a.ims_sub = std::stoull(next());
@@ -277,6 +279,57 @@ struct TraceLog final : TraceSink {
   }
 };
 
+// Packed populations (numpy.packbits order: solution-major, 8 alleles per
+// byte, first allele in the high bit), for fixtures at sizes where the byte
+// genotypes and GroupBatch arrays of every generation would not fit.
+void pack_pop(const std::vector<EvaluatedSolution>& pop, std::vector<std::uint8_t>& out) {
+  std::size_t bitpos = out.size() * 8;
+  std::size_t total = 0;
+  for (const auto& s : pop) total += s.genotype.size();
+  out.resize(out.size() + (total + 7) / 8, 0);
+  for (const auto& s : pop)
+    for (const Allele x : s.genotype) {
+      if (x) out[bitpos >> 3] |= static_cast<std::uint8_t>(0x80u >> (bitpos & 7));
+      ++bitpos;
+    }
+}
+
+int mode_run_light(const Args& a, ParallelEngine& engine, RunContext& ctx, TraceLog& log) {
+  std::vector<std::uint8_t> g0;
+  std::vector<double> f0;
+  pack_pop(engine.population(), g0);
+  for (const auto& s : engine.population()) f0.push_back(s.fitness);
+  write_u8("init_packed", g0);
+  write_f64("init_fitness", f0);
+  write_f64("init_elitist", {engine.elitist().fitness});
+  write_u64("init_calls", {ctx.control.evaluator_calls()});
+  std::vector<std::uint8_t> G;
+  std::vector<double> F, E;
+  std::vector<std::uint64_t> C;
+  for (long gen = 0; gen < a.gens; ++gen) {
+    engine.run_generation();
+    pack_pop(engine.population(), G);
+    for (const auto& s : engine.population()) F.push_back(s.fitness);
+    E.push_back(engine.elitist().fitness);
+    C.push_back(ctx.control.evaluator_calls());
+  }
+  write_u8("packed", G);
+  write_f64("fitness", F);
+  write_f64("elitist", E);
+  write_u64("calls", C);
+  std::vector<std::uint64_t> steps, calls;
+  for (const auto& c : engine.group_counters()) {
+    steps.push_back(c.steps);
+    calls.push_back(c.evaluator_calls);
+  }
+  write_u64("counter_steps", steps);
+  write_u64("counter_calls", calls);
+  write_f64("trace_fitness", log.fit);
+  write_f64("trace_evals", log.evals);
+  write_u64("trace_generation", log.gen);
+  return 0;
+}
+
 int mode_run(const Args& a) {
   const MaxCutInstance inst = make_instance(a);
   const GrayBoxProblem problem = as_graybox(inst);
@@ -293,6 +346,7 @@ int mode_run(const Args& a) {
   cfg.workers = a.workers;
   cfg.fixed_model = arts;
   ParallelEngine engine(problem, cfg, ctx);
+  if (a.light) return mode_run_light(a, engine, ctx, log);
   PhaseReplica rep(problem, arts, a.n, a.seed, a.workers);
 
   std::vector<std::uint8_t> g0;

@@ -381,7 +381,7 @@ struct gomix_gpu_engine {
   double elit_fit = 0.0;
   bool ctl_stale = false;  // a device-side IMS offer may have changed the elitist since read_ctl()
   std::vector<uint32_t> h_pop;
-  std::vector<uint64_t> perm;
+  std::vector<uint64_t> perm, perm_touched;  // replay donor scans (draw_replay_tape)
   int64_t last_group = -1;
   uint64_t launches = 0;
   std::vector<cudaEvent_t> ev_free;
@@ -488,8 +488,14 @@ struct gomix_gpu_engine {
     const int per_sm = gom_max_blocks_per_sm(P->univariate, P->i32, (int)wpt, tw > 1, (int)block, smem);
     if (per_sm < 1) invalid("engine: GOM kernel does not fit on an SM with this configuration");
     grid_cap = per_sm * sms;
-    if (P->univariate && P->i32 && mode == GOMIX_MODE_PHILOX && !(flags & GOMIX_FLAG_RECORD_BATCH) &&
-        !(flags & GOMIX_FLAG_LANE_PER_SOLUTION)) {
+    // The bit-sliced univariate kernels draw no donor: for F = {v} every
+    // member that differs on F holds !x_v, so the step is the same whatever
+    // donor the reference's scan picks (engine_serial.hpp:30-46) and only its
+    // presence (some member differs) matters.  They therefore serve REPLAY
+    // as well: the host walks the reference's RngStream through the same
+    // donor scans to stay in step (walk_replay_rng) and the kernel computes
+    // presence from the group-start row.
+    if (P->univariate && P->i32 && !(flags & GOMIX_FLAG_RECORD_BATCH) && !(flags & GOMIX_FLAG_LANE_PER_SOLUTION)) {
       univ_planes = univ_sliced_planes(P->max_abs_row);
       univ_tt = P->urec != nullptr && Wp <= 4 && !(flags & GOMIX_FLAG_NO_TRUTH_TABLE);
       if (univ_planes) univ_grid_cap = univ_sliced_max_blocks_per_sm(univ_planes, (int)Wp, univ_tt) * sms;
@@ -981,25 +987,35 @@ struct gomix_gpu_engine {
     fill_stats(out);
   }
 
-  void draw_replay_tape(uint64_t group) {
-    ensure_tape();
+  // upload == false: only walk the stream (the bit-sliced univariate kernels
+  // need no donors, see setup); the draws are the same either way.
+  void draw_replay_tape(uint64_t group, bool upload = true) {
+    if (upload) ensure_tape();
     const uint64_t nv = P->nv;
     h_pop.resize(nv * Wp);
     GOMIX_CUDA(cudaMemcpyAsync(h_pop.data(), pop, nv * Wp * 4, cudaMemcpyDeviceToHost, stream));
     GOMIX_CUDA(cudaStreamSynchronize(stream));
     const uint64_t g0 = P->group_off[group], G = P->group_off[group + 1] - g0;
-    perm.resize(n);
+    // perm is the identity between scans: each scan restores the entries it
+    // swapped (a scan touches ~2 entries on average, not n)
+    if (perm.size() != n) {
+      perm.resize(n);
+      for (uint64_t i = 0; i < n; ++i) perm[i] = i;
+    }
+    std::vector<uint64_t>& touched = perm_touched;
     auto bit = [&](uint32_t v, uint64_t s) { return (h_pop[(uint64_t)v * Wp + (s >> 5)] >> (s & 31)) & 1u; };
     for (uint64_t p = 0; p < G; ++p) {
       const uint64_t sid = P->group_sets[g0 + p];
       const uint32_t* vars = P->h_set_vars.data() + P->h_set_off[sid];
       const uint64_t f = P->h_set_off[sid + 1] - P->h_set_off[sid];
       for (uint64_t s = 0; s < n; ++s) {
-        for (uint64_t i = 0; i < n; ++i) perm[i] = i;
         int32_t donor = -1;
+        touched.clear();
         for (uint64_t i = 0; i < n && donor < 0; ++i) {
           const uint64_t j = i + rng.uniform_index(n - i);
           std::swap(perm[i], perm[j]);
+          touched.push_back(i);
+          touched.push_back(j);
           const uint64_t c = perm[i];
           for (uint64_t t = 0; t < f; ++t)
             if (bit(vars[t], c) != bit(vars[t], s)) {
@@ -1007,10 +1023,11 @@ struct gomix_gpu_engine {
               break;
             }
         }
-        h_tape_pinned[p * n + s] = donor;
+        for (uint64_t t : touched) perm[t] = t;
+        if (upload) h_tape_pinned[p * n + s] = donor;
       }
     }
-    GOMIX_CUDA(cudaMemcpyAsync(tape, h_tape_pinned, G * n * 4, cudaMemcpyHostToDevice, stream));
+    if (upload) GOMIX_CUDA(cudaMemcpyAsync(tape, h_tape_pinned, G * n * 4, cudaMemcpyHostToDevice, stream));
   }
 
   void upload_tape(uint64_t group, const int32_t* donor_sp) {
@@ -1159,9 +1176,9 @@ struct gomix_gpu_engine {
           read_ctl();
           if (h_ctl->stop) break;
         }
-        draw_replay_tape(gi);
+        draw_replay_tape(gi, !univ_planes);  // the bit-sliced kernels take no donor tape
       }
-      launch_group(gi, mode == GOMIX_MODE_REPLAY);
+      launch_group(gi, mode == GOMIX_MODE_REPLAY && !univ_planes);
     }
     if (fi_on) fi_after_generation();
     read_ctl();
@@ -1231,12 +1248,14 @@ struct gomix_gpu_engine {
     if (group >= P->k) invalid("run_group: group index out of range");
     begin_call(stop);
     bool with_tape = true;
-    if (donor_tape)
+    if (donor_tape) {
       upload_tape(group, donor_tape);
-    else if (mode == GOMIX_MODE_REPLAY)
-      draw_replay_tape(group);
-    else
+    } else if (mode == GOMIX_MODE_REPLAY) {
+      draw_replay_tape(group, !univ_planes);
+      with_tape = !univ_planes;
+    } else {
       with_tape = false;
+    }
     launch_group(group, with_tape);
     read_ctl();
     fill_stats(out);

@@ -14,23 +14,28 @@ namespace gomix_b200 {
 
 constexpr uint32_t kEpiSmemFit = 256;  // fitness values the epilogue keeps in shared memory
 
-// Timing probes for latency studies (GOMIX_EXP bit 32): CTA 0 / thread 0
-// records %globaltimer at numbered points of its first set.
+// Timing probes for latency studies: CTA 0 / thread 0 records %globaltimer at
+// numbered points.  Compiled in only with -DGOMIX_PROBES (and then enabled at
+// run time by GOMIX_EXP bit 32); production builds carry no probe code.
 static __device__ unsigned long long g_probe[64];  // one copy per translation unit
 __device__ __forceinline__ void probe(uint32_t flags, uint32_t i) {
+#ifdef GOMIX_PROBES
   if ((flags & 32u) && blockIdx.x == 0 && threadIdx.x == 0 && i < 64) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     if (g_probe[i] == 0) g_probe[i] = t;
   }
+#endif
 }
 // the same from thread 0 of whichever CTA calls it (the last-CTA epilogue)
 __device__ __forceinline__ void probe_last(uint32_t flags, uint32_t i) {
+#ifdef GOMIX_PROBES
   if ((flags & 32u) && threadIdx.x == 0 && i < 64) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     if (g_probe[i] == 0) g_probe[i] = t;
   }
+#endif
 }
 
 // ---------------------------------------------------------------------------

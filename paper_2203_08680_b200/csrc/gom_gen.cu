@@ -234,6 +234,7 @@ __global__ void __launch_bounds__(LEAN ? 256 : (TEAM ? 32 * TW : 256), LEAN ? 3 
       atomicAdd(CNT + 1, s_calls);
     }
     probe(a.exp_flags, 16 + 4 * slot);
+#ifdef GOMIX_PROBES
     if ((a.exp_flags & 32u) && slot == 0 && threadIdx.x == 0 && blockIdx.x < 4096) {
       unsigned long long t;
       uint32_t smid;
@@ -242,6 +243,7 @@ __global__ void __launch_bounds__(LEAN ? 256 : (TEAM ? 32 * TW : 256), LEAN ? 3 
       g_cta_probe[2 * blockIdx.x] = t;
       g_cta_probe[2 * blockIdx.x + 1] = smid;
     }
+#endif
     grid_barrier(ga.bar, gridDim.x);
     probe(a.exp_flags, 17 + 4 * slot);
 
@@ -364,7 +366,9 @@ __global__ void __launch_bounds__(LEAN ? 256 : (TEAM ? 32 * TW : 256), LEAN ? 3 
     c->done = 0;
     c->cur_gen = gen;
     c->gen_counter = gen + 1;
-    c->gen_buf = buf0 + (slot < ga.k ? slot + 1 : ga.k);
+    // the accumulator index itself (mod 3), not a running count: a count
+    // would wrap at 2^32, where 2^32 = 1 (mod 3) breaks the rotation
+    c->gen_buf = (buf0 + (slot < ga.k ? slot + 1 : ga.k)) % 3u;
     for (uint32_t i = 0; i < ga.k; ++i) ga.order[i] = s_order[i];
   }
 }

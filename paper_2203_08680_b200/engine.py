@@ -518,11 +518,17 @@ class GpuLocalGroup:
         ctl = self.ctx.control
         if ctl.stop_requested():
             return
+        mg = ctl.cfg.max_generations
+        if mg is not None and self.generation() >= mg:  # engine_parallel.hpp:284-289
+            ctl.request_stop("generation-limit")
+            return
         gen = self.generation()
         stats = _capi.RunStats()
         crit = ctl.criteria()
         check(lib().gomix_gpu_local_group_run_generation(self.h, C.byref(crit), C.byref(stats)))
         self.shards[0]._absorb(stats, gen)
+        if not stats.stopped:  # wall clock + trace boundary row, like GpuParallelEngine
+            self.ctx.report_boundary(self.shards[0]._elitist_fitness, self.generation(), 1)
 
     def generation(self) -> int:
         return self.shards[0].generation()

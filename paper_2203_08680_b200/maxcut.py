@@ -8,6 +8,8 @@ type (linkage.hpp:124-131).  Generators run in the product library's host code
 from __future__ import annotations
 
 import math
+import os
+import re
 from dataclasses import dataclass
 
 import ctypes as C
@@ -103,37 +105,90 @@ def save_edge_list(path: str, inst: MaxCutInstance) -> None:
             fh.write(f"{a + 1} {b + 1} {ws}\n")
 
 
-def load_edge_list(path: str) -> MaxCutInstance:
-    """maxcut.hpp:163-226 (1-based, '#' comments, duplicates rejected)."""
-    rows = []
-    header = None
-    with open(path) as fh:
-        for ln, line in enumerate(fh, 1):
-            s = line.strip()
-            if not s or s.startswith("#"):
-                continue
+class ParseError(ValueError):
+    """maxcut.hpp:149-158: a malformed edge list; `line` is the 1-based line
+    the error was detected on (the message starts with "line N: ")."""
+
+    def __init__(self, line: int, what: str):
+        super().__init__(f"line {line}: {what}")
+        self.line = line
+
+
+def _int_token(t: str) -> int:
+    """A whole token read by istream >> long long: optional sign, digits."""
+    if not re.fullmatch(r"[+-]?[0-9]+", t):
+        raise ValueError(t)
+    return int(t)
+
+
+def load_edge_list(source) -> MaxCutInstance:
+    """load_edge_list (maxcut.hpp:160-226): a "<num_vertices> <num_edges>"
+    header, then one "<u> <v> <w>" line per edge, 1-based endpoints; blank
+    lines and lines starting with '#' skipped.  Errors raise ParseError with
+    the reference's line numbers (KATs: test_maxcut.cpp:182-201).  `source`
+    is a path or a text stream."""
+    fh = open(source) if isinstance(source, (str, bytes, os.PathLike)) else source
+    try:
+        lines = iter(fh)
+        line_no = 0
+
+        def next_payload():
+            nonlocal line_no
+            for line in lines:
+                line_no += 1
+                s = line.strip()
+                if not s or s.startswith("#"):
+                    continue
+                return s
+            return None
+
+        head = next_payload()
+        if head is None:
+            raise ParseError(line_no, "missing header")
+        parts = head.split()
+        try:
+            if len(parts) != 2:
+                raise ValueError(head)
+            nv, ne = _int_token(parts[0]), _int_token(parts[1])
+            if nv < 1 or ne < 0:
+                raise ValueError(head)
+        except ValueError:
+            raise ParseError(line_no, "malformed header, expected '<num_vertices> <num_edges>'") from None
+        rows = []
+        seen = set()
+        while len(rows) < ne:
+            s = next_payload()
+            if s is None:
+                raise ParseError(line_no, "fewer edge lines than the header declares")
             parts = s.split()
-            if header is None:
-                if len(parts) != 2:
-                    raise ValueError(f"line {ln}: malformed header")
-                header = (int(parts[0]), int(parts[1]))
-                continue
-            if len(parts) != 3:
-                raise ValueError(f"line {ln}: malformed edge line")
-            a, b, w = int(parts[0]) - 1, int(parts[1]) - 1, float(parts[2])
-            if a == b:
-                raise ValueError(f"line {ln}: self-loop")
-            rows.append((min(a, b), max(a, b), w))
-    if header is None:
-        raise ValueError("missing header")
-    if len(rows) != header[1]:
-        raise ValueError("edge count differs from the header")
-    rows.sort()
+            try:
+                if len(parts) != 3:
+                    raise ValueError(s)
+                u, v, w = _int_token(parts[0]), _int_token(parts[1]), float(parts[2])
+                if not math.isfinite(w):  # istream >> double reads no inf / nan / overflow
+                    raise ValueError(s)
+            except ValueError:
+                raise ParseError(line_no, "malformed edge line, expected '<u> <v> <w>'") from None
+            if u < 1 or v < 1 or u > nv or v > nv:
+                raise ParseError(line_no, "vertex index out of range")
+            if u == v:
+                raise ParseError(line_no, "self-loop")
+            if not math.isfinite(w):
+                raise ParseError(line_no, "non-finite weight")
+            a, b = min(u, v) - 1, max(u, v) - 1
+            if (a, b) in seen:
+                raise ParseError(line_no, "duplicate edge")
+            seen.add((a, b))
+            rows.append((a, b, w))
+        if next_payload() is not None:
+            raise ParseError(line_no, "more edge lines than the header declares")
+    finally:
+        if fh is not source:
+            fh.close()
+    rows.sort(key=lambda r: (r[0], r[1]))
     u = np.array([r[0] for r in rows], np.uint32)
     v = np.array([r[1] for r in rows], np.uint32)
-    if len(set(zip(u.tolist(), v.tolist()))) != len(rows):
-        raise ValueError("duplicate edge")
-    return MaxCutInstance(header[0], u, v, np.array([r[2] for r in rows], np.float64))
+    return MaxCutInstance(nv, u, v, np.array([r[2] for r in rows], np.float64))
 
 
 @dataclass

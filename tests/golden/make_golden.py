@@ -69,6 +69,64 @@ IMS_CASES = [
 ]
 
 
+# Full-size replay fixtures (ref_driver run --light: per-generation packed
+# populations are hashed here, fitness / elitist / calls / counters / traces
+# kept whole): (name, torus w, h, weights, inst seed, fos, n, seed, gens).
+# These pin the bit-sliced univariate kernels (gom_univ_tt_kernel,
+# gom_univ_sliced_kernel) that run the BASELINE configs C3 and C5.
+LIGHT_CASES = [
+    ("c3_full", 1000, 1000, "int:1:10", 1, "univariate", 128, 1, 3),
+    ("c5_n16", 316, 316, "int:1:10", 1, "univariate", 16, 2, 6),
+    ("c5_n1024", 316, 316, "int:1:10", 1, "univariate", 1024, 3, 2),
+    ("c1_long", 10, 10, "int:1:10", 1, "univariate", 32, 4, 60),
+    ("c3_pm", 200, 150, "int:-6:9", 5, "univariate", 100, 9, 4),
+]
+
+
+def array_hash(*arrays) -> np.uint64:
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return np.frombuffer(h.digest()[:8], np.uint64)[0]
+
+
+def packed_hash(packed: np.ndarray) -> np.uint64:
+    """Hash of one population as numpy.packbits of its (n, l) genotype bytes."""
+    return np.frombuffer(hashlib.sha256(np.ascontiguousarray(packed).tobytes()).digest()[:8], np.uint64)[0]
+
+
+def make_light(cases):
+    with tempfile.TemporaryDirectory() as tmp:
+        for name, w, h, weights, iseed, fos, n, seed, gens in cases:
+            out = os.path.join(tmp, name + ".bin")
+            d = O.run_ref("run", "--torus", w, h, "--weights", weights, "--inst-seed", iseed, "--fos", fos,
+                          "--n", n, "--seed", seed, "--gens", gens, "--workers", os.cpu_count() or 4, "--light",
+                          out=out, timeout=7200)
+            nv = int(d["num_vertices"][0])
+            per = (n * nv + 7) // 8
+            packed = d["packed"].reshape(gens, per)
+            lo, hi = (int(x) for x in weights.split(":")[1:]) if weights != "unit" else (0, 0)
+            f = {"torus": np.array([w, h], np.uint64), "weights": np.array([weights]),
+                 "inst_seed": np.array([iseed], np.uint64), "fos_kind": np.array([fos]),
+                 "n": np.array([n], np.uint64), "seed": np.array([seed], np.uint64),
+                 "gens": np.array([gens], np.uint64), "num_vertices": d["num_vertices"],
+                 "edges_hash": np.array([array_hash(d["edge_u"].astype(np.uint32), d["edge_v"].astype(np.uint32),
+                                                    d["edge_w"].astype(np.float64))], np.uint64),
+                 "group_off": d["group_off"],
+                 "group_sets_hash": np.array([array_hash(d["group_sets"].astype(np.uint64))], np.uint64),
+                 "init_hash": np.array([packed_hash(d["init_packed"])], np.uint64),
+                 "init_fitness": d["init_fitness"], "init_elitist": d["init_elitist"],
+                 "init_calls": d["init_calls"],
+                 "pop_hash": np.array([packed_hash(p) for p in packed], np.uint64),
+                 "fitness": d["fitness"], "elitist": d["elitist"], "calls": d["calls"],
+                 "counter_steps": d["counter_steps"], "counter_calls": d["counter_calls"],
+                 "trace_fitness": d["trace_fitness"], "trace_evals": d["trace_evals"],
+                 "trace_generation": d["trace_generation"]}
+            np.savez_compressed(os.path.join(HERE, name + ".npz"), **f)
+            print(f"{name}: nv={nv} groups={len(d['group_off']) - 1} best={d['elitist'][-1]} "
+                  f"trace={len(d['trace_fitness'])}", flush=True)
+
+
 def random_regular(nv: int, d: int, seed: int):
     """Random d-regular simple graph (configuration-model pairing, redrawn on
     self-loops/duplicates) with fp64 weights uniform in [0, 1).  The reference
@@ -155,4 +213,8 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if "--light" in sys.argv[1:]:
+        names = [a for a in sys.argv[1:] if not a.startswith("--")]
+        make_light([c for c in LIGHT_CASES if not names or c[0] in names])
+    else:
+        main()

@@ -49,8 +49,15 @@ def test_gpu_colouring_equals_reference_welsh_powell(name):
     assert P.info.lmig_edges == int(d["lmig_edges"][0])
 
 
-@pytest.mark.parametrize("name", RUN_CASES)
-def test_replay_generations_match_reference(name):
+# univariate integer fixtures run the bit-sliced kernels in replay; each is
+# also replayed through the other two univariate kernels
+UNIV_INT = ["c1_int", "c1_pm5", "torus6_w"]
+KERNEL_VARIANTS = {"default": {}, "adder": dict(truth_table=False), "lane": dict(lane_per_solution=True)}
+
+
+@pytest.mark.parametrize("name,variant", [(c, "default") for c in RUN_CASES] +
+                         [(c, v) for c in UNIV_INT for v in ("adder", "lane")])
+def test_replay_generations_match_reference(name, variant):
     """ParallelEngine::run_generation replayed: bit-identical per generation."""
     d = GU.load(name)
     inst, fos, P = fixture_problem(d)
@@ -58,7 +65,10 @@ def test_replay_generations_match_reference(name):
     n, seed, gens = int(d["n"][0]), int(d["seed"][0]), int(d["gens"][0])
     sink = G.RecordingSink()
     ctx = G.RunContext(G.TerminationConfig(), P.comparator(), inst.num_edges, sink)
-    E = G.GpuParallelEngine(P, n, seed, ctx=ctx, mode="replay")
+    E = G.GpuParallelEngine(P, n, seed, ctx=ctx, mode="replay", **KERNEL_VARIANTS[variant])
+    if name in UNIV_INT:
+        assert E.kernel_name() == {"default": "gom_univ_tt_kernel", "adder": "gom_univ_sliced_kernel",
+                                   "lane": "gom_group_kernel"}[variant]
     g, f = E.population()
     assert (g.ravel() == d["init_genotypes"]).all()
     assert (f == d["init_fitness"]).all()
@@ -286,6 +296,54 @@ def test_philox_group_step_semantics(kind, n):
                     expect = delta > 0 or (delta == 0 and not is_elit)
                     assert bool(ac[s, p]) == expect
             _check_consistent(inst, E)
+
+
+def _nbr_tables(inst):
+    """Per vertex its (up to 4) neighbours and edge weights, zero-padded."""
+    nv = inst.num_vertices
+    nb = np.tile(np.arange(nv)[:, None], (1, 4))
+    w = np.zeros((nv, 4))
+    cnt = np.zeros(nv, int)
+    for a, b, x in zip(inst.edge_u.tolist(), inst.edge_v.tolist(), inst.edge_w.tolist()):
+        for p, q in ((a, b), (b, a)):
+            nb[p, cnt[p]] = q
+            w[p, cnt[p]] = x
+            cnt[p] += 1
+    return nb, w
+
+
+@pytest.mark.parametrize("shape,weights,n", [((24, 20), ("int", -4, 9), 128), ((30, 16), ("int", 1, 10), 32),
+                                             ((20, 20), ("int", -3, 3), 100), ((18, 14), ("int", 0, 2), 64)])
+def test_philox_truth_table_group_step_semantics(shape, weights, n):
+    """The benchmarked kernel (gom_univ_tt_kernel, no batch recording) pair by
+    pair: (s, {v}) is present iff some member holds the other value; its delta
+    is the cut difference of flipping v; it is accepted iff delta > 0 or
+    (delta == 0 and s is not the group-start elitist) (engine_parallel.hpp:
+    104-247); accepted pairs flip, fitness += sum of accepted deltas."""
+    inst = G.generate_torus(shape[0], shape[1], weights, 11)
+    P = G.GpuProblem(inst, G.univariate_fos(inst.num_vertices))
+    E = G.GpuParallelEngine(P, n, 5, mode="philox")
+    assert E.kernel_name() == "gom_univ_tt_kernel"
+    nb, w = _nbr_tables(inst)
+    for rnd in range(4):
+        for gi in range(P.num_groups):
+            g0, f0 = E.population()
+            eg, _ = E.elitist()
+            E.run_group(gi)
+            g1, f1 = E.population()
+            vs = P.group_sets[P.group_offset[gi]:P.group_offset[gi + 1]].astype(np.int64)
+            x = g0[:, vs].astype(bool)
+            present = x.min(axis=0) != x.max(axis=0)
+            cut = x[:, :, None] != g0[:, nb[vs]].astype(bool)
+            delta = (w[vs][None] * (1 - 2 * cut.astype(np.int64))).sum(axis=2)
+            is_elit = (g0 == eg).all(axis=1)
+            acc = present[None] & ((delta > 0) | ((delta == 0) & ~is_elit[:, None]))
+            assert (g1[:, vs].astype(bool) == (x ^ acc)).all(), (rnd, gi)
+            rest = np.ones(inst.num_vertices, bool)
+            rest[vs] = False
+            assert (g1[:, rest] == g0[:, rest]).all()
+            assert (f1 == f0 + (acc * delta).sum(axis=1)).all()
+    _check_consistent(inst, E)
 
 
 @pytest.mark.parametrize("kind,shape,n,gens", [("uni", (1000, 1000), 128, 3), ("neigh", (100, 100), 64, 10),
