@@ -10,10 +10,14 @@ evaluation = one executed (solution, linkage set) GOM step
 
 Default workload: BASELINE.json configs[2] = C3, Max-Cut 2-D torus 1000x1000
 (10^6 vertices), integer weights U[1,10] (generate_torus seed 1), univariate
-FOS, population 128 per GPU, Philox donors.  The metric is quoted "at
-1/2/4/8 B200", which is this config ("sharded 1/2/4/8 B200"), and the north
+FOS, population 128, Philox donors.  The metric is quoted "at 1/2/4/8 B200",
+which is this config ("population 128, sharded 1/2/4/8 B200"), and the north
 star's target is stated on it (the 10^6-vertex grid on 1 B200); it fits one
 GPU.  configs[1] (C2: 100x100, neighbourhood FOS, n=64) is --config c2.
+
+Scaling: --scaling strong (default) keeps BASELINE's population of 128 in
+total and shards it over the N GPUs (128/N members each, NCCL exchange per
+colour group); --scaling weak gives every GPU 128 members.
 
 ours:
   value  device throughput, inputs resident in HBM: CUDA events on the engine's
@@ -47,7 +51,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "Max-Cut partial evals/sec; time-to-best-known cut (s) at 1/2/4/8 B200"
-REF_BUDGET_S = 90.0  # reference arm: cap on the generations it times (bounded sample)
+REF_BUDGET_S = 900.0  # reference arm: safety cap on its W + K generations (C3: ~12 s each on 16 threads)
+# time-to-target leg: a FIXED cut per config (from the reference's own IMS
+# runs, tools/success_rate.py pilots), so every run and every N aim at the
+# same value; the CPU reference is timed to it in the same run
+TTT_TARGETS = {"c1": 1110.0, "c2": 103400.0, "c3": 9600000.0, "c5": None}
 UNIT = "partial evaluations/s"
 
 CONFIGS = {
@@ -75,8 +83,10 @@ def parse():
     ap.add_argument("--population", type=int, default=None)
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ttt-seconds", type=float, default=20.0,
-                    help="time-to-best-known-cut leg: reference IMS budget T_ref (0 = skip)")
+    ap.add_argument("--ttt-seconds", type=float, default=60.0,
+                    help="time-to-target leg: wall budget of the reference IMS and of ours (0 = skip)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: BASELINE's population in total over the N GPUs; weak: that many per GPU")
     return ap.parse_args()
 
 
@@ -105,13 +115,32 @@ def run_reference(cfg, n, gens, workers, timeout=3600, max_seconds=0.0):
     return json.loads(res.stdout)
 
 
-def base_line(args, cfg, n, world):
+def population_total(args, cfg, world):
+    """BASELINE C3 is "population 128, sharded 1/2/4/8 B200": strong scaling
+    keeps the population fixed; weak scaling gives every GPU that many."""
+    n = args.population or cfg["n"]
+    return n if args.scaling == "strong" else n * world
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def base_line(args, cfg, n_total, world):
     return {"metric": METRIC, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "int32",
             "data": "synthetic (generated Max-Cut torus, reference generator and seed)",
-            "config": {"workload": cfg["workload"], "population": n * world, "population_per_gpu": n,
-                       "parallelism": f"population sharded over {world} GPUs (NCCL all-gather of the donor pool "
-                                      f"per colour group)" if world > 1 else "single",
+            "config": {"workload": cfg["workload"], "population": n_total, "population_per_gpu": n_total // world,
+                       "parallelism": f"population sharded over {world} GPUs ({n_total // world} members each; "
+                                      f"NCCL exchange of fitness / hashes / counters per colour group, row "
+                                      f"1-counts per generation)" if world > 1 else "single",
                        "l2": "flushed between timed steps (256 MiB write)",
                        "donors": "philox", "fos": cfg["fos"]}}
 
@@ -124,27 +153,29 @@ def bench_reference(args):
     if rank != 0:
         return
     cfg = CONFIGS[args.config]
-    n = args.population or cfg["n"]
+    n_total = population_total(args, cfg, world)
     workers = os.cpu_count() or 1
     if not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "ref_driver")):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/ref_driver was not built"}))
         return
-    # the same population as our arm at N GPUs (n per GPU, weak scaling);
-    # bounded sample: W + K generations, or as many as fit in REF_BUDGET_S
-    out = run_reference(cfg, n * world, args.warmup + args.steps, workers, max_seconds=REF_BUDGET_S)
+    # the same population and workload as our arm at N GPUs; one step = one
+    # generation, W + K of them (a safety cap of REF_BUDGET_S s of
+    # generations; steps reports how many were timed)
+    out = run_reference(cfg, n_total, args.warmup + args.steps, workers, max_seconds=REF_BUDGET_S)
     allg = out["gens"]
     warm = min(args.warmup, max(0, len(allg) - 1))
     gens = allg[warm:]
     secs = sum(g["seconds"] for g in gens)
     steps = sum(g["steps"] for g in gens)
     value = steps / secs
-    line = base_line(args, cfg, n, world)
+    line = base_line(args, cfg, n_total, world)
     line.update({"impl": "reference", "value": value, "ms_per_step": 1e3 * secs / len(gens), "dtype": "f64",
-                 "steps_timed": len(gens), "warmup_run": warm,
+                 "steps": len(gens), "steps_requested": args.steps, "warmup": warm,
                  "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "reference",
+                                  "cpu": cpu_model(),
                                   "sample": f"{len(gens)} generations of {args.config} after {warm} warm-up "
-                                            f"(W + K = {args.warmup + args.steps} requested, capped at "
-                                            f"{REF_BUDGET_S:g} s of generations), ParallelEngine(workers={workers})"},
+                                            f"generations, ParallelEngine(workers={workers}) built from the "
+                                            f"reference headers (oracle/_ref/ref_driver)"},
                  "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
     line["config"]["parallelism"] = f"cpu ParallelEngine workers={workers}"
     line["config"]["donors"] = "reference RngStream"
@@ -217,6 +248,15 @@ def algorithmic_bytes_per_step(inst, fos, n):
     return total / fos.num_sets
 
 
+def make_engine(G, P, n_total, seed, stream, rank, world, uid):
+    """One population of n_total members: single GPU, or sharded over the
+    ranks (rank r holds n_total / world)."""
+    if world > 1:
+        return G.GpuParallelEngine(P, n_total, seed=seed, mode="philox", stream=stream.cuda_stream, rank=rank,
+                                   world_size=world, nccl_unique_id=uid)
+    return G.GpuParallelEngine(P, n_total, seed=seed, mode="philox", stream=stream.cuda_stream)
+
+
 def bench_ours(args):
     import numpy as np
     import torch
@@ -234,27 +274,34 @@ def bench_ours(args):
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
     cfg = CONFIGS[args.config]
-    n = args.population or cfg["n"]
+    n_total = population_total(args, cfg, world)
+    if n_total % world:
+        raise SystemExit(f"population {n_total} is not divisible by {world} GPUs")
     inst = G.generate_torus(cfg["width"], cfg["height"], cfg["weights"], 1)
     fos = G.univariate_fos(inst.num_vertices) if cfg["fos"] == "uni" else G.neighbourhood_fos(inst)
     P = G.GpuProblem(inst, fos, device=dev)
     stream = torch.cuda.Stream()  # a real stream: the legacy NULL stream would not see our kernels
     torch.cuda.set_stream(stream)
-    if world > 1:
-        # one population of n * world members sharded over the ranks (weak
-        # scaling: n members per GPU); the NCCL id travels over the PG
-        uid = [G.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        E = G.GpuParallelEngine(P, n * world, seed=1, mode="philox", stream=stream.cuda_stream, rank=rank,
-                                world_size=world, nccl_unique_id=uid[0])
-        gen = E.run_generation          # collective per colour group: host-ordered
-    else:
-        E = G.GpuParallelEngine(P, n, seed=1, mode="philox", stream=stream.cuda_stream)
-        gen = E.run_generation_async    # one CUDA graph per generation, no host sync
+    uid = None
+    if world > 1:  # the NCCL id of the engines' communicator travels over the process group
+        box = [G.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        uid = box[0]
+    E = make_engine(G, P, n_total, 1, stream, rank, world, uid)
+    # single GPU: one CUDA graph per generation, no host sync; sharded: the
+    # collective per colour group is host-ordered
+    gen = E.run_generation_async if world == 1 else E.run_generation
 
     def barrier():
         if dist is not None:
             dist.barrier()
+
+    def max_over_ranks(*xs):
+        if dist is None:
+            return xs
+        t = torch.tensor(list(xs), dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return tuple(float(v) for v in t.tolist())
 
     # warm-up
     for _ in range(max(args.warmup, 3)):
@@ -304,7 +351,7 @@ def bench_ours(args):
     E.synchronize()
     clk = clocks.stop()
     # dominant-kernel durations (roofline): the same generations issued launch
-    # by launch with CUDA events around every gom_group_kernel
+    # by launch with CUDA events around every GOM kernel launch
     kern_gens = min(args.steps, 50)
     _, ksteps0, _ = E.group_counters()
     E.set_timing(True)
@@ -321,13 +368,34 @@ def bench_ours(args):
     dev_s = sum(step_ms) / 1e3
     steps = int((steps1 - steps0).sum())
     calls = int((calls1 - calls0).sum())
-    if dist is not None:
-        t = torch.tensor([dev_s], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        # sharded counters are already global (every rank accounts all ranks'
-        # steps in its epilogue): no sum over ranks
-        dev_s = float(t.item())
+    # sharded counters are already global (every rank accounts all ranks'
+    # steps in its epilogue): no sum over ranks, the time is the max
+    (dev_s,) = max_over_ranks(dev_s)
     value = steps / dev_s
+
+    # ---- active phase: generations 1-5 of a fresh population ----
+    # (the timed generations above are the steady state, where most pairs are
+    # neutral or rejected; early generations accept and improve far more)
+    E_act = make_engine(G, P, n_total, 2, stream, rank, world, uid)
+    act_gens = 5
+    a0 = [torch.cuda.Event(enable_timing=True) for _ in range(act_gens)]
+    a1 = [torch.cuda.Event(enable_timing=True) for _ in range(act_gens)]
+    _, as0, _ = E_act.group_counters()
+    barrier()
+    torch.cuda.synchronize()
+    for i in range(act_gens):
+        flush.zero_()
+        a0[i].record(stream)
+        (E_act.run_generation_async if world == 1 else E_act.run_generation)()
+        a1[i].record(stream)
+    torch.cuda.synchronize()
+    E_act.synchronize()
+    _, as1, _ = E_act.group_counters()
+    (act_s,) = max_over_ranks(sum(x.elapsed_time(y) for x, y in zip(a0, a1)) / 1e3)
+    act_steps = int((as1 - as0).sum())
+    active = {"value": act_steps / act_s, "unit": UNIT, "generations": "1-5 of a fresh population (seed 2)",
+              "ms_per_step": 1e3 * act_s / act_gens}
+    del E_act
 
     # ---- e2e through the C-ABI with host buffers ----
     # (1) the drop-in call pattern: what the reference's run loop / ImsDriver
@@ -357,8 +425,9 @@ def bench_ours(args):
     # (2) the whole population in and out every step (n*l genotype bytes +
     #     n fitness doubles each way): the cost of a caller that keeps the
     #     population on the host
-    g_host = torch.empty((n, inst.num_vertices), dtype=torch.uint8, pin_memory=True).numpy()
-    f_host = torch.empty((n,), dtype=torch.float64, pin_memory=True).numpy()
+    n_local = n_total // world
+    g_host = torch.empty((n_local, inst.num_vertices), dtype=torch.uint8, pin_memory=True).numpy()
+    f_host = torch.empty((n_local,), dtype=torch.float64, pin_memory=True).numpy()
     E.population(g_host, f_host)
     for _ in range(3):  # warm the transfer path
         E.load_population(g_host, f_host)
@@ -377,13 +446,16 @@ def bench_ours(args):
     torch.cuda.synchronize()
     barrier()
     rt_s = time.perf_counter() - t0
-    if dist is not None:
-        t = torch.tensor([e2e_s, rt_s], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s, rt_s = float(t[0].item()), float(t[1].item())
-    io_bytes = n * inst.num_vertices + 8 * n
+    e2e_s, rt_s = max_over_ranks(e2e_s, rt_s)
+    io_bytes = n_local * inst.num_vertices + 8 * n_local
     crit_bytes = 40           # gomix_stop_criteria
     stats_bytes = 48 + 1024   # gomix_run_stats + control block and inline improvement log read back
+
+    # ---- time to a fixed target cut (every rank: one IMS per GPU) ----
+    time_to_target = None
+    target = TTT_TARGETS.get(args.config)
+    if args.ttt_seconds > 0 and target is not None:
+        time_to_target = time_to_target_leg(args, cfg, G, P, inst, fos, target, rank, world, dist, dev)
 
     if rank != 0:
         if dist is not None:
@@ -399,14 +471,14 @@ def bench_ours(args):
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"
-    b_step = algorithmic_bytes_per_step(inst, fos, n)
+    b_step = algorithmic_bytes_per_step(inst, fos, n_local)
     kern_s = float(np.sum(kern_ms)) / 1e3
-    achieved = kern_steps * b_step / kern_s / 1e9 if kern_s > 0 else None
+    achieved = kern_steps / world * b_step / kern_s / 1e9 if kern_s > 0 else None  # this rank's share of the steps
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
             tr = json.load(fh).get(args.config)
-            if tr and tr.get("population") == n and tr.get("kernel", "gom_group_kernel") == E.kernel_name():
+            if tr and tr.get("population") == n_local and tr.get("kernel", "gom_group_kernel") == E.kernel_name():
                 traffic = tr["dram_bytes_per_launch"]
     except (OSError, ValueError):
         pass
@@ -425,42 +497,24 @@ def bench_ours(args):
         gens = 8 if args.config in ("c2", "c1") else 2
         if os.path.exists(ref):
             try:
-                out = run_reference(cfg, n, gens, workers, timeout=900)
-                secs = sum(g["seconds"] for g in out["gens"])
-                st = sum(g["steps"] for g in out["gens"])
+                out = run_reference(cfg, n_total, gens + 1, workers, timeout=900)
+                timed = out["gens"][1:]  # the first generation is the warm-up
+                secs = sum(g["seconds"] for g in timed)
+                st = sum(g["steps"] for g in timed)
                 cpu_baseline = {"value": st / secs, "unit": UNIT, "cores": workers, "kind": "reference",
-                                "sample": f"{gens} generations of {args.config} ({st} partial evaluations), "
-                                          f"reference ParallelEngine(workers={workers}) built from its headers"}
+                                "cpu": cpu_model(),
+                                "sample": f"generations 2-{gens + 1} of {args.config} ({st} partial evaluations) "
+                                          f"after 1 warm-up generation, reference ParallelEngine(workers={workers}) "
+                                          f"built from its headers"}
             except Exception as exc:  # noqa: BLE001
                 cpu_baseline = {"value": None, "unit": UNIT, "cores": workers, "kind": "reference",
                                 "sample": f"failed: {exc}"}
 
-    time_to_target = None
-    if world == 1 and args.ttt_seconds > 0:
-        try:
-            sys.path.insert(0, os.path.join(ROOT, "tools"))
-            import time_to_target as TT
-
-            ref = TT.reference_ims(cfg, 1, args.ttt_seconds, os.cpu_count() or 1)
-            gpu = TT.gpu_ims(cfg, ref["best"], 1, args.ttt_seconds)
-            time_to_target = {
-                "unit": "s", "target_cut": ref["best"],
-                "target": f"best cut of the reference IMS (base 16, sub 4, {cfg['fos']} FOS, "
-                          f"{os.cpu_count()} threads) within {args.ttt_seconds:g} s, seed 1",
-                "cpu_s": ref["seconds_to_best"], "gpu_s": gpu["seconds_to_target"],
-                "gpu_s_incl_build": gpu["seconds_to_target_incl_build"], "gpu_reached": gpu["reached"],
-                "speedup": (ref["seconds_to_best"] / gpu["seconds_to_target"]) if gpu["reached"] else None,
-                "gpu_build_s": gpu["build_seconds"], "gpu_evaluations": gpu["evaluations"],
-                "cpu_evaluations": ref["evaluations"],
-                "timing": "both from RunContext creation to the improvement reaching the cut (model prebuilt); "
-                          "gpu_s_incl_build adds the device problem build (CSR, GPU colouring)"}
-        except Exception as exc:  # noqa: BLE001
-            time_to_target = {"error": str(exc)[:300]}
-
-    line = base_line(args, cfg, n, world)
+    line = base_line(args, cfg, n_total, world)
     line.update({
         "value": value,
         "ms_per_step": 1e3 * dev_s / args.steps,
+        "active_phase": active,
         "e2e": {"value": e2e_done / e2e_s, "unit": UNIT, "h2d_bytes_per_step": crit_bytes,
                 "d2h_bytes_per_step": stats_bytes + (inst.num_vertices + 8) * elit_reads / e2e_steps,
                 "steps": e2e_steps, "elitist_reads": elit_reads,
@@ -468,11 +522,11 @@ def bench_ours(args):
                         "GenerationRunner calls: run_generation (stop criteria in, stats + improvements out) "
                         "+ the elitist genotype read back after every generation that improved it (the C++ "
                         "adapter's lazy elitist(): the genotype changes only with a strictly better fitness, "
-                        "engine_parallel.hpp:305-310); wall clock"},
+                        "engine_parallel.hpp:305-310); wall clock, max over ranks"},
         "e2e_population_roundtrip": {"value": rt_done / rt_s, "unit": UNIT, "h2d_bytes_per_step": io_bytes,
                                      "d2h_bytes_per_step": io_bytes, "steps": rt_steps,
                                      "what": "load_population + run_generation + read_population (the whole "
-                                             "population as genotype bytes both ways every step)"},
+                                             "population as genotype bytes both ways every step, per rank)"},
         "roofline": roofline,
         "cpu_baseline": cpu_baseline,
         "time_to_target": time_to_target,
@@ -485,6 +539,59 @@ def bench_ours(args):
     print(json.dumps(line))
     if dist is not None:
         dist.destroy_process_group()
+
+
+def time_to_target_leg(args, cfg, G, P, inst, fos, target, rank, world, dist, dev):
+    """Time to a fixed cut: the reference's run_parallel IMS (rank 0, every
+    host thread) and ours — one IMS per GPU with the run-wide best exchanged
+    between them (paper_2203_08680_b200/islands.py; one GPU = run_gpu's IMS).
+    Both clocks run from RunContext creation with the model prebuilt; every
+    GPU rank starts after a barrier; the GPU time is the first rank to reach
+    the cut."""
+    import torch
+
+    from paper_2203_08680_b200.islands import BestExchange, run_islands
+
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import time_to_target as TT
+
+    cpu = None
+    if rank == 0:
+        try:
+            cpu = TT.reference_to_target(cfg, 1, target, args.ttt_seconds, os.cpu_count() or 1)
+        except Exception as exc:  # noqa: BLE001
+            cpu = {"error": str(exc)[:300]}
+    # the IMS population sizes' kernels load on first use: a one-time process
+    # cost, paid here untimed on a tiny problem
+    TT.warm_device()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    G.GpuProblem(inst, fos, device=dev)  # the device model build, timed apart (CSR, colouring, plans)
+    build_s = time.perf_counter() - t0
+    ex = BestExchange(inst.num_vertices, device=torch.device("cuda", dev)) if world > 1 else None
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    r = run_islands(P, G.TerminationConfig(target_fitness=target, max_seconds=args.ttt_seconds), seed=1,
+                    exchange=ex)
+    if rank != 0:
+        return None
+    out = {"unit": "s", "target_cut": target,
+           "target": f"fixed cut for {args.config} (tools/success_rate.py STUDY; the reference's IMS reaches it "
+                     f"in most runs), seed 1, wall budget {args.ttt_seconds:g} s each side",
+           "cpu": cpu, "cpu_s": (cpu or {}).get("seconds_to_target"),
+           "gpu_s": r.seconds_to_target, "gpu_reached": r.reason == "target-reached",
+           "gpu_rank_s": r.rank_seconds_to_target, "gpu_build_s": build_s,
+           "gpu_s_incl_build": (r.seconds_to_target + build_s) if r.seconds_to_target is not None else None,
+           "gpu_evaluations": r.evaluations, "gpu_populations": r.populations,
+           "gpu_exchanges": r.exchanges,
+           "timing": "both from RunContext creation to the improvement reaching the cut (model prebuilt); "
+                     "gpu_s_incl_build adds the device problem build; N GPUs = one IMS per GPU with the best "
+                     "exchanged (islands.py), time of the first rank to reach the cut"}
+    if out["cpu_s"] and out["gpu_s"]:
+        out["speedup"] = out["cpu_s"] / out["gpu_s"]
+        out["speedup_incl_build"] = out["cpu_s"] / out["gpu_s_incl_build"]
+    return out
 
 
 def main():

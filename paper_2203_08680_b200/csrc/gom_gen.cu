@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(LEAN ? 256 : (TEAM ? 32 * TW : 256), LEAN ? 3 
       for (uint32_t p = gwarp / Wp; p < d.G; p += per_round) {
         const LeanPre cur = (p == gwarp / Wp && slot > 0) ? pre : lean_prefetch(a, gmeta, p, lane);
         gom_lean_unit(a, p, cur, lean_w, gen, wsm, lane, is_elit[0], esrc, ever_cur, false, acc[0], dh1[0],
-                      dh2[0], steps, calls);
+                      dh2[0], steps, calls, Wp > 1 ? ga.sib + (size_t)bi * ga.sib_stride : nullptr);
       }
       // the next group's first unit: plan inputs in flight during the barrier
       if (slot + 1 < ga.k) {
@@ -276,6 +276,10 @@ __global__ void __launch_bounds__(LEAN ? 256 : (TEAM ? 32 * TW : 256), LEAN ? 3 
       ga.cnt[2 * zb] = 0;
       ga.cnt[2 * zb + 1] = 0;
     }
+    if (LEAN && lead && Wp > 1) {  // the previous group's sibling counters, same rotation as D
+      unsigned int* z = ga.sib + (size_t)((bi + 2u) % 3u) * ga.sib_stride;
+      for (uint32_t i = threadIdx.x; i < ga.sib_stride; i += blockDim.x) z[i] = 0u;
+    }
     if (threadIdx.x == 0) {
       const unsigned long long st = cnt_st, ca = cnt_ca;
       s_calls_total += ca;
@@ -325,6 +329,7 @@ __global__ void __launch_bounds__(LEAN ? 256 : (TEAM ? 32 * TW : 256), LEAN ? 3 
           m = __ballot_sync(0xFFFFFFFFu, s < n && lane > l && f > cur);
         }
       }
+      __syncwarp();  // every lane read s_elit_fit / s_nimpr above before lane 0 rewrites them
       if (lane == 0) {
         s_nimpr = ni;
         if (hit && !s_stop) {

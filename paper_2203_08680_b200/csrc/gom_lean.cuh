@@ -55,7 +55,7 @@ __device__ __forceinline__ void gom_lean_unit(const GomArgs& a, uint32_t p, cons
                                               uint32_t generation, uint32_t* wsm, uint32_t lane, bool is_elit,
                                               int32_t esrc, uint32_t ever_cur, bool record, long long& acc,
                                               unsigned long long& dh1, unsigned long long& dh2, uint32_t& steps,
-                                              unsigned long long& calls) {
+                                              unsigned long long& calls, unsigned int* sib = nullptr) {
   constexpr uint32_t FULL = 0xFFFFFFFFu;
   const uint32_t Wp = a.Wp, n = a.n, lwp = 31u - __clz(Wp);
   const uint4 gm = pre.gm;
@@ -83,6 +83,13 @@ __device__ __forceinline__ void gom_lean_unit(const GomArgs& a, uint32_t p, cons
   }
   if (lane < f) zobrist(vj, zW[2 * lane], zW[2 * lane + 1]);
   __syncwarp();
+  // The Wp warps of this set (one per population word) each read ALL words
+  // of F's rows as the group-start donor pool, and each commits its own word.
+  // Arrive once this warp's copy is complete; commits wait for every sibling
+  // (below), so no sibling reads a word already committed.  The siblings
+  // walk the same unit sequence and are co-resident (persistent kernel), so
+  // the wait cannot deadlock.
+  if (sib != nullptr && lane == 0) atomicAdd(sib + p, 1u);
   // ---- every member's pattern on F: lane jv holds row jv, one transpose per word
   for (uint32_t wg = 0; wg < Wp; ++wg) {
     const uint32_t r = lane < f ? rowsW[lane * Wp + wg] : 0u;
@@ -186,6 +193,11 @@ __device__ __forceinline__ void gom_lean_unit(const GomArgs& a, uint32_t p, cons
   // ---- phases 3 + 4: accept (:194-214, exact comparator) and commit (:221-247)
   const bool accept = present && (delta > 0 || (delta == 0 && !is_elit));
   const uint32_t accw = __ballot_sync(FULL, accept);
+  if (sib != nullptr) {
+    if (lane == 0)
+      while (*(volatile unsigned int*)(sib + p) < Wp) __nanosleep(32);
+    __syncwarp();
+  }
   if (lane < f) {
     const uint32_t nw = (oldT & ~accw) | (xT & accw);
     if (nw != oldT) a.pop[(size_t)vj * Wp + w] = nw;

@@ -249,6 +249,8 @@ struct GenArgs {
   unsigned long long* dh;      // [3][2][n] Zobrist deltas
   unsigned long long* cnt;     // [3][2] steps, calls
   unsigned int* bar;           // grid barrier {arrivals, generation}
+  unsigned int* sib;           // LEAN, Wp > 1: [3][sib_stride] per-position sibling arrival counters
+  uint32_t sib_stride;         // largest colour group
 };
 
 // Per-call control values, passed as kernel parameters (captured at launch,

@@ -30,103 +30,66 @@
 
 namespace gomix_b200 {
 
-// ---- caching device allocator (internal.cuh) ---------------------------------
+// ---- device allocator (internal.cuh) -------------------------------------------
+// Stream-ordered allocation from each device's default memory pool, with a
+// release threshold so freed memory stays in the pool (cudaFree-free
+// rebuilds: IMS creates and drops populations, bench / tests rebuild
+// problems).  Allocations and frees go through one internal stream per
+// device; an allocation is complete before cached_malloc returns, so any
+// stream may use it.  Frees: callers synchronise the streams that used the
+// block first (engine and problem destructors do), which makes the
+// stream-ordered free safe.  The pool hands a freed block to the next
+// allocation on the same internal stream; nothing is cleared, exactly like
+// cudaMalloc.
 namespace {
-struct DeviceCache {
-  std::mutex mu;
-  std::map<std::pair<int, size_t>, std::vector<void*>> free_blocks;  // (device, rounded size)
-  std::unordered_map<void*, std::pair<int, size_t>> live;
-  size_t cached_bytes = 0;
-  static constexpr size_t kCap = 8ull << 30;
+constexpr uint64_t kPoolKeep = 8ull << 30;  // bytes the pool keeps reserved across frees
+struct DevicePool {
+  std::once_flag once;
+  cudaStream_t stream = nullptr;
 };
-DeviceCache& cache() {
-  static DeviceCache* c = new DeviceCache;  // never destroyed: frees may run during process exit
-  return *c;
+DevicePool& pool_of(int dev) {
+  static std::mutex mu;
+  static std::map<int, DevicePool*> pools;  // never destroyed: frees may run during process exit
+  std::lock_guard<std::mutex> lk(mu);
+  DevicePool*& p = pools[dev];
+  if (!p) p = new DevicePool;
+  return *p;
 }
-size_t round_block(size_t b) {
-  if (b >= (1u << 20)) return (b + (1u << 20) - 1) & ~((size_t)(1u << 20) - 1);
-  size_t r = 256;
-  while (r < b) r <<= 1;
-  return r;
+DevicePool& current_pool() {
+  int dev = 0;
+  GOMIX_CUDA(cudaGetDevice(&dev));
+  DevicePool& p = pool_of(dev);
+  std::call_once(p.once, [&] {
+    cudaMemPool_t mp = nullptr;
+    GOMIX_CUDA(cudaDeviceGetDefaultMemPool(&mp, dev));
+    uint64_t keep = kPoolKeep;
+    GOMIX_CUDA(cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &keep));
+    GOMIX_CUDA(cudaStreamCreateWithFlags(&p.stream, cudaStreamNonBlocking));
+  });
+  return p;
 }
 }  // namespace
 
-// The cache is opt-in (GOMIX_ALLOC_CACHE=1): with it, one stop-criteria
-// comparison test (tests/test_gen_kernel.py, budget stop inside a generation)
-// fails intermittently in full-suite runs — recycled block addresses, not
-// their contents or the missing implicit synchronisation (both ruled out) —
-// and the cause is not found yet.  Plain cudaMalloc / cudaFree by default.
-bool cache_disabled() {
-  static const bool off = std::getenv("GOMIX_ALLOC_CACHE") == nullptr;
-  return off;
-}
-
 void* cached_malloc(size_t bytes) {
-  if (cache_disabled()) {
-    void* p = nullptr;
-    GOMIX_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 1)));
-    return p;
-  }
-  // cudaMalloc / cudaFree synchronise the device implicitly and callers
-  // have come to rely on it (a stop-criteria test turned flaky without): keep
-  // that, minus the allocation itself
-  GOMIX_CUDA(cudaDeviceSynchronize());
-  int dev = 0;
-  GOMIX_CUDA(cudaGetDevice(&dev));
-  const size_t sz = round_block(std::max<size_t>(bytes, 1));
-  DeviceCache& c = cache();
-  void* reused = nullptr;
-  {
-    std::lock_guard<std::mutex> lk(c.mu);
-    auto it = c.free_blocks.find({dev, sz});
-    if (it != c.free_blocks.end() && !it->second.empty()) {
-      void* p = it->second.back();
-      it->second.pop_back();
-      c.cached_bytes -= sz;
-      c.live[p] = {dev, sz};
-      reused = p;
-    }
-  }
-  if (reused) return reused;
-  void* p = nullptr;
-  cudaError_t e = cudaMalloc(&p, sz);
-  if (e == cudaErrorMemoryAllocation) {  // give the cached blocks back and retry once
-    cudaGetLastError();
-    std::lock_guard<std::mutex> lk(c.mu);
-    for (auto& kv : c.free_blocks)
-      for (void* q : kv.second) cudaFree(q);
-    c.free_blocks.clear();
-    c.cached_bytes = 0;
-    e = cudaMalloc(&p, sz);
-  }
-  GOMIX_CUDA(e);
-  std::lock_guard<std::mutex> lk(c.mu);
-  c.live[p] = {dev, sz};
-  return p;
+  DevicePool& p = current_pool();
+  void* ptr = nullptr;
+  GOMIX_CUDA(cudaMallocAsync(&ptr, std::max<size_t>(bytes, 1), p.stream));
+  GOMIX_CUDA(cudaStreamSynchronize(p.stream));
+  return ptr;
 }
 
-void cached_free(void* p) {
-  if (!p) return;
-  if (cache_disabled()) {
-    cudaFree(p);
-    return;
-  }
-  cudaDeviceSynchronize();  // as cudaFree would
-  DeviceCache& c = cache();
-  std::lock_guard<std::mutex> lk(c.mu);
-  auto it = c.live.find(p);
-  if (it == c.live.end()) {
-    cudaFree(p);
-    return;
-  }
-  const auto key = it->second;
-  c.live.erase(it);
-  if (c.cached_bytes + key.second > DeviceCache::kCap) {
-    cudaFree(p);
-    return;
-  }
-  c.free_blocks[key].push_back(p);
-  c.cached_bytes += key.second;
+void cached_free(void* ptr) {
+  if (!ptr) return;
+  cudaPointerAttributes at{};
+  int dev = 0;
+  if (cudaPointerGetAttributes(&at, ptr) == cudaSuccess) dev = at.device;
+  cudaGetLastError();
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (dev != cur) cudaSetDevice(dev);
+  DevicePool& p = current_pool();
+  cudaFreeAsync(ptr, p.stream);
+  if (dev != cur) cudaSetDevice(cur);
 }
 
 void cached_free_all(std::vector<void*>& blocks) {
@@ -135,7 +98,8 @@ void cached_free_all(std::vector<void*>& blocks) {
 }
 
 Problem::~Problem() {
-  cudaDeviceSynchronize();  // engines' streams may still read the problem (cudaFree used to wait)
+  cudaSetDevice(device);
+  cudaDeviceSynchronize();  // engines' streams may still read the problem
   cached_free_all(allocations);
 }
 
@@ -288,6 +252,13 @@ constexpr uint64_t kWpSmemMax = 100000;
 constexpr int kJpBatches = 256;  // x 16 rounds before switching to the dataflow kernel
 constexpr uint32_t kWpUncoloured = 0xFFFFu;
 
+// Welsh-Powell as a dataflow: a vertex's warp spins (volatile loads) until
+// every lower-ranked neighbour has its colour, then writes its own.  The
+// volatile read / write pairs on the colour array are the synchronisation
+// itself: compute-sanitizer racecheck reports them as shared-memory hazards
+// (it does not model spin-wait handoffs); every colour is written once, and
+// the result equals the reference's sequential Welsh-Powell
+// (tests/test_gpu_parity.py colouring cases).
 template <bool SMEM>
 __global__ void wp_dataflow_kernel(const int64_t* off, const uint32_t* adj, const uint32_t* rank,
                                    const uint64_t* sorted_key, uint64_t m, int32_t* colour) {
