@@ -298,6 +298,7 @@ struct gomix_gpu_engine {
   int grid_cap = 1;
   int univ_planes = 0;     // > 0: Philox groups run the bit-sliced lane-per-set kernel
   bool univ_tt = false;    // ... its truth-table variant (degree <= 4 plan records)
+  uint32_t tt_chunks = 1;  // > 1: n > 128, rows processed in 4-word chunks (counted rows in `ones`)
   int univ_grid_cap = 1;
   // Sharded univariate runs on a variable-once FOS: a row changes only in its
   // own group, so its count of 1s over all ranks (the presence test) is
@@ -498,7 +499,12 @@ struct gomix_gpu_engine {
     // presence from the group-start row.
     if (P->univariate && P->i32 && !(flags & GOMIX_FLAG_RECORD_BATCH) && !(flags & GOMIX_FLAG_LANE_PER_SOLUTION)) {
       univ_planes = univ_sliced_planes(P->max_abs_row);
-      univ_tt = P->urec != nullptr && Wp <= 4 && !(flags & GOMIX_FLAG_NO_TRUTH_TABLE);
+      // rows wider than 4 words run in 4-word chunks, one per CTA; their
+      // presence test reads per-row counts of 1s taken at generation start,
+      // valid when every variable sits in one set (a row then changes only
+      // in its own group)
+      univ_tt = P->urec != nullptr && (Wp <= 4 || P->var_once) && !(flags & GOMIX_FLAG_NO_TRUTH_TABLE);
+      tt_chunks = univ_tt && Wp > 4 ? Wp / 4 : 1;
       if (univ_planes) univ_grid_cap = univ_sliced_max_blocks_per_sm(univ_planes, (int)Wp, univ_tt) * sms;
       if (univ_grid_cap < 1) univ_planes = 0;
     }
@@ -581,8 +587,9 @@ struct gomix_gpu_engine {
       rec_accept = dev_alloc<uint8_t>(allocs, max_group * n);
     }
     lite = R > 1 && P->univariate && P->var_once && mode == GOMIX_MODE_PHILOX;
+    if (tt_chunks > 1 && R > 1 && !lite) invalid("engine: internal: chunked rows need the sharded row counts");
+    if (lite || tt_chunks > 1) ones = dev_alloc<uint32_t>(allocs, nv);
     if (lite) {
-      ones = dev_alloc<uint32_t>(allocs, nv);
       ones_local = dev_alloc<uint32_t>(allocs, nv);
       if (!cfg.nccl_unique_id) ones_stage = dev_alloc<uint32_t>(allocs, (uint64_t)R * nv);
     }
@@ -677,6 +684,7 @@ struct gomix_gpu_engine {
     // pays the capture and instantiation.
     if (!graph_exec && graph_warm < kGraphAfter) {
       ++graph_warm;
+      count_rows(stream);
       OrderArgs o{ctl, d_order, (uint32_t)P->k, seed};
       launch_order(d_begin, o, stream);
       for (uint64_t slot = 0; slot < P->k; ++slot) launch_group(0, false, (int32_t)slot, stream);
@@ -687,9 +695,10 @@ struct gomix_gpu_engine {
       cudaStream_t cap = nullptr;
       GOMIX_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
       GOMIX_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+      const uint64_t saved = launches;
+      count_rows(cap);
       OrderArgs o{ctl, d_order, (uint32_t)P->k, seed};
       launch_order(d_begin, o, cap);
-      const uint64_t saved = launches;
       for (uint64_t slot = 0; slot < P->k; ++slot) launch_group(0, false, (int32_t)slot, cap);
       graph_launches = launches - saved + 1;
       launches = saved;
@@ -701,6 +710,15 @@ struct gomix_gpu_engine {
     }
     GOMIX_CUDA(cudaGraphLaunch(graph_exec, stream));
     launches += graph_launches;
+  }
+
+  // Chunked truth-table rows (n > 128): every row's count of 1s at
+  // generation start, the presence test of its set (the FOS is univariate and
+  // variable-once: a row changes only in its own group).
+  void count_rows(cudaStream_t st) {
+    if (tt_chunks <= 1 || R > 1) return;  // sharded runs count (and all-reduce) in run_generation_sharded
+    launch_count_ones(pop, P->nv, Wp, ones, st);
+    ++launches;
   }
 
   // Stage this call's stop criteria for the graph's begin kernel.  The pinned
@@ -827,7 +845,7 @@ struct gomix_gpu_engine {
     a.n = (uint32_t)n;
     a.Wp = Wp;
     a.pool = pool;
-    a.ones = lite ? ones : nullptr;
+    a.ones = (lite || tt_chunks > 1) ? ones : nullptr;
     a.nv = P->nv;
     a.R = R;
     a.rank = rank;
@@ -859,7 +877,9 @@ struct gomix_gpu_engine {
     }
     if (univ_planes && !with_tape) {
       const uint64_t per = (uint64_t)univ_sliced_sets_per_cta();
-      const int g = (int)std::max<uint64_t>(1, std::min<uint64_t>((G + per - 1) / per, (uint64_t)univ_grid_cap));
+      // chunked rows: tt_chunks CTAs per set range, one per chunk
+      const uint64_t slots = std::max<uint64_t>(1, (uint64_t)univ_grid_cap / tt_chunks);
+      const int g = (int)(tt_chunks * std::max<uint64_t>(1, std::min<uint64_t>((G + per - 1) / per, slots)));
       a.epi = epi_args(group, (uint32_t)G, (uint32_t)g);
       // graph path, groups after the first: programmatic dependent launch
       // (truth-table kernel only: it waits on griddepcontrol before reading
@@ -1175,6 +1195,7 @@ struct gomix_gpu_engine {
     }
     begin_call(stop);
     if (fi_on) fi_snapshot();
+    count_rows(stream);
     std::vector<uint64_t> order;
     rng.permutation(order, P->k);  // engine_parallel.hpp:291
     for (uint64_t gi : order) {
@@ -1206,6 +1227,7 @@ struct gomix_gpu_engine {
     } else if (flags & GOMIX_FLAG_TIME_KERNELS) {
       begin_call(nullptr);
       if (fi_on) fi_snapshot();
+      count_rows(stream);
       std::vector<uint64_t> order;
       rng.permutation(order, P->k);
       for (uint64_t gi : order) launch_group(gi, false);
@@ -1263,6 +1285,7 @@ struct gomix_gpu_engine {
     } else {
       with_tape = false;
     }
+    if (!with_tape) count_rows(stream);
     launch_group(group, with_tape);
     read_ctl();
     fill_stats(out);

@@ -900,8 +900,35 @@ void launch_ims_offer(const SnapArgs& a, ImsBestDev* b, const uint32_t* bits, in
   GOMIX_CUDA(cudaGetLastError());
 }
 
+// Rows of Wp >= 4 words: Wp / 4 lanes per row, one 16-byte load each
+// (a warp reads 512 contiguous bytes), counts summed across the row's lanes.
+__global__ void count_ones_wide_kernel(const uint32_t* pop, uint64_t nv, uint32_t Wp, uint32_t* ones) {
+  const uint32_t L = Wp >> 2;  // lanes per row (1 .. 32)
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint32_t rows_per_warp = 32u / min(L, 32u);
+  for (uint64_t base = warp * rows_per_warp; base < nv; base += nwarps * rows_per_warp) {
+    uint32_t c = 0;
+    for (uint32_t part = 0; part < max(1u, L / 32u); ++part) {  // rows wider than 128 words: several loads
+      const uint64_t v = base + lane / min(L, 32u);
+      const uint32_t q = (lane % min(L, 32u)) + part * 32u;
+      if (v < nv) {
+        const uint4 x = __ldg(reinterpret_cast<const uint4*>(pop + v * Wp) + q);
+        c += __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
+      }
+    }
+    for (uint32_t o = min(L, 32u) >> 1; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+    const uint64_t v = base + lane / min(L, 32u);
+    if (lane % min(L, 32u) == 0 && v < nv) ones[v] = c;
+  }
+}
+
 void launch_count_ones(const uint32_t* pop, uint64_t nv, uint32_t Wp, uint32_t* ones, cudaStream_t s) {
-  count_ones_kernel<<<grid_for(nv, 256, 148 * 8), 256, 0, s>>>(pop, nv, Wp, ones);
+  if (Wp >= 4)
+    count_ones_wide_kernel<<<148 * 8, 256, 0, s>>>(pop, nv, Wp, ones);
+  else
+    count_ones_kernel<<<grid_for(nv, 256, 148 * 8), 256, 0, s>>>(pop, nv, Wp, ones);
   GOMIX_CUDA(cudaGetLastError());
 }
 

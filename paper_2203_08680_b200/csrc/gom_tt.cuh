@@ -110,23 +110,53 @@ __device__ __forceinline__ TtNext tt_fetch(const uint4* urec, const ulonglong2* 
   return r;
 }
 
+// Which part of the population a CTA works on.  Rows of up to WC words
+// (n <= 32 WC): every CTA takes whole rows.  Wider rows (n > 128): the row is
+// cut into chunks of WC words and CTA i takes chunk i % chunks of the sets
+// assigned to CTA slot i / chunks; a CTA's per-solution accumulators then
+// cover only its chunk's 32 WC solutions.
+struct TtPart {
+  uint32_t chunk;   // this CTA's chunk of every row
+  uint32_t cta;     // this CTA's slot among the CTAs of its chunk
+  uint32_t ctas;    // CTAs per chunk (gridDim.x / chunks)
+  uint32_t cbase;   // first solution of the chunk
+  uint32_t n_chunk; // solutions in the chunk
+};
+
+template <int WC>
+__device__ __forceinline__ TtPart tt_part(const GomArgs& a) {
+  TtPart t;
+  const uint32_t chunks = a.Wp / (uint32_t)WC;
+  t.chunk = blockIdx.x % chunks;
+  t.cta = blockIdx.x / chunks;
+  t.ctas = gridDim.x / chunks;
+  t.cbase = t.chunk * (uint32_t)WC * 32u;
+  t.n_chunk = min((uint32_t)WC * 32u, a.n - min(a.n, t.cbase));
+  return t;
+}
+
 // The batches of one colour group handled by this warp: warp-major batch
-// order (bt = warp * gridDim.x + blockIdx.x, then + gridDim.x * kUnivWarps),
-// `nx` = the first batch's records (fetched by the caller).  Commits the
-// accepted flips in place, records the elitist's old bits copy-on-write,
-// accumulates fitness deltas into s_dfit (per solution, shared atomics) and
-// hash deltas into sh.wh[warp] (this warp's own slice), counts steps/calls.
-// s_elit: group-start "parent == elitist" mask per word.
+// order (bt = warp * ctas + cta, then + ctas * kUnivWarps), `nx` = the first
+// batch's records (fetched by the caller).  Commits the accepted flips in
+// place, records the elitist's old bits copy-on-write, accumulates fitness
+// deltas into s_dfit (per chunk solution, shared atomics) and hash deltas
+// into sh.wh[warp] (this warp's own slice), counts steps/calls.  s_elit:
+// group-start "parent == elitist" mask per word of the chunk.  Chunked rows
+// take the presence test from a.ones (every row's count of 1s at group
+// start, counted per generation: a univariate, variable-once FOS changes a
+// row only in its own group).
 template <int B, int WC>
-__device__ __forceinline__ void tt_batches(const GomArgs& a, const uint4* urec, const ulonglong2* ukey, uint32_t G,
-                                           TtNext nx, const uint32_t* s_elit, long long* s_dfit, TtShared& sh,
-                                           int32_t esrc, uint32_t ever_cur, uint32_t lane, uint32_t warp,
-                                           unsigned long long& steps, unsigned long long& calls) {
-  constexpr uint32_t Wp = (uint32_t)WC;
+__device__ __forceinline__ void tt_batches(const GomArgs& a, const TtPart& part, const uint4* urec,
+                                           const ulonglong2* ukey, uint32_t G, TtNext nx, const uint32_t* s_elit,
+                                           long long* s_dfit, TtShared& sh, int32_t esrc, uint32_t ever_cur,
+                                           uint32_t lane, uint32_t warp, unsigned long long& steps,
+                                           unsigned long long& calls) {
+  const uint32_t Wp = a.Wp;  // row stride (words)
+  const uint32_t cw = part.chunk * (uint32_t)WC;  // first word of the chunk
   const uint32_t n = a.n;
   const uint32_t batches = (G + 31u) / 32u;
-  const uint32_t bstride = gridDim.x * kUnivWarps;
-  for (uint32_t bt = warp * gridDim.x + blockIdx.x; bt < batches; bt += bstride) {
+  const uint32_t bstride = part.ctas * kUnivWarps;
+  for (uint32_t bt = warp * part.ctas + part.cta; bt < batches; bt += bstride) {
     const uint32_t p = bt * 32u + lane;
     const bool live = p < G;
     const uint4 ra = nx.ra, rc = nx.rc;
@@ -142,9 +172,9 @@ __device__ __forceinline__ void tt_batches(const GomArgs& a, const uint4* urec, 
       for (int t = 0; t < 4; ++t) nb[t][j] = 0;
     }
     if (live) {
-      load_row<WC>(a.pop + (size_t)v * Wp, x);
+      load_row<WC>(a.pop + (size_t)v * Wp + cw, x);
 #pragma unroll
-      for (int t = 0; t < 4; ++t) load_row<WC>(a.pop + (size_t)u[t] * Wp, nb[t]);
+      for (int t = 0; t < 4; ++t) load_row<WC>(a.pop + (size_t)u[t] * Wp + cw, nb[t]);
     }
     int32_t w[4];
     w[0] = w16(ra.z, 0);
@@ -174,8 +204,8 @@ __device__ __forceinline__ void tt_batches(const GomArgs& a, const uint4* urec, 
     }
     const bool present = live && ones > 0u && ones < a.n_global;
     if (present) {
-      steps += n;
-      calls += (unsigned long long)n * deg;
+      steps += part.n_chunk;
+      calls += (unsigned long long)part.n_chunk * deg;
     }
     const uint32_t pmask = present ? 0xFFFFFFFFu : 0u;
     // ---- b words (edge "uncut-gain" bits), then accept via the LE table
@@ -204,7 +234,7 @@ __device__ __forceinline__ void tt_batches(const GomArgs& a, const uint4* urec, 
           }
           ac &= keep;
         }
-        acc[j] = ac & pmask & valid_mask((uint32_t)j, n);
+        acc[j] = ac & pmask & valid_mask(cw + (uint32_t)j, n);
         any |= acc[j] != 0u;
       }
     }
@@ -213,8 +243,8 @@ __device__ __forceinline__ void tt_batches(const GomArgs& a, const uint4* urec, 
       uint32_t nw[WC];
 #pragma unroll
       for (int j = 0; j < WC; ++j) nw[j] = x[j] ^ acc[j];
-      store_row<WC>(a.pop + (size_t)v * Wp, nw);
-      if (esrc >= 0) {
+      store_row<WC>(a.pop + (size_t)v * Wp + cw, nw);
+      if (esrc >= 0) {  // (esrc is relative to the chunk: -1 when the elitist lives elsewhere)
         const uint32_t ew = (uint32_t)esrc >> 5, eb = (uint32_t)esrc & 31u;
         uint32_t aw = 0, xw = 0;
 #pragma unroll

@@ -382,8 +382,9 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_tt_kernel(const G
   probe(a.exp_flags, 40);
 
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  constexpr uint32_t Wp = (uint32_t)WC;
+  constexpr uint32_t Wp = (uint32_t)WC;  // words of this CTA's chunk (whole rows when a.Wp == WC)
   const uint32_t n = a.n;
+  const TtPart part = tt_part<WC>(a);
   uint32_t G = a.G;
   const uint4* urec = a.urec;
   const ulonglong2* ukey = a.ukey;
@@ -400,7 +401,7 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_tt_kernel(const G
   // the plan records of the warp's first batch (static data, like the group
   // order read above, which the generation's begin kernel wrote before the
   // previous launch started): in flight before the dependency wait
-  const TtNext first = tt_fetch(urec, ukey, G, (warp * gridDim.x + blockIdx.x) * 32u + lane);
+  const TtNext first = tt_fetch(urec, ukey, G, (warp * part.ctas + part.cta) * 32u + lane);
   // programmatic dependent launch (graph path): everything below reads what
   // the previous group's launch wrote (population, control block, hashes)
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -409,14 +410,16 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_tt_kernel(const G
   const unsigned long long eh1 = a.ctl->eh1, eh2 = a.ctl->eh2;
   const int32_t esrc_g = a.ctl->elit_src;
   const uint32_t ever_cur = a.ctl->elit_ver;
-  const uint32_t sw = warp * 32u + lane;
+  const uint32_t sw = part.cbase + warp * 32u + lane;
   unsigned long long hs1 = 0, hs2 = 0;
   if (warp < Wp && sw < n) {
     hs1 = a.h1[sw];
     hs2 = a.h2[sw];
   }
   if (stopped) return;
-  const int32_t esrc = (esrc_g >= 0 && (uint32_t)esrc_g / n == a.rank) ? (int32_t)((uint32_t)esrc_g % n) : -1;
+  // the elitist's column relative to this CTA's chunk (-1: not here)
+  int32_t esrc = (esrc_g >= 0 && (uint32_t)esrc_g / n == a.rank) ? (int32_t)((uint32_t)esrc_g % n) : -1;
+  esrc = (esrc >= (int32_t)part.cbase && esrc < (int32_t)(part.cbase + Wp * 32u)) ? esrc - (int32_t)part.cbase : -1;
   if (warp < Wp) {  // group-start "parent == elitist" (engine_parallel.hpp:202) as word masks
     const uint32_t m = __ballot_sync(0xFFFFFFFFu, sw < n && hs1 == eh1 && hs2 == eh2);
     if (lane == 0) s_elit[warp] = m;
@@ -433,7 +436,7 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_tt_kernel(const G
   __syncthreads();
   probe(a.exp_flags, 41);
   unsigned long long steps = 0, calls = 0;
-  tt_batches<B, WC>(a, urec, ukey, G, first, s_elit, s_dfit, sh, esrc, ever_cur, lane, warp, steps, calls);
+  tt_batches<B, WC>(a, part, urec, ukey, G, first, s_elit, s_dfit, sh, esrc, ever_cur, lane, warp, steps, calls);
 
   probe(a.exp_flags, 42);
   // the next group's launch may start its prologue (it waits for this grid's
@@ -452,7 +455,7 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_tt_kernel(const G
     }
   }
   __syncthreads();
-  for (uint32_t s = threadIdx.x; s < n && s < Wp * 32u; s += blockDim.x) {
+  for (uint32_t s = threadIdx.x; s < part.n_chunk; s += blockDim.x) {
     unsigned long long x1 = 0, x2 = 0;
 #pragma unroll
     for (int q = 0; q < kUnivWarps; ++q) {
@@ -461,10 +464,11 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_tt_kernel(const G
     }
     s_dh1[s] = x1;
     s_dh2[s] = x2;
-    if (s_dfit[s]) atomicAdd(&a.dfit[s], (double)s_dfit[s]);
+    const uint32_t g = part.cbase + s;
+    if (s_dfit[s]) atomicAdd(&a.dfit[g], (double)s_dfit[s]);
     if (x1 | x2) {
-      atomicXor(&a.dh1[s], x1);
-      atomicXor(&a.dh2[s], x2);
+      atomicXor(&a.dh1[g], x1);
+      atomicXor(&a.dh2[g], x2);
     }
   }
   if (threadIdx.x == 0) {
@@ -495,7 +499,7 @@ namespace {
 template <int WC, bool MULTI>
 void* univ_kernel_wc(int planes, bool tt) {
 #define GOMIX_UNIV_CASE(b) \
-  case b: return tt && !MULTI ? (void*)gom_univ_tt_kernel<b, WC> : (void*)gom_univ_sliced_kernel<b, WC, MULTI>;
+  case b: return tt ? (void*)gom_univ_tt_kernel<b, WC> : (void*)gom_univ_sliced_kernel<b, WC, MULTI>;
   switch (planes) {
     GOMIX_UNIV_CASE(4)
     GOMIX_UNIV_CASE(6)
@@ -511,6 +515,13 @@ void* univ_kernel_wc(int planes, bool tt) {
 int words_per_chunk(int wp) { return wp >= 4 ? 4 : wp; }
 
 void* univ_kernel(int planes, int wp, bool tt) {
+  if (tt) {  // truth tables: 1, 2 or 4 words per row, wider rows in 4-word chunks (one chunk per CTA)
+    switch (words_per_chunk(wp)) {
+      case 1: return univ_kernel_wc<1, false>(planes, true);
+      case 2: return univ_kernel_wc<2, false>(planes, true);
+      case 4: return univ_kernel_wc<4, false>(planes, true);
+    }
+  }
   // 12/16-plane counters for 4-word chunks do not fit the register budget
   // (T alone is 48/64 registers): 2-word passes instead
   if (planes >= 12 && wp >= 4 && !(tt && wp == 4)) return univ_kernel_wc<2, true>(planes, false);
@@ -523,7 +534,8 @@ void* univ_kernel(int planes, int wp, bool tt) {
   throw GomixError(GOMIX_E_INVALID, "univariate sliced kernel: unsupported row width");
 }
 
-size_t univ_smem(int wp) { return (size_t)wp * 32 * 24 + (size_t)wp * 4; }
+// dynamic shared memory of the adder kernel (the truth-table kernel's is static)
+size_t univ_smem(int wp, bool tt) { return tt ? 0 : (size_t)wp * 32 * 24 + (size_t)wp * 4; }
 }  // namespace
 
 int univ_sliced_planes(uint64_t max_abs_row_sum) {
@@ -539,9 +551,9 @@ int univ_sliced_sets_per_cta() { return kUnivWarps * 32; }
 
 int univ_sliced_max_blocks_per_sm(int planes, int wp, bool tt) {
   void* fn = univ_kernel(planes, wp, tt);
-  GOMIX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)univ_smem(wp)));
+  GOMIX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)univ_smem(wp, tt)));
   int blocks = 0;
-  GOMIX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, kUnivWarps * 32, univ_smem(wp)));
+  GOMIX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, kUnivWarps * 32, univ_smem(wp, tt)));
   return blocks;
 }
 
@@ -549,7 +561,7 @@ void launch_univ_sliced(const GomArgs& a, int planes, int wp, bool tt, int grid,
   void* fn = univ_kernel(planes, wp, tt);
   void* args[] = {(void*)&a};
   if (!pdl) {
-    GOMIX_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kUnivWarps * 32), args, univ_smem(wp), s));
+    GOMIX_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kUnivWarps * 32), args, univ_smem(wp, tt), s));
     return;
   }
   // programmatic dependent launch: may begin while the previous kernel on the
@@ -557,7 +569,7 @@ void launch_univ_sliced(const GomArgs& a, int planes, int wp, bool tt, int grid,
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kUnivWarps * 32);
-  cfg.dynamicSmemBytes = univ_smem(wp);
+  cfg.dynamicSmemBytes = univ_smem(wp, tt);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

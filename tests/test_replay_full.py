@@ -11,9 +11,9 @@ evaluator calls, group counters and traces kept whole.
 In replay mode the engine walks the reference's RngStream on the host
 (init bits, `permutation(k)`, every lazy Fisher-Yates donor scan,
 engine_serial.hpp:30-46, rng.hpp:21-59) and launches the SAME kernel the
-Philox production path launches (gom_univ_tt_kernel at C3/C1,
-gom_univ_sliced_kernel at n > 128): univariate steps are donor-independent,
-only presence and the group order matter.  Integer weights: bit-exact.
+Philox production path launches (gom_univ_tt_kernel; rows above 4 words in
+4-word chunks, one per CTA): univariate steps are donor-independent, only
+presence and the group order matter.  Integer weights: bit-exact.
 """
 import numpy as np
 import pytest
@@ -29,7 +29,7 @@ EXPECT = {
     "c1_long": "gom_univ_tt_kernel",      # C1: n = 32, one word per row
     "c3_pm": "gom_univ_tt_kernel",        # signed weights, n = 100 (ragged last word)
     "c5_n16": "gom_univ_tt_kernel",       # C5 smallest population
-    "c5_n1024": "gom_univ_sliced_kernel",  # C5, 32 words per row (MULTI passes)
+    "c5_n1024": "gom_univ_tt_kernel",     # C5, 32 words per row: 8 chunks of 4 words
     "c3_full": "gom_univ_tt_kernel",      # C3 as benchmarked: 10^6 vertices, n = 128
 }
 
@@ -88,8 +88,9 @@ def test_replay_full_size_matches_reference(name):
     assert E.kernel_name() == EXPECT[name]
 
 
-@pytest.mark.parametrize("name", ["c1_long", "c3_pm", "c5_n16"])
-@pytest.mark.parametrize("variant", [dict(truth_table=False), dict(lane_per_solution=True)])
+@pytest.mark.parametrize("name,variant", [(c, v) for c in ("c1_long", "c3_pm", "c5_n16")
+                                          for v in (dict(truth_table=False), dict(lane_per_solution=True))]
+                         + [("c5_n1024", dict(truth_table=False))])
 def test_replay_full_size_other_kernels(name, variant):
     """The adder kernel (gom_univ_sliced_kernel) and the lane-per-solution
     kernel (gom_group_kernel, donor tape) give the same bit-exact replay."""

@@ -159,6 +159,13 @@ def _triple(P, n, seed):
     ("torus_c1", 32, 30),       # C1: tiny, clones of the elitist are common
     ("deg4", 128, 25),          # degrees 0..4, padding slots
     ("deg4_big", 96, 20),       # |w| up to 8000: 16 planes
+    # n > 128: rows in 4-word chunks, one chunk per CTA, presence from the
+    # per-generation row counts
+    ("torus_pos", 256, 20),     # 2 chunks
+    ("torus_pm", 1000, 12),     # 8 chunks, last one partial (1000 = 7 x 128 + 104)
+    ("torus_c1", 4096, 8),      # 32 chunks: the largest population
+    ("deg4", 520, 10),          # padding slots, ragged last chunk
+    ("deg4_big", 384, 8),       # 16 planes, 3 chunks
 ])
 def test_truth_table_equals_adder_and_lane_per_solution(inst_kind, n, gens):
     inst = {
@@ -206,6 +213,22 @@ def test_truth_table_full_size_c3():
     b = G.GpuParallelEngine(P, 128, 1, mode="philox", truth_table=False)
     assert a.kernel_name() == "gom_univ_tt_kernel"
     for _ in range(30):
+        a.run_generation_async()
+        b.run_generation_async()
+    a.synchronize()
+    b.synchronize()
+    _same(inst, a, b)
+
+
+def test_truth_table_full_size_c5_large_population():
+    """C5 at the top of its sweep (316 x 316 torus, n = 4096: 32 chunks per
+    row): the chunked truth-table kernel agrees with the adder kernel."""
+    inst = G.generate_torus(316, 316, ("int", 1, 10), 1)
+    P = G.GpuProblem(inst, G.univariate_fos(inst.num_vertices))
+    a = G.GpuParallelEngine(P, 4096, 1, mode="philox")
+    b = G.GpuParallelEngine(P, 4096, 1, mode="philox", truth_table=False)
+    assert a.kernel_name() == "gom_univ_tt_kernel" and b.kernel_name() == "gom_univ_sliced_kernel"
+    for _ in range(6):
         a.run_generation_async()
         b.run_generation_async()
     a.synchronize()
