@@ -31,6 +31,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+
 #include "gom_common.cuh"
 #include "gom_tt.cuh"
 
@@ -371,8 +373,8 @@ __global__ void build_univ_records_kernel(const uint32_t* gvars, const int32_t* 
   key[p] = make_ulonglong2(z1, z2);
 }
 
-template <int B, int WC>
-__global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_tt_kernel(const GomArgs a) {
+template <int B, int WC, int MINB = 3>
+__global__ void __launch_bounds__(kUnivWarps * 32, MINB) gom_univ_tt_kernel(const GomArgs a) {
   __shared__ __align__(16) TtShared sh;
   __shared__ long long s_dfit[WC * 32];
   __shared__ unsigned long long s_dh1[WC * 32], s_dh2[WC * 32];
@@ -496,10 +498,22 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_tt_kernel(const G
 // launchers
 // ---------------------------------------------------------------------------
 namespace {
+// CTAs per SM the truth-table kernel is register-capped for (GOMIX_TT_OCC=4:
+// 64 registers, for A/B measurements; default 3: 80 registers)
+int tt_occupancy() {
+  static const int occ = [] {
+    const char* e = std::getenv("GOMIX_TT_OCC");
+    return (e && std::atoi(e) == 4) ? 4 : 3;
+  }();
+  return occ;
+}
+
 template <int WC, bool MULTI>
 void* univ_kernel_wc(int planes, bool tt) {
-#define GOMIX_UNIV_CASE(b) \
-  case b: return tt ? (void*)gom_univ_tt_kernel<b, WC> : (void*)gom_univ_sliced_kernel<b, WC, MULTI>;
+#define GOMIX_UNIV_CASE(b)                                                                            \
+  case b:                                                                                             \
+    return tt ? (tt_occupancy() == 4 ? (void*)gom_univ_tt_kernel<b, WC, 4> : (void*)gom_univ_tt_kernel<b, WC, 3>) \
+              : (void*)gom_univ_sliced_kernel<b, WC, MULTI>;
   switch (planes) {
     GOMIX_UNIV_CASE(4)
     GOMIX_UNIV_CASE(6)

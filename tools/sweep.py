@@ -25,11 +25,19 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def device_rate(G, P, n, gens=20, warm=3, seed=1):
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        return 6650.0
+
+
+def device_rate(G, P, n, gens=20, warm=3, seed=1, **kw):
     import torch
 
     s = torch.cuda.Stream()
-    E = G.GpuParallelEngine(P, n, seed, mode="philox", stream=s.cuda_stream)
+    E = G.GpuParallelEngine(P, n, seed, mode="philox", stream=s.cuda_stream, **kw)
     for _ in range(warm):
         E.run_generation_async()
     E.synchronize()
@@ -70,14 +78,20 @@ def c5(G, ref_points=(16, 64, 256)):
     inst = G.generate_torus(316, 316, ("int", 1, 10), 1)
     P = G.GpuProblem(inst, G.univariate_fos(inst.num_vertices))
     rows = []
+    peak = hbm_peak()
     for n in (16, 32, 64, 128, 256, 512, 1024, 2048, 4096):
         r = device_rate(G, P, n, gens=20 if n <= 1024 else 8)
+        # B_step = 0.875 + 60 / n bytes for a degree-4 torus vertex
+        r["bytes_per_step"] = 0.875 + 60.0 / n
+        r["hbm_frac"] = r["steps_per_s"] * r["bytes_per_step"] / 1e9 / peak
+        if n > 128:
+            r["adder_kernel_steps_per_s"] = device_rate(G, P, n, gens=8, truth_table=False)["steps_per_s"]
         rows.append(r)
         print(json.dumps(r), flush=True)
     cfg = dict(CONFIGS["c5"])
     ref = []
     workers = os.cpu_count() or 1
-    if os.path.exists(os.path.join(ROOT, "oracle", "_ref", "ref_driver")):
+    if ref_points and os.path.exists(os.path.join(ROOT, "oracle", "_ref", "ref_driver")):
         for n in ref_points:
             out = run_reference(cfg, n, 2, workers, timeout=900)
             secs = sum(g["seconds"] for g in out["gens"])
@@ -93,6 +107,7 @@ def main():
     ap.add_argument("--c4", action="store_true")
     ap.add_argument("--c5", action="store_true")
     ap.add_argument("--out-dir", default="gpurun_out")
+    ap.add_argument("--no-ref", action="store_true", help="skip the reference CPU points")
     a = ap.parse_args()
     import paper_2203_08680_b200 as G
 
@@ -100,7 +115,8 @@ def main():
     if a.c4 or not (a.c4 or a.c5):
         json.dump(c4(G), open(os.path.join(a.out_dir, "sweep_c4.json"), "w"), indent=1)
     if a.c5 or not (a.c4 or a.c5):
-        json.dump(c5(G), open(os.path.join(a.out_dir, "sweep_c5.json"), "w"), indent=1)
+        json.dump(c5(G, () if a.no_ref else (16, 64, 256)), open(os.path.join(a.out_dir, "sweep_c5.json"), "w"),
+                  indent=1)
 
 
 if __name__ == "__main__":
