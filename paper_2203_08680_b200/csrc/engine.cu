@@ -203,6 +203,7 @@ std::unique_ptr<Problem> create_problem(const gomix_maxcut* inst, const gomix_fo
   // degree <= 4, int16 weights)
   if (P->univariate && P->i32 && P->max_fp <= 4 && maxw < 32768.0 && univ_sliced_planes(P->max_abs_row) > 0)
     build_univ_records(*P);
+  if (P->univariate) build_univ_plan(*P);  // {v, row} records + keys of every position (gom_univ_f64.cu)
   GOMIX_CUDA(cudaDeviceSynchronize());  // engines read the problem from their own (non-blocking) streams
   mark("device");
   if (P->univariate) {
@@ -299,6 +300,8 @@ struct gomix_gpu_engine {
   int univ_planes = 0;     // > 0: Philox groups run the bit-sliced lane-per-set kernel
   bool univ_tt = false;    // ... its truth-table variant (degree <= 4 plan records)
   uint32_t tt_chunks = 1;  // > 1: n > 128, rows processed in 4-word chunks (counted rows in `ones`)
+  bool univ_f64 = false;   // univariate, non-int32 weights, Philox: gom_univ_f64_kernel
+  int f64_grid_cap = 1;
   int univ_grid_cap = 1;
   // Sharded univariate runs on a variable-once FOS: a row changes only in its
   // own group, so its count of 1s over all ranks (the presence test) is
@@ -342,8 +345,8 @@ struct gomix_gpu_engine {
   uint32_t* elit = nullptr;
   DevCtl* ctl = nullptr;
   DevCtl* h_ctl = nullptr;  // pinned
-  BeginArgs* d_begin = nullptr;  // per-call criteria read by the graph's begin kernel
-  BeginArgs* h_begin = nullptr;  // pinned staging of d_begin
+  BeginArgs* d_begin = nullptr;  // per-call criteria read by the graph's begin kernel: the device
+  BeginArgs* h_begin = nullptr;  // view of h_begin, mapped pinned host memory read in place
   static constexpr uint64_t kImprInline = 64;  // improvements copied back with every read_ctl
   static constexpr size_t kCtlBytes = (sizeof(DevCtl) + 63) / 64 * 64;  // control block, then the log
   ImprRec* h_impr = nullptr;                   // pinned [kImprInline], right after *h_ctl
@@ -508,6 +511,15 @@ struct gomix_gpu_engine {
       if (univ_planes) univ_grid_cap = univ_sliced_max_blocks_per_sm(univ_planes, (int)Wp, univ_tt) * sms;
       if (univ_grid_cap < 1) univ_planes = 0;
     }
+    // float weights on a univariate FOS (BASELINE C4): one warp per set with
+    // its record / weights staged (gom_univ_f64.cu); the lane-per-solution
+    // group kernel stays the A/B reference (GOMIX_FLAG_LANE_PER_SOLUTION)
+    if (P->univariate && !P->i32 && P->uvr && mode == GOMIX_MODE_PHILOX && R == 1 && epi_mode != 2 && !record &&
+        Wp <= 4 && P->max_fp <= (uint64_t)univ_f64_max_degree() && !(flags & GOMIX_FLAG_LANE_PER_SOLUTION)) {
+      f64_grid_cap = univ_f64_max_blocks_per_sm((int)Wp) * sms;
+      univ_f64 = f64_grid_cap >= 1;
+      grid_cap = std::max(grid_cap, f64_grid_cap);  // float partials are sized by grid_cap below
+    }
     for (uint64_t c = 0; c < P->k; ++c)
       max_group = std::max(max_group, P->group_off[c + 1] - P->group_off[c]);
     if (mode == GOMIX_MODE_PHILOX && P->i32 && !P->univariate && R == 1 && n <= kGenMaxN && P->k <= kGenMaxK &&
@@ -595,8 +607,9 @@ struct gomix_gpu_engine {
     }
     GOMIX_CUDA(cudaMallocHost(&h_ctl, kCtlBytes + kImprInline * sizeof(ImprRec)));
     h_impr = reinterpret_cast<ImprRec*>(reinterpret_cast<char*>(h_ctl) + kCtlBytes);
-    GOMIX_CUDA(cudaMallocHost(&h_begin, sizeof(BeginArgs)));
-    d_begin = dev_alloc<BeginArgs>(allocs, 1);
+    GOMIX_CUDA(cudaHostAlloc(&h_begin, sizeof(BeginArgs), cudaHostAllocMapped));
+    GOMIX_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_begin), h_begin, 0));
+    *h_begin = make_begin(nullptr);
     std::memset(h_ctl, 0, sizeof(DevCtl));
     h_ctl->elit_src = -1;
     h_ctl->exact = P->exact;
@@ -726,8 +739,14 @@ struct gomix_gpu_engine {
   // pending (sync calls wait first; async calls always stage "no criteria").
   void stage_criteria(const gomix_stop_criteria* stop, bool sync_first) {
     if (sync_first) GOMIX_CUDA(cudaStreamSynchronize(stream));
-    *h_begin = make_begin(stop);
-    GOMIX_CUDA(cudaMemcpyAsync(d_begin, h_begin, sizeof(BeginArgs), cudaMemcpyHostToDevice, stream));
+    // the begin kernel reads the criteria in place over the bus: no copy to
+    // queue.  Async calls stage "no criteria" every time, so a generation
+    // still queued reads the same values (the generation number is the
+    // device's own counter, begin_generation_kernel)
+    BeginArgs b = make_begin(stop);
+    if (!sync_first) b.gen = 0;  // (unused by the graph kernels; keeps queued reads byte-identical)
+    *h_begin = b;
+    std::atomic_thread_fence(std::memory_order_release);
   }
 
   void read_ctl() {
@@ -820,6 +839,7 @@ struct gomix_gpu_engine {
     a.gvars = P->gvars ? P->gvars + g0 : nullptr;
     a.urec = P->urec ? P->urec + 2 * g0 : nullptr;
     a.ukey = P->ukey ? P->ukey + g0 : nullptr;
+    a.uvr = P->uvr ? P->uvr + g0 : nullptr;
     a.gmeta = P->gmeta ? P->gmeta + g0 : nullptr;
     a.wbits = P->wbits;
     a.G = (uint32_t)G;
@@ -875,7 +895,12 @@ struct gomix_gpu_engine {
       e1 = take_event();
       GOMIX_CUDA(cudaEventRecord(e0, st));
     }
-    if (univ_planes && !with_tape) {
+    if (univ_f64 && !with_tape) {
+      const uint64_t per = (uint64_t)univ_f64_sets_per_cta();
+      const int g = (int)std::max<uint64_t>(1, std::min<uint64_t>((G + per - 1) / per, (uint64_t)f64_grid_cap));
+      a.epi = epi_args(group, (uint32_t)G, (uint32_t)g);
+      launch_univ_f64(a, (int)Wp, g, st);
+    } else if (univ_planes && !with_tape) {
       const uint64_t per = (uint64_t)univ_sliced_sets_per_cta();
       // chunked rows: tt_chunks CTAs per set range, one per chunk
       const uint64_t slots = std::max<uint64_t>(1, (uint64_t)univ_grid_cap / tt_chunks);
@@ -1843,6 +1868,7 @@ int gomix_gpu_set_timing(gomix_gpu_engine* e, int32_t enable) {
 
 const char* gomix_gpu_engine_kernel_name(const gomix_gpu_engine* e) {
   if (!e) return "";
+  if (e->univ_f64) return "gom_univ_f64_kernel";
   return e->univ_planes ? (e->univ_tt ? "gom_univ_tt_kernel" : "gom_univ_sliced_kernel") : e->gen_ok ? "gom_generation_kernel" : "gom_group_kernel";
 }
 

@@ -19,6 +19,7 @@
 
 #include "gom_common.cuh"
 #include "gom_general.cuh"
+#include "gom_tail.cuh"
 
 namespace gomix_b200 {
 
@@ -450,115 +451,7 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
     }
   }
 
-  // ---- per-CTA reductions: counters, fitness deltas, elitist distances ----
-  __syncthreads();
-  __shared__ unsigned long long s_steps, s_calls;
-  __shared__ int s_last;
-  if (threadIdx.x == 0) {
-    s_steps = 0;
-    s_calls = 0;
-  }
-  __syncthreads();
-  {
-    const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, steps);
-    unsigned long long wc = calls;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) wc += __shfl_xor_sync(0xFFFFFFFFu, wc, o);
-    if (lane == 0 && (ws | wc)) {
-      atomicAdd(&s_steps, (unsigned long long)ws);
-      atomicAdd(&s_calls, wc);
-    }
-  }
-  const bool float_parts = a.part != nullptr;
-  if (teams_per_cta > 1) {
-    // several teams per CTA: combine them in fixed order (deterministic)
-    double* sacc = reinterpret_cast<double*>(smem);
-    unsigned long long* sh1 = reinterpret_cast<unsigned long long*>(sacc + (size_t)teams_per_cta * Wp * 32u);
-    unsigned long long* sh2 = sh1 + (size_t)teams_per_cta * Wp * 32u;
-#pragma unroll
-    for (int j = 0; j < WPT; ++j) {
-      const uint32_t s = (wit + tw * (uint32_t)j) * 32u + lane;
-      sacc[(size_t)team * Wp * 32u + s] = (double)acc[j];
-      sh1[(size_t)team * Wp * 32u + s] = dh1[j];
-      sh2[(size_t)team * Wp * 32u + s] = dh2[j];
-    }
-    __syncthreads();
-    for (uint32_t s = threadIdx.x; s < Wp * 32u; s += blockDim.x) {
-      double v = 0.0;
-      unsigned long long x1 = 0, x2 = 0;
-      for (uint32_t t = 0; t < teams_per_cta; ++t) {
-        v += sacc[(size_t)t * Wp * 32u + s];
-        x1 ^= sh1[(size_t)t * Wp * 32u + s];
-        x2 ^= sh2[(size_t)t * Wp * 32u + s];
-      }
-      if (s < n) {
-        if (float_parts)
-          a.part[(size_t)blockIdx.x * n + s] = v;
-        else if (a.dfit && v != 0.0)
-          atomicAdd(&a.dfit[s], v);
-        if (x1 | x2) {
-          atomicXor(&a.dh1[s], x1);
-          atomicXor(&a.dh2[s], x2);
-        }
-      }
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < WPT; ++j) {
-      const uint32_t s = (wit + tw * (uint32_t)j) * 32u + lane;
-      if (s < n) {
-        if (float_parts)
-          a.part[(size_t)blockIdx.x * n + s] = (double)acc[j];
-        else if (a.dfit && acc[j] != 0)
-          atomicAdd(&a.dfit[s], (double)acc[j]);
-        if (dh1[j] | dh2[j]) {
-          atomicXor(&a.dh1[s], dh1[j]);
-          atomicXor(&a.dh2[s], dh2[j]);
-        }
-      }
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0 && (s_steps | s_calls)) {
-    atomicAdd(&a.ctl->grp_steps, s_steps);
-    atomicAdd(&a.ctl->grp_calls, s_calls);
-  }
-  uint32_t parties = gridDim.x;
-  if (float_parts && a.part1 && gridDim.x > kPartBlock) {
-    // two-level deterministic sum of the float partials: the last CTA of each
-    // block of kPartBlock CTAs adds that block's rows in CTA order into one
-    // level-1 row, so the epilogue adds ceil(grid / kPartBlock) rows instead
-    // of one per CTA (the serial tail of float launches)
-    const uint32_t blk = blockIdx.x / kPartBlock;
-    const uint32_t b0 = blk * kPartBlock, members = min(kPartBlock, gridDim.x - b0);
-    if (threadIdx.x == 0) {
-      __threadfence();
-      s_last = atomicAdd(&a.part_cnt[blk], 1u) == members - 1;
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    for (uint32_t s = threadIdx.x; s < n; s += blockDim.x) {
-      double sum = 0.0;
-      for (uint32_t b = b0; b < b0 + members; ++b) sum += __ldcg(a.part + (size_t)b * n + s);
-      a.part1[(size_t)blk * n + s] = sum;
-    }
-    if (threadIdx.x == 0) a.part_cnt[blk] = 0;
-    parties = (gridDim.x + kPartBlock - 1) / kPartBlock;
-    epi.part = a.part1;
-    epi.nparts = parties;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    // last-party ticket: everything above is visible to the last one
-    __threadfence();
-    s_last = atomicAdd(&a.ctl->done, 1u) == parties - 1;
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  epilogue_body(epi);
-  if (threadIdx.x == 0) a.ctl->done = 0;
+  gom_group_tail<WPT, Acc>(a, epi, smem, teams_per_cta, team, wit, tw, lane, acc, dh1, dh2, steps, calls);
 }
 
 __global__ void begin_call_kernel(const BeginArgs b) {

@@ -96,7 +96,8 @@ struct Problem {
   uint32_t* gvars = nullptr;
   uint4* gmeta = nullptr;
   uint4* urec = nullptr;       // univariate, degree <= 4, |w| < 2^15: truth-table plan records (2 per position)
-  ulonglong2* ukey = nullptr;  // ... and the Zobrist key of each position's variable
+  ulonglong2* ukey = nullptr;  // ... and the Zobrist key of each position's variable (every univariate FOS)
+  uint4* uvr = nullptr;        // univariate FOS: {v, row start, row end, 0} per group position
   uint32_t wbits = 1;
   int64_t* fp_off = nullptr;
   FpEntry* fp = nullptr;
@@ -164,6 +165,7 @@ struct GomArgs {
   const uint4* gmeta;     // general FOS: {set id, vars offset, footprint offset, f << 24 | footprint}
   const uint4* urec;       // truth-table plan records of this group (gom_univ_tt_kernel)
   const ulonglong2* ukey;  // Zobrist keys of this group's variables
+  const uint4* uvr;        // univariate plan records of this group (gom_univ_f64_kernel)
   uint32_t wbits;         // bit-planes of max |w| (integer path)
   uint32_t G;             // |G|
   uint32_t* pop;
@@ -349,6 +351,12 @@ int univ_sliced_max_blocks_per_sm(int planes, int wp, bool tt);
 void launch_univ_sliced(const GomArgs& a, int planes, int wp, bool tt, int grid, cudaStream_t s,
                         bool pdl = false);
 void build_univ_records(Problem& P);
+// float univariate kernel (gom_univ_f64.cu)
+void build_univ_plan(Problem& P);
+int univ_f64_max_blocks_per_sm(int wp);
+int univ_f64_sets_per_cta();
+int univ_f64_max_degree();
+void launch_univ_f64(const GomArgs& a, int wp, int grid, cudaStream_t s);
 void build_csr_device(Problem& P, bool exact, int32_t* d_eid, uint64_t* max_abs_row);  // problem.cu
 void launch_fi_snapshot(const FiArgs& a, cudaStream_t s);
 void launch_fi_flags(const FiArgs& a, bool given, cudaStream_t s);

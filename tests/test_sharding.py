@@ -75,6 +75,9 @@ def _single(P, n, seed, crit=None):
     ("uni", (20, 10), 96, 2, 5),      # 48 per shard: padded words, shard boundary inside a word
     ("neigh", (9, 9), 96, 3, 4),
     ("uni", (64, 64), 256, 8, 3),
+    ("uni", (1000, 1000), 128, 8, 2),  # BASELINE C3 strong-scaled to 8 GPUs: 16 members per shard
+    ("uni", (1000, 1000), 128, 2, 2),  # ... to 2 GPUs: 64 per shard
+    ("uni", (100, 100), 1024, 2, 3),   # 512 per shard: truth-table rows in 4 chunks per shard
 ])
 def test_sharded_equals_single_engine(kind, shape, n, R, gens):
     inst = G.generate_torus(shape[0], shape[1], ("int", -3, 9), 5)
