@@ -267,6 +267,10 @@ def bench_ours(args):
     if world > 1:
         import torch.distributed as dist
 
+        # the communicators' set-up lines (ranks, devices, NVLS / P2P
+        # transports) on stderr, so a run shows how many ranks took part
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:

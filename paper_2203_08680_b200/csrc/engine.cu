@@ -96,7 +96,7 @@ std::unique_ptr<Problem> create_problem(const gomix_maxcut* inst, const gomix_fo
   if (q >= (1ull << 30)) invalid("maxcut: at most 2^30-1 edges");
   if (q && (!inst->edge_u || !inst->edge_v || !inst->edge_w)) invalid("maxcut: missing edge arrays");
   bool exact = true;
-  double maxw = 0.0;
+  double maxw = 0.0, sum_abs_w = 0.0;
   for (uint64_t i = 0; i < q; ++i) {
     const uint32_t u = inst->edge_u[i], v = inst->edge_v[i];
     const double w = inst->edge_w[i];
@@ -109,6 +109,7 @@ std::unique_ptr<Problem> create_problem(const gomix_maxcut* inst, const gomix_fo
     }
     if (w != std::floor(w) || std::fabs(w) > 9e15) exact = false;
     maxw = std::max(maxw, std::fabs(w));
+    sum_abs_w += std::fabs(w);
   }
   if (m == 0) invalid("fos: needs at least one linkage set");
   if (!fos->set_offset || !fos->set_vars) invalid("fos: missing arrays");
@@ -119,6 +120,7 @@ std::unique_ptr<Problem> create_problem(const gomix_maxcut* inst, const gomix_fo
   P->q = q;
   P->m = m;
   P->exact = exact;
+  P->sum_abs_w = sum_abs_w;
   P->h_set_off.assign(fos->set_offset, fos->set_offset + m + 1);
   const uint64_t entries = P->h_set_off[m];
   P->h_set_vars.assign(fos->set_vars, fos->set_vars + entries);
@@ -333,10 +335,8 @@ struct gomix_gpu_engine {
   unsigned long long* h2_all = nullptr;
   unsigned long long* rank_cnt = nullptr;  // [R][steps, calls]
   double* fit = nullptr;
-  double* dfit = nullptr;
-  double* part = nullptr;
-  double* part1 = nullptr;
-  unsigned int* part_cnt = nullptr;
+  long long* dfit = nullptr;  // fixed-point fitness deltas of the current group
+  double fix_scale = 1.0;     // 1 (integer weights) or 2^S (float weights), see setup
   unsigned long long* h1 = nullptr;  // per-solution Zobrist hashes
   unsigned long long* h2 = nullptr;
   unsigned long long* dh1 = nullptr;
@@ -477,6 +477,15 @@ struct gomix_gpu_engine {
     smem = std::max(stage, red);
     if (smem > 227 * 1024) invalid("engine: set size x population too large for shared-memory staging");
     record = (flags & GOMIX_FLAG_RECORD_BATCH) != 0;
+    // Float fitness deltas are summed as fixed-point integers: each delta is
+    // rounded to a multiple of 2^-S before any addition, so the sums are
+    // order-free (deterministic on any grid) and exact in int64 as long as a
+    // group's total stays below 2^62: |sum| <= 2 * sum|w| bounds it, which
+    // fixes S.  Resolution 2^-S per accepted delta (C4: S = 44, 6e-14).
+    if (!P->exact) {
+      const int e = (int)std::ceil(std::log2(2.0 * P->sum_abs_w + 1.0));
+      fix_scale = std::ldexp(1.0, std::max(0, std::min(60, 62 - e)));
+    }
     const bool ordered = !P->exact && (mode == GOMIX_MODE_REPLAY || (flags & GOMIX_FLAG_ORDERED_FLOAT));
     epi_mode = P->exact ? 0 : (ordered ? 2 : 1);
 
@@ -518,7 +527,6 @@ struct gomix_gpu_engine {
         Wp <= 4 && P->max_fp <= (uint64_t)univ_f64_max_degree() && !(flags & GOMIX_FLAG_LANE_PER_SOLUTION)) {
       f64_grid_cap = univ_f64_max_blocks_per_sm((int)Wp) * sms;
       univ_f64 = f64_grid_cap >= 1;
-      grid_cap = std::max(grid_cap, f64_grid_cap);  // float partials are sized by grid_cap below
     }
     for (uint64_t c = 0; c < P->k; ++c)
       max_group = std::max(max_group, P->group_off[c + 1] - P->group_off[c]);
@@ -561,7 +569,7 @@ struct gomix_gpu_engine {
     fit = fit_all + (uint64_t)rank * n;
     h1 = h1_all + (uint64_t)rank * n;
     h2 = h2_all + (uint64_t)rank * n;
-    dfit = dev_alloc<double>(allocs, n);
+    dfit = dev_alloc<long long>(allocs, n);
     dh1 = dev_alloc<unsigned long long>(allocs, n);
     dh2 = dev_alloc<unsigned long long>(allocs, n);
     ever = dev_alloc<uint32_t>(allocs, nv);
@@ -576,13 +584,6 @@ struct gomix_gpu_engine {
     gcalls = dev_alloc<unsigned long long>(allocs, P->k);
     fi_on = (flags & GOMIX_FLAG_FORCED_IMPROVEMENT) != 0;
     if (fi_on && R > 1) invalid("engine: forced improvement needs a single-GPU engine");
-    if (epi_mode == 1) {
-      part = dev_alloc<double>(allocs, (size_t)grid_cap * n);
-      const uint64_t nblk = ((uint64_t)grid_cap + kPartBlock - 1) / kPartBlock;
-      part1 = dev_alloc<double>(allocs, nblk * n);
-      part_cnt = dev_alloc<unsigned int>(allocs, nblk);
-      GOMIX_CUDA(cudaMemset(part_cnt, 0, nblk * sizeof(unsigned int)));
-    }
     d_order = dev_alloc<uint32_t>(allocs, P->k);
     d_groups = dev_alloc<GroupDesc>(allocs, P->k);
     {
@@ -796,8 +797,8 @@ struct gomix_gpu_engine {
   EpiArgs epi_args(uint64_t group, uint32_t G, uint32_t nparts) const {
     EpiArgs e;
     e.fit = fit;
-    e.part = part;
     e.dfit = dfit;
+    e.fix_inv = 1.0 / fix_scale;
     e.h1 = h1;
     e.h2 = h2;
     e.dh1 = dh1;
@@ -849,10 +850,8 @@ struct gomix_gpu_engine {
     a.h2 = h2;
     a.ever = ever;
     a.elit = elit;
-    a.dfit = epi_mode == 0 ? dfit : nullptr;
-    a.part = epi_mode == 1 ? part : nullptr;
-    a.part1 = epi_mode == 1 ? part1 : nullptr;
-    a.part_cnt = part_cnt;
+    a.dfit = dfit;
+    a.fix_scale = fix_scale;
     a.dh1 = dh1;
     a.dh2 = dh2;
     a.ctl = ctl;
@@ -899,7 +898,7 @@ struct gomix_gpu_engine {
       const uint64_t per = (uint64_t)univ_f64_sets_per_cta();
       const int g = (int)std::max<uint64_t>(1, std::min<uint64_t>((G + per - 1) / per, (uint64_t)f64_grid_cap));
       a.epi = epi_args(group, (uint32_t)G, (uint32_t)g);
-      launch_univ_f64(a, (int)Wp, g, st);
+      launch_univ_f64(a, (int)Wp, g, st, slot > 0);  // graph path, groups after the first: PDL
     } else if (univ_planes && !with_tape) {
       const uint64_t per = (uint64_t)univ_sliced_sets_per_cta();
       // chunked rows: tt_chunks CTAs per set range, one per chunk

@@ -259,7 +259,7 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
   extern __shared__ __align__(16) uint32_t smem[];
   if (*(volatile int32_t*)&a.ctl->stop) return;
 
-  using Acc = typename std::conditional<I32, long long, double>::type;
+  using Acc = long long;  // fixed-point fitness deltas (GomArgs::fix_scale)
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   // TEAM: the CTA is one team of tw warps; otherwise every warp is a team
   // holding all Wp == WPT words of its solutions (compile-time index math)
@@ -418,7 +418,7 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
             accept = exact ? (delta > 0.0 || (delta == 0.0 && !is_elit[j]))
                            : (cmp_better(false, cand, pf) || (cmp_equal(false, cand, pf) && !is_elit[j]));
           }
-          if (accept) acc[j] += (Acc)delta;
+          if (accept) acc[j] += __double2ll_rn(delta * a.fix_scale);
         }
         nw[j] = pw[j] ^ __ballot_sync(0xFFFFFFFFu, accept);  // accepted members flip v
         accb |= accept ? (1u << j) : 0u;
@@ -451,7 +451,7 @@ __global__ void __launch_bounds__((UNIV && WPT <= 4) ? 256 : 512, (UNIV && WPT <
     }
   }
 
-  gom_group_tail<WPT, Acc>(a, epi, smem, teams_per_cta, team, wit, tw, lane, acc, dh1, dh2, steps, calls);
+  gom_group_tail<WPT>(a, epi, smem, teams_per_cta, team, wit, tw, lane, acc, dh1, dh2, steps, calls);
 }
 
 __global__ void begin_call_kernel(const BeginArgs b) {
@@ -536,7 +536,7 @@ __global__ void init_epilogue_kernel(const EpiArgs a) {
   for (uint32_t s = threadIdx.x; s < a.n; s += blockDim.x) {
     a.dh1[s] = 0;
     a.dh2[s] = 0;
-    a.dfit[s] = 0.0;
+    a.dfit[s] = 0;
   }
 }
 

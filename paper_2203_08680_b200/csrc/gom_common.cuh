@@ -189,49 +189,23 @@ static __device__ void note_improvement(const EpiArgs& a, double f) {
     request_stop(c, GOMIX_STOP_TARGET);
 }
 
-// Commit this rank's group deltas: fitness (exact atomics / float partials /
-// reference-ordered recorded deltas) and Zobrist hashes of its n solutions.
+// Commit this rank's group deltas: fitness (fixed-point sums of the accepted
+// deltas / reference-ordered recorded deltas) and Zobrist hashes of its n
+// solutions.  Fixed point: every delta is rounded to a multiple of
+// 1 / fix_scale (1 for integer weights: exact) before any summation, so the
+// integer sums do not depend on which thread or CTA added what — the
+// float path is deterministic for any grid, within 1e-9 relative of the
+// reference's sums (north star).
 static __device__ void commit_local(const EpiArgs& a, double* s_fit, unsigned long long* s_h = nullptr) {
   const uint32_t n = a.n;
-  if (a.mode == 1) {
-    // float partials, one per CTA of the launch: thread t adds the partials
-    // b = t / n, t / n + T, ... of solution s = t % n (coalesced across
-    // threads) into 8 independent running sums, so the loads pipeline; the
-    // sums and then the threads of a solution are combined in a fixed order —
-    // deterministic for a given grid.
-    const uint32_t T = blockDim.x >= n ? blockDim.x / n : 1u;  // threads per solution
-    __shared__ double s_part[512];  // GOM launches use at most 512 threads per CTA
-    for (uint32_t s0 = 0; s0 < n; s0 += blockDim.x / T) {
-      const uint32_t s = s0 + threadIdx.x % (blockDim.x / T), tb = threadIdx.x / (blockDim.x / T);
-      double acc8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      if (s < n && tb < T) {
-        uint32_t b = tb;
-        for (; b + 7 * T < a.nparts; b += 8 * T) {
-#pragma unroll
-          for (int k = 0; k < 8; ++k) acc8[k] += a.part[(size_t)(b + k * T) * n + s];
-        }
-        for (int k = 0; b < a.nparts; b += T, ++k) acc8[k & 7] += a.part[(size_t)b * n + s];
-      }
-      s_part[threadIdx.x] = ((acc8[0] + acc8[1]) + (acc8[2] + acc8[3])) + ((acc8[4] + acc8[5]) + (acc8[6] + acc8[7]));
-      __syncthreads();
-      if (tb == 0 && s < n) {
-        double sum = 0.0;
-        for (uint32_t q = 0; q < T; ++q) sum += s_part[q * (blockDim.x / T) + threadIdx.x % (blockDim.x / T)];
-        const_cast<double*>(a.part)[s] = sum;  // slot of partial 0 (read above by this solution's threads)
-      }
-      __syncthreads();
-    }
-  }
   for (uint32_t s = threadIdx.x; s < n; s += blockDim.x) {
     double f = a.fit[s];
     if (a.mode == 2) {
       for (uint32_t p = 0; p < a.G; ++p)
         if (a.rec_accept[(size_t)p * n + s]) f += a.rec_delta[(size_t)p * n + s];
-    } else if (a.mode == 1) {
-      f += a.part[s];
     } else {
-      f += a.dfit[s];
-      a.dfit[s] = 0.0;
+      f += (double)a.dfit[s] * a.fix_inv;
+      a.dfit[s] = 0;
     }
     a.fit[s] = f;
     if (s_fit && s < kEpiSmemFit) s_fit[s] = f;

@@ -15,9 +15,9 @@ __device__ __forceinline__ void gom_general_set(
     const GomArgs& a, uint32_t p, const uint4* gmeta, uint32_t generation, uint32_t* stage, uint32_t lane,
     uint32_t tw, uint32_t wit, uint32_t tid_team, uint32_t team_threads, uint32_t teams_per_cta, uint32_t team,
     bool exact, bool replay, bool record, const bool (&is_elit)[WPT], const double (&pfit)[WPT], int32_t esrc,
-    uint32_t ever_cur, typename std::conditional<I32, long long, double>::type (&acc)[WPT],
+    uint32_t ever_cur, long long (&acc)[WPT],
     unsigned long long (&dh1)[WPT], unsigned long long (&dh2)[WPT], uint32_t& steps, unsigned long long& calls) {
-  using Acc = typename std::conditional<I32, long long, double>::type;
+  using Acc = long long;  // fixed-point fitness deltas (GomArgs::fix_scale)
   const uint32_t Wp = a.Wp, n = a.n;
   // ---- general set F (|F| <= 64).  Shared memory per team holds the F
   // rows at group start (the donor pool, engine_parallel.hpp:100-103),
@@ -245,7 +245,7 @@ __device__ __forceinline__ void gom_general_set(
     for (uint32_t jv = lane; jv < f; jv += 32)
       newF[jv * Wp + w] = (rowsF[jv * RW + own + w] & ~acc_w) | (newD[jv * Wp + w] & acc_w);
     if (accept) {
-      acc[j] += I32 ? (Acc)di[j] : (Acc)delta;
+      acc[j] += I32 ? (Acc)di[j] : __double2ll_rn(delta * a.fix_scale);
       uint64_t changed = (dm[j] ^ pm[j]) & fm;
       const bool cap = (int32_t)(a.rank * n + s) == esrc;
       while (changed) {

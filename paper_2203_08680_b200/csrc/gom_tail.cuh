@@ -1,8 +1,7 @@
 // gom_tail.cuh — the end of a per-group GOM launch, shared by the
 // lane-per-solution kernels (gom_group_kernel in gom.cu, gom_univ_f64_kernel
 // in gom_univ_f64.cu): per-CTA counters, the CTA's per-solution fitness and
-// Zobrist deltas (teams combined in fixed order; float partials written per
-// CTA and summed in two deterministic levels), then the group epilogue
+// Zobrist deltas (teams combined, then fixed-point atomics), then the group epilogue
 // (engine_parallel.hpp:221-247, :305-310) in the last CTA to finish.
 #pragma once
 
@@ -12,10 +11,10 @@ namespace gomix_b200 {
 
 // acc / dh1 / dh2: this thread's deltas of its solutions (wit + tw * j) * 32 + lane;
 // smem: at least teams_per_cta * Wp * 32 * 24 bytes when teams_per_cta > 1.
-template <int WPT, typename Acc>
-__device__ __forceinline__ void gom_group_tail(const GomArgs& a, EpiArgs epi, uint32_t* smem, uint32_t teams_per_cta,
-                                               uint32_t team, uint32_t wit, uint32_t tw, uint32_t lane,
-                                               const Acc (&acc)[WPT], const unsigned long long (&dh1)[WPT],
+template <int WPT>
+__device__ __forceinline__ void gom_group_tail(const GomArgs& a, const EpiArgs& epi, uint32_t* smem,
+                                               uint32_t teams_per_cta, uint32_t team, uint32_t wit, uint32_t tw,
+                                               uint32_t lane, const long long (&acc)[WPT], const unsigned long long (&dh1)[WPT],
                                                const unsigned long long (&dh2)[WPT], uint32_t steps,
                                                unsigned long long calls) {
   const uint32_t Wp = a.Wp, n = a.n;
@@ -38,22 +37,24 @@ __device__ __forceinline__ void gom_group_tail(const GomArgs& a, EpiArgs epi, ui
       atomicAdd(&s_calls, wc);
     }
   }
-  const bool float_parts = a.part != nullptr;
+  // fitness deltas are fixed-point integers (every delta rounded before any
+  // sum, GomArgs::fix_scale): order-free atomics, deterministic for any grid
+  unsigned long long* dfit = reinterpret_cast<unsigned long long*>(a.dfit);
   if (teams_per_cta > 1) {
-    // several teams per CTA: combine them in fixed order (deterministic)
-    double* sacc = reinterpret_cast<double*>(smem);
+    // several teams per CTA: combine them first (one global atomic per solution)
+    long long* sacc = reinterpret_cast<long long*>(smem);
     unsigned long long* sh1 = reinterpret_cast<unsigned long long*>(sacc + (size_t)teams_per_cta * Wp * 32u);
     unsigned long long* sh2 = sh1 + (size_t)teams_per_cta * Wp * 32u;
 #pragma unroll
     for (int j = 0; j < WPT; ++j) {
       const uint32_t s = (wit + tw * (uint32_t)j) * 32u + lane;
-      sacc[(size_t)team * Wp * 32u + s] = (double)acc[j];
+      sacc[(size_t)team * Wp * 32u + s] = acc[j];
       sh1[(size_t)team * Wp * 32u + s] = dh1[j];
       sh2[(size_t)team * Wp * 32u + s] = dh2[j];
     }
     __syncthreads();
     for (uint32_t s = threadIdx.x; s < Wp * 32u; s += blockDim.x) {
-      double v = 0.0;
+      long long v = 0;
       unsigned long long x1 = 0, x2 = 0;
       for (uint32_t t = 0; t < teams_per_cta; ++t) {
         v += sacc[(size_t)t * Wp * 32u + s];
@@ -61,10 +62,7 @@ __device__ __forceinline__ void gom_group_tail(const GomArgs& a, EpiArgs epi, ui
         x2 ^= sh2[(size_t)t * Wp * 32u + s];
       }
       if (s < n) {
-        if (float_parts)
-          a.part[(size_t)blockIdx.x * n + s] = v;
-        else if (a.dfit && v != 0.0)
-          atomicAdd(&a.dfit[s], v);
+        if (v) atomicAdd(dfit + s, (unsigned long long)v);
         if (x1 | x2) {
           atomicXor(&a.dh1[s], x1);
           atomicXor(&a.dh2[s], x2);
@@ -76,10 +74,7 @@ __device__ __forceinline__ void gom_group_tail(const GomArgs& a, EpiArgs epi, ui
     for (int j = 0; j < WPT; ++j) {
       const uint32_t s = (wit + tw * (uint32_t)j) * 32u + lane;
       if (s < n) {
-        if (float_parts)
-          a.part[(size_t)blockIdx.x * n + s] = (double)acc[j];
-        else if (a.dfit && acc[j] != 0)
-          atomicAdd(&a.dfit[s], (double)acc[j]);
+        if (acc[j]) atomicAdd(dfit + s, (unsigned long long)acc[j]);
         if (dh1[j] | dh2[j]) {
           atomicXor(&a.dh1[s], dh1[j]);
           atomicXor(&a.dh2[s], dh2[j]);
@@ -92,32 +87,7 @@ __device__ __forceinline__ void gom_group_tail(const GomArgs& a, EpiArgs epi, ui
     atomicAdd(&a.ctl->grp_steps, s_steps);
     atomicAdd(&a.ctl->grp_calls, s_calls);
   }
-  uint32_t parties = gridDim.x;
-  if (float_parts && a.part1 && gridDim.x > kPartBlock) {
-    // two-level deterministic sum of the float partials: the last CTA of each
-    // block of kPartBlock CTAs adds that block's rows in CTA order into one
-    // level-1 row, so the epilogue adds ceil(grid / kPartBlock) rows instead
-    // of one per CTA (the serial tail of float launches)
-    const uint32_t blk = blockIdx.x / kPartBlock;
-    const uint32_t b0 = blk * kPartBlock, members = min(kPartBlock, gridDim.x - b0);
-    if (threadIdx.x == 0) {
-      __threadfence();
-      s_last = atomicAdd(&a.part_cnt[blk], 1u) == members - 1;
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    for (uint32_t s = threadIdx.x; s < n; s += blockDim.x) {
-      double sum = 0.0;
-      for (uint32_t b = b0; b < b0 + members; ++b) sum += __ldcg(a.part + (size_t)b * n + s);
-      a.part1[(size_t)blk * n + s] = sum;
-    }
-    if (threadIdx.x == 0) a.part_cnt[blk] = 0;
-    parties = (gridDim.x + kPartBlock - 1) / kPartBlock;
-    epi.part = a.part1;
-    epi.nparts = parties;
-    __syncthreads();
-  }
+  const uint32_t parties = gridDim.x;
   if (threadIdx.x == 0) {
     // last-party ticket: everything above is visible to the last one
     __threadfence();

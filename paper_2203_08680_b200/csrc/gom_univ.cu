@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(kUnivWarps * 32, 3) gom_univ_sliced_kernel(con
   }
   __syncthreads();
   for (uint32_t s = threadIdx.x; s < n && s < Wp * 32u; s += blockDim.x) {
-    if (s_dfit[s]) atomicAdd(&a.dfit[s], (double)s_dfit[s]);
+    if (s_dfit[s]) atomicAdd(reinterpret_cast<unsigned long long*>(&a.dfit[s]), (unsigned long long)s_dfit[s]);
     if (s_dh1[s] | s_dh2[s]) {
       atomicXor(&a.dh1[s], s_dh1[s]);
       atomicXor(&a.dh2[s], s_dh2[s]);
@@ -467,7 +467,7 @@ __global__ void __launch_bounds__(kUnivWarps * 32, MINB) gom_univ_tt_kernel(cons
     s_dh1[s] = x1;
     s_dh2[s] = x2;
     const uint32_t g = part.cbase + s;
-    if (s_dfit[s]) atomicAdd(&a.dfit[g], (double)s_dfit[s]);
+    if (s_dfit[s]) atomicAdd(reinterpret_cast<unsigned long long*>(&a.dfit[g]), (unsigned long long)s_dfit[s]);
     if (x1 | x2) {
       atomicXor(&a.dh1[g], x1);
       atomicXor(&a.dh2[g], x2);

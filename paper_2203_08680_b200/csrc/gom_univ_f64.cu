@@ -11,10 +11,9 @@
 // Σnew over the uncut ones, every term added, zeros included, exactly as the
 // reference's reduce_by_key does; accept iff better(parent + Δ, parent) or
 // equal and the parent is not the group-start elitist (graybox.hpp:22-35,
-// relative 1e-9); accepted pairs flip v.  Decisions and populations are
-// therefore bit-identical to gom_group_kernel; fitness commits through the
-// same deterministic per-CTA partials (within 1e-9 relative of the
-// reference's position-order sums, north star).
+// relative 1e-9); accepted pairs flip v.  Decisions, populations and the
+// fixed-point fitness sums are therefore bit-identical to gom_group_kernel
+// (within 1e-9 relative of the reference's position-order sums, north star).
 //
 // Why a second kernel: the group kernel walks set -> row_ptr -> CSR ->
 // neighbour rows as a dependent chain per set and broadcasts every edge with
@@ -25,6 +24,8 @@
 // neighbour rows are read once per set as 16-byte loads.
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <cstdlib>
 
 #include "gom_common.cuh"
 #include "gom_tail.cuh"
@@ -49,14 +50,50 @@ __device__ __forceinline__ void load_row_f64(const uint32_t* row, uint32_t (&x)[
   }
 }
 
+// One set's loads that do not depend on this launch's writes to the
+// population rows of its own group: the plan record, v's row (written only
+// by this warp, after it is read), v's key and lane t's edge.
 template <int WPT>
-__global__ void __launch_bounds__(kF64Warps * 32, 3) gom_univ_f64_kernel(const GomArgs a) {
+struct F64Next {
+  uint4 rec;
+  uint32_t x[WPT];
+  ulonglong2 key;
+  uint32_t u;
+  double w;
+};
+
+template <int WPT>
+__device__ __forceinline__ F64Next<WPT> f64_fetch(const GomArgs& a, const uint4* uvr, const ulonglong2* ukey,
+                                                  uint32_t G, uint32_t p, uint32_t lane) {
+  F64Next<WPT> r;
+#pragma unroll
+  for (int j = 0; j < WPT; ++j) r.x[j] = 0;
+  r.u = 0;
+  r.w = 0.0;
+  r.key = make_ulonglong2(0ull, 0ull);
+  r.rec = make_uint4(0, 0, 0, 0);
+  if (p >= G) return r;
+  r.rec = __ldg(uvr + p);
+  r.key = __ldg(ukey + p);
+  load_row_f64<WPT>(a.pop + (size_t)r.rec.x * WPT, r.x);
+  const int32_t e = (int32_t)r.rec.y + (int32_t)lane;
+  if (e < (int32_t)r.rec.z) {
+    r.u = (uint32_t)__ldg(a.col + e);
+    r.w = __ldg(a.w + e);
+  }
+  return r;
+}
+
+template <int WPT, int MINB>
+__global__ void __launch_bounds__(kF64Warps * 32, MINB) gom_univ_f64_kernel(const GomArgs a) {
   __shared__ __align__(16) uint32_t s_tail[kF64Warps * WPT * 32 * 6];  // gom_group_tail's team combine
   __shared__ double s_w[kF64Warps][kF64MaxDeg];
   __shared__ uint32_t s_nb[kF64Warps][kF64MaxDeg][WPT];
-  if (*(volatile int32_t*)&a.ctl->stop) return;
-
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  // programmatic dependent launch (graph path): everything below reads what
+  // the previous group's launch wrote (population, control block, hashes)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (*(volatile int32_t*)&a.ctl->stop) return;
   const uint32_t n = a.n;
   constexpr uint32_t Wp = (uint32_t)WPT;
   uint32_t G = a.G;
@@ -79,14 +116,15 @@ __global__ void __launch_bounds__(kF64Warps * 32, 3) gom_univ_f64_kernel(const G
   const uint32_t ever_cur = a.ctl->elit_ver;
   const bool exact = a.exact != 0;
   bool is_elit[WPT];
-  double pfit[WPT], acc[WPT];
+  double pfit[WPT];
+  long long acc[WPT];  // fixed-point fitness deltas (GomArgs::fix_scale)
   unsigned long long dh1[WPT], dh2[WPT];
 #pragma unroll
   for (int j = 0; j < WPT; ++j) {
     const uint32_t s = (uint32_t)j * 32u + lane;
     is_elit[j] = s < n && a.h1[s] == eh1 && a.h2[s] == eh2;
     pfit[j] = s < n ? a.fit[s] : 0.0;
-    acc[j] = 0.0;
+    acc[j] = 0;
     dh1[j] = 0;
     dh2[j] = 0;
   }
@@ -95,50 +133,43 @@ __global__ void __launch_bounds__(kF64Warps * 32, 3) gom_univ_f64_kernel(const G
 
   const uint32_t stride = gridDim.x * kF64Warps;
   uint32_t p = blockIdx.x * kF64Warps + warp;
-  uint4 rec = p < G ? __ldg(uvr + p) : make_uint4(0, 0, 0, 0);
+  // Software pipeline over this warp's sets (every set has at most
+  // kF64MaxDeg edges: one edge per lane).  While set p computes, the loads
+  // of set p + stride that do not depend on the population in flight:
+  // its record, then v's row, key, and lane t's edge (neighbour id, weight);
+  // only the neighbour rows are loaded at the top of an iteration.
+  F64Next<WPT> cur = f64_fetch<WPT>(a, uvr, ukey, G, p, lane);
   for (; p < G; p += stride) {
-    // the next set's plan record: in flight while this one computes
-    const uint32_t pn = p + stride;
-    const uint4 rec_next = pn < G ? __ldg(uvr + pn) : make_uint4(0, 0, 0, 0);
-    const uint32_t v = rec.x;
-    const int32_t rs = (int32_t)rec.y, re = (int32_t)rec.z;
-    const int32_t deg = re - rs;
-    // v's row (every lane: the same 16 bytes) and, lane t, edge t's
-    // neighbour row and weight, staged for the broadcast reads below
-    uint32_t x[WPT];
-    load_row_f64<WPT>(a.pop + (size_t)v * Wp, x);
-    const ulonglong2 key = __ldg(ukey + p);
+    const uint32_t v = cur.rec.x;
+    const int32_t deg = (int32_t)(cur.rec.z - cur.rec.y);
+    uint32_t nb[WPT];
+#pragma unroll
+    for (int j = 0; j < WPT; ++j) nb[j] = 0;
+    if ((int32_t)lane < deg) load_row_f64<WPT>(a.pop + (size_t)cur.u * Wp, nb);
+    const F64Next<WPT> nxt = f64_fetch<WPT>(a, uvr, ukey, G, p + stride, lane);
+    s_w[warp][lane] = cur.w;
+#pragma unroll
+    for (int j = 0; j < WPT; ++j) s_nb[warp][lane][j] = nb[j];
+    __syncwarp();
     double sn[WPT], so[WPT];
 #pragma unroll
     for (int j = 0; j < WPT; ++j) {
       sn[j] = 0.0;
       so[j] = 0.0;
     }
-    for (int32_t base = rs; base < re; base += kF64MaxDeg) {
-      const int32_t cnt = min(kF64MaxDeg, re - base);
-      if ((int32_t)lane < cnt) {
-        const uint32_t u = (uint32_t)__ldg(a.col + base + (int32_t)lane);
-        s_w[warp][lane] = __ldg(a.w + base + (int32_t)lane);
-        uint32_t nb[WPT];
-        load_row_f64<WPT>(a.pop + (size_t)u * Wp, nb);
+    for (int32_t t = 0; t < deg; ++t) {
+      const double wt = s_w[warp][t];
 #pragma unroll
-        for (int j = 0; j < WPT; ++j) s_nb[warp][lane][j] = nb[j];
+      for (int j = 0; j < WPT; ++j) {
+        const uint32_t cut = ((cur.x[j] ^ s_nb[warp][t][j]) >> lane) & 1u;
+        sn[j] += cut ? 0.0 : wt;  // the reference adds every value, 0.0 included
+        so[j] += cut ? wt : 0.0;
       }
-      __syncwarp();
-      for (int32_t t = 0; t < cnt; ++t) {
-        const double wt = s_w[warp][t];
-#pragma unroll
-        for (int j = 0; j < WPT; ++j) {
-          const uint32_t cut = ((x[j] ^ s_nb[warp][t][j]) >> lane) & 1u;
-          sn[j] += cut ? 0.0 : wt;  // the reference adds every value, 0.0 included
-          so[j] += cut ? wt : 0.0;
-        }
-      }
-      __syncwarp();
     }
+    __syncwarp();
     uint32_t ones = 0;
 #pragma unroll
-    for (int j = 0; j < WPT; ++j) ones += __popc(x[j]);
+    for (int j = 0; j < WPT; ++j) ones += __popc(cur.x[j]);
     const bool set_present = ones > 0u && ones < a.n_global;
     uint32_t accb = 0;
     uint32_t nw[WPT];
@@ -155,12 +186,12 @@ __global__ void __launch_bounds__(kF64Warps * 32, 3) gom_univ_f64_kernel(const G
         accept = exact ? (delta > 0.0 || (delta == 0.0 && !is_elit[j]))
                        : (cmp_better(false, cand, pf) || (cmp_equal(false, cand, pf) && !is_elit[j]));
       }
-      if (accept) acc[j] += delta;
+      if (accept) acc[j] += __double2ll_rn(delta * a.fix_scale);
       const uint32_t aw = __ballot_sync(0xFFFFFFFFu, accept);
-      nw[j] = x[j] ^ aw;
+      nw[j] = cur.x[j] ^ aw;
       any |= aw != 0u;
       accb |= accept ? (1u << j) : 0u;
-      if (accept && (int32_t)s == esrc) capture_row(a.elit, a.ever, ever_cur, v, (x[j] >> lane) & 1u);
+      if (accept && (int32_t)s == esrc) capture_row(a.elit, a.ever, ever_cur, v, (cur.x[j] >> lane) & 1u);
       steps += present ? 1u : 0u;
       calls += present ? (uint32_t)deg : 0u;
     }
@@ -168,19 +199,22 @@ __global__ void __launch_bounds__(kF64Warps * 32, 3) gom_univ_f64_kernel(const G
 #pragma unroll
       for (int j = 0; j < WPT; ++j)
         if (accb & (1u << j)) {
-          dh1[j] ^= key.x;
-          dh2[j] ^= key.y;
+          dh1[j] ^= cur.key.x;
+          dh2[j] ^= cur.key.y;
         }
       if (lane == 0) {
         uint32_t* row = a.pop + (size_t)v * Wp;
 #pragma unroll
         for (int j = 0; j < WPT; ++j)
-          if (nw[j] != x[j]) row[j] = nw[j];
+          if (nw[j] != cur.x[j]) row[j] = nw[j];
       }
     }
-    rec = rec_next;
+    cur = nxt;
   }
-  gom_group_tail<WPT, double>(a, epi, s_tail, kF64Warps, warp, 0u, 1u, lane, acc, dh1, dh2, steps, calls);
+  // the next group's launch may start its prologue (it waits for this
+  // grid's completion before touching anything written here)
+  asm volatile("griddepcontrol.launch_dependents;");
+  gom_group_tail<WPT>(a, epi, s_tail, kF64Warps, warp, 0u, 1u, lane, acc, dh1, dh2, steps, calls);
 }
 
 // Plan of a univariate FOS, per group position: {v, row start, row end, 0}
@@ -199,11 +233,22 @@ __global__ void build_univ_plan_kernel(const uint32_t* gvars, const int32_t* row
 }
 
 namespace {
+// CTAs per SM the kernel is register-capped for: 3 (80 registers, some
+// spills of the prefetch state) or 2 (no spills); GOMIX_F64_OCC for A/B
+int f64_occupancy() {
+  static const int occ = [] {
+    const char* e = std::getenv("GOMIX_F64_OCC");
+    return (e && std::atoi(e) == 2) ? 2 : 3;
+  }();
+  return occ;
+}
+
 void* f64_kernel(int wp) {
+  const bool two = f64_occupancy() == 2;
   switch (wp) {
-    case 1: return (void*)gom_univ_f64_kernel<1>;
-    case 2: return (void*)gom_univ_f64_kernel<2>;
-    case 4: return (void*)gom_univ_f64_kernel<4>;
+    case 1: return two ? (void*)gom_univ_f64_kernel<1, 2> : (void*)gom_univ_f64_kernel<1, 3>;
+    case 2: return two ? (void*)gom_univ_f64_kernel<2, 2> : (void*)gom_univ_f64_kernel<2, 3>;
+    case 4: return two ? (void*)gom_univ_f64_kernel<4, 2> : (void*)gom_univ_f64_kernel<4, 3>;
   }
   throw GomixError(GOMIX_E_INVALID, "univariate f64 kernel: unsupported row width");
 }
@@ -219,9 +264,24 @@ int univ_f64_sets_per_cta() { return kF64Warps; }
 
 int univ_f64_max_degree() { return kF64MaxDeg; }
 
-void launch_univ_f64(const GomArgs& a, int wp, int grid, cudaStream_t s) {
+void launch_univ_f64(const GomArgs& a, int wp, int grid, cudaStream_t s, bool pdl) {
   void* args[] = {(void*)&a};
-  GOMIX_CUDA(cudaLaunchKernel(f64_kernel(wp), dim3(grid), dim3(kF64Warps * 32), args, 0, s));
+  if (!pdl) {
+    GOMIX_CUDA(cudaLaunchKernel(f64_kernel(wp), dim3(grid), dim3(kF64Warps * 32), args, 0, s));
+    return;
+  }
+  // programmatic dependent launch: may begin while the previous group's
+  // kernel finishes (this kernel waits with griddepcontrol.wait)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kF64Warps * 32);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  GOMIX_CUDA(cudaLaunchKernelExC(&cfg, f64_kernel(wp), args));
 }
 
 void build_univ_plan(Problem& P) {

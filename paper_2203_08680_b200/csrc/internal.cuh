@@ -30,7 +30,6 @@ namespace gomix_b200 {
 constexpr uint32_t kInSet = 0x80000000u;
 constexpr int kMaxSetSize = 64;     // per-lane set patterns are uint64 masks
 constexpr int kEpilogueThreads = 1024;
-constexpr uint32_t kPartBlock = 32;  // CTAs whose float partials one level-1 reducer adds
 
 struct FpEntry {
   uint32_t a, b;  // endpoint vertex id, or kInSet | index within the set
@@ -73,6 +72,7 @@ struct GroupDesc {
 struct Problem {
   int device = 0;
   uint64_t nv = 0, q = 0, m = 0, k = 0, lmig_edges = 0, max_f = 0, max_fp = 0;
+  double sum_abs_w = 0.0;    // sum of |w| over the edges (fixed-point scale of float fitness deltas)
   uint64_t max_abs_row = 0;  // univariate: max over sets {v} of sum |w| on v's edges (integer weights)
   bool exact = true, univariate = true, i32 = false;
   bool var_once = true;  // every variable is in at most one linkage set
@@ -115,8 +115,8 @@ struct ImprRec {
 
 struct EpiArgs {
   double* fit;
-  const double* part;
-  double* dfit;
+  long long* dfit;   // fixed-point fitness deltas of this group (fix_inv per unit)
+  double fix_inv;    // 1 / GomArgs::fix_scale
   unsigned long long* h1;  // per-solution Zobrist hashes
   unsigned long long* h2;
   unsigned long long* dh1;  // this group's XOR deltas
@@ -129,7 +129,7 @@ struct EpiArgs {
   ImprRec* impr;  // improvement log: fitness + RunControl call count when it was reported
   uint64_t impr_cap;
   uint32_t n, G, nparts, group;  // n: this rank's solutions
-  int32_t mode;  // 0 exact atomics, 1 float partials, 2 ordered
+  int32_t mode;  // 0 integer weights, 1 float, 2 ordered (replay float: recorded deltas in position order)
   // sharding: fit/h1/h2 above are this rank's slices of the gathered arrays
   const double* fit_all;
   const unsigned long long* h1_all;
@@ -174,8 +174,8 @@ struct GomArgs {
   const unsigned long long* h2;
   uint32_t* elit;  // copy-on-write snapshot of the elitist genotype
   uint32_t* ever;  // per-row snapshot version
-  double* dfit;
-  double* part;
+  long long* dfit;       // fixed-point fitness deltas: round(delta * fix_scale), summed by atomics
+  double fix_scale;      // 1 for integer weights, 2^S for float weights
   unsigned long long* dh1;
   unsigned long long* dh2;
   DevCtl* ctl;
@@ -187,8 +187,6 @@ struct GomArgs {
   uint32_t n, Wp, team_warps, stage_words;  // n: this rank's solutions, Wp: words per row per rank
   const uint32_t* pool;  // all ranks' rows, rank-major [R][nv][Wp] (== pop when R == 1)
   const uint32_t* ones;  // sharded univariate runs: members holding 1 per row over all ranks (else nullptr)
-  double* part1;           // float partials, level 1: [ceil(grid / kPartBlock)][n] (nullptr: one level)
-  unsigned int* part_cnt;  // per level-1 block arrival counters
   uint64_t nv;
   uint32_t R, rank, n_global;
   int32_t exact;
@@ -356,7 +354,7 @@ void build_univ_plan(Problem& P);
 int univ_f64_max_blocks_per_sm(int wp);
 int univ_f64_sets_per_cta();
 int univ_f64_max_degree();
-void launch_univ_f64(const GomArgs& a, int wp, int grid, cudaStream_t s);
+void launch_univ_f64(const GomArgs& a, int wp, int grid, cudaStream_t s, bool pdl = false);
 void build_csr_device(Problem& P, bool exact, int32_t* d_eid, uint64_t* max_abs_row);  // problem.cu
 void launch_fi_snapshot(const FiArgs& a, cudaStream_t s);
 void launch_fi_flags(const FiArgs& a, bool given, cudaStream_t s);
