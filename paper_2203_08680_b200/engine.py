@@ -182,6 +182,7 @@ class GpuProblem:
         check(L.gomix_gpu_problem_create(C.byref(instance._struct()), C.byref(fos._struct()),
                                          _capi.ptr(col), device, C.byref(h)))
         self.h = h
+        self._destroy = L.gomix_gpu_problem_destroy  # kept: module globals are gone at interpreter exit
         info = _capi.ProblemInfo()
         check(L.gomix_gpu_problem_info(self.h, C.byref(info)))
         self.info = info
@@ -196,7 +197,7 @@ class GpuProblem:
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().gomix_gpu_problem_destroy(self.h)
+            self._destroy(self.h)
             self.h = None
 
     @property
@@ -262,6 +263,7 @@ class GpuParallelEngine:
         h = C.c_void_p()
         check(lib().gomix_gpu_engine_create(problem.h, C.byref(cfg), C.byref(h)))
         self.h = h
+        self._destroy = lib().gomix_gpu_engine_destroy
         if stream is not None:
             check(lib().gomix_gpu_set_stream(self.h, C.c_void_p(stream)))
         self._elitist_fitness = None
@@ -277,7 +279,7 @@ class GpuParallelEngine:
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().gomix_gpu_engine_destroy(self.h)
+            self._destroy(self.h)
             self.h = None
 
     # ---- bookkeeping shared with RunContext -----------------------------------
@@ -496,6 +498,7 @@ class GpuLocalGroup:
         h = C.c_void_p()
         check(lib().gomix_gpu_local_group_create(C.cast(arr, C.c_void_p), C.byref(cfg), C.byref(h)))
         self.h = h
+        self._destroy = lib().gomix_gpu_local_group_destroy
         self.shards = []
         for r in range(self.world_size):
             eh = C.c_void_p()
@@ -511,7 +514,7 @@ class GpuLocalGroup:
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().gomix_gpu_local_group_destroy(self.h)
+            self._destroy(self.h)
             self.h = None
 
     def run_generation(self):

@@ -59,10 +59,11 @@ class DeviceBest:
         h = C.c_void_p()
         check(lib().gomix_gpu_ims_best_create(problem.h, C.byref(h)))
         self.h = h
+        self._destroy = lib().gomix_gpu_ims_best_destroy  # kept: module globals are gone at interpreter exit
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().gomix_gpu_ims_best_destroy(self.h)
+            self._destroy(self.h)
             self.h = None
 
     def collect(self, engine: GpuParallelEngine):
