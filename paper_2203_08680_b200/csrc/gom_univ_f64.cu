@@ -35,7 +35,6 @@ namespace gomix_b200 {
 namespace {
 constexpr int kF64Warps = 8;
 constexpr int kF64MaxDeg = 32;  // edges per set handled in one pass (one per lane)
-constexpr int kF64TableEdges = 6;  // ordered subset-sum table over the first 6 edges (64 entries)
 }  // namespace
 
 template <int WPT>
@@ -90,7 +89,6 @@ __global__ void __launch_bounds__(kF64Warps * 32, MINB) gom_univ_f64_kernel(cons
   __shared__ __align__(16) uint32_t s_tail[kF64Warps * WPT * 32 * 6];  // gom_group_tail's team combine
   __shared__ double s_w[kF64Warps][kF64MaxDeg];
   __shared__ uint32_t s_nb[kF64Warps][kF64MaxDeg][WPT];
-  __shared__ double s_tab[kF64Warps][1 << kF64TableEdges];
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   // programmatic dependent launch (graph path): everything below reads what
   // the previous group's launch wrote (population, control block, hashes)
@@ -153,30 +151,13 @@ __global__ void __launch_bounds__(kF64Warps * 32, MINB) gom_univ_f64_kernel(cons
 #pragma unroll
     for (int j = 0; j < WPT; ++j) s_nb[warp][lane][j] = nb[j];
     __syncwarp();
-    // Σold / Σnew over the first dt <= kF64TableEdges edges from a table
-    // of ordered subset sums: T[m] = (((0 + a_0) + a_1) + ...) with a_t =
-    // w_t if bit t of m is set, else 0.0 — adding 0.0 changes no value (the
-    // running sum never becomes -0), so T[m] is bit for bit the reference's
-    // left-to-right sum of the selected values (zeros included).  Σold of a
-    // solution is T[cut pattern], Σnew is T[~pattern]; edges past dt are
-    // added one by one in the same order.
-    const int32_t dt = min(deg, kF64TableEdges);
-    const uint32_t tsize = 1u << dt;
-    for (uint32_t m = lane; m < tsize; m += 32u) {
-      double acc_s = 0.0;
-      for (int32_t t = 0; t < dt; ++t) acc_s += ((m >> t) & 1u) ? s_w[warp][t] : 0.0;
-      s_tab[warp][m] = acc_s;
-    }
-    __syncwarp();
     double sn[WPT], so[WPT];
 #pragma unroll
     for (int j = 0; j < WPT; ++j) {
-      uint32_t pat = 0;
-      for (int32_t t = 0; t < dt; ++t) pat |= (((cur.x[j] ^ s_nb[warp][t][j]) >> lane) & 1u) << t;
-      so[j] = s_tab[warp][pat];
-      sn[j] = s_tab[warp][~pat & (tsize - 1u)];
+      sn[j] = 0.0;
+      so[j] = 0.0;
     }
-    for (int32_t t = dt; t < deg; ++t) {
+    for (int32_t t = 0; t < deg; ++t) {
       const double wt = s_w[warp][t];
 #pragma unroll
       for (int j = 0; j < WPT; ++j) {
