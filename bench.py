@@ -85,6 +85,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ttt-seconds", type=float, default=60.0,
                     help="time-to-target leg: wall budget of the reference IMS and of ours (0 = skip)")
+    ap.add_argument("--transport", default=None, choices=["peer", "nccl"],
+                    help="N > 1: exchanges over peer memory inside the kernels (default for univariate FOS) or NCCL")
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="strong: BASELINE's population in total over the N GPUs; weak: that many per GPU")
     return ap.parse_args()
@@ -139,8 +141,8 @@ def base_line(args, cfg, n_total, world):
             "data": "synthetic (generated Max-Cut torus, reference generator and seed)",
             "config": {"workload": cfg["workload"], "population": n_total, "population_per_gpu": n_total // world,
                        "parallelism": f"population sharded over {world} GPUs ({n_total // world} members each; "
-                                      f"NCCL exchange of fitness / hashes / counters per colour group, row "
-                                      f"1-counts per generation)" if world > 1 else "single",
+                                      f"exchange of fitness / hashes / counters per colour group, row presence "
+                                      f"per generation)" if world > 1 else "single",
                        "l2": "flushed between timed steps (256 MiB write)",
                        "donors": "philox", "fos": cfg["fos"]}}
 
@@ -248,12 +250,13 @@ def algorithmic_bytes_per_step(inst, fos, n):
     return total / fos.num_sets
 
 
-def make_engine(G, P, n_total, seed, stream, rank, world, uid):
+def make_engine(G, P, n_total, seed, stream, rank, world, uid, transport):
     """One population of n_total members: single GPU, or sharded over the
-    ranks (rank r holds n_total / world)."""
+    ranks (rank r holds n_total / world; transport "peer": exchanges inside
+    the GOM kernels over peer memory, "nccl": NCCL calls between launches)."""
     if world > 1:
         return G.GpuParallelEngine(P, n_total, seed=seed, mode="philox", stream=stream.cuda_stream, rank=rank,
-                                   world_size=world, nccl_unique_id=uid)
+                                   world_size=world, nccl_unique_id=uid, transport=transport)
     return G.GpuParallelEngine(P, n_total, seed=seed, mode="philox", stream=stream.cuda_stream)
 
 
@@ -271,8 +274,16 @@ def bench_ours(args):
         # transports) on stderr, so a run shows how many ranks took part
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("GOMIX_BENCH_ONE_GPU"):
+            # code-path check on a one-GPU box: every rank on cuda:0, gloo for
+            # the host plumbing (NCCL refuses two ranks on one device); the
+            # peer transport itself works within a device (CUDA IPC)
+            local = 0
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         dist = None
         torch.cuda.set_device(0)
@@ -287,14 +298,17 @@ def bench_ours(args):
     stream = torch.cuda.Stream()  # a real stream: the legacy NULL stream would not see our kernels
     torch.cuda.set_stream(stream)
     uid = None
-    if world > 1:  # the NCCL id of the engines' communicator travels over the process group
+    # univariate FOS (C1/C3/C5): the peer transport — every exchange inside
+    # the GOM kernels over NVLink peer memory, generations queued as CUDA
+    # graphs; other FOS: NCCL between launches, host-ordered
+    transport = args.transport or ("peer" if cfg["fos"] == "uni" else "nccl")
+    if world > 1 and transport == "nccl":  # the NCCL id travels over the process group
         box = [G.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(box, src=0)
         uid = box[0]
-    E = make_engine(G, P, n_total, 1, stream, rank, world, uid)
-    # single GPU: one CUDA graph per generation, no host sync; sharded: the
-    # collective per colour group is host-ordered
-    gen = E.run_generation_async if world == 1 else E.run_generation
+    E = make_engine(G, P, n_total, 1, stream, rank, world, uid, transport)
+    queued = world == 1 or transport == "peer"
+    gen = E.run_generation_async if queued else E.run_generation
 
     def barrier():
         if dist is not None:
@@ -380,7 +394,7 @@ def bench_ours(args):
     # ---- active phase: generations 1-5 of a fresh population ----
     # (the timed generations above are the steady state, where most pairs are
     # neutral or rejected; early generations accept and improve far more)
-    E_act = make_engine(G, P, n_total, 2, stream, rank, world, uid)
+    E_act = make_engine(G, P, n_total, 2, stream, rank, world, uid, transport)
     act_gens = 5
     a0 = [torch.cuda.Event(enable_timing=True) for _ in range(act_gens)]
     a1 = [torch.cuda.Event(enable_timing=True) for _ in range(act_gens)]
@@ -390,7 +404,7 @@ def bench_ours(args):
     for i in range(act_gens):
         flush.zero_()
         a0[i].record(stream)
-        (E_act.run_generation_async if world == 1 else E_act.run_generation)()
+        (E_act.run_generation_async if queued else E_act.run_generation)()
         a1[i].record(stream)
     torch.cuda.synchronize()
     E_act.synchronize()
@@ -515,6 +529,8 @@ def bench_ours(args):
                                 "sample": f"failed: {exc}"}
 
     line = base_line(args, cfg, n_total, world)
+    if world > 1:
+        line["config"]["transport"] = transport
     line.update({
         "value": value,
         "ms_per_step": 1e3 * dev_s / args.steps,

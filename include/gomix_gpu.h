@@ -83,7 +83,14 @@ enum {
    * triggered solutions take the elitist as donor group by group, halt after
    * the first group that strictly improved them, else become elitist copies
    * (engine_serial.hpp:98-128 restated group-wise; see gom_fi.cu). */
-  GOMIX_FLAG_FORCED_IMPROVEMENT = 1u << 6
+  GOMIX_FLAG_FORCED_IMPROVEMENT = 1u << 6,
+  /* Sharded engines (world_size > 1), univariate variable-once FOS: exchange
+   * over peer memory instead of NCCL — the last CTA of every GOM launch
+   * publishes its members into every rank's exchange block and runs the
+   * global elitist scan itself (gom_peer.cuh).  Each rank exports its block
+   * (gomix_gpu_peer_export) and maps everyone's (gomix_gpu_peer_connect)
+   * before gomix_gpu_init_population; no NCCL id is needed. */
+  GOMIX_FLAG_PEER_TRANSPORT = 1u << 7
 };
 
 enum { GOMIX_STOP_NONE = 0, GOMIX_STOP_BUDGET = 1, GOMIX_STOP_CLOCK = 2, GOMIX_STOP_TARGET = 3,
@@ -289,6 +296,14 @@ GOMIX_API int gomix_gpu_ims_best_read(gomix_gpu_ims_best* b, uint8_t* genotype, 
 /* 128-byte NCCL unique id for gomix_engine_config.nccl_unique_id (NCCL is
  * loaded at run time: the process's libnccl.so.2, e.g. PyTorch's). */
 GOMIX_API int gomix_gpu_nccl_unique_id(uint8_t* id);
+
+#define GOMIX_PEER_HANDLE_BYTES 64
+/* GOMIX_FLAG_PEER_TRANSPORT: allocate this rank's exchange block and return
+ * its CUDA IPC handle (GOMIX_PEER_HANDLE_BYTES) for the other ranks. */
+GOMIX_API int gomix_gpu_peer_export(gomix_gpu_engine* e, uint8_t* handle);
+/* Map every rank's block (handles: world_size x GOMIX_PEER_HANDLE_BYTES in
+ * rank order, this rank's own entry ignored); then init_population. */
+GOMIX_API int gomix_gpu_peer_connect(gomix_gpu_engine* e, const uint8_t* handles);
 /* In-process shards: world_size engines (problems[r] on the device of rank r;
  * the same problem may serve several ranks on one device) driven in lock step
  * by one host thread; the exchange is device-to-device copies. */

@@ -25,7 +25,8 @@ if _alt:
 GOMIX_OK, GOMIX_E_INVALID, GOMIX_E_CUDA, GOMIX_E_NCCL, GOMIX_E_OOM, GOMIX_E_STATE = range(6)
 MODE_REPLAY, MODE_PHILOX = 0, 1
 FLAG_ORDERED_FLOAT, FLAG_RECORD_BATCH, FLAG_TIME_KERNELS, FLAG_LANE_PER_SOLUTION, FLAG_PER_GROUP_KERNELS, \
-    FLAG_NO_TRUTH_TABLE, FLAG_FORCED_IMPROVEMENT = 1, 2, 4, 8, 16, 32, 64
+    FLAG_NO_TRUTH_TABLE, FLAG_FORCED_IMPROVEMENT, FLAG_PEER_TRANSPORT = 1, 2, 4, 8, 16, 32, 64, 128
+PEER_HANDLE_BYTES = 64
 STOP_NAMES = {0: "none", 1: "evaluation-budget", 2: "wall-clock", 3: "target-reached",
               4: "generation-limit"}
 
@@ -116,6 +117,8 @@ _SIGNATURES = {
     "gomix_gpu_ims_offer": ([_P, _P], C.c_int),
     "gomix_gpu_ims_best_read": ([_P, _P, C.POINTER(C.c_double), C.POINTER(C.c_int32)], C.c_int),
     "gomix_gpu_nccl_unique_id": ([_P], C.c_int),
+    "gomix_gpu_peer_export": ([_P, _P], C.c_int),
+    "gomix_gpu_peer_connect": ([_P, _P], C.c_int),
     "gomix_gpu_local_group_create": ([_P, C.POINTER(EngineConfig), C.POINTER(_P)], C.c_int),
     "gomix_gpu_local_group_destroy": ([_P], C.c_int),
     "gomix_gpu_local_group_engine": ([_P, C.c_int32, C.POINTER(_P)], C.c_int),

@@ -12,7 +12,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libgomix_b200.so")
-SOURCES = ["problem.cu", "gom.cu", "gom_univ.cu", "gom_univ_f64.cu", "gom_gen.cu", "gom_fi.cu", "engine.cu", "instances.cu", "linkage.cu"]
+SOURCES = ["problem.cu", "gom.cu", "gom_univ.cu", "gom_univ_f64.cu", "gom_peer.cu", "gom_gen.cu", "gom_fi.cu", "engine.cu", "instances.cu", "linkage.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC,-fvisibility=hidden", "-Xptxas", "-v", "--expt-relaxed-constexpr",

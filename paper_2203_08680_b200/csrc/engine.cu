@@ -25,6 +25,7 @@
 
 #include "gomix_gpu.h"
 #include "internal.cuh"
+#include "gom_peer.cuh"
 
 namespace gomix_b200 {
 void build_problem_device_impl(Problem& P, const int32_t* given_colour, const int32_t* eid);
@@ -295,6 +296,14 @@ struct gomix_gpu_engine {
   uint64_t n_global = 0;   // population size
   uint32_t R = 1, rank = 0;
   std::unique_ptr<NcclComm> nccl;    // one process per GPU
+  // peer transport (GOMIX_FLAG_PEER_TRANSPORT, gom_peer.cuh): this rank's
+  // exchange block (cudaMalloc: IPC-exportable), every rank's mapped block
+  bool peer_on = false;
+  char* xblock = nullptr;
+  size_t xbytes = 0;
+  std::vector<void*> peer_opened;  // cudaIpcOpenMemHandle mappings to close
+  PeerArgs* d_peer = nullptr;
+  unsigned long long xe_epoch = 0;  // elitist broadcasts (host-driven; group / presence epochs live in DevCtl)
   gomix_gpu_local_group* local = nullptr;  // several shards in one process
   uint32_t W = 0, Wp = 0, wpt = 1, tw = 1, block = 256, teams = 8, stage_words = 0;
   size_t smem = 0;
@@ -401,6 +410,8 @@ struct gomix_gpu_engine {
     }
     for (auto e : ev_free) cudaEventDestroy(e);
     cudaDeviceSynchronize();
+    for (void* p : peer_opened) cudaIpcCloseMemHandle(p);
+    if (xblock) cudaFree(xblock);
     cached_free_all(allocs);
     if (h_ctl) cudaFreeHost(h_ctl);
     if (h_begin) cudaFreeHost(h_begin);
@@ -600,6 +611,8 @@ struct gomix_gpu_engine {
       rec_accept = dev_alloc<uint8_t>(allocs, max_group * n);
     }
     lite = R > 1 && P->univariate && P->var_once && mode == GOMIX_MODE_PHILOX;
+    if ((flags & GOMIX_FLAG_PEER_TRANSPORT) && R > 1 && !lite)
+      invalid("engine: the peer transport needs a univariate FOS with every variable in one set (use NCCL)");
     if (tt_chunks > 1 && R > 1 && !lite) invalid("engine: internal: chunked rows need the sharded row counts");
     if (lite || tt_chunks > 1) ones = dev_alloc<uint32_t>(allocs, nv);
     if (lite) {
@@ -730,7 +743,12 @@ struct gomix_gpu_engine {
   // generation start, the presence test of its set (the FOS is univariate and
   // variable-once: a row changes only in its own group).
   void count_rows(cudaStream_t st) {
-    if (tt_chunks <= 1 || R > 1) return;  // sharded runs count (and all-reduce) in run_generation_sharded
+    if (R > 1 && peer_on) {  // sharded over peer memory: every rank's presence maps (graph path)
+      launch_presence(d_peer, ctl, pop, P->nv, Wp, (uint32_t)n, (uint32_t)n_global, ones, st);
+      launches += 2;
+      return;
+    }
+    if (tt_chunks <= 1 || R > 1) return;  // sharded NCCL runs count (and all-reduce) in run_generation_sharded
     launch_count_ones(pop, P->nv, Wp, ones, st);
     ++launches;
   }
@@ -817,6 +835,7 @@ struct gomix_gpu_engine {
     e.n_global = (uint32_t)n_global;
     e.R = R;
     e.rank = rank;
+    e.peer = peer_on ? d_peer : nullptr;
     e.n = (uint32_t)n;
     e.G = G;
     e.nparts = nparts;
@@ -1093,6 +1112,59 @@ struct gomix_gpu_engine {
     GOMIX_CUDA(cudaMemcpyAsync(tape, h_tape_pinned, G * n * 4, cudaMemcpyHostToDevice, stream));
   }
 
+  // ---- peer transport -------------------------------------------------------
+  // This rank's exchange block: plain cudaMalloc (pool memory cannot be
+  // exported through a CUDA IPC handle), zeroed once; epochs start at 1.
+  void peer_alloc() {
+    if (R < 2 || !(flags & GOMIX_FLAG_PEER_TRANSPORT)) invalid("peer transport: needs world_size > 1 and GOMIX_FLAG_PEER_TRANSPORT");
+    if (R > kMaxRanks) invalid("peer transport: at most 16 ranks");
+    if (xblock) return;
+    xbytes = peer_block_bytes(R, (uint32_t)n, (uint32_t)((P->nv + 31) / 32));
+    GOMIX_CUDA(cudaSetDevice(P->device));
+    GOMIX_CUDA(cudaMalloc(&xblock, xbytes));
+    GOMIX_CUDA(cudaMemset(xblock, 0, xbytes));
+    GOMIX_CUDA(cudaDeviceSynchronize());
+  }
+
+  // blocks[r]: rank r's block as mapped in this process (own = xblock)
+  void peer_set_blocks(char* const* blocks) {
+    PeerArgs h{};
+    for (uint32_t r = 0; r < R; ++r) h.blocks[r] = r == rank ? xblock : blocks[r];
+    h.R = R;
+    h.rank = rank;
+    h.n = (uint32_t)n;
+    h.w32 = (uint32_t)((P->nv + 31) / 32);
+    h.timeout_ns = 60ull * 1000000000ull;  // a rank that stopped calling: fault after a minute, never a hang
+    if (!d_peer) d_peer = dev_alloc<PeerArgs>(allocs, 1);
+    GOMIX_CUDA(cudaMemcpy(d_peer, &h, sizeof(PeerArgs), cudaMemcpyHostToDevice));
+    peer_on = true;
+  }
+
+  void peer_export(uint8_t* handle) {
+    peer_alloc();
+    cudaIpcMemHandle_t h;
+    GOMIX_CUDA(cudaIpcGetMemHandle(&h, xblock));
+    static_assert(sizeof(cudaIpcMemHandle_t) == GOMIX_PEER_HANDLE_BYTES, "IPC handle size");
+    std::memcpy(handle, &h, sizeof(h));
+  }
+
+  void peer_connect(const uint8_t* handles) {
+    if (!xblock) invalid("peer_connect: export this rank's block first (gomix_gpu_peer_export)");
+    if (initialized) throw GomixError(GOMIX_E_STATE, "peer_connect: call before init_population");
+    GOMIX_CUDA(cudaSetDevice(P->device));
+    std::vector<char*> blocks(R, nullptr);
+    for (uint32_t r = 0; r < R; ++r) {
+      if (r == rank) continue;
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, handles + (size_t)r * GOMIX_PEER_HANDLE_BYTES, sizeof(h));
+      void* p = nullptr;
+      GOMIX_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+      peer_opened.push_back(p);
+      blocks[r] = static_cast<char*>(p);
+    }
+    peer_set_blocks(blocks.data());
+  }
+
   // ---- API operations ---------------------------------------------------------
   void init_population(const uint8_t* genotypes, const gomix_stop_criteria* stop,
                        gomix_run_stats* out) {
@@ -1121,8 +1193,13 @@ struct gomix_gpu_engine {
     launch_full_eval(*P, pop, fit, (uint32_t)n, Wp, epi_mode == 2, stream);
     launch_hash_population(snap_args(), stream);
     launches += 2;
-    if (R > 1 && nccl) exchange();
-    if (R == 1 || nccl) init_global(stop, out);
+    if (R > 1 && peer_on) {
+      launch_peer_exchange(epi_args(0, 0, 0), stream);  // every rank's fitness and hashes
+      ++launches;
+    } else if (R > 1 && nccl) {
+      exchange();
+    }
+    if (R == 1 || nccl || (peer_on && !local)) init_global(stop, out);
   }
 
   // the part of init after every rank's fitness and hashes are known
@@ -1177,6 +1254,19 @@ struct gomix_gpu_engine {
     begin_call(stop);
     std::vector<uint64_t> order;
     rng.permutation(order, P->k);  // same seed on every rank: same order
+    if (peer_on) {
+      // presence maps over peer memory, then per group ONE launch: the GOM
+      // kernel's last CTA publishes, waits for every rank and runs the
+      // global elitist scan (gom_peer.cuh) — no NCCL call, no extra launch
+      launch_presence(d_peer, ctl, pop, P->nv, Wp, (uint32_t)n, (uint32_t)n_global, ones, stream);
+      launches += 2;
+      for (uint64_t gi : order) launch_group(gi, false);
+      read_ctl();
+      if (h_ctl->peer_fault) throw GomixError(GOMIX_E_NCCL, "peer exchange timed out (a rank stopped calling)");
+      fill_stats(out);
+      if (!h_ctl->stop) ++generation;
+      return;
+    }
     if (lite) {  // members holding 1 per row, summed over the ranks
       launch_count_ones(pop, P->nv, Wp, ones_local, stream);
       const NcclApi& api = nccl_or_throw();
@@ -1200,7 +1290,8 @@ struct gomix_gpu_engine {
   void run_generation(const gomix_stop_criteria* stop, gomix_run_stats* out) {
     if (!initialized) throw GomixError(GOMIX_E_STATE, "run_generation: population not initialised");
     if (R > 1) {
-      if (!nccl) throw GomixError(GOMIX_E_STATE, "run_generation: in-process shards are driven by their local group");
+      if (!nccl && !peer_on)
+        throw GomixError(GOMIX_E_STATE, "run_generation: in-process shards are driven by their local group");
       run_generation_sharded(stop, out);
       return;
     }
@@ -1243,7 +1334,10 @@ struct gomix_gpu_engine {
   void run_generation_async() {
     if (!initialized) throw GomixError(GOMIX_E_STATE, "run_generation: population not initialised");
     if (mode != GOMIX_MODE_PHILOX) invalid("run_generation_async: needs GOMIX_MODE_PHILOX");
-    if (R > 1) invalid("run_generation_async: single-GPU engines only");
+    // sharded over peer memory (one process per GPU): the same CUDA graph
+    // with the presence maps in front — every exchange runs inside the
+    // kernels, the group order comes from the shared seed on the device
+    if (R > 1 && (!peer_on || local)) invalid("run_generation_async: single-GPU or peer-transport engines only");
     if (gen_ok) {
       stage_criteria(nullptr, false);
       if (fi_on) fi_snapshot();
@@ -1273,7 +1367,7 @@ struct gomix_gpu_engine {
   // (NULL = evaluate on the device); the elitist is kept.
   void load_population(const uint8_t* genotypes, const double* fitness) {
     if (!initialized) throw GomixError(GOMIX_E_STATE, "load_population: population not initialised");
-    if (R > 1 && !nccl) invalid("load_population: in-process shards are driven by their local group");
+    if (R > 1 && !nccl && !peer_on) invalid("load_population: in-process shards are driven by their local group");
     const uint64_t nv = P->nv;
     // the elitist snapshot may still point into the old population: finish it
     launch_finalize_elitist(snap_args(), stream);
@@ -1290,7 +1384,12 @@ struct gomix_gpu_engine {
     }
     launch_hash_population(snap_args(), stream);  // hashes of the new members
     ++launches;
-    if (R > 1) exchange();  // every rank's pool rows, fitness and hashes (collective)
+    if (R > 1 && peer_on) {  // every rank's fitness and hashes (collective)
+      launch_peer_exchange(epi_args(0, 0, 0), stream);
+      ++launches;
+    } else if (R > 1) {
+      exchange();  // every rank's pool rows, fitness and hashes (collective)
+    }
     GOMIX_CUDA(cudaStreamSynchronize(stream));
   }
 
@@ -1365,12 +1464,16 @@ struct gomix_gpu_local_group {
     }
   }
 
+  bool peer() const { return eng[0]->peer_on; }
+
   void init(const gomix_stop_criteria* stop, gomix_run_stats* out) {
+    // every rank's work is queued before any rank synchronises: with the
+    // peer transport the ranks' kernels wait for each other on the device
     for (uint32_t r = 0; r < R(); ++r) {
       set_device(r);
       eng[r]->init_population(nullptr, stop, nullptr);
     }
-    exchange();
+    if (!peer()) exchange();
     for (uint32_t r = 0; r < R(); ++r) {
       set_device(r);
       eng[r]->init_global(stop, r == 0 ? out : nullptr);
@@ -1387,6 +1490,31 @@ struct gomix_gpu_local_group {
       std::vector<uint64_t> o;
       eng[r]->rng.permutation(o, eng[r]->P->k);
       if (r == 0) order = o;
+    }
+    if (peer()) {
+      // presence maps, then per group one launch per rank whose last CTA
+      // exchanges over peer memory and runs the global scan (gom_peer.cuh);
+      // every rank's launches are queued before any rank synchronises
+      for (uint32_t r = 0; r < R(); ++r) {
+        set_device(r);
+        gomix_gpu_engine& e = *eng[r];
+        launch_presence(e.d_peer, e.ctl, e.pop, e.P->nv, e.Wp, (uint32_t)e.n, (uint32_t)e.n_global, e.ones,
+                        e.stream);
+        e.launches += 2;
+      }
+      for (uint64_t gi : order)
+        for (uint32_t r = 0; r < R(); ++r) {
+          set_device(r);
+          eng[r]->launch_group(gi, false);
+        }
+      for (uint32_t r = 0; r < R(); ++r) {
+        set_device(r);
+        eng[r]->read_ctl();
+        if (eng[r]->h_ctl->peer_fault) throw GomixError(GOMIX_E_NCCL, "peer exchange timed out");
+        eng[r]->fill_stats(r == 0 ? out : nullptr);
+        if (!eng[r]->h_ctl->stop) ++eng[r]->generation;
+      }
+      return;
     }
     const bool lite = eng[0]->lite;
     if (lite) {  // members holding 1 per row, summed over the ranks (the NCCL all-reduce)
@@ -1658,7 +1786,15 @@ int gomix_gpu_read_elitist(gomix_gpu_engine* e, uint8_t* genotype, double* fitne
     if (genotype) {
       launch_finalize_elitist(e->snap_args(), e->stream);  // complete the copy-on-write snapshot
       ++e->launches;
-      if (e->R > 1) {
+      if (e->R > 1 && e->peer_on && !e->local) {
+        // collective over the ranks over peer memory: the owner's snapshot
+        const int32_t owner = e->elitist_owner();
+        if (owner >= 0) {
+          launch_peer_elitist(e->d_peer, e->ctl, e->elit, e->P->nv, (uint32_t)owner == e->rank, ++e->xe_epoch,
+                              e->stream);
+          ++e->launches;
+        }
+      } else if (e->R > 1) {
         // collective over the ranks: the owner's snapshot is the valid one
         if (!e->nccl) invalid("read_elitist: use gomix_gpu_local_group_read_elitist for in-process shards");
         const int32_t owner = e->elitist_owner();
@@ -1901,6 +2037,20 @@ int gomix_gpu_nccl_unique_id(uint8_t* id) {
   });
 }
 
+int gomix_gpu_peer_export(gomix_gpu_engine* e, uint8_t* handle) {
+  return guarded([&] {
+    if (!e || !handle) invalid("peer_export: NULL argument");
+    e->peer_export(handle);
+  });
+}
+
+int gomix_gpu_peer_connect(gomix_gpu_engine* e, const uint8_t* handles) {
+  return guarded([&] {
+    if (!e || !handles) invalid("peer_connect: NULL argument");
+    e->peer_connect(handles);
+  });
+}
+
 int gomix_gpu_local_group_create(gomix_gpu_problem* const* problems, const gomix_engine_config* cfg,
                                  gomix_gpu_local_group** out) {
   return guarded([&] {
@@ -1925,6 +2075,14 @@ int gomix_gpu_local_group_create(gomix_gpu_problem* const* problems, const gomix
       g->ev_step.push_back(a);
       g->ev_done.push_back(b);
       g->eng.push_back(std::move(e));
+    }
+    if (cfg->flags & GOMIX_FLAG_PEER_TRANSPORT) {  // in process: every rank's block by its device pointer
+      std::vector<char*> blocks;
+      for (auto& e : g->eng) {
+        e->peer_alloc();
+        blocks.push_back(e->xblock);
+      }
+      for (auto& e : g->eng) e->peer_set_blocks(blocks.data());
     }
     *out = g.release();
   });

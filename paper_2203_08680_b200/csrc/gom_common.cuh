@@ -9,6 +9,7 @@
 #include <stdint.h>
 
 #include "internal.cuh"
+#include "gom_peer.cuh"
 
 namespace gomix_b200 {
 
@@ -357,7 +358,13 @@ static __device__ void epilogue_body(const EpiArgs& a) {
   __shared__ unsigned long long s_h[2 * kEpiSmemFit];  // ... and hashes (a new elitist's)
   commit_local(a, a.R == 1 ? s_fit : nullptr, a.R == 1 ? s_h : nullptr);
   __syncthreads();
-  if (a.R == 1) elitist_scan(a, s_fit, s_h);
+  if (a.R == 1) {
+    elitist_scan(a, s_fit, s_h);
+  } else if (a.peer != nullptr) {
+    // sharded, peer transport: the exchange and the global scan happen here,
+    // in the same kernel (gom_peer.cuh); with NCCL they follow the launch
+    if (peer_exchange(a)) elitist_scan(a, nullptr);
+  }
 }
 
 }  // namespace gomix_b200

@@ -60,6 +60,10 @@ struct DevCtl {
   unsigned long long eh1, eh2;  // 128-bit Zobrist hash of the elitist genotype
   unsigned int elit_ver;        // snapshot version: row v is captured iff ever[v] == elit_ver
   unsigned int gen_buf;         // persistent generation kernel: running accumulator index
+  // peer transport (gom_peer.cuh): exchange epochs, identical on every rank
+  unsigned long long xg_epoch, xp_epoch, xe_epoch;
+  unsigned int xp_ticket;       // last-CTA ticket of the presence publish
+  unsigned int peer_fault;      // a peer exchange timed out
 };
 
 // One colour group as the device sees it (graph path: kernels look their
@@ -113,6 +117,8 @@ struct ImprRec {
   unsigned long long calls;
 };
 
+struct PeerArgs;
+
 struct EpiArgs {
   double* fit;
   long long* dfit;   // fixed-point fitness deltas of this group (fix_inv per unit)
@@ -136,6 +142,7 @@ struct EpiArgs {
   const unsigned long long* h2_all;
   unsigned long long* rank_cnt;  // [R][steps, calls] of the current group
   uint32_t n_global, R, rank;
+  const PeerArgs* peer;  // sharded, peer transport: the exchange runs inside the epilogue (gom_peer.cuh)
 };
 
 // elitist snapshot / hashing kernels
@@ -372,6 +379,13 @@ void launch_external_elitist(const SnapArgs& a, double fitness, cudaStream_t s);
 void launch_ims_collect(const SnapArgs& a, ImsBestDev* b, uint32_t* bits, int exact, cudaStream_t s);
 void launch_ims_offer(const SnapArgs& a, ImsBestDev* b, const uint32_t* bits, int exact, cudaStream_t s);
 void launch_count_ones(const uint32_t* pop, uint64_t nv, uint32_t Wp, uint32_t* ones, cudaStream_t s);
+// peer transport (gom_peer.cu / gom_peer.cuh)
+size_t peer_block_bytes(uint32_t R, uint32_t n, uint32_t w32);
+void launch_peer_exchange(const EpiArgs& a, cudaStream_t s);
+void launch_presence(const PeerArgs* d_peer, DevCtl* ctl, const uint32_t* pop, uint64_t nv, uint32_t Wp,
+                     uint32_t n_local, uint32_t n_global, uint32_t* ones, cudaStream_t s);
+void launch_peer_elitist(const PeerArgs* d_peer, DevCtl* ctl, uint32_t* elit, uint64_t nv, bool owner,
+                        unsigned long long epoch, cudaStream_t s);
 void launch_sum_ones(const uint32_t* stage, uint32_t R, uint64_t nv, uint32_t* ones, cudaStream_t s);
 void debug_probes(unsigned long long* out, bool reset);
 void debug_probes_gen(unsigned long long* out, bool reset);

@@ -236,11 +236,14 @@ class GpuParallelEngine:
                  genotypes: Optional[np.ndarray] = None, stream=None, rank: int = 0, world_size: int = 1,
                  nccl_unique_id: Optional[bytes] = None, lane_per_solution: bool = False,
                  per_group_kernels: bool = False, truth_table: bool = True,
-                 forced_improvement: bool = False):
+                 forced_improvement: bool = False, transport: str = "nccl", process_group=None):
         """world_size > 1: this process's shard of a population of
         `population_size` members over world_size GPUs (Philox mode); every
-        rank passes the same nccl_unique_id (see nccl_unique_id()) and calls
-        run_generation / elitist collectively."""
+        rank calls run_generation / elitist collectively.  transport "nccl":
+        every rank passes the same nccl_unique_id (see nccl_unique_id());
+        "peer": the GOM kernels exchange over peer memory themselves
+        (gom_peer.cuh; univariate variable-once FOS), the blocks' CUDA IPC
+        handles are all-gathered over torch.distributed (process_group)."""
         if population_size <= 0:
             raise ValueError("engine: population must be non-empty")
         self.problem = problem
@@ -255,7 +258,8 @@ class GpuParallelEngine:
             | (_capi.FLAG_LANE_PER_SOLUTION if lane_per_solution else 0) \
             | (_capi.FLAG_PER_GROUP_KERNELS if per_group_kernels else 0) \
             | (0 if truth_table else _capi.FLAG_NO_TRUTH_TABLE) \
-            | (_capi.FLAG_FORCED_IMPROVEMENT if forced_improvement else 0)
+            | (_capi.FLAG_FORCED_IMPROVEMENT if forced_improvement else 0) \
+            | (_capi.FLAG_PEER_TRANSPORT if transport == "peer" and self.world_size > 1 else 0)
         self._nid = None if nccl_unique_id is None else C.create_string_buffer(bytes(nccl_unique_id), 128)
         cfg = _capi.EngineConfig(self.n_global, seed, _capi.MODE_REPLAY if mode == "replay" else _capi.MODE_PHILOX,
                                  flags, population_id, self.rank, self.world_size,
@@ -264,6 +268,15 @@ class GpuParallelEngine:
         check(lib().gomix_gpu_engine_create(problem.h, C.byref(cfg), C.byref(h)))
         self.h = h
         self._destroy = lib().gomix_gpu_engine_destroy
+        if transport == "peer" and self.world_size > 1:
+            import torch.distributed as dist
+
+            mine = C.create_string_buffer(_capi.PEER_HANDLE_BYTES)
+            check(lib().gomix_gpu_peer_export(self.h, C.cast(mine, C.c_void_p)))
+            every = [None] * self.world_size
+            dist.all_gather_object(every, mine.raw, group=process_group)
+            allh = C.create_string_buffer(b"".join(every), _capi.PEER_HANDLE_BYTES * self.world_size)
+            check(lib().gomix_gpu_peer_connect(self.h, C.cast(allh, C.c_void_p)))
         if stream is not None:
             check(lib().gomix_gpu_set_stream(self.h, C.c_void_p(stream)))
         self._elitist_fitness = None
@@ -483,7 +496,9 @@ class GpuLocalGroup:
     process per GPU over NCCL, and equal to a single-engine Philox run."""
 
     def __init__(self, problems, population_size: int, seed: int = 1, world_size: Optional[int] = None,
-                 ctx: Optional[RunContext] = None):
+                 ctx: Optional[RunContext] = None, transport: str = "copy"):
+        """transport "copy": device-to-device copies between the launches;
+        "peer": the GOM kernels exchange over peer memory (gom_peer.cuh)."""
         if isinstance(problems, GpuProblem):
             problems = [problems] * int(world_size or 1)
         self.problems = list(problems)
@@ -494,7 +509,8 @@ class GpuLocalGroup:
         self.ctx = ctx if ctx is not None else RunContext(TerminationConfig(), self.problem.comparator(),
                                                           self.problem.info.num_edges)
         arr = (C.c_void_p * self.world_size)(*[p.h for p in self.problems])
-        cfg = _capi.EngineConfig(self.n_global, seed, _capi.MODE_PHILOX, 0, 1, 0, self.world_size, None)
+        flags = _capi.FLAG_PEER_TRANSPORT if transport == "peer" else 0
+        cfg = _capi.EngineConfig(self.n_global, seed, _capi.MODE_PHILOX, flags, 1, 0, self.world_size, None)
         h = C.c_void_p()
         check(lib().gomix_gpu_local_group_create(C.cast(arr, C.c_void_p), C.byref(cfg), C.byref(h)))
         self.h = h

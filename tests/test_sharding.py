@@ -79,12 +79,18 @@ def _single(P, n, seed, crit=None):
     ("uni", (1000, 1000), 128, 2, 2),  # ... to 2 GPUs: 64 per shard
     ("uni", (100, 100), 1024, 2, 3),   # 512 per shard: truth-table rows in 4 chunks per shard
 ])
-def test_sharded_equals_single_engine(kind, shape, n, R, gens):
+@pytest.mark.parametrize("transport", ["copy", "peer"])
+def test_sharded_equals_single_engine(kind, shape, n, R, gens, transport):
+    """transport "copy": device-to-device copies between the launches (the
+    NCCL schedule); "peer": the GOM kernels' last CTAs exchange over peer
+    memory and run the global scan themselves (gom_peer.cuh)."""
+    if transport == "peer" and kind != "uni":
+        pytest.skip("the peer transport serves univariate variable-once FOS")
     inst = G.generate_torus(shape[0], shape[1], ("int", -3, 9), 5)
     fos = G.univariate_fos(inst.num_vertices) if kind == "uni" else G.neighbourhood_fos(inst)
     P = G.GpuProblem(inst, fos)
     E, _ = _single(P, n, 11)
-    S = G.GpuLocalGroup(P, n, seed=11, world_size=R)
+    S = G.GpuLocalGroup(P, n, seed=11, world_size=R, transport=transport)
     g1, f1 = E.population()
     g2, f2 = S.population()
     assert (g1 == g2).all() and (f1 == f2).all()
@@ -106,13 +112,14 @@ def test_sharded_equals_single_engine(kind, shape, n, R, gens):
 
 
 @pytest.mark.gpu
-def test_sharded_stop_criteria_match_single_engine():
+@pytest.mark.parametrize("transport", ["copy", "peer"])
+def test_sharded_stop_criteria_match_single_engine(transport):
     inst = G.generate_torus(16, 16, ("int", 1, 10), 3)
     P = G.GpuProblem(inst, G.univariate_fos(256))
     crit = dict(max_evaluations=900.0)
     E, ce = _single(P, 64, 4, crit)
     cs = G.RunContext(G.TerminationConfig(**crit), P.comparator(), inst.num_edges)
-    S = G.GpuLocalGroup(P, 64, seed=4, world_size=4, ctx=cs)
+    S = G.GpuLocalGroup(P, 64, seed=4, world_size=4, ctx=cs, transport=transport)
     for _ in range(50):
         E.run_generation()
         S.run_generation()
