@@ -27,17 +27,22 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, probes: bool = False) -> str:
+    """probes: an instrumented copy (-DGOMIX_PROBES: %globaltimer marks in
+    the GOM kernels) as libgomix_b200_probes.so, loaded with
+    GOMIX_LIB=paper_2203_08680_b200/libgomix_b200_probes.so."""
+    lib = LIB.replace(".so", "_probes.so") if probes else LIB
+    if not force and not probes and not _stale():
         return LIB
     objs = []
-    build_dir = os.path.join(PKG, "build")
+    build_dir = os.path.join(PKG, "build_probes" if probes else "build")
+    flags = FLAGS + (["-DGOMIX_PROBES"] if probes else [])
     os.makedirs(build_dir, exist_ok=True)
     procs = []
     for src in SOURCES:
         obj = os.path.join(build_dir, src.replace(".cu", ".o"))
         objs.append(obj)
-        cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *flags, "-c", os.path.join(CSRC, src), "-o", obj]
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
     for cmd, p in procs:
         out, _ = p.communicate()
@@ -47,12 +52,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError("nvcc failed: " + " ".join(cmd))
         with open(os.path.join(build_dir, os.path.basename(cmd[-3]) + ".ptxas.txt"), "w") as fh:
             fh.write(out)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     subprocess.run([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp, *objs,
                     "-lcudart_static", "-ldl", "-lrt", "-lpthread"], check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, probes="--probes" in sys.argv))

@@ -1591,6 +1591,12 @@ GOMIX_API int gomix_debug_probes(unsigned long long* out, int32_t reset) {
   });
 }
 
+// truth-table kernel launch timeline, probes builds (build.py --probes):
+// out[2i] / out[2i+1] = first / last CTA at point i (%globaltimer ns); resets
+GOMIX_API int gomix_debug_timeline(unsigned long long* out) {
+  return guarded([&] { debug_timeline_univ(out); });
+}
+
 const char* gomix_gpu_last_error(void) { return g_last_error.c_str(); }
 
 int gomix_gpu_problem_create(const gomix_maxcut* instance, const gomix_fos* fos,

@@ -39,6 +39,21 @@ __device__ __forceinline__ void probe_last(uint32_t flags, uint32_t i) {
 #endif
 }
 
+// Launch timeline (probes builds only): for point i, the earliest and latest
+// CTA to reach it (thread 0), as %globaltimer ns; read and reset through
+// gomix_debug_timeline.
+static __device__ unsigned long long g_timeline[32];  // one copy per translation unit
+__device__ __forceinline__ void timeline_mark(uint32_t i) {
+#ifdef GOMIX_PROBES
+  if (threadIdx.x == 0 && i < 16) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMin(&g_timeline[2 * i], t);
+    atomicMax(&g_timeline[2 * i + 1], t);
+  }
+#endif
+}
+
 // ---------------------------------------------------------------------------
 // Philox4x32-10 (Salmon et al., SC'11), counter-based: every (generation, set,
 // solution, call) has its own counter, so draws need no state and no order.

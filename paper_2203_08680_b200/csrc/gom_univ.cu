@@ -382,6 +382,7 @@ __global__ void __launch_bounds__(kUnivWarps * 32, MINB) gom_univ_tt_kernel(cons
   __shared__ unsigned long long s_steps, s_calls;
   __shared__ int s_last;
   probe(a.exp_flags, 40);
+  timeline_mark(0);  // CTA start
 
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   constexpr uint32_t Wp = (uint32_t)WC;  // words of this CTA's chunk (whole rows when a.Wp == WC)
@@ -437,11 +438,12 @@ __global__ void __launch_bounds__(kUnivWarps * 32, MINB) gom_univ_tt_kernel(cons
   }
   __syncthreads();
   probe(a.exp_flags, 41);
+  timeline_mark(1);  // prologue done
   unsigned long long steps = 0, calls = 0;
   tt_batches<B, WC>(a, part, urec, ukey, G, first, s_elit, s_dfit, sh, esrc, ever_cur, lane, warp, steps, calls);
 
   probe(a.exp_flags, 42);
-  // the next group's launch may start its prologue (it waits for this grid's
+  timeline_mark(2);  // warp 0's batches done (it waits for this grid's
   // completion before touching anything written here)
   asm volatile("griddepcontrol.launch_dependents;");
   {
@@ -457,6 +459,7 @@ __global__ void __launch_bounds__(kUnivWarps * 32, MINB) gom_univ_tt_kernel(cons
     }
   }
   __syncthreads();
+  timeline_mark(6);  // every warp of the CTA done with its batches
   for (uint32_t s = threadIdx.x; s < part.n_chunk; s += blockDim.x) {
     unsigned long long x1 = 0, x2 = 0;
 #pragma unroll
@@ -480,6 +483,7 @@ __global__ void __launch_bounds__(kUnivWarps * 32, MINB) gom_univ_tt_kernel(cons
     }
   }
   __syncthreads();
+  timeline_mark(3);  // CTA flushed
   if (threadIdx.x == 0) {
     __threadfence();
     s_last = atomicAdd(&a.ctl->done, 1u) == gridDim.x - 1;
@@ -489,8 +493,10 @@ __global__ void __launch_bounds__(kUnivWarps * 32, MINB) gom_univ_tt_kernel(cons
   if (!s_last) return;
   __threadfence();
   probe_last(a.exp_flags, 44);
+  timeline_mark(4);  // epilogue start (last CTA)
   epilogue_body(epi);
   probe_last(a.exp_flags, 45);
+  timeline_mark(5);  // epilogue end
   if (threadIdx.x == 0) a.ctl->done = 0;
 }
 
@@ -591,6 +597,14 @@ void launch_univ_sliced(const GomArgs& a, int planes, int wp, bool tt, int grid,
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   GOMIX_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
+}
+
+void debug_timeline_univ(unsigned long long* out) {
+  GOMIX_CUDA(cudaDeviceSynchronize());
+  GOMIX_CUDA(cudaMemcpyFromSymbol(out, g_timeline, sizeof(unsigned long long) * 32));
+  unsigned long long z[32];
+  for (int i = 0; i < 32; ++i) z[i] = (i & 1) ? 0ull : ~0ull;
+  GOMIX_CUDA(cudaMemcpyToSymbol(g_timeline, z, sizeof(z)));
 }
 
 void debug_probes_univ(unsigned long long* out, bool reset) {

@@ -390,6 +390,7 @@ void launch_sum_ones(const uint32_t* stage, uint32_t R, uint64_t nv, uint32_t* o
 void debug_probes(unsigned long long* out, bool reset);
 void debug_probes_gen(unsigned long long* out, bool reset);
 void debug_probes_univ(unsigned long long* out, bool reset);
+void debug_timeline_univ(unsigned long long* out);  // gom_univ_tt_kernel launch timeline (probes builds)
 void debug_cta_probes(unsigned long long* out);
 void launch_philox_init(uint32_t* pop, uint64_t nv, uint32_t n, uint32_t Wp, uint64_t seed,
                         uint32_t rank, cudaStream_t s);
