@@ -311,6 +311,9 @@ struct gomix_gpu_engine {
   int univ_planes = 0;     // > 0: Philox groups run the bit-sliced lane-per-set kernel
   bool univ_tt = false;    // ... its truth-table variant (degree <= 4 plan records)
   uint32_t tt_chunks = 1;  // > 1: n > 128, rows processed in 4-word chunks (counted rows in `ones`)
+  unsigned int* chunk_done = nullptr;  // ... per-chunk CTA tickets of a launch
+  double* word_max = nullptr;          // ... per-word fitness maxima after the chunk commits
+  unsigned int* tail_ctr = nullptr;    // truth-table kernel: dynamic batch counters (one per chunk)
   bool univ_f64 = false;   // univariate, non-int32 weights, Philox: gom_univ_f64_kernel
   int f64_grid_cap = 1;
   int univ_grid_cap = 1;
@@ -615,6 +618,13 @@ struct gomix_gpu_engine {
       invalid("engine: the peer transport needs a univariate FOS with every variable in one set (use NCCL)");
     if (tt_chunks > 1 && R > 1 && !lite) invalid("engine: internal: chunked rows need the sharded row counts");
     if (lite || tt_chunks > 1) ones = dev_alloc<uint32_t>(allocs, nv);
+    tail_ctr = dev_alloc<unsigned int>(allocs, tt_chunks);
+    GOMIX_CUDA(cudaMemset(tail_ctr, 0, tt_chunks * sizeof(unsigned int)));
+    if (tt_chunks > 1) {
+      chunk_done = dev_alloc<unsigned int>(allocs, tt_chunks);
+      word_max = dev_alloc<double>(allocs, Wp);
+      GOMIX_CUDA(cudaMemset(chunk_done, 0, tt_chunks * sizeof(unsigned int)));
+    }
     if (lite) {
       ones_local = dev_alloc<uint32_t>(allocs, nv);
       if (!cfg.nccl_unique_id) ones_stage = dev_alloc<uint32_t>(allocs, (uint64_t)R * nv);
@@ -635,6 +645,7 @@ struct gomix_gpu_engine {
                           kCtlBytes - sizeof(DevCtl) + std::min(kImprInline, impr_cap) * sizeof(ImprRec)));
     GOMIX_CUDA(cudaMemset(pool, 0, (uint64_t)R * nv * Wp * 4));
     GOMIX_CUDA(cudaMemset(gsteps, 0, P->k * 8));
+    GOMIX_CUDA(cudaMemset(rank_cnt, 0, 2 * (uint64_t)R * 8));  // gathered at init before any group ran
     GOMIX_CUDA(cudaMemset(gcalls, 0, P->k * 8));
     GOMIX_CUDA(cudaMemset(dfit, 0, n * 8));
     GOMIX_CUDA(cudaMemset(dh1, 0, n * 8));
@@ -836,6 +847,7 @@ struct gomix_gpu_engine {
     e.R = R;
     e.rank = rank;
     e.peer = peer_on ? d_peer : nullptr;
+    e.word_max = nullptr;  // set by the chunked truth-table kernel itself
     e.n = (uint32_t)n;
     e.G = G;
     e.nparts = nparts;
@@ -860,6 +872,10 @@ struct gomix_gpu_engine {
     a.urec = P->urec ? P->urec + 2 * g0 : nullptr;
     a.ukey = P->ukey ? P->ukey + g0 : nullptr;
     a.uvr = P->uvr ? P->uvr + g0 : nullptr;
+    a.chunk_done = chunk_done;
+    a.tail = tail_ctr;
+    a.tail_per_chunk = tt_chunks > 1;
+    a.word_max = word_max;
     a.gmeta = P->gmeta ? P->gmeta + g0 : nullptr;
     a.wbits = P->wbits;
     a.G = (uint32_t)G;

@@ -212,9 +212,11 @@ static __device__ void note_improvement(const EpiArgs& a, double f) {
 // integer sums do not depend on which thread or CTA added what — the
 // float path is deterministic for any grid, within 1e-9 relative of the
 // reference's sums (north star).
-static __device__ void commit_local(const EpiArgs& a, double* s_fit, unsigned long long* s_h = nullptr) {
+static __device__ void commit_range(const EpiArgs& a, uint32_t s0, uint32_t s1, double* s_fit,
+                                    unsigned long long* s_h) {
   const uint32_t n = a.n;
-  for (uint32_t s = threadIdx.x; s < n; s += blockDim.x) {
+#pragma unroll 4
+  for (uint32_t s = s0 + threadIdx.x; s < s1; s += blockDim.x) {
     double f = a.fit[s];
     if (a.mode == 2) {
       for (uint32_t p = 0; p < a.G; ++p)
@@ -235,14 +237,9 @@ static __device__ void commit_local(const EpiArgs& a, double* s_fit, unsigned lo
     a.dh1[s] = 0;
     a.dh2[s] = 0;
   }
-  if (a.R > 1 && threadIdx.x == 0) {  // this rank's counters, all-gathered next
-    DevCtl* c = a.ctl;
-    a.rank_cnt[2 * a.rank] = c->grp_steps;
-    a.rank_cnt[2 * a.rank + 1] = c->grp_calls;
-    c->grp_steps = 0;
-    c->grp_calls = 0;
-  }
 }
+
+
 
 // Evaluator-call accounting (budget stop first, runtime.hpp:75-80), then the
 // elitist scan of engine_parallel.hpp:305-310 over all n_global members in
@@ -255,7 +252,8 @@ static __device__ void elitist_scan(const EpiArgs& a, const double* s_fit,
                                     const unsigned long long* s_h = nullptr) {
   DevCtl* c = a.ctl;
   const uint32_t n = a.n_global;
-  __shared__ double s_chunkmax[32];
+  const uint32_t nchunks = (n + 31u) / 32u;  // <= 128 (populations up to 4096)
+  __shared__ double s_chunkmax[128];
   __shared__ double s_cur, s_target;
   __shared__ unsigned long long s_ni, s_calls_now;
   __shared__ int32_t s_exact, s_has_target, s_stopped;
@@ -306,15 +304,22 @@ static __device__ void elitist_scan(const EpiArgs& a, const double* s_fit,
     s_has_target = has_target;
   }
   __syncthreads();
-  // chunk maxima let the serial scan skip chunks that cannot hold a record
+  // chunk maxima let the serial scan skip chunks that cannot hold a record:
+  // precomputed by the CTAs that committed the chunks (a.word_max), else
+  // one warp per chunk
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u, nwarps = blockDim.x >> 5;
   auto fit_at = [&](uint32_t s) { return (s_fit && s < kEpiSmemFit) ? s_fit[s] : a.fit_all[s]; };
-  for (uint32_t chunk = warp; chunk * 32u < n && chunk < 32; chunk += nwarps) {
-    const uint32_t s = chunk * 32u + lane;
-    double f = s < n ? fit_at(s) : -INFINITY;
+  if (a.word_max != nullptr && a.R == 1) {
+    for (uint32_t chunk = threadIdx.x; chunk < nchunks; chunk += blockDim.x) s_chunkmax[chunk] = __ldcg(a.word_max + chunk);
+  } else {
+#pragma unroll 4
+    for (uint32_t chunk = warp; chunk < nchunks; chunk += nwarps) {
+      const uint32_t s = chunk * 32u + lane;
+      double f = s < n ? fit_at(s) : -INFINITY;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) f = fmax(f, __shfl_xor_sync(0xFFFFFFFFu, f, o));
-    if (lane == 0) s_chunkmax[chunk] = f;
+      for (int o = 16; o > 0; o >>= 1) f = fmax(f, __shfl_xor_sync(0xFFFFFFFFu, f, o));
+      if (lane == 0) s_chunkmax[chunk] = f;
+    }
   }
   __syncthreads();
   if (warp == 0) {
@@ -328,7 +333,7 @@ static __device__ void elitist_scan(const EpiArgs& a, const double* s_fit,
     bool hit = false;
     for (uint32_t base = 0; base < n; base += 32u) {
       const uint32_t chunk = base >> 5;
-      if (chunk < 32 && !(s_chunkmax[chunk] > cur)) continue;  // better() implies >
+      if (!(s_chunkmax[chunk] > cur)) continue;  // better() implies >
       const uint32_t s = base + lane;
       const double f = s < n ? fit_at(s) : -INFINITY;
       uint32_t m = __ballot_sync(0xFFFFFFFFu, s < n && cmp_better(exact, f, cur));
@@ -368,18 +373,32 @@ static __device__ void elitist_scan(const EpiArgs& a, const double* s_fit,
   __syncthreads();
 }
 
+// After this rank's members are committed: the elitist scan (one GPU), or
+// the rank's counters for the exchange and — with the peer transport — the
+// exchange and the global scan in the same kernel (gom_peer.cuh; with NCCL
+// they follow the launch).
+static __device__ void epilogue_global(const EpiArgs& a, const double* s_fit, const unsigned long long* s_h) {
+  if (a.R == 1) {
+    elitist_scan(a, s_fit, s_h);
+    return;
+  }
+  if (threadIdx.x == 0) {  // this rank's counters, all-gathered next
+    DevCtl* c = a.ctl;
+    a.rank_cnt[2 * a.rank] = c->grp_steps;
+    a.rank_cnt[2 * a.rank + 1] = c->grp_calls;
+    c->grp_steps = 0;
+    c->grp_calls = 0;
+  }
+  __syncthreads();
+  if (a.peer != nullptr && peer_exchange(a)) elitist_scan(a, nullptr);
+}
+
 static __device__ void epilogue_body(const EpiArgs& a) {
   __shared__ double s_fit[kEpiSmemFit];              // this group's fitness, scanned without global loads
   __shared__ unsigned long long s_h[2 * kEpiSmemFit];  // ... and hashes (a new elitist's)
-  commit_local(a, a.R == 1 ? s_fit : nullptr, a.R == 1 ? s_h : nullptr);
+  commit_range(a, 0, a.n, a.R == 1 ? s_fit : nullptr, a.R == 1 ? s_h : nullptr);
   __syncthreads();
-  if (a.R == 1) {
-    elitist_scan(a, s_fit, s_h);
-  } else if (a.peer != nullptr) {
-    // sharded, peer transport: the exchange and the global scan happen here,
-    // in the same kernel (gom_peer.cuh); with NCCL they follow the launch
-    if (peer_exchange(a)) elitist_scan(a, nullptr);
-  }
+  epilogue_global(a, s_fit, s_h);
 }
 
 }  // namespace gomix_b200

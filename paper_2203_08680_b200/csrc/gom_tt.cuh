@@ -156,12 +156,36 @@ __device__ __forceinline__ void tt_batches(const GomArgs& a, const TtPart& part,
   const uint32_t n = a.n;
   const uint32_t batches = (G + 31u) / 32u;
   const uint32_t bstride = part.ctas * kUnivWarps;
-  for (uint32_t bt = warp * part.ctas + part.cta; bt < batches; bt += bstride) {
+  // Every warp takes the same number of batches statically (warp-major, so
+  // every SM gets the same mix); the remainder — less than one batch per
+  // warp — goes to whichever warps finish first, claimed from a counter:
+  // the CTAs that run slow (memory latency, accept-heavy sets) no longer
+  // set the launch's tail.
+  const uint32_t nstatic = batches / bstride;
+  const uint32_t dyn0 = nstatic * bstride;
+  unsigned int* tail = a.tail + (a.tail_per_chunk ? part.chunk : 0u);
+  uint32_t k = 0;
+  uint32_t bt = warp * part.ctas + part.cta;  // the caller prefetched this batch's records
+  if (nstatic == 0) {  // fewer batches than warps: every batch is claimed
+    uint32_t c = 0;
+    if (lane == 0) c = atomicAdd(tail, 1u);
+    bt = dyn0 + __shfl_sync(0xFFFFFFFFu, c, 0);
+    nx = tt_fetch(urec, ukey, G, bt * 32u + lane);
+  }
+  while (bt < batches) {
     const uint32_t p = bt * 32u + lane;
     const bool live = p < G;
     const uint4 ra = nx.ra, rc = nx.rc;
     const ulonglong2 zk = nx.zk;
-    nx = tt_fetch(urec, ukey, G, p + bstride * 32u);
+    uint32_t bt_next;
+    if (++k < nstatic) {
+      bt_next = bt + bstride;
+    } else {
+      uint32_t c = 0;
+      if (lane == 0) c = atomicAdd(tail, 1u);
+      bt_next = dyn0 + __shfl_sync(0xFFFFFFFFu, c, 0);
+    }
+    nx = tt_fetch(urec, ukey, G, bt_next * 32u + lane);
     const uint32_t v = ra.x;
     const uint32_t u[4] = {rc.x, rc.y, rc.z, rc.w};
     uint32_t x[WC], nb[4][WC];
@@ -347,6 +371,7 @@ __device__ __forceinline__ void tt_batches(const GomArgs& a, const TtPart& part,
       }
     }
     __syncwarp();
+    bt = bt_next;
   }
 }
 

@@ -484,6 +484,45 @@ __global__ void __launch_bounds__(kUnivWarps * 32, MINB) gom_univ_tt_kernel(cons
   }
   __syncthreads();
   timeline_mark(3);  // CTA flushed
+  const uint32_t chunks = a.Wp / (uint32_t)WC;
+  if (chunks > 1) {
+    // Rows in chunks (n > 128): the last CTA of every chunk commits that
+    // chunk's solutions and their per-word fitness maxima, so the group's
+    // last CTA only scans (the commit of up to 4096 solutions no longer
+    // runs serially in one CTA after the grid)
+    if (threadIdx.x == 0) {
+      __threadfence();
+      s_last = atomicAdd(&a.chunk_done[part.chunk], 1u) == part.ctas - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    commit_range(epi, part.cbase, part.cbase + part.n_chunk, nullptr, nullptr);
+    __syncthreads();
+    if (warp < Wp) {
+      const uint32_t s = part.cbase + warp * 32u + lane;
+      double f = s < n ? __ldcg(epi.fit + s) : -INFINITY;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) f = fmax(f, __shfl_xor_sync(0xFFFFFFFFu, f, o));
+      if (lane == 0 && part.cbase + warp * 32u < n) a.word_max[part.cbase / 32u + warp] = f;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      a.chunk_done[part.chunk] = 0;
+      a.tail[part.chunk] = 0;  // every CTA of the chunk is done claiming
+      __threadfence();
+      s_last = atomicAdd(&a.ctl->done, 1u) == chunks - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    timeline_mark(4);  // epilogue start (last chunk CTA)
+    epi.word_max = a.word_max;
+    epilogue_global(epi, nullptr, nullptr);
+    timeline_mark(5);  // epilogue end
+    if (threadIdx.x == 0) a.ctl->done = 0;
+    return;
+  }
   if (threadIdx.x == 0) {
     __threadfence();
     s_last = atomicAdd(&a.ctl->done, 1u) == gridDim.x - 1;
@@ -497,7 +536,10 @@ __global__ void __launch_bounds__(kUnivWarps * 32, MINB) gom_univ_tt_kernel(cons
   epilogue_body(epi);
   probe_last(a.exp_flags, 45);
   timeline_mark(5);  // epilogue end
-  if (threadIdx.x == 0) a.ctl->done = 0;
+  if (threadIdx.x == 0) {
+    a.ctl->done = 0;
+    a.tail[0] = 0;
+  }
 }
 
 // ---------------------------------------------------------------------------

@@ -143,6 +143,7 @@ struct EpiArgs {
   unsigned long long* rank_cnt;  // [R][steps, calls] of the current group
   uint32_t n_global, R, rank;
   const PeerArgs* peer;  // sharded, peer transport: the exchange runs inside the epilogue (gom_peer.cuh)
+  const double* word_max;  // per 32-solution word: max fitness after the commit (nullptr: the scan computes it)
 };
 
 // elitist snapshot / hashing kernels
@@ -200,6 +201,10 @@ struct GomArgs {
   uint32_t generation;
   uint64_t seed;
   EpiArgs epi;         // run by the last CTA
+  unsigned int* chunk_done;  // truth-table rows in chunks: per-chunk CTA tickets
+  unsigned int* tail;        // truth-table kernel: counters of the dynamically claimed batches
+  uint32_t tail_per_chunk;   // ... one per chunk (rows in chunks) or one per launch
+  double* word_max;          // ... and per-word maxima written by each chunk's last CTA
   int32_t slot;                 // >= 0: group = order[slot] (graph path)
   uint32_t exp_flags;           // latency studies only (GOMIX_EXP env): 32 = %globaltimer probes
   const uint32_t* order;
