@@ -362,6 +362,9 @@ struct gomix_gpu_engine {
   static constexpr uint64_t kImprInline = 64;  // improvements copied back with every read_ctl
   static constexpr size_t kCtlBytes = (sizeof(DevCtl) + 63) / 64 * 64;  // control block, then the log
   ImprRec* h_impr = nullptr;                   // pinned [kImprInline], right after *h_ctl
+  DevCtl* d_hctl = nullptr;                    // device view of h_ctl (mapped)
+  volatile unsigned long long* h_seq = nullptr;  // publish sequence, after the inline log
+  unsigned long long pub_seq = 0;
   unsigned long long* gsteps = nullptr;
   unsigned long long* gcalls = nullptr;
   ImprRec* impr = nullptr;  // right after *ctl
@@ -629,7 +632,12 @@ struct gomix_gpu_engine {
       ones_local = dev_alloc<uint32_t>(allocs, nv);
       if (!cfg.nccl_unique_id) ones_stage = dev_alloc<uint32_t>(allocs, (uint64_t)R * nv);
     }
-    GOMIX_CUDA(cudaMallocHost(&h_ctl, kCtlBytes + kImprInline * sizeof(ImprRec)));
+    // mapped: the synchronous generation path has the device write it in place (publish_ctl)
+    GOMIX_CUDA(cudaHostAlloc(&h_ctl, kCtlBytes + kImprInline * sizeof(ImprRec) + 64, cudaHostAllocMapped));
+    GOMIX_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_hctl), h_ctl, 0));
+    h_seq = reinterpret_cast<volatile unsigned long long*>(reinterpret_cast<char*>(h_ctl) + kCtlBytes +
+                                                          kImprInline * sizeof(ImprRec));
+    *h_seq = 0;
     h_impr = reinterpret_cast<ImprRec*>(reinterpret_cast<char*>(h_ctl) + kCtlBytes);
     GOMIX_CUDA(cudaHostAlloc(&h_begin, sizeof(BeginArgs), cudaHostAllocMapped));
     GOMIX_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_begin), h_begin, 0));
@@ -777,6 +785,28 @@ struct gomix_gpu_engine {
     if (!sync_first) b.gen = 0;  // (unused by the graph kernels; keeps queued reads byte-identical)
     *h_begin = b;
     std::atomic_thread_fence(std::memory_order_release);
+  }
+
+  // Synchronous read-back after a generation: the device writes the control
+  // block and inline log into h_ctl (mapped) and then bumps the sequence;
+  // the host spins on it (a device-to-host copy plus a stream synchronise
+  // cost microseconds per generation).  A failed stream still surfaces: the
+  // spin checks the stream every few thousand polls.
+  void read_ctl_published() {
+    const size_t bytes = kCtlBytes + std::min(kImprInline, impr_cap) * sizeof(ImprRec);
+    launch_publish_ctl(ctl, d_hctl, (bytes + 15) / 16 * 16,
+                       const_cast<unsigned long long*>(reinterpret_cast<volatile unsigned long long*>(
+                           reinterpret_cast<char*>(d_hctl) + kCtlBytes + kImprInline * sizeof(ImprRec))),
+                       ++pub_seq, stream);
+    ++launches;
+    for (uint64_t spins = 1; *h_seq < pub_seq; ++spins) {
+      if ((spins & 4095u) == 0) {
+        const cudaError_t e = cudaStreamQuery(stream);
+        if (e != cudaSuccess && e != cudaErrorNotReady) GOMIX_CUDA(e);
+      }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    ctl_stale = false;
   }
 
   void read_ctl() {
@@ -1319,7 +1349,7 @@ struct gomix_gpu_engine {
       else
         launch_generation_graph();
       if (fi_on) fi_after_generation();
-      read_ctl();
+      read_ctl_published();
       fill_stats(out);
       if (!h_ctl->stop) ++generation;
       return;

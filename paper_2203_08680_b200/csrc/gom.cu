@@ -752,6 +752,25 @@ void launch_order(const BeginArgs* d_b, const OrderArgs& o, cudaStream_t s) {
   GOMIX_CUDA(cudaGetLastError());
 }
 
+// The control block and the first improvement-log entries, written straight
+// into mapped pinned host memory, then a sequence number (system-scope
+// release): a synchronous call spins on that number instead of a device-to-
+// host copy plus a stream synchronisation.
+__global__ void publish_ctl_kernel(const uint4* src, uint4* dst, uint32_t words, unsigned long long* seq_dst,
+                                   unsigned long long seq) {
+  for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(seq_dst), "l"(seq) : "memory");
+}
+
+void launch_publish_ctl(const void* ctl, void* host_dst, size_t bytes, unsigned long long* host_seq,
+                        unsigned long long seq, cudaStream_t s) {
+  publish_ctl_kernel<<<1, 128, 0, s>>>(static_cast<const uint4*>(ctl), static_cast<uint4*>(host_dst),
+                                       (uint32_t)(bytes / 16), host_seq, seq);
+  GOMIX_CUDA(cudaGetLastError());
+}
+
 void launch_global_epilogue(const EpiArgs& a, cudaStream_t s) {
   global_epilogue_kernel<<<1, 256, 0, s>>>(a);
   GOMIX_CUDA(cudaGetLastError());

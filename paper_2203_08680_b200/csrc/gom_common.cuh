@@ -39,6 +39,15 @@ __device__ __forceinline__ void probe_last(uint32_t flags, uint32_t i) {
 #endif
 }
 
+// Last-CTA ticket with release / acquire semantics in one instruction (the
+// CTA's earlier writes are visible to whoever draws the last ticket, and the
+// last one sees everyone's): replaces __threadfence() + atomicAdd.
+__device__ __forceinline__ unsigned int ticket_acq_rel(unsigned int* p) {
+  unsigned int old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(p) : "memory");
+  return old;
+}
+
 // Launch timeline (probes builds only): for point i, the earliest and latest
 // CTA to reach it (thread 0), as %globaltimer ns; read and reset through
 // gomix_debug_timeline.

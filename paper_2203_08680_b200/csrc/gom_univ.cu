@@ -523,10 +523,7 @@ __global__ void __launch_bounds__(kUnivWarps * 32, MINB) gom_univ_tt_kernel(cons
     if (threadIdx.x == 0) a.ctl->done = 0;
     return;
   }
-  if (threadIdx.x == 0) {
-    __threadfence();
-    s_last = atomicAdd(&a.ctl->done, 1u) == gridDim.x - 1;
-  }
+  if (threadIdx.x == 0) s_last = ticket_acq_rel(&a.ctl->done) == gridDim.x - 1;
   __syncthreads();
   probe(a.exp_flags, 43);
   if (!s_last) return;

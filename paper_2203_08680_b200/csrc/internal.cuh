@@ -378,6 +378,8 @@ void launch_order(const BeginArgs* d_b, const OrderArgs& o, cudaStream_t s);
 void prepare_gom(bool univariate, bool i32, int wpt, bool team, size_t smem);
 void launch_init_epilogue(const EpiArgs& a, cudaStream_t s);
 void launch_global_epilogue(const EpiArgs& a, cudaStream_t s);
+void launch_publish_ctl(const void* ctl, void* host_dst, size_t bytes, unsigned long long* host_seq,
+                        unsigned long long seq, cudaStream_t s);
 void launch_hash_population(const SnapArgs& a, cudaStream_t s);
 void launch_finalize_elitist(const SnapArgs& a, cudaStream_t s);
 void launch_external_elitist(const SnapArgs& a, double fitness, cudaStream_t s);
