@@ -704,7 +704,7 @@ struct gomix_gpu_engine {
   void launch_generation_persistent() {
     GomArgs a = gom_args(0, max_group, false, -1);
     a.epi = epi_args(0, 0, 0);
-    GenArgs ga{d_begin, (uint32_t)P->k, d_order, gen_dfit, gen_dh, gen_cnt, gen_bar, gen_sib, (uint32_t)max_group};
+    GenArgs ga{*h_begin, (uint32_t)P->k, d_order, gen_dfit, gen_dh, gen_cnt, gen_bar, gen_sib, (uint32_t)max_group};
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (flags & GOMIX_FLAG_TIME_KERNELS) {
       e0 = take_event();

@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(LEAN ? 256 : (TEAM ? 32 * TW : 256), LEAN ? 3 
   const uint32_t lean_w = LEAN ? gwarp % Wp : 0u;  // the grid's warp count is a multiple of Wp
   // solution of this thread's word j
   auto sol = [&](int j) -> uint32_t { return LEAN ? lean_w * 32u + lane : (wit + tw * (uint32_t)j) * 32u + lane; };
-  const BeginArgs b = *ga.begin;
+  const BeginArgs& b = ga.begin;
   DevCtl* c = a.ctl;
   const uint32_t gen = *(volatile unsigned int*)&c->gen_counter;
   const uint32_t buf0 = *(volatile unsigned int*)&c->gen_buf;

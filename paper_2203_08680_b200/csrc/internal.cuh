@@ -252,9 +252,15 @@ struct OrderArgs {
 constexpr uint32_t kGenMaxN = 256;  // members kept in shared memory by every CTA
 constexpr uint32_t kGenMaxK = 256;  // colour groups
 constexpr uint32_t kAccStride = 32;  // persistent kernel accumulators: one per 256-byte line
-struct BeginArgs;
+struct BeginArgs {
+  DevCtl* ctl;
+  int32_t has_budget, has_target, exact;
+  double max_evals, q, target;
+  unsigned long long calls_before;
+  uint32_t gen;  // host generation (direct path keeps the device counter in step)
+};
 struct GenArgs {
-  const BeginArgs* begin;
+  BeginArgs begin;  // by value: the persistent kernel is launched directly, never captured
   uint32_t k;
   uint32_t* order;             // this generation's group order (written back for inspection)
   long long* dfit;             // [3][n] fitness deltas
@@ -265,15 +271,9 @@ struct GenArgs {
   uint32_t sib_stride;         // largest colour group
 };
 
-// Per-call control values, passed as kernel parameters (captured at launch,
-// so host calls can be queued back to back without host syncs).
-struct BeginArgs {
-  DevCtl* ctl;
-  int32_t has_budget, has_target, exact;
-  double max_evals, q, target;
-  unsigned long long calls_before;
-  uint32_t gen;  // host generation (direct path keeps the device counter in step)
-};
+// BeginArgs (above): per-call control values, passed as kernel parameters
+// (captured at launch, so host calls can be queued back to back without host
+// syncs) or read in place from mapped host memory by the graph's begin kernel.
 
 // -------------------------------------------------------------------------
 // errors

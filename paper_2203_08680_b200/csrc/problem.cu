@@ -630,7 +630,12 @@ void build_problem_device_impl(Problem& P, const int32_t* given_colour, const in
       // left (e.g. neighbourhood sets in index order: one chain of m links)
       unsigned long long* coloured = S.get<unsigned long long>(1);
       GOMIX_CUDA(cudaMemset(coloured, 0, sizeof(unsigned long long)));
-      for (int batch = 0; batch < kJpBatches && done < m; ++batch) {
+      // GOMIX_JP_BATCHES (A/B measurements): 0 = the dataflow kernel alone
+      static const int jp_batches = [] {
+        const char* e = std::getenv("GOMIX_JP_BATCHES");
+        return e ? std::atoi(e) : kJpBatches;
+      }();
+      for (int batch = 0; batch < jp_batches && done < m; ++batch) {
         for (int r = 0; r < 16; ++r)
           jp_round_kernel<<<blocks_for(m), 256>>>(lmig_off, lmig_adj, rank, colour, m, coloured);
         GOMIX_CUDA(cudaGetLastError());
