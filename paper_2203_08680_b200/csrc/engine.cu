@@ -967,8 +967,12 @@ struct gomix_gpu_engine {
     } else if (univ_planes && !with_tape) {
       const uint64_t per = (uint64_t)univ_sliced_sets_per_cta();
       // chunked rows: tt_chunks CTAs per set range, one per chunk
-      const uint64_t slots = std::max<uint64_t>(1, (uint64_t)univ_grid_cap / tt_chunks);
-      const int g = (int)(tt_chunks * std::max<uint64_t>(1, std::min<uint64_t>((G + per - 1) / per, slots)));
+      // chunked rows: every chunk's CTAs split its sets; the grid stays a
+      // multiple of the SM count when the work fills it (chunks then differ
+      // by at most one CTA), and covers every chunk at least once
+      const uint64_t want = tt_chunks * ((G + per - 1) / per);
+      const int g = (int)std::max<uint64_t>(tt_chunks, std::min<uint64_t>(std::max<uint64_t>(1, want),
+                                                                          (uint64_t)univ_grid_cap));
       a.epi = epi_args(group, (uint32_t)G, (uint32_t)g);
       // graph path, groups after the first: programmatic dependent launch
       // (truth-table kernel only: it waits on griddepcontrol before reading

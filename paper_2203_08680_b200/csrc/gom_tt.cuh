@@ -114,7 +114,8 @@ __device__ __forceinline__ TtNext tt_fetch(const uint4* urec, const ulonglong2* 
 // (n <= 32 WC): every CTA takes whole rows.  Wider rows (n > 128): the row is
 // cut into chunks of WC words and CTA i takes chunk i % chunks of the sets
 // assigned to CTA slot i / chunks; a CTA's per-solution accumulators then
-// cover only its chunk's 32 WC solutions.
+// cover only its chunk's 32 WC solutions.  The grid is a whole number of
+// CTAs per SM (every SM equally loaded), so chunks may differ by one CTA.
 struct TtPart {
   uint32_t chunk;   // this CTA's chunk of every row
   uint32_t cta;     // this CTA's slot among the CTAs of its chunk
@@ -129,7 +130,7 @@ __device__ __forceinline__ TtPart tt_part(const GomArgs& a) {
   const uint32_t chunks = a.Wp / (uint32_t)WC;
   t.chunk = blockIdx.x % chunks;
   t.cta = blockIdx.x / chunks;
-  t.ctas = gridDim.x / chunks;
+  t.ctas = (gridDim.x - t.chunk + chunks - 1) / chunks;  // the grid need not be a multiple of chunks
   t.cbase = t.chunk * (uint32_t)WC * 32u;
   t.n_chunk = min((uint32_t)WC * 32u, a.n - min(a.n, t.cbase));
   return t;
