@@ -95,18 +95,40 @@ def packed_hash(packed: np.ndarray) -> np.uint64:
     return np.frombuffer(hashlib.sha256(np.ascontiguousarray(packed).tobytes()).digest()[:8], np.uint64)[0]
 
 
+# Float weights at BASELINE C4 size: random d-regular graphs from this repo's
+# generator (the reference has none), handed to the reference as an edge-list
+# file: (name, vertices, degree, generator seed, fos, n, seed, gens).
+LIGHT_REGULAR_CASES = [
+    ("c4_d4", 100000, 4, 4, "univariate", 128, 5, 2),
+    ("c4_d8_small", 20000, 8, 8, "univariate", 64, 6, 3),
+]
+
+
 def make_light(cases):
     with tempfile.TemporaryDirectory() as tmp:
-        for name, w, h, weights, iseed, fos, n, seed, gens in cases:
+        for case in cases:
+            name = case[0]
+            if case in LIGHT_REGULAR_CASES:
+                _, nv_, deg, gseed, fos, n, seed, gens = case
+                import paper_2203_08680_b200 as G
+
+                inst = G.generate_regular(nv_, deg, ("real",), seed=gseed)
+                path = os.path.join(tmp, name + ".txt")
+                G.save_edge_list(path, inst)
+                src = ["--edges", path]
+                w = h = iseed = 0
+                weights = "real"
+            else:
+                _, w, h, weights, iseed, fos, n, seed, gens = case
+                src = ["--torus", w, h, "--weights", weights, "--inst-seed", iseed]
             out = os.path.join(tmp, name + ".bin")
-            d = O.run_ref("run", "--torus", w, h, "--weights", weights, "--inst-seed", iseed, "--fos", fos,
-                          "--n", n, "--seed", seed, "--gens", gens, "--workers", os.cpu_count() or 4, "--light",
-                          out=out, timeout=7200)
+            d = O.run_ref("run", *src, "--fos", fos, "--n", n, "--seed", seed, "--gens", gens,
+                          "--workers", os.cpu_count() or 4, "--light", out=out, timeout=7200)
             nv = int(d["num_vertices"][0])
             per = (n * nv + 7) // 8
             packed = d["packed"].reshape(gens, per)
-            lo, hi = (int(x) for x in weights.split(":")[1:]) if weights != "unit" else (0, 0)
             f = {"torus": np.array([w, h], np.uint64), "weights": np.array([weights]),
+                 "regular": np.array(case[1:4] if case in LIGHT_REGULAR_CASES else [0, 0, 0], np.uint64),
                  "inst_seed": np.array([iseed], np.uint64), "fos_kind": np.array([fos]),
                  "n": np.array([n], np.uint64), "seed": np.array([seed], np.uint64),
                  "gens": np.array([gens], np.uint64), "num_vertices": d["num_vertices"],
@@ -215,6 +237,6 @@ def main():
 if __name__ == "__main__":
     if "--light" in sys.argv[1:]:
         names = [a for a in sys.argv[1:] if not a.startswith("--")]
-        make_light([c for c in LIGHT_CASES if not names or c[0] in names])
+        make_light([c for c in LIGHT_CASES + LIGHT_REGULAR_CASES if not names or c[0] in names])
     else:
         main()
