@@ -405,6 +405,16 @@ __global__ void __launch_bounds__(kUnivWarps * 32, MINB) gom_univ_tt_kernel(cons
   // order read above, which the generation's begin kernel wrote before the
   // previous launch started): in flight before the dependency wait
   const TtNext first = tt_fetch(urec, ukey, G, (warp * part.ctas + part.cta) * 32u + lane);
+  // this CTA's accumulators: shared memory only, also before the wait
+  for (uint32_t i = threadIdx.x; i < Wp * 32u; i += blockDim.x) {
+    s_dfit[i] = 0;
+#pragma unroll
+    for (int q = 0; q < kUnivWarps; ++q) sh.wh[q][i] = make_ulonglong2(0ull, 0ull);
+  }
+  if (threadIdx.x == 0) {
+    s_steps = 0;
+    s_calls = 0;
+  }
   // programmatic dependent launch (graph path): everything below reads what
   // the previous group's launch wrote (population, control block, hashes)
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -427,15 +437,6 @@ __global__ void __launch_bounds__(kUnivWarps * 32, MINB) gom_univ_tt_kernel(cons
     const uint32_t m = __ballot_sync(0xFFFFFFFFu, sw < n && hs1 == eh1 && hs2 == eh2);
     if (lane == 0) s_elit[warp] = m;
   }
-  for (uint32_t i = threadIdx.x; i < Wp * 32u; i += blockDim.x) {
-    s_dfit[i] = 0;
-#pragma unroll
-    for (int q = 0; q < kUnivWarps; ++q) sh.wh[q][i] = make_ulonglong2(0ull, 0ull);
-  }
-  if (threadIdx.x == 0) {
-    s_steps = 0;
-    s_calls = 0;
-  }
   __syncthreads();
   probe(a.exp_flags, 41);
   timeline_mark(1);  // prologue done
@@ -443,7 +444,8 @@ __global__ void __launch_bounds__(kUnivWarps * 32, MINB) gom_univ_tt_kernel(cons
   tt_batches<B, WC>(a, part, urec, ukey, G, first, s_elit, s_dfit, sh, esrc, ever_cur, lane, warp, steps, calls);
 
   probe(a.exp_flags, 42);
-  timeline_mark(2);  // warp 0's batches done (it waits for this grid's
+  timeline_mark(2);  // warp 0's batches done
+  // the next group's launch may start its prologue (it waits for this grid's
   // completion before touching anything written here)
   asm volatile("griddepcontrol.launch_dependents;");
   {

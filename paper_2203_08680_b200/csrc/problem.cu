@@ -11,6 +11,7 @@
 // same function computed in parallel (Jones-Plassmann with that priority);
 // here it runs as a dataflow kernel (wp_dataflow_kernel).  So the groups, and
 // with them replay parity, are identical to the reference's.
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
 
@@ -21,6 +22,7 @@
 #include <cmath>
 #include <cstring>
 #include <numeric>
+#include <string>
 
 #include <map>
 #include <mutex>
@@ -29,6 +31,7 @@
 #include "internal.cuh"
 
 namespace gomix_b200 {
+namespace cg = cooperative_groups;
 
 // ---- device allocator (internal.cuh) -------------------------------------------
 // Stream-ordered allocation from each device's default memory pool, with a
@@ -240,6 +243,71 @@ __global__ void jp_round_kernel(const int64_t* off, const uint32_t* adj, const u
   if (mine) atomicAdd(coloured, mine);
 }
 
+// Welsh-Powell level by level (Kahn's order on the "lower-ranked neighbour"
+// DAG): a vertex's colour depends only on its lower-ranked neighbours', so
+// any topological order gives exactly the sequential greedy's colouring
+// (scheduling.hpp:85-114).  pending[v] = lower-ranked neighbours not yet
+// coloured; level 0 = the vertices with none.
+__global__ void kahn_init_kernel(const int64_t* off, const uint32_t* adj, const uint32_t* rank, uint64_t m,
+                                 uint32_t* pending, uint32_t* frontier, unsigned int* count) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < m; v += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t rv = rank[v];
+    uint32_t c = 0;
+    for (int64_t t = off[v]; t < off[v + 1]; ++t) c += rank[adj[t]] < rv ? 1u : 0u;
+    pending[v] = c;
+    if (c == 0) frontier[atomicAdd(count, 1u)] = (uint32_t)v;
+  }
+}
+
+// One cooperative grid walks the levels: colour every vertex of the current
+// level (smallest colour its lower-ranked neighbours leave free), release its
+// higher-ranked neighbours into the next level, grid barrier.  Level counts
+// rotate over three slots (read at L, appended at L + 1, cleared at L + 2).
+// Stops after max_levels; whatever is left (long chains) goes to the
+// dataflow kernel.  count[3] = levels run, count[4] = vertices coloured.
+__global__ void kahn_levels_kernel(const int64_t* off, const uint32_t* adj, const uint32_t* rank, int32_t* colour,
+                                   uint32_t* pending, uint32_t* fr0, uint32_t* fr1, uint32_t* fr2,
+                                   unsigned int* count, uint32_t max_levels) {
+  cg::grid_group grid = cg::this_grid();
+  uint32_t* fr[3] = {fr0, fr1, fr2};
+  const uint64_t gtid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t gsize = (uint64_t)gridDim.x * blockDim.x;
+  unsigned long long coloured = 0;
+  uint32_t level = 0;
+  for (; level < max_levels; ++level) {
+    const uint32_t cur = level % 3u, nxt = (level + 1u) % 3u, old = (level + 2u) % 3u;
+    const uint32_t n_cur = *(volatile unsigned int*)&count[cur];
+    if (n_cur == 0) break;
+    if (gtid == 0) count[old] = 0;
+    for (uint64_t i = gtid; i < n_cur; i += gsize) {
+      const uint32_t v = fr[cur][i];
+      const uint32_t rv = rank[v];
+      int32_t c = -1;
+      for (int32_t base = 0; c < 0; base += 64) {
+        uint64_t used = 0;
+        for (int64_t t = off[v]; t < off[v + 1]; ++t) {
+          const uint32_t j = adj[t];
+          if (rank[j] < rv) {
+            const int32_t cj = __ldcg(colour + j);
+            if (cj >= base && cj < base + 64) used |= 1ull << (cj - base);
+          }
+        }
+        if (~used) c = base + __ffsll((long long)~used) - 1;
+      }
+      colour[v] = c;
+      ++coloured;
+      for (int64_t t = off[v]; t < off[v + 1]; ++t) {
+        const uint32_t u = adj[t];
+        if (rank[u] > rv && atomicSub(&pending[u], 1u) == 1u) fr[nxt][atomicAdd(&count[nxt], 1u)] = u;
+      }
+    }
+    __threadfence();
+    grid.sync();
+  }
+  if (coloured) atomicAdd(reinterpret_cast<unsigned long long*>(count + 4), coloured);
+  if (gtid == 0) count[3] = level;
+}
+
 // Welsh-Powell as a dataflow: the warp holding the vertex of rank r colours
 // it as soon as every lower-ranked neighbour is coloured, with the smallest
 // colour none of them uses — exactly the sequential greedy (scheduling.hpp:
@@ -250,6 +318,7 @@ __global__ void jp_round_kernel(const int64_t* off, const uint32_t* adj, const u
 // shared memory (m <= kWpSmemMax); otherwise colours in global memory.
 constexpr uint64_t kWpSmemMax = 100000;
 constexpr int kJpBatches = 256;  // x 16 rounds before switching to the dataflow kernel
+constexpr uint32_t kKahnMaxLevels = 8192;  // levels before the dataflow kernel takes the rest
 constexpr uint32_t kWpUncoloured = 0xFFFFu;
 
 // Welsh-Powell as a dataflow: a vertex's warp spins (volatile loads) until
@@ -625,21 +694,51 @@ void build_problem_device_impl(Problem& P, const int32_t* given_colour, const in
       wp_dataflow_kernel<true><<<1, 1024, sm>>>(lmig_off, lmig_adj, rank, key_sorted, m, colour);
       GOMIX_CUDA(cudaGetLastError());
     } else {
-      // Jones-Plassmann rounds while the graph is wide (grids, univariate:
-      // ~2W rounds), then the dataflow kernel for whatever long chains are
-      // left (e.g. neighbourhood sets in index order: one chain of m links)
-      unsigned long long* coloured = S.get<unsigned long long>(1);
-      GOMIX_CUDA(cudaMemset(coloured, 0, sizeof(unsigned long long)));
-      // GOMIX_JP_BATCHES (A/B measurements): 0 = the dataflow kernel alone
-      static const int jp_batches = [] {
-        const char* e = std::getenv("GOMIX_JP_BATCHES");
-        return e ? std::atoi(e) : kJpBatches;
+      // Kahn levels in one cooperative grid while the levels are wide
+      // (grids, univariate: ~2W levels), then the dataflow kernel for
+      // whatever long chains are left (e.g. neighbourhood sets in index
+      // order: one chain of m links).  GOMIX_COLOUR=jp: Jones-Plassmann
+      // rounds instead (round 1's scheme, A/B measurements).
+      static const bool use_jp = [] {
+        const char* e = std::getenv("GOMIX_COLOUR");
+        return e && std::string(e) == "jp";
       }();
-      for (int batch = 0; batch < jp_batches && done < m; ++batch) {
-        for (int r = 0; r < 16; ++r)
-          jp_round_kernel<<<blocks_for(m), 256>>>(lmig_off, lmig_adj, rank, colour, m, coloured);
+      if (!use_jp) {
+        uint32_t* pending = S.get<uint32_t>(m);
+        uint32_t* fr0 = S.get<uint32_t>(m);
+        uint32_t* fr1 = S.get<uint32_t>(m);
+        uint32_t* fr2 = S.get<uint32_t>(m);
+        unsigned int* count = S.get<unsigned int>(6);  // 3 level slots, levels, coloured (u64)
+        GOMIX_CUDA(cudaMemset(count, 0, 6 * sizeof(unsigned int)));
+        kahn_init_kernel<<<blocks_for(m), 256>>>(lmig_off, lmig_adj, rank, m, pending, fr0, count);
         GOMIX_CUDA(cudaGetLastError());
-        GOMIX_CUDA(cudaMemcpy(&done, coloured, sizeof(done), cudaMemcpyDeviceToHost));
+        int dev = 0, sms = 0, per = 0;
+        GOMIX_CUDA(cudaGetDevice(&dev));
+        GOMIX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        GOMIX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kahn_levels_kernel, 256, 0));
+        static const int kahn_grid = [] {  // GOMIX_KAHN_GRID: CTAs of the level walk (A/B)
+          const char* e = std::getenv("GOMIX_KAHN_GRID");
+          return e ? std::atoi(e) : 0;
+        }();
+        // one CTA per SM: a level costs its dependent memory round trips, not
+        // threads (measured: 18 ms at C3 for 148 CTAs as for 4, 21 ms for 296)
+        const int grid = std::max(1, std::min(kahn_grid > 0 ? kahn_grid : sms, per * sms));
+        uint32_t max_levels = kKahnMaxLevels;
+        void* args[] = {(void*)&lmig_off, (void*)&lmig_adj, (void*)&rank, (void*)&colour, (void*)&pending,
+                        (void*)&fr0, (void*)&fr1, (void*)&fr2, (void*)&count, (void*)&max_levels};
+        GOMIX_CUDA(cudaLaunchCooperativeKernel((void*)kahn_levels_kernel, dim3(grid), dim3(256), args, 0, nullptr));
+        unsigned long long got = 0;
+        GOMIX_CUDA(cudaMemcpy(&got, count + 4, sizeof(got), cudaMemcpyDeviceToHost));
+        done = got;
+      } else {
+        unsigned long long* coloured = S.get<unsigned long long>(1);
+        GOMIX_CUDA(cudaMemset(coloured, 0, sizeof(unsigned long long)));
+        for (int batch = 0; batch < kJpBatches && done < m; ++batch) {
+          for (int r = 0; r < 16; ++r)
+            jp_round_kernel<<<blocks_for(m), 256>>>(lmig_off, lmig_adj, rank, colour, m, coloured);
+          GOMIX_CUDA(cudaGetLastError());
+          GOMIX_CUDA(cudaMemcpy(&done, coloured, sizeof(done), cudaMemcpyDeviceToHost));
+        }
       }
     }
     if ((m > kWpSmemMax || maxdeg >= kWpUncoloured) && done < m) {

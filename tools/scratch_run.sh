@@ -1,3 +1,3 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_replay_full.py -q --timeout 600 -p no:cacheprovider > gpurun_out/r2t_tests.txt 2>&1
+for g in 0 148 64 16 4 1; do echo "== grid $g"; GOMIX_KAHN_GRID=$g GOMIX_TRACE_BUILD=1 timeout 300 python tools/prof_build.py 2>&1 | grep -E "colouring|build [0-9]" | tail -2; done > gpurun_out/r2v_build.txt 2>&1
