@@ -974,10 +974,11 @@ struct gomix_gpu_engine {
       const int g = (int)std::max<uint64_t>(tt_chunks, std::min<uint64_t>(std::max<uint64_t>(1, want),
                                                                           (uint64_t)univ_grid_cap));
       a.epi = epi_args(group, (uint32_t)G, (uint32_t)g);
-      // graph path, groups after the first: programmatic dependent launch
+      // graph path: programmatic dependent launches (the first group after
+      // the begin kernel, later groups after the previous group)
       // (truth-table kernel only: it waits on griddepcontrol before reading
       // the previous group's results)
-      launch_univ_sliced(a, univ_planes, (int)Wp, univ_tt, g, st, univ_tt && slot > 0);
+      launch_univ_sliced(a, univ_planes, (int)Wp, univ_tt, g, st, univ_tt && slot >= 0);
     } else {
       a.epi = epi_args(group, (uint32_t)G, (uint32_t)grid);
       launch_gom(a, P->univariate, P->i32, (int)wpt, tw > 1, grid, (int)block, smem, st);

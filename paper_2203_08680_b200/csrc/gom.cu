@@ -478,6 +478,9 @@ constexpr uint32_t kTagOrder = 0x4F524400u;  // "ORD"
 // Graph path: reset the per-call block and draw this generation's group
 // order (Fisher-Yates, engine_parallel.hpp:291) from the counter-based stream.
 __global__ void begin_generation_kernel(const BeginArgs* bp, const OrderArgs o) {
+  // the first group's launch may start now: it waits for this kernel's
+  // completion before reading the order or the control block
+  asm volatile("griddepcontrol.launch_dependents;");
   const BeginArgs b = *bp;  // criteria uploaded before each graph launch
   DevCtl* c = b.ctl;
   c->stop = 0;

@@ -392,20 +392,7 @@ __global__ void __launch_bounds__(kUnivWarps * 32, MINB) gom_univ_tt_kernel(cons
   const uint4* urec = a.urec;
   const ulonglong2* ukey = a.ukey;
   EpiArgs epi = a.epi;
-  if (a.slot >= 0) {  // graph path: this launch's group comes from the device-side order
-    const uint32_t gi = a.order[a.slot];
-    const GroupDesc d = a.groups[gi];
-    G = d.G;
-    urec += 2u * (size_t)d.g0;
-    ukey += d.g0;
-    epi.group = gi;
-    epi.G = G;
-  }
-  // the plan records of the warp's first batch (static data, like the group
-  // order read above, which the generation's begin kernel wrote before the
-  // previous launch started): in flight before the dependency wait
-  const TtNext first = tt_fetch(urec, ukey, G, (warp * part.ctas + part.cta) * 32u + lane);
-  // this CTA's accumulators: shared memory only, also before the wait
+  // this CTA's accumulators: shared memory only, before any dependency wait
   for (uint32_t i = threadIdx.x; i < Wp * 32u; i += blockDim.x) {
     s_dfit[i] = 0;
 #pragma unroll
@@ -415,9 +402,25 @@ __global__ void __launch_bounds__(kUnivWarps * 32, MINB) gom_univ_tt_kernel(cons
     s_steps = 0;
     s_calls = 0;
   }
-  // programmatic dependent launch (graph path): everything below reads what
-  // the previous group's launch wrote (population, control block, hashes)
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // Programmatic dependent launches (graph path): the first group's launch
+  // follows the begin kernel, which writes this generation's group order, so
+  // it waits before reading it; later groups' launches read the order (written
+  // before the previous launch could start) and prefetch their first batch's
+  // plan records before waiting for the previous group.
+  if (a.slot == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (a.slot >= 0) {  // graph path: this launch's group comes from the device-side order
+    const uint32_t gi = a.order[a.slot];
+    const GroupDesc d = a.groups[gi];
+    G = d.G;
+    urec += 2u * (size_t)d.g0;
+    ukey += d.g0;
+    epi.group = gi;
+    epi.G = G;
+  }
+  const TtNext first = tt_fetch(urec, ukey, G, (warp * part.ctas + part.cta) * 32u + lane);
+  // everything below reads what the previous group's launch wrote
+  // (population, control block, hashes)
+  if (a.slot != 0) asm volatile("griddepcontrol.wait;" ::: "memory");
   // the control block and this warp's hashes in one round trip, then the stop check
   const int32_t stopped = *(volatile int32_t*)&a.ctl->stop;
   const unsigned long long eh1 = a.ctl->eh1, eh2 = a.ctl->eh2;

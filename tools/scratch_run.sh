@@ -1,3 +1,4 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-for g in 0 148 64 16 4 1; do echo "== grid $g"; GOMIX_KAHN_GRID=$g GOMIX_TRACE_BUILD=1 timeout 300 python tools/prof_build.py 2>&1 | grep -E "colouring|build [0-9]" | tail -2; done > gpurun_out/r2v_build.txt 2>&1
+timeout 1500 python -m pytest tests -m gpu -q --timeout 900 -p no:cacheprovider > gpurun_out/r2w_gputest.txt 2>&1
+for i in 1 2; do timeout 600 python bench.py --ttt-seconds 0 --no-cpu-baseline > gpurun_out/r2w_bench$i.json 2> gpurun_out/r2w_bench$i.err; done
