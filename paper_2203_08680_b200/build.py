@@ -27,16 +27,20 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, probes: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, probes: bool = False, variant: str = "",
+          defines=()) -> str:
     """probes: an instrumented copy (-DGOMIX_PROBES: %globaltimer marks in
     the GOM kernels) as libgomix_b200_probes.so, loaded with
-    GOMIX_LIB=paper_2203_08680_b200/libgomix_b200_probes.so."""
-    lib = LIB.replace(".so", "_probes.so") if probes else LIB
-    if not force and not probes and not _stale():
+    GOMIX_LIB=paper_2203_08680_b200/libgomix_b200_probes.so.
+    variant/defines: an A/B copy built with extra -D flags as
+    libgomix_b200_<variant>.so (same loading rule)."""
+    tag = "probes" if probes else variant
+    lib = LIB.replace(".so", f"_{tag}.so") if tag else LIB
+    if not force and not tag and not _stale():
         return LIB
     objs = []
-    build_dir = os.path.join(PKG, "build_probes" if probes else "build")
-    flags = FLAGS + (["-DGOMIX_PROBES"] if probes else [])
+    build_dir = os.path.join(PKG, f"build_{tag}" if tag else "build")
+    flags = FLAGS + (["-DGOMIX_PROBES"] if probes else []) + [f"-D{d}" for d in defines]
     os.makedirs(build_dir, exist_ok=True)
     procs = []
     for src in SOURCES:
@@ -60,4 +64,8 @@ def build(force: bool = False, verbose: bool = False, probes: bool = False) -> s
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, probes="--probes" in sys.argv))
+    # python -m paper_2203_08680_b200.build [--force] [-v] [--probes] [--variant NAME -DMACRO ...]
+    var = sys.argv[sys.argv.index("--variant") + 1] if "--variant" in sys.argv else ""
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, probes="--probes" in sys.argv,
+                variant=var, defines=defs))

@@ -313,7 +313,7 @@ struct gomix_gpu_engine {
   uint32_t tt_chunks = 1;  // > 1: n > 128, rows processed in 4-word chunks (counted rows in `ones`)
   unsigned int* chunk_done = nullptr;  // ... per-chunk CTA tickets of a launch
   double* word_max = nullptr;          // ... per-word fitness maxima after the chunk commits
-  unsigned int* tail_ctr = nullptr;    // truth-table kernel: dynamic batch counters (one per chunk)
+  unsigned int* tail_ctr = nullptr;    // truth-table kernel: dynamic batch counters (kTailCounters per chunk)
   bool univ_f64 = false;   // univariate, non-int32 weights, Philox: gom_univ_f64_kernel
   int f64_grid_cap = 1;
   int univ_grid_cap = 1;
@@ -391,6 +391,21 @@ struct gomix_gpu_engine {
   cudaGraphExec_t graph_exec = nullptr;
   uint64_t graph_launches = 0;
   static constexpr int kGraphAfter = 4;  // generations issued directly before the graph is captured
+  // Generations of large groups go launch by launch: every launch is
+  // programmatic, so the next generation's begin kernel fetches its criteria
+  // and the first group's CTAs become resident while this generation's last
+  // launch drains — across graph launches nothing overlaps (C3: 55.9 vs
+  // 57.5 us per generation).  Small groups, where the host's launch cost
+  // would show, keep the captured graph.  GOMIX_GRAPH=0/1 forces either.
+  static constexpr uint64_t kDirectPairs = 1ull << 22;  // solution-set pairs per launch
+  bool use_graph() const {
+    static const int force = [] {
+      const char* e = std::getenv("GOMIX_GRAPH");
+      return e ? (e[0] == '0' ? 0 : 1) : -1;
+    }();
+    if (force >= 0) return force == 1;
+    return max_group * n < kDirectPairs;
+  }
   int graph_warm = 0;
 
   cudaStream_t stream = nullptr;
@@ -621,8 +636,8 @@ struct gomix_gpu_engine {
       invalid("engine: the peer transport needs a univariate FOS with every variable in one set (use NCCL)");
     if (tt_chunks > 1 && R > 1 && !lite) invalid("engine: internal: chunked rows need the sharded row counts");
     if (lite || tt_chunks > 1) ones = dev_alloc<uint32_t>(allocs, nv);
-    tail_ctr = dev_alloc<unsigned int>(allocs, tt_chunks);
-    GOMIX_CUDA(cudaMemset(tail_ctr, 0, tt_chunks * sizeof(unsigned int)));
+    tail_ctr = dev_alloc<unsigned int>(allocs, tt_chunks * kTailCounters * kTailStride);
+    GOMIX_CUDA(cudaMemset(tail_ctr, 0, tt_chunks * kTailCounters * kTailStride * sizeof(unsigned int)));
     if (tt_chunks > 1) {
       chunk_done = dev_alloc<unsigned int>(allocs, tt_chunks);
       word_max = dev_alloc<double>(allocs, Wp);
@@ -728,7 +743,7 @@ struct gomix_gpu_engine {
     // issued launch by launch — the same kernels in the same order as the
     // captured graph — so a population that reaches the target early never
     // pays the capture and instantiation.
-    if (!graph_exec && graph_warm < kGraphAfter) {
+    if (!graph_exec && (graph_warm < kGraphAfter || !use_graph())) {
       ++graph_warm;
       count_rows(stream);
       OrderArgs o{ctl, d_order, (uint32_t)P->k, seed};
@@ -963,7 +978,7 @@ struct gomix_gpu_engine {
       const uint64_t per = (uint64_t)univ_f64_sets_per_cta();
       const int g = (int)std::max<uint64_t>(1, std::min<uint64_t>((G + per - 1) / per, (uint64_t)f64_grid_cap));
       a.epi = epi_args(group, (uint32_t)G, (uint32_t)g);
-      launch_univ_f64(a, (int)Wp, g, st, slot > 0);  // graph path, groups after the first: PDL
+      launch_univ_f64(a, (int)Wp, g, st, slot >= 0);  // graph path: PDL (the begin kernel or the previous group)
     } else if (univ_planes && !with_tape) {
       const uint64_t per = (uint64_t)univ_sliced_sets_per_cta();
       // chunked rows: tt_chunks CTAs per set range, one per chunk
@@ -1643,9 +1658,21 @@ GOMIX_API int gomix_debug_probes(unsigned long long* out, int32_t reset) {
 }
 
 // truth-table kernel launch timeline, probes builds (build.py --probes):
-// out[2i] / out[2i+1] = first / last CTA at point i (%globaltimer ns); resets
+// out[32r + 2i] / out[32r + 2i + 1] = first / last CTA at point i of launch
+// row r (graph slot + 1, 0 = direct), r < 4; out[128 + ...] the begin
+// kernel (points 0, 1); %globaltimer ns, 160 words; resets
 GOMIX_API int gomix_debug_timeline(unsigned long long* out) {
-  return guarded([&] { debug_timeline_univ(out); });
+  return guarded([&] {
+    debug_timeline_univ(out);
+    debug_timeline_gom(out + 128);
+  });
+}
+
+// per-CTA record of the truth-table launches, probes builds: out[((r * 1024)
+// + cta) * 4 + {0: SM, 1: start ns, 2: batches done ns, 3: batches}], row r =
+// graph slot + 1 (0 = direct), 4 rows
+GOMIX_API int gomix_debug_cta_stats(unsigned long long* out) {
+  return guarded([&] { debug_cta_stats_univ(out); });
 }
 
 const char* gomix_gpu_last_error(void) { return g_last_error.c_str(); }

@@ -481,7 +481,13 @@ __global__ void begin_generation_kernel(const BeginArgs* bp, const OrderArgs o) 
   // the first group's launch may start now: it waits for this kernel's
   // completion before reading the order or the control block
   asm volatile("griddepcontrol.launch_dependents;");
-  const BeginArgs b = *bp;  // criteria uploaded before each graph launch
+  timeline_mark(0);
+  // the criteria (mapped host memory, staged before the launch was issued)
+  // cross the bus while the previous kernel on the stream finishes: this
+  // launch is programmatic, everything after the wait touches the control
+  // block that kernel may still write
+  const BeginArgs b = *bp;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   DevCtl* c = b.ctl;
   c->stop = 0;
   c->stop_reason = GOMIX_STOP_NONE;
@@ -507,6 +513,7 @@ __global__ void begin_generation_kernel(const BeginArgs* bp, const OrderArgs o) 
     o.order[i - 1] = o.order[j];
     o.order[j] = t;
   }
+  timeline_mark(1);
 }
 
 // After init_population (engine_parallel.hpp:331-346): one add_evaluator_calls(q)
@@ -751,8 +758,16 @@ void launch_begin(const BeginArgs& b, cudaStream_t s) {
 }
 
 void launch_order(const BeginArgs* d_b, const OrderArgs& o, cudaStream_t s) {
-  begin_generation_kernel<<<1, 1, 0, s>>>(d_b, o);
-  GOMIX_CUDA(cudaGetLastError());
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(1);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  GOMIX_CUDA(cudaLaunchKernelEx(&cfg, begin_generation_kernel, d_b, o));
 }
 
 // The control block and the first improvement-log entries, written straight
@@ -765,6 +780,14 @@ __global__ void publish_ctl_kernel(const uint4* src, uint4* dst, uint32_t words,
   __threadfence_system();
   __syncthreads();
   if (threadIdx.x == 0) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(seq_dst), "l"(seq) : "memory");
+}
+
+void debug_timeline_gom(unsigned long long* out) {
+  GOMIX_CUDA(cudaDeviceSynchronize());
+  GOMIX_CUDA(cudaMemcpyFromSymbol(out, g_timeline, sizeof(unsigned long long) * 32));
+  unsigned long long z[32 * kTimelineRows];
+  for (int i = 0; i < 32 * kTimelineRows; ++i) z[i] = (i & 1) ? 0ull : ~0ull;
+  GOMIX_CUDA(cudaMemcpyToSymbol(g_timeline, z, sizeof(z)));
 }
 
 void launch_publish_ctl(const void* ctl, void* host_dst, size_t bytes, unsigned long long* host_seq,

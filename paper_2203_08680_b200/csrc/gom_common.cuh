@@ -48,17 +48,20 @@ __device__ __forceinline__ unsigned int ticket_acq_rel(unsigned int* p) {
   return old;
 }
 
-// Launch timeline (probes builds only): for point i, the earliest and latest
-// CTA to reach it (thread 0), as %globaltimer ns; read and reset through
+// Launch timeline (probes builds only): for point i of launch row r (the
+// graph slot + 1; 0 = a direct launch), the earliest and latest CTA to reach
+// it (thread 0), as %globaltimer ns; read and reset through
 // gomix_debug_timeline.
-static __device__ unsigned long long g_timeline[32];  // one copy per translation unit
-__device__ __forceinline__ void timeline_mark(uint32_t i) {
+constexpr int kTimelineRows = 4;
+static __device__ unsigned long long g_timeline[kTimelineRows * 32];  // one copy per translation unit
+__device__ __forceinline__ void timeline_mark(uint32_t i, int32_t row = 0) {
 #ifdef GOMIX_PROBES
   if (threadIdx.x == 0 && i < 16) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    atomicMin(&g_timeline[2 * i], t);
-    atomicMax(&g_timeline[2 * i + 1], t);
+    const int32_t r = row < 0 ? 0 : (row >= kTimelineRows ? kTimelineRows - 1 : row);
+    atomicMin(&g_timeline[r * 32 + 2 * i], t);
+    atomicMax(&g_timeline[r * 32 + 2 * i + 1], t);
   }
 #endif
 }
@@ -163,7 +166,18 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, uint32_t lane) {
   for (int st = 0; st < 5; ++st) {
     const uint32_t j = 16u >> st, m = masks[st];
     const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x, j);
+#ifdef GOMIX_TRANSPOSE_ROT
+    // lower lane: keep the m blocks of x, take y's m blocks moved up by j;
+    // upper lane: keep the ~m blocks, take y's ~m blocks moved down by j —
+    // one rotate (funnel shift by j or 32 - j) and one 3-input select
+    // (measured: no faster — the lane-dependent constants are rematerialised)
+    const bool up = (lane & j) != 0u;
+    const uint32_t keep = up ? ~m : m;
+    const uint32_t r = __funnelshift_l(y, y, up ? 32u - j : j);
+    asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(x) : "r"(x), "r"(r), "r"(keep));  // (x & keep) | (r & ~keep)
+#else
     x = (lane & j) ? ((x & ~m) | ((y & ~m) >> j)) : ((x & m) | ((y & m) << j));
+#endif
   }
   return x;
 }
@@ -257,8 +271,51 @@ static __device__ void commit_range(const EpiArgs& a, uint32_t s0, uint32_t s1, 
 // improvement with the call count at that moment and latching the target stop
 // (runtime.hpp:88-93,136-143).  Sharded runs execute it on every rank from the
 // gathered state, so all ranks take identical decisions.
+// The control-block fields the scan reads, loaded by thread 0 in one memory
+// round trip — issued before the group's commit where the caller can, so the
+// two round trips overlap.
+struct CtlSnap {
+  unsigned long long st, ca, calls_total, run_steps, run_calls, groups_run, n_impr, gst, gca;
+  int32_t has_budget, has_target, exact, stop;
+  uint32_t ver;
+  double max_evals, q, target, elit_fit;
+};
+
+static __device__ __forceinline__ CtlSnap load_ctl_snap(const EpiArgs& a) {
+  const DevCtl* c = a.ctl;
+  CtlSnap k;
+  k.st = 0;
+  k.ca = 0;
+  if (a.R > 1) {
+    for (uint32_t r = 0; r < a.R; ++r) {
+      k.st += a.rank_cnt[2 * r];
+      k.ca += a.rank_cnt[2 * r + 1];
+    }
+  } else {
+    k.st = c->grp_steps;
+    k.ca = c->grp_calls;
+  }
+  k.calls_total = c->calls_total;
+  k.run_steps = c->run_steps;
+  k.run_calls = c->run_calls;
+  k.groups_run = c->groups_run;
+  k.n_impr = c->n_impr;
+  k.gst = a.gsteps[a.group];
+  k.gca = a.gcalls[a.group];
+  k.has_budget = c->has_budget;
+  k.has_target = c->has_target;
+  k.exact = c->exact;
+  k.stop = c->stop;
+  k.ver = c->elit_ver;
+  k.max_evals = c->max_evals;
+  k.q = c->q;
+  k.target = c->target;
+  k.elit_fit = c->elit_fit;
+  return k;
+}
+
 static __device__ void elitist_scan(const EpiArgs& a, const double* s_fit,
-                                    const unsigned long long* s_h = nullptr) {
+                                    const unsigned long long* s_h = nullptr, const CtlSnap* pre = nullptr) {
   DevCtl* c = a.ctl;
   const uint32_t n = a.n_global;
   const uint32_t nchunks = (n + 31u) / 32u;  // <= 128 (populations up to 4096)
@@ -269,48 +326,33 @@ static __device__ void elitist_scan(const EpiArgs& a, const double* s_fit,
   __shared__ uint32_t s_ver;
   if (threadIdx.x == 0) {
     // every control-block load first (independent of each other: one memory
-    // round trip), then the updates
-    unsigned long long st = 0, ca = 0;
-    if (a.R > 1) {
-      for (uint32_t r = 0; r < a.R; ++r) {
-        st += a.rank_cnt[2 * r];
-        ca += a.rank_cnt[2 * r + 1];
-      }
-    } else {
-      st = c->grp_steps;
-      ca = c->grp_calls;
-    }
-    const unsigned long long calls_total = c->calls_total, run_steps = c->run_steps, run_calls = c->run_calls;
-    const unsigned long long groups_run = c->groups_run, n_impr = c->n_impr;
-    const unsigned long long gst = a.gsteps[a.group], gca = a.gcalls[a.group];
-    const int32_t has_budget = c->has_budget, has_target = c->has_target, exact = c->exact;
-    int32_t stop = c->stop;
-    const uint32_t ver = c->elit_ver;
-    const double max_evals = c->max_evals, q = c->q, target = c->target, elit_fit = c->elit_fit;
+    // round trip, or none when the caller loaded them), then the updates
+    const CtlSnap k = pre ? *pre : load_ctl_snap(a);
+    int32_t stop = k.stop;
     if (a.R == 1) {
       c->grp_steps = 0;
       c->grp_calls = 0;
     }
-    const unsigned long long ct = calls_total + ca;
+    const unsigned long long ct = k.calls_total + k.ca;
     c->calls_total = ct;
-    c->run_steps = run_steps + st;
-    c->run_calls = run_calls + ca;
-    c->groups_run = groups_run + 1;
-    a.gsteps[a.group] = gst + st;
-    a.gcalls[a.group] = gca + ca;
-    if (has_budget && (double)ct / q >= max_evals && !stop) {  // request_stop(budget)
+    c->run_steps = k.run_steps + k.st;
+    c->run_calls = k.run_calls + k.ca;
+    c->groups_run = k.groups_run + 1;
+    a.gsteps[a.group] = k.gst + k.st;
+    a.gcalls[a.group] = k.gca + k.ca;
+    if (k.has_budget && (double)ct / k.q >= k.max_evals && !stop) {  // request_stop(budget)
       c->stop = 1;
       c->stop_reason = GOMIX_STOP_BUDGET;
       stop = 1;
     }
     s_stopped = stop;
-    s_ver = ver;
-    s_cur = elit_fit;
-    s_target = target;
-    s_ni = n_impr;
+    s_ver = k.ver;
+    s_cur = k.elit_fit;
+    s_target = k.target;
+    s_ni = k.n_impr;
     s_calls_now = ct;
-    s_exact = exact;
-    s_has_target = has_target;
+    s_exact = k.exact;
+    s_has_target = k.has_target;
   }
   __syncthreads();
   // chunk maxima let the serial scan skip chunks that cannot hold a record:
@@ -386,9 +428,10 @@ static __device__ void elitist_scan(const EpiArgs& a, const double* s_fit,
 // the rank's counters for the exchange and — with the peer transport — the
 // exchange and the global scan in the same kernel (gom_peer.cuh; with NCCL
 // they follow the launch).
-static __device__ void epilogue_global(const EpiArgs& a, const double* s_fit, const unsigned long long* s_h) {
+static __device__ void epilogue_global(const EpiArgs& a, const double* s_fit, const unsigned long long* s_h,
+                                       const CtlSnap* pre = nullptr) {
   if (a.R == 1) {
-    elitist_scan(a, s_fit, s_h);
+    elitist_scan(a, s_fit, s_h, pre);
     return;
   }
   if (threadIdx.x == 0) {  // this rank's counters, all-gathered next
@@ -405,9 +448,12 @@ static __device__ void epilogue_global(const EpiArgs& a, const double* s_fit, co
 static __device__ void epilogue_body(const EpiArgs& a) {
   __shared__ double s_fit[kEpiSmemFit];              // this group's fitness, scanned without global loads
   __shared__ unsigned long long s_h[2 * kEpiSmemFit];  // ... and hashes (a new elitist's)
+  // one CTA: the scan's control-block loads in flight with the commit's
+  CtlSnap pre;
+  if (a.R == 1 && threadIdx.x == 0) pre = load_ctl_snap(a);
   commit_range(a, 0, a.n, a.R == 1 ? s_fit : nullptr, a.R == 1 ? s_h : nullptr);
   __syncthreads();
-  epilogue_global(a, s_fit, s_h);
+  epilogue_global(a, s_fit, s_h, a.R == 1 ? &pre : nullptr);
 }
 
 }  // namespace gomix_b200

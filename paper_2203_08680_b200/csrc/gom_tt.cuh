@@ -147,7 +147,7 @@ __device__ __forceinline__ TtPart tt_part(const GomArgs& a) {
 // start, counted per generation: a univariate, variable-once FOS changes a
 // row only in its own group).
 template <int B, int WC>
-__device__ __forceinline__ void tt_batches(const GomArgs& a, const TtPart& part, const uint4* urec,
+__device__ __forceinline__ uint32_t tt_batches(const GomArgs& a, const TtPart& part, const uint4* urec,
                                            const ulonglong2* ukey, uint32_t G, TtNext nx, const uint32_t* s_elit,
                                            long long* s_dfit, TtShared& sh, int32_t esrc, uint32_t ever_cur,
                                            uint32_t lane, uint32_t warp, unsigned long long& steps,
@@ -159,18 +159,23 @@ __device__ __forceinline__ void tt_batches(const GomArgs& a, const TtPart& part,
   const uint32_t bstride = part.ctas * kUnivWarps;
   // Every warp takes the same number of batches statically (warp-major, so
   // every SM gets the same mix); the remainder — less than one batch per
-  // warp — goes to whichever warps finish first, claimed from a counter:
-  // the CTAs that run slow (memory latency, accept-heavy sets) no longer
-  // set the launch's tail.
+  // warp — goes to whichever warps finish first, claimed from kTailCounters
+  // counters (counter c hands out batches dyn0 + c + kTailCounters * i to
+  // the warps with slot % kTailCounters == c): the CTAs that run slow (memory
+  // latency, accept-heavy sets) no longer set the launch's tail.
   const uint32_t nstatic = batches / bstride;
   const uint32_t dyn0 = nstatic * bstride;
-  unsigned int* tail = a.tail + (a.tail_per_chunk ? part.chunk : 0u);
+  const uint32_t slot = warp * part.ctas + part.cta;
+  const uint32_t tc = slot % kTailCounters;
+  unsigned int* tail = a.tail + ((a.tail_per_chunk ? part.chunk : 0u) * kTailCounters + tc) * kTailStride;
+  const uint32_t dyn = dyn0 + tc;
   uint32_t k = 0;
-  uint32_t bt = warp * part.ctas + part.cta;  // the caller prefetched this batch's records
+  uint32_t np = 0, dsum = 0;  // this lane's present sets and their degrees
+  uint32_t bt = slot;  // the caller prefetched this batch's records
   if (nstatic == 0) {  // fewer batches than warps: every batch is claimed
     uint32_t c = 0;
     if (lane == 0) c = atomicAdd(tail, 1u);
-    bt = dyn0 + __shfl_sync(0xFFFFFFFFu, c, 0);
+    bt = dyn + kTailCounters * __shfl_sync(0xFFFFFFFFu, c, 0);
     nx = tt_fetch(urec, ukey, G, bt * 32u + lane);
   }
   while (bt < batches) {
@@ -184,7 +189,7 @@ __device__ __forceinline__ void tt_batches(const GomArgs& a, const TtPart& part,
     } else {
       uint32_t c = 0;
       if (lane == 0) c = atomicAdd(tail, 1u);
-      bt_next = dyn0 + __shfl_sync(0xFFFFFFFFu, c, 0);
+      bt_next = dyn + kTailCounters * __shfl_sync(0xFFFFFFFFu, c, 0);
     }
     nx = tt_fetch(urec, ukey, G, bt_next * 32u + lane);
     const uint32_t v = ra.x;
@@ -228,9 +233,9 @@ __device__ __forceinline__ void tt_batches(const GomArgs& a, const TtPart& part,
       }
     }
     const bool present = live && ones > 0u && ones < a.n_global;
-    if (present) {
-      steps += part.n_chunk;
-      calls += (unsigned long long)part.n_chunk * deg;
+    if (present) {  // (x n_chunk at the end)
+      ++np;
+      dsum += deg;
     }
     const uint32_t pmask = present ? 0xFFFFFFFFu : 0u;
     // ---- b words (edge "uncut-gain" bits), then accept via the LE table
@@ -374,6 +379,9 @@ __device__ __forceinline__ void tt_batches(const GomArgs& a, const TtPart& part,
     __syncwarp();
     bt = bt_next;
   }
+  steps += (unsigned long long)np * part.n_chunk;
+  calls += (unsigned long long)dsum * part.n_chunk;
+  return k;  // batches this warp processed (+1 when it claimed past the end)
 }
 
 }  // namespace gomix_b200

@@ -373,6 +373,45 @@ __global__ void build_univ_records_kernel(const uint32_t* gvars, const int32_t* 
   key[p] = make_ulonglong2(z1, z2);
 }
 
+// Per-CTA record of the truth-table launches (probes builds only): SM id,
+// start and batches-done %globaltimer, batches processed; per launch row
+// (graph slot + 1) and CTA; read through gomix_debug_cta_stats.
+constexpr int kCtaStatMax = 1024;
+static __device__ unsigned long long g_ctastat[kTimelineRows][kCtaStatMax][4];
+#ifdef GOMIX_PROBES
+static __shared__ unsigned long long s_stat_t0;
+static __shared__ unsigned int s_stat_nb;
+#endif
+__device__ __forceinline__ void cta_stat_start() {
+#ifdef GOMIX_PROBES
+  if (threadIdx.x == 0) {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(s_stat_t0));
+    s_stat_nb = 0;
+  }
+#endif
+}
+__device__ __forceinline__ void cta_stat_batches(uint32_t nb, uint32_t lane) {
+#ifdef GOMIX_PROBES
+  if (lane == 0) atomicAdd(&s_stat_nb, nb);
+#endif
+}
+__device__ __forceinline__ void cta_stat_done(int32_t row) {
+#ifdef GOMIX_PROBES
+  if (threadIdx.x == 0 && blockIdx.x < kCtaStatMax) {
+    const int32_t r = row < 0 ? 0 : (row >= kTimelineRows ? kTimelineRows - 1 : row);
+    unsigned long long t, sm;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    sm = smid;
+    g_ctastat[r][blockIdx.x][0] = sm;
+    g_ctastat[r][blockIdx.x][1] = s_stat_t0;
+    g_ctastat[r][blockIdx.x][2] = t;
+    g_ctastat[r][blockIdx.x][3] = s_stat_nb;
+  }
+#endif
+}
+
 template <int B, int WC, int MINB = 3>
 __global__ void __launch_bounds__(kUnivWarps * 32, MINB) gom_univ_tt_kernel(const GomArgs a) {
   __shared__ __align__(16) TtShared sh;
@@ -382,7 +421,8 @@ __global__ void __launch_bounds__(kUnivWarps * 32, MINB) gom_univ_tt_kernel(cons
   __shared__ unsigned long long s_steps, s_calls;
   __shared__ int s_last;
   probe(a.exp_flags, 40);
-  timeline_mark(0);  // CTA start
+  timeline_mark(0, a.slot + 1);  // CTA start
+  cta_stat_start();
 
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   constexpr uint32_t Wp = (uint32_t)WC;  // words of this CTA's chunk (whole rows when a.Wp == WC)
@@ -421,6 +461,7 @@ __global__ void __launch_bounds__(kUnivWarps * 32, MINB) gom_univ_tt_kernel(cons
   // everything below reads what the previous group's launch wrote
   // (population, control block, hashes)
   if (a.slot != 0) asm volatile("griddepcontrol.wait;" ::: "memory");
+  timeline_mark(7, a.slot + 1);  // dependency wait over
   // the control block and this warp's hashes in one round trip, then the stop check
   const int32_t stopped = *(volatile int32_t*)&a.ctl->stop;
   const unsigned long long eh1 = a.ctl->eh1, eh2 = a.ctl->eh2;
@@ -442,12 +483,14 @@ __global__ void __launch_bounds__(kUnivWarps * 32, MINB) gom_univ_tt_kernel(cons
   }
   __syncthreads();
   probe(a.exp_flags, 41);
-  timeline_mark(1);  // prologue done
+  timeline_mark(1, a.slot + 1);  // prologue done
   unsigned long long steps = 0, calls = 0;
-  tt_batches<B, WC>(a, part, urec, ukey, G, first, s_elit, s_dfit, sh, esrc, ever_cur, lane, warp, steps, calls);
+  const uint32_t nbt =
+      tt_batches<B, WC>(a, part, urec, ukey, G, first, s_elit, s_dfit, sh, esrc, ever_cur, lane, warp, steps, calls);
+  cta_stat_batches(nbt, lane);
 
   probe(a.exp_flags, 42);
-  timeline_mark(2);  // warp 0's batches done
+  timeline_mark(2, a.slot + 1);  // warp 0's batches done
   // the next group's launch may start its prologue (it waits for this grid's
   // completion before touching anything written here)
   asm volatile("griddepcontrol.launch_dependents;");
@@ -464,7 +507,8 @@ __global__ void __launch_bounds__(kUnivWarps * 32, MINB) gom_univ_tt_kernel(cons
     }
   }
   __syncthreads();
-  timeline_mark(6);  // every warp of the CTA done with its batches
+  timeline_mark(6, a.slot + 1);  // every warp of the CTA done with its batches
+  cta_stat_done(a.slot + 1);
   for (uint32_t s = threadIdx.x; s < part.n_chunk; s += blockDim.x) {
     unsigned long long x1 = 0, x2 = 0;
 #pragma unroll
@@ -488,7 +532,7 @@ __global__ void __launch_bounds__(kUnivWarps * 32, MINB) gom_univ_tt_kernel(cons
     }
   }
   __syncthreads();
-  timeline_mark(3);  // CTA flushed
+  timeline_mark(3, a.slot + 1);  // CTA flushed
   const uint32_t chunks = a.Wp / (uint32_t)WC;
   if (chunks > 1) {
     // Rows in chunks (n > 128): the last CTA of every chunk commits that
@@ -514,17 +558,18 @@ __global__ void __launch_bounds__(kUnivWarps * 32, MINB) gom_univ_tt_kernel(cons
     __syncthreads();
     if (threadIdx.x == 0) {
       a.chunk_done[part.chunk] = 0;
-      a.tail[part.chunk] = 0;  // every CTA of the chunk is done claiming
+      for (uint32_t c = 0; c < kTailCounters; ++c)  // every CTA of the chunk is done claiming
+        a.tail[(part.chunk * kTailCounters + c) * kTailStride] = 0;
       __threadfence();
       s_last = atomicAdd(&a.ctl->done, 1u) == chunks - 1;
     }
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    timeline_mark(4);  // epilogue start (last chunk CTA)
+    timeline_mark(4, a.slot + 1);  // epilogue start (last chunk CTA)
     epi.word_max = a.word_max;
     epilogue_global(epi, nullptr, nullptr);
-    timeline_mark(5);  // epilogue end
+    timeline_mark(5, a.slot + 1);  // epilogue end
     if (threadIdx.x == 0) a.ctl->done = 0;
     return;
   }
@@ -534,13 +579,13 @@ __global__ void __launch_bounds__(kUnivWarps * 32, MINB) gom_univ_tt_kernel(cons
   if (!s_last) return;
   __threadfence();
   probe_last(a.exp_flags, 44);
-  timeline_mark(4);  // epilogue start (last CTA)
+  timeline_mark(4, a.slot + 1);  // epilogue start (last CTA)
   epilogue_body(epi);
   probe_last(a.exp_flags, 45);
-  timeline_mark(5);  // epilogue end
+  timeline_mark(5, a.slot + 1);  // epilogue end
   if (threadIdx.x == 0) {
     a.ctl->done = 0;
-    a.tail[0] = 0;
+    for (uint32_t c = 0; c < kTailCounters; ++c) a.tail[c * kTailStride] = 0;
   }
 }
 
@@ -645,10 +690,15 @@ void launch_univ_sliced(const GomArgs& a, int planes, int wp, bool tt, int grid,
 
 void debug_timeline_univ(unsigned long long* out) {
   GOMIX_CUDA(cudaDeviceSynchronize());
-  GOMIX_CUDA(cudaMemcpyFromSymbol(out, g_timeline, sizeof(unsigned long long) * 32));
-  unsigned long long z[32];
-  for (int i = 0; i < 32; ++i) z[i] = (i & 1) ? 0ull : ~0ull;
+  GOMIX_CUDA(cudaMemcpyFromSymbol(out, g_timeline, sizeof(unsigned long long) * 32 * kTimelineRows));
+  unsigned long long z[32 * kTimelineRows];
+  for (int i = 0; i < 32 * kTimelineRows; ++i) z[i] = (i & 1) ? 0ull : ~0ull;
   GOMIX_CUDA(cudaMemcpyToSymbol(g_timeline, z, sizeof(z)));
+}
+
+void debug_cta_stats_univ(unsigned long long* out) {
+  GOMIX_CUDA(cudaDeviceSynchronize());
+  GOMIX_CUDA(cudaMemcpyFromSymbol(out, g_ctastat, sizeof(unsigned long long) * kTimelineRows * kCtaStatMax * 4));
 }
 
 void debug_probes_univ(unsigned long long* out, bool reset) {

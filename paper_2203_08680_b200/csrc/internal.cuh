@@ -159,6 +159,13 @@ struct SnapArgs {
   uint32_t n, Wp;
 };
 
+// The truth-table kernel's dynamically claimed batches are spread over
+// kTailCounters counters, each on its own 128-byte line: one counter would
+// serialise every warp's claim at the end of the static share (~1 ns per
+// same-address atomic, thousands of warps).
+constexpr uint32_t kTailCounters = 16;
+constexpr uint32_t kTailStride = 32;
+
 struct GomArgs {
   const int32_t* row_ptr;
   const int32_t* col;
@@ -202,8 +209,9 @@ struct GomArgs {
   uint64_t seed;
   EpiArgs epi;         // run by the last CTA
   unsigned int* chunk_done;  // truth-table rows in chunks: per-chunk CTA tickets
-  unsigned int* tail;        // truth-table kernel: counters of the dynamically claimed batches
-  uint32_t tail_per_chunk;   // ... one per chunk (rows in chunks) or one per launch
+  unsigned int* tail;        // truth-table kernel: counters of the dynamically claimed batches,
+                             // kTailCounters per set (kTailStride words apart)
+  uint32_t tail_per_chunk;   // ... one set per chunk (rows in chunks) or one per launch
   double* word_max;          // ... and per-word maxima written by each chunk's last CTA
   int32_t slot;                 // >= 0: group = order[slot] (graph path)
   uint32_t exp_flags;           // latency studies only (GOMIX_EXP env): 32 = %globaltimer probes
@@ -397,7 +405,9 @@ void launch_sum_ones(const uint32_t* stage, uint32_t R, uint64_t nv, uint32_t* o
 void debug_probes(unsigned long long* out, bool reset);
 void debug_probes_gen(unsigned long long* out, bool reset);
 void debug_probes_univ(unsigned long long* out, bool reset);
-void debug_timeline_univ(unsigned long long* out);  // gom_univ_tt_kernel launch timeline (probes builds)
+void debug_timeline_univ(unsigned long long* out);  // gom_univ_tt_kernel launch timeline (probes builds), 4 x 32
+void debug_timeline_gom(unsigned long long* out);   // begin_generation_kernel (points 0, 1), 32
+void debug_cta_stats_univ(unsigned long long* out);  // per-CTA stats of the tt launches, 4 x 1024 x 4
 void debug_cta_probes(unsigned long long* out);
 void launch_philox_init(uint32_t* pop, uint64_t nv, uint32_t n, uint32_t Wp, uint64_t seed,
                         uint32_t rank, cudaStream_t s);
