@@ -1670,7 +1670,8 @@ GOMIX_API int gomix_debug_timeline(unsigned long long* out) {
 
 // per-CTA record of the truth-table launches, probes builds: out[((r * 1024)
 // + cta) * 4 + {0: SM, 1: start ns, 2: batches done ns, 3: batches}], row r =
-// graph slot + 1 (0 = direct), 4 rows
+// graph slot + 1 (0 = direct), 4 rows; then 16 batch-loop path counters
+// (gom_tt.cuh tt_count, reset on read)
 GOMIX_API int gomix_debug_cta_stats(unsigned long long* out) {
   return guarded([&] { debug_cta_stats_univ(out); });
 }

@@ -54,8 +54,17 @@ __device__ __forceinline__ unsigned int ticket_acq_rel(unsigned int* p) {
 // gomix_debug_timeline.
 constexpr int kTimelineRows = 4;
 static __device__ unsigned long long g_timeline[kTimelineRows * 32];  // one copy per translation unit
+#ifdef GOMIX_PROBES
+static __shared__ int32_t s_tl_row;  // the launch's row, for marks in shared device code (row -1)
+#endif
+__device__ __forceinline__ void timeline_set_row(int32_t row) {
+#ifdef GOMIX_PROBES
+  if (threadIdx.x == 0) s_tl_row = row;
+#endif
+}
 __device__ __forceinline__ void timeline_mark(uint32_t i, int32_t row = 0) {
 #ifdef GOMIX_PROBES
+  if (row == -1) row = s_tl_row;
   if (threadIdx.x == 0 && i < 16) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -354,6 +363,7 @@ static __device__ void elitist_scan(const EpiArgs& a, const double* s_fit,
     s_exact = k.exact;
     s_has_target = k.has_target;
   }
+  timeline_mark(9, -1);  // scan: control block accounted
   __syncthreads();
   // chunk maxima let the serial scan skip chunks that cannot hold a record:
   // precomputed by the CTAs that committed the chunks (a.word_max), else
@@ -373,6 +383,7 @@ static __device__ void elitist_scan(const EpiArgs& a, const double* s_fit,
     }
   }
   __syncthreads();
+  timeline_mark(10, -1);  // scan: chunk maxima
   if (warp == 0) {
     const bool exact = s_exact != 0;
     const int32_t has_target = s_has_target;
@@ -421,6 +432,7 @@ static __device__ void elitist_scan(const EpiArgs& a, const double* s_fit,
       }
     }
   }
+  timeline_mark(11, -1);  // scan: done (warp 0)
   __syncthreads();
 }
 
@@ -448,12 +460,18 @@ static __device__ void epilogue_global(const EpiArgs& a, const double* s_fit, co
 static __device__ void epilogue_body(const EpiArgs& a) {
   __shared__ double s_fit[kEpiSmemFit];              // this group's fitness, scanned without global loads
   __shared__ unsigned long long s_h[2 * kEpiSmemFit];  // ... and hashes (a new elitist's)
-  // one CTA: the scan's control-block loads in flight with the commit's
+  __shared__ CtlSnap s_snap;
+  // one CTA: the scan's control-block loads in flight with the commit's —
+  // issued by the last thread, parked in registers until its commit share
+  // is done (a thread that stored them right away would wait for them first)
+  const bool loader = a.R == 1 && threadIdx.x == blockDim.x - 1;
   CtlSnap pre;
-  if (a.R == 1 && threadIdx.x == 0) pre = load_ctl_snap(a);
+  if (loader) pre = load_ctl_snap(a);
   commit_range(a, 0, a.n, a.R == 1 ? s_fit : nullptr, a.R == 1 ? s_h : nullptr);
+  if (loader) s_snap = pre;
   __syncthreads();
-  epilogue_global(a, s_fit, s_h, a.R == 1 ? &pre : nullptr);
+  timeline_mark(8, -1);  // epilogue: committed
+  epilogue_global(a, s_fit, s_h, a.R == 1 ? &s_snap : nullptr);
 }
 
 }  // namespace gomix_b200

@@ -10,6 +10,15 @@
 namespace gomix_b200 {
 
 constexpr int kUnivWarps = 8;        // warps per CTA of the univariate kernels
+
+// Path counters of the batch loop (probes builds only; lane 0 adds v):
+// read with gomix_debug_cta_stats after the per-CTA records.
+static __device__ unsigned long long g_ttcount[16];
+__device__ __forceinline__ void tt_count(uint32_t i, uint32_t v, uint32_t lane) {
+#ifdef GOMIX_PROBES
+  if (lane == 0 && v) atomicAdd(&g_ttcount[i], (unsigned long long)v);
+#endif
+}
 constexpr uint32_t kSparseKeys = 6;  // hash deltas key by key up to this many accepted sets per solution
 
 template <int WP>
@@ -268,6 +277,17 @@ __device__ __forceinline__ uint32_t tt_batches(const GomArgs& a, const TtPart& p
         any |= acc[j] != 0u;
       }
     }
+#ifdef GOMIX_PROBES
+    tt_count(0, 1, lane);
+    tt_count(6, __any_sync(0xFFFFFFFFu, any) ? 1u : 0u, lane);
+#pragma unroll
+    for (int j = 0; j < WC; ++j) {
+      tt_count(1, __any_sync(0xFFFFFFFFu, acc[j] != 0u) ? 1u : 0u, lane);
+      tt_count(7, s_elit[j] ? 1u : 0u, lane);
+      tt_count(8, __reduce_add_sync(0xFFFFFFFFu, (uint32_t)__popc(acc[j])), lane);
+      tt_count(9, __popc(__ballot_sync(0xFFFFFFFFu, acc[j] != 0u)), lane);
+    }
+#endif
     // ---- commit: accepted solutions flip v (apply_acceptance, :221-247)
     if (any) {
       uint32_t nw[WC];
@@ -301,6 +321,7 @@ __device__ __forceinline__ uint32_t tt_batches(const GomArgs& a, const TtPart& p
         // strict improvements: T(p) < A/2  <=>  T(~p) = A - T(p) > A/2  <=>
         // ~p is not in LE — the LE table at the complemented pattern, no LT masks
         const uint32_t imp = acc[j] & ~tt_mux_not(mle, b0, b1, b2, b3);
+        tt_count(2, __any_sync(0xFFFFFFFFu, imp != 0u) ? 1u : 0u, lane);
         if (__any_sync(0xFFFFFFFFu, imp != 0u)) {
           // T planes of this word (only words with a strictly improving pair)
           uint32_t T[B];
@@ -331,8 +352,18 @@ __device__ __forceinline__ uint32_t tt_batches(const GomArgs& a, const TtPart& p
         // hash delta of solution 32j+lane: XOR of the keys of its accepted
         // sets — key by key when every solution of the word accepted few
         // sets (the steady state: neutral flips are sparse), else through the
-        // 4-bit-chunk table of key XORs
+        // 4-bit-chunk table of key XORs.  (Walking the accepting sets
+        // instead — ~2.5 of 32 per word at C3 — each set's accept word
+        // broadcast from its lane, saves the transpose but measured 11%
+        // slower: registers spill; so did LT muxes for the elitist copies.)
         unsigned long long x1 = 0, x2 = 0;
+#ifdef GOMIX_PROBES
+        {
+          const uint32_t mx = __reduce_max_sync(0xFFFFFFFFu, (uint32_t)__popc(accT));
+          tt_count(mx <= kSparseKeys ? 3 : 4, 1, lane);
+          tt_count(5, mx, lane);
+        }
+#endif
         if (__reduce_max_sync(0xFFFFFFFFu, (uint32_t)__popc(accT)) <= kSparseKeys) {
           uint32_t r = accT;
           while (r) {

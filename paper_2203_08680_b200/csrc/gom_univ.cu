@@ -422,6 +422,7 @@ __global__ void __launch_bounds__(kUnivWarps * 32, MINB) gom_univ_tt_kernel(cons
   __shared__ int s_last;
   probe(a.exp_flags, 40);
   timeline_mark(0, a.slot + 1);  // CTA start
+  timeline_set_row(a.slot + 1);
   cta_stat_start();
 
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
@@ -481,6 +482,7 @@ __global__ void __launch_bounds__(kUnivWarps * 32, MINB) gom_univ_tt_kernel(cons
     const uint32_t m = __ballot_sync(0xFFFFFFFFu, sw < n && hs1 == eh1 && hs2 == eh2);
     if (lane == 0) s_elit[warp] = m;
   }
+  timeline_mark(12, a.slot + 1);  // prologue: control block and hashes back
   __syncthreads();
   probe(a.exp_flags, 41);
   timeline_mark(1, a.slot + 1);  // prologue done
@@ -598,17 +600,27 @@ namespace {
 int tt_occupancy() {
   static const int occ = [] {
     const char* e = std::getenv("GOMIX_TT_OCC");
+#ifdef GOMIX_TT_OCC2  // A/B builds: 2 CTAs per SM, 128 registers
+    if (e && std::atoi(e) == 2) return 2;
+#endif
     return (e && std::atoi(e) == 4) ? 4 : 3;
   }();
   return occ;
+}
+
+template <int b, int WC>
+void* tt_kernel_for_occupancy() {
+#ifdef GOMIX_TT_OCC2
+  if (tt_occupancy() == 2) return (void*)gom_univ_tt_kernel<b, WC, 2>;
+#endif
+  return tt_occupancy() == 4 ? (void*)gom_univ_tt_kernel<b, WC, 4> : (void*)gom_univ_tt_kernel<b, WC, 3>;
 }
 
 template <int WC, bool MULTI>
 void* univ_kernel_wc(int planes, bool tt) {
 #define GOMIX_UNIV_CASE(b)                                                                            \
   case b:                                                                                             \
-    return tt ? (tt_occupancy() == 4 ? (void*)gom_univ_tt_kernel<b, WC, 4> : (void*)gom_univ_tt_kernel<b, WC, 3>) \
-              : (void*)gom_univ_sliced_kernel<b, WC, MULTI>;
+    return tt ? tt_kernel_for_occupancy<b, WC>() : (void*)gom_univ_sliced_kernel<b, WC, MULTI>;
   switch (planes) {
     GOMIX_UNIV_CASE(4)
     GOMIX_UNIV_CASE(6)
@@ -699,6 +711,9 @@ void debug_timeline_univ(unsigned long long* out) {
 void debug_cta_stats_univ(unsigned long long* out) {
   GOMIX_CUDA(cudaDeviceSynchronize());
   GOMIX_CUDA(cudaMemcpyFromSymbol(out, g_ctastat, sizeof(unsigned long long) * kTimelineRows * kCtaStatMax * 4));
+  GOMIX_CUDA(cudaMemcpyFromSymbol(out + kTimelineRows * kCtaStatMax * 4, g_ttcount, sizeof(unsigned long long) * 16));
+  unsigned long long z[16] = {};
+  GOMIX_CUDA(cudaMemcpyToSymbol(g_ttcount, z, sizeof(z)));
 }
 
 void debug_probes_univ(unsigned long long* out, bool reset) {

@@ -26,13 +26,36 @@ for _ in range(30):
     E.run_generation()
 L = lib()
 L.gomix_debug_cta_stats.argtypes = [C.c_void_p]
-buf = np.zeros(4 * 1024 * 4, dtype=np.uint64)
+buf = np.zeros(4 * 1024 * 4 + 16, dtype=np.uint64)
+CNT = ["batches", "words with accepts", "words with strict improvements", "hash: sparse path", "hash: table path",
+       "hash: sum of max accepted sets per solution", "batches with accepts", "words with elitist copies",
+       "accepted pairs", "sets with accepts (per word)"]
+
+
+def counters(label):
+    c = buf[4 * 1024 * 4:].astype(np.float64)
+    b = max(c[0], 1)
+    out = {"phase": label, "batches": int(c[0])}
+    for i in range(1, 10):
+        out[CNT[i] + " per batch"] = round(c[i] / b, 3)
+    print(json.dumps(out))
+
+
+# path counters: a fresh population's first generations, then the steady state
+E2 = G.GpuParallelEngine(P, n, 2, mode="philox")
+L.gomix_debug_cta_stats.argtypes = [C.c_void_p]
+L.gomix_debug_cta_stats(C.c_void_p(buf.ctypes.data))  # reset
+for g in range(1, 6):
+    E2.run_generation()
+    L.gomix_debug_cta_stats(C.c_void_p(buf.ctypes.data))
+    counters(f"fresh population, generation {g}")
 for rep in range(3):
     buf[:] = 0
     E.run_generation_async()
     E.synchronize()
     L.gomix_debug_cta_stats(C.c_void_p(buf.ctypes.data))
-    st = buf.reshape(4, 1024, 4).astype(np.float64)
+    counters(f"generation {31 + rep} (steady state)")
+    st = buf[:4 * 1024 * 4].reshape(4, 1024, 4).astype(np.float64)
     for r in (1, 2):
         rows = st[r][st[r][:, 2] > 0]
         if len(rows) == 0:

@@ -32,12 +32,15 @@ buf = (C.c_ulonglong * 160)()
 L = lib()
 L.gomix_debug_timeline.argtypes = [C.c_void_p]
 names = ["cta start", "prologue done", "warp 0 batches done", "cta flushed", "epilogue start", "epilogue end",
-         "all warps' batches done", "dependency wait over"]
+         "all warps' batches done", "dependency wait over", "epilogue committed", "epilogue control block done",
+         "scan chunk maxima", "scan done", "prologue loads back"]
 
 
 def rows_of(t0, r):
     row = {}
     for i, nm in enumerate(names):
+        if nm == "-":
+            continue
         lo, hi = buf[32 * r + 2 * i], buf[32 * r + 2 * i + 1]
         if hi == 0:
             continue
