@@ -62,12 +62,24 @@ __device__ __forceinline__ void timeline_set_row(int32_t row) {
   if (threadIdx.x == 0) s_tl_row = row;
 #endif
 }
+// SM cycle stamps of the epilogue CTA (probes builds): point i, thread 0
+static __device__ long long g_epiclk[16];
+__device__ __forceinline__ void epi_clock(uint32_t i) {
+#ifdef GOMIX_PROBES
+  if (threadIdx.x == 0 && i < 16) {
+    long long t;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t) : : "memory");
+    g_epiclk[i] = t;
+  }
+#endif
+}
 __device__ __forceinline__ void timeline_mark(uint32_t i, int32_t row = 0) {
+  epi_clock(i);
 #ifdef GOMIX_PROBES
   if (row == -1) row = s_tl_row;
   if (threadIdx.x == 0 && i < 16) {
     unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t) : : "memory");  // memory: no load/store moves across
     const int32_t r = row < 0 ? 0 : (row >= kTimelineRows ? kTimelineRows - 1 : row);
     atomicMin(&g_timeline[r * 32 + 2 * i], t);
     atomicMax(&g_timeline[r * 32 + 2 * i + 1], t);
@@ -393,9 +405,18 @@ static __device__ void elitist_scan(const EpiArgs& a, const double* s_fit,
     double cur = s_cur;
     int32_t best = -1;
     bool hit = false;
-    for (uint32_t base = 0; base < n; base += 32u) {
-      const uint32_t chunk = base >> 5;
+    // the chunks that can hold a record, found 32 at a time: the running
+    // elitist only rises, so a chunk whose maximum does not beat its value
+    // at scan start never will (steady state: none qualifies — the serial
+    // walk over all chunks cost ~150 cycles each, 10 us at n = 4096)
+    const double cur0 = cur;
+    for (uint32_t q = 0; q * 32u < nchunks; ++q) {
+     uint32_t cand = __ballot_sync(0xFFFFFFFFu, q * 32u + lane < nchunks && s_chunkmax[q * 32u + lane] > cur0);
+     while (cand) {
+      const uint32_t chunk = q * 32u + (uint32_t)(__ffs(cand) - 1);
+      cand &= cand - 1u;
       if (!(s_chunkmax[chunk] > cur)) continue;  // better() implies >
+      const uint32_t base = chunk * 32u;
       const uint32_t s = base + lane;
       const double f = s < n ? fit_at(s) : -INFINITY;
       uint32_t m = __ballot_sync(0xFFFFFFFFu, s < n && cmp_better(exact, f, cur));
@@ -411,6 +432,7 @@ static __device__ void elitist_scan(const EpiArgs& a, const double* s_fit,
         hit |= has_target && (cmp_better(exact, cur, target) || cmp_equal(exact, cur, target));
         m = __ballot_sync(0xFFFFFFFFu, s < n && lane > l && cmp_better(exact, f, cur));
       }
+     }
     }
     if (lane == 0) {
       c->n_impr = ni;

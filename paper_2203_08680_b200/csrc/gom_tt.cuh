@@ -11,11 +11,12 @@ namespace gomix_b200 {
 
 constexpr int kUnivWarps = 8;        // warps per CTA of the univariate kernels
 
-// Path counters of the batch loop (probes builds only; lane 0 adds v):
-// read with gomix_debug_cta_stats after the per-CTA records.
+// Path counters of the batch loop (builds with -DGOMIX_PROBES
+// -DGOMIX_PROBE_COUNTS only — the same-address atomics distort timing;
+// lane 0 adds v): read with gomix_debug_cta_stats after the per-CTA records.
 static __device__ unsigned long long g_ttcount[16];
 __device__ __forceinline__ void tt_count(uint32_t i, uint32_t v, uint32_t lane) {
-#ifdef GOMIX_PROBES
+#ifdef GOMIX_PROBE_COUNTS
   if (lane == 0 && v) atomicAdd(&g_ttcount[i], (unsigned long long)v);
 #endif
 }
@@ -277,7 +278,7 @@ __device__ __forceinline__ uint32_t tt_batches(const GomArgs& a, const TtPart& p
         any |= acc[j] != 0u;
       }
     }
-#ifdef GOMIX_PROBES
+#ifdef GOMIX_PROBE_COUNTS
     tt_count(0, 1, lane);
     tt_count(6, __any_sync(0xFFFFFFFFu, any) ? 1u : 0u, lane);
 #pragma unroll
@@ -357,7 +358,7 @@ __device__ __forceinline__ uint32_t tt_batches(const GomArgs& a, const TtPart& p
         // broadcast from its lane, saves the transpose but measured 11%
         // slower: registers spill; so did LT muxes for the elitist copies.)
         unsigned long long x1 = 0, x2 = 0;
-#ifdef GOMIX_PROBES
+#ifdef GOMIX_PROBE_COUNTS
         {
           const uint32_t mx = __reduce_max_sync(0xFFFFFFFFu, (uint32_t)__popc(accT));
           tt_count(mx <= kSparseKeys ? 3 : 4, 1, lane);

@@ -712,6 +712,7 @@ void debug_cta_stats_univ(unsigned long long* out) {
   GOMIX_CUDA(cudaDeviceSynchronize());
   GOMIX_CUDA(cudaMemcpyFromSymbol(out, g_ctastat, sizeof(unsigned long long) * kTimelineRows * kCtaStatMax * 4));
   GOMIX_CUDA(cudaMemcpyFromSymbol(out + kTimelineRows * kCtaStatMax * 4, g_ttcount, sizeof(unsigned long long) * 16));
+  GOMIX_CUDA(cudaMemcpyFromSymbol(out + kTimelineRows * kCtaStatMax * 4 + 16, g_epiclk, sizeof(long long) * 16));
   unsigned long long z[16] = {};
   GOMIX_CUDA(cudaMemcpyToSymbol(g_ttcount, z, sizeof(z)));
 }

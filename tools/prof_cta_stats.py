@@ -2,6 +2,8 @@
 
     python -m paper_2203_08680_b200.build --probes
     GOMIX_LIB=paper_2203_08680_b200/libgomix_b200_probes.so python tools/prof_cta_stats.py [c3]
+(path counters: a build with -DGOMIX_PROBES -DGOMIX_PROBE_COUNTS, e.g.
+python -m paper_2203_08680_b200.build --variant counts -DGOMIX_PROBES -DGOMIX_PROBE_COUNTS)
 
 One queued generation after warm-up; per launch (graph slot): the spread of
 the CTAs' batches-done times, batches per CTA, and finish time by SM and
@@ -26,7 +28,7 @@ for _ in range(30):
     E.run_generation()
 L = lib()
 L.gomix_debug_cta_stats.argtypes = [C.c_void_p]
-buf = np.zeros(4 * 1024 * 4 + 16, dtype=np.uint64)
+buf = np.zeros(4 * 1024 * 4 + 32, dtype=np.uint64)
 CNT = ["batches", "words with accepts", "words with strict improvements", "hash: sparse path", "hash: table path",
        "hash: sum of max accepted sets per solution", "batches with accepts", "words with elitist copies",
        "accepted pairs", "sets with accepts (per word)"]
@@ -55,6 +57,11 @@ for rep in range(3):
     E.synchronize()
     L.gomix_debug_cta_stats(C.c_void_p(buf.ctypes.data))
     counters(f"generation {31 + rep} (steady state)")
+    clk = buf[4 * 1024 * 4 + 16:].astype(np.int64)
+    # the last launch's epilogue CTA: cycles from epilogue start (point 4)
+    pts = {4: "epilogue start", 8: "committed", 9: "control block", 10: "chunk maxima", 11: "scan done",
+           5: "epilogue end"}
+    print(json.dumps({"epilogue cycles": {nm: int(clk[i] - clk[4]) for i, nm in pts.items() if clk[i]}}))
     st = buf[:4 * 1024 * 4].reshape(4, 1024, 4).astype(np.float64)
     for r in (1, 2):
         rows = st[r][st[r][:, 2] > 0]
