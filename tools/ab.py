@@ -31,7 +31,7 @@ n = {n} or cfg["n"]
 inst = G.generate_torus(cfg["width"], cfg["height"], cfg["weights"], 1)
 fos = G.univariate_fos(inst.num_vertices) if cfg["fos"] == "uni" else G.neighbourhood_fos(inst)
 P = G.GpuProblem(inst, fos)
-r = device_rate(G, P, n, gens={gens}, warm=10)
+r = device_rate(G, P, n, gens={gens}, warm=10, flush={flush})
 print("RESULT " + json.dumps(r))
 """
 
@@ -43,13 +43,14 @@ def main():
     ap.add_argument("--n", type=int, default=0)
     ap.add_argument("--rounds", type=int, default=5)
     ap.add_argument("--gens", type=int, default=200)
+    ap.add_argument("--flush", action="store_true", help="flush L2 between generations (the bench's condition)")
     args = ap.parse_args()
     specs = []
     for s in args.specs:
         name, _, envs = s.partition(":")
         env = dict(e.split("=", 1) for e in envs.split(",") if e)
         specs.append((name, env))
-    code = CHILD.format(root=ROOT, config=args.config, n=args.n, gens=args.gens)
+    code = CHILD.format(root=ROOT, config=args.config, n=args.n, gens=args.gens, flush=args.flush)
     res = {name: [] for name, _ in specs}
     for rnd in range(args.rounds):
         for name, env in specs:

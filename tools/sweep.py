@@ -33,7 +33,10 @@ def hbm_peak():
         return 6650.0
 
 
-def device_rate(G, P, n, gens=20, warm=3, seed=1, **kw):
+def device_rate(G, P, n, gens=20, warm=3, seed=1, flush=False, **kw):
+    """Queued Philox generations timed with CUDA events on the engine stream.
+    flush: write 256 MiB between generations (outside the events), the
+    bench's L2 condition."""
     import torch
 
     s = torch.cuda.Stream()
@@ -42,15 +45,28 @@ def device_rate(G, P, n, gens=20, warm=3, seed=1, **kw):
         E.run_generation_async()
     E.synchronize()
     _, st0, _ = E.group_counters()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(s)
-    for _ in range(gens):
-        E.run_generation_async()
-    e1.record(s)
-    E.synchronize()
-    torch.cuda.synchronize()
+    if flush:
+        buf = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(gens)]
+        with torch.cuda.stream(s):
+            for a, b in ev:
+                buf.fill_(1)
+                a.record(s)
+                E.run_generation_async()
+                b.record(s)
+        E.synchronize()
+        torch.cuda.synchronize()
+        ms = sum(a.elapsed_time(b) for a, b in ev)
+    else:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(gens):
+            E.run_generation_async()
+        e1.record(s)
+        E.synchronize()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
     _, st1, _ = E.group_counters()
-    ms = e0.elapsed_time(e1)
     steps = int((st1 - st0).sum())
     return {"population": n, "steps_per_s": steps / (ms / 1e3), "ms_per_generation": ms / gens,
             "kernel": E.kernel_name(), "elitist": E.elitist_fitness}
