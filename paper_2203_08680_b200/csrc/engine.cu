@@ -1668,6 +1668,12 @@ GOMIX_API int gomix_debug_timeline(unsigned long long* out) {
   });
 }
 
+// the persistent generation kernel's timeline, probes builds (gom_gen.cu
+// gen_mark): 128 words, first / last arrival per point; resets
+GOMIX_API int gomix_debug_gen_timeline(unsigned long long* out) {
+  return guarded([&] { debug_gen_timeline(out); });
+}
+
 // per-CTA record of the truth-table launches, probes builds: out[((r * 1024)
 // + cta) * 4 + {0: SM, 1: start ns, 2: batches done ns, 3: batches}], row r =
 // graph slot + 1 (0 = direct), 4 rows; then 16 batch-loop path counters

@@ -38,6 +38,23 @@ namespace {
 constexpr uint32_t kTagOrderGen = 0x4F524400u;
 __device__ unsigned long long g_cta_probe[8192];  // latency study: per-CTA arrival time and SM id  // same stream as begin_generation_kernel ("ORD")
 
+// Launch timeline of the persistent generation kernel (probes builds only):
+// point i = [2i] first / [2i+1] last arrival (%globaltimer ns) over every
+// caller; point 0 = CTA start, then per slot s points 1 + 6s + {0: unit
+// start, 1: unit done (lane 0 of every warp with a unit), 2: CTA flushed,
+// 3: barrier passed, 4: epilogue done (thread 0 of every CTA)}.
+__device__ unsigned long long g_gen_tl[128];
+__device__ __forceinline__ void gen_mark(uint32_t i, bool who) {
+#ifdef GOMIX_PROBES
+  if (who && i < 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t) : : "memory");
+    atomicMin(&g_gen_tl[2 * i], t);
+    atomicMax(&g_gen_tl[2 * i + 1], t);
+  }
+#endif
+}
+
 // Two-level grid barrier.  ~1,250 single-team CTAs arriving on one counter
 // serialise in one L2 slice (measured ~4 us per barrier on C2), so CTAs
 // arrive on kBarSub counters (one 128-byte line each), the last arriver of
@@ -146,10 +163,222 @@ __global__ void __launch_bounds__(LEAN ? 256 : (TEAM ? 32 * TW : 256), LEAN ? 3 
     s_h2[s] = a.h2[s];
   }
   __syncthreads();
+  gen_mark(0, threadIdx.x == 0);
 
   uint32_t slot = 0;
+  uint32_t ran = 0;   // groups whose epilogue ran (the accumulator rotation advances by this)
   LeanPre pre{};     // LEAN: the next group's first unit, prefetched before the barrier
   GroupDesc dnext{};  // the next group's descriptor, loaded before the barrier
+  if constexpr (LEAN) {
+    // LEAN: the epilogue of group t runs in ONE warp per CTA (the last one)
+    // while the other warps already work on group t + 1: a unit's donor draw
+    // and partial evaluation read only the rows committed before the barrier,
+    // so only its accept / commit waits for the epilogue (the gate: s_gate
+    // counts the epilogues done in this CTA; group t + 1's units pass at t + 1).
+    __shared__ uint32_t s_gate;
+    if (threadIdx.x == 0) s_gate = 0;
+    __syncthreads();
+    const uint32_t epi_warp = (blockDim.x >> 5) - 1u;
+    uint32_t* wsm = smem + (size_t)warp * kLeanSmemWords;
+    const uint32_t per_round = (gridDim.x * (blockDim.x >> 5)) / Wp;
+    // the epilogue of slot t: commit, accounting, chained scan (one warp)
+    auto epilogue = [&](uint32_t t) {
+      const uint32_t gi_t = s_order[t];
+      const uint32_t bt = (buf0 + t) % 3u;
+      const long long* Dt = ga.dfit + (size_t)bt * n * kAccStride;
+      const unsigned long long* DH1t = ga.dh + (size_t)bt * 2 * n * kAccStride;
+      const unsigned long long* DH2t = DH1t + (size_t)n * kAccStride;
+      const unsigned long long* CNTt = ga.cnt + 2 * bt;
+      const uint32_t zb = (bt + 2u) % 3u;  // group t - 1's accumulators: every CTA read them before barrier t
+      unsigned long long cnt_st = 0, cnt_ca = 0;
+      if (lane == 0) {
+        cnt_st = __ldcg(CNTt);
+        cnt_ca = __ldcg(CNTt + 1);
+      }
+#pragma unroll 4
+      for (uint32_t s = lane; s < n; s += 32u) {
+        const double f = s_fit[s] + (double)__ldcg(Dt + s * kAccStride);
+        const unsigned long long x1 = s_h1[s] ^ __ldcg(DH1t + s * kAccStride);
+        const unsigned long long x2 = s_h2[s] ^ __ldcg(DH2t + s * kAccStride);
+        s_fit[s] = f;
+        s_h1[s] = x1;
+        s_h2[s] = x2;
+        if (lead) {
+          a.epi.fit[s] = f;
+          a.epi.h1[s] = x1;
+          a.epi.h2[s] = x2;
+          ga.dfit[((size_t)zb * n + s) * kAccStride] = 0;
+          ga.dh[((size_t)zb * 2 * n + s) * kAccStride] = 0;
+          ga.dh[((size_t)zb * 2 * n + n + s) * kAccStride] = 0;
+        }
+      }
+      if (lead) {
+        if (lane == 0) {
+          ga.cnt[2 * zb] = 0;
+          ga.cnt[2 * zb + 1] = 0;
+        }
+        if (Wp > 1) {
+          unsigned int* z = ga.sib + (size_t)zb * ga.sib_stride;
+          for (uint32_t i = lane; i < ga.sib_stride; i += 32u) z[i] = 0u;
+        }
+      }
+      if (lane == 0) {
+        s_calls_total += cnt_ca;
+        s_run_steps += cnt_st;
+        s_run_calls += cnt_ca;
+        s_groups += 1;
+        if (lead) {
+          a.epi.gsteps[gi_t] += cnt_st;
+          a.epi.gcalls[gi_t] += cnt_ca;
+        }
+        if (b.has_budget && (double)s_calls_total / b.q >= b.max_evals && !s_stop) {
+          s_stop = 1;
+          s_stop_reason = GOMIX_STOP_BUDGET;
+        }
+      }
+      __syncwarp();
+      for (uint32_t ch = 0; ch * 32u < n; ++ch) {
+        const uint32_t s = ch * 32u + lane;
+        double f = s < n ? s_fit[s] : -INFINITY;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) f = fmax(f, __shfl_xor_sync(0xFFFFFFFFu, f, o));
+        if (lane == 0) s_chunkmax[ch] = f;
+      }
+      __syncwarp();
+      // chained elitist scan over all members in index order (:305-310)
+      double cur = s_elit_fit;
+      int32_t best = -1;
+      bool hit = false;
+      unsigned long long ni = s_nimpr;
+      const unsigned long long calls_now = s_calls_total;
+      for (uint32_t base = 0; base < n; base += 32u) {
+        if (!(s_chunkmax[base >> 5] > cur)) continue;  // better() implies >
+        const uint32_t s = base + lane;
+        const double f = s < n ? s_fit[s] : -INFINITY;
+        uint32_t m = __ballot_sync(0xFFFFFFFFu, s < n && f > cur);
+        while (m) {
+          const uint32_t l = __ffs(m) - 1;
+          cur = __shfl_sync(0xFFFFFFFFu, f, l);
+          best = (int32_t)(base + l);
+          if (lead && lane == 0 && ni < a.epi.impr_cap) {
+            a.epi.impr[ni].fit = cur;
+            a.epi.impr[ni].calls = calls_now;
+          }
+          ++ni;
+          hit |= b.has_target && cur >= b.target;
+          m = __ballot_sync(0xFFFFFFFFu, s < n && lane > l && f > cur);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        s_nimpr = ni;
+        if (hit && !s_stop) {
+          s_stop = 1;
+          s_stop_reason = GOMIX_STOP_TARGET;
+        }
+        if (best >= 0) {  // new elitist: member `best` (snapshot taken copy-on-write)
+          s_elit_fit = cur;
+          s_elit_src = best;
+          s_eh1 = s_h1[best];
+          s_eh2 = s_h2[best];
+          s_ver += 1;
+        }
+        __threadfence_block();
+        *(volatile uint32_t*)&s_gate = t + 1u;  // group t + 1's units may accept / commit
+      }
+      __syncwarp();
+    };
+    bool aborted = false;
+    for (; slot < ga.k; ++slot) {
+      const uint32_t gi = s_order[slot];
+      const GroupDesc d = slot == 0 ? a.groups[gi] : dnext;
+      const uint4* gmeta = a.gmeta + d.g0;
+      const uint32_t bi = (buf0 + slot) % 3u;
+      long long* D = ga.dfit + (size_t)bi * n * kAccStride;
+      unsigned long long* DH1 = ga.dh + (size_t)bi * 2 * n * kAccStride;
+      unsigned long long* DH2 = DH1 + (size_t)n * kAccStride;
+      unsigned long long* CNT = ga.cnt + 2 * bi;
+      if (warp == epi_warp && slot > 0) epilogue(slot - 1u);
+      // group-start state of this slot, read once the gate opens
+      auto gate = [&](uint32_t s) -> LeanGate {
+        if (lane == 0)
+          while (*(volatile uint32_t*)&s_gate < slot) __nanosleep(20);
+        __syncwarp();
+        __threadfence_block();
+        LeanGate g;
+        g.stop = *(volatile int32_t*)&s_stop != 0;
+        const unsigned long long e1 = *(volatile unsigned long long*)&s_eh1;
+        const unsigned long long e2 = *(volatile unsigned long long*)&s_eh2;
+        g.is_elit = s < n && ((volatile unsigned long long*)s_h1)[s] == e1 &&
+                    ((volatile unsigned long long*)s_h2)[s] == e2;
+        g.esrc = *(volatile int32_t*)&s_elit_src;
+        g.ever_cur = *(volatile uint32_t*)&s_ver;
+        return g;
+      };
+      long long acc = 0;
+      unsigned long long dh1 = 0, dh2 = 0, calls = 0;
+      uint32_t steps = 0;
+      for (uint32_t p = gwarp / Wp; p < d.G; p += per_round) {
+        const LeanPre cur = (p == gwarp / Wp && slot > 0) ? pre : lean_prefetch(a, gmeta, p, lane);
+        gen_mark(1 + 6 * slot, lane == 0);
+        gom_lean_unit(a, p, cur, lean_w, gen, wsm, lane, gate, false, acc, dh1, dh2, steps, calls,
+                      Wp > 1 ? ga.sib + (size_t)bi * ga.sib_stride : nullptr);
+        gen_mark(2 + 6 * slot, lane == 0);
+      }
+      // the next group's first unit: plan inputs in flight during the barrier
+      if (slot + 1 < ga.k) {
+        dnext = a.groups[s_order[slot + 1]];
+        if (gwarp / Wp < dnext.G) pre = lean_prefetch(a, a.gmeta + dnext.g0, gwarp / Wp, lane);
+      }
+      if (threadIdx.x == 0) {
+        s_steps = 0;
+        s_calls = 0;
+      }
+      __syncthreads();  // this CTA's units and the epilogue of slot - 1 are done
+      if (s_stop) {     // stopped by the epilogue of slot - 1: nothing of this slot was committed
+        aborted = true;
+        break;
+      }
+      {
+        const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, steps);
+        const uint32_t wc = __reduce_add_sync(0xFFFFFFFFu, (uint32_t)calls);
+        if (lane == 0 && (ws | wc)) {
+          atomicAdd(reinterpret_cast<unsigned int*>(&s_steps), ws);
+          atomicAdd(reinterpret_cast<unsigned int*>(&s_calls), wc);
+        }
+      }
+      const uint32_t s0 = lean_w * 32u + lane;
+      if (s0 < n) {
+        if (acc) atomicAdd(reinterpret_cast<unsigned long long*>(D + s0 * kAccStride), (unsigned long long)acc);
+        if (dh1 | dh2) {
+          atomicXor(DH1 + s0 * kAccStride, dh1);
+          atomicXor(DH2 + s0 * kAccStride, dh2);
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0 && (s_steps | s_calls)) {
+        atomicAdd(CNT, s_steps);
+        atomicAdd(CNT + 1, s_calls);
+      }
+      gen_mark(3 + 6 * slot, threadIdx.x == 0);
+      grid_barrier(ga.bar, gridDim.x);
+      gen_mark(4 + 6 * slot, threadIdx.x == 0);
+    }
+    if (!aborted) {
+      if (warp == epi_warp) epilogue(ga.k - 1u);
+      __syncthreads();
+      ran = ga.k;
+    } else {
+      // the aborted slot's units arrived on its sibling counters: zero them
+      // once every CTA is past its units (all CTAs abort at the same slot)
+      ran = slot;
+      grid_barrier(ga.bar, gridDim.x);
+      if (lead && Wp > 1) {
+        unsigned int* z = ga.sib + (size_t)((buf0 + slot) % 3u) * ga.sib_stride;
+        for (uint32_t i = threadIdx.x; i < ga.sib_stride; i += blockDim.x) z[i] = 0u;
+      }
+    }
+  } else {
   for (; slot < ga.k; ++slot) {
     const uint32_t gi = s_order[slot];
     const GroupDesc d = slot == 0 ? a.groups[gi] : dnext;
@@ -181,20 +410,7 @@ __global__ void __launch_bounds__(LEAN ? 256 : (TEAM ? 32 * TW : 256), LEAN ? 3 
     }
     uint32_t steps = 0;
     unsigned long long calls = 0;
-    if constexpr (LEAN) {
-      uint32_t* wsm = smem + (size_t)warp * kLeanSmemWords;
-      const uint32_t per_round = (gridDim.x * (blockDim.x >> 5)) / Wp;
-      for (uint32_t p = gwarp / Wp; p < d.G; p += per_round) {
-        const LeanPre cur = (p == gwarp / Wp && slot > 0) ? pre : lean_prefetch(a, gmeta, p, lane);
-        gom_lean_unit(a, p, cur, lean_w, gen, wsm, lane, is_elit[0], esrc, ever_cur, false, acc[0], dh1[0],
-                      dh2[0], steps, calls, Wp > 1 ? ga.sib + (size_t)bi * ga.sib_stride : nullptr);
-      }
-      // the next group's first unit: plan inputs in flight during the barrier
-      if (slot + 1 < ga.k) {
-        dnext = a.groups[s_order[slot + 1]];
-        if (gwarp / Wp < dnext.G) pre = lean_prefetch(a, a.gmeta + dnext.g0, gwarp / Wp, lane);
-      }
-    } else {
+    {  // teams (the LEAN kernel runs the overlapped loop above)
       for (uint32_t p = blockIdx.x * teams_per_cta + team; p < d.G; p += gridDim.x * teams_per_cta)
         gom_general_set<WPT, true, TEAM>(a, p, gmeta, gen, stage, lane, tw, wit, tid_team, team_threads,
                                          teams_per_cta, team, true, false, false, is_elit, pfit, esrc, ever_cur,
@@ -244,7 +460,9 @@ __global__ void __launch_bounds__(LEAN ? 256 : (TEAM ? 32 * TW : 256), LEAN ? 3 
       g_cta_probe[2 * blockIdx.x + 1] = smid;
     }
 #endif
+    gen_mark(3 + 6 * slot, threadIdx.x == 0);
     grid_barrier(ga.bar, gridDim.x);
+    gen_mark(4 + 6 * slot, threadIdx.x == 0);
     probe(a.exp_flags, 17 + 4 * slot);
 
     // ---- epilogue (every CTA): fitness / hash commit ------------------------
@@ -346,8 +564,11 @@ __global__ void __launch_bounds__(LEAN ? 256 : (TEAM ? 32 * TW : 256), LEAN ? 3 
       }
     }
     __syncthreads();
+    gen_mark(5 + 6 * slot, threadIdx.x == 0);
     probe(a.exp_flags, 18 + 4 * slot);
     if (s_stop) break;
+  }
+  ran = slot < ga.k ? slot + 1 : ga.k;
   }
 
   if (lead && threadIdx.x == 0) {
@@ -373,7 +594,7 @@ __global__ void __launch_bounds__(LEAN ? 256 : (TEAM ? 32 * TW : 256), LEAN ? 3 
     c->gen_counter = gen + 1;
     // the accumulator index itself (mod 3), not a running count: a count
     // would wrap at 2^32, where 2^32 = 1 (mod 3) breaks the rotation
-    c->gen_buf = (buf0 + (slot < ga.k ? slot + 1 : ga.k)) % 3u;
+    c->gen_buf = (buf0 + ran) % 3u;
     for (uint32_t i = 0; i < ga.k; ++i) ga.order[i] = s_order[i];
   }
 }
@@ -406,6 +627,18 @@ void* gen_kernel(int wpt, bool team, int tw, bool lean) {
 void debug_cta_probes(unsigned long long* out) {
   GOMIX_CUDA(cudaDeviceSynchronize());
   GOMIX_CUDA(cudaMemcpyFromSymbol(out, g_cta_probe, sizeof(unsigned long long) * 8192));
+}
+
+// the generation kernel's timeline (probes builds): 128 words, then reset
+void debug_gen_timeline(unsigned long long* out) {
+  GOMIX_CUDA(cudaDeviceSynchronize());
+  GOMIX_CUDA(cudaMemcpyFromSymbol(out, g_gen_tl, sizeof(unsigned long long) * 128));
+  unsigned long long z[128];
+  for (int i = 0; i < 64; ++i) {
+    z[2 * i] = ~0ull;
+    z[2 * i + 1] = 0ull;
+  }
+  GOMIX_CUDA(cudaMemcpyToSymbol(g_gen_tl, z, sizeof(z)));
 }
 
 void debug_probes_gen(unsigned long long* out, bool reset) {

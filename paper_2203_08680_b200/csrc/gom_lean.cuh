@@ -51,11 +51,27 @@ __device__ __forceinline__ LeanPre lean_prefetch(const GomArgs& a, const uint4* 
   return r;
 }
 
+// What the accept / commit step needs from the previous colour group's
+// epilogue: whether it stopped the run, and this lane's group-start
+// "parent == elitist" with the elitist's column and snapshot version.
+struct LeanGate {
+  bool stop;
+  bool is_elit;
+  int32_t esrc;
+  uint32_t ever_cur;
+};
+
+// gate(s) is called once per unit by every lane (s = its solution) right
+// before the accept decision: everything up to there (donor draw, partial
+// evaluation) depends only on the group-start rows, so it overlaps the
+// previous group's epilogue when the caller runs that concurrently.  A gate
+// that reports stop ends the unit with nothing committed or counted.
+template <class Gate>
 __device__ __forceinline__ void gom_lean_unit(const GomArgs& a, uint32_t p, const LeanPre& pre, uint32_t w,
-                                              uint32_t generation, uint32_t* wsm, uint32_t lane, bool is_elit,
-                                              int32_t esrc, uint32_t ever_cur, bool record, long long& acc,
-                                              unsigned long long& dh1, unsigned long long& dh2, uint32_t& steps,
-                                              unsigned long long& calls, unsigned int* sib = nullptr) {
+                                              uint32_t generation, uint32_t* wsm, uint32_t lane, Gate&& gate,
+                                              bool record, long long& acc, unsigned long long& dh1,
+                                              unsigned long long& dh2, uint32_t& steps, unsigned long long& calls,
+                                              unsigned int* sib = nullptr) {
   constexpr uint32_t FULL = 0xFFFFFFFFu;
   const uint32_t Wp = a.Wp, n = a.n, lwp = 31u - __clz(Wp);
   const uint4 gm = pre.gm;
@@ -191,6 +207,14 @@ __device__ __forceinline__ void gom_lean_unit(const GomArgs& a, uint32_t p, cons
   const int32_t delta = (e1 == e0) ? 0 : di;
 
   // ---- phases 3 + 4: accept (:194-214, exact comparator) and commit (:221-247)
+  const LeanGate gt = gate(s);
+  if (gt.stop) {
+    __syncwarp();
+    return;
+  }
+  const bool is_elit = gt.is_elit;
+  const int32_t esrc = gt.esrc;
+  const uint32_t ever_cur = gt.ever_cur;
   const bool accept = present && (delta > 0 || (delta == 0 && !is_elit));
   const uint32_t accw = __ballot_sync(FULL, accept);
   if (sib != nullptr) {

@@ -404,6 +404,7 @@ void launch_peer_elitist(const PeerArgs* d_peer, DevCtl* ctl, uint32_t* elit, ui
 void launch_sum_ones(const uint32_t* stage, uint32_t R, uint64_t nv, uint32_t* ones, cudaStream_t s);
 void debug_probes(unsigned long long* out, bool reset);
 void debug_probes_gen(unsigned long long* out, bool reset);
+void debug_gen_timeline(unsigned long long* out);
 void debug_probes_univ(unsigned long long* out, bool reset);
 void debug_timeline_univ(unsigned long long* out);  // gom_univ_tt_kernel launch timeline (probes builds), 4 x 32
 void debug_timeline_gom(unsigned long long* out);   // begin_generation_kernel (points 0, 1), 32
