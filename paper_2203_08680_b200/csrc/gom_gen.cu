@@ -92,6 +92,36 @@ __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nbl
   __syncthreads();
 }
 
+// Flat grid barrier on a monotonic 64-bit counter (bar word 1536, never
+// reset): every CTA adds 1 with acq_rel semantics and waits until the
+// counter reaches the next multiple of the grid size — the last arrival
+// releases everyone with no further hop (the two-level barrier above needs
+// two more dependent atomics and a generation store after the last arrival).
+__device__ __forceinline__ void grid_barrier_flat(unsigned int* bar, unsigned int nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long* ctr = reinterpret_cast<unsigned long long*>(bar + 1536);
+    unsigned long long old;
+    asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;" : "=l"(old) : "l"(ctr) : "memory");
+    const unsigned long long target = (old / nblocks + 1ull) * nblocks;
+    if (old + 1ull != target) {
+      unsigned long long v;
+      do {
+        __nanosleep(32);
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+      } while (v < target);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+#ifdef GOMIX_GEN_TWO_LEVEL
+#define GOMIX_GEN_BARRIER grid_barrier
+#else
+#define GOMIX_GEN_BARRIER grid_barrier_flat
+#endif
+
 }  // namespace
 
 // Every set of a group should get its own team in ONE wave (a second set per
@@ -361,7 +391,7 @@ __global__ void __launch_bounds__(LEAN ? 256 : (TEAM ? 32 * TW : 256), LEAN ? 3 
         atomicAdd(CNT + 1, s_calls);
       }
       gen_mark(3 + 6 * slot, threadIdx.x == 0);
-      grid_barrier(ga.bar, gridDim.x);
+      GOMIX_GEN_BARRIER(ga.bar, gridDim.x);
       gen_mark(4 + 6 * slot, threadIdx.x == 0);
     }
     if (!aborted) {
@@ -372,7 +402,7 @@ __global__ void __launch_bounds__(LEAN ? 256 : (TEAM ? 32 * TW : 256), LEAN ? 3 
       // the aborted slot's units arrived on its sibling counters: zero them
       // once every CTA is past its units (all CTAs abort at the same slot)
       ran = slot;
-      grid_barrier(ga.bar, gridDim.x);
+      GOMIX_GEN_BARRIER(ga.bar, gridDim.x);
       if (lead && Wp > 1) {
         unsigned int* z = ga.sib + (size_t)((buf0 + slot) % 3u) * ga.sib_stride;
         for (uint32_t i = threadIdx.x; i < ga.sib_stride; i += blockDim.x) z[i] = 0u;
@@ -461,7 +491,7 @@ __global__ void __launch_bounds__(LEAN ? 256 : (TEAM ? 32 * TW : 256), LEAN ? 3 
     }
 #endif
     gen_mark(3 + 6 * slot, threadIdx.x == 0);
-    grid_barrier(ga.bar, gridDim.x);
+    GOMIX_GEN_BARRIER(ga.bar, gridDim.x);
     gen_mark(4 + 6 * slot, threadIdx.x == 0);
     probe(a.exp_flags, 17 + 4 * slot);
 
