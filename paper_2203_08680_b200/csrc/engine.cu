@@ -568,7 +568,7 @@ struct gomix_gpu_engine {
       gen_lean = P->max_f <= 32 && !(flags & GOMIX_FLAG_LANE_PER_SOLUTION);
       const int gblock = gen_lean ? 256 : (int)block;
       const size_t gsmem = gen_lean ? (size_t)gen_lean_smem() : smem;
-      const int per = gen_kernel_max_blocks((int)wpt, tw > 1, gblock, gsmem, gen_lean);
+      const int per = gen_kernel_max_blocks(gen_lean ? (int)Wp : (int)wpt, tw > 1, gblock, gsmem, gen_lean);
       const uint64_t want = gen_lean ? std::max<uint64_t>(1, (max_group * Wp + 7) / 8)
                                      : std::max<uint64_t>(1, (max_group + teams - 1) / teams);
       if (per >= 1) {
@@ -726,7 +726,7 @@ struct gomix_gpu_engine {
       e1 = take_event();
       GOMIX_CUDA(cudaEventRecord(e0, stream));
     }
-    launch_generation_kernel(a, ga, (int)wpt, tw > 1, gen_grid, gen_lean ? 256 : (int)block,
+    launch_generation_kernel(a, ga, gen_lean ? (int)Wp : (int)wpt, tw > 1, gen_grid, gen_lean ? 256 : (int)block,
                              gen_lean ? (size_t)gen_lean_smem() : smem, stream, gen_lean);
     ++launches;
     if (e1) {

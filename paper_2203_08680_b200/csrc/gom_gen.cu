@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(LEAN ? 256 : (TEAM ? 32 * TW : 256), LEAN ? 3 
       for (uint32_t p = gwarp / Wp; p < d.G; p += per_round) {
         const LeanPre cur = (p == gwarp / Wp && slot > 0) ? pre : lean_prefetch(a, gmeta, p, lane);
         gen_mark(1 + 6 * slot, lane == 0);
-        gom_lean_unit(a, p, cur, lean_w, gen, wsm, lane, gate, false, acc, dh1, dh2, steps, calls,
+        gom_lean_unit<(uint32_t)WPT>(a, p, cur, lean_w, gen, wsm, lane, gate, false, acc, dh1, dh2, steps, calls,
                       Wp > 1 ? ga.sib + (size_t)bi * ga.sib_stride : nullptr);
         gen_mark(2 + 6 * slot, lane == 0);
       }
@@ -634,7 +634,15 @@ __global__ void __launch_bounds__(LEAN ? 256 : (TEAM ? 32 * TW : 256), LEAN ? 3 
 // ---------------------------------------------------------------------------
 namespace {
 void* gen_kernel(int wpt, bool team, int tw, bool lean) {
-  if (lean) return (void*)gom_generation_kernel<1, false, 1, true>;
+  if (lean) {  // wpt = the population's words per row (Wp)
+    switch (wpt) {
+      case 1: return (void*)gom_generation_kernel<1, false, 1, true>;
+      case 2: return (void*)gom_generation_kernel<2, false, 1, true>;
+      case 4: return (void*)gom_generation_kernel<4, false, 1, true>;
+      case 8: return (void*)gom_generation_kernel<8, false, 1, true>;
+    }
+    return nullptr;
+  }
   if (team) {
     if (wpt != 1) return nullptr;
     switch (tw) {

@@ -66,14 +66,17 @@ struct LeanGate {
 // evaluation) depends only on the group-start rows, so it overlaps the
 // previous group's epilogue when the caller runs that concurrently.  A gate
 // that reports stop ends the unit with nothing committed or counted.
-template <class Gate>
+// MW: the population words the kernel was built for (>= Wp; the donor
+// search's per-word masks are unrolled over MW).
+template <uint32_t MW, class Gate>
 __device__ __forceinline__ void gom_lean_unit(const GomArgs& a, uint32_t p, const LeanPre& pre, uint32_t w,
                                               uint32_t generation, uint32_t* wsm, uint32_t lane, Gate&& gate,
                                               bool record, long long& acc, unsigned long long& dh1,
                                               unsigned long long& dh2, uint32_t& steps, unsigned long long& calls,
                                               unsigned int* sib = nullptr) {
   constexpr uint32_t FULL = 0xFFFFFFFFu;
-  const uint32_t Wp = a.Wp, n = a.n, lwp = 31u - __clz(Wp);
+  constexpr uint32_t Wp = MW;  // the kernel is instantiated for the population's row width (a.Wp)
+  const uint32_t n = a.n, lwp = 31u - __clz(Wp);
   const uint4 gm = pre.gm;
   const uint32_t sid = gm.x, f = gm.w >> 24;
   const uint32_t* vars = a.set_vars + gm.y;
@@ -131,25 +134,25 @@ __device__ __forceinline__ void gom_lean_unit(const GomArgs& a, uint32_t p, cons
     } else {
       // k-th member (k uniform) among those differing from m on F, in one
       // pass over F's rows: dwa[wg] = members of pool word wg that differ
-      uint32_t dwa[kLeanMaxWords];
+      uint32_t dwa[MW];
 #pragma unroll
-      for (uint32_t wg = 0; wg < kLeanMaxWords; ++wg) dwa[wg] = 0;
+      for (uint32_t wg = 0; wg < MW; ++wg) dwa[wg] = 0;
       for (uint32_t jv = 0; jv < f; ++jv) {
         const uint32_t mk = 0u - ((m >> jv) & 1u);
 #pragma unroll
-        for (uint32_t wg = 0; wg < kLeanMaxWords; ++wg)
+        for (uint32_t wg = 0; wg < MW; ++wg)
           if (wg < Wp) dwa[wg] |= rowsW[jv * Wp + wg] ^ mk;
       }
       uint32_t total = 0;
 #pragma unroll
-      for (uint32_t wg = 0; wg < kLeanMaxWords; ++wg) {
+      for (uint32_t wg = 0; wg < MW; ++wg) {
         if (wg < Wp) dwa[wg] &= valid_mask(wg, n);
         total += __popc(dwa[wg]);
       }
       if (total > 0) {
         uint32_t kth = bounded(hi64(rr), total);
 #pragma unroll
-        for (uint32_t wg = 0; wg < kLeanMaxWords; ++wg) {
+        for (uint32_t wg = 0; wg < MW; ++wg) {
           const uint32_t c = __popc(dwa[wg]);
           if (d < 0) {
             if (kth < c)
