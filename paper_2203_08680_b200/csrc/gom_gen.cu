@@ -41,7 +41,7 @@ __device__ unsigned long long g_cta_probe[8192];  // latency study: per-CTA arri
 // Launch timeline of the persistent generation kernel (probes builds only):
 // point i = [2i] first / [2i+1] last arrival (%globaltimer ns) over every
 // caller; point 0 = CTA start, then per slot s points 1 + 6s + {0: unit
-// start, 1: unit done (lane 0 of every warp with a unit), 2: CTA flushed,
+// start, 1: unit done (warp 0 of every CTA with a unit), 2: CTA flushed,
 // 3: barrier passed, 4: epilogue done (thread 0 of every CTA)}.
 __device__ unsigned long long g_gen_tl[128];
 __device__ __forceinline__ void gen_mark(uint32_t i, bool who) {
@@ -111,9 +111,11 @@ __device__ __forceinline__ void grid_barrier_flat(unsigned int* bar, unsigned in
         asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
       } while (v < target);
     }
+#ifdef GOMIX_GEN_BAR_FENCE
     __threadfence();
+#endif
   }
-  __syncthreads();
+  __syncthreads();  // the acquire above orders every thread's later loads (the CTA shares the SM's L1)
 }
 
 #ifdef GOMIX_GEN_TWO_LEVEL
@@ -156,8 +158,14 @@ __global__ void __launch_bounds__(LEAN ? 256 : (TEAM ? 32 * TW : 256), LEAN ? 3 
   uint32_t* stage = smem + (size_t)team * a.stage_words;
   // LEAN units go to warps in warp-major order (slot w of every CTA before
   // slot w + 1), so every SM gets the same number of busy warps
-  const uint32_t gwarp = LEAN ? warp * gridDim.x + blockIdx.x : blockIdx.x * (blockDim.x >> 5) + warp;
-  const uint32_t lean_w = LEAN ? gwarp % Wp : 0u;  // the grid's warp count is a multiple of Wp
+  // LEAN: the Wp sibling warps of a unit (one per population word) are
+  // adjacent warps of one CTA (they meet at a named barrier before
+  // committing), and units go to sibling groups warp-major (group g of every
+  // CTA before group g + 1), so every SM gets the same number of busy warps:
+  // unit p = (warp / Wp) * gridDim + blockIdx, word = warp % Wp
+  const uint32_t gwarp = LEAN ? (warp / Wp) * (gridDim.x * Wp) + blockIdx.x * Wp + warp % Wp
+                              : blockIdx.x * (blockDim.x >> 5) + warp;
+  const uint32_t lean_w = LEAN ? gwarp % Wp : 0u;  // Wp divides the CTA's 8 warps
   // solution of this thread's word j
   auto sol = [&](int j) -> uint32_t { return LEAN ? lean_w * 32u + lane : (wit + tw * (uint32_t)j) * 32u + lane; };
   const BeginArgs& b = ga.begin;
@@ -246,10 +254,6 @@ __global__ void __launch_bounds__(LEAN ? 256 : (TEAM ? 32 * TW : 256), LEAN ? 3 
         if (lane == 0) {
           ga.cnt[2 * zb] = 0;
           ga.cnt[2 * zb + 1] = 0;
-        }
-        if (Wp > 1) {
-          unsigned int* z = ga.sib + (size_t)zb * ga.sib_stride;
-          for (uint32_t i = lane; i < ga.sib_stride; i += 32u) z[i] = 0u;
         }
       }
       if (lane == 0) {
@@ -350,10 +354,10 @@ __global__ void __launch_bounds__(LEAN ? 256 : (TEAM ? 32 * TW : 256), LEAN ? 3 
       uint32_t steps = 0;
       for (uint32_t p = gwarp / Wp; p < d.G; p += per_round) {
         const LeanPre cur = (p == gwarp / Wp && slot > 0) ? pre : lean_prefetch(a, gmeta, p, lane);
-        gen_mark(1 + 6 * slot, lane == 0);
+        gen_mark(1 + 6 * slot, lane == 0 && warp == 0);
         gom_lean_unit<(uint32_t)WPT>(a, p, cur, lean_w, gen, wsm, lane, gate, false, acc, dh1, dh2, steps, calls,
-                      Wp > 1 ? ga.sib + (size_t)bi * ga.sib_stride : nullptr);
-        gen_mark(2 + 6 * slot, lane == 0);
+                      1u + warp / Wp);
+        gen_mark(2 + 6 * slot, lane == 0 && warp == 0);
       }
       // the next group's first unit: plan inputs in flight during the barrier
       if (slot + 1 < ga.k) {
@@ -399,14 +403,7 @@ __global__ void __launch_bounds__(LEAN ? 256 : (TEAM ? 32 * TW : 256), LEAN ? 3 
       __syncthreads();
       ran = ga.k;
     } else {
-      // the aborted slot's units arrived on its sibling counters: zero them
-      // once every CTA is past its units (all CTAs abort at the same slot)
-      ran = slot;
-      GOMIX_GEN_BARRIER(ga.bar, gridDim.x);
-      if (lead && Wp > 1) {
-        unsigned int* z = ga.sib + (size_t)((buf0 + slot) % 3u) * ga.sib_stride;
-        for (uint32_t i = threadIdx.x; i < ga.sib_stride; i += blockDim.x) z[i] = 0u;
-      }
+      ran = slot;  // stopped by the epilogue of slot - 1
     }
   } else {
   for (; slot < ga.k; ++slot) {
@@ -523,10 +520,6 @@ __global__ void __launch_bounds__(LEAN ? 256 : (TEAM ? 32 * TW : 256), LEAN ? 3 
       const uint32_t zb = (bi + 2u) % 3u;
       ga.cnt[2 * zb] = 0;
       ga.cnt[2 * zb + 1] = 0;
-    }
-    if (LEAN && lead && Wp > 1) {  // the previous group's sibling counters, same rotation as D
-      unsigned int* z = ga.sib + (size_t)((bi + 2u) % 3u) * ga.sib_stride;
-      for (uint32_t i = threadIdx.x; i < ga.sib_stride; i += blockDim.x) z[i] = 0u;
     }
     if (threadIdx.x == 0) {
       const unsigned long long st = cnt_st, ca = cnt_ca;

@@ -73,7 +73,7 @@ __device__ __forceinline__ void gom_lean_unit(const GomArgs& a, uint32_t p, cons
                                               uint32_t generation, uint32_t* wsm, uint32_t lane, Gate&& gate,
                                               bool record, long long& acc, unsigned long long& dh1,
                                               unsigned long long& dh2, uint32_t& steps, unsigned long long& calls,
-                                              unsigned int* sib = nullptr) {
+                                              uint32_t sib_bar = 0u) {
   constexpr uint32_t FULL = 0xFFFFFFFFu;
   constexpr uint32_t Wp = MW;  // the kernel is instantiated for the population's row width (a.Wp)
   const uint32_t n = a.n, lwp = 31u - __clz(Wp);
@@ -102,13 +102,12 @@ __device__ __forceinline__ void gom_lean_unit(const GomArgs& a, uint32_t p, cons
   }
   if (lane < f) zobrist(vj, zW[2 * lane], zW[2 * lane + 1]);
   __syncwarp();
-  // The Wp warps of this set (one per population word) each read ALL words
-  // of F's rows as the group-start donor pool, and each commits its own word.
-  // Arrive once this warp's copy is complete; commits wait for every sibling
-  // (below), so no sibling reads a word already committed.  The siblings
-  // walk the same unit sequence and are co-resident (persistent kernel), so
-  // the wait cannot deadlock.
-  if (sib != nullptr && lane == 0) atomicAdd(sib + p, 1u);
+  // The Wp warps of this set (one per population word, warps of one CTA)
+  // each read ALL words of F's rows as the group-start donor pool and each
+  // commits its own word: they meet at named barrier sib_bar (1 + their
+  // index, 32 Wp threads) before committing, so no sibling reads a word
+  // already committed.  The siblings walk the same unit sequence and take
+  // the same gate decision, so every barrier is reached by all of them.
   // ---- every member's pattern on F: lane jv holds row jv, one transpose per word
   for (uint32_t wg = 0; wg < Wp; ++wg) {
     const uint32_t r = lane < f ? rowsW[lane * Wp + wg] : 0u;
@@ -220,11 +219,7 @@ __device__ __forceinline__ void gom_lean_unit(const GomArgs& a, uint32_t p, cons
   const uint32_t ever_cur = gt.ever_cur;
   const bool accept = present && (delta > 0 || (delta == 0 && !is_elit));
   const uint32_t accw = __ballot_sync(FULL, accept);
-  if (sib != nullptr) {
-    if (lane == 0)
-      while (*(volatile unsigned int*)(sib + p) < Wp) __nanosleep(32);
-    __syncwarp();
-  }
+  if (Wp > 1 && sib_bar != 0u) asm volatile("bar.sync %0, %1;" ::"r"(sib_bar), "r"(32u * Wp) : "memory");
   if (lane < f) {
     const uint32_t nw = (oldT & ~accw) | (xT & accw);
     if (nw != oldT) a.pop[(size_t)vj * Wp + w] = nw;
