@@ -16,3 +16,5 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"
   python bench.py --steps 20 --warmup 3 --ttt-seconds 0 --no-cpu-baseline > /dev/null 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:gom_univ_tt_kernel -s 20 -c 1 \
   -o gpurun_out/ncu_c3_tt python bench.py --steps 5 --warmup 3 --ttt-seconds 0 --no-cpu-baseline > /dev/null 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:gom_generation_kernel -s 10 -c 1 \
+  -o gpurun_out/ncu_c2_gen python bench.py --config c2 --steps 5 --warmup 3 --ttt-seconds 0 --no-cpu-baseline > /dev/null 2>&1
