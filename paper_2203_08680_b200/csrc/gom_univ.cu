@@ -579,7 +579,11 @@ __global__ void __launch_bounds__(kUnivWarps * 32, MINB) gom_univ_tt_kernel(cons
   __syncthreads();
   probe(a.exp_flags, 43);
   if (!s_last) return;
+#ifdef GOMIX_TT_LAST_FENCE
   __threadfence();
+#endif
+  // (no fence: thread 0's acq_rel ticket and the barrier order this CTA's
+  // loads after every other CTA's flush)
   probe_last(a.exp_flags, 44);
   timeline_mark(4, a.slot + 1);  // epilogue start (last CTA)
   epilogue_body(epi);
