@@ -26,10 +26,16 @@ sys.path.insert(0, {root!r}); sys.path.insert(0, os.path.join({root!r}, "tools")
 import paper_2203_08680_b200 as G
 from bench import CONFIGS
 from sweep import device_rate
-cfg = CONFIGS[{config!r}]
-n = {n} or cfg["n"]
-inst = G.generate_torus(cfg["width"], cfg["height"], cfg["weights"], 1)
-fos = G.univariate_fos(inst.num_vertices) if cfg["fos"] == "uni" else G.neighbourhood_fos(inst)
+if {config!r}.startswith("c4"):  # c4 / c4d16: random d-regular, 1e5 vertices, fp64 weights, univariate, n = 128
+    deg = int({config!r}[3:]) if len({config!r}) > 2 else 4
+    n = {n} or 128
+    inst = G.generate_regular(100000, deg, ("real",), seed=deg)
+    fos = G.univariate_fos(inst.num_vertices)
+else:
+    cfg = CONFIGS[{config!r}]
+    n = {n} or cfg["n"]
+    inst = G.generate_torus(cfg["width"], cfg["height"], cfg["weights"], 1)
+    fos = G.univariate_fos(inst.num_vertices) if cfg["fos"] == "uni" else G.neighbourhood_fos(inst)
 P = G.GpuProblem(inst, fos)
 r = device_rate(G, P, n, gens={gens}, warm=10, flush={flush})
 print("RESULT " + json.dumps(r))
