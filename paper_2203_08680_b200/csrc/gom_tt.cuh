@@ -57,6 +57,21 @@ __device__ __forceinline__ void xor_shared64(unsigned long long* p, unsigned lon
   if (hi) atomicXor(q + 1, hi);
 }
 
+// 64-bit add into shared memory as two native 32-bit atomics (the 64-bit
+// shared atomicAdd compiles to a compare-and-swap loop): the low word's
+// carry, read from the returned old value, goes into the high word
+__device__ __forceinline__ void add_shared64(long long* p, long long v) {
+  unsigned int* q = reinterpret_cast<unsigned int*>(p);
+  const unsigned int lo = (unsigned int)v;
+  const unsigned int old = atomicAdd(q, lo);
+  const unsigned int hi = (unsigned int)((unsigned long long)v >> 32) + ((old + lo) < old ? 1u : 0u);
+  if (hi) atomicAdd(q + 1, hi);
+}
+#ifndef GOMIX_TT_SPARSE_IMP
+#define GOMIX_TT_SPARSE_IMP 2
+#endif
+constexpr uint32_t kSparseImp = GOMIX_TT_SPARSE_IMP;  // strict improvements pair by pair up to this many per set and word
+
 // leaf masks of a 16-entry table held in bits [16*half, 16*half + 16) of tt
 __device__ __forceinline__ void tt_masks(uint32_t tt, int half, uint32_t (&m)[16]) {
 #pragma unroll
@@ -323,7 +338,26 @@ __device__ __forceinline__ uint32_t tt_batches(const GomArgs& a, const TtPart& p
         // ~p is not in LE — the LE table at the complemented pattern, no LT masks
         const uint32_t imp = acc[j] & ~tt_mux_not(mle, b0, b1, b2, b3);
         tt_count(2, __any_sync(0xFFFFFFFFu, imp != 0u) ? 1u : 0u, lane);
+#ifndef GOMIX_TT_IMP_PLANES_ONLY
+        const uint32_t imax = __reduce_max_sync(0xFFFFFFFFu, (uint32_t)__popc(imp));
+        if (imax != 0u && imax <= kSparseImp) {
+          // few strict improvements per set (generations after the first):
+          // each set adds its delta A - 2T(p) to the solutions it improves,
+          // pair by pair, instead of transposing every T plane
+          const int32_t m0 = abs(w[0]), m1 = abs(w[1]), m2 = abs(w[2]), m3 = abs(w[3]);
+          const int32_t A = m0 + m1 + m2 + m3;
+          uint32_t r = imp;
+          while (r) {
+            const uint32_t b = (uint32_t)(__ffs(r) - 1);
+            r &= r - 1u;
+            const int32_t T = (((b0 >> b) & 1u) ? m0 : 0) + (((b1 >> b) & 1u) ? m1 : 0) +
+                              (((b2 >> b) & 1u) ? m2 : 0) + (((b3 >> b) & 1u) ? m3 : 0);
+            add_shared64(&s_dfit[(uint32_t)j * 32u + b], (long long)(A - 2 * T));
+          }
+        } else if (imax != 0u) {
+#else
         if (__any_sync(0xFFFFFFFFu, imp != 0u)) {
+#endif
           // T planes of this word (only words with a strictly improving pair)
           uint32_t T[B];
 #pragma unroll
@@ -349,7 +383,7 @@ __device__ __forceinline__ uint32_t tt_batches(const GomArgs& a, const TtPart& p
           for (int k = 0; k < B - 1; ++k) d -= (long long)__popc(transpose32(T[k] & imp, lane)) << (k + 1);
         }
         const uint32_t sj = (uint32_t)j * 32u + lane;
-        if (d) atomicAdd(reinterpret_cast<unsigned long long*>(&s_dfit[sj]), (unsigned long long)d);
+        if (d) add_shared64(&s_dfit[sj], d);
         // hash delta of solution 32j+lane: XOR of the keys of its accepted
         // sets — key by key when every solution of the word accepted few
         // sets (the steady state: neutral flips are sparse), else through the
