@@ -331,7 +331,6 @@ struct gomix_gpu_engine {
   unsigned long long* gen_dh = nullptr;
   unsigned long long* gen_cnt = nullptr;
   unsigned int* gen_bar = nullptr;
-  unsigned int* gen_sib = nullptr;  // lean sibling arrivals (gom_lean.cuh)
   int sms = 148;
   uint32_t mode = GOMIX_MODE_PHILOX, flags = 0;
   int32_t pop_id = 1;
@@ -582,8 +581,6 @@ struct gomix_gpu_engine {
         gen_dh = dev_alloc<unsigned long long>(allocs, 6 * n * kAccStride);
         gen_cnt = dev_alloc<unsigned long long>(allocs, 6);
         gen_bar = dev_alloc<unsigned int>(allocs, 2048);  // two-level barrier (gom_gen.cu)
-        gen_sib = dev_alloc<unsigned int>(allocs, 3 * max_group);
-        GOMIX_CUDA(cudaMemset(gen_sib, 0, 3 * max_group * sizeof(unsigned int)));
         GOMIX_CUDA(cudaMemset(gen_dfit, 0, 3 * n * kAccStride * 8));
         GOMIX_CUDA(cudaMemset(gen_dh, 0, 6 * n * kAccStride * 8));
         GOMIX_CUDA(cudaMemset(gen_cnt, 0, 6 * 8));
@@ -719,7 +716,7 @@ struct gomix_gpu_engine {
   void launch_generation_persistent() {
     GomArgs a = gom_args(0, max_group, false, -1);
     a.epi = epi_args(0, 0, 0);
-    GenArgs ga{*h_begin, (uint32_t)P->k, d_order, gen_dfit, gen_dh, gen_cnt, gen_bar, gen_sib, (uint32_t)max_group};
+    GenArgs ga{*h_begin, (uint32_t)P->k, d_order, gen_dfit, gen_dh, gen_cnt, gen_bar};
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (flags & GOMIX_FLAG_TIME_KERNELS) {
       e0 = take_event();

@@ -274,9 +274,7 @@ struct GenArgs {
   long long* dfit;             // [3][n] fitness deltas
   unsigned long long* dh;      // [3][2][n] Zobrist deltas
   unsigned long long* cnt;     // [3][2] steps, calls
-  unsigned int* bar;           // grid barrier {arrivals, generation}
-  unsigned int* sib;           // LEAN, Wp > 1: [3][sib_stride] per-position sibling arrival counters
-  uint32_t sib_stride;         // largest colour group
+  unsigned int* bar;           // grid barrier: flat monotonic counter at word 1536 (two-level layout below it for GOMIX_GEN_TWO_LEVEL A/B builds)
 };
 
 // BeginArgs (above): per-call control values, passed as kernel parameters
