@@ -23,6 +23,12 @@
 //              and zeroes the accumulator of group g-1 (last read before the
 //              barrier of g, next written after the barrier of g+1).
 //
+// LEAN kernels (C2) differ in three ways: the barrier is the flat one
+// (grid_barrier_flat); the epilogue of group g runs in one warp per CTA while
+// the other warps already run group g+1's units, which wait for it only at
+// their accept step; and a unit's sibling warps (one per population word)
+// are adjacent warps of one CTA and meet at a named barrier.
+//
 // Results are bit-identical to the per-group path with the same device group
 // order (tests/test_gen_kernel.py).
 #include <cuda_runtime.h>
